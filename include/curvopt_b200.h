@@ -1,0 +1,147 @@
+/*
+ * curvopt_b200 -- C ABI of the B200-native curvature-matvec hot path.
+ *
+ * Drop-in boundary for the reference package `curvopt` 0.1.0 (paths relative to
+ * /root/reference/pkg/src/curvopt).  The reference has no FFI; its seams are
+ * Python callables, and each entry point below replaces one of them:
+ *
+ *   cv_linearize          models.py:337-396 (linearize) + curvature.py:87-131 (make_snapshot)
+ *   cv_matvec             curvature.py:109-110 (GGN closure) / models.py:287-307 (Linearization.hvp)
+ *   cv_jvp / cv_vjp       models.py:243-255 / models.py:274-285
+ *   cv_cg_solve           solvers.py:60-143 (_cg_core, cg_solve)
+ *   cv_hutchinson         telemetry.py:91-110 (hutchinson_diag / hutchinson_trace)
+ *   cv_power_iter         telemetry.py:113-126 (power_iter_top_eig)
+ *   cv_rademacher         numeric.py:124-128,157-162 (Rng._raw, rademacher)
+ *   cv_diag_ema           control.py:70-77 + method.py:404-409
+ *   cv_loss_at            curvature.py:82-84 (Snapshot.loss_at) -> models.py:399-408
+ *   cv_rho_terms          control.py:94-96 (g.u and u.Hu of compute_rho)
+ *   cv_row_rhs            curvature.py:112-119 (RowOps seeds / rhs)
+ *   cv_row_gram           models.py:309-334 (output_gram) via curvature.py:62-65
+ *   cv_row_solve_cholesky solvers.py:146-161
+ *   cv_backproject        curvature.py:53-60 (scaled_row_transpose)
+ *   cv_apply_update       method.py:345-357 (chain of scale links + w + update + norms)
+ *
+ * Conventions
+ *   - Every pointer argument is a DEVICE pointer owned by the caller, unless its
+ *     comment says "host".  Vectors are fp32, scalar results are fp64 (device).
+ *   - Parameter vectors use the reference flat layout (models.py:87-93): per layer
+ *     W[fan_in][fan_out] row-major, then b[fan_out].
+ *   - All work is enqueued on the context stream (cv_ctx_set_stream); nothing in
+ *     this API synchronises the host except cv_row_solve_cholesky's PD check flag
+ *     reads (documented there) and cv_ctx_create/destroy.
+ *   - Return 0 on success; CV_E_* otherwise, with a message in cv_last_error().
+ *     CV_E_CONTRACT mirrors the reference's ContractError (same message text where
+ *     the reference has one); CV_E_NOT_PD mirrors solvers.py:157-160.
+ *   - World > 1: the batch is sharded (b_local rows per rank, b_global overall);
+ *     gradients, losses and every curvature product are NCCL all-reduced inside
+ *     the library, so all returned vectors/scalars are replicated and global.
+ */
+#ifndef CURVOPT_B200_H
+#define CURVOPT_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define CV_API __attribute__((visibility("default")))
+#else
+#define CV_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct cv_ctx cv_ctx;
+typedef struct cv_snap cv_snap;
+
+enum {
+  CV_OK = 0,
+  CV_E_CONTRACT = 1,  /* ContractError */
+  CV_E_NOT_PD = 2,    /* row system not positive definite */
+  CV_E_CUDA = 3,
+  CV_E_NCCL = 4,
+  CV_E_UNSUPPORTED = 5
+};
+
+enum { CV_ACT_RELU = 0, CV_ACT_TANH = 1 };
+enum { CV_LOSS_MSE = 0, CV_LOSS_CE = 1 };
+enum { CV_KIND_GGN = 0, CV_KIND_HESSIAN = 1 };
+enum { CV_ENGINE_AUTO = 0, CV_ENGINE_SIMT = 1, CV_ENGINE_TC = 2 };
+
+/* CG solve statistics written to device memory (solvers.py:36-42). */
+typedef struct cv_cg_stats {
+  double relres;        /* final_relative_residual */
+  double bnorm;         /* ||g|| */
+  int32_t iterations;
+  int32_t converged;    /* 0/1 */
+  int32_t neg_curv;     /* 0/1 */
+  int32_t gv_count;     /* curvature products applied */
+  int32_t done;         /* internal */
+  int32_t x0_nonzero;   /* internal */
+  int32_t pad[2];
+} cv_cg_stats;
+
+/* ---- context ------------------------------------------------------------ */
+/* nccl_id: host pointer to a 128-byte ncclUniqueId (required when world > 1). */
+CV_API int cv_ctx_create(int device, int world, int rank, const void* nccl_id, cv_ctx** out);
+CV_API int cv_ctx_destroy(cv_ctx* ctx);
+CV_API int cv_ctx_set_stream(cv_ctx* ctx, void* cuda_stream);
+CV_API int cv_ctx_set_engine(cv_ctx* ctx, int engine);   /* CV_ENGINE_*: GEMM engine selection */
+CV_API const char* cv_last_error(const cv_ctx* ctx);
+CV_API int cv_nccl_unique_id(void* out128);               /* host buffer of 128 bytes */
+CV_API const char* cv_version(void);
+CV_API int64_t cv_kernel_launches(const cv_ctx* ctx);     /* kernels enqueued so far (instrumentation) */
+
+/* ---- snapshot (one linearization) --------------------------------------- */
+/* dims: host array of n_layers+1 ints.  y: int64[b_local] class ids (CE) or
+ * float[b_local*c] targets (MSE).  loss_out: device double; grad_out: device
+ * float[d] (may be NULL).  The snapshot keeps copies of everything it needs. */
+CV_API int cv_linearize(cv_ctx* ctx, int n_layers, const int* dims, int act, int loss,
+                 const float* w, const float* X, const void* y, int b_local, int b_global,
+                 cv_snap** snap, double* loss_out, float* grad_out);
+CV_API int cv_snap_free(cv_snap* snap);
+CV_API int64_t cv_snap_dim(const cv_snap* snap);
+CV_API int cv_snap_outputs(cv_snap* snap, float* out /* b_local*c logits */);
+
+/* ---- curvature products ------------------------------------------------- */
+CV_API int cv_matvec(cv_snap* snap, int kind, const float* v, float* out);
+CV_API int cv_jvp(cv_snap* snap, const float* v, float* out_bc);
+CV_API int cv_vjp(cv_snap* snap, const float* U_bc, float* out);
+
+/* ---- solver --------------------------------------------------------------- */
+/* precond, x0 nullable.  lam/tol/floor are host doubles. */
+CV_API int cv_cg_solve(cv_snap* snap, int kind, const float* g, double lam, double tol, int maxiter,
+                int stabilise_every, const float* precond, double floor, const float* x0,
+                float* x, cv_cg_stats* stats);
+
+/* ---- estimators / control ----------------------------------------------- */
+CV_API int cv_rademacher(cv_ctx* ctx, uint64_t seed, uint64_t counter, int64_t n, float* out);
+/* Probes consume counter .. counter + n_probes*d (host keeps the Rng counter). */
+CV_API int cv_hutchinson(cv_snap* snap, int kind, uint64_t seed, uint64_t counter, int n_probes,
+                  float* diag_out /*nullable*/, double* trace_out /*nullable*/);
+CV_API int cv_power_iter(cv_snap* snap, int kind, uint64_t seed, uint64_t counter, int iters,
+                  double* eig_out);
+/* mode 0: diag = max(beta*diag + (1-beta)*est, 0); mode 1: diag = max(est, 0). */
+CV_API int cv_diag_ema(cv_ctx* ctx, float* diag, const float* est, double beta, int64_t d, int mode,
+                double* mean_out /*nullable*/);
+CV_API int cv_loss_at(cv_snap* snap, const float* w_next, double* loss_out);
+CV_API int cv_rho_terms(cv_snap* snap, int kind, const float* g, const float* u,
+                 double* g_dot_u, double* u_H_u);
+/* update = coef * direction; w_next = w + update; scal[0]=||update||, scal[1]=#nonfinite
+ * (direction, update, w_next), scal[2]=||direction||^2 (device doubles). */
+CV_API int cv_apply_update(cv_ctx* ctx, const float* w, const float* direction, double coef, int64_t d,
+                    float* update, float* w_next, double* scal);
+/* scal[0] = ||x||^2, scal[1] = #nonfinite(x) (device doubles). */
+CV_API int cv_norm_check(cv_ctx* ctx, const float* x, int64_t d, double* scal);
+
+/* ---- row lane ------------------------------------------------------------- */
+CV_API int64_t cv_row_dim(const cv_snap* snap);                        /* m = b * c */
+CV_API int cv_row_rhs(cv_snap* snap, float* rhs_out /* m */);
+CV_API int cv_row_gram(cv_snap* snap, float* gram_out /* m*m, nullable: keep on device */);
+CV_API int cv_row_solve_cholesky(cv_snap* snap, double mu, const float* rhs, float* v_out);
+CV_API int cv_backproject(cv_snap* snap, const float* v_row, float* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

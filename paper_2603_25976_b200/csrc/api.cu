@@ -1,0 +1,351 @@
+// extern "C" entry points (include/curvopt_b200.h).
+#include <stdio.h>
+#include <string.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace cv {
+void nccl_unique_id(void* out);
+void nccl_init(cv_ctx* ctx, const void* id_bytes);
+void nccl_destroy(cv_ctx* ctx);
+// row.cu
+void row_rhs(cv_ctx* ctx, cv_snap* s, float* rhs);
+void row_gram(cv_ctx* ctx, cv_snap* s, float* gram_out);
+int row_solve_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, float* v);
+void row_backproject(cv_ctx* ctx, cv_snap* s, const float* v, float* out);
+}  // namespace cv
+
+using namespace cv;
+
+struct CvError : std::runtime_error {
+  int code;
+  CvError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CV_TRY(ctxp)                                   \
+  cv_ctx* _ctx = (ctxp);                               \
+  if (!_ctx) return CV_E_CONTRACT;                     \
+  try {                                                \
+    cudaSetDevice(_ctx->device);
+#define CV_CATCH                                       \
+    check_launch(_ctx);                                \
+    return CV_OK;                                      \
+  } catch (const CvError& e) {                         \
+    _ctx->err = e.what();                              \
+    return e.code;                                     \
+  } catch (const std::exception& e) {                  \
+    _ctx->err = e.what();                              \
+    return strstr(e.what(), "NCCL") ? CV_E_NCCL : CV_E_CUDA; \
+  }
+
+static void contract(bool ok, const char* msg) {
+  if (!ok) throw CvError(CV_E_CONTRACT, msg);
+}
+
+extern "C" {
+
+const char* cv_version(void) { return "curvopt_b200 0.1.0 (sm_100a, tcgen05 3xTF32 + SIMT fp32)"; }
+
+int cv_nccl_unique_id(void* out128) {
+  try {
+    nccl_unique_id(out128);
+    return CV_OK;
+  } catch (...) {
+    return CV_E_NCCL;
+  }
+}
+
+int cv_ctx_create(int device, int world, int rank, const void* nccl_id, cv_ctx** out) {
+  if (!out || world < 1 || rank < 0 || rank >= world) return CV_E_CONTRACT;
+  cv_ctx* c = new cv_ctx();
+  c->device = device;
+  c->world = world;
+  c->rank = rank;
+  *out = c;
+  CV_TRY(c)
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  if (sms > 0) c->sm_count = sms;
+  c->red_ws = (double*)c->pool.get(sizeof(double) * kRedBlocks * 8);
+  c->scal_ws = (double*)c->pool.get(sizeof(double) * 64);
+  if (world > 1) {
+    contract(nccl_id != nullptr, "world > 1 requires an NCCL unique id");
+    nccl_init(c, nccl_id);
+  }
+  CV_CATCH
+}
+
+int cv_ctx_destroy(cv_ctx* ctx) {
+  if (!ctx) return CV_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  try { nccl_destroy(ctx); } catch (...) {}
+  ctx->pool.release_all();
+  delete ctx;
+  return CV_OK;
+}
+
+int cv_ctx_set_stream(cv_ctx* ctx, void* stream) {
+  if (!ctx) return CV_E_CONTRACT;
+  ctx->stream = (cudaStream_t)stream;
+  return CV_OK;
+}
+
+int cv_ctx_set_engine(cv_ctx* ctx, int engine) {
+  if (!ctx || engine < 0 || engine > 2) return CV_E_CONTRACT;
+  ctx->engine = engine;
+  return CV_OK;
+}
+
+const char* cv_last_error(const cv_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int64_t cv_kernel_launches(const cv_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+// ---------------------------------------------------------------------------
+static float* alloc_f(cv_snap* s, int64_t n) {
+  float* p = (float*)s->ctx->pool.get(sizeof(float) * (size_t)(n > 0 ? n : 1));
+  s->owned.push_back(p);
+  return p;
+}
+
+static SplitBuf alloc_split(cv_snap* s, int rows, int n) {
+  SplitBuf b;
+  b.ld = ld_for(n);
+  b.hi = alloc_f(s, (int64_t)rows * b.ld);
+  b.lo = alloc_f(s, (int64_t)rows * b.ld);
+  return b;
+}
+
+static void zero_col(cv_ctx* ctx, const SplitBuf& b, int rows, int col) { set_col_value(ctx, b, rows, col, 0.f); }
+
+int cv_linearize(cv_ctx* ctx, int n_layers, const int* dims, int act, int loss, const float* w, const float* X,
+                 const void* y, int b_local, int b_global, cv_snap** snap, double* loss_out, float* grad_out) {
+  CV_TRY(ctx)
+  contract(snap && dims && w && X && y && loss_out, "null argument");
+  contract(n_layers >= 1, "model needs at least one layer");
+  contract(b_local >= 1 && b_global >= b_local, "batch inputs must be a (b, input_dim) matrix with b >= 1");
+  contract(act == CV_ACT_RELU || act == CV_ACT_TANH, "unknown activation");
+  contract(loss == CV_LOSS_MSE || loss == CV_LOSS_CE, "unknown loss kind");
+  for (int i = 0; i <= n_layers; ++i) contract(dims[i] >= 1, "layer widths must be >= 1");
+  const int c = dims[n_layers];
+  if (loss == CV_LOSS_CE) contract(c >= 2, "ce loss requires output_dim >= 2");
+  if (c > 32) throw CvError(CV_E_UNSUPPORTED, "output_dim > 32 is not supported by the skinny output kernels");
+
+  cv_snap* s = new cv_snap();
+  s->ctx = ctx;
+  s->L = n_layers;
+  s->dims.assign(dims, dims + n_layers + 1);
+  s->act = act;
+  s->loss = loss;
+  s->bl = b_local;
+  s->bg = b_global;
+  s->c = c;
+  int64_t off = 0;
+  for (int l = 0; l < n_layers; ++l) {
+    s->off.push_back(off);
+    off += (int64_t)(dims[l] + 1) * dims[l + 1];
+  }
+  s->d = off;
+  const int L = n_layers, b = b_local;
+  try {
+    s->w_hi = alloc_f(s, s->d);
+    s->w_lo = alloc_f(s, s->d);
+    s->v_hi = alloc_f(s, s->d);
+    s->v_lo = alloc_f(s, s->d);
+    for (int l = 0; l < L; ++l) s->acts.push_back(alloc_split(s, b, dims[l]));
+    s->logits = alloc_f(s, (int64_t)b * c);
+    s->probs = alloc_f(s, (int64_t)b * c);
+    s->gout = alloc_f(s, (int64_t)b * c);
+    s->U = alloc_f(s, (int64_t)b * c);
+    s->U2 = alloc_f(s, (int64_t)b * c);
+    if (loss == CV_LOSS_CE) {
+      s->y_i = (int64_t*)ctx->pool.get(sizeof(int64_t) * b);
+      s->owned.push_back(s->y_i);
+      cudaMemcpyAsync(s->y_i, y, sizeof(int64_t) * b, cudaMemcpyDeviceToDevice, ctx->stream);
+    } else {
+      s->y_f = alloc_f(s, (int64_t)b * c);
+      cudaMemcpyAsync(s->y_f, y, sizeof(float) * b * c, cudaMemcpyDeviceToDevice, ctx->stream);
+    }
+    for (int l = 0; l + 1 < L; ++l) {
+      const int n = dims[l + 1];
+      s->G.push_back(alloc_split(s, b, n));
+      s->da.push_back(alloc_split(s, b, n));
+      s->gs.push_back(alloc_split(s, b, n));
+      s->P.push_back(act == CV_ACT_TANH ? alloc_f(s, (int64_t)b * ld_for(n)) : nullptr);
+      s->dz.push_back(act == CV_ACT_TANH ? alloc_f(s, (int64_t)b * ld_for(n)) : nullptr);
+    }
+    // skinny weight-gradient partials: up to 2*SMs column blocks x (n+1) x c
+    int64_t need = 0;
+    const int mrows = dims[L - 1] + 1;
+    need = (int64_t)(2 * ctx->sm_count + 1) * mrows * c;
+    s->skinny_ws_elems = need;
+    s->skinny_ws = alloc_f(s, need);
+  } catch (...) {
+    for (void* p : s->owned) ctx->pool.put(p);
+    delete s;
+    throw;
+  }
+  split_vec(ctx, w, s->w_hi, s->w_lo, s->d, nullptr);
+  split_rows(ctx, X, dims[0], b, dims[0], s->acts[0], 1);
+  for (int l = 1; l < L; ++l) set_ones_col(ctx, s->acts[l], b, dims[l]);
+  for (int l = 0; l + 1 < L; ++l) zero_col(ctx, s->da[l], b, dims[l + 1]);
+  mlp_linearize(ctx, s, loss_out, grad_out);
+  *snap = s;
+  CV_CATCH
+}
+
+int cv_snap_free(cv_snap* s) {
+  if (!s) return CV_OK;
+  for (void* p : s->owned) s->ctx->pool.put(p);
+  delete s;
+  return CV_OK;
+}
+
+int64_t cv_snap_dim(const cv_snap* s) { return s ? s->d : -1; }
+
+int cv_snap_outputs(cv_snap* s, float* out) {
+  if (!s) return CV_E_CONTRACT;
+  CV_TRY(s->ctx)
+  cudaMemcpyAsync(out, s->logits, sizeof(float) * s->bl * s->c, cudaMemcpyDeviceToDevice, _ctx->stream);
+  CV_CATCH
+}
+
+int cv_matvec(cv_snap* s, int kind, const float* v, float* out) {
+  if (!s) return CV_E_CONTRACT;
+  CV_TRY(s->ctx)
+  contract(kind == CV_KIND_GGN || kind == CV_KIND_HESSIAN, "unknown curvature kind");
+  split_vec(_ctx, v, s->v_hi, s->v_lo, s->d, nullptr);
+  matvec_fn(kind)(_ctx, s, s->v_hi, s->v_lo, out, nullptr);
+  CV_CATCH
+}
+
+int cv_jvp(cv_snap* s, const float* v, float* out_bc) {
+  if (!s) return CV_E_CONTRACT;
+  CV_TRY(s->ctx)
+  split_vec(_ctx, v, s->v_hi, s->v_lo, s->d, nullptr);
+  mlp_jvp(_ctx, s, s->v_hi, s->v_lo, out_bc);
+  CV_CATCH
+}
+
+int cv_vjp(cv_snap* s, const float* U, float* out) {
+  if (!s) return CV_E_CONTRACT;
+  CV_TRY(s->ctx)
+  mlp_vjp(_ctx, s, U, out);
+  CV_CATCH
+}
+
+int cv_cg_solve(cv_snap* s, int kind, const float* g, double lam, double tol, int maxiter, int stabilise_every,
+                const float* precond, double floor, const float* x0, float* x, cv_cg_stats* stats) {
+  if (!s) return CV_E_CONTRACT;
+  CV_TRY(s->ctx)
+  contract(tol > 0, "cg tol must be positive");
+  contract(maxiter >= 1, "cg maxiter must be >= 1");
+  contract(g && x && stats, "null argument");
+  cg_solve(_ctx, s, kind, g, lam, tol, maxiter, stabilise_every, precond, floor, x0, x, stats);
+  CV_CATCH
+}
+
+int cv_rademacher(cv_ctx* ctx, uint64_t seed, uint64_t counter, int64_t n, float* out) {
+  CV_TRY(ctx)
+  contract(n >= 1, "rademacher requires n >= 1");
+  rademacher(_ctx, seed, counter, n, out, nullptr, nullptr);
+  CV_CATCH
+}
+
+int cv_hutchinson(cv_snap* s, int kind, uint64_t seed, uint64_t counter, int n_probes, float* diag_out,
+                  double* trace_out) {
+  if (!s) return CV_E_CONTRACT;
+  CV_TRY(s->ctx)
+  contract(n_probes >= 1, "hutchinson_diag requires n_probes >= 1");
+  hutchinson(_ctx, s, kind, seed, counter, n_probes, diag_out, trace_out);
+  CV_CATCH
+}
+
+int cv_power_iter(cv_snap* s, int kind, uint64_t seed, uint64_t counter, int iters, double* eig_out) {
+  if (!s) return CV_E_CONTRACT;
+  CV_TRY(s->ctx)
+  contract(iters >= 1, "power_iter_top_eig requires iters >= 1");
+  power_iter(_ctx, s, kind, seed, counter, iters, eig_out);
+  CV_CATCH
+}
+
+int cv_diag_ema(cv_ctx* ctx, float* diag, const float* est, double beta, int64_t d, int mode, double* mean_out) {
+  CV_TRY(ctx)
+  diag_ema(_ctx, diag, est, beta, d, mode, mean_out);
+  CV_CATCH
+}
+
+int cv_loss_at(cv_snap* s, const float* w_next, double* loss_out) {
+  if (!s) return CV_E_CONTRACT;
+  CV_TRY(s->ctx)
+  mlp_loss_at(_ctx, s, w_next, loss_out);
+  CV_CATCH
+}
+
+int cv_rho_terms(cv_snap* s, int kind, const float* g, const float* u, double* g_dot_u, double* u_H_u) {
+  if (!s) return CV_E_CONTRACT;
+  CV_TRY(s->ctx)
+  dot_into(_ctx, g, u, s->d, g_dot_u);
+  float* hu = s->cg_ap;
+  if (!hu) {
+    hu = (float*)_ctx->pool.get(sizeof(float) * s->d);
+    s->owned.push_back(hu);
+    s->cg_ap = hu;
+  }
+  split_vec(_ctx, u, s->v_hi, s->v_lo, s->d, nullptr);
+  matvec_fn(kind)(_ctx, s, s->v_hi, s->v_lo, hu, nullptr);
+  dot_into(_ctx, hu, u, s->d, u_H_u);
+  CV_CATCH
+}
+
+int cv_apply_update(cv_ctx* ctx, const float* w, const float* direction, double coef, int64_t d, float* update,
+                    float* w_next, double* scal) {
+  CV_TRY(ctx)
+  apply_update(_ctx, w, direction, coef, d, update, w_next, scal);
+  CV_CATCH
+}
+
+int cv_norm_check(cv_ctx* ctx, const float* x, int64_t d, double* scal) {
+  CV_TRY(ctx)
+  norm_check(_ctx, x, d, scal);
+  CV_CATCH
+}
+
+int64_t cv_row_dim(const cv_snap* s) { return s ? (int64_t)s->bl * s->c : -1; }
+
+int cv_row_rhs(cv_snap* s, float* rhs_out) {
+  if (!s) return CV_E_CONTRACT;
+  CV_TRY(s->ctx)
+  row_rhs(_ctx, s, rhs_out);
+  CV_CATCH
+}
+
+int cv_row_gram(cv_snap* s, float* gram_out) {
+  if (!s) return CV_E_CONTRACT;
+  CV_TRY(s->ctx)
+  contract(_ctx->world == 1, "row lane is single-GPU (replicas only)");
+  row_gram(_ctx, s, gram_out);
+  CV_CATCH
+}
+
+int cv_row_solve_cholesky(cv_snap* s, double mu, const float* rhs, float* v_out) {
+  if (!s) return CV_E_CONTRACT;
+  CV_TRY(s->ctx)
+  contract(_ctx->world == 1, "row lane is single-GPU (replicas only)");
+  if (row_solve_cholesky(_ctx, s, mu, rhs, v_out) != 0)
+    throw CvError(CV_E_NOT_PD, "row system is not positive definite; mu too small or gram invalid");
+  CV_CATCH
+}
+
+int cv_backproject(cv_snap* s, const float* v_row, float* out) {
+  if (!s) return CV_E_CONTRACT;
+  CV_TRY(s->ctx)
+  row_backproject(_ctx, s, v_row, out);
+  CV_CATCH
+}
+
+}  // extern "C"

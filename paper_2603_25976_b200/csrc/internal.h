@@ -1,0 +1,194 @@
+// Internal (non-ABI) structures of curvopt_b200.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/curvopt_b200.h"
+
+namespace cv {
+
+// ---------------------------------------------------------------------------
+// Logical operand views.  X(i, j) = hi[i*si + j*sj] + lo[i*si + j*sj].
+// ---------------------------------------------------------------------------
+struct Operand {
+  const float* hi = nullptr;
+  const float* lo = nullptr;
+  int64_t si = 0, sj = 0;
+};
+
+struct GemmSeg {
+  Operand A;  // M x K
+  Operand B;  // K x N
+  int K = 0;
+};
+
+enum EpiMode : int {
+  EPI_STORE = 0,       // out[m*ld+n] = acc                      (weight gradients)
+  EPI_SPLIT_ACT = 1,   // a = act(acc) -> split(out_hi/out_lo)   (forward hidden layers)
+  EPI_SPLIT_MASK = 2,  // v = acc * act'(mask) -> split          (tangents, backward)
+  EPI_HVP = 3,         // v = acc*sp + P*spp*dz (tanh) -> split   (HVP backward)
+  EPI_GRAM = 4,        // out (+)= acc * SA[m/k, n/k]             (row-space Gram, models.py:323-333)
+  EPI_ACCUM = 5,       // out += alpha * acc                      (Cholesky trailing update)
+};
+
+struct Epilogue {
+  int mode = EPI_STORE;
+  int act = 0;                   // CV_ACT_*
+  float* out = nullptr;          // fp32 output (EPI_STORE)
+  float* out_hi = nullptr;       // split outputs
+  float* out_lo = nullptr;
+  int64_t ld = 0;
+  const float* mask_hi = nullptr;  // stored activation a (hi/lo) at [m, n] for act'
+  const float* mask_lo = nullptr;
+  int64_t mask_ld = 0;
+  float* raw = nullptr;          // optional: pre-mask value (fp32), ld raw_ld
+  int64_t raw_ld = 0;
+  const float* P = nullptr;      // EPI_HVP tanh: pre-mask G W^T from linearize
+  int64_t P_ld = 0;
+  const float* dz = nullptr;     // EPI_HVP tanh: pre-mask tangent from the JVP
+  int64_t dz_ld = 0;
+  int mask_div = 1;              // mask row = m / mask_div (row lane: k rows per example)
+  const float* sa = nullptr;     // EPI_GRAM: b x b activation Gram, ld sa_ld
+  int64_t sa_ld = 0;
+  int kdiv = 1;                  // EPI_GRAM: rows per example
+  int first = 0;                 // EPI_GRAM: overwrite instead of accumulate
+  float alpha = 1.f;             // EPI_ACCUM
+};
+
+struct GemmArgs {
+  int M = 0, N = 0;
+  int nseg = 1;
+  GemmSeg seg[2];
+  Epilogue epi;
+  const int* skip = nullptr;     // device flag: kernel returns immediately when != 0
+  int lower_only = 0;            // only tiles intersecting the lower triangle (m >= n)
+};
+
+struct SplitBuf {
+  float* hi = nullptr;
+  float* lo = nullptr;
+  int64_t ld = 0;
+};
+
+// Caching device allocator: exact-size free lists, never returns memory to the
+// driver until the context dies (allocation on the step path must be free).
+class Pool {
+ public:
+  void* get(size_t bytes);
+  void put(void* p);
+  void release_all();
+  ~Pool() { release_all(); }
+
+ private:
+  std::map<void*, size_t> live_;
+  std::multimap<size_t, void*> free_;
+};
+
+}  // namespace cv
+
+struct cv_ctx {
+  int device = 0, world = 1, rank = 0;
+  cudaStream_t stream = nullptr;
+  int engine = CV_ENGINE_AUTO;
+  int sm_count = 148;
+  std::string err;
+  cv::Pool pool;
+  void* nccl = nullptr;          // ncclComm_t
+  double* red_ws = nullptr;      // reduction partials: kRedBlocks * 8 doubles
+  double* scal_ws = nullptr;     // scratch scalars (64 doubles)
+  int64_t launches = 0;
+};
+
+struct cv_snap {
+  cv_ctx* ctx = nullptr;
+  int L = 0;
+  std::vector<int> dims;
+  std::vector<int64_t> off;       // flat offset of layer l's [W; b] block
+  int64_t d = 0;
+  int act = 0, loss = 0;
+  int bl = 0, bg = 0;             // local / global batch
+  int c = 0;
+  // weights of the linearization point, split, flat layout
+  float* w_hi = nullptr;
+  float* w_lo = nullptr;
+  // augmented activations: acts[0] = [X | 1], acts[l] = [a_l | 1]; b x ld(n_l)
+  std::vector<cv::SplitBuf> acts;
+  // loss state
+  float* logits = nullptr;        // b x c
+  float* probs = nullptr;         // b x c (ce)
+  float* gout = nullptr;          // G[L-1] = out_grad / b_global, b x c fp32
+  float* y_f = nullptr;           // mse targets copy
+  int64_t* y_i = nullptr;         // ce labels copy
+  // G[l] for hidden layers (l < L-1): b x ld(n_{l+1}); P[l] = G[l+1] W^T pre-mask (tanh)
+  std::vector<cv::SplitBuf> G;
+  std::vector<float*> P;
+  // per-product scratch
+  float* v_hi = nullptr;          // split of the product input (d)
+  float* v_lo = nullptr;
+  std::vector<cv::SplitBuf> da;   // tangents of acts[l+1], zero column at n
+  std::vector<float*> dz;         // pre-mask tangents (tanh HVP)
+  std::vector<cv::SplitBuf> gs;   // backward scratch (ping-pong size L-1)
+  float* U = nullptr;             // b x c cotangent
+  float* U2 = nullptr;            // b x c (HVP last-layer dz)
+  float* skinny_ws = nullptr;     // partial sums for skinny weight-gradient kernels
+  int64_t skinny_ws_elems = 0;
+  // row lane (lazily built)
+  float* seeds = nullptr;         // b x c x c  (H_z^{1/2})
+  float* pinv = nullptr;          // b x c x c
+  float* rhs = nullptr;           // m
+  float* gram = nullptr;          // m x m
+  float* chol = nullptr;          // m x m, Cholesky factor of gram + mu I (lower)
+  float* dinv = nullptr;          // inverses of the diagonal blocks of chol
+  int row_state = 0;              // bit0 seeds built, bit1 gram built
+  // solver scratch (lazily allocated, d each)
+  float* cg_r = nullptr; float* cg_p = nullptr; float* cg_ap = nullptr;
+  float* tmp_d = nullptr; float* tmp_d2 = nullptr;
+  std::vector<void*> owned;
+};
+
+// ---- internal launch helpers (defined in the .cu files) ----
+namespace cv {
+int64_t ld_for(int n);
+void gemm_simt(cv_ctx* ctx, const GemmArgs& a);
+bool gemm_tc_supported(const GemmArgs& a);
+void gemm_tc(cv_ctx* ctx, const GemmArgs& a);
+void gemm(cv_ctx* ctx, const GemmArgs& a);  // engine dispatch
+
+// runtime.cu
+void allreduce_f32(cv_ctx* ctx, float* buf, int64_t n);
+void allreduce_f64(cv_ctx* ctx, double* buf, int64_t n);
+void check_launch(cv_ctx* ctx);
+
+// mlp.cu
+void split_vec(cv_ctx* ctx, const float* x, float* hi, float* lo, int64_t n, const int* skip);
+void split_rows(cv_ctx* ctx, const float* src, int64_t lds, int rows, int cols, const SplitBuf& dst, int ones);
+void set_ones_col(cv_ctx* ctx, const SplitBuf& b, int rows, int col);
+void set_col_value(cv_ctx* ctx, const SplitBuf& b, int rows, int col, float v);
+void mlp_linearize(cv_ctx* ctx, cv_snap* s, double* loss_out, float* grad_out);
+void mlp_ggn(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, float* out, const int* skip);
+void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, float* out, const int* skip);
+void mlp_jvp(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, float* out_bc);
+void mlp_vjp(cv_ctx* ctx, cv_snap* s, const float* U, float* out);
+void mlp_loss_at(cv_ctx* ctx, cv_snap* s, const float* w, double* loss_out);
+
+using MatvecFn = void (*)(cv_ctx*, cv_snap*, const float*, const float*, float*, const int*);
+inline MatvecFn matvec_fn(int kind) { return kind == CV_KIND_HESSIAN ? mlp_hvp : mlp_ggn; }
+
+// vec.cu
+void scale_scalar(cv_ctx* ctx, double* x, double s);
+void cg_solve(cv_ctx* ctx, cv_snap* s, int kind, const float* g, double lam, double tol, int maxiter,
+              int stab, const float* precond, double floor, const float* x0, float* x, cv_cg_stats* stats);
+void rademacher(cv_ctx* ctx, uint64_t seed, uint64_t counter, int64_t n, float* out, float* hi, float* lo);
+void hutchinson(cv_ctx* ctx, cv_snap* s, int kind, uint64_t seed, uint64_t counter, int n_probes, float* diag,
+                double* trace);
+void power_iter(cv_ctx* ctx, cv_snap* s, int kind, uint64_t seed, uint64_t counter, int iters, double* eig);
+void diag_ema(cv_ctx* ctx, float* diag, const float* est, double beta, int64_t d, int mode, double* mean);
+void dot_into(cv_ctx* ctx, const float* a, const float* b, int64_t n, double* out);
+void apply_update(cv_ctx* ctx, const float* w, const float* dir, double coef, int64_t d, float* upd,
+                  float* wn, double* scal);
+void norm_check(cv_ctx* ctx, const float* x, int64_t d, double* scal);
+}  // namespace cv

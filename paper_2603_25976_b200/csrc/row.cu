@@ -1,0 +1,441 @@
+// Row-space lane: per-example H_z roots, Gram of the seeded Jacobian rows,
+// blocked Cholesky of (Gram + mu I), triangular solves and backprojection.
+//   seeds / rhs        curvature.py:112-119, models.py:206-239
+//   Gram               models.py:309-334 (layer-wise, the m x d row matrix never exists)
+//   Cholesky + solve   solvers.py:146-161 (LAPACK potrf/potrs in the reference)
+//   backprojection     curvature.py:53-60
+#include "common.cuh"
+#include "internal.h"
+
+#include <stdexcept>
+#include <vector>
+
+namespace cv {
+
+constexpr int CH_NB = 64;  // Cholesky block size
+
+// ---------------------------------------------------------------------------
+// Per-example symmetric eigen-decomposition of H_z = diag(p) - p p^T (c x c) by
+// cyclic Jacobi in fp64, one thread per example; then the root and pseudo-inverse
+// root with the reference's floor (1e-10 * max(lambda_max, 0)).  MSE: identity.
+// ---------------------------------------------------------------------------
+template <int CM>
+__global__ void k_hz_roots(const float* probs, const float* gout, int b, int c, int loss, float bscale,
+                           float* seeds, float* pinv, float* rhs) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= b) return;
+  const size_t cc = (size_t)c * c;
+  if (loss == CV_LOSS_MSE) {
+    for (int a = 0; a < c; ++a) {
+      for (int j = 0; j < c; ++j) {
+        seeds[i * cc + a * c + j] = a == j ? 1.f : 0.f;
+        pinv[i * cc + a * c + j] = a == j ? 1.f : 0.f;
+      }
+      rhs[(size_t)i * c + a] = gout[(size_t)i * c + a] * bscale;
+    }
+    return;
+  }
+  double H[CM][CM], Q[CM][CM], p[CM];
+  bool finite = true;
+  for (int a = 0; a < c; ++a) {
+    p[a] = probs[(size_t)i * c + a];
+    finite = finite && isfinite(p[a]);
+  }
+  if (!finite) {
+    for (size_t e = 0; e < cc; ++e) { seeds[i * cc + e] = NAN; pinv[i * cc + e] = NAN; }
+    for (int a = 0; a < c; ++a) rhs[(size_t)i * c + a] = NAN;
+    return;
+  }
+  for (int a = 0; a < c; ++a)
+    for (int j = 0; j < c; ++j) {
+      H[a][j] = (a == j ? p[a] : 0.0) - p[a] * p[j];
+      Q[a][j] = a == j ? 1.0 : 0.0;
+    }
+  for (int sweep = 0; sweep < 30; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int a = 0; a < c; ++a)
+      for (int j = 0; j < c; ++j) {
+        tot += H[a][j] * H[a][j];
+        if (a != j) off += H[a][j] * H[a][j];
+      }
+    if (off <= 1e-30 * tot || off == 0.0) break;
+    for (int pp = 0; pp < c - 1; ++pp)
+      for (int q = pp + 1; q < c; ++q) {
+        const double apq = H[pp][q];
+        if (fabs(apq) < 1e-300) continue;
+        const double theta = (H[q][q] - H[pp][pp]) / (2.0 * apq);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        const double cs = 1.0 / sqrt(t * t + 1.0), sn = t * cs;
+        for (int k = 0; k < c; ++k) {  // H <- J^T H J
+          const double hkp = H[k][pp], hkq = H[k][q];
+          H[k][pp] = cs * hkp - sn * hkq;
+          H[k][q] = sn * hkp + cs * hkq;
+        }
+        for (int k = 0; k < c; ++k) {
+          const double hpk = H[pp][k], hqk = H[q][k];
+          H[pp][k] = cs * hpk - sn * hqk;
+          H[q][k] = sn * hpk + cs * hqk;
+        }
+        for (int k = 0; k < c; ++k) {  // Q <- Q J
+          const double qkp = Q[k][pp], qkq = Q[k][q];
+          Q[k][pp] = cs * qkp - sn * qkq;
+          Q[k][q] = sn * qkp + cs * qkq;
+        }
+      }
+  }
+  double lmax = -1e300;
+  for (int a = 0; a < c; ++a) lmax = fmax(lmax, H[a][a]);
+  const double floor_ = 1e-10 * fmax(lmax, 0.0);
+  double r[CM], ri[CM];
+  for (int a = 0; a < c; ++a) {
+    const bool keep = H[a][a] > floor_;
+    r[a] = keep ? sqrt(fmax(H[a][a], 0.0)) : 0.0;
+    ri[a] = keep ? 1.0 / r[a] : 0.0;
+  }
+  double og[CM];
+  for (int a = 0; a < c; ++a) og[a] = (double)gout[(size_t)i * c + a] * bscale;
+  for (int a = 0; a < c; ++a) {
+    double acc_rhs = 0.0;
+    for (int j = 0; j < c; ++j) {
+      double s = 0.0, si = 0.0;
+      for (int k = 0; k < c; ++k) {
+        s += Q[a][k] * r[k] * Q[j][k];
+        si += Q[a][k] * ri[k] * Q[j][k];
+      }
+      seeds[i * cc + a * c + j] = (float)s;
+      pinv[i * cc + a * c + j] = (float)si;
+      acc_rhs += si * og[j];
+    }
+    rhs[(size_t)i * c + a] = (float)acc_rhs;
+  }
+}
+
+// D0 rows (i, a) = seeds[i, a, :], split into an m x ld(c) buffer
+__global__ void k_seed_rows(const float* seeds, int m, int c, float* hi, float* lo, int64_t ld) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)m * c; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / c;
+    const int j = (int)(e - r * c);
+    float h, l;
+    split2(seeds[e], h, l);
+    hi[r * ld + j] = h;
+    lo[r * ld + j] = l;
+  }
+}
+
+// cot[i, a] = sum_j seeds[i, a, j] u[i, j]  (curvature.py:58-59)
+__global__ void k_seed_apply(const float* seeds, const float* u, int b, int c, float* out) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (int64_t)b * c) return;
+  const int64_t i = e / c;
+  const int a = (int)(e - i * c);
+  float s = 0.f;
+  for (int j = 0; j < c; ++j) s = fmaf(seeds[(i * c + a) * c + j], u[i * c + j], s);
+  out[e] = s;
+}
+
+static float* snap_alloc(cv_snap* s, int64_t n) {
+  float* p = (float*)s->ctx->pool.get(sizeof(float) * (size_t)n);
+  s->owned.push_back(p);
+  return p;
+}
+
+static void ensure_seeds(cv_ctx* ctx, cv_snap* s) {
+  if (s->row_state & 1) return;
+  const int b = s->bl, c = s->c;
+  s->seeds = snap_alloc(s, (int64_t)b * c * c);
+  s->pinv = snap_alloc(s, (int64_t)b * c * c);
+  s->rhs = snap_alloc(s, (int64_t)b * c);
+  // gout = out_grad / b_global  ->  out_grad = gout * b_global
+  if (c <= 16)
+    k_hz_roots<16><<<(b + 63) / 64, 64, 0, ctx->stream>>>(s->probs, s->gout, b, c, s->loss, (float)s->bg, s->seeds,
+                                                          s->pinv, s->rhs);
+  else
+    k_hz_roots<32><<<(b + 31) / 32, 32, 0, ctx->stream>>>(s->probs, s->gout, b, c, s->loss, (float)s->bg, s->seeds,
+                                                          s->pinv, s->rhs);
+  ctx->launches++;
+  s->row_state |= 1;
+}
+
+void row_rhs(cv_ctx* ctx, cv_snap* s, float* rhs) {
+  ensure_seeds(ctx, s);
+  cudaMemcpyAsync(rhs, s->rhs, sizeof(float) * s->bl * s->c, cudaMemcpyDeviceToDevice, ctx->stream);
+}
+
+static void ensure_gram(cv_ctx* ctx, cv_snap* s) {
+  if (s->row_state & 2) return;
+  ensure_seeds(ctx, s);
+  const int b = s->bl, c = s->c, L = s->L;
+  const int64_t m = (int64_t)b * c;
+  if (!s->gram) s->gram = snap_alloc(s, m * m);
+  float* sa = snap_alloc(s, (int64_t)b * b);
+  // D ping-pong buffers sized for the widest layer
+  int wmax = c;
+  for (int l = 1; l < L; ++l) wmax = wmax > s->dims[l] ? wmax : s->dims[l];
+  const int64_t ldD = ld_for(wmax);
+  SplitBuf D[2];
+  for (int k = 0; k < 2; ++k) {
+    D[k].hi = snap_alloc(s, m * ldD);
+    D[k].lo = snap_alloc(s, m * ldD);
+    D[k].ld = ldD;
+  }
+  k_seed_rows<<<1024, 256, 0, ctx->stream>>>(s->seeds, (int)m, c, D[0].hi, D[0].lo, ldD);
+  ctx->launches++;
+  int cur = 0;
+  for (int l = L - 1; l >= 0; --l) {
+    const int nout = s->dims[l + 1];
+    // SA = A_l A_l^T  (A augmented with the ones column: +1 covers the bias)
+    GemmArgs g;
+    g.M = b;
+    g.N = b;
+    g.nseg = 1;
+    g.seg[0] = GemmSeg{Operand{s->acts[l].hi, s->acts[l].lo, s->acts[l].ld, 1},
+                       Operand{s->acts[l].hi, s->acts[l].lo, 1, s->acts[l].ld}, s->dims[l] + 1};
+    g.epi.mode = EPI_STORE;
+    g.epi.out = sa;
+    g.epi.ld = b;
+    gemm(ctx, g);
+    // gram (+)= (D D^T) o kron(SA, 1 1^T)
+    GemmArgs h;
+    h.M = (int)m;
+    h.N = (int)m;
+    h.nseg = 1;
+    h.seg[0] = GemmSeg{Operand{D[cur].hi, D[cur].lo, ldD, 1}, Operand{D[cur].hi, D[cur].lo, 1, ldD}, nout};
+    h.epi.mode = EPI_GRAM;
+    h.epi.out = s->gram;
+    h.epi.ld = m;
+    h.epi.sa = sa;
+    h.epi.sa_ld = b;
+    h.epi.kdiv = c;
+    h.epi.first = l == L - 1;
+    gemm(ctx, h);
+    if (l > 0) {
+      // D <- (D W_l^T) * act'(a_l) broadcast over the k rows of each example
+      GemmArgs q;
+      q.M = (int)m;
+      q.N = s->dims[l];
+      q.nseg = 1;
+      q.seg[0] = GemmSeg{Operand{D[cur].hi, D[cur].lo, ldD, 1},
+                         Operand{s->w_hi + s->off[l], s->w_lo + s->off[l], 1, nout}, nout};
+      q.epi.mode = EPI_SPLIT_MASK;
+      q.epi.act = s->act;
+      q.epi.out_hi = D[cur ^ 1].hi;
+      q.epi.out_lo = D[cur ^ 1].lo;
+      q.epi.ld = ldD;
+      q.epi.mask_hi = s->acts[l].hi;
+      q.epi.mask_lo = s->acts[l].lo;
+      q.epi.mask_ld = s->acts[l].ld;
+      q.epi.mask_div = c;
+      gemm(ctx, q);
+      cur ^= 1;
+    }
+  }
+  s->row_state |= 2;
+}
+
+void row_gram(cv_ctx* ctx, cv_snap* s, float* gram_out) {
+  ensure_gram(ctx, s);
+  const int64_t m = (int64_t)s->bl * s->c;
+  if (gram_out) cudaMemcpyAsync(gram_out, s->gram, sizeof(float) * m * m, cudaMemcpyDeviceToDevice, ctx->stream);
+}
+
+// ---------------------------------------------------------------------------
+// Blocked right-looking Cholesky, lower, in place on chol = gram + mu I.
+// ---------------------------------------------------------------------------
+__global__ void k_copy_add_diag(const float* src, float* dst, int64_t m, float mu) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * m; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / m, j = e - i * m;
+    dst[e] = src[e] + (i == j ? mu : 0.f);
+  }
+}
+
+// Factor the nb x nb diagonal block at j0 in fp64 shared memory, write L11 back
+// and its inverse (fp32) into dinv[blk]; flag <- 1 if not positive definite.
+__global__ void __launch_bounds__(256) k_potrf_diag(float* A, int64_t lda, int j0, int nb, float* dinv_blk,
+                                                    int* flag) {
+  __shared__ double T[CH_NB][CH_NB + 1];
+  __shared__ int bad;
+  const int tid = threadIdx.x;
+  if (tid == 0) bad = 0;
+  for (int e = tid; e < nb * nb; e += blockDim.x) {
+    const int i = e / nb, j = e % nb;
+    T[i][j] = j <= i ? (double)A[(int64_t)(j0 + i) * lda + j0 + j] : 0.0;
+  }
+  __syncthreads();
+  for (int k = 0; k < nb; ++k) {
+    if (tid == 0) {
+      const double dkk = T[k][k];
+      if (!(dkk > 0.0) || !isfinite(dkk)) { bad = 1; T[k][k] = 1.0; }
+      else T[k][k] = sqrt(dkk);
+    }
+    __syncthreads();
+    const double dk = T[k][k];
+    for (int i = k + 1 + tid; i < nb; i += blockDim.x) T[i][k] /= dk;
+    __syncthreads();
+    for (int e = tid; e < (nb - k - 1) * (nb - k - 1); e += blockDim.x) {
+      const int i = k + 1 + e / (nb - k - 1), j = k + 1 + e % (nb - k - 1);
+      if (j <= i) T[i][j] -= T[i][k] * T[j][k];
+    }
+    __syncthreads();
+  }
+  // inverse of the lower-triangular factor, one column per thread
+  // (column j of the inverse lives in dinv_blk[:, j]; only its own thread touches it)
+  for (int j = tid; j < nb; j += blockDim.x) {
+    double xc[CH_NB];
+    for (int i = 0; i < nb; ++i) {
+      if (i < j) { xc[i] = 0.0; dinv_blk[i * nb + j] = 0.f; continue; }
+      double s = i == j ? 1.0 : 0.0;
+      for (int k = j; k < i; ++k) s -= T[i][k] * xc[k];
+      xc[i] = s / T[i][i];
+      dinv_blk[i * nb + j] = (float)xc[i];
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < nb * nb; e += blockDim.x) {
+    const int i = e / nb, j = e % nb;
+    if (j <= i) A[(int64_t)(j0 + i) * lda + j0 + j] = (float)T[i][j];
+  }
+  if (tid == 0 && bad) *flag = 1;
+}
+
+// forward substitution, one diagonal block: y_blk = Dinv (r_blk) ; then
+// r[j0+nb:] -= L[j0+nb:, blk] y_blk    (r, y in fp64)
+__global__ void k_trsv_fwd_diag(const float* dinv, int nb, int j0, double* r, double* y) {
+  __shared__ double rb[CH_NB];
+  const int t = threadIdx.x;
+  if (t < nb) rb[t] = r[j0 + t];
+  __syncthreads();
+  if (t < nb) {
+    double s = 0.0;
+    for (int k = 0; k <= t; ++k) s += (double)dinv[t * nb + k] * rb[k];
+    y[j0 + t] = s;
+  }
+}
+__global__ void k_trsv_fwd_update(const float* A, int64_t lda, int64_t m, int j0, int nb, const double* y, double* r) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = j0 + nb + (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= m) return;
+  double s = 0.0;
+  for (int k = lane; k < nb; k += 32) s += (double)A[row * lda + j0 + k] * y[j0 + k];
+  s = warp_sum(s);
+  if (lane == 0) r[row] -= s;
+}
+// backward: s_blk = L[j0+nb:, blk]^T v[j0+nb:]; v_blk = Dinv^T (y_blk - s_blk)
+__global__ void k_trsv_bwd_gather(const float* A, int64_t lda, int64_t m, int j0, int nb, const double* v,
+                                  double* partial, int rows_per_block) {
+  // partial[blockIdx.x * nb + k] = sum over this block's rows of A[row, j0+k] v[row]
+  const int k = threadIdx.x;
+  if (k >= nb) return;
+  const int64_t r0 = j0 + nb + (int64_t)blockIdx.x * rows_per_block;
+  double s = 0.0;
+  for (int64_t row = r0; row < r0 + rows_per_block && row < m; ++row) s += (double)A[row * lda + j0 + k] * v[row];
+  partial[blockIdx.x * nb + k] = s;
+}
+__global__ void k_trsv_bwd_diag(const float* dinv, int nb, int j0, const double* y, const double* partial,
+                                int nparts, double* v) {
+  __shared__ double rb[CH_NB];
+  const int t = threadIdx.x;
+  if (t < nb) {
+    double s = 0.0;
+    for (int p = 0; p < nparts; ++p) s += partial[p * nb + t];
+    rb[t] = y[j0 + t] - s;
+  }
+  __syncthreads();
+  if (t < nb) {
+    double s = 0.0;
+    for (int k = t; k < nb; ++k) s += (double)dinv[k * nb + t] * rb[k];  // Dinv^T
+    v[j0 + t] = s;
+  }
+}
+__global__ void k_f2d(const float* x, double* y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) y[i] = x[i];
+}
+__global__ void k_d2f(const double* x, float* y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) y[i] = (float)x[i];
+}
+
+int row_solve_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, float* v_out) {
+  ensure_gram(ctx, s);
+  const int64_t m = (int64_t)s->bl * s->c;
+  if (!s->chol) s->chol = snap_alloc(s, m * m);
+  const int nblk = (int)((m + CH_NB - 1) / CH_NB);
+  if (!s->dinv) s->dinv = snap_alloc(s, (int64_t)nblk * CH_NB * CH_NB);
+  cudaStream_t st = ctx->stream;
+  k_copy_add_diag<<<4096, 256, 0, st>>>(s->gram, s->chol, m, (float)mu);
+  int* flag = (int*)(ctx->scal_ws + 32);
+  cudaMemsetAsync(flag, 0, sizeof(int), st);
+  ctx->launches++;
+  for (int bi = 0; bi < nblk; ++bi) {
+    const int j0 = bi * CH_NB;
+    const int nb = (int)((m - j0) < CH_NB ? (m - j0) : CH_NB);
+    float* dblk = s->dinv + (int64_t)bi * CH_NB * CH_NB;
+    k_potrf_diag<<<1, 256, 0, st>>>(s->chol, m, j0, nb, dblk, flag);
+    ctx->launches++;
+    const int rest = (int)(m - j0 - nb);
+    if (rest <= 0) continue;
+    float* A21 = s->chol + (int64_t)(j0 + nb) * m + j0;
+    // A21 <- A21 * L11^-T
+    GemmArgs p;
+    p.M = rest;
+    p.N = nb;
+    p.nseg = 1;
+    p.seg[0] = GemmSeg{Operand{A21, nullptr, m, 1}, Operand{dblk, nullptr, 1, nb}, nb};
+    p.epi.mode = EPI_STORE;
+    p.epi.out = A21;
+    p.epi.ld = m;
+    gemm_simt(ctx, p);  // in place: one N tile per CTA row block
+    // A22 -= A21 A21^T (lower tiles)
+    GemmArgs u;
+    u.M = rest;
+    u.N = rest;
+    u.nseg = 1;
+    u.seg[0] = GemmSeg{Operand{A21, nullptr, m, 1}, Operand{A21, nullptr, 1, m}, nb};
+    u.epi.mode = EPI_ACCUM;
+    u.epi.alpha = -1.f;
+    u.epi.out = s->chol + (int64_t)(j0 + nb) * m + (j0 + nb);
+    u.epi.ld = m;
+    u.lower_only = 1;
+    gemm(ctx, u);
+  }
+  int hflag = 0;
+  cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  if (hflag) return 1;
+  // triangular solves in fp64
+  double* r = (double*)ctx->pool.get(sizeof(double) * m * 3);
+  double* y = r + m;
+  double* v = r + 2 * m;
+  const int rpb = 256;
+  const int nparts_max = (int)((m + rpb - 1) / rpb);
+  double* part = (double*)ctx->pool.get(sizeof(double) * (size_t)nparts_max * CH_NB);
+  k_f2d<<<256, 256, 0, st>>>(rhs, r, m);
+  for (int bi = 0; bi < nblk; ++bi) {
+    const int j0 = bi * CH_NB;
+    const int nb = (int)((m - j0) < CH_NB ? (m - j0) : CH_NB);
+    k_trsv_fwd_diag<<<1, CH_NB, 0, st>>>(s->dinv + (int64_t)bi * CH_NB * CH_NB, nb, j0, r, y);
+    const int64_t rest = m - j0 - nb;
+    if (rest > 0) k_trsv_fwd_update<<<(int)((rest + 7) / 8), 256, 0, st>>>(s->chol, m, m, j0, nb, y, r);
+  }
+  for (int bi = nblk - 1; bi >= 0; --bi) {
+    const int j0 = bi * CH_NB;
+    const int nb = (int)((m - j0) < CH_NB ? (m - j0) : CH_NB);
+    const int64_t rest = m - j0 - nb;
+    const int nparts = (int)((rest + rpb - 1) / rpb);
+    if (nparts > 0) k_trsv_bwd_gather<<<nparts, CH_NB, 0, st>>>(s->chol, m, m, j0, nb, v, part, rpb);
+    k_trsv_bwd_diag<<<1, CH_NB, 0, st>>>(s->dinv + (int64_t)bi * CH_NB * CH_NB, nb, j0, y, part, nparts, v);
+  }
+  k_d2f<<<256, 256, 0, st>>>(v, v_out, m);
+  ctx->launches += 2 + 4 * nblk;
+  ctx->pool.put(part);
+  ctx->pool.put(r);
+  return 0;
+}
+
+void row_backproject(cv_ctx* ctx, cv_snap* s, const float* v, float* out) {
+  ensure_seeds(ctx, s);
+  const int64_t m = (int64_t)s->bl * s->c;
+  k_seed_apply<<<(int)((m + 255) / 256), 256, 0, ctx->stream>>>(s->seeds, v, s->bl, s->c, s->U2);
+  ctx->launches++;
+  mlp_vjp(ctx, s, s->U2, out);
+}
+
+}  // namespace cv

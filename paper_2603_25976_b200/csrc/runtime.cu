@@ -1,0 +1,151 @@
+// Runtime: caching allocator, NCCL (loaded on demand), GEMM engine dispatch.
+#include <dlfcn.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <stdexcept>
+
+#include "common.cuh"
+#include "internal.h"
+#include "nccl.h"
+
+namespace cv {
+
+// ---------------------------------------------------------------------------
+// Pool
+// ---------------------------------------------------------------------------
+void* Pool::get(size_t bytes) {
+  bytes = (bytes + 255) / 256 * 256;
+  if (bytes == 0) bytes = 256;
+  auto it = free_.find(bytes);
+  void* p = nullptr;
+  if (it != free_.end()) {
+    p = it->second;
+    free_.erase(it);
+  } else {
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      // drop cached blocks and retry once
+      for (auto& kv : free_) cudaFree(kv.second);
+      free_.clear();
+      if (cudaMalloc(&p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        throw std::runtime_error("cudaMalloc failed (" + std::to_string(bytes) + " bytes)");
+      }
+    }
+  }
+  live_[p] = bytes;
+  return p;
+}
+
+void Pool::put(void* p) {
+  if (!p) return;
+  auto it = live_.find(p);
+  if (it == live_.end()) return;
+  free_.emplace(it->second, p);
+  live_.erase(it);
+}
+
+void Pool::release_all() {
+  for (auto& kv : free_) cudaFree(kv.second);
+  for (auto& kv : live_) cudaFree(kv.first);
+  free_.clear();
+  live_.clear();
+}
+
+// ---------------------------------------------------------------------------
+// NCCL, resolved with dlopen so single-GPU use never needs the library.
+// ---------------------------------------------------------------------------
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi& nccl_api() {
+  static NcclApi api;
+  if (api.h) return api;
+  const char* cands[] = {getenv("CURVOPT_NCCL_LIB"), "libnccl.so.2",
+#ifdef CV_NCCL_LIB_PATH
+                         CV_NCCL_LIB_PATH,
+#endif
+                         nullptr};
+  for (const char* c : cands) {
+    if (!c) continue;
+    api.h = dlopen(c, RTLD_NOW | RTLD_GLOBAL);
+    if (api.h) break;
+  }
+  if (!api.h) throw std::runtime_error("NCCL library not found (set CURVOPT_NCCL_LIB)");
+  api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(api.h, "ncclGetUniqueId");
+  api.CommInitRank = (decltype(api.CommInitRank))dlsym(api.h, "ncclCommInitRank");
+  api.CommDestroy = (decltype(api.CommDestroy))dlsym(api.h, "ncclCommDestroy");
+  api.AllReduce = (decltype(api.AllReduce))dlsym(api.h, "ncclAllReduce");
+  api.GetErrorString = (decltype(api.GetErrorString))dlsym(api.h, "ncclGetErrorString");
+  if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce)
+    throw std::runtime_error("NCCL library lacks required symbols");
+  return api;
+}
+
+static void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) {
+    NcclApi& a = nccl_api();
+    throw std::runtime_error(std::string("NCCL ") + what + ": " + (a.GetErrorString ? a.GetErrorString(r) : "error"));
+  }
+}
+
+void nccl_unique_id(void* out) {
+  ncclUniqueId id;
+  nccl_check(nccl_api().GetUniqueId(&id), "GetUniqueId");
+  memcpy(out, &id, sizeof(id));
+}
+
+void nccl_init(cv_ctx* ctx, const void* id_bytes) {
+  ncclUniqueId id;
+  memcpy(&id, id_bytes, sizeof(id));
+  ncclComm_t comm;
+  nccl_check(nccl_api().CommInitRank(&comm, ctx->world, id, ctx->rank), "CommInitRank");
+  ctx->nccl = comm;
+}
+
+void nccl_destroy(cv_ctx* ctx) {
+  if (ctx->nccl) nccl_api().CommDestroy((ncclComm_t)ctx->nccl);
+  ctx->nccl = nullptr;
+}
+
+void allreduce_f32(cv_ctx* ctx, float* buf, int64_t n) {
+  if (ctx->world <= 1) return;
+  nccl_check(nccl_api().AllReduce(buf, buf, (size_t)n, ncclFloat32, ncclSum, (ncclComm_t)ctx->nccl, ctx->stream),
+             "AllReduce");
+}
+
+void allreduce_f64(cv_ctx* ctx, double* buf, int64_t n) {
+  if (ctx->world <= 1) return;
+  nccl_check(nccl_api().AllReduce(buf, buf, (size_t)n, ncclFloat64, ncclSum, (ncclComm_t)ctx->nccl, ctx->stream),
+             "AllReduce");
+}
+
+void check_launch(cv_ctx* ctx) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------------------
+// GEMM engine dispatch: tensor-core (tcgen05, 3xTF32) where the operand
+// geometry allows TMA, exact-fp32 SIMT otherwise.
+// ---------------------------------------------------------------------------
+void gemm(cv_ctx* ctx, const GemmArgs& a) {
+  if (ctx->engine != CV_ENGINE_SIMT && gemm_tc_supported(a)) {
+    gemm_tc(ctx, a);
+    return;
+  }
+  if (ctx->engine == CV_ENGINE_TC && getenv("CURVOPT_TC_STRICT"))
+    throw std::runtime_error("tensor-core engine requested but GEMM shape unsupported");
+  gemm_simt(ctx, a);
+}
+
+}  // namespace cv

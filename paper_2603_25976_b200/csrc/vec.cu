@@ -1,0 +1,566 @@
+// Device-resident CG/PCG, SplitMix64 probes, Hutchinson estimators, EMA and the
+// step-tail vector kernels.  Every d-length pass is a grid-stride loop over a fixed
+// grid (kRedBlocks x 256) whose fp64 block partials are summed in a fixed order,
+// so all scalars are bitwise reproducible run to run.
+#include "common.cuh"
+#include "internal.h"
+
+#include <float.h>
+
+namespace cv {
+
+constexpr int NB = kRedBlocks, NT = kRedThreads;
+#define GRID_STRIDE(i, n) for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); \
+                               i += (int64_t)gridDim.x * blockDim.x)
+
+// Sum the NV partials of every block (ws[blk*8 + v]); result valid in thread 0.
+template <int NV>
+CV_DEV void sum_partials(const double* ws, double (&t)[NV]) {
+#pragma unroll
+  for (int v = 0; v < NV; ++v) t[v] = 0.0;
+  for (int b = threadIdx.x; b < NB; b += NT)
+#pragma unroll
+    for (int v = 0; v < NV; ++v) t[v] += ws[b * 8 + v];
+  block_sum<NV>(t);
+}
+
+template <int NV>
+CV_DEV void write_partials(double* ws, double (&t)[NV]) {
+  block_sum<NV>(t);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int v = 0; v < NV; ++v) ws[blockIdx.x * 8 + v] = t[v];
+}
+
+CV_DEV float minv_of(const float* pre, int64_t i, float lam, float floor_) {
+  return pre ? 1.f / (fmaxf(pre[i], floor_) + lam) : 1.f;
+}
+
+// ---------------------------------------------------------------------------
+// SplitMix64 (numeric.py:95-104, 124-128, 157-162)
+// ---------------------------------------------------------------------------
+CV_DEV uint64_t splitmix(uint64_t seed, uint64_t idx) {
+  uint64_t x = seed + 0x9E3779B97F4A7C15ull * idx;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+// element i (0-based) of rademacher(Rng(seed, counter), n): index counter + 1 + i
+CV_DEV float rad(uint64_t seed, uint64_t counter, int64_t i) {
+  return (splitmix(seed, counter + 1 + (uint64_t)i) >> 63) ? 1.f : -1.f;
+}
+
+__global__ void k_rademacher(uint64_t seed, uint64_t counter, int64_t n, float scale, float* out, float* hi,
+                             float* lo) {
+  GRID_STRIDE(i, n) {
+    const float z = rad(seed, counter, i) * scale;
+    if (out) out[i] = z;
+    if (hi) {
+      float h, l;
+      split2(z, h, l);
+      hi[i] = h;
+      lo[i] = l;
+    }
+  }
+}
+
+void rademacher(cv_ctx* ctx, uint64_t seed, uint64_t counter, int64_t n, float* out, float* hi, float* lo) {
+  k_rademacher<<<NB, NT, 0, ctx->stream>>>(seed, counter, n, 1.f, out, hi, lo);
+  ctx->launches++;
+}
+
+// ---------------------------------------------------------------------------
+// small scalar utilities
+// ---------------------------------------------------------------------------
+__global__ void k_scale_scalar(double* x, double s) { *x *= s; }
+void scale_scalar(cv_ctx* ctx, double* x, double s) {
+  k_scale_scalar<<<1, 1, 0, ctx->stream>>>(x, s);
+  ctx->launches++;
+}
+
+__global__ void k_dot(const float* a, const float* b, int64_t n, double* ws) {
+  double t[1] = {0.0};
+  GRID_STRIDE(i, n) t[0] += (double)a[i] * (double)b[i];
+  write_partials<1>(ws, t);
+}
+__global__ void k_dot_final(const double* ws, double* out) {
+  double t[1];
+  sum_partials<1>(ws, t);
+  if (threadIdx.x == 0) *out = t[0];
+}
+void dot_into(cv_ctx* ctx, const float* a, const float* b, int64_t n, double* out) {
+  k_dot<<<NB, NT, 0, ctx->stream>>>(a, b, n, ctx->red_ws);
+  k_dot_final<<<1, NT, 0, ctx->stream>>>(ctx->red_ws, out);
+  ctx->launches += 2;
+}
+
+// update = coef*dir; w_next = w + update; scal = [||update||, #nonfinite, ||dir||^2]
+// (method.py:345-357; the all-`scale` chain collapses to one coefficient)
+__global__ void k_apply_update(const float* w, const float* dir, float coef, int64_t d, float* upd, float* wn,
+                               double* ws) {
+  double t[3] = {0.0, 0.0, 0.0};
+  GRID_STRIDE(i, d) {
+    const float di = dir[i];
+    const float u = di * coef;
+    const float x = w[i] + u;
+    upd[i] = u;
+    wn[i] = x;
+    t[0] += (double)u * u;
+    t[1] += (!isfinite(di) || !isfinite(u) || !isfinite(x)) ? 1.0 : 0.0;
+    t[2] += (double)di * di;
+  }
+  write_partials<3>(ws, t);
+}
+__global__ void k_apply_update_final(const double* ws, double* scal) {
+  double t[3];
+  sum_partials<3>(ws, t);
+  if (threadIdx.x == 0) { scal[0] = sqrt(t[0]); scal[1] = t[1]; scal[2] = t[2]; }
+}
+void apply_update(cv_ctx* ctx, const float* w, const float* dir, double coef, int64_t d, float* upd, float* wn,
+                  double* scal) {
+  k_apply_update<<<NB, NT, 0, ctx->stream>>>(w, dir, (float)coef, d, upd, wn, ctx->red_ws);
+  k_apply_update_final<<<1, NT, 0, ctx->stream>>>(ctx->red_ws, scal);
+  ctx->launches += 2;
+}
+
+__global__ void k_norm_check(const float* x, int64_t d, double* ws) {
+  double t[2] = {0.0, 0.0};
+  GRID_STRIDE(i, d) {
+    const float v = x[i];
+    t[0] += (double)v * v;
+    t[1] += isfinite(v) ? 0.0 : 1.0;
+  }
+  write_partials<2>(ws, t);
+}
+__global__ void k_norm_check_final(const double* ws, double* scal) {
+  double t[2];
+  sum_partials<2>(ws, t);
+  if (threadIdx.x == 0) { scal[0] = t[0]; scal[1] = t[1]; }
+}
+void norm_check(cv_ctx* ctx, const float* x, int64_t d, double* scal) {
+  k_norm_check<<<NB, NT, 0, ctx->stream>>>(x, d, ctx->red_ws);
+  k_norm_check_final<<<1, NT, 0, ctx->stream>>>(ctx->red_ws, scal);
+  ctx->launches += 2;
+}
+
+// diag EMA (control.py:70-77) / floored store (method.py:407-408) + mean (method.py:409)
+__global__ void k_diag_ema(float* diag, const float* est, float beta, int64_t d, int mode, double* ws) {
+  double t[1] = {0.0};
+  GRID_STRIDE(i, d) {
+    const float e = est[i];
+    const float v = mode == 0 ? fmaxf(beta * diag[i] + (1.f - beta) * e, 0.f) : fmaxf(e, 0.f);
+    diag[i] = v;
+    t[0] += v;
+  }
+  write_partials<1>(ws, t);
+}
+__global__ void k_mean_final(const double* ws, double inv_n, double* out) {
+  double t[1];
+  sum_partials<1>(ws, t);
+  if (threadIdx.x == 0) *out = t[0] * inv_n;
+}
+void diag_ema(cv_ctx* ctx, float* diag, const float* est, double beta, int64_t d, int mode, double* mean) {
+  k_diag_ema<<<NB, NT, 0, ctx->stream>>>(diag, est, (float)beta, d, mode, ctx->red_ws);
+  ctx->launches++;
+  if (mean) {
+    k_mean_final<<<1, NT, 0, ctx->stream>>>(ctx->red_ws, 1.0 / (double)d, mean);
+    ctx->launches++;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Hutchinson (telemetry.py:91-110): z regenerated from (seed, counter) in the
+// accumulation pass instead of being re-read.
+// ---------------------------------------------------------------------------
+__global__ void k_hutch_acc(uint64_t seed, uint64_t counter, const float* hz, int64_t d, float* diag, int first,
+                            int last, float inv_n, double* ws) {
+  double t[1] = {0.0};
+  GRID_STRIDE(i, d) {
+    const float z = rad(seed, counter, i);
+    const float zh = z * hz[i];
+    t[0] += (double)zh;
+    if (diag) {
+      float a = first ? zh : diag[i] + zh;
+      if (last) a *= inv_n;
+      diag[i] = a;
+    }
+  }
+  write_partials<1>(ws, t);
+}
+__global__ void k_trace_final(const double* ws, double inv_n, double* out, int first) {
+  double t[1];
+  sum_partials<1>(ws, t);
+  if (threadIdx.x == 0) *out = (first ? 0.0 : *out) + t[0] * inv_n;
+}
+
+static float* snap_tmp(cv_snap* s, float** slot) {
+  if (!*slot) {
+    *slot = (float*)s->ctx->pool.get(sizeof(float) * s->d);
+    s->owned.push_back(*slot);
+  }
+  return *slot;
+}
+
+void hutchinson(cv_ctx* ctx, cv_snap* s, int kind, uint64_t seed, uint64_t counter, int n_probes, float* diag,
+                double* trace) {
+  float* hz = snap_tmp(s, &s->tmp_d);
+  MatvecFn mv = matvec_fn(kind);
+  for (int j = 0; j < n_probes; ++j) {
+    const uint64_t ctr = counter + (uint64_t)j * (uint64_t)s->d;
+    rademacher(ctx, seed, ctr, s->d, nullptr, s->v_hi, s->v_lo);
+    mv(ctx, s, s->v_hi, s->v_lo, hz, nullptr);
+    k_hutch_acc<<<NB, NT, 0, ctx->stream>>>(seed, ctr, hz, s->d, diag, j == 0, j == n_probes - 1,
+                                            1.f / (float)n_probes, ctx->red_ws);
+    ctx->launches++;
+    if (trace) {
+      k_trace_final<<<1, NT, 0, ctx->stream>>>(ctx->red_ws, 1.0 / (double)n_probes, trace, j == 0);
+      ctx->launches++;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Power iteration (telemetry.py:113-126)
+// ---------------------------------------------------------------------------
+struct PiDev { double ray, result; int done; };
+
+__global__ void k_pi_init(PiDev* st) { st->ray = 0.0; st->result = 0.0; st->done = 0; }
+__global__ void k_pi_reduce(const float* v, const float* hv, int64_t d, double* ws, const int* skip) {
+  if (skip_if(skip)) return;
+  double t[2] = {0.0, 0.0};
+  GRID_STRIDE(i, d) {
+    t[0] += (double)v[i] * hv[i];
+    t[1] += (double)hv[i] * hv[i];
+  }
+  write_partials<2>(ws, t);
+}
+__global__ void k_pi_final(const double* ws, PiDev* st, double* norm_out) {
+  if (st->done) return;
+  double t[2];
+  sum_partials<2>(ws, t);
+  if (threadIdx.x == 0) {
+    const double nrm = sqrt(t[1]);
+    st->ray = t[0];
+    if (nrm == 0.0) { st->result = 0.0; st->done = 1; }
+    else st->result = t[0];
+    *norm_out = nrm;
+  }
+}
+__global__ void k_pi_next(const float* hv, const double* nrm, int64_t d, float* v, float* hi, float* lo,
+                          const int* skip) {
+  if (skip_if(skip)) return;
+  const float inv = (float)(1.0 / *nrm);
+  GRID_STRIDE(i, d) {
+    const float x = (float)((double)hv[i] / *nrm);
+    (void)inv;
+    v[i] = x;
+    float h, l;
+    split2(x, h, l);
+    hi[i] = h;
+    lo[i] = l;
+  }
+}
+__global__ void k_pi_out(const PiDev* st, double* out) { *out = st->result; }
+
+void power_iter(cv_ctx* ctx, cv_snap* s, int kind, uint64_t seed, uint64_t counter, int iters, double* eig) {
+  float* v = snap_tmp(s, &s->tmp_d);
+  float* hv = snap_tmp(s, &s->tmp_d2);
+  PiDev* st = (PiDev*)ctx->scal_ws;
+  double* nrm = ctx->scal_ws + 4;
+  k_pi_init<<<1, 1, 0, ctx->stream>>>(st);
+  const float scale = (float)(1.0 / sqrt((double)s->d));
+  k_rademacher<<<NB, NT, 0, ctx->stream>>>(seed, counter, s->d, scale, v, s->v_hi, s->v_lo);
+  ctx->launches += 2;
+  MatvecFn mv = matvec_fn(kind);
+  for (int it = 0; it < iters; ++it) {
+    mv(ctx, s, s->v_hi, s->v_lo, hv, &st->done);
+    k_pi_reduce<<<NB, NT, 0, ctx->stream>>>(v, hv, s->d, ctx->red_ws, &st->done);
+    k_pi_final<<<1, NT, 0, ctx->stream>>>(ctx->red_ws, st, nrm);
+    k_pi_next<<<NB, NT, 0, ctx->stream>>>(hv, nrm, s->d, v, s->v_hi, s->v_lo, &st->done);
+    ctx->launches += 3;
+  }
+  k_pi_out<<<1, 1, 0, ctx->stream>>>(st, eig);
+  ctx->launches++;
+}
+
+// ---------------------------------------------------------------------------
+// (P)CG, device resident (solvers.py:60-114).  Control decisions are taken by
+// single-block "final" kernels that also write the predicate read by every later
+// kernel of the solve, so the host enqueues the whole loop without reading back.
+// ---------------------------------------------------------------------------
+struct CgDev {
+  double bnorm, rz, alpha, rr, relres;
+  int done, x0nz, gv_skip, iters, conv, neg, gv;
+};
+
+__global__ void k_cg_init(const float* g, const float* x0, int64_t d, double* ws) {
+  double t[2] = {0.0, 0.0};
+  GRID_STRIDE(i, d) {
+    t[0] += (double)g[i] * g[i];
+    if (x0) t[1] += x0[i] != 0.f ? 1.0 : 0.0;
+  }
+  write_partials<2>(ws, t);
+}
+__global__ void k_cg_init_final(const double* ws, CgDev* st) {
+  double t[2];
+  sum_partials<2>(ws, t);
+  if (threadIdx.x == 0) {
+    st->bnorm = sqrt(t[0]);
+    st->x0nz = t[1] > 0.0;
+    st->rz = st->alpha = st->rr = 0.0;
+    st->relres = 0.0;
+    st->iters = 0; st->conv = 0; st->neg = 0; st->gv = 0;
+    st->done = st->bnorm == 0.0;
+    if (st->done) { st->conv = 1; st->x0nz = 0; }
+    st->gv_skip = st->done || !st->x0nz;
+  }
+}
+// x = x0 (if any nonzero entry) else 0; split x for the warm-start product
+__global__ void k_cg_setup_x(const float* x0, const CgDev* st, int64_t d, float* x, float* hi, float* lo) {
+  const bool use = st->x0nz;
+  GRID_STRIDE(i, d) {
+    const float v = use ? x0[i] : 0.f;
+    x[i] = v;
+    if (use) { float h, l; split2(v, h, l); hi[i] = h; lo[i] = l; }
+  }
+}
+// r = g - (Ax + lam x) (warm) or g; partial ||r||^2
+__global__ void k_cg_r0(const float* g, const float* ax, const float* x, float lam, const CgDev* st, int64_t d,
+                        float* r, double* ws) {
+  if (st->done) return;
+  const bool warm = st->x0nz;
+  double t[1] = {0.0};
+  GRID_STRIDE(i, d) {
+    const float v = warm ? g[i] - (ax[i] + lam * x[i]) : g[i];
+    r[i] = v;
+    t[0] += (double)v * v;
+  }
+  write_partials<1>(ws, t);
+}
+__global__ void k_cg_r0_final(const double* ws, CgDev* st, double tol) {
+  if (st->done) return;
+  double t[1];
+  sum_partials<1>(ws, t);
+  if (threadIdx.x == 0) {
+    if (st->x0nz) st->gv++;
+    st->relres = sqrt(t[0]) / st->bnorm;
+    if (st->relres <= tol) { st->done = 1; st->conv = 1; st->iters = 0; }
+    st->gv_skip = st->done;
+  }
+}
+// p = z = M^-1 r; rz = r.z
+__global__ void k_cg_p0(const float* r, const float* pre, float lam, float floor_, const CgDev* st, int64_t d,
+                        float* p, float* hi, float* lo, double* ws) {
+  if (st->done) return;
+  double t[1] = {0.0};
+  GRID_STRIDE(i, d) {
+    const float ri = r[i];
+    const float z = minv_of(pre, i, lam, floor_) * ri;
+    p[i] = z;
+    float h, l;
+    split2(z, h, l);
+    hi[i] = h;
+    lo[i] = l;
+    t[0] += (double)ri * z;
+  }
+  write_partials<1>(ws, t);
+}
+__global__ void k_cg_p0_final(const double* ws, CgDev* st) {
+  if (st->done) return;
+  double t[1];
+  sum_partials<1>(ws, t);
+  if (threadIdx.x == 0) st->rz = t[0];
+}
+// Ap = Gv(p) + lam p (in place); partials p.Ap, max|p|, #nonfinite(p)
+__global__ void k_cg_pap(float* ap, const float* p, float lam, const CgDev* st, int64_t d, double* ws) {
+  if (st->done) return;
+  double t[3] = {0.0, 0.0, 0.0};
+  GRID_STRIDE(i, d) {
+    const float pi = p[i];
+    const float a = ap[i] + lam * pi;
+    ap[i] = a;
+    t[0] += (double)pi * a;
+    t[2] += isfinite(pi) ? 0.0 : 1.0;
+    t[1] = fmax(t[1], (double)fabsf(pi));
+  }
+  // max is not a sum: reduce it separately through the same shared buffer
+  double mx = t[1];
+  t[1] = 0.0;
+  write_partials<3>(ws, t);
+  __shared__ double smx[NT / 32];
+  mx = warp_max_d(mx);
+  if ((threadIdx.x & 31) == 0) smx[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int w = 0; w < NT / 32; ++w) m = fmax(m, smx[w]);
+    ws[blockIdx.x * 8 + 1] = m;
+  }
+}
+__global__ void k_cg_pap_final(const double* ws, CgDev* st, int k, int stab) {
+  if (st->done) return;
+  double t[3];
+  // sums of slots 0 and 2; max of slot 1
+  double s0 = 0.0, s2 = 0.0, mx = 0.0;
+  for (int b = threadIdx.x; b < NB; b += NT) {
+    s0 += ws[b * 8 + 0];
+    s2 += ws[b * 8 + 2];
+    mx = fmax(mx, ws[b * 8 + 1]);
+  }
+  t[0] = s0; t[1] = 0.0; t[2] = s2;
+  block_sum<3>(t);
+  __shared__ double smx[NT / 32];
+  mx = warp_max_d(mx);
+  if ((threadIdx.x & 31) == 0) smx[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < NT / 32; ++w) mx = fmax(mx, smx[w]);
+    st->gv++;
+    const double pap = t[0];
+    if (!isfinite(pap)) { st->done = 1; st->iters = k; st->conv = 0; }
+    else if (pap <= 0.0) { st->done = 1; st->iters = k; st->conv = 0; st->neg = 1; }
+    else {
+      const double alpha = st->rz / pap;
+      const bool step_ok = isfinite(alpha) && t[2] == 0.0 && fabs((double)(float)alpha) * mx < (double)FLT_MAX;
+      if (!step_ok) { st->done = 1; st->iters = k; st->conv = 0; }
+      st->alpha = alpha;
+    }
+    st->gv_skip = st->done || !stab;
+  }
+}
+// plain iteration: x += a p; r -= a Ap; partials ||r||^2, r.M^-1 r
+__global__ void k_cg_update(float* x, float* r, const float* p, const float* ap, const float* pre, float lam,
+                            float floor_, const CgDev* st, int64_t d, double* ws) {
+  if (st->done) return;
+  const float a = (float)st->alpha;
+  double t[2] = {0.0, 0.0};
+  GRID_STRIDE(i, d) {
+    x[i] += a * p[i];
+    const float ri = r[i] - a * ap[i];
+    r[i] = ri;
+    t[0] += (double)ri * ri;
+    t[1] += (double)ri * (minv_of(pre, i, lam, floor_) * ri);
+  }
+  write_partials<2>(ws, t);
+}
+// stabilising iteration: x += a p, split x for the explicit residual product
+__global__ void k_cg_xupdate(float* x, const float* p, const CgDev* st, int64_t d, float* hi, float* lo) {
+  if (st->done) return;
+  const float a = (float)st->alpha;
+  GRID_STRIDE(i, d) {
+    const float v = x[i] + a * p[i];
+    x[i] = v;
+    float h, l;
+    split2(v, h, l);
+    hi[i] = h;
+    lo[i] = l;
+  }
+}
+// r = g - (Ax + lam x); partials ||r||^2, r.M^-1 r
+__global__ void k_cg_rstab(const float* g, const float* ax, const float* x, float* r, const float* pre, float lam,
+                           float floor_, const CgDev* st, int64_t d, double* ws) {
+  if (st->done) return;
+  double t[2] = {0.0, 0.0};
+  GRID_STRIDE(i, d) {
+    const float ri = g[i] - (ax[i] + lam * x[i]);
+    r[i] = ri;
+    t[0] += (double)ri * ri;
+    t[1] += (double)ri * (minv_of(pre, i, lam, floor_) * ri);
+  }
+  write_partials<2>(ws, t);
+}
+__global__ void k_cg_r_final(const double* ws, CgDev* st, int k, int maxiter, int stab, double tol) {
+  if (st->done) return;
+  double t[2];
+  sum_partials<2>(ws, t);
+  if (threadIdx.x == 0) {
+    if (stab) st->gv++;
+    const double relres = sqrt(t[0]) / st->bnorm;
+    st->relres = relres;
+    if (!isfinite(relres)) { st->done = 1; st->iters = k; st->conv = 0; }
+    else if (relres <= tol) { st->done = 1; st->iters = k; st->conv = 1; }
+    else {
+      const double rz_new = t[1];
+      st->alpha = rz_new / st->rz;  // beta, consumed by k_cg_pnext
+      st->rz = rz_new;
+      if (k == maxiter) { st->done = 1; st->iters = maxiter; st->conv = 0; }
+    }
+    st->gv_skip = st->done;
+  }
+}
+// p = M^-1 r + beta p, split p for the next product
+__global__ void k_cg_pnext(const float* r, const float* pre, float lam, float floor_, const CgDev* st, int64_t d,
+                           float* p, float* hi, float* lo) {
+  if (st->done) return;
+  const float beta = (float)st->alpha;
+  GRID_STRIDE(i, d) {
+    const float v = minv_of(pre, i, lam, floor_) * r[i] + beta * p[i];
+    p[i] = v;
+    float h, l;
+    split2(v, h, l);
+    hi[i] = h;
+    lo[i] = l;
+  }
+}
+__global__ void k_cg_finish(const CgDev* st, cv_cg_stats* out) {
+  out->relres = st->relres;
+  out->bnorm = st->bnorm;
+  out->iterations = st->iters;
+  out->converged = st->conv;
+  out->neg_curv = st->neg;
+  out->gv_count = st->gv;
+  out->done = st->done;
+  out->x0_nonzero = st->x0nz;
+}
+
+void cg_solve(cv_ctx* ctx, cv_snap* s, int kind, const float* g, double lam, double tol, int maxiter, int stab,
+              const float* precond, double floor, const float* x0, float* x, cv_cg_stats* stats) {
+  const int64_t d = s->d;
+  float* r = snap_tmp(s, &s->cg_r);
+  float* p = snap_tmp(s, &s->cg_p);
+  float* ap = snap_tmp(s, &s->cg_ap);
+  CgDev* st = (CgDev*)(ctx->scal_ws + 8);
+  double* ws = ctx->red_ws;
+  cudaStream_t sm = ctx->stream;
+  const float flam = (float)lam, ffl = (float)floor;
+  MatvecFn mv = matvec_fn(kind);
+
+  k_cg_init<<<NB, NT, 0, sm>>>(g, x0, d, ws);
+  k_cg_init_final<<<1, NT, 0, sm>>>(ws, st);
+  ctx->launches += 2;
+  if (x0) {
+    k_cg_setup_x<<<NB, NT, 0, sm>>>(x0, st, d, x, s->v_hi, s->v_lo);
+    ctx->launches++;
+    mv(ctx, s, s->v_hi, s->v_lo, ap, &st->gv_skip);
+  } else {
+    cudaMemsetAsync(x, 0, sizeof(float) * d, sm);
+  }
+  k_cg_r0<<<NB, NT, 0, sm>>>(g, ap, x, flam, st, d, r, ws);
+  k_cg_r0_final<<<1, NT, 0, sm>>>(ws, st, tol);
+  k_cg_p0<<<NB, NT, 0, sm>>>(r, precond, flam, ffl, st, d, p, s->v_hi, s->v_lo, ws);
+  k_cg_p0_final<<<1, NT, 0, sm>>>(ws, st);
+  ctx->launches += 4;
+  for (int k = 1; k <= maxiter; ++k) {
+    const int is_stab = (stab > 0 && k % stab == 0) ? 1 : 0;
+    mv(ctx, s, s->v_hi, s->v_lo, ap, &st->done);
+    k_cg_pap<<<NB, NT, 0, sm>>>(ap, p, flam, st, d, ws);
+    k_cg_pap_final<<<1, NT, 0, sm>>>(ws, st, k, is_stab);
+    ctx->launches += 2;
+    if (is_stab) {
+      k_cg_xupdate<<<NB, NT, 0, sm>>>(x, p, st, d, s->v_hi, s->v_lo);
+      ctx->launches++;
+      mv(ctx, s, s->v_hi, s->v_lo, ap, &st->gv_skip);
+      k_cg_rstab<<<NB, NT, 0, sm>>>(g, ap, x, r, precond, flam, ffl, st, d, ws);
+    } else {
+      k_cg_update<<<NB, NT, 0, sm>>>(x, r, p, ap, precond, flam, ffl, st, d, ws);
+    }
+    k_cg_r_final<<<1, NT, 0, sm>>>(ws, st, k, maxiter, is_stab, tol);
+    k_cg_pnext<<<NB, NT, 0, sm>>>(r, precond, flam, ffl, st, d, p, s->v_hi, s->v_lo);
+    ctx->launches += 3;
+  }
+  k_cg_finish<<<1, 1, 0, sm>>>(st, stats);
+  ctx->launches++;
+}
+
+}  // namespace cv

@@ -1,0 +1,250 @@
+"""GPU parity: the native CUDA path (through the C ABI / public API) against the
+reference's golden fixtures and the CPU oracle on identical inputs.
+
+Tolerances: the device computes in fp32 (3xTF32 tensor-core GEMMs or fp32 SIMT)
+with fp64 scalar reductions; the north star bound is 1e-4 relative L2 per step.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2603_25976_b200 as P  # noqa: E402
+from oracle import curvopt_oracle as O  # noqa: E402
+
+REL = 1e-4
+
+
+def rel(a, b):
+    a = a.detach().double().cpu().numpy() if hasattr(a, "detach") else np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a.ravel() - b.ravel()) / max(np.linalg.norm(b.ravel()), 1e-300))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    yield
+
+
+def test_device_rademacher_bit_exact(golden):
+    g = golden("rng")
+    for i in range(4):
+        s, c, n = (int(x) for x in g[f"case{i}"])
+        z = P.numeric.device_rademacher(P.Rng(s, c), n).cpu().numpy().astype(np.float64)
+        assert np.array_equal(z, g[f"rad{i}"])
+
+
+NAMES = ["relu_ce", "tanh_ce", "relu_mse", "tanh_mse", "lin_ce"]
+
+
+def _case(golden, name):
+    g = golden("primitives")
+    k = lambda s: g[f"{name}/{s}"]  # noqa: E731
+    dims = tuple(int(x) for x in k("dims"))
+    m = P.Model(dims[0], dims[1:-1], dims[-1], str(k("act")))
+    loss = str(k("loss"))
+    w = P.ParamVector(k("w"), P.models.param_layout(m))
+    batch = P.Batch(k("X"), k("y"), loss)
+    return m, w, batch, k
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_primitives(golden, name):
+    m, w, batch, k = _case(golden, name)
+    kind = "ggn_ce" if batch.loss_kind == "ce" else "ggn_mse"
+    snap = P.make_snapshot(kind, m, w, batch)
+    assert snap.loss_before == pytest.approx(float(k("value")), rel=1e-5)
+    assert rel(snap.grad.data, k("grad")) < REL
+    assert rel(snap.outputs(), k("out")) < REL
+    v = P.ParamVector(k("v"), w.layout)
+    assert rel(snap.jvp(v), k("jvp")) < REL
+    assert rel(snap.vjp(k("U")).data, k("vjp")) < REL
+    assert rel(snap.matvec(v).data, k("ggn")) < REL
+    assert rel(snap.hvp(v).data, k("hvp")) < REL
+    la = snap.loss_at(P.ParamVector(k("w") + 0.01 * k("v"), w.layout))
+    assert la == pytest.approx(float(k("loss_at")), rel=1e-5)
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_cg_solve(golden, name):
+    m, w, batch, k = _case(golden, name)
+    kind = "ggn_ce" if batch.loss_kind == "ce" else "ggn_mse"
+    snap = P.make_snapshot(kind, m, w, batch)
+    cfg = P.CgConfig(tol=1e-5, maxiter=10, stabilise_every=3)
+    res = P.cg_solve(snap.matvec, snap.grad, 0.5, cfg)
+    st = k("cg_stats")
+    assert res.iterations == int(st[0]) and int(res.converged) == int(st[1])
+    assert rel(res.direction.data, k("cg_x")) < REL
+    res = P.cg_solve(snap.matvec, snap.grad, 0.5, cfg, precond=P.ParamVector(k("pcg_pre"), w.layout),
+                     x0=P.ParamVector(k("pcg_x0"), w.layout))
+    st = k("pcg_stats")
+    assert res.iterations == int(st[0]) and int(res.converged) == int(st[1])
+    assert rel(res.direction.data, k("pcg_x")) < REL
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_estimators(golden, name):
+    m, w, batch, k = _case(golden, name)
+    kind = "ggn_ce" if batch.loss_kind == "ce" else "ggn_mse"
+    snap = P.make_snapshot(kind, m, w, batch)
+    rng = P.Rng(5)
+    d = w.dim
+    assert rel(P.hutchinson_diag(snap.matvec, rng, d, 3), k("hutch_diag")) < REL
+    assert P.hutchinson_trace(snap.matvec, rng, d, 2) == pytest.approx(float(k("hutch_trace")), rel=REL)
+    assert P.power_iter_top_eig(snap.matvec, rng, d, 7) == pytest.approx(float(k("top_eig")), rel=REL)
+    assert rng.counter == int(k("rng_after")[0])
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_row_lane(golden, name):
+    m, w, batch, k = _case(golden, name)
+    kind = "ggn_ce" if batch.loss_kind == "ce" else "ggn_mse"
+    snap = P.make_snapshot(kind, m, w, batch)
+    assert rel(snap.row.rhs, k("rhs")) < REL
+    assert rel(snap.row.gram(), k("gram")) < REL
+    v = snap.row.solve_cholesky(float(k("mu")))
+    assert rel(snap.row.scaled_row_transpose(v).data, k("rowdir")) < REL
+
+
+def test_row_not_pd_raises(golden):
+    m, w, batch, k = _case(golden, "relu_ce")
+    snap = P.make_snapshot("ggn_ce", m, w, batch)
+    with pytest.raises(P.ContractError, match="not positive definite"):
+        snap.row.solve_cholesky(-1e6)
+
+
+def _rows(infos):
+    return np.array([i.to_row() for i in infos], dtype=np.float64)
+
+
+def _cmp_info(mine, ref, rtol):
+    mine = np.asarray(mine, dtype=np.float64)
+    assert np.array_equal(np.isnan(mine), np.isnan(ref)), "sentinel placement differs"
+    ints = [P.STEP_INFO_FIELDS.index(f) for f in ("solver_iterations", "solver_converged", "step_index")]
+    assert np.array_equal(mine[..., ints], ref[..., ints])
+    ok = ~np.isnan(ref)
+    np.testing.assert_allclose(mine[ok], ref[ok], rtol=rtol, atol=1e-7)
+
+
+def _spec_c1(**kw):
+    cg = P.CgConfig(tol=1e-5, maxiter=kw.pop("maxiter", 10), stabilise_every=10, warm_start=True)
+    return P.MethodSpec(curvature=P.CurvatureSpec(kw.pop("curvature", "ggn_ce")),
+                        solver=P.SolverSpec(kw.pop("solver", "cg"), cg), precond=kw.pop("precond", None),
+                        damping=kw.pop("damping", P.DampingSpec("constant", 1.0)),
+                        estimator=kw.pop("estimator", None), telemetry=kw.pop("telemetry", P.TelemetrySpec()),
+                        chain=(P.transforms.scale(1e-3), P.transforms.scale(-1.0)))
+
+
+def test_c1_planned_step(golden):
+    g = golden("trajectories")
+    m = P.Model(784, (128,), 10, "relu")
+    w = P.init_params(m, P.Rng(0))
+    X, y = O.synthetic_batch(128, 784, 10)
+    batch = P.Batch(X, y, "ce")
+    meth = P.assemble(_spec_c1(), m)
+    st = meth.init(w, 0)
+    w1, st, info = meth.step(w, batch, st)
+    _cmp_info(info.to_row(), g["c1/info0"], rtol=2e-4)
+    assert rel(st.warm_start, g["c1/direction"]) < REL
+    w2, st, info = meth.step(w1, batch, st)
+    _cmp_info(info.to_row(), g["c1/info1"], rtol=2e-4)
+
+
+def test_c2_trajectory_loss_tracks_within_1e3(golden):
+    g = golden("trajectories")
+    ref = g["c2/info"]
+    m = P.Model(784, (128,), 10, "relu")
+    (Xtr, ytr), _ = O.gen_classification(20000, 784, 10, 10.0, 0)
+    bat = O.Batcher(Xtr, ytr, 128, O.ORng(0).split())
+    spec = _spec_c1(damping=P.DampingSpec("trust_region", 1.0, P.control.TrustRegionConfig(every_k=5)),
+                    estimator=P.EstimatorSpec("hutchinson", 1, every_k=10))
+    meth = P.assemble(spec, m)
+    w = P.init_params(m, P.Rng(0)).to_device()
+    st = meth.init(w, 0)
+    rows = []
+    for _ in range(100):
+        X, y = bat.next()
+        w, st, info = meth.step(w, P.Batch(X, y, "ce"), st)
+        rows.append(info.to_row())
+    rows = np.array(rows, dtype=np.float64)
+    li = P.STEP_INFO_FIELDS.index("loss_before")
+    loss_rel = np.abs(rows[:, li] - ref[:, li]) / np.abs(ref[:, li])
+    assert loss_rel.max() < 1e-3, loss_rel.max()
+    # plan output (gating / sentinels / lane) bit-exact
+    assert np.array_equal(np.isnan(rows), np.isnan(ref))
+    lam_i = P.STEP_INFO_FIELDS.index("lam")
+    np.testing.assert_allclose(rows[:, lam_i], ref[:, lam_i], rtol=1e-12)
+
+
+def test_c3_reduced_pcg(golden):
+    g = golden("trajectories")
+    m = P.Model(784, (1024, 1024), 10, "relu")
+    w = P.init_params(m, P.Rng(0))
+    X, y = O.synthetic_batch(256, 784, 10)
+    spec = _spec_c1(precond=P.PrecondSpec("diag_ema", 0.99), estimator=P.EstimatorSpec("hutchinson", 1, every_k=2))
+    meth = P.assemble(spec, m)
+    st = meth.init(w, 0)
+    batch = P.Batch(X, y, "ce")
+    rows = []
+    for _ in range(3):
+        w, st, info = meth.step(w, batch, st)
+        rows.append(info.to_row())
+    _cmp_info(np.array(rows), g["c3r/info"], rtol=1e-3)
+
+
+def test_c4_reduced_row_lane(golden):
+    g = golden("trajectories")
+    m = P.Model(96, (64, 64), 10, "relu")
+    w = P.init_params(m, P.Rng(0))
+    X, y = O.synthetic_batch(32, 96, 10)
+    meth = P.assemble(_spec_c1(solver="row_cholesky"), m)
+    st = meth.init(w, 0)
+    batch = P.Batch(X, y, "ce")
+    rows = []
+    for _ in range(2):
+        w, st, info = meth.step(w, batch, st)
+        rows.append(info.to_row())
+    _cmp_info(np.array(rows), g["c4r/info"], rtol=1e-4)
+    assert rel(w.data, g["c4r/w_final"]) < 1e-6
+
+
+def test_c5_reduced_hessian(golden):
+    g = golden("trajectories")
+    m = P.Model(48, (32, 32, 32, 32), 10, "relu")
+    w = P.init_params(m, P.Rng(0))
+    X, y = O.synthetic_batch(64, 48, 10)
+    spec = _spec_c1(curvature="hessian", estimator=P.EstimatorSpec("hutchinson", 1, every_k=1),
+                    telemetry=P.TelemetrySpec(trace_every_k=1, trace_probes=2, rho_every_k=2))
+    meth = P.assemble(spec, m)
+    st = meth.init(w, 0)
+    batch = P.Batch(X, y, "ce")
+    rows = []
+    for _ in range(3):
+        w, st, info = meth.step(w, batch, st)
+        rows.append(info.to_row())
+    _cmp_info(np.array(rows), g["c5r/info"], rtol=1e-3)
+
+
+def test_c3_full_size_gv_and_step_vs_oracle():
+    """784-1024-1024-10 at b=8192: one GGN product and one planned step vs the oracle."""
+    dims = (784, 1024, 1024, 10)
+    m = P.Model(784, (1024, 1024), 10, "relu")
+    w = P.init_params(m, P.Rng(0))
+    X, y = O.synthetic_batch(8192, 784, 10)
+    lin = O.linearize(dims, "relu", "ce", w.data, X, y)
+    snap = P.make_snapshot("ggn_ce", m, w, P.Batch(X, y, "ce"))
+    assert snap.loss_before == pytest.approx(lin.value, rel=1e-5)
+    assert rel(snap.grad.data, lin.grad) < REL
+    v = O.ORng(2).normal(w.dim)
+    assert rel(snap.matvec(P.ParamVector(v, w.layout)).data, O.ggn_matvec(lin, v)) < REL
+    # symmetry of the device operator at full size (size-independent property)
+    u = O.ORng(3).normal(w.dim)
+    gv = snap.matvec(P.ParamVector(v, w.layout)).data.double().cpu().numpy()
+    gu = snap.matvec(P.ParamVector(u, w.layout)).data.double().cpu().numpy()
+    assert abs(u @ gv - v @ gu) <= 1e-5 * abs(u @ gv)
