@@ -19,10 +19,12 @@ CV_DEV float tf32_rna(float x) {
   return __uint_as_float(r);
 }
 
-// x ~= hi + lo with hi, lo both exact tf32 values (|x - hi - lo| <= 2^-22 |x|).
+// x = hi + lo exactly: hi is the tf32 rounding of x, lo = x - hi (exact in fp32,
+// <= 13 significant bits).  The tensor core reads lo at tf32 precision, so the
+// 3xTF32 product sees x to 2^-21; the SIMT path (hi + lo) sees x exactly.
 CV_DEV void split2(float x, float& hi, float& lo) {
   hi = tf32_rna(x);
-  lo = tf32_rna(x - hi);
+  lo = x - hi;
 }
 
 CV_DEV float relu_f(float x) { return x > 0.f ? x : 0.f; }

@@ -58,7 +58,9 @@ class Batch:
             if X.dim() != 2 or X.shape[0] < 1:
                 raise ContractError("batch inputs must be a (b, input_dim) matrix with b >= 1")
         else:
-            X = np.asarray(X, dtype=np.float64)
+            # float32 host arrays stay float32 (the device precision); anything else
+            # is coerced to float64 like the reference Batch (models.py:60)
+            X = np.asarray(X) if getattr(X, "dtype", None) == np.float32 else np.asarray(X, dtype=np.float64)
             if X.ndim != 2 or X.shape[0] < 1:
                 raise ContractError("batch inputs must be a (b, input_dim) matrix with b >= 1")
             object.__setattr__(self, "inputs", X)
@@ -113,12 +115,12 @@ class Batch:
             return hit
         X, y = self.inputs, self.targets
         if _is_torch(X):
-            Xd = X.to(device=device, dtype=torch.float32).contiguous()
+            Xd = X.to(device=device, dtype=torch.float32, non_blocking=True).contiguous()
         else:
             Xd = torch.from_numpy(np.ascontiguousarray(X, dtype=np.float32)).pin_memory().to(device, non_blocking=True)
         if self.loss_kind == "ce":
             if _is_torch(y):
-                yd = y.to(device=device, dtype=torch.int64).contiguous()
+                yd = y.to(device=device, dtype=torch.int64, non_blocking=True).contiguous()
             else:
                 yd = torch.from_numpy(np.ascontiguousarray(y, dtype=np.int64)).pin_memory().to(device, non_blocking=True)
         else:

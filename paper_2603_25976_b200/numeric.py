@@ -42,7 +42,8 @@ class ParamVector:
                 d = d.contiguous()
             n = d.numel()
         else:
-            d = np.asarray(d, dtype=np.float64).reshape(-1)
+            # host: float64 like the reference (numeric.py:41-45); float32 is kept as is
+            d = (np.asarray(d) if getattr(d, "dtype", None) == np.float32 else np.asarray(d, dtype=np.float64)).reshape(-1)
             n = d.size
         object.__setattr__(self, "data", d)
         if n != layout_size(self.layout):
@@ -50,11 +51,11 @@ class ParamVector:
 
     @property
     def dim(self) -> int:
-        return int(self.data.numel() if self.on_device else self.data.size)
+        return int(self.data.numel() if _is_torch(self.data) else self.data.size)
 
     @property
     def on_device(self) -> bool:
-        return _is_torch(self.data)
+        return _is_torch(self.data) and self.data.is_cuda
 
     def like(self, data) -> "ParamVector":
         return ParamVector(data, self.layout)
@@ -88,13 +89,22 @@ class ParamVector:
         import torch
 
         dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        if _is_torch(self.data):  # host torch tensor (pinned for async copies)
+            return self.like(self.data.to(device=dev, dtype=torch.float32, non_blocking=True))
         t = torch.from_numpy(np.ascontiguousarray(self.data, dtype=np.float32))
-        return self.like(t.pin_memory().to(dev, non_blocking=True) if dev.type == "cuda" else t)
+        return self.like(t.to(dev))
 
-    def to_host(self) -> "ParamVector":
+    def to_host(self, like: "ParamVector | None" = None) -> "ParamVector":
+        """Device -> host as float32 (numpy, or a torch CPU tensor when `like` is one)."""
         if not self.on_device:
             return self
-        return self.like(self.data.detach().double().cpu().numpy())
+        if like is not None and _is_torch(like.data):
+            import torch
+
+            host = torch.empty(self.data.shape, dtype=self.data.dtype, pin_memory=True)  # caching host allocator
+            host.copy_(self.data)
+            return self.like(host)
+        return self.like(self.data.detach().cpu().numpy())
 
     def numpy(self) -> np.ndarray:
         return self.to_host().data
