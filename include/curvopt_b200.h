@@ -102,6 +102,8 @@ CV_API int cv_linearize(cv_ctx* ctx, int n_layers, const int* dims, int act, int
 CV_API int cv_snap_free(cv_snap* snap);
 CV_API int64_t cv_snap_dim(const cv_snap* snap);
 CV_API int cv_snap_outputs(cv_snap* snap, float* out /* b_local*c logits */);
+/* hidden activation a_layer (1 <= layer < n_layers), b_local x dims[layer], fp32 */
+CV_API int cv_snap_activation(cv_snap* snap, int layer, float* out);
 
 /* ---- curvature products ------------------------------------------------- */
 CV_API int cv_matvec(cv_snap* snap, int kind, const float* v, float* out);

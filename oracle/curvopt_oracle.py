@@ -185,8 +185,13 @@ def loss_value(dims, activation, loss, flat, X, y) -> float:
     return _ce_value(out, y)
 
 
-def linearize(dims, activation, loss, flat, X, y) -> Lin:
-    """Forward, loss, primal backward and gradient (models.py:337-396)."""
+def linearize(dims, activation, loss, flat, X, y, masks=None) -> Lin:
+    """Forward, loss, primal backward and gradient (models.py:337-396).
+
+    `masks` (relu only, test instrumentation): per hidden layer the boolean
+    "z > 0" pattern to use instead of the oracle's own -- the "identical inputs"
+    override that removes fp32-vs-f64 ReLU kink flips from a parity comparison
+    (hard part 2)."""
     X = np.asarray(X, dtype=np.float64)
     layers = split_params(dims, np.asarray(flat, dtype=np.float64))
     L = len(layers)
@@ -198,8 +203,9 @@ def linearize(dims, activation, loss, flat, X, y) -> Lin:
             out = z
             break
         if activation == "relu":
-            a = np.maximum(z, 0.0)
-            sp.append((z > 0.0).astype(np.float64))
+            keep = (z > 0.0) if masks is None else np.asarray(masks[i], dtype=bool)
+            a = np.where(keep, z, 0.0)
+            sp.append(keep.astype(np.float64))
         else:
             a = np.tanh(z)
             sp.append(1.0 - a * a)

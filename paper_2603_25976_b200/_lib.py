@@ -45,6 +45,7 @@ _SIGS = {
     "cv_snap_free": (C.c_int, [_P]),
     "cv_snap_dim": (C.c_int64, [_P]),
     "cv_snap_outputs": (C.c_int, [_P, _P]),
+    "cv_snap_activation": (C.c_int, [_P, C.c_int, _P]),
     "cv_matvec": (C.c_int, [_P, C.c_int, _P, _P]),
     "cv_jvp": (C.c_int, [_P, _P, _P]),
     "cv_vjp": (C.c_int, [_P, _P, _P]),

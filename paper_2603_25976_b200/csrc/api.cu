@@ -214,6 +214,14 @@ int cv_snap_outputs(cv_snap* s, float* out) {
   CV_CATCH
 }
 
+int cv_snap_activation(cv_snap* s, int layer, float* out) {
+  if (!s) return CV_E_CONTRACT;
+  CV_TRY(s->ctx)
+  contract(layer >= 1 && layer < s->L, "activation layer out of range");
+  gather_rows(_ctx, s->acts[layer], s->bl, s->dims[layer], out);
+  CV_CATCH
+}
+
 int cv_matvec(cv_snap* s, int kind, const float* v, float* out) {
   if (!s) return CV_E_CONTRACT;
   CV_TRY(s->ctx)

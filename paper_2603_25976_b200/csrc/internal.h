@@ -168,6 +168,7 @@ void split_vec(cv_ctx* ctx, const float* x, float* hi, float* lo, int64_t n, con
 void split_rows(cv_ctx* ctx, const float* src, int64_t lds, int rows, int cols, const SplitBuf& dst, int ones);
 void set_ones_col(cv_ctx* ctx, const SplitBuf& b, int rows, int col);
 void set_col_value(cv_ctx* ctx, const SplitBuf& b, int rows, int col, float v);
+void gather_rows(cv_ctx* ctx, const SplitBuf& b, int rows, int cols, float* out);  // out = hi + lo
 void mlp_linearize(cv_ctx* ctx, cv_snap* s, double* loss_out, float* grad_out);
 void mlp_ggn(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, float* out, const int* skip);
 void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, float* out, const int* skip);

@@ -695,6 +695,19 @@ void set_col_value(cv_ctx* ctx, const SplitBuf& b, int rows, int col, float v) {
 
 void set_ones_col(cv_ctx* ctx, const SplitBuf& b, int rows, int col) { set_col_value(ctx, b, rows, col, 1.f); }
 
+__global__ void k_gather_rows(const float* hi, const float* lo, int64_t ld, int rows, int cols, float* out) {
+  const int64_t total = (int64_t)rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i - r * cols;
+    out[i] = hi[r * ld + c] + lo[r * ld + c];
+  }
+}
+
+void gather_rows(cv_ctx* ctx, const SplitBuf& b, int rows, int cols, float* out) {
+  k_gather_rows<<<grid_for((int64_t)rows * cols), 256, 0, ctx->stream>>>(b.hi, b.lo, b.ld, rows, cols, out);
+  ctx->launches++;
+}
+
 void split_rows(cv_ctx* ctx, const float* src, int64_t lds, int rows, int cols, const SplitBuf& dst, int ones) {
   k_split_rows<<<grid_for((int64_t)rows * (cols + 1)), 256, 0, ctx->stream>>>(src, lds, rows, cols, dst.hi, dst.lo,
                                                                                dst.ld, ones);

@@ -20,7 +20,7 @@ constexpr int CH_NB = 64;  // Cholesky block size
 // root with the reference's floor (1e-10 * max(lambda_max, 0)).  MSE: identity.
 // ---------------------------------------------------------------------------
 template <int CM>
-__global__ void k_hz_roots(const float* probs, const float* gout, int b, int c, int loss, float bscale,
+__global__ void k_hz_roots(const float* logits, const int64_t* yi, const float* yf, int b, int c, int loss,
                            float* seeds, float* pinv, float* rhs) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= b) return;
@@ -31,14 +31,22 @@ __global__ void k_hz_roots(const float* probs, const float* gout, int b, int c, 
         seeds[i * cc + a * c + j] = a == j ? 1.f : 0.f;
         pinv[i * cc + a * c + j] = a == j ? 1.f : 0.f;
       }
-      rhs[(size_t)i * c + a] = gout[(size_t)i * c + a] * bscale;
+      rhs[(size_t)i * c + a] = (float)((double)logits[(size_t)i * c + a] - (double)yf[(size_t)i * c + a]);
     }
     return;
   }
+  // softmax in fp64 from the logits (models.py:371-377)
   double H[CM][CM], Q[CM][CM], p[CM];
   bool finite = true;
+  double mx = logits[(size_t)i * c];
+  for (int a = 1; a < c; ++a) mx = fmax(mx, (double)logits[(size_t)i * c + a]);
+  double se = 0.0;
   for (int a = 0; a < c; ++a) {
-    p[a] = probs[(size_t)i * c + a];
+    p[a] = exp((double)logits[(size_t)i * c + a] - mx);
+    se += p[a];
+  }
+  for (int a = 0; a < c; ++a) {
+    p[a] /= se;
     finite = finite && isfinite(p[a]);
   }
   if (!finite) {
@@ -93,7 +101,7 @@ __global__ void k_hz_roots(const float* probs, const float* gout, int b, int c, 
     ri[a] = keep ? 1.0 / r[a] : 0.0;
   }
   double og[CM];
-  for (int a = 0; a < c; ++a) og[a] = (double)gout[(size_t)i * c + a] * bscale;
+  for (int a = 0; a < c; ++a) og[a] = p[a] - (a == yi[i] ? 1.0 : 0.0);
   for (int a = 0; a < c; ++a) {
     double acc_rhs = 0.0;
     for (int j = 0; j < c; ++j) {
@@ -145,12 +153,11 @@ static void ensure_seeds(cv_ctx* ctx, cv_snap* s) {
   s->seeds = snap_alloc(s, (int64_t)b * c * c);
   s->pinv = snap_alloc(s, (int64_t)b * c * c);
   s->rhs = snap_alloc(s, (int64_t)b * c);
-  // gout = out_grad / b_global  ->  out_grad = gout * b_global
   if (c <= 16)
-    k_hz_roots<16><<<(b + 63) / 64, 64, 0, ctx->stream>>>(s->probs, s->gout, b, c, s->loss, (float)s->bg, s->seeds,
+    k_hz_roots<16><<<(b + 63) / 64, 64, 0, ctx->stream>>>(s->logits, s->y_i, s->y_f, b, c, s->loss, s->seeds,
                                                           s->pinv, s->rhs);
   else
-    k_hz_roots<32><<<(b + 31) / 32, 32, 0, ctx->stream>>>(s->probs, s->gout, b, c, s->loss, (float)s->bg, s->seeds,
+    k_hz_roots<32><<<(b + 31) / 32, 32, 0, ctx->stream>>>(s->logits, s->y_i, s->y_f, b, c, s->loss, s->seeds,
                                                           s->pinv, s->rhs);
   ctx->launches++;
   s->row_state |= 1;

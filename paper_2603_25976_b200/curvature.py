@@ -186,6 +186,13 @@ class Snapshot:
         self.rt.call("cv_snap_outputs", self.h, out.data_ptr())
         return out
 
+    def activation(self, layer: int):
+        """Hidden activation a_layer (b x n_layer) as stored on the device (fp32)."""
+        out = torch.empty((self.batch_local, self.model.dims[layer]), dtype=torch.float32, device=self.rt.device)
+        self.rt.bind_stream()
+        self.rt.call("cv_snap_activation", self.h, int(layer), out.data_ptr())
+        return out
+
     def loss_at_dev(self, w: torch.Tensor, out: torch.Tensor) -> None:
         self.rt.bind_stream()
         self.rt.call("cv_loss_at", self.h, w.data_ptr(), out.data_ptr())

@@ -278,8 +278,17 @@ def test_c3_full_size_gv_and_step_vs_oracle():
     m = P.Model(784, (1024, 1024), 10, "relu")
     w = P.init_params(m, P.Rng(0))
     X, y = O.synthetic_batch(8192, 784, 10)
-    lin = O.linearize(dims, "relu", "ce", w.data, X, y)
     snap = P.make_snapshot("ggn_ce", m, w, P.Batch(X, y, "ce"))
+    # ReLU kink flips: pre-activations within fp32 noise of 0 take a different
+    # branch than the f64 oracle; compare against the oracle run with the
+    # device's masks and report the flip count (hard part 2).
+    masks = [(snap.activation(l) > 0).cpu().numpy() for l in (1, 2)]
+    lin0 = O.linearize(dims, "relu", "ce", w.data, X, y)
+    flips = sum(int(np.sum(mk != (s > 0))) for mk, s in zip(masks, lin0.sp))
+    lin = O.linearize(dims, "relu", "ce", w.data, X, y, masks=masks)
+    print(f"relu mask flips vs f64 oracle: {flips} of {2 * 8192 * 1024}; raw grad rel err "
+          f"{rel(snap.grad.data, lin0.grad):.2e}")
+    assert flips < 100
     assert snap.loss_before == pytest.approx(lin.value, rel=1e-5)
     assert rel(snap.grad.data, lin.grad) < REL
     v = O.ORng(2).normal(w.dim)
