@@ -136,6 +136,13 @@ CV_API int cv_apply_update(cv_ctx* ctx, const float* w, const float* direction, 
 /* scal[0] = ||x||^2, scal[1] = #nonfinite(x) (device doubles). */
 CV_API int cv_norm_check(cv_ctx* ctx, const float* x, int64_t d, double* scal);
 
+/* ---- engine unit test ----------------------------------------------------- */
+/* out[M x N] (ld ldo) = A B with A, B given as fp32 (split inside): A(m,k) =
+ * a[m*lda + k] if a_kmajor else a[k*lda + m]; B(k,n) = b[k*ldb + n] if !b_kmajor
+ * else b[n*ldb + k].  engine: CV_ENGINE_SIMT or CV_ENGINE_TC (strict). */
+CV_API int cv_gemm_test(cv_ctx* ctx, int engine, int M, int N, int K, const float* a, int64_t lda, int a_kmajor,
+                        const float* b, int64_t ldb, int b_kmajor, float* out, int64_t ldo);
+
 /* ---- row lane ------------------------------------------------------------- */
 CV_API int64_t cv_row_dim(const cv_snap* snap);                        /* m = b * c */
 CV_API int cv_row_rhs(cv_snap* snap, float* rhs_out /* m */);

@@ -59,6 +59,8 @@ _SIGS = {
     "cv_rho_terms": (C.c_int, [_P, C.c_int, _P, _P, _P, _P]),
     "cv_apply_update": (C.c_int, [_P, _P, _P, C.c_double, C.c_int64, _P, _P, _P]),
     "cv_norm_check": (C.c_int, [_P, _P, C.c_int64, _P]),
+    "cv_gemm_test": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, _P, C.c_int64, C.c_int, _P, C.c_int64,
+                               C.c_int, _P, C.c_int64]),
     "cv_row_dim": (C.c_int64, [_P]),
     "cv_row_rhs": (C.c_int, [_P, _P]),
     "cv_row_gram": (C.c_int, [_P, _P]),

@@ -323,6 +323,37 @@ int cv_norm_check(cv_ctx* ctx, const float* x, int64_t d, double* scal) {
   CV_CATCH
 }
 
+int cv_gemm_test(cv_ctx* ctx, int engine, int M, int N, int K, const float* a, int64_t lda, int a_kmajor,
+                 const float* b, int64_t ldb, int b_kmajor, float* out, int64_t ldo) {
+  CV_TRY(ctx)
+  const int64_t na = a_kmajor ? (int64_t)M * lda : (int64_t)K * lda;
+  const int64_t nb = b_kmajor ? (int64_t)N * ldb : (int64_t)K * ldb;
+  float* buf = (float*)_ctx->pool.get(sizeof(float) * (size_t)(2 * na + 2 * nb));
+  float *ahi = buf, *alo = buf + na, *bhi = buf + 2 * na, *blo = buf + 2 * na + nb;
+  split_vec(_ctx, a, ahi, alo, na, nullptr);
+  split_vec(_ctx, b, bhi, blo, nb, nullptr);
+  GemmArgs g;
+  g.M = M;
+  g.N = N;
+  g.nseg = 1;
+  g.seg[0].A = a_kmajor ? Operand{ahi, alo, lda, 1} : Operand{ahi, alo, 1, lda};
+  g.seg[0].B = b_kmajor ? Operand{bhi, blo, 1, ldb} : Operand{bhi, blo, ldb, 1};
+  g.seg[0].K = K;
+  g.epi.mode = EPI_STORE;
+  g.epi.out = out;
+  g.epi.ld = ldo;
+  if (engine == CV_ENGINE_TC || engine == 3) {
+    contract(gemm_tc_supported(g), "shape/alignment not supported by the tensor-core engine");
+    if (engine == 3) g_tc_debug = out + (int64_t)M * ldo;  // caller provides room for one smem stage
+    gemm_tc(_ctx, g);
+    g_tc_debug = nullptr;
+  } else {
+    gemm_simt(_ctx, g);
+  }
+  _ctx->pool.put(buf);
+  CV_CATCH
+}
+
 int64_t cv_row_dim(const cv_snap* s) { return s ? (int64_t)s->bl * s->c : -1; }
 
 int cv_row_rhs(cv_snap* s, float* rhs_out) {

@@ -46,6 +46,7 @@ struct TcArgs {
   const int* skip;
   int lower_only;
   float* partial;     // split-K partials (nullptr: apply the epilogue directly)
+  float* dbg;         // debug: copy of smem stage 0 (block 0,0,0)
 };
 
 // ---------------------------------------------------------------------------
@@ -83,14 +84,16 @@ CV_DEV void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
 
-// UMMA shared-memory descriptor, SWIZZLE_128B, version 1 (sm_100).
-CV_DEV uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// UMMA shared-memory descriptor, version 1 (sm_100).  layout: 2 = SWIZZLE_128B
+// (K-major: 16 B granules, 8-row atoms), 1 = SWIZZLE_128B_BASE32B (the only
+// MN-major layout for 32-bit operands: 32 B granules, 4-row atoms).
+CV_DEV uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
   d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;   // version
-  d |= (uint64_t)2 << 61;   // SWIZZLE_128B
+  d |= (uint64_t)layout << 61;
   return d;
 }
 
@@ -223,12 +226,16 @@ __global__ void __launch_bounds__(128, 1) k_gemm_tc(const __grid_constant__ TcMa
       const uint32_t b_hi = st + 2 * Cfg::A_BYTES, b_lo = b_hi + Cfg::B_BYTES;
 #pragma unroll
       for (int kk = 0; kk < TC_BK / 8; ++kk) {
-        // K-major: +32 B inside the 128 B swizzled row; MN-major: +8 rows = +1024 B
+        // K-major (SW128): rows of 128 B, 8-row atoms (SBO 1024), k-step = +32 B in the row.
+        // MN-major (SW128_BASE32B): 32-wide MN chunks 4 KB apart (LBO), K rows of 128 B in
+        // 4-row atoms (SBO 512), k-step = 8 rows = +1024 B.
         const uint32_t aoff = amn ? kk * 1024 : kk * 32;
         const uint32_t boff = bmn ? kk * 1024 : kk * 32;
         const uint32_t albo = amn ? 4096 : 16, blbo = bmn ? 4096 : 16;
-        const uint64_t dah = umma_desc(a_hi + aoff, albo, 1024), dal = umma_desc(a_lo + aoff, albo, 1024);
-        const uint64_t dbh = umma_desc(b_hi + boff, blbo, 1024), dbl = umma_desc(b_lo + boff, blbo, 1024);
+        const uint32_t asbo = amn ? 512 : 1024, bsbo = bmn ? 512 : 1024;
+        const uint32_t alay = amn ? 1 : 2, blay = bmn ? 1 : 2;
+        const uint64_t dah = umma_desc(a_hi + aoff, albo, asbo, alay), dal = umma_desc(a_lo + aoff, albo, asbo, alay);
+        const uint64_t dbh = umma_desc(b_hi + boff, blbo, bsbo, blay), dbl = umma_desc(b_lo + boff, blbo, bsbo, blay);
         const uint32_t acc0 = (i > 0 || kk > 0) ? 1u : 0u;
         umma_tf32(tmem, dah, dbh, idesc, acc0);
         umma_tf32(tmem, dah, dbl, idesc, 1u);
@@ -272,6 +279,10 @@ __global__ void __launch_bounds__(128, 1) k_gemm_tc(const __grid_constant__ TcMa
       }
     }
   }
+  if (a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+    const float* src = (const float*)smem;
+    for (int i = threadIdx.x; i < Cfg::STAGE_BYTES / 4; i += blockDim.x) a.dbg[i] = src[i];
+  }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1) {
@@ -311,9 +322,10 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 struct MapKey {
   const void* ptr;
   int64_t inner, outer, ld;
-  int box0, box1;
+  int box0, box1, mn;
   bool operator==(const MapKey& o) const {
-    return ptr == o.ptr && inner == o.inner && outer == o.outer && ld == o.ld && box0 == o.box0 && box1 == o.box1;
+    return ptr == o.ptr && inner == o.inner && outer == o.outer && ld == o.ld && box0 == o.box0 && box1 == o.box1 &&
+           mn == o.mn;
   }
 };
 struct MapKeyHash {
@@ -322,16 +334,18 @@ struct MapKeyHash {
     h = h * 1000003u ^ (size_t)k.inner;
     h = h * 1000003u ^ (size_t)k.outer;
     h = h * 1000003u ^ (size_t)k.ld;
-    h = h * 1000003u ^ (size_t)(k.box0 * 4096 + k.box1);
+    h = h * 1000003u ^ (size_t)(k.box0 * 4096 + k.box1 * 2 + k.mn);
     return h;
   }
 };
 
-// 2D fp32 map: dims {inner, outer}, row stride ld elements, SWIZZLE_128B, OOB zero fill.
-static CUtensorMap make_map(const float* ptr, int64_t inner, int64_t outer, int64_t ld, int box0, int box1) {
+// 2D fp32 map: dims {inner, outer}, row stride ld elements, OOB zero fill; K-major
+// operands use SWIZZLE_128B, MN-major ones SWIZZLE_128B_ATOM_32B (UMMA BASE32B).
+static CUtensorMap make_map(const float* ptr, int64_t inner, int64_t outer, int64_t ld, int box0, int box1,
+                            int mn) {
   static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
   static std::mutex mu;
-  MapKey key{ptr, inner, outer, ld, box0, box1};
+  MapKey key{ptr, inner, outer, ld, box0, box1, mn};
   {
     std::lock_guard<std::mutex> g(mu);
     auto it = cache.find(key);
@@ -345,7 +359,8 @@ static CUtensorMap make_map(const float* ptr, int64_t inner, int64_t outer, int6
   cuuint32_t box[2] = {(cuuint32_t)box0, (cuuint32_t)box1};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)ptr, dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, mn ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   std::lock_guard<std::mutex> g(mu);
@@ -353,6 +368,8 @@ static CUtensorMap make_map(const float* ptr, int64_t inner, int64_t outer, int6
   cache.emplace(key, m);
   return m;
 }
+
+float* g_tc_debug = nullptr;  // set by cv_gemm_test's debug mode
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
@@ -399,8 +416,8 @@ static void launch_tc(cv_ctx* ctx, const GemmArgs& g, int splits) {
     for (int h = 0; h < 2; ++h) {
       const float* pa = h ? sg.A.lo : sg.A.hi;
       const float* pb = h ? sg.B.lo : sg.B.hi;
-      maps.m[s][h] = akm ? make_map(pa, sg.K, g.M, lda, TC_BK, TC_BM) : make_map(pa, g.M, sg.K, lda, 32, TC_BK);
-      maps.m[s][2 + h] = bkm ? make_map(pb, sg.K, g.N, ldb, TC_BK, BN) : make_map(pb, g.N, sg.K, ldb, 32, TC_BK);
+      maps.m[s][h] = akm ? make_map(pa, sg.K, g.M, lda, TC_BK, TC_BM, 0) : make_map(pa, g.M, sg.K, lda, 32, TC_BK, 1);
+      maps.m[s][2 + h] = bkm ? make_map(pb, sg.K, g.N, ldb, TC_BK, BN, 0) : make_map(pb, g.N, sg.K, ldb, 32, TC_BK, 1);
     }
   }
   if (g.nseg < 2) a.kb[1] = 0;
@@ -408,6 +425,7 @@ static void launch_tc(cv_ctx* ctx, const GemmArgs& g, int splits) {
   a.skip = g.skip;
   a.lower_only = g.lower_only;
   a.kb_per_split = (a.kb_total + splits - 1) / splits;
+  a.dbg = g_tc_debug;
   splits = (a.kb_total + a.kb_per_split - 1) / a.kb_per_split;
   float* part = nullptr;
   if (splits > 1) {
