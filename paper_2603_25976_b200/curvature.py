@@ -11,6 +11,7 @@ reference's test instrumentation, curvature.py:24-29).
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 
 import numpy as np
 import torch
@@ -43,7 +44,9 @@ class RowOps:
     """Row-space primitives of a GGN snapshot (curvature.py:32-65)."""
 
     def __init__(self, snap: "Snapshot"):
-        self._snap = snap
+        # weak: a strong back-reference would make every snapshot a GC cycle and keep
+        # its device buffers alive until the next collection
+        self._snap = weakref.proxy(snap)
         self.m = snap.batch_local * snap.model.output_dim
         self._rhs = None
         self._gram = None
