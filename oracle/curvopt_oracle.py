@@ -591,11 +591,11 @@ def oracle_init(spec: OSpec, d: int, seed: int = 0) -> OState:  # method.py:286-
     return OState(spec.lam0, np.zeros(d), chain_init(spec.chain, d), None, 0, ORng(seed))
 
 
-def oracle_step(spec: OSpec, dims, activation, loss, w, X, y, st: OState, gv_log=None):
+def oracle_step(spec: OSpec, dims, activation, loss, w, X, y, st: OState, gv_log=None, masks=None):
     """One planned step; returns (w', state', info dict, direction).  method.py:302-389."""
     t = st.t
     rng = st.rng.clone()
-    lin = linearize(dims, activation, loss, w, X, y)
+    lin = linearize(dims, activation, loss, w, X, y, masks=masks)
     kind = spec.curvature
     mv = lambda v: matvec(lin, kind, v)  # noqa: E731
     g = lin.grad

@@ -19,12 +19,14 @@ CV_DEV float tf32_rna(float x) {
   return __uint_as_float(r);
 }
 
-// x = hi + lo exactly: hi is the tf32 rounding of x, lo = x - hi (exact in fp32,
-// <= 13 significant bits).  The tensor core reads lo at tf32 precision, so the
-// 3xTF32 product sees x to 2^-21; the SIMT path (hi + lo) sees x exactly.
+// x ~= hi + lo, both exact tf32 values (|x - hi - lo| <= 2^-22 |x|).  lo is rounded
+// to nearest here rather than left with 13 significant bits: the tensor core
+// truncates operand bits beyond tf32, which biases every 3xTF32 product toward
+// zero (measured -8e-7 relative, amplified ~20x by the per-example cancellation
+// in the weight gradients).
 CV_DEV void split2(float x, float& hi, float& lo) {
   hi = tf32_rna(x);
-  lo = x - hi;
+  lo = tf32_rna(x - hi);
 }
 
 CV_DEV float relu_f(float x) { return x > 0.f ? x : 0.f; }

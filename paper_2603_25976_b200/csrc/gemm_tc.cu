@@ -8,10 +8,10 @@
 // either K-major (K contiguous) or MN-major (M/N contiguous); both are native
 // tcgen05 operand majors for tf32, so no transposed copies exist anywhere.
 //
-// One CTA = one 128 x BN output tile (BN = 128 or 256), 4 warps:
+// One CTA = one 128 x BN output tile (BN = 128 or 256), 8 warps:
 //   warp 0 lane 0 : TMA producer      (cp.async.bulk.tensor.2d, SWIZZLE_128B)
 //   warp 1 lane 0 : MMA issuer        (tcgen05.mma.cta_group::1.kind::tf32)
-//   warps 0-3     : epilogue          (tcgen05.ld 32x32b -> registers -> fused epilogue)
+//   warps 0-7     : epilogue          (tcgen05.ld 32x32b -> registers -> 128-bit fused epilogue)
 // smem ring of STAGES x {A_hi, A_lo, B_hi, B_lo} 32-wide K slabs, full/empty
 // mbarriers between TMA and MMA, tcgen05.commit frees a slab / signals the epilogue.
 // Split-K (grid.z) writes fp32 partials that a fixed-order reduction folds in.
@@ -146,7 +146,7 @@ struct TcCfg {
 };
 
 template <int BN, int STAGES>
-__global__ void __launch_bounds__(128, 1) k_gemm_tc(const __grid_constant__ TcMaps maps, const TcArgs a) {
+__global__ void __launch_bounds__(256, 1) k_gemm_tc(const __grid_constant__ TcMaps maps, const TcArgs a) {
   using Cfg = TcCfg<BN, STAGES>;
   if (skip_if(a.skip)) return;
   const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * BN;
@@ -252,10 +252,13 @@ __global__ void __launch_bounds__(128, 1) k_gemm_tc(const __grid_constant__ TcMa
     mbar_wait(done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   }
-  const int m = m0 + warp * 32 + lane;
-  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  // 8 warps: warp w reads TMEM lane quadrant (w % 4) -> rows m0 + 32 (w % 4) + lane, and
+  // the column half (w / 4) of the tile.
+  const int q = warp & 3, half = warp >> 2;
+  const int m = m0 + q * 32 + lane;
+  const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
-  for (int c = 0; c < BN / 32; ++c) {
+  for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
     uint32_t r[32];
     if (nkb > 0) {
       tmem_ld32(trow + c * 32, r);
@@ -265,16 +268,25 @@ __global__ void __launch_bounds__(128, 1) k_gemm_tc(const __grid_constant__ TcMa
     }
     if (m < a.M) {
       const int nb = n0 + c * 32;
-      if (a.partial) {
-        float* dst = a.partial + ((int64_t)blockIdx.z * a.M + m) * a.N;
+      float v[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (nb + j < a.N) dst[nb + j] = __uint_as_float(r[j]);
-      } else {
+      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+      const bool full_chunk = nb + 32 <= a.N && (!a.lower_only || nb + 31 <= m);
+      if (a.partial) {
+        float* dst = a.partial + ((int64_t)blockIdx.z * a.M + m) * a.N + nb;
+        if (full_chunk && al16(dst)) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (nb + j < a.N) dst[j] = v[j];
+        }
+      } else if (!(full_chunk && epi_apply32(a.epi, m, nb, v))) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int n = nb + j;
-          if (n < a.N && (!a.lower_only || n <= m)) epi_apply(a.epi, m, n, __uint_as_float(r[j]));
+          if (n < a.N && (!a.lower_only || n <= m)) epi_apply(a.epi, m, n, v[j]);
         }
       }
     }
@@ -433,7 +445,7 @@ static void launch_tc(cv_ctx* ctx, const GemmArgs& g, int splits) {
     a.partial = part;
   }
   dim3 grid((g.N + BN - 1) / BN, (g.M + TC_BM - 1) / TC_BM, splits);
-  k_gemm_tc<BN, STAGES><<<grid, 128, Cfg::SMEM, ctx->stream>>>(maps, a);
+  k_gemm_tc<BN, STAGES><<<grid, 256, Cfg::SMEM, ctx->stream>>>(maps, a);
   ctx->launches++;
   if (splits > 1) {
     k_splitk_reduce<<<4 * ctx->sm_count, 256, 0, ctx->stream>>>(part, splits, g.M, g.N, g.epi, g.skip, g.lower_only);
