@@ -342,11 +342,9 @@ int cv_gemm_test(cv_ctx* ctx, int engine, int M, int N, int K, const float* a, i
   g.epi.mode = EPI_STORE;
   g.epi.out = out;
   g.epi.ld = ldo;
-  if (engine == CV_ENGINE_TC || engine == 3) {
+  if (engine == CV_ENGINE_TC) {
     contract(gemm_tc_supported(g), "shape/alignment not supported by the tensor-core engine");
-    if (engine == 3) g_tc_debug = out + (int64_t)M * ldo;  // caller provides room for one smem stage
     gemm_tc(_ctx, g);
-    g_tc_debug = nullptr;
   } else {
     gemm_simt(_ctx, g);
   }

@@ -60,17 +60,18 @@ CV_DEV void epi_apply(const Epilogue& e, int m, int n, float v) {
 
 CV_DEV bool al16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
-// 32 consecutive columns [nb, nb+32) of row m with 128-bit accesses.  Returns false
-// (nothing written) when the row segment is not 16-byte aligned; the caller then
-// falls back to the per-element path.
-CV_DEV bool epi_apply32(const Epilogue& e, int m, int nb, const float (&v)[32]) {
+// NC (multiple of 4) consecutive columns [nb, nb+NC) of row m with 128-bit accesses.
+// Returns false (nothing written) when the row segment is not 16-byte aligned; the
+// caller then falls back to the per-element path.
+template <int NC>
+CV_DEV bool epi_applyV(const Epilogue& e, int m, int nb, const float (&v)[NC]) {
   const int64_t o = (int64_t)m * e.ld + nb;
   switch (e.mode) {
     case EPI_STORE: {
       float* out = e.out + o;
       if (!al16(out)) return false;
 #pragma unroll
-      for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(out + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      for (int j = 0; j < NC; j += 4) *reinterpret_cast<float4*>(out + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
       return true;
     }
     case EPI_SPLIT_ACT: {
@@ -78,7 +79,7 @@ CV_DEV bool epi_apply32(const Epilogue& e, int m, int nb, const float (&v)[32]) 
       float* ol = e.out_lo + o;
       if (!al16(oh) || !al16(ol)) return false;
 #pragma unroll
-      for (int j = 0; j < 32; j += 4) {
+      for (int j = 0; j < NC; j += 4) {
         float h[4], l[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) split2(e.act == CV_ACT_RELU ? relu_f(v[j + t]) : tanhf(v[j + t]), h[t], l[t]);
@@ -103,7 +104,7 @@ CV_DEV bool epi_apply32(const Epilogue& e, int m, int nb, const float (&v)[32]) 
           (hvp_t && (!al16(P) || !al16(dz))))
         return false;
 #pragma unroll
-      for (int j = 0; j < 32; j += 4) {
+      for (int j = 0; j < NC; j += 4) {
         const float4 a4 = *reinterpret_cast<const float4*>(mh + j);
         float a[4] = {a4.x, a4.y, a4.z, a4.w};
         if (tanh_) {
@@ -134,7 +135,7 @@ CV_DEV bool epi_apply32(const Epilogue& e, int m, int nb, const float (&v)[32]) 
       const float* sa = e.sa + (int64_t)(m / e.kdiv) * e.sa_ld;
       if (!al16(out)) return false;
 #pragma unroll
-      for (int j = 0; j < 32; j += 4) {
+      for (int j = 0; j < NC; j += 4) {
         float4 cur = e.first ? make_float4(0.f, 0.f, 0.f, 0.f) : *reinterpret_cast<float4*>(out + j);
         cur.x += v[j] * sa[(nb + j) / e.kdiv];
         cur.y += v[j + 1] * sa[(nb + j + 1) / e.kdiv];
@@ -148,7 +149,7 @@ CV_DEV bool epi_apply32(const Epilogue& e, int m, int nb, const float (&v)[32]) 
       float* out = e.out + o;
       if (!al16(out)) return false;
 #pragma unroll
-      for (int j = 0; j < 32; j += 4) {
+      for (int j = 0; j < NC; j += 4) {
         float4 cur = *reinterpret_cast<float4*>(out + j);
         cur.x += e.alpha * v[j];
         cur.y += e.alpha * v[j + 1];
@@ -161,5 +162,7 @@ CV_DEV bool epi_apply32(const Epilogue& e, int m, int nb, const float (&v)[32]) 
   }
   return false;
 }
+
+CV_DEV bool epi_apply32(const Epilogue& e, int m, int nb, const float (&v)[32]) { return epi_applyV<32>(e, m, nb, v); }
 
 }  // namespace cv

@@ -46,7 +46,7 @@ struct TcArgs {
   const int* skip;
   int lower_only;
   float* partial;     // split-K partials (nullptr: apply the epilogue directly)
-  float* dbg;         // debug: copy of smem stage 0 (block 0,0,0)
+  int tiles_m, tiles_n, splits;
 };
 
 // ---------------------------------------------------------------------------
@@ -142,34 +142,53 @@ struct TcCfg {
   static constexpr int B_BYTES = BN * TC_BK * 4;     // 16 / 32 KB
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-  static constexpr int TMEM_COLS = BN;
+  static constexpr int TMEM_COLS = 2 * BN;           // double-buffered accumulator
+  static constexpr int THREADS = 320;                // w0 TMA, w1 MMA, w2..w9 epilogue
 };
 
+CV_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// work item -> (m0, n0, first k-block, k-blocks); split index slowest so that
+// co-resident CTAs share K ranges (and therefore L2-resident operand panels)
+CV_DEV bool tc_work(const TcArgs& a, int w, int bn, int& m0, int& n0, int& kb0, int& nkb) {
+  const int tiles = a.tiles_m * a.tiles_n;
+  const int split = w / tiles, t = w % tiles;
+  m0 = (t / a.tiles_n) * TC_BM;
+  n0 = (t % a.tiles_n) * bn;
+  kb0 = split * a.kb_per_split;
+  nkb = min(a.kb_total, kb0 + a.kb_per_split) - kb0;
+  return !(a.lower_only && n0 > m0 + TC_BM - 1);
+}
+
+// Persistent: grid = min(work, SMs); each CTA loops over work items.  The TMEM
+// accumulator is double buffered so the epilogue of item i overlaps the
+// mainloop of item i+1.
 template <int BN, int STAGES>
-__global__ void __launch_bounds__(256, 1) k_gemm_tc(const __grid_constant__ TcMaps maps, const TcArgs a) {
+__global__ void __launch_bounds__(320, 1) k_gemm_tc(const __grid_constant__ TcMaps maps, const TcArgs a) {
   using Cfg = TcCfg<BN, STAGES>;
   if (skip_if(a.skip)) return;
-  const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * BN;
-  if (a.lower_only && n0 > m0 + TC_BM - 1) return;
-  const int kb_begin = blockIdx.z * a.kb_per_split;
-  const int kb_end = min(a.kb_total, kb_begin + a.kb_per_split);
-  const int nkb = kb_end - kb_begin;
-
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + STAGES * Cfg::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* done = empty + STAGES;
-  uint32_t* tmem_slot = (uint32_t*)(done + 1);
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int total = a.tiles_m * a.tiles_n * a.splits;
   if (warp == 0) {
     if (lane == 0) {
       for (int s = 0; s < STAGES; ++s) {
         mbar_init(&full[s], 1);
         mbar_init(&empty[s], 1);
       }
-      mbar_init(done, 1);
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&tfull[b], 1);
+        mbar_init(&tempty[b], 8);
+      }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       for (int sg = 0; sg < a.nseg; ++sg)
         for (int q = 0; q < 4; ++q) tma_prefetch(&maps.m[sg][q]);
@@ -184,120 +203,136 @@ __global__ void __launch_bounds__(256, 1) k_gemm_tc(const __grid_constant__ TcMa
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 && lane == 0 && nkb > 0) {
+  if (warp == 0 && lane == 0) {
     // ---------------- TMA producer ----------------
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % STAGES;
-      if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
-      const int kb = kb_begin + i;
-      const int sg = kb < a.kb[0] ? 0 : 1;
-      const int k0 = (sg == 0 ? kb : kb - a.kb[0]) * TC_BK;
-      uint8_t* st = smem + s * Cfg::STAGE_BYTES;
-      mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
-      for (int h = 0; h < 2; ++h) {  // hi, lo
-        uint8_t* sa = st + h * Cfg::A_BYTES;
-        if (a.a[sg].kmajor) {
-          tma_load_2d(sa, &maps.m[sg][h], &full[s], k0, m0);
-        } else {
+    int it = 0;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      int m0, n0, kb0, nkb;
+      if (!tc_work(a, w, BN, m0, n0, kb0, nkb)) continue;
+      for (int i = 0; i < nkb; ++i, ++it) {
+        const int s = it % STAGES;
+        if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+        const int kb = kb0 + i;
+        const int sg = kb < a.kb[0] ? 0 : 1;
+        const int k0 = (sg == 0 ? kb : kb - a.kb[0]) * TC_BK;
+        uint8_t* st = smem + s * Cfg::STAGE_BYTES;
+        mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
+        for (int h = 0; h < 2; ++h) {  // hi, lo
+          uint8_t* sa = st + h * Cfg::A_BYTES;
+          if (a.a[sg].kmajor) {
+            tma_load_2d(sa, &maps.m[sg][h], &full[s], k0, m0);
+          } else {
 #pragma unroll
-          for (int j = 0; j < TC_BM / 32; ++j) tma_load_2d(sa + j * 4096, &maps.m[sg][h], &full[s], m0 + 32 * j, k0);
-        }
-        uint8_t* sb = st + 2 * Cfg::A_BYTES + h * Cfg::B_BYTES;
-        if (a.b[sg].kmajor) {
-          tma_load_2d(sb, &maps.m[sg][2 + h], &full[s], k0, n0);
-        } else {
+            for (int j = 0; j < TC_BM / 32; ++j) tma_load_2d(sa + j * 4096, &maps.m[sg][h], &full[s], m0 + 32 * j, k0);
+          }
+          uint8_t* sb = st + 2 * Cfg::A_BYTES + h * Cfg::B_BYTES;
+          if (a.b[sg].kmajor) {
+            tma_load_2d(sb, &maps.m[sg][2 + h], &full[s], k0, n0);
+          } else {
 #pragma unroll
-          for (int j = 0; j < BN / 32; ++j) tma_load_2d(sb + j * 4096, &maps.m[sg][2 + h], &full[s], n0 + 32 * j, k0);
+            for (int j = 0; j < BN / 32; ++j)
+              tma_load_2d(sb + j * 4096, &maps.m[sg][2 + h], &full[s], n0 + 32 * j, k0);
+          }
         }
       }
     }
-  } else if (warp == 1 && lane == 0 && nkb > 0) {
+  } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ----------------
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % STAGES;
-      mbar_wait(&full[s], (i / STAGES) & 1);
+    int it = 0, acc_i = 0;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      int m0, n0, kb0, nkb;
+      if (!tc_work(a, w, BN, m0, n0, kb0, nkb)) continue;
+      const int ab = acc_i & 1;
+      if (acc_i >= 2) mbar_wait(&tempty[ab], ((acc_i >> 1) - 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int kb = kb_begin + i;
-      const int sg = kb < a.kb[0] ? 0 : 1;
-      const int amn = a.a[sg].kmajor ? 0 : 1, bmn = a.b[sg].kmajor ? 0 : 1;
-      const uint32_t idesc = tf32_idesc(TC_BM, BN, amn, bmn);
-      const uint32_t st = smem_u32(smem + s * Cfg::STAGE_BYTES);
-      const uint32_t a_hi = st, a_lo = st + Cfg::A_BYTES;
-      const uint32_t b_hi = st + 2 * Cfg::A_BYTES, b_lo = b_hi + Cfg::B_BYTES;
+      const uint32_t dtm = tmem + ab * BN;
+      for (int i = 0; i < nkb; ++i, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&full[s], (it / STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int kb = kb0 + i;
+        const int sg = kb < a.kb[0] ? 0 : 1;
+        const int amn = a.a[sg].kmajor ? 0 : 1, bmn = a.b[sg].kmajor ? 0 : 1;
+        const uint32_t idesc = tf32_idesc(TC_BM, BN, amn, bmn);
+        const uint32_t st = smem_u32(smem + s * Cfg::STAGE_BYTES);
+        const uint32_t a_hi = st, a_lo = st + Cfg::A_BYTES;
+        const uint32_t b_hi = st + 2 * Cfg::A_BYTES, b_lo = b_hi + Cfg::B_BYTES;
 #pragma unroll
-      for (int kk = 0; kk < TC_BK / 8; ++kk) {
-        // K-major (SW128): rows of 128 B, 8-row atoms (SBO 1024), k-step = +32 B in the row.
-        // MN-major (SW128_BASE32B): 32-wide MN chunks 4 KB apart (LBO), K rows of 128 B in
-        // 4-row atoms (SBO 512), k-step = 8 rows = +1024 B.
-        const uint32_t aoff = amn ? kk * 1024 : kk * 32;
-        const uint32_t boff = bmn ? kk * 1024 : kk * 32;
-        const uint32_t albo = amn ? 4096 : 16, blbo = bmn ? 4096 : 16;
-        const uint32_t asbo = amn ? 512 : 1024, bsbo = bmn ? 512 : 1024;
-        const uint32_t alay = amn ? 1 : 2, blay = bmn ? 1 : 2;
-        const uint64_t dah = umma_desc(a_hi + aoff, albo, asbo, alay), dal = umma_desc(a_lo + aoff, albo, asbo, alay);
-        const uint64_t dbh = umma_desc(b_hi + boff, blbo, bsbo, blay), dbl = umma_desc(b_lo + boff, blbo, bsbo, blay);
-        const uint32_t acc0 = (i > 0 || kk > 0) ? 1u : 0u;
-        umma_tf32(tmem, dah, dbh, idesc, acc0);
-        umma_tf32(tmem, dah, dbl, idesc, 1u);
-        umma_tf32(tmem, dal, dbh, idesc, 1u);
+        for (int kk = 0; kk < TC_BK / 8; ++kk) {
+          // K-major (SW128): rows of 128 B, 8-row atoms (SBO 1024), k-step = +32 B in the row.
+          // MN-major (SW128_BASE32B): 32-wide MN chunks 4 KB apart (LBO), K rows of 128 B in
+          // 4-row atoms (SBO 512), k-step = 8 rows = +1024 B.
+          const uint32_t aoff = amn ? kk * 1024 : kk * 32;
+          const uint32_t boff = bmn ? kk * 1024 : kk * 32;
+          const uint32_t albo = amn ? 4096 : 16, blbo = bmn ? 4096 : 16;
+          const uint32_t asbo = amn ? 512 : 1024, bsbo = bmn ? 512 : 1024;
+          const uint32_t alay = amn ? 1 : 2, blay = bmn ? 1 : 2;
+          const uint64_t dah = umma_desc(a_hi + aoff, albo, asbo, alay), dal = umma_desc(a_lo + aoff, albo, asbo, alay);
+          const uint64_t dbh = umma_desc(b_hi + boff, blbo, bsbo, blay), dbl = umma_desc(b_lo + boff, blbo, bsbo, blay);
+          const uint32_t acc0 = (i > 0 || kk > 0) ? 1u : 0u;
+          umma_tf32(dtm, dah, dbh, idesc, acc0);
+          umma_tf32(dtm, dah, dbl, idesc, 1u);
+          umma_tf32(dtm, dal, dbh, idesc, 1u);
+        }
+        umma_commit(&empty[s]);  // slab free once these MMAs retire
       }
-      umma_commit(&empty[s]);  // slab free once these MMAs retire
+      umma_commit(&tfull[ab]);   // accumulator ready for the epilogue
+      ++acc_i;
     }
-    umma_commit(done);
-  }
-  __syncwarp();
-
-  // ---------------- epilogue: TMEM -> registers -> fused epilogue ----------------
-  if (nkb > 0) {
-    mbar_wait(done, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  }
-  // 8 warps: warp w reads TMEM lane quadrant (w % 4) -> rows m0 + 32 (w % 4) + lane, and
-  // the column half (w / 4) of the tile.
-  const int q = warp & 3, half = warp >> 2;
-  const int m = m0 + q * 32 + lane;
-  const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+  } else if (warp >= 2) {
+    // ---------------- epilogue: TMEM -> registers -> fused epilogue ----------------
+    // warp w reads TMEM lane quadrant (w % 4); warps 2-5 take the first column half,
+    // warps 6-9 the second.
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    int acc_i = 0;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      int m0, n0, kb0, nkb;
+      if (!tc_work(a, w, BN, m0, n0, kb0, nkb)) continue;
+      const int ab = acc_i & 1;
+      mbar_wait(&tfull[ab], (acc_i >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int m = m0 + q * 32 + lane;
+      const int split = w / (a.tiles_m * a.tiles_n);
+      const uint32_t trow = tmem + ab * BN + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
-  for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
-    uint32_t r[32];
-    if (nkb > 0) {
-      tmem_ld32(trow + c * 32, r);
-    } else {
+      for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
+        uint32_t r[32];
+        tmem_ld32(trow + c * 32, r);
+        if (m >= a.M) continue;
+        const int nb = n0 + c * 32;
+        float v[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) r[j] = 0u;
-    }
-    if (m < a.M) {
-      const int nb = n0 + c * 32;
-      float v[32];
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        const bool full_chunk = nb + 32 <= a.N && (!a.lower_only || nb + 31 <= m);
+        if (a.partial) {
+          float* dst = a.partial + ((int64_t)split * a.M + m) * a.N + nb;
+          if (full_chunk && al16(dst)) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-      const bool full_chunk = nb + 32 <= a.N && (!a.lower_only || nb + 31 <= m);
-      if (a.partial) {
-        float* dst = a.partial + ((int64_t)blockIdx.z * a.M + m) * a.N + nb;
-        if (full_chunk && al16(dst)) {
+            for (int j = 0; j < 32; j += 4)
+              *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          } else {
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-        } else {
+            for (int j = 0; j < 32; ++j)
+              if (nb + j < a.N) dst[j] = v[j];
+          }
+        } else if (!(full_chunk && epi_apply32(a.epi, m, nb, v))) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (nb + j < a.N) dst[j] = v[j];
-        }
-      } else if (!(full_chunk && epi_apply32(a.epi, m, nb, v))) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int n = nb + j;
-          if (n < a.N && (!a.lower_only || n <= m)) epi_apply(a.epi, m, n, v[j]);
+          for (int j = 0; j < 32; ++j) {
+            const int n = nb + j;
+            if (n < a.N && (!a.lower_only || n <= m)) epi_apply(a.epi, m, n, v[j]);
+          }
         }
       }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[ab]);
+      ++acc_i;
     }
-  }
-  if (a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
-    const float* src = (const float*)smem;
-    for (int i = threadIdx.x; i < Cfg::STAGE_BYTES / 4; i += blockDim.x) a.dbg[i] = src[i];
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cfg::TMEM_COLS));
   }
 }
@@ -381,8 +416,6 @@ static CUtensorMap make_map(const float* ptr, int64_t inner, int64_t outer, int6
   return m;
 }
 
-float* g_tc_debug = nullptr;  // set by cv_gemm_test's debug mode
-
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
 // Operand majors: A(m,k) = p[m*si + k*sj]; K-major iff sj == 1.
@@ -437,15 +470,18 @@ static void launch_tc(cv_ctx* ctx, const GemmArgs& g, int splits) {
   a.skip = g.skip;
   a.lower_only = g.lower_only;
   a.kb_per_split = (a.kb_total + splits - 1) / splits;
-  a.dbg = g_tc_debug;
   splits = (a.kb_total + a.kb_per_split - 1) / a.kb_per_split;
+  a.splits = splits;
+  a.tiles_m = (g.M + TC_BM - 1) / TC_BM;
+  a.tiles_n = (g.N + BN - 1) / BN;
   float* part = nullptr;
   if (splits > 1) {
     part = (float*)ctx->pool.get(sizeof(float) * (size_t)splits * g.M * g.N);
     a.partial = part;
   }
-  dim3 grid((g.N + BN - 1) / BN, (g.M + TC_BM - 1) / TC_BM, splits);
-  k_gemm_tc<BN, STAGES><<<grid, 256, Cfg::SMEM, ctx->stream>>>(maps, a);
+  const int work = a.tiles_m * a.tiles_n * splits;
+  const int grid = work < ctx->sm_count ? work : ctx->sm_count;
+  k_gemm_tc<BN, STAGES><<<grid, Cfg::THREADS, Cfg::SMEM, ctx->stream>>>(maps, a);
   ctx->launches++;
   if (splits > 1) {
     k_splitk_reduce<<<4 * ctx->sm_count, 256, 0, ctx->stream>>>(part, splits, g.M, g.N, g.epi, g.skip, g.lower_only);
@@ -456,7 +492,8 @@ static void launch_tc(cv_ctx* ctx, const GemmArgs& g, int splits) {
 
 void gemm_tc(cv_ctx* ctx, const GemmArgs& g) {
   const int tiles_n256 = (g.N + 255) / 256, tiles_m = (g.M + TC_BM - 1) / TC_BM;
-  const bool wide = g.N >= 512;
+  static const int force_bn = getenv("CURVOPT_TC_BN") ? atoi(getenv("CURVOPT_TC_BN")) : 0;
+  const bool wide = force_bn ? force_bn == 256 : g.N >= 512;
   const int tiles = (wide ? tiles_n256 : (g.N + 127) / 128) * tiles_m;
   int kb_total = 0;
   for (int s = 0; s < g.nseg; ++s) kb_total += (g.seg[s].K + TC_BK - 1) / TC_BK;

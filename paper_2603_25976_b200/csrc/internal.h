@@ -157,7 +157,6 @@ void gemm_simt(cv_ctx* ctx, const GemmArgs& a);
 bool gemm_tc_supported(const GemmArgs& a);
 void gemm_tc(cv_ctx* ctx, const GemmArgs& a);
 void gemm(cv_ctx* ctx, const GemmArgs& a);  // engine dispatch
-extern float* g_tc_debug;                   // engine unit-test hook (smem stage dump)
 
 // runtime.cu
 void allreduce_f32(cv_ctx* ctx, float* buf, int64_t n);

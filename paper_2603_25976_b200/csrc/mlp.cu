@@ -11,6 +11,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "epilogue.cuh"
+#include "skinny.cuh"
 
 namespace cv {
 
@@ -66,212 +67,6 @@ void split_vec(cv_ctx* ctx, const float* x, float* hi, float* lo, int64_t n, con
 }
 
 // ---------------------------------------------------------------------------
-// Skinny kernels for the output layer (N = c <= 32)
-// ---------------------------------------------------------------------------
-struct SkinnySeg {
-  const float* a_hi; const float* a_lo; int64_t lda;  // A: b x K row-major (split)
-  const float* b_hi; const float* b_lo; int64_t ldb;  // B: K x c row-major (split)
-  int K;
-};
-
-enum SkinnyPost : int { POST_LOGITS = 0, POST_HZ = 1 };
-
-struct SkinnyRowsArgs {
-  int rows, c, nseg;
-  SkinnySeg seg[2];
-  int post;               // SkinnyPost
-  int loss;               // CV_LOSS_*
-  const float* probs;     // b x c (POST_HZ, ce)
-  float scale;            // POST_HZ: 1/b_global
-  float* out;             // b x c
-  const int* skip;
-};
-
-constexpr int SK_KC = 128;  // K chunk staged in shared memory
-
-// out[m, :] = sum_s A_s[m, :] @ B_s, one warp per row (lanes split K), fused
-// loss-Hessian application H_z (models.py:199-204) for the GGN / HVP cotangent.
-template <int CM, int RPW>
-__global__ void __launch_bounds__(256) k_skinny_rows(SkinnyRowsArgs a) {
-  if (skip_if(a.skip)) return;
-  __shared__ float Bs[SK_KC][CM + 1];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int row0 = (blockIdx.x * 8 + w) * RPW;
-  float acc[RPW][CM];
-#pragma unroll
-  for (int r = 0; r < RPW; ++r)
-#pragma unroll
-    for (int j = 0; j < CM; ++j) acc[r][j] = 0.f;
-  for (int s = 0; s < a.nseg; ++s) {
-    const SkinnySeg g = a.seg[s];
-    for (int k0 = 0; k0 < g.K; k0 += SK_KC) {
-      __syncthreads();
-      for (int e = threadIdx.x; e < SK_KC * CM; e += 256) {
-        const int kk = e / CM, j = e % CM;
-        float v = 0.f;
-        if (k0 + kk < g.K && j < a.c) {
-          const int64_t idx = (int64_t)(k0 + kk) * g.ldb + j;
-          v = g.b_hi[idx] + g.b_lo[idx];
-        }
-        Bs[kk][j] = v;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int r = 0; r < RPW; ++r) {
-        const int m = row0 + r;
-        if (m >= a.rows) break;
-        const float* ah = g.a_hi + (int64_t)m * g.lda + k0;
-        const float* al = g.a_lo + (int64_t)m * g.lda + k0;
-        const int kmax = min(SK_KC, g.K - k0);
-        for (int kk = lane; kk < kmax; kk += 32) {
-          const float av = ah[kk] + al[kk];
-#pragma unroll
-          for (int j = 0; j < CM; ++j) acc[r][j] = fmaf(av, Bs[kk][j], acc[r][j]);
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < RPW; ++r) {
-    const int m = row0 + r;
-#pragma unroll
-    for (int j = 0; j < CM; ++j) acc[r][j] = warp_sum(acc[r][j]);
-    if (m >= a.rows) continue;
-    if (a.post == POST_LOGITS || a.loss == CV_LOSS_MSE) {
-      if (lane < a.c) {
-        float v = 0.f;
-#pragma unroll
-        for (int j = 0; j < CM; ++j) if (j == lane) v = acc[r][j];
-        a.out[(int64_t)m * a.c + lane] = a.post == POST_LOGITS ? v : v * a.scale;
-      }
-    } else {
-      // H_z T = p*T - p*(p.T)   (softmax-CE, per example)
-      const float* p = a.probs + (int64_t)m * a.c;
-      float pt = 0.f;
-#pragma unroll
-      for (int j = 0; j < CM; ++j) if (j < a.c) pt = fmaf(p[j], acc[r][j], pt);
-      if (lane < a.c) {
-        float t = 0.f;
-#pragma unroll
-        for (int j = 0; j < CM; ++j) if (j == lane) t = acc[r][j];
-        const float pj = p[lane];
-        a.out[(int64_t)m * a.c + lane] = (pj * t - pj * pt) * a.scale;
-      }
-    }
-  }
-}
-
-// G[m, n] = epi( sum_s U_s[m, :] . Wt_s[n, :] ), Wt_s is the n x c (row-major,
-// ld c) weight slice, i.e. U W^T with K = c.  (models.py:282-284, 378-381)
-struct SkinnyDxArgs {
-  int rows, n, c, nseg;
-  const float* U[2];
-  const float* w_hi[2]; const float* w_lo[2];
-  Epilogue epi;
-  const int* skip;
-};
-
-template <int CM>
-__global__ void __launch_bounds__(256) k_skinny_dx(SkinnyDxArgs a) {
-  if (skip_if(a.skip)) return;
-  constexpr int RB = 32;
-  __shared__ float Us[2][RB][CM];
-  const int n = blockIdx.x * 256 + threadIdx.x;
-  const int m0 = blockIdx.y * RB;
-  float w[2][CM];
-#pragma unroll
-  for (int s = 0; s < 2; ++s)
-#pragma unroll
-    for (int j = 0; j < CM; ++j) {
-      float v = 0.f;
-      if (s < a.nseg && n < a.n && j < a.c) {
-        const int64_t idx = (int64_t)n * a.c + j;
-        v = a.w_hi[s][idx] + a.w_lo[s][idx];
-      }
-      w[s][j] = v;
-    }
-  for (int e = threadIdx.x; e < 2 * RB * CM; e += 256) {
-    const int s = e / (RB * CM), rem = e % (RB * CM), r = rem / CM, j = rem % CM;
-    float v = 0.f;
-    if (s < a.nseg && m0 + r < a.rows && j < a.c) v = a.U[s][(int64_t)(m0 + r) * a.c + j];
-    Us[s][r][j] = v;
-  }
-  __syncthreads();
-  if (n >= a.n) return;
-  for (int r = 0; r < RB; ++r) {
-    const int m = m0 + r;
-    if (m >= a.rows) break;
-    float acc = 0.f;
-#pragma unroll
-    for (int s = 0; s < 2; ++s)
-#pragma unroll
-      for (int j = 0; j < CM; ++j) acc = fmaf(Us[s][r][j], w[s][j], acc);
-    epi_apply(a.epi, m, n, acc);
-  }
-}
-
-
-// out[m, j] (m < M = n+1, ld c) = sum_s sum_k A_s[k, m] U_s[k, j]: the last layer's
-// weight+bias gradient, A_s = augmented activations (b x lda, split), U_s (b x c).
-// Phase 1 writes KSPLIT partials, phase 2 sums them in fixed order (deterministic).
-struct SkinnyDwArgs {
-  int rows, M, c, nseg, ksplit;
-  const float* a_hi[2]; const float* a_lo[2]; int64_t lda[2];
-  const float* U[2];
-  float* partial;   // ksplit x M x c
-  float* out;       // M x c
-  const int* skip;
-};
-
-template <int CM>
-__global__ void __launch_bounds__(256) k_skinny_dw_partial(SkinnyDwArgs a) {
-  if (skip_if(a.skip)) return;
-  __shared__ float red[8][32][CM + 1];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int m = blockIdx.x * 32 + lane;
-  const int ks = blockIdx.y;
-  const int chunk = (a.rows + a.ksplit - 1) / a.ksplit;
-  const int k_begin = ks * chunk, k_end = min(a.rows, k_begin + chunk);
-  float acc[CM];
-#pragma unroll
-  for (int j = 0; j < CM; ++j) acc[j] = 0.f;
-  for (int s = 0; s < a.nseg; ++s) {
-    for (int k = k_begin + w; k < k_end; k += 8) {
-      float av = 0.f;
-      if (m < a.M) {
-        const int64_t idx = (int64_t)k * a.lda[s] + m;
-        av = a.a_hi[s][idx] + a.a_lo[s][idx];
-      }
-      const float* u = a.U[s] + (int64_t)k * a.c;
-#pragma unroll
-      for (int j = 0; j < CM; ++j) if (j < a.c) acc[j] = fmaf(av, u[j], acc[j]);
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < CM; ++j) red[w][lane][j] = acc[j];
-  __syncthreads();
-  for (int e = threadIdx.x; e < 32 * CM; e += 256) {
-    const int l = e / CM, j = e % CM;
-    const int mm = blockIdx.x * 32 + l;
-    if (mm >= a.M || j >= a.c) continue;
-    float s = 0.f;
-#pragma unroll
-    for (int ww = 0; ww < 8; ++ww) s += red[ww][l][j];
-    a.partial[((int64_t)ks * a.M + mm) * a.c + j] = s;
-  }
-}
-
-__global__ void k_skinny_dw_final(SkinnyDwArgs a) {
-  if (skip_if(a.skip)) return;
-  const int64_t total = (int64_t)a.M * a.c;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int ks = 0; ks < a.ksplit; ++ks) s += a.partial[(int64_t)ks * total + i];
-    a.out[i] = s;
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Loss rows: softmax-CE / MSE value, probabilities and G[L-1] = out_grad / b
 // (models.py:358-383).  Per-block fp64 partial sums of the per-example loss.
 // ---------------------------------------------------------------------------
@@ -322,40 +117,9 @@ __global__ void k_finalize_sum(const double* partial, int nblk, double scale, do
 // ---------------------------------------------------------------------------
 // Host orchestration
 // ---------------------------------------------------------------------------
-static void launch_skinny_rows(cv_ctx* ctx, const SkinnyRowsArgs& a) {
-  const int c = a.c;
-  if (c <= 16) {
-    const int rows_per_block = 8 * 4;
-    k_skinny_rows<16, 4><<<(a.rows + rows_per_block - 1) / rows_per_block, 256, 0, ctx->stream>>>(a);
-  } else {
-    const int rows_per_block = 8 * 2;
-    k_skinny_rows<32, 2><<<(a.rows + rows_per_block - 1) / rows_per_block, 256, 0, ctx->stream>>>(a);
-  }
-  ctx->launches++;
-}
-
-static void launch_skinny_dx(cv_ctx* ctx, const SkinnyDxArgs& a) {
-  dim3 grid((a.n + 255) / 256, (a.rows + 31) / 32);
-  if (a.c <= 16) k_skinny_dx<16><<<grid, 256, 0, ctx->stream>>>(a);
-  else k_skinny_dx<32><<<grid, 256, 0, ctx->stream>>>(a);
-  ctx->launches++;
-}
-
-static void launch_skinny_dw(cv_ctx* ctx, cv_snap* s, SkinnyDwArgs a) {
-  const int mblocks = (a.M + 31) / 32;
-  int ks = (2 * ctx->sm_count + mblocks - 1) / mblocks;
-  ks = ks < 1 ? 1 : ks;
-  const int maxks = (a.rows + 63) / 64;
-  if (ks > maxks) ks = maxks < 1 ? 1 : maxks;
-  while ((int64_t)ks * a.M * a.c > s->skinny_ws_elems && ks > 1) --ks;
-  a.ksplit = ks;
-  a.partial = s->skinny_ws;
-  dim3 grid(mblocks, ks);
-  if (a.c <= 16) k_skinny_dw_partial<16><<<grid, 256, 0, ctx->stream>>>(a);
-  else k_skinny_dw_partial<32><<<grid, 256, 0, ctx->stream>>>(a);
-  k_skinny_dw_final<<<grid_for((int64_t)a.M * a.c), 256, 0, ctx->stream>>>(a);
-  ctx->launches += 2;
-}
+static void launch_skinny_rows(cv_ctx* ctx, const SkinnyRowsArgs& a) { skinny_rows(ctx, a); }
+static void launch_skinny_dx(cv_ctx* ctx, const SkinnyDxArgs& a) { skinny_dx(ctx, a); }
+static void launch_skinny_dw(cv_ctx* ctx, cv_snap* s, SkinnyDwArgs a) { skinny_dw(ctx, a, s->skinny_ws, s->skinny_ws_elems); }
 
 // Operand views --------------------------------------------------------------
 static Operand op_rows(const SplitBuf& b) { return Operand{b.hi, b.lo, b.ld, 1}; }          // X(m,k)=buf[m,k]

@@ -76,7 +76,16 @@ def _fp32_cg(lin, rhs, lam, tol, maxiter, stab, pre=None, x0=None):
     accuracy any fp32 implementation can reach on this (tiny, ill-conditioned)
     system.  Used to scale the CG tolerance where fp32 itself loses digits."""
     f = np.float32
-    A = lambda x: (O.ggn_matvec(lin, x.astype(np.float64)) + lam * x.astype(np.float64)).astype(f)  # noqa: E731
+
+    def tf32(x):  # round-to-nearest (ties away) to 11 significant bits, like cvt.rna.tf32
+        u = np.asarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+        return ((u + 0x1000) & 0xFFFFE000).astype(np.uint32).view(np.float32)
+
+    def split(x):  # the device's operand representation: x ~= hi + lo, both tf32
+        h = tf32(x)
+        return h.astype(np.float64) + tf32(x.astype(f) - h).astype(np.float64)
+
+    A = lambda x: (O.ggn_matvec(lin, split(x)) + lam * x.astype(np.float64)).astype(f)  # noqa: E731
     g = rhs.astype(f)
     minv = None if pre is None else (1.0 / (np.maximum(pre, 1e-12) + lam)).astype(f)
     bn = np.linalg.norm(rhs)
