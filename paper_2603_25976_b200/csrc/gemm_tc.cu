@@ -490,11 +490,15 @@ static void launch_tc(cv_ctx* ctx, const GemmArgs& g, int splits) {
   }
 }
 
+#include "gemm_tc2.cuh"
+
 void gemm_tc(cv_ctx* ctx, const GemmArgs& g) {
-  const int tiles_n256 = (g.N + 255) / 256, tiles_m = (g.M + TC_BM - 1) / TC_BM;
   static const int force_bn = getenv("CURVOPT_TC_BN") ? atoi(getenv("CURVOPT_TC_BN")) : 0;
+  static const int use_2sm = getenv("CURVOPT_TC_2SM") ? atoi(getenv("CURVOPT_TC_2SM")) : 1;
+  const bool pair = use_2sm && !force_bn && g.M >= 256 && g.N >= 256;
   const bool wide = force_bn ? force_bn == 256 : g.N >= 512;
-  const int tiles = (wide ? tiles_n256 : (g.N + 127) / 128) * tiles_m;
+  const int tiles = pair ? ((g.M + 255) / 256) * ((g.N + 255) / 256) * 2
+                         : (wide ? (g.N + 255) / 256 : (g.N + 127) / 128) * ((g.M + TC_BM - 1) / TC_BM);
   int kb_total = 0;
   for (int s = 0; s < g.nseg; ++s) kb_total += (g.seg[s].K + TC_BK - 1) / TC_BK;
   // split K when the tile grid cannot fill the machine (weight-gradient GEMMs: M, N ~ 1e3, K = batch)
@@ -504,7 +508,9 @@ void gemm_tc(cv_ctx* ctx, const GemmArgs& g) {
     if (splits > kb_total / 4) splits = kb_total / 4;
     if (splits < 1) splits = 1;
   }
-  if (wide)
+  if (pair)
+    launch_tc2<3>(ctx, g, splits);
+  else if (wide)
     launch_tc<256, 2>(ctx, g, splits);
   else
     launch_tc<128, 3>(ctx, g, splits);
