@@ -184,12 +184,29 @@ int cv_linearize(cv_ctx* ctx, int n_layers, const int* dims, int act, int loss, 
     need = (int64_t)(2 * ctx->sm_count + 1) * mrows * c;
     s->skinny_ws_elems = need;
     s->skinny_ws = alloc_f(s, need);
+    // output layer on the tensor-core engine when the shapes allow TMA operands
+    const char* env = getenv("CURVOPT_TC_OUT");
+    s->cp = c;
+    s->tc_out = ctx->engine != CV_ENGINE_SIMT && !(env && env[0] == '0') && c >= 8 && b >= 128 && dims[L - 1] >= 64;
+    if (s->tc_out) {
+      s->cp = c <= 16 ? 16 : 32;
+      const int64_t wrows = dims[L - 1] + 1;
+      s->wl_hi = alloc_f(s, wrows * s->cp);
+      s->wl_lo = alloc_f(s, wrows * s->cp);
+      s->vl_hi = alloc_f(s, wrows * s->cp);
+      s->vl_lo = alloc_f(s, wrows * s->cp);
+      s->U_hi = alloc_f(s, (int64_t)b * s->cp);
+      s->U_lo = alloc_f(s, (int64_t)b * s->cp);
+      s->gout_hi = alloc_f(s, (int64_t)b * s->cp);
+      s->gout_lo = alloc_f(s, (int64_t)b * s->cp);
+    }
   } catch (...) {
     for (void* p : s->owned) ctx->pool.put(p);
     delete s;
     throw;
   }
   split_vec(ctx, w, s->w_hi, s->w_lo, s->d, nullptr);
+  if (s->tc_out) pad_last_weights(ctx, s);
   split_rows(ctx, X, dims[0], b, dims[0], s->acts[0], 1);
   for (int l = 1; l < L; ++l) set_ones_col(ctx, s->acts[l], b, dims[l]);
   for (int l = 0; l + 1 < L; ++l) zero_col(ctx, s->da[l], b, dims[l + 1]);

@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(320, 1) k_gemm_tc(const __grid_constant__ TcMa
       const int split = w / (a.tiles_m * a.tiles_n);
       const uint32_t trow = tmem + ab * BN + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
-      for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
+      for (int c = half; c < BN / 32; c += 2) {
         uint32_t r[32];
         tmem_ld32(trow + c * 32, r);
         if (m >= a.M) continue;
@@ -342,6 +342,23 @@ __global__ void k_splitk_reduce(const float* partial, int splits, int M, int N, 
                                 int lower_only) {
   if (skip_if(skip)) return;
   const int64_t total = (int64_t)M * N;
+  if ((N & 3) == 0 && !lower_only) {
+    // 4 adjacent columns per thread: 128-bit partial loads, vectorized epilogue
+    const int64_t quads = total >> 2;
+    for (int64_t qd = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; qd < quads;
+         qd += (int64_t)gridDim.x * blockDim.x) {
+      float4 s = *reinterpret_cast<const float4*>(partial + 4 * qd);
+      for (int z = 1; z < splits; ++z) {
+        const float4 p = *reinterpret_cast<const float4*>(partial + (int64_t)z * total + 4 * qd);
+        s.x += p.x; s.y += p.y; s.z += p.z; s.w += p.w;
+      }
+      const int m = (int)((4 * qd) / N), n = (int)((4 * qd) % N);
+      const float v[4] = {s.x, s.y, s.z, s.w};
+      if (!epi_applyV<4>(epi, m, n, v))
+        for (int t = 0; t < 4; ++t) epi_apply(epi, m, n + t, v[t]);
+    }
+    return;
+  }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     float s = 0.f;
     for (int z = 0; z < splits; ++z) s += partial[(int64_t)z * total + i];
@@ -427,7 +444,7 @@ static bool op_ok(const Operand& o) {
 }
 
 bool gemm_tc_supported(const GemmArgs& g) {
-  if (g.M < 64 || g.N < 64) return false;
+  if (g.M < 64 || g.N < 8) return false;
   for (int s = 0; s < g.nseg; ++s) {
     if (g.seg[s].K < 8) return false;
     if (!op_ok(g.seg[s].A) || !op_ok(g.seg[s].B)) return false;
@@ -436,7 +453,7 @@ bool gemm_tc_supported(const GemmArgs& g) {
 }
 
 template <int BN, int STAGES>
-static void launch_tc(cv_ctx* ctx, const GemmArgs& g, int splits) {
+static int launch_tc(cv_ctx* ctx, const GemmArgs& g, int splits, float* ext_partial = nullptr) {
   using Cfg = TcCfg<BN, STAGES>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -475,7 +492,9 @@ static void launch_tc(cv_ctx* ctx, const GemmArgs& g, int splits) {
   a.tiles_m = (g.M + TC_BM - 1) / TC_BM;
   a.tiles_n = (g.N + BN - 1) / BN;
   float* part = nullptr;
-  if (splits > 1) {
+  if (ext_partial) {
+    a.partial = ext_partial;  // raw split-K partials for the caller, no epilogue
+  } else if (splits > 1) {
     part = (float*)ctx->pool.get(sizeof(float) * (size_t)splits * g.M * g.N);
     a.partial = part;
   }
@@ -483,11 +502,12 @@ static void launch_tc(cv_ctx* ctx, const GemmArgs& g, int splits) {
   const int grid = work < ctx->sm_count ? work : ctx->sm_count;
   k_gemm_tc<BN, STAGES><<<grid, Cfg::THREADS, Cfg::SMEM, ctx->stream>>>(maps, a);
   ctx->launches++;
-  if (splits > 1) {
+  if (part) {
     k_splitk_reduce<<<4 * ctx->sm_count, 256, 0, ctx->stream>>>(part, splits, g.M, g.N, g.epi, g.skip, g.lower_only);
     ctx->launches++;
     ctx->pool.put(part);  // stream-ordered reuse: later users enqueue after this kernel
   }
+  return splits;
 }
 
 #include "gemm_tc2.cuh"
@@ -508,12 +528,29 @@ void gemm_tc(cv_ctx* ctx, const GemmArgs& g) {
     if (splits > kb_total / 4) splits = kb_total / 4;
     if (splits < 1) splits = 1;
   }
-  if (pair)
+  if (g.N <= 32)
+    launch_tc<32, 5>(ctx, g, splits);
+  else if (pair)
     launch_tc2<3>(ctx, g, splits);
   else if (wide)
     launch_tc<256, 2>(ctx, g, splits);
   else
     launch_tc<128, 3>(ctx, g, splits);
+}
+
+// Narrow (N <= 32) GEMM returning raw split-K partials [splits][M][N]: the output
+// layer's JVP, whose row-wise loss Hessian cannot be applied per element.
+int gemm_tc_partial(cv_ctx* ctx, const GemmArgs& g, float** partial) {
+  int kb_total = 0;
+  for (int s = 0; s < g.nseg; ++s) kb_total += (g.seg[s].K + TC_BK - 1) / TC_BK;
+  const int tiles = (g.M + TC_BM - 1) / TC_BM;
+  int splits = tiles < ctx->sm_count ? ctx->sm_count / tiles : 1;
+  if (splits > kb_total / 4) splits = kb_total / 4;
+  if (splits < 1) splits = 1;
+  const int kbs = (kb_total + splits - 1) / splits;
+  splits = (kb_total + kbs - 1) / kbs;
+  *partial = (float*)ctx->pool.get(sizeof(float) * (size_t)splits * g.M * g.N);
+  return launch_tc<32, 5>(ctx, g, splits, *partial);
 }
 
 }  // namespace cv

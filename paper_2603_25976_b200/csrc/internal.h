@@ -136,6 +136,14 @@ struct cv_snap {
   float* U2 = nullptr;            // b x c (HVP last-layer dz)
   float* skinny_ws = nullptr;     // partial sums for skinny weight-gradient kernels
   int64_t skinny_ws_elems = 0;
+  // tensor-core output layer (tc_out): the c-wide operands padded to cp columns
+  // (16-byte rows for TMA), split: last-layer [W; b] (wl), per-product [V; Vb] (vl),
+  // cotangent U and G[L-1] (gout).  cp == c when the SIMT skinny kernels are used.
+  int tc_out = 0, cp = 0;
+  float* wl_hi = nullptr; float* wl_lo = nullptr;
+  float* vl_hi = nullptr; float* vl_lo = nullptr;
+  float* U_hi = nullptr; float* U_lo = nullptr;
+  float* gout_hi = nullptr; float* gout_lo = nullptr;
   // row lane (lazily built)
   float* seeds = nullptr;         // b x c x c  (H_z^{1/2})
   float* pinv = nullptr;          // b x c x c
@@ -157,6 +165,7 @@ void gemm_simt(cv_ctx* ctx, const GemmArgs& a);
 bool gemm_tc_supported(const GemmArgs& a);
 void gemm_tc(cv_ctx* ctx, const GemmArgs& a);
 void gemm(cv_ctx* ctx, const GemmArgs& a);  // engine dispatch
+int gemm_tc_partial(cv_ctx* ctx, const GemmArgs& g, float** partial);  // N <= 32, raw split-K partials
 
 // runtime.cu
 void allreduce_f32(cv_ctx* ctx, float* buf, int64_t n);
@@ -170,6 +179,7 @@ void set_ones_col(cv_ctx* ctx, const SplitBuf& b, int rows, int col);
 void set_col_value(cv_ctx* ctx, const SplitBuf& b, int rows, int col, float v);
 void gather_rows(cv_ctx* ctx, const SplitBuf& b, int rows, int cols, float* out);  // out = hi + lo
 void mlp_linearize(cv_ctx* ctx, cv_snap* s, double* loss_out, float* grad_out);
+void pad_last_weights(cv_ctx* ctx, cv_snap* s);
 void mlp_ggn(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, float* out, const int* skip);
 void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, float* out, const int* skip);
 void mlp_jvp(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, float* out_bc);

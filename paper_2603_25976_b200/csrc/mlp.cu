@@ -115,6 +115,75 @@ __global__ void k_finalize_sum(const double* partial, int nblk, double scale, do
 }
 
 // ---------------------------------------------------------------------------
+// Tensor-core output layer helpers (tc_out): padded split copies of the c-wide
+// operands and the row-wise post-processing of the JVP partials.
+// ---------------------------------------------------------------------------
+// rows x c (ld ld_src) -> rows x cp split, zero padded; from (hi, lo) or from plain fp32
+__global__ void k_pad_split(const float* hi, const float* lo, const float* plain, int64_t ld_src, int rows, int c,
+                            int cp, float* ohi, float* olo, const int* skip) {
+  if (skip_if(skip)) return;
+  const int64_t total = (int64_t)rows * cp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cp;
+    const int j = (int)(i - r * cp);
+    float h = 0.f, l = 0.f;
+    if (j < c) {
+      if (plain) split2(plain[r * ld_src + j], h, l);
+      else { h = hi[r * ld_src + j]; l = lo[r * ld_src + j]; }
+    }
+    ohi[i] = h;
+    olo[i] = l;
+  }
+}
+
+// out-layer JVP: sum the split-K partials of z = J v per row, then either store
+// the logits tangent (POST_LOGITS) or U = H_z(z) * scale (models.py:199-204)
+template <int CM>
+__global__ void k_out_reduce(const float* part, int splits, int rows, int c, int post, int loss, const float* probs,
+                             float scale, float* out_plain, float* ohi, float* olo, int cp, const int* skip) {
+  if (skip_if(skip)) return;
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= rows) return;
+  float t[CM];
+#pragma unroll
+  for (int j = 0; j < CM; ++j) t[j] = 0.f;
+  for (int z = 0; z < splits; ++z) {
+    const float* p = part + ((int64_t)z * rows + m) * c;
+#pragma unroll
+    for (int j = 0; j < CM; ++j)
+      if (j < c) t[j] += p[j];
+  }
+  if (post == 1) {
+    if (loss == CV_LOSS_CE) {
+      const float* p = probs + (int64_t)m * c;
+      float pt = 0.f;
+#pragma unroll
+      for (int j = 0; j < CM; ++j)
+        if (j < c) pt = fmaf(p[j], t[j], pt);
+#pragma unroll
+      for (int j = 0; j < CM; ++j)
+        if (j < c) t[j] = (p[j] * t[j] - p[j] * pt) * scale;
+    } else {
+#pragma unroll
+      for (int j = 0; j < CM; ++j) t[j] *= scale;
+    }
+  }
+  if (out_plain)
+#pragma unroll
+    for (int j = 0; j < CM; ++j)
+      if (j < c) out_plain[(int64_t)m * c + j] = t[j];
+  if (ohi)
+#pragma unroll
+    for (int j = 0; j < CM; ++j)
+      if (j < cp) {
+        float h = 0.f, l = 0.f;
+        if (j < c) split2(t[j], h, l);
+        ohi[(int64_t)m * cp + j] = h;
+        olo[(int64_t)m * cp + j] = l;
+      }
+}
+
+// ---------------------------------------------------------------------------
 // Host orchestration
 // ---------------------------------------------------------------------------
 static void launch_skinny_rows(cv_ctx* ctx, const SkinnyRowsArgs& a) { skinny_rows(ctx, a); }
@@ -126,6 +195,31 @@ static Operand op_rows(const SplitBuf& b) { return Operand{b.hi, b.lo, b.ld, 1};
 static Operand op_trans(const SplitBuf& b) { return Operand{b.hi, b.lo, 1, b.ld}; }         // X(m,k)=buf[k,m]
 static Operand op_wblock(const float* hi, const float* lo, int nout) { return Operand{hi, lo, nout, 1}; }
 static Operand op_wT(const float* hi, const float* lo, int nout) { return Operand{hi, lo, 1, nout}; }
+
+// last-layer block of a split flat vector -> padded split copy (tc_out)
+static void pad_last(cv_ctx* ctx, cv_snap* s, const float* hi, const float* lo, float* ohi, float* olo,
+                     const int* skip) {
+  const int l = s->L - 1;
+  const int rows = s->dims[l] + 1;
+  k_pad_split<<<grid_for((int64_t)rows * s->cp), 256, 0, ctx->stream>>>(hi + s->off[l], lo + s->off[l], nullptr, s->c,
+                                                                         rows, s->c, s->cp, ohi, olo, skip);
+  ctx->launches++;
+}
+
+void pad_last_weights(cv_ctx* ctx, cv_snap* s) { pad_last(ctx, s, s->w_hi, s->w_lo, s->wl_hi, s->wl_lo, nullptr); }
+
+// the split (ld cp) form of a b x c cotangent: U / G[L-1] map to their resident
+// splits, any other (plain, ld c) matrix is split into U_hi / U_lo
+static void cot_split(cv_ctx* ctx, cv_snap* s, const float* U, const float** hi, const float** lo, const int* skip) {
+  if (U == s->gout) { *hi = s->gout_hi; *lo = s->gout_lo; return; }
+  if (U != s->U) {
+    k_pad_split<<<grid_for((int64_t)s->bl * s->cp), 256, 0, ctx->stream>>>(nullptr, nullptr, U, s->c, s->bl, s->c,
+                                                                           s->cp, s->U_hi, s->U_lo, skip);
+    ctx->launches++;
+  }
+  *hi = s->U_hi;
+  *lo = s->U_lo;
+}
 
 void mlp_forward_layer(cv_ctx* ctx, cv_snap* s, int l, const SplitBuf& in, const float* whi, const float* wlo,
                        const SplitBuf& out) {
@@ -146,6 +240,24 @@ void mlp_forward_layer(cv_ctx* ctx, cv_snap* s, int l, const SplitBuf& in, const
 void mlp_output_layer(cv_ctx* ctx, cv_snap* s, const SplitBuf& in, const float* whi, const float* wlo,
                       float* logits) {
   const int l = s->L - 1;
+  if (s->tc_out) {
+    const float *bh = s->wl_hi, *bl = s->wl_lo;
+    if (whi != s->w_hi) {  // another parameter point (loss_at): pad its last block
+      pad_last(ctx, s, whi, wlo, s->vl_hi, s->vl_lo, nullptr);
+      bh = s->vl_hi;
+      bl = s->vl_lo;
+    }
+    GemmArgs g;
+    g.M = s->bl;
+    g.N = s->c;
+    g.nseg = 1;
+    g.seg[0] = GemmSeg{op_rows(in), Operand{bh, bl, s->cp, 1}, s->dims[l] + 1};
+    g.epi.mode = EPI_STORE;
+    g.epi.out = logits;
+    g.epi.ld = s->c;
+    gemm(ctx, g);
+    return;
+  }
   SkinnyRowsArgs a{};
   a.rows = s->bl;
   a.c = s->c;
@@ -164,6 +276,28 @@ void mlp_loss(cv_ctx* ctx, cv_snap* s, const float* logits, int write_state, dou
 static void skinny_backward(cv_ctx* ctx, cv_snap* s, const float* U, const float* whi, const float* wlo,
                             const SplitBuf& out, float* raw, const int* skip) {
   const int l = s->L - 1;
+  if (s->tc_out) {
+    const float *uh, *ul;
+    cot_split(ctx, s, U, &uh, &ul, skip);
+    GemmArgs g;
+    g.M = s->bl;
+    g.N = s->dims[l];
+    g.nseg = 1;
+    g.seg[0] = GemmSeg{Operand{uh, ul, s->cp, 1}, Operand{s->wl_hi, s->wl_lo, 1, s->cp}, s->c};
+    g.epi.mode = EPI_SPLIT_MASK;
+    g.epi.act = s->act;
+    g.epi.out_hi = out.hi;
+    g.epi.out_lo = out.lo;
+    g.epi.ld = out.ld;
+    g.epi.mask_hi = s->acts[l].hi;
+    g.epi.mask_lo = s->acts[l].lo;
+    g.epi.mask_ld = s->acts[l].ld;
+    g.epi.raw = raw;
+    g.epi.raw_ld = out.ld;
+    g.skip = skip;
+    gemm(ctx, g);
+    return;
+  }
   SkinnyDxArgs a{};
   a.rows = s->bl;
   a.n = s->dims[l];
@@ -227,6 +361,23 @@ static void weight_grad(cv_ctx* ctx, cv_snap* s, int l, const SplitBuf& G1, cons
 static void skinny_weight_grad(cv_ctx* ctx, cv_snap* s, const float* U, const SplitBuf* A2, const float* U2,
                                float* out, const int* skip) {
   const int l = s->L - 1;
+  if (s->tc_out) {
+    const float *uh, *ul, *u2h = nullptr, *u2l = nullptr;
+    cot_split(ctx, s, U, &uh, &ul, skip);
+    if (A2) cot_split(ctx, s, U2, &u2h, &u2l, skip);
+    GemmArgs g;
+    g.M = s->dims[l] + 1;
+    g.N = s->c;
+    g.nseg = A2 ? 2 : 1;
+    g.seg[0] = GemmSeg{op_trans(s->acts[l]), Operand{uh, ul, s->cp, 1}, s->bl};
+    if (A2) g.seg[1] = GemmSeg{op_trans(*A2), Operand{u2h, u2l, s->cp, 1}, s->bl};
+    g.epi.mode = EPI_STORE;
+    g.epi.out = out + s->off[l];
+    g.epi.ld = s->c;
+    g.skip = skip;
+    gemm(ctx, g);
+    return;
+  }
   SkinnyDwArgs a{};
   a.rows = s->bl;
   a.M = s->dims[l] + 1;
@@ -295,6 +446,33 @@ static void jvp_hidden(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* v
 static void jvp_out(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, int post, float scale,
                     float* out, const int* skip) {
   const int l = s->L - 1;
+  if (s->tc_out) {
+    pad_last(ctx, s, vhi, vlo, s->vl_hi, s->vl_lo, skip);
+    GemmArgs g;
+    g.M = s->bl;
+    g.N = s->c;
+    g.nseg = 1;
+    g.seg[0] = GemmSeg{op_rows(s->acts[l]), Operand{s->vl_hi, s->vl_lo, s->cp, 1}, s->dims[l] + 1};
+    if (l > 0) {
+      g.seg[1] = GemmSeg{op_rows(s->da[l - 1]), Operand{s->wl_hi, s->wl_lo, s->cp, 1}, s->dims[l]};
+      g.nseg = 2;
+    }
+    g.skip = skip;
+    float* part = nullptr;
+    const int splits = gemm_tc_partial(ctx, g, &part);
+    const bool hz = post == POST_HZ;
+    if (s->c <= 16)
+      k_out_reduce<16><<<(s->bl + 127) / 128, 128, 0, ctx->stream>>>(part, splits, s->bl, s->c, hz, s->loss, s->probs,
+                                                                    scale, out, hz ? s->U_hi : nullptr,
+                                                                    hz ? s->U_lo : nullptr, s->cp, skip);
+    else
+      k_out_reduce<32><<<(s->bl + 127) / 128, 128, 0, ctx->stream>>>(part, splits, s->bl, s->c, hz, s->loss, s->probs,
+                                                                    scale, out, hz ? s->U_hi : nullptr,
+                                                                    hz ? s->U_lo : nullptr, s->cp, skip);
+    ctx->launches++;
+    ctx->pool.put(part);
+    return;
+  }
   SkinnyRowsArgs a{};
   a.rows = s->bl;
   a.c = s->c;
@@ -360,6 +538,31 @@ void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, float*
   if (L >= 2) {
     // dG_{L-2} = (dG W^T + G_{L-1} V^T) * sp + [tanh] P * spp * dz
     const int l = L - 1;
+    if (s->tc_out) {
+      // vl holds this product's padded last block (written by jvp_out)
+      GemmArgs g;
+      g.M = s->bl;
+      g.N = s->dims[l];
+      g.nseg = 2;
+      g.seg[0] = GemmSeg{Operand{s->U_hi, s->U_lo, s->cp, 1}, Operand{s->wl_hi, s->wl_lo, 1, s->cp}, s->c};
+      g.seg[1] = GemmSeg{Operand{s->gout_hi, s->gout_lo, s->cp, 1}, Operand{s->vl_hi, s->vl_lo, 1, s->cp}, s->c};
+      g.epi.mode = EPI_HVP;
+      g.epi.act = s->act;
+      g.epi.out_hi = s->gs[l - 1].hi;
+      g.epi.out_lo = s->gs[l - 1].lo;
+      g.epi.ld = s->gs[l - 1].ld;
+      g.epi.mask_hi = s->acts[l].hi;
+      g.epi.mask_lo = s->acts[l].lo;
+      g.epi.mask_ld = s->acts[l].ld;
+      if (tanh_) {
+        g.epi.P = s->P[l - 1];
+        g.epi.P_ld = s->gs[l - 1].ld;
+        g.epi.dz = s->dz[l - 1];
+        g.epi.dz_ld = s->da[l - 1].ld;
+      }
+      g.skip = skip;
+      gemm(ctx, g);
+    }
     SkinnyDxArgs a{};
     a.rows = s->bl;
     a.n = s->dims[l];
@@ -386,7 +589,7 @@ void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, float*
       a.epi.dz_ld = s->da[l - 1].ld;
     }
     a.skip = skip;
-    launch_skinny_dx(ctx, a);
+    if (!s->tc_out) launch_skinny_dx(ctx, a);
     for (int h = L - 2; h >= 0; --h) {
       weight_grad(ctx, s, h, s->gs[h], h > 0 ? &s->da[h - 1] : nullptr, h > 0 ? &s->G[h] : nullptr, out, skip);
       if (h > 0) {
@@ -424,6 +627,12 @@ void mlp_loss(cv_ctx* ctx, cv_snap* s, const float* logits, int write_state, dou
   const int nblk = 64;
   k_loss_rows<<<nblk, 256, 0, ctx->stream>>>(logits, s->bl, s->c, s->loss, s->y_i, s->y_f, s->probs, s->gout,
                                              1.0f / (float)s->bg, ctx->red_ws, write_state);
+  if (write_state && s->tc_out) {
+    k_pad_split<<<grid_for((int64_t)s->bl * s->cp), 256, 0, ctx->stream>>>(nullptr, nullptr, s->gout, s->c, s->bl,
+                                                                           s->c, s->cp, s->gout_hi, s->gout_lo,
+                                                                           nullptr);
+    ctx->launches++;
+  }
   const double scale = 1.0 / (double)s->bg;
   k_finalize_sum<<<1, 32, 0, ctx->stream>>>(ctx->red_ws, nblk, ctx->world > 1 ? 1.0 : scale, loss_out);
   ctx->launches += 2;
