@@ -200,7 +200,60 @@ def trajectory_cases():
     save("trajectories", **out)
 
 
+def plan_cases():
+    """Plans of every preset and the stable AssemblyError messages (method.py:181-218, 412-552)."""
+    import dataclasses
+    import json
+
+    from curvopt.errors import AssemblyError
+    from curvopt.method import PRESET_NAMES, make
+
+    m = Model(6, (5,), 3, "relu")
+    plans = {}
+    for name in PRESET_NAMES:
+        p = make(name, m).plan
+        g = p.gates
+        plans[name] = {
+            "lane": p.lane, "algo": p.algo, "schema": list(p.schema),
+            "gates": {k: getattr(g, k).k for k in ("rho", "trace", "top_eig", "estimator", "tr_rho")},
+            "solver_config": dataclasses.asdict(p.solver_config),
+            "needs_row_primitives": p.needs_row_primitives, "needs_rho": p.needs_rho,
+        }
+    bad = {
+        "solver_without_curvature": {"curvature": None},
+        "row_with_hessian": {"curvature": {"kind": "hessian"}, "solver": {"kind": "row_cholesky"}},
+        "diag_without_source": {"solver": {"kind": "diag"}},
+        "gnb_with_mse": {"curvature": {"kind": "ggn_mse"}, "estimator": {"kind": "gnb"}},
+        "sq_grad_with_estimator": {"precond": {"kind": "sq_grad"}, "estimator": {"kind": "hutchinson"}},
+        "ema_without_estimator": {"precond": {"kind": "diag_ema"}},
+        "tr_disabled_cadence": {"damping": {"policy": "trust_region", "tr": {"every_k": -1}}},
+        "unknown_field": {"bogus": 1},
+        "unknown_curvature": {"curvature": {"kind": "fisher"}},
+        "unknown_solver": {"solver": {"kind": "lbfgs"}},
+        "unknown_policy": {"damping": {"policy": "step_norm"}},
+    }
+    msgs = {}
+    for key, ov in bad.items():
+        try:
+            make("sgn_ce", m, **ov)
+            msgs[key] = None
+        except (AssemblyError, TypeError, ValueError) as e:
+            msgs[key] = f"{type(e).__name__}: {e}"
+    for key, ov in {"telemetry_without_curvature": {"telemetry": {"rho_every_k": 2}},
+                    "tr_without_curvature": {"damping": {"policy": "trust_region"}}}.items():
+        try:
+            make("sgd", m, **ov)
+            msgs[key] = None
+        except (AssemblyError, ValueError) as e:
+            msgs[key] = f"{type(e).__name__}: {e}"
+    with open(os.path.join(HERE, "plans.json"), "w") as f:
+        json.dump({"plans": plans, "errors": msgs, "overrides": {k: v for k, v in bad.items()}}, f, indent=1,
+                  sort_keys=True)
+    print("wrote plans.json")
+
+
 if __name__ == "__main__":
     rng_cases()
     primitive_cases()
     trajectory_cases()
+    plan_cases()
