@@ -353,6 +353,30 @@ __global__ void k_trsv_bwd_diag(const float* dinv, int nb, int j0, const double*
     v[j0 + t] = s;
   }
 }
+// r = rhs - (G + mu I) v, one warp per row, fp64 accumulation (refinement residual)
+__global__ void k_row_residual(const float* G, int64_t m, float mu, const float* rhs, const double* v, double* r) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= m) return;
+  const float* g = G + row * m;
+  const bool vec = (m & 3) == 0;
+  double s = 0.0;
+  for (int64_t k = lane * 4; k < m; k += 128) {
+    if (vec && k + 3 < m) {
+      const float4 q = *reinterpret_cast<const float4*>(g + k);
+      s += (double)q.x * v[k] + (double)q.y * v[k + 1] + (double)q.z * v[k + 2] + (double)q.w * v[k + 3];
+    } else {
+      for (int64_t t = k; t < m; ++t) s += (double)g[t] * v[t];
+    }
+  }
+  s = warp_sum(s);
+  if (lane == 0) r[row] = (double)rhs[row] - (s + (double)mu * v[row]);
+}
+
+__global__ void k_axpy_d(const double* x, double* y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) y[i] += x[i];
+}
+
 __global__ void k_f2d(const float* x, double* y, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) y[i] = x[i];
 }
@@ -407,31 +431,43 @@ int row_solve_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, flo
   cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
   cudaStreamSynchronize(st);
   if (hflag) return 1;
-  // triangular solves in fp64
-  double* r = (double*)ctx->pool.get(sizeof(double) * m * 3);
+  // fp64 triangular solves, then iterative refinement against the fp32 Gram:
+  // v <- v + (L L^T)^-1 (rhs - (Gram + mu I) v), residual accumulated in fp64
+  double* r = (double*)ctx->pool.get(sizeof(double) * m * 4);
   double* y = r + m;
   double* v = r + 2 * m;
+  double* dv = r + 3 * m;
   const int rpb = 256;
   const int nparts_max = (int)((m + rpb - 1) / rpb);
   double* part = (double*)ctx->pool.get(sizeof(double) * (size_t)nparts_max * CH_NB);
+  auto tri_solve = [&](double* x) {  // r -> x = (L L^T)^-1 r   (r is consumed)
+    for (int bi = 0; bi < nblk; ++bi) {
+      const int j0 = bi * CH_NB;
+      const int nb = (int)((m - j0) < CH_NB ? (m - j0) : CH_NB);
+      k_trsv_fwd_diag<<<1, CH_NB, 0, st>>>(s->dinv + (int64_t)bi * CH_NB * CH_NB, nb, j0, r, y);
+      const int64_t rest = m - j0 - nb;
+      if (rest > 0) k_trsv_fwd_update<<<(int)((rest + 7) / 8), 256, 0, st>>>(s->chol, m, m, j0, nb, y, r);
+    }
+    for (int bi = nblk - 1; bi >= 0; --bi) {
+      const int j0 = bi * CH_NB;
+      const int nb = (int)((m - j0) < CH_NB ? (m - j0) : CH_NB);
+      const int64_t rest = m - j0 - nb;
+      const int nparts = (int)((rest + rpb - 1) / rpb);
+      if (nparts > 0) k_trsv_bwd_gather<<<nparts, CH_NB, 0, st>>>(s->chol, m, m, j0, nb, x, part, rpb);
+      k_trsv_bwd_diag<<<1, CH_NB, 0, st>>>(s->dinv + (int64_t)bi * CH_NB * CH_NB, nb, j0, y, part, nparts, x);
+    }
+    ctx->launches += 4 * nblk;
+  };
   k_f2d<<<256, 256, 0, st>>>(rhs, r, m);
-  for (int bi = 0; bi < nblk; ++bi) {
-    const int j0 = bi * CH_NB;
-    const int nb = (int)((m - j0) < CH_NB ? (m - j0) : CH_NB);
-    k_trsv_fwd_diag<<<1, CH_NB, 0, st>>>(s->dinv + (int64_t)bi * CH_NB * CH_NB, nb, j0, r, y);
-    const int64_t rest = m - j0 - nb;
-    if (rest > 0) k_trsv_fwd_update<<<(int)((rest + 7) / 8), 256, 0, st>>>(s->chol, m, m, j0, nb, y, r);
-  }
-  for (int bi = nblk - 1; bi >= 0; --bi) {
-    const int j0 = bi * CH_NB;
-    const int nb = (int)((m - j0) < CH_NB ? (m - j0) : CH_NB);
-    const int64_t rest = m - j0 - nb;
-    const int nparts = (int)((rest + rpb - 1) / rpb);
-    if (nparts > 0) k_trsv_bwd_gather<<<nparts, CH_NB, 0, st>>>(s->chol, m, m, j0, nb, v, part, rpb);
-    k_trsv_bwd_diag<<<1, CH_NB, 0, st>>>(s->dinv + (int64_t)bi * CH_NB * CH_NB, nb, j0, y, part, nparts, v);
+  tri_solve(v);
+  for (int it = 0; it < 2; ++it) {
+    k_row_residual<<<(int)((m + 7) / 8), 256, 0, st>>>(s->gram, m, (float)mu, rhs, v, r);
+    tri_solve(dv);
+    k_axpy_d<<<256, 256, 0, st>>>(dv, v, m);
+    ctx->launches += 2;
   }
   k_d2f<<<256, 256, 0, st>>>(v, v_out, m);
-  ctx->launches += 2 + 4 * nblk;
+  ctx->launches += 2;
   ctx->pool.put(part);
   ctx->pool.put(r);
   return 0;
