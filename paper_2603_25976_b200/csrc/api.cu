@@ -75,6 +75,11 @@ int cv_ctx_create(int device, int world, int rank, const void* nccl_id, cv_ctx**
   if (world > 1) {
     contract(nccl_id != nullptr, "world > 1 requires an NCCL unique id");
     nccl_init(c, nccl_id);
+  } else if (getenv("CURVOPT_FORCE_NCCL")) {
+    // single-rank communicator: exercises the NCCL path of every product on one GPU
+    char id[128];
+    nccl_unique_id(id);
+    nccl_init(c, id);
   }
   CV_CATCH
 }

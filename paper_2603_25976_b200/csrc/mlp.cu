@@ -408,7 +408,7 @@ void mlp_linearize(cv_ctx* ctx, cv_snap* s, double* loss_out, float* grad_out) {
   if (grad_out) {
     skinny_weight_grad(ctx, s, s->gout, nullptr, nullptr, grad_out, nullptr);
     for (int l = L - 2; l >= 0; --l) weight_grad(ctx, s, l, s->G[l], nullptr, nullptr, grad_out, nullptr);
-    if (ctx->world > 1) allreduce_f32(ctx, grad_out, s->d);
+    if (ctx->nccl) allreduce_f32(ctx, grad_out, s->d);
   }
 }
 
@@ -513,7 +513,7 @@ void mlp_ggn(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, float*
   jvp_hidden(ctx, s, vhi, vlo, false, skip);
   jvp_out(ctx, s, vhi, vlo, POST_HZ, 1.0f / (float)s->bg, s->U, skip);
   vjp_from(ctx, s, s->U, out, skip);
-  if (ctx->world > 1) allreduce_f32(ctx, out, s->d);
+  if (ctx->nccl) allreduce_f32(ctx, out, s->d);
 }
 
 void mlp_jvp(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, float* out_bc) {
@@ -523,7 +523,7 @@ void mlp_jvp(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, float*
 
 void mlp_vjp(cv_ctx* ctx, cv_snap* s, const float* U, float* out) {
   vjp_from(ctx, s, U, out, nullptr);
-  if (ctx->world > 1) allreduce_f32(ctx, out, s->d);
+  if (ctx->nccl) allreduce_f32(ctx, out, s->d);
 }
 
 // Exact Hessian-vector product (models.py:287-307), forward-over-reverse.
@@ -620,7 +620,7 @@ void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, float*
       }
     }
   }
-  if (ctx->world > 1) allreduce_f32(ctx, out, s->d);
+  if (ctx->nccl) allreduce_f32(ctx, out, s->d);
 }
 
 void mlp_loss(cv_ctx* ctx, cv_snap* s, const float* logits, int write_state, double* loss_out) {
@@ -634,9 +634,9 @@ void mlp_loss(cv_ctx* ctx, cv_snap* s, const float* logits, int write_state, dou
     ctx->launches++;
   }
   const double scale = 1.0 / (double)s->bg;
-  k_finalize_sum<<<1, 32, 0, ctx->stream>>>(ctx->red_ws, nblk, ctx->world > 1 ? 1.0 : scale, loss_out);
+  k_finalize_sum<<<1, 32, 0, ctx->stream>>>(ctx->red_ws, nblk, ctx->nccl ? 1.0 : scale, loss_out);
   ctx->launches += 2;
-  if (ctx->world > 1) {
+  if (ctx->nccl) {
     allreduce_f64(ctx, loss_out, 1);
     scale_scalar(ctx, loss_out, scale);
   }

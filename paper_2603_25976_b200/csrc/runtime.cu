@@ -118,13 +118,13 @@ void nccl_destroy(cv_ctx* ctx) {
 }
 
 void allreduce_f32(cv_ctx* ctx, float* buf, int64_t n) {
-  if (ctx->world <= 1) return;
+  if (!ctx->nccl) return;
   nccl_check(nccl_api().AllReduce(buf, buf, (size_t)n, ncclFloat32, ncclSum, (ncclComm_t)ctx->nccl, ctx->stream),
              "AllReduce");
 }
 
 void allreduce_f64(cv_ctx* ctx, double* buf, int64_t n) {
-  if (ctx->world <= 1) return;
+  if (!ctx->nccl) return;
   nccl_check(nccl_api().AllReduce(buf, buf, (size_t)n, ncclFloat64, ncclSum, (ncclComm_t)ctx->nccl, ctx->stream),
              "AllReduce");
 }

@@ -1,0 +1,49 @@
+"""The NCCL code path (all-reduce of gradients, losses and every curvature
+product inside libcurvopt_b200) exercised on one GPU through a single-rank
+communicator (CURVOPT_FORCE_NCCL=1): results must be bitwise identical to the
+communicator-free run."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import sys, json; sys.path.insert(0, %r)
+import numpy as np, torch
+import paper_2603_25976_b200 as P
+from oracle import curvopt_oracle as O
+m = P.Model(784, (256, 256), 10, "relu")
+w = P.init_params(m, P.Rng(0))
+X, y = O.synthetic_batch(512, 784, 10)
+meth = P.make("sgn_ce", m, solver={"cg": {"maxiter": 10}}, estimator={"kind": "hutchinson", "every_k": 1},
+              precond={"kind": "diag_ema"})
+st = meth.init(w, 0)
+rows = []
+for _ in range(2):
+    w, st, info = meth.step(w, P.Batch(X, y, "ce"), st)
+    rows.append(info.to_row())
+print(json.dumps({"rows": rows, "w": float(np.asarray(w.data, dtype=np.float64).sum())}))
+""" % ROOT
+
+
+def _run(env_extra):
+    env = dict(os.environ, **env_extra)
+    out = subprocess.run([sys.executable, "-c", SCRIPT], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def test_forced_single_rank_nccl_matches():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    a = _run({})
+    b = _run({"CURVOPT_FORCE_NCCL": "1"})
+    assert a["rows"] == b["rows"] or json.dumps(a["rows"]) == json.dumps(b["rows"])
+    assert a["w"] == b["w"]
