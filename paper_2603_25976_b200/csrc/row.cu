@@ -366,7 +366,7 @@ __global__ void k_row_residual(const float* G, int64_t m, float mu, const float*
       const float4 q = *reinterpret_cast<const float4*>(g + k);
       s += (double)q.x * v[k] + (double)q.y * v[k + 1] + (double)q.z * v[k + 2] + (double)q.w * v[k + 3];
     } else {
-      for (int64_t t = k; t < m; ++t) s += (double)g[t] * v[t];
+      for (int64_t t = k; t < k + 4 && t < m; ++t) s += (double)g[t] * v[t];
     }
   }
   s = warp_sum(s);

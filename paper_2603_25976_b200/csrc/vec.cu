@@ -32,6 +32,8 @@ CV_DEV void write_partials(double* ws, double (&t)[NV]) {
     for (int v = 0; v < NV; ++v) ws[blockIdx.x * 8 + v] = t[v];
 }
 
+CV_DEV float4 ld4g(const float* p) { return *reinterpret_cast<const float4*>(p); }
+
 CV_DEV float minv_of(const float* pre, int64_t i, float lam, float floor_) {
   return pre ? 1.f / (fmaxf(pre[i], floor_) + lam) : 1.f;
 }
@@ -376,13 +378,23 @@ __global__ void k_cg_p0_final(const double* ws, CgDev* st) {
 __global__ void k_cg_pap(float* ap, const float* p, float lam, const CgDev* st, int64_t d, double* ws) {
   if (st->done) return;
   double t[3] = {0.0, 0.0, 0.0};
-  GRID_STRIDE(i, d) {
-    const float pi = p[i];
-    const float a = ap[i] + lam * pi;
-    ap[i] = a;
+  auto body = [&](float pi, float& a) {
+    a += lam * pi;
     t[0] += (double)pi * a;
     t[2] += isfinite(pi) ? 0.0 : 1.0;
     t[1] = fmax(t[1], (double)fabsf(pi));
+  };
+  const int64_t nq = d >> 2;  // 128-bit body (vectors are 256-byte aligned pool buffers)
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+    const float4 p4 = ld4g(p + 4 * q);
+    float4 a4 = ld4g(ap + 4 * q);
+    body(p4.x, a4.x); body(p4.y, a4.y); body(p4.z, a4.z); body(p4.w, a4.w);
+    *reinterpret_cast<float4*>(ap + 4 * q) = a4;
+  }
+  for (int64_t i = 4 * nq + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d; i += (int64_t)gridDim.x * blockDim.x) {
+    float a = ap[i];
+    body(p[i], a);
+    ap[i] = a;
   }
   // max is not a sum: reduce it separately through the same shared buffer
   double mx = t[1];
@@ -435,12 +447,27 @@ __global__ void k_cg_update(float* x, float* r, const float* p, const float* ap,
   if (st->done) return;
   const float a = (float)st->alpha;
   double t[2] = {0.0, 0.0};
-  GRID_STRIDE(i, d) {
-    x[i] += a * p[i];
-    const float ri = r[i] - a * ap[i];
-    r[i] = ri;
+  auto body = [&](int64_t i, float& xi, float& ri, float pi, float api) {
+    xi += a * pi;
+    ri -= a * api;
     t[0] += (double)ri * ri;
     t[1] += (double)ri * (minv_of(pre, i, lam, floor_) * ri);
+  };
+  const int64_t nq = d >> 2;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = 4 * q;
+    float4 x4 = ld4g(x + i), r4 = ld4g(r + i);
+    const float4 p4 = ld4g(p + i), a4 = ld4g(ap + i);
+    body(i, x4.x, r4.x, p4.x, a4.x); body(i + 1, x4.y, r4.y, p4.y, a4.y);
+    body(i + 2, x4.z, r4.z, p4.z, a4.z); body(i + 3, x4.w, r4.w, p4.w, a4.w);
+    *reinterpret_cast<float4*>(x + i) = x4;
+    *reinterpret_cast<float4*>(r + i) = r4;
+  }
+  for (int64_t i = 4 * nq + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d; i += (int64_t)gridDim.x * blockDim.x) {
+    float xi = x[i], ri = r[i];
+    body(i, xi, ri, p[i], ap[i]);
+    x[i] = xi;
+    r[i] = ri;
   }
   write_partials<2>(ws, t);
 }
@@ -494,7 +521,22 @@ __global__ void k_cg_pnext(const float* r, const float* pre, float lam, float fl
                            float* p, float* hi, float* lo) {
   if (st->done) return;
   const float beta = (float)st->alpha;
-  GRID_STRIDE(i, d) {
+  const int64_t nq = d >> 2;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = 4 * q;
+    const float4 r4 = ld4g(r + i);
+    float4 p4 = ld4g(p + i);
+    p4.x = minv_of(pre, i, lam, floor_) * r4.x + beta * p4.x;
+    p4.y = minv_of(pre, i + 1, lam, floor_) * r4.y + beta * p4.y;
+    p4.z = minv_of(pre, i + 2, lam, floor_) * r4.z + beta * p4.z;
+    p4.w = minv_of(pre, i + 3, lam, floor_) * r4.w + beta * p4.w;
+    *reinterpret_cast<float4*>(p + i) = p4;
+    float4 h4, l4;
+    split2(p4.x, h4.x, l4.x); split2(p4.y, h4.y, l4.y); split2(p4.z, h4.z, l4.z); split2(p4.w, h4.w, l4.w);
+    *reinterpret_cast<float4*>(hi + i) = h4;
+    *reinterpret_cast<float4*>(lo + i) = l4;
+  }
+  for (int64_t i = 4 * nq + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d; i += (int64_t)gridDim.x * blockDim.x) {
     const float v = minv_of(pre, i, lam, floor_) * r[i] + beta * p[i];
     p[i] = v;
     float h, l;
