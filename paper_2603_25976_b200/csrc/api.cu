@@ -194,6 +194,8 @@ int cv_linearize(cv_ctx* ctx, int n_layers, const int* dims, int act, int loss, 
     s->cp = c;
     s->tc_out = ctx->engine != CV_ENGINE_SIMT && !(env && env[0] == '0') && c >= 8 && b >= 128 && dims[L - 1] >= 64;
     if (s->tc_out) {
+      const char* dx = getenv("CURVOPT_TC_DX");
+      s->tc_dx = dx && dx[0] == '1';
       s->cp = c <= 16 ? 16 : 32;
       const int64_t wrows = dims[L - 1] + 1;
       s->wl_hi = alloc_f(s, wrows * s->cp);

@@ -140,6 +140,7 @@ struct cv_snap {
   // (16-byte rows for TMA), split: last-layer [W; b] (wl), per-product [V; Vb] (vl),
   // cotangent U and G[L-1] (gout).  cp == c when the SIMT skinny kernels are used.
   int tc_out = 0, cp = 0;
+  int tc_dx = 0;  // output-layer backward on tensor cores (default: bandwidth kernel)
   float* wl_hi = nullptr; float* wl_lo = nullptr;
   float* vl_hi = nullptr; float* vl_lo = nullptr;
   float* U_hi = nullptr; float* U_lo = nullptr;

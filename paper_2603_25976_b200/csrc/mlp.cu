@@ -276,7 +276,7 @@ void mlp_loss(cv_ctx* ctx, cv_snap* s, const float* logits, int write_state, dou
 static void skinny_backward(cv_ctx* ctx, cv_snap* s, const float* U, const float* whi, const float* wlo,
                             const SplitBuf& out, float* raw, const int* skip) {
   const int l = s->L - 1;
-  if (s->tc_out) {
+  if (s->tc_out && s->tc_dx) {
     const float *uh, *ul;
     cot_split(ctx, s, U, &uh, &ul, skip);
     GemmArgs g;
@@ -538,7 +538,7 @@ void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, float*
   if (L >= 2) {
     // dG_{L-2} = (dG W^T + G_{L-1} V^T) * sp + [tanh] P * spp * dz
     const int l = L - 1;
-    if (s->tc_out) {
+    if (s->tc_out && s->tc_dx) {
       // vl holds this product's padded last block (written by jvp_out)
       GemmArgs g;
       g.M = s->bl;
@@ -589,7 +589,7 @@ void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, float*
       a.epi.dz_ld = s->da[l - 1].ld;
     }
     a.skip = skip;
-    if (!s->tc_out) launch_skinny_dx(ctx, a);
+    if (!(s->tc_out && s->tc_dx)) launch_skinny_dx(ctx, a);
     for (int h = L - 2; h >= 0; --h) {
       weight_grad(ctx, s, h, s->gs[h], h > 0 ? &s->da[h - 1] : nullptr, h > 0 ? &s->G[h] : nullptr, out, skip);
       if (h > 0) {

@@ -307,3 +307,34 @@ def test_c3_full_size_gv_and_step_vs_oracle():
     gv = snap.matvec(P.ParamVector(v, w.layout)).data.double().cpu().numpy()
     gu = snap.matvec(P.ParamVector(u, w.layout)).data.double().cpu().numpy()
     assert abs(u @ gv - v @ gu) <= 1e-5 * abs(u @ gv)
+
+
+def test_abort_on_nonfinite_batch_matches_oracle():
+    """A non-finite loss aborts the step (method.py:317-319): w unchanged, TR damping
+    escalated, no probe drawn -- so the next (clean) step's Hutchinson probe is the
+    oracle's.  The gate is evaluated at the step's single host sync."""
+    dims = (784, 128, 10)
+    m = P.Model(784, (128,), 10, "relu")
+    w0 = P.init_params(m, P.Rng(0))
+    X, y = O.synthetic_batch(128, 784, 10)
+    Xbad = X.copy()
+    Xbad[3, 5] = np.nan
+    spec = _spec_c1(damping=P.DampingSpec("trust_region", 1.0, P.control.TrustRegionConfig(every_k=1)),
+                    estimator=P.EstimatorSpec("hutchinson", 1, every_k=1),
+                    precond=P.PrecondSpec("diag_ema", 0.9))
+    meth = P.assemble(spec, m)
+    st = meth.init(w0.to_device(), 0)
+    ospec = O.OSpec(damping="trust_region", tr_every_k=1, estimator_every_k=1, precond="diag_ema",
+                    precond_beta=0.9)
+    ost = O.oracle_init(ospec, w0.dim)
+    w, ow = w0.to_device(), np.asarray(w0.data, dtype=np.float64)
+    for Xs in (Xbad, X, Xbad, X):
+        w_prev = w.data.clone()
+        w, st, info = meth.step(w, P.Batch(Xs, y, "ce"), st)
+        ow, ost, oinfo, _ = O.oracle_step(ospec, dims, "relu", "ce", ow, Xs.astype(np.float64), y, ost)
+        ref = np.array([oinfo[f] for f in O.STEP_FIELDS], dtype=np.float64)
+        _cmp_info(info.to_row(), ref, rtol=2e-4)
+        if np.isnan(Xs).any():
+            assert torch.equal(w.data, w_prev)
+        assert st.damping.lam == pytest.approx(ost.lam, rel=1e-12)
+    assert rel(w.data.cpu().numpy(), ow) < 1e-4
