@@ -113,70 +113,107 @@ void skinny_rows(cv_ctx* ctx, const SkinnyRowsArgs& a) {
 }
 
 // ---------------------------------------------------------------------------
-// dx: block = 32 rows x NT columns; thread = 4 adjacent columns x 8 rows; W^T tile
-// and U rows in smem; 128-bit fused epilogue
+// dx: thread = 4 adjacent columns with their W^T entries held in registers; a
+// warp covers 128 contiguous columns of a row (512-byte coalesced accesses); the
+// block walks 32-row tiles (U rows staged in smem) and issues the R activation
+// loads of a row group before any of its stores.
 // ---------------------------------------------------------------------------
-template <int CM, int NT>
-__global__ void __launch_bounds__(256) k_dx(SkinnyDxArgs a) {
+template <int C, int NSEG, bool TANH>
+__global__ void __launch_bounds__(128) k_dx(SkinnyDxArgs a) {
   if (skip_if(a.skip)) return;
-  constexpr int RB = 32;
-  constexpr int QPR = NT / 4;             // column quads per block row
-  constexpr int RSTEP = 256 / QPR;        // row groups
-  __shared__ __align__(16) float Wt[2][CM][NT];
-  __shared__ float Us[2][RB][CM];
-  const int n0 = blockIdx.x * NT, m0 = blockIdx.y * RB;
-  for (int e = threadIdx.x; e < 2 * CM * NT; e += 256) {
-    const int s = e / (CM * NT), rem = e % (CM * NT), j = rem / NT, nn = rem % NT;
-    float v = 0.f;
-    if (s < a.nseg && j < a.c && n0 + nn < a.n) {
-      const int64_t idx = (int64_t)(n0 + nn) * a.c + j;
-      v = a.w_hi[s][idx] + a.w_lo[s][idx];
+  constexpr int RT = 32;   // rows per tile
+  constexpr int R = 8;     // rows per thread in flight
+  __shared__ __align__(16) float Us[NSEG][RT][C];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = blockIdx.x * 128 + lane * 4;
+  const bool colok = nb < a.n;
+  float w[NSEG][C][4];
+#pragma unroll
+  for (int s = 0; s < NSEG; ++s)
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const bool ok = nb + t < a.n;
+      const int64_t base = (int64_t)(nb + t) * a.c;
+#pragma unroll
+      for (int j = 0; j < C; ++j) w[s][j][t] = (ok && j < a.c) ? a.w_hi[s][base + j] + a.w_lo[s][base + j] : 0.f;
     }
-    Wt[s][j][nn] = v;
-  }
-  for (int e = threadIdx.x; e < 2 * RB * CM; e += 256) {
-    const int s = e / (RB * CM), rem = e % (RB * CM), r = rem / CM, j = rem % CM;
-    float v = 0.f;
-    if (s < a.nseg && m0 + r < a.rows && j < a.c) v = a.U[s][(int64_t)(m0 + r) * a.c + j];
-    Us[s][r][j] = v;
-  }
-  __syncthreads();
-  const int q = threadIdx.x % QPR, rg = threadIdx.x / QPR;
-  const int nb = n0 + 4 * q;
-  if (nb >= a.n) return;
-  for (int r = rg; r < RB; r += RSTEP) {
-    const int m = m0 + r;
-    if (m >= a.rows) break;
-    float v[4] = {0.f, 0.f, 0.f, 0.f};
+  const Epilogue& e = a.epi;
+  constexpr bool tanh_ = TANH;
+  const bool fast = (e.mode == EPI_SPLIT_MASK || (e.mode == EPI_HVP && !tanh_)) && e.mask_div == 1 &&
+                    al16(e.out_hi) && al16(e.out_lo) && al16(e.mask_hi) && (!tanh_ || al16(e.mask_lo)) &&
+                    (e.ld & 3) == 0 && (e.mask_ld & 3) == 0 && (!e.raw || (al16(e.raw) && (e.raw_ld & 3) == 0));
+  const bool full = nb + 4 <= a.n;
+  const int tiles = (a.rows + RT - 1) / RT;
+  for (int tile = blockIdx.y; tile < tiles; tile += gridDim.y) {
+    const int m0 = tile * RT;
+    __syncthreads();
+    for (int i = threadIdx.x; i < NSEG * RT * C; i += 128) {
+      const int s = i / (RT * C), rem = i % (RT * C), r = rem / C, j = rem % C;
+      Us[s][r][j] = (m0 + r < a.rows && j < a.c) ? a.U[s][(int64_t)(m0 + r) * a.c + j] : 0.f;
+    }
+    __syncthreads();
+    if (!colok) continue;
+    float4 mh[R], ml[TANH ? R : 1];
+    if (fast) {
 #pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      if (s >= a.nseg) break;
-#pragma unroll
-      for (int j = 0; j < CM; ++j) {
-        const float u = Us[s][r][j];
-        const float4 w4 = *reinterpret_cast<const float4*>(&Wt[s][j][4 * q]);
-        v[0] = fmaf(u, w4.x, v[0]);
-        v[1] = fmaf(u, w4.y, v[1]);
-        v[2] = fmaf(u, w4.z, v[2]);
-        v[3] = fmaf(u, w4.w, v[3]);
+      for (int i = 0; i < R; ++i) {
+        const int m = m0 + warp + 4 * i;
+        if (m < a.rows && full) {
+          const int64_t mo = (int64_t)m * e.mask_ld + nb;
+          mh[i] = ld4(e.mask_hi + mo);
+          if constexpr (TANH) ml[i] = ld4(e.mask_lo + mo);
+        }
       }
     }
-    if (!(nb + 4 <= a.n && epi_applyV<4>(a.epi, m, nb, v))) {
 #pragma unroll
-      for (int t = 0; t < 4; ++t)
-        if (nb + t < a.n) epi_apply(a.epi, m, nb + t, v[t]);
+    for (int i = 0; i < R; ++i) {
+      const int r = warp + 4 * i, m = m0 + r;
+      if (m >= a.rows) break;
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int s = 0; s < NSEG; ++s)
+#pragma unroll
+        for (int j = 0; j < C; ++j) {
+          const float u = Us[s][r][j];
+          v[0] = fmaf(u, w[s][j][0], v[0]);
+          v[1] = fmaf(u, w[s][j][1], v[1]);
+          v[2] = fmaf(u, w[s][j][2], v[2]);
+          v[3] = fmaf(u, w[s][j][3], v[3]);
+        }
+      if (fast && full) {
+        float av[4] = {mh[i].x, mh[i].y, mh[i].z, mh[i].w};
+        if constexpr (TANH) { av[0] += ml[i].x; av[1] += ml[i].y; av[2] += ml[i].z; av[3] += ml[i].w; }
+        if (e.raw) *reinterpret_cast<float4*>(e.raw + (int64_t)m * e.raw_ld + nb) = make_float4(v[0], v[1], v[2], v[3]);
+        float h[4], l[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) split2(v[t] * act_deriv(TANH ? CV_ACT_TANH : CV_ACT_RELU, av[t]), h[t], l[t]);
+        const int64_t o = (int64_t)m * e.ld + nb;
+        *reinterpret_cast<float4*>(e.out_hi + o) = make_float4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<float4*>(e.out_lo + o) = make_float4(l[0], l[1], l[2], l[3]);
+      } else if (!(full && epi_applyV<4>(e, m, nb, v))) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (nb + t < a.n) epi_apply(e, m, nb + t, v[t]);
+      }
     }
   }
 }
 
+template <int C, int NSEG>
+static void launch_dx(cv_ctx* ctx, const SkinnyDxArgs& a) {
+  const int gx = (a.n + 127) / 128;
+  const int tiles = (a.rows + 31) / 32;
+  int gy = (ctx->sm_count * 4 + gx - 1) / gx;  // ~4 resident 128-thread blocks per SM
+  if (gy > tiles) gy = tiles;
+  if (a.epi.act == CV_ACT_TANH) k_dx<C, NSEG, true><<<dim3(gx, gy), 128, 0, ctx->stream>>>(a);
+  else k_dx<C, NSEG, false><<<dim3(gx, gy), 128, 0, ctx->stream>>>(a);
+}
+
 void skinny_dx(cv_ctx* ctx, const SkinnyDxArgs& a) {
-  if (a.c <= 16) {
-    dim3 grid((a.n + 255) / 256, (a.rows + 31) / 32);
-    k_dx<16, 256><<<grid, 256, 0, ctx->stream>>>(a);
-  } else {
-    dim3 grid((a.n + 127) / 128, (a.rows + 31) / 32);
-    k_dx<32, 128><<<grid, 256, 0, ctx->stream>>>(a);
-  }
+  const bool two = a.nseg > 1;
+  if (a.c == 10) two ? launch_dx<10, 2>(ctx, a) : launch_dx<10, 1>(ctx, a);
+  else if (a.c <= 16) two ? launch_dx<16, 2>(ctx, a) : launch_dx<16, 1>(ctx, a);
+  else two ? launch_dx<32, 2>(ctx, a) : launch_dx<32, 1>(ctx, a);
   ctx->launches++;
 }
 
