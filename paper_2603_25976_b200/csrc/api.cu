@@ -48,7 +48,7 @@ static void contract(bool ok, const char* msg) {
 
 extern "C" {
 
-const char* cv_version(void) { return "curvopt_b200 0.1.0 (sm_100a, tcgen05 3xTF32 + SIMT fp32)"; }
+const char* cv_version(void) { return "curvopt_b200 0.2.0 (sm_100a, tcgen05 scaled 3xFP16 + SIMT fp32)"; }
 
 int cv_nccl_unique_id(void* out128) {
   try {
@@ -72,6 +72,9 @@ int cv_ctx_create(int device, int world, int rank, const void* nccl_id, cv_ctx**
   if (sms > 0) c->sm_count = sms;
   c->red_ws = (double*)c->pool.get(sizeof(double) * kRedBlocks * 8);
   c->scal_ws = (double*)c->pool.get(sizeof(double) * 64);
+  c->amax_ws = (float*)c->pool.get(sizeof(float) * 2 * 148 * 16);
+  c->amax_counter = (unsigned*)c->pool.get(sizeof(unsigned) * 64);
+  cudaMemsetAsync(c->amax_counter, 0, sizeof(unsigned) * 64, c->stream);
   if (world > 1) {
     contract(nccl_id != nullptr, "world > 1 requires an NCCL unique id");
     nccl_init(c, nccl_id);
@@ -117,15 +120,20 @@ static float* alloc_f(cv_snap* s, int64_t n) {
   return p;
 }
 
-static SplitBuf alloc_split(cv_snap* s, int rows, int n) {
-  SplitBuf b;
-  b.ld = ld_for(n);
-  b.hi = alloc_f(s, (int64_t)rows * b.ld);
-  b.lo = alloc_f(s, (int64_t)rows * b.ld);
-  return b;
+static __half* alloc_h(cv_snap* s, int64_t n) {
+  __half* p = (__half*)s->ctx->pool.get(sizeof(__half) * (size_t)(n > 0 ? n : 1));
+  s->owned.push_back(p);
+  return p;
 }
 
-static void zero_col(cv_ctx* ctx, const SplitBuf& b, int rows, int col) { set_col_value(ctx, b, rows, col, 0.f); }
+static SplitBuf alloc_split(cv_snap* s, int rows, int n, Scale* sc) {
+  SplitBuf b;
+  b.ld = ld_for(n);
+  b.hi = alloc_h(s, (int64_t)rows * b.ld);
+  b.lo = alloc_h(s, (int64_t)rows * b.ld);
+  b.sc = sc;
+  return b;
+}
 
 int cv_linearize(cv_ctx* ctx, int n_layers, const int* dims, int act, int loss, const float* w, const float* X,
                  const void* y, int b_local, int b_global, cv_snap** snap, double* loss_out, float* grad_out) {
@@ -157,11 +165,33 @@ int cv_linearize(cv_ctx* ctx, int n_layers, const int* dims, int act, int loss, 
   s->d = off;
   const int L = n_layers, b = b_local;
   try {
-    s->w_hi = alloc_f(s, s->d);
-    s->w_lo = alloc_f(s, s->d);
-    s->v_hi = alloc_f(s, s->d);
-    s->v_lo = alloc_f(s, s->d);
-    for (int l = 0; l < L; ++l) s->acts.push_back(alloc_split(s, b, dims[l]));
+    // Scale slots: w[L] v[L] acts[L] G[L-1] P[L-1] gout | per product: da[L-1] gs[L-1] U U2 dz[L-1] | scratch[8]
+    const int H = L - 1;
+    s->n_scales = 3 * L + 2 * H + 1 + (3 * H + 2) + 8;
+    s->scales = (Scale*)ctx->pool.get(sizeof(Scale) * s->n_scales);
+    s->owned.push_back(s->scales);
+    Scale* p = s->scales;
+    s->w_sc = p; p += L;
+    s->v_sc = p; p += L;
+    Scale* acts_sc = p; p += L;
+    Scale* G_sc = p; p += H;
+    Scale* P_sc = p; p += H;
+    s->gout_sc = p; p += 1;
+    s->prod_sc = p;
+    Scale* da_sc = p; p += H;
+    Scale* gs_sc = p; p += H;
+    s->U_sc = p; p += 1;
+    s->U2_sc = p; p += 1;
+    Scale* dz_sc = p; p += H;
+    s->n_prod = (int)(p - s->prod_sc);
+    s->scratch_sc = p; p += 8;
+    cudaMemsetAsync(s->scales, 0, sizeof(Scale) * s->n_scales, ctx->stream);
+
+    s->w_hi = alloc_h(s, s->d);
+    s->w_lo = alloc_h(s, s->d);
+    s->v_hi = alloc_h(s, s->d);
+    s->v_lo = alloc_h(s, s->d);
+    for (int l = 0; l < L; ++l) s->acts.push_back(alloc_split(s, b, dims[l], acts_sc + l));
     s->logits = alloc_f(s, (int64_t)b * c);
     s->probs = alloc_f(s, (int64_t)b * c);
     s->gout = alloc_f(s, (int64_t)b * c);
@@ -177,11 +207,13 @@ int cv_linearize(cv_ctx* ctx, int n_layers, const int* dims, int act, int loss, 
     }
     for (int l = 0; l + 1 < L; ++l) {
       const int n = dims[l + 1];
-      s->G.push_back(alloc_split(s, b, n));
-      s->da.push_back(alloc_split(s, b, n));
-      s->gs.push_back(alloc_split(s, b, n));
+      s->G.push_back(alloc_split(s, b, n, G_sc + l));
+      s->da.push_back(alloc_split(s, b, n, da_sc + l));
+      s->gs.push_back(alloc_split(s, b, n, gs_sc + l));
       s->P.push_back(act == CV_ACT_TANH ? alloc_f(s, (int64_t)b * ld_for(n)) : nullptr);
       s->dz.push_back(act == CV_ACT_TANH ? alloc_f(s, (int64_t)b * ld_for(n)) : nullptr);
+      s->P_sc.push_back(P_sc + l);
+      s->dz_sc.push_back(dz_sc + l);
     }
     // skinny weight-gradient partials: up to 2*SMs column blocks x (n+1) x c
     int64_t need = 0;
@@ -197,26 +229,26 @@ int cv_linearize(cv_ctx* ctx, int n_layers, const int* dims, int act, int loss, 
       const char* dx = getenv("CURVOPT_TC_DX");
       s->tc_dx = dx && dx[0] == '1';
       s->cp = c <= 16 ? 16 : 32;
-      const int64_t wrows = dims[L - 1] + 1;
-      s->wl_hi = alloc_f(s, wrows * s->cp);
-      s->wl_lo = alloc_f(s, wrows * s->cp);
-      s->vl_hi = alloc_f(s, wrows * s->cp);
-      s->vl_lo = alloc_f(s, wrows * s->cp);
-      s->U_hi = alloc_f(s, (int64_t)b * s->cp);
-      s->U_lo = alloc_f(s, (int64_t)b * s->cp);
-      s->gout_hi = alloc_f(s, (int64_t)b * s->cp);
-      s->gout_lo = alloc_f(s, (int64_t)b * s->cp);
+      s->ldw = ((int64_t)dims[L - 1] + 1 + 7) / 8 * 8;
+      s->ldb = ((int64_t)b + 7) / 8 * 8;
+      s->wl_hi = alloc_h(s, s->cp * s->ldw);
+      s->wl_lo = alloc_h(s, s->cp * s->ldw);
+      s->vl_hi = alloc_h(s, s->cp * s->ldw);
+      s->vl_lo = alloc_h(s, s->cp * s->ldw);
+      s->U_hi = alloc_h(s, s->cp * s->ldb);
+      s->U_lo = alloc_h(s, s->cp * s->ldb);
+      s->gout_hi = alloc_h(s, s->cp * s->ldb);
+      s->gout_lo = alloc_h(s, s->cp * s->ldb);
     }
   } catch (...) {
     for (void* p : s->owned) ctx->pool.put(p);
     delete s;
     throw;
   }
-  split_vec(ctx, w, s->w_hi, s->w_lo, s->d, nullptr);
+  split_flat(ctx, w, s->d, s->off, s->w_hi, s->w_lo, s->w_sc, nullptr, 0, nullptr);
   if (s->tc_out) pad_last_weights(ctx, s);
   split_rows(ctx, X, dims[0], b, dims[0], s->acts[0], 1);
-  for (int l = 1; l < L; ++l) set_ones_col(ctx, s->acts[l], b, dims[l]);
-  for (int l = 0; l + 1 < L; ++l) zero_col(ctx, s->da[l], b, dims[l + 1]);
+  for (int l = 0; l + 1 < L; ++l) set_col_value(ctx, s->da[l], b, dims[l + 1], 0.f);
   mlp_linearize(ctx, s, loss_out, grad_out);
   *snap = s;
   CV_CATCH
@@ -250,16 +282,14 @@ int cv_matvec(cv_snap* s, int kind, const float* v, float* out) {
   if (!s) return CV_E_CONTRACT;
   CV_TRY(s->ctx)
   contract(kind == CV_KIND_GGN || kind == CV_KIND_HESSIAN, "unknown curvature kind");
-  split_vec(_ctx, v, s->v_hi, s->v_lo, s->d, nullptr);
-  matvec_fn(kind)(_ctx, s, s->v_hi, s->v_lo, out, nullptr);
+  matvec_fn(kind)(_ctx, s, v, out, nullptr);
   CV_CATCH
 }
 
 int cv_jvp(cv_snap* s, const float* v, float* out_bc) {
   if (!s) return CV_E_CONTRACT;
   CV_TRY(s->ctx)
-  split_vec(_ctx, v, s->v_hi, s->v_lo, s->d, nullptr);
-  mlp_jvp(_ctx, s, s->v_hi, s->v_lo, out_bc);
+  mlp_jvp(_ctx, s, v, out_bc);
   CV_CATCH
 }
 
@@ -284,7 +314,7 @@ int cv_cg_solve(cv_snap* s, int kind, const float* g, double lam, double tol, in
 int cv_rademacher(cv_ctx* ctx, uint64_t seed, uint64_t counter, int64_t n, float* out) {
   CV_TRY(ctx)
   contract(n >= 1, "rademacher requires n >= 1");
-  rademacher(_ctx, seed, counter, n, out, nullptr, nullptr);
+  rademacher(_ctx, seed, counter, n, out);
   CV_CATCH
 }
 
@@ -328,8 +358,7 @@ int cv_rho_terms(cv_snap* s, int kind, const float* g, const float* u, double* g
     s->owned.push_back(hu);
     s->cg_ap = hu;
   }
-  split_vec(_ctx, u, s->v_hi, s->v_lo, s->d, nullptr);
-  matvec_fn(kind)(_ctx, s, s->v_hi, s->v_lo, hu, nullptr);
+  matvec_fn(kind)(_ctx, s, u, hu, nullptr);
   dot_into(_ctx, hu, u, s->d, u_H_u);
   CV_CATCH
 }
@@ -350,18 +379,26 @@ int cv_norm_check(cv_ctx* ctx, const float* x, int64_t d, double* scal) {
 int cv_gemm_test(cv_ctx* ctx, int engine, int M, int N, int K, const float* a, int64_t lda, int a_kmajor,
                  const float* b, int64_t ldb, int b_kmajor, float* out, int64_t ldo) {
   CV_TRY(ctx)
-  const int64_t na = a_kmajor ? (int64_t)M * lda : (int64_t)K * lda;
-  const int64_t nb = b_kmajor ? (int64_t)N * ldb : (int64_t)K * ldb;
-  float* buf = (float*)_ctx->pool.get(sizeof(float) * (size_t)(2 * na + 2 * nb));
-  float *ahi = buf, *alo = buf + na, *bhi = buf + 2 * na, *blo = buf + 2 * na + nb;
-  split_vec(_ctx, a, ahi, alo, na, nullptr);
-  split_vec(_ctx, b, bhi, blo, nb, nullptr);
+  // a: M x K (K-major, ld lda) or K x M (M-major); b: K x N (N-major, ld ldb) or N x K (K-major)
+  const int ar = a_kmajor ? M : K, ac = a_kmajor ? K : M;
+  const int br = b_kmajor ? N : K, bc = b_kmajor ? K : N;
+  const int64_t na = (int64_t)ar * lda, nb = (int64_t)br * ldb;
+  __half* buf = (__half*)_ctx->pool.get(sizeof(__half) * (size_t)(2 * na + 2 * nb) + 64);
+  Scale* sc = (Scale*)_ctx->pool.get(sizeof(Scale) * 2);
+  __half *ahi = buf, *alo = buf + na, *bhi = buf + 2 * na, *blo = buf + 2 * na + nb;
+  split_mat(_ctx, a, lda, ar, ac, ahi, alo, lda, 0, sc, 0, nullptr);
+  split_mat(_ctx, b, ldb, br, bc, bhi, blo, ldb, 0, sc + 1, 0, nullptr);
   GemmArgs g;
   g.M = M;
   g.N = N;
   g.nseg = 1;
-  g.seg[0].A = a_kmajor ? Operand{ahi, alo, lda, 1} : Operand{ahi, alo, 1, lda};
-  g.seg[0].B = b_kmajor ? Operand{bhi, blo, 1, ldb} : Operand{bhi, blo, ldb, 1};
+  Operand A, B;
+  A.hi = ahi; A.lo = alo; A.sc = sc;
+  B.hi = bhi; B.lo = blo; B.sc = sc + 1;
+  if (a_kmajor) { A.si = lda; A.sj = 1; } else { A.si = 1; A.sj = lda; }
+  if (b_kmajor) { B.si = 1; B.sj = ldb; } else { B.si = ldb; B.sj = 1; }
+  g.seg[0].A = A;
+  g.seg[0].B = B;
   g.seg[0].K = K;
   g.epi.mode = EPI_STORE;
   g.epi.out = out;
@@ -372,6 +409,7 @@ int cv_gemm_test(cv_ctx* ctx, int engine, int M, int N, int K, const float* a, i
   } else {
     gemm_simt(_ctx, g);
   }
+  _ctx->pool.put(sc);
   _ctx->pool.put(buf);
   CV_CATCH
 }

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <math.h>
+#include <cuda_fp16.h>
 
 #define CV_DEV __device__ __forceinline__
 
@@ -11,22 +12,53 @@ namespace cv {
 constexpr int kRedBlocks = 592;    // 4 x 148 SMs; fixed => deterministic reductions
 constexpr int kRedThreads = 256;
 
-// Round-to-nearest (ties away) fp32 -> tf32, returned as an fp32 bit pattern with
-// the low 13 mantissa bits cleared.  The tensor core consumes exactly these bits.
-CV_DEV float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+// ---------------------------------------------------------------------------
+// Scaled fp16 split ("3xFP16"): a tensor X is stored as two fp16 planes with one
+// power-of-two exponent e per tensor,
+//     X ~= (hi + lo) * 2^-e,   hi = rn(X 2^e),  lo = rn(X 2^e - hi),
+// which carries 22 significant bits (|X - (hi+lo)2^-e| <= 2^-22 |X| for entries
+// whose scaled magnitude is >= 2^-3; smaller entries keep an absolute error of
+// 2^-25 in scaled units).  e is chosen from a rigorous bound B >= max|X| so that
+// B 2^e <= 2^14: no overflow is possible and the scaled range keeps 14 binades of
+// headroom above fp16's subnormal floor.  The tensor core consumes the fp16
+// planes at twice the TF32 rate (hi.hi + hi.lo + lo.hi, fp32 accumulation).
+// ---------------------------------------------------------------------------
+struct Scale {
+  int e;        // X = (hi + lo) * 2^-e
+  float amax;   // max |X| of the stored tensor (true scale), maintained by its producer
+};
+
+// 2^e as a float for |e| <= 126
+CV_DEV float pow2f(int e) { return __int_as_float((127 + e) << 23); }
+
+// largest e with B * 2^e <= 2^14; 0 for zero / non-finite bounds (then the data
+// itself is zero or non-finite and the scale is irrelevant)
+CV_DEV int exp_for_bound(float B) {
+  if (!(B > 0.f) || !(B < 3.0e38f)) return 0;
+  int x;
+  frexpf(B, &x);  // B = f 2^x, f in [0.5, 1)  =>  B < 2^x
+  int e = 14 - x;
+  return e < -100 ? -100 : (e > 100 ? 100 : e);
 }
 
-// x ~= hi + lo, both exact tf32 values (|x - hi - lo| <= 2^-22 |x|).  lo is rounded
-// to nearest here rather than left with 13 significant bits: the tensor core
-// truncates operand bits beyond tf32, which biases every 3xTF32 product toward
-// zero (measured -8e-7 relative, amplified ~20x by the per-example cancellation
-// in the weight gradients).
-CV_DEV void split2(float x, float& hi, float& lo) {
-  hi = tf32_rna(x);
-  lo = tf32_rna(x - hi);
+CV_DEV void split16(float x, float s, __half& hi, __half& lo) {
+  const float xs = x * s;
+  hi = __float2half_rn(xs);
+  lo = __float2half_rn(xs - __half2float(hi));
+}
+
+CV_DEV float join16(__half hi, __half lo, float inv) { return (__half2float(hi) + __half2float(lo)) * inv; }
+
+// max|x| of non-negative float bit patterns via integer atomicMax (exact, order free)
+CV_DEV void atomic_amax(float* slot, float v) {
+  if (slot && v > 0.f) atomicMax(reinterpret_cast<int*>(slot), __float_as_int(v));
+  else if (slot && !(v == v)) atomicMax(reinterpret_cast<int*>(slot), 0x7fc00000);  // NaN poisons the bound
+}
+
+CV_DEV float warp_max_f(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
 }
 
 CV_DEV float relu_f(float x) { return x > 0.f ? x : 0.f; }

@@ -27,6 +27,7 @@ __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs a) {
 
   for (int s = 0; s < a.nseg; ++s) {
     const GemmSeg& g = a.seg[s];
+    const float ainv = op_inv(g.A), binv = op_inv(g.B);
     const bool a_kc = g.A.sj == 1;  // K contiguous in A
     const bool b_nc = g.B.sj == 1;  // N contiguous in B
     for (int k0 = 0; k0 < g.K; k0 += SB_K) {
@@ -36,11 +37,11 @@ __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs a) {
         int mm, kk;
         if (a_kc) { mm = e >> 4; kk = e & 15; } else { kk = e >> 6; mm = e & 63; }
         const int gm = m0 + mm, gk = k0 + kk;
-        As[kk][mm] = (gm < a.M && gk < g.K) ? ld_op(g.A, gm, gk) : 0.f;
+        As[kk][mm] = (gm < a.M && gk < g.K) ? ld_op(g.A, ainv, gm, gk) : 0.f;
         int nn;
         if (b_nc) { kk = e >> 6; nn = e & 63; } else { nn = e >> 4; kk = e & 15; }
         const int gn = n0 + nn, gk2 = k0 + kk;
-        Bs[kk][nn] = (gn < a.N && gk2 < g.K) ? ld_op(g.B, gk2, gn) : 0.f;
+        Bs[kk][nn] = (gn < a.N && gk2 < g.K) ? ld_op(g.B, binv, gk2, gn) : 0.f;
       }
       __syncthreads();
 #pragma unroll
@@ -57,6 +58,9 @@ __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs a) {
       __syncthreads();
     }
   }
+  const EpiRt rt = epi_prepare(a.epi);
+  if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) epi_publish(a.epi, rt);
+  float amax = 0.f, ramax = 0.f;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int m = m0 + ty * 4 + i;
@@ -64,9 +68,10 @@ __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs a) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int n = n0 + tx * 4 + j;
-      if (n < a.N && (!a.lower_only || n <= m)) epi_apply(a.epi, m, n, acc[i][j]);
+      if (n < a.N && (!a.lower_only || n <= m)) epi_apply(a.epi, rt, m, n, acc[i][j], amax, ramax);
     }
   }
+  epi_flush_amax(a.epi, amax, ramax);
 }
 
 void gemm_simt(cv_ctx* ctx, const GemmArgs& a) {

@@ -1,20 +1,27 @@
-// tcgen05 / TMA split-precision (3xTF32) GEMM engine for sm_100a.
+// tcgen05 / TMA split-precision (3xFP16, scaled) GEMM engine for sm_100a.
 //
 //   D[M x N] = sum_seg A_seg[M x K] . B_seg[K x N]        (fp32 accumulate in TMEM)
-//   with X = X_hi + X_lo (both stored fp32, hi exactly tf32):
-//   D = A_hi.B_hi + A_hi.B_lo + A_lo.B_hi                 (3 tcgen05.mma kind::tf32)
+//   with X = (X_hi + X_lo) 2^-e_X (scaled fp16 pairs, common.cuh):
+//   D = 2^-(eA+eB) (A_hi.B_hi + A_hi.B_lo + A_lo.B_hi)    (3 tcgen05.mma kind::f16)
 //
 // Operands are the split buffers of internal.h (row-major, leading dim ld), each
 // either K-major (K contiguous) or MN-major (M/N contiguous); both are native
-// tcgen05 operand majors for tf32, so no transposed copies exist anywhere.
+// tcgen05 operand majors for 16-bit types, so no transposed copies exist anywhere.
 //
-// One CTA = one 128 x BN output tile (BN = 128 or 256), 8 warps:
+// Two K segments (A1.B1 + A2.B2, e.g. the JVP's [A | da][V; W]) carry different
+// product exponents S = eA + eB.  They share one TMEM accumulator: the segment
+// with the larger S runs first and the first MMA of the second segment rescales
+// the partial sum by 2^-(S1-S2) through tcgen05.mma's scale-input-d operand
+// (plus zero-operand MMAs for shifts beyond 15), so the accumulator always holds
+// 2^S_last * D exactly as if both products had been formed at the smaller scale.
+//
+// One CTA = one 128 x BN output tile (BN = 32, 128 or 256), 10 warps:
 //   warp 0 lane 0 : TMA producer      (cp.async.bulk.tensor.2d, SWIZZLE_128B)
-//   warp 1 lane 0 : MMA issuer        (tcgen05.mma.cta_group::1.kind::tf32)
-//   warps 0-7     : epilogue          (tcgen05.ld 32x32b -> registers -> 128-bit fused epilogue)
-// smem ring of STAGES x {A_hi, A_lo, B_hi, B_lo} 32-wide K slabs, full/empty
+//   warp 1 lane 0 : MMA issuer        (tcgen05.mma.cta_group::1.kind::f16)
+//   warps 2-9     : epilogue          (tcgen05.ld 32x32b -> registers -> 128-bit fused epilogue)
+// smem ring of STAGES x {A_hi, A_lo, B_hi, B_lo} 64-deep K slabs, full/empty
 // mbarriers between TMA and MMA, tcgen05.commit frees a slab / signals the epilogue.
-// Split-K (grid.z) writes fp32 partials that a fixed-order reduction folds in.
+// Split-K writes fp32 partials (already unscaled) that a fixed-order reduction folds in.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -29,7 +36,8 @@
 namespace cv {
 
 constexpr int TC_BM = 128;
-constexpr int TC_BK = 32;  // fp32 elements = 128 bytes = one SWIZZLE_128B row
+constexpr int TC_BK = 64;                   // fp16 elements = 128 bytes = one SWIZZLE_128B row
+constexpr int TC_ZERO_BYTES = TC_BM * 128;  // all-zero K-major A tile for pure rescaling MMAs
 
 struct TcOperand {
   int kmajor;   // 1: K contiguous, 0: M/N contiguous
@@ -38,6 +46,8 @@ struct TcOperand {
 struct TcArgs {
   int M, N;
   int nseg;
+  const Scale* asc[2];
+  const Scale* bsc[2];
   int kb[2];          // k-blocks per segment
   int kb_total;
   int kb_per_split;
@@ -72,6 +82,10 @@ CV_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+CV_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 CV_DEV void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
@@ -84,36 +98,107 @@ CV_DEV void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
 
-// UMMA shared-memory descriptor, version 1 (sm_100).  layout: 2 = SWIZZLE_128B
-// (K-major: 16 B granules, 8-row atoms), 1 = SWIZZLE_128B_BASE32B (the only
-// MN-major layout for 32-bit operands: 32 B granules, 4-row atoms).
+// UMMA shared-memory descriptor, version 1 (sm_100), layout 2 = SWIZZLE_128B.
 CV_DEV uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
   d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;   // version
+  d |= (uint64_t)1 << 46;  // version
   d |= (uint64_t)layout << 61;
   return d;
 }
 
-// Instruction descriptor: kind::tf32, D f32, A/B tf32, majors, N, M.
-__host__ __device__ constexpr uint32_t tf32_idesc(int M, int N, int a_mn, int b_mn) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
-         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+// Operand slab descriptors for k-step kk (16 K-elements) of a 64-deep slab:
+//   K-major : rows of 128 B (64 fp16), 8-row atoms (SBO 1024), k-step = +32 B in the row.
+//   MN-major: 64-wide MN chunks of 64 K-rows x 128 B each (LBO 8192 between chunks),
+//             8-row K groups (SBO 1024), k-step = 16 K-rows = +2048 B.
+CV_DEV uint64_t op_desc(uint32_t base, int mn, int kk) {
+  return mn ? umma_desc(base + kk * 2048, 8192, 1024, 2) : umma_desc(base + kk * 32, 16, 1024, 2);
 }
 
-CV_DEV void umma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accum) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+// Instruction descriptor: kind::f16, D f32, A/B f16, majors, N, M.
+__host__ __device__ constexpr uint32_t f16_idesc(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
 }
 
+// D = A.B + (accum ? D : 0)
+template <int CG>
+CV_DEV void umma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accum) {
+  if constexpr (CG == 1)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accum));
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+
+// D = A.B + D * 2^-SH   (scale-input-d, immediate 1..15)
+template <int CG, int SH>
+CV_DEV void umma_f16_sh(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc) {
+  if constexpr (CG == 1)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p, %4;\n}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "n"(SH));
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p, %4;\n}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "n"(SH));
+}
+
+template <int CG>
+CV_DEV void umma_f16_shift(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, int sh) {
+  switch (sh) {
+#define CV_SH(k) \
+  case k:        \
+    umma_f16_sh<CG, k>(tmem_d, a, b, idesc); \
+    break;
+    CV_SH(1) CV_SH(2) CV_SH(3) CV_SH(4) CV_SH(5) CV_SH(6) CV_SH(7) CV_SH(8)
+    CV_SH(9) CV_SH(10) CV_SH(11) CV_SH(12) CV_SH(13) CV_SH(14) CV_SH(15)
+#undef CV_SH
+    default:
+      umma_f16<CG>(tmem_d, a, b, idesc, 1u);
+      break;
+  }
+}
+
+// The 3 products of one 16-deep k-step; shift > 0 first rescales the running sum.
+template <int CG>
+CV_DEV void umma_kstep(uint32_t dtm, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl, uint64_t zero_a,
+                       uint32_t idesc, bool accum, int shift) {
+  if (accum && shift > 0) {
+    while (shift > 15) {  // D <- 0.B + D 2^-15
+      umma_f16_shift<CG>(dtm, zero_a, bh, idesc, 15);
+      shift -= 15;
+    }
+    umma_f16_shift<CG>(dtm, ah, bh, idesc, shift);
+  } else {
+    umma_f16<CG>(dtm, ah, bh, idesc, accum ? 1u : 0u);
+  }
+  umma_f16<CG>(dtm, ah, bl, idesc, 1u);
+  umma_f16<CG>(dtm, al, bh, idesc, 1u);
+}
+
+template <int CG>
 CV_DEV void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
+  if constexpr (CG == 1) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+  } else {
+    const uint16_t mask = 3;
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+  }
 }
 
 CV_DEV void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
@@ -129,8 +214,85 @@ CV_DEV void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// product exponents and processing order of the K segments (larger S first)
+struct SegPlan {
+  int S[2];
+  float inv_a[2], inv_b[2];
+  int ord;
+};
+
+CV_DEV SegPlan seg_plan(const TcArgs& a) {
+  SegPlan p;
+  for (int s = 0; s < 2; ++s) {
+    const int ea = s < a.nseg ? a.asc[s]->e : 0, eb = s < a.nseg ? a.bsc[s]->e : 0;
+    p.S[s] = ea + eb;
+    p.inv_a[s] = pow2f(-ea);
+    p.inv_b[s] = pow2f(-eb);
+  }
+  p.ord = (a.nseg > 1 && p.S[1] > p.S[0]) ? 1 : 0;
+  return p;
+}
+
+// virtual k-block v (processing order) -> segment, and the k-block within it
+CV_DEV int vseg(const TcArgs& a, const SegPlan& p, int v, int& lkb) {
+  const int n0 = a.kb[p.ord];
+  if (v < n0) {
+    lkb = v;
+    return p.ord;
+  }
+  lkb = v - n0;
+  return 1 - p.ord;
+}
+
+// zero the rescaling tile (all threads), visible to the tensor core's async proxy
+CV_DEV void zero_tile_init(uint8_t* z) {
+  for (int i = threadIdx.x; i < TC_ZERO_BYTES / 16; i += blockDim.x) reinterpret_cast<uint4*>(z)[i] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// The epilogue of one accumulator tile (TMEM -> registers -> fused epilogue), run by
+// 8 warps: warp w reads TMEM lane quadrant (w % 4), half = column half.
+template <int BN>
+CV_DEV void tile_epilogue(const TcArgs& a, const EpiRt& rt, uint32_t tacc, int m_base, int n0, int split, float inv,
+                          int q, int half, int lane) {
+  const int m = m_base + q * 32 + lane;
+  const uint32_t trow = tacc + ((uint32_t)(q * 32) << 16);
+  constexpr int NCH = BN / 32;
+  constexpr int C0 = NCH >= 2 ? NCH / 2 : 1;
+  float amax = 0.f, ramax = 0.f;
+#pragma unroll 1
+  for (int c = half * C0; c < (NCH >= 2 ? (half + 1) * C0 : (half == 0 ? 1 : 0)); ++c) {
+    uint32_t r[32];
+    tmem_ld32(trow + c * 32, r);
+    if (m >= a.M) continue;
+    const int nb = n0 + c * 32;
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * inv;
+    const bool full_chunk = nb + 32 <= a.N && (!a.lower_only || nb + 31 <= m);
+    if (a.partial) {
+      float* dst = a.partial + ((int64_t)split * a.M + m) * a.N + nb;
+      if (full_chunk && al16(dst)) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (nb + j < a.N) dst[j] = v[j];
+      }
+    } else if (!(full_chunk && epi_applyV<32>(a.epi, rt, m, nb, v, amax, ramax))) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int n = nb + j;
+        if (n < a.N && (!a.lower_only || n <= m)) epi_apply(a.epi, rt, m, n, v[j], amax, ramax);
+      }
+    }
+  }
+  if (!a.partial) epi_flush_amax(a.epi, amax, ramax);
+}
+
 // ---------------------------------------------------------------------------
-// Kernel
+// Kernel (1-CTA)
 // ---------------------------------------------------------------------------
 struct TcMaps {
   CUtensorMap m[2][4];  // [seg][A_hi, A_lo, B_hi, B_lo]
@@ -138,28 +300,34 @@ struct TcMaps {
 
 template <int BN, int STAGES>
 struct TcCfg {
-  static constexpr int A_BYTES = TC_BM * TC_BK * 4;  // 16 KB
-  static constexpr int B_BYTES = BN * TC_BK * 4;     // 16 / 32 KB
+  static constexpr int A_BYTES = TC_BM * TC_BK * 2;  // 16 KB
+  static constexpr int B_BYTES = BN * TC_BK * 2;     // 4 / 16 / 32 KB
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-  static constexpr int TMEM_COLS = 2 * BN;           // double-buffered accumulator
-  static constexpr int THREADS = 320;                // w0 TMA, w1 MMA, w2..w9 epilogue
+  static constexpr int SMEM = STAGES * STAGE_BYTES + TC_ZERO_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered accumulator
+  static constexpr int THREADS = 320;                          // w0 TMA, w1 MMA, w2..w9 epilogue
 };
-
-CV_DEV void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
 // work item -> (m0, n0, first k-block, k-blocks); split index slowest so that
 // co-resident CTAs share K ranges (and therefore L2-resident operand panels)
-CV_DEV bool tc_work(const TcArgs& a, int w, int bn, int& m0, int& n0, int& kb0, int& nkb) {
+CV_DEV bool tc_work(const TcArgs& a, int w, int bm, int bn, int& m0, int& n0, int& kb0, int& nkb) {
   const int tiles = a.tiles_m * a.tiles_n;
   const int split = w / tiles, t = w % tiles;
-  m0 = (t / a.tiles_n) * TC_BM;
+  m0 = (t / a.tiles_n) * bm;
   n0 = (t % a.tiles_n) * bn;
   kb0 = split * a.kb_per_split;
   nkb = min(a.kb_total, kb0 + a.kb_per_split) - kb0;
-  return !(a.lower_only && n0 > m0 + TC_BM - 1);
+  return !(a.lower_only && n0 > m0 + bm - 1);
+}
+
+// TMA of one operand slab: K-major = one box {64 K, rows}; MN-major = rows/64 boxes
+// {64 MN, 64 K} of 8 KB each.
+CV_DEV void load_slab(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, bool kmajor, int k0, int r0, int rows) {
+  if (kmajor) {
+    tma_load_2d(dst, map, bar, k0, r0);
+  } else {
+    for (int j = 0; j < rows / 64; ++j) tma_load_2d(dst + j * 8192, map, bar, r0 + 64 * j, k0);
+  }
 }
 
 // Persistent: grid = min(work, SMs); each CTA loops over work items.  The TMEM
@@ -171,7 +339,8 @@ __global__ void __launch_bounds__(320, 1) k_gemm_tc(const __grid_constant__ TcMa
   if (skip_if(a.skip)) return;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = (uint64_t*)(smem + STAGES * Cfg::STAGE_BYTES);
+  uint8_t* zero = smem + STAGES * Cfg::STAGE_BYTES;
+  uint64_t* full = (uint64_t*)(zero + TC_ZERO_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -179,6 +348,7 @@ __global__ void __launch_bounds__(320, 1) k_gemm_tc(const __grid_constant__ TcMa
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = a.tiles_m * a.tiles_n * a.splits;
+  zero_tile_init(zero);
   if (warp == 0) {
     if (lane == 0) {
       for (int s = 0; s < STAGES; ++s) {
@@ -202,127 +372,79 @@ __global__ void __launch_bounds__(320, 1) k_gemm_tc(const __grid_constant__ TcMa
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  const SegPlan plan = seg_plan(a);
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer ----------------
     int it = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
       int m0, n0, kb0, nkb;
-      if (!tc_work(a, w, BN, m0, n0, kb0, nkb)) continue;
+      if (!tc_work(a, w, TC_BM, BN, m0, n0, kb0, nkb)) continue;
       for (int i = 0; i < nkb; ++i, ++it) {
         const int s = it % STAGES;
         if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
-        const int kb = kb0 + i;
-        const int sg = kb < a.kb[0] ? 0 : 1;
-        const int k0 = (sg == 0 ? kb : kb - a.kb[0]) * TC_BK;
+        int lkb;
+        const int sg = vseg(a, plan, kb0 + i, lkb);
+        const int k0 = lkb * TC_BK;
         uint8_t* st = smem + s * Cfg::STAGE_BYTES;
         mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
         for (int h = 0; h < 2; ++h) {  // hi, lo
-          uint8_t* sa = st + h * Cfg::A_BYTES;
-          if (a.a[sg].kmajor) {
-            tma_load_2d(sa, &maps.m[sg][h], &full[s], k0, m0);
-          } else {
-#pragma unroll
-            for (int j = 0; j < TC_BM / 32; ++j) tma_load_2d(sa + j * 4096, &maps.m[sg][h], &full[s], m0 + 32 * j, k0);
-          }
-          uint8_t* sb = st + 2 * Cfg::A_BYTES + h * Cfg::B_BYTES;
-          if (a.b[sg].kmajor) {
-            tma_load_2d(sb, &maps.m[sg][2 + h], &full[s], k0, n0);
-          } else {
-#pragma unroll
-            for (int j = 0; j < BN / 32; ++j)
-              tma_load_2d(sb + j * 4096, &maps.m[sg][2 + h], &full[s], n0 + 32 * j, k0);
-          }
+          load_slab(st + h * Cfg::A_BYTES, &maps.m[sg][h], &full[s], a.a[sg].kmajor, k0, m0, TC_BM);
+          load_slab(st + 2 * Cfg::A_BYTES + h * Cfg::B_BYTES, &maps.m[sg][2 + h], &full[s], a.b[sg].kmajor, k0, n0,
+                    BN);
         }
       }
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ----------------
     int it = 0, acc_i = 0;
+    const uint64_t zdesc = op_desc(smem_u32(zero), 0, 0);
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
       int m0, n0, kb0, nkb;
-      if (!tc_work(a, w, BN, m0, n0, kb0, nkb)) continue;
+      if (!tc_work(a, w, TC_BM, BN, m0, n0, kb0, nkb)) continue;
       const int ab = acc_i & 1;
       if (acc_i >= 2) mbar_wait(&tempty[ab], ((acc_i >> 1) - 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t dtm = tmem + ab * BN;
+      int prev = -1;
       for (int i = 0; i < nkb; ++i, ++it) {
         const int s = it % STAGES;
         mbar_wait(&full[s], (it / STAGES) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int kb = kb0 + i;
-        const int sg = kb < a.kb[0] ? 0 : 1;
+        int lkb;
+        const int sg = vseg(a, plan, kb0 + i, lkb);
+        const int shift = (prev >= 0 && prev != sg) ? plan.S[prev] - plan.S[sg] : 0;
+        prev = sg;
         const int amn = a.a[sg].kmajor ? 0 : 1, bmn = a.b[sg].kmajor ? 0 : 1;
-        const uint32_t idesc = tf32_idesc(TC_BM, BN, amn, bmn);
+        const uint32_t idesc = f16_idesc(TC_BM, BN, amn, bmn);
         const uint32_t st = smem_u32(smem + s * Cfg::STAGE_BYTES);
         const uint32_t a_hi = st, a_lo = st + Cfg::A_BYTES;
         const uint32_t b_hi = st + 2 * Cfg::A_BYTES, b_lo = b_hi + Cfg::B_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < TC_BK / 8; ++kk) {
-          // K-major (SW128): rows of 128 B, 8-row atoms (SBO 1024), k-step = +32 B in the row.
-          // MN-major (SW128_BASE32B): 32-wide MN chunks 4 KB apart (LBO), K rows of 128 B in
-          // 4-row atoms (SBO 512), k-step = 8 rows = +1024 B.
-          const uint32_t aoff = amn ? kk * 1024 : kk * 32;
-          const uint32_t boff = bmn ? kk * 1024 : kk * 32;
-          const uint32_t albo = amn ? 4096 : 16, blbo = bmn ? 4096 : 16;
-          const uint32_t asbo = amn ? 512 : 1024, bsbo = bmn ? 512 : 1024;
-          const uint32_t alay = amn ? 1 : 2, blay = bmn ? 1 : 2;
-          const uint64_t dah = umma_desc(a_hi + aoff, albo, asbo, alay), dal = umma_desc(a_lo + aoff, albo, asbo, alay);
-          const uint64_t dbh = umma_desc(b_hi + boff, blbo, bsbo, blay), dbl = umma_desc(b_lo + boff, blbo, bsbo, blay);
-          const uint32_t acc0 = (i > 0 || kk > 0) ? 1u : 0u;
-          umma_tf32(dtm, dah, dbh, idesc, acc0);
-          umma_tf32(dtm, dah, dbl, idesc, 1u);
-          umma_tf32(dtm, dal, dbh, idesc, 1u);
-        }
-        umma_commit(&empty[s]);  // slab free once these MMAs retire
+        for (int kk = 0; kk < TC_BK / 16; ++kk)
+          umma_kstep<1>(dtm, op_desc(a_hi, amn, kk), op_desc(a_lo, amn, kk), op_desc(b_hi, bmn, kk),
+                        op_desc(b_lo, bmn, kk), zdesc, idesc, i > 0 || kk > 0, kk == 0 ? shift : 0);
+        umma_commit<1>(&empty[s]);  // slab free once these MMAs retire
       }
-      umma_commit(&tfull[ab]);   // accumulator ready for the epilogue
+      umma_commit<1>(&tfull[ab]);   // accumulator ready for the epilogue
       ++acc_i;
     }
   } else if (warp >= 2) {
-    // ---------------- epilogue: TMEM -> registers -> fused epilogue ----------------
-    // warp w reads TMEM lane quadrant (w % 4); warps 2-5 take the first column half,
-    // warps 6-9 the second.
+    // ---------------- epilogue ----------------
     const int q = warp & 3, half = (warp - 2) >> 2;
+    const EpiRt rt = epi_prepare(a.epi);
+    if (blockIdx.x == 0 && warp == 2 && lane == 0 && !a.partial) epi_publish(a.epi, rt);
     int acc_i = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
       int m0, n0, kb0, nkb;
-      if (!tc_work(a, w, BN, m0, n0, kb0, nkb)) continue;
+      if (!tc_work(a, w, TC_BM, BN, m0, n0, kb0, nkb)) continue;
       const int ab = acc_i & 1;
       mbar_wait(&tfull[ab], (acc_i >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int m = m0 + q * 32 + lane;
-      const int split = w / (a.tiles_m * a.tiles_n);
-      const uint32_t trow = tmem + ab * BN + ((uint32_t)(q * 32) << 16);
-#pragma unroll 1
-      for (int c = half; c < BN / 32; c += 2) {
-        uint32_t r[32];
-        tmem_ld32(trow + c * 32, r);
-        if (m >= a.M) continue;
-        const int nb = n0 + c * 32;
-        float v[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        const bool full_chunk = nb + 32 <= a.N && (!a.lower_only || nb + 31 <= m);
-        if (a.partial) {
-          float* dst = a.partial + ((int64_t)split * a.M + m) * a.N + nb;
-          if (full_chunk && al16(dst)) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (nb + j < a.N) dst[j] = v[j];
-          }
-        } else if (!(full_chunk && epi_apply32(a.epi, m, nb, v))) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int n = nb + j;
-            if (n < a.N && (!a.lower_only || n <= m)) epi_apply(a.epi, m, n, v[j]);
-          }
-        }
-      }
+      int lkb;
+      const int last = vseg(a, plan, kb0 + nkb - 1, lkb);
+      const float inv = plan.inv_a[last] * plan.inv_b[last];
+      tile_epilogue<BN>(a, rt, tmem + ab * BN, m0, n0, w / (a.tiles_m * a.tiles_n), inv, q, half, lane);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[ab]);
@@ -341,30 +463,36 @@ __global__ void __launch_bounds__(320, 1) k_gemm_tc(const __grid_constant__ TcMa
 __global__ void k_splitk_reduce(const float* partial, int splits, int M, int N, Epilogue epi, const int* skip,
                                 int lower_only) {
   if (skip_if(skip)) return;
+  const EpiRt rt = epi_prepare(epi);
+  if (blockIdx.x == 0 && threadIdx.x == 0) epi_publish(epi, rt);
   const int64_t total = (int64_t)M * N;
-  if ((N & 3) == 0 && !lower_only) {
-    // 4 adjacent columns per thread: 128-bit partial loads, vectorized epilogue
-    const int64_t quads = total >> 2;
-    for (int64_t qd = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; qd < quads;
-         qd += (int64_t)gridDim.x * blockDim.x) {
-      float4 s = *reinterpret_cast<const float4*>(partial + 4 * qd);
+  float amax = 0.f, ramax = 0.f;
+  if ((N & 7) == 0 && !lower_only) {
+    // 8 adjacent columns per thread: 128-bit partial loads, vectorized epilogue
+    const int64_t oct = total >> 3;
+    for (int64_t qd = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; qd < oct; qd += (int64_t)gridDim.x * blockDim.x) {
+      float v[8];
+      const float4 p0 = *reinterpret_cast<const float4*>(partial + 8 * qd);
+      const float4 p1 = *reinterpret_cast<const float4*>(partial + 8 * qd + 4);
+      v[0] = p0.x; v[1] = p0.y; v[2] = p0.z; v[3] = p0.w; v[4] = p1.x; v[5] = p1.y; v[6] = p1.z; v[7] = p1.w;
       for (int z = 1; z < splits; ++z) {
-        const float4 p = *reinterpret_cast<const float4*>(partial + (int64_t)z * total + 4 * qd);
-        s.x += p.x; s.y += p.y; s.z += p.z; s.w += p.w;
+        const float4 a0 = *reinterpret_cast<const float4*>(partial + (int64_t)z * total + 8 * qd);
+        const float4 a1 = *reinterpret_cast<const float4*>(partial + (int64_t)z * total + 8 * qd + 4);
+        v[0] += a0.x; v[1] += a0.y; v[2] += a0.z; v[3] += a0.w; v[4] += a1.x; v[5] += a1.y; v[6] += a1.z; v[7] += a1.w;
       }
-      const int m = (int)((4 * qd) / N), n = (int)((4 * qd) % N);
-      const float v[4] = {s.x, s.y, s.z, s.w};
-      if (!epi_applyV<4>(epi, m, n, v))
-        for (int t = 0; t < 4; ++t) epi_apply(epi, m, n + t, v[t]);
+      const int m = (int)((8 * qd) / N), n = (int)((8 * qd) % N);
+      if (!epi_applyV<8>(epi, rt, m, n, v, amax, ramax))
+        for (int t = 0; t < 8; ++t) epi_apply(epi, rt, m, n + t, v[t], amax, ramax);
     }
-    return;
+  } else {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+      float s = 0.f;
+      for (int z = 0; z < splits; ++z) s += partial[(int64_t)z * total + i];
+      const int m = (int)(i / N), n = (int)(i % N);
+      if (!lower_only || n <= m) epi_apply(epi, rt, m, n, s, amax, ramax);
+    }
   }
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int z = 0; z < splits; ++z) s += partial[(int64_t)z * total + i];
-    const int m = (int)(i / N), n = (int)(i % N);
-    if (!lower_only || n <= m) epi_apply(epi, m, n, s);
-  }
+  epi_flush_amax(epi, amax, ramax);
 }
 
 // ---------------------------------------------------------------------------
@@ -386,10 +514,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 struct MapKey {
   const void* ptr;
   int64_t inner, outer, ld;
-  int box0, box1, mn;
+  int box0, box1;
   bool operator==(const MapKey& o) const {
-    return ptr == o.ptr && inner == o.inner && outer == o.outer && ld == o.ld && box0 == o.box0 && box1 == o.box1 &&
-           mn == o.mn;
+    return ptr == o.ptr && inner == o.inner && outer == o.outer && ld == o.ld && box0 == o.box0 && box1 == o.box1;
   }
 };
 struct MapKeyHash {
@@ -398,18 +525,17 @@ struct MapKeyHash {
     h = h * 1000003u ^ (size_t)k.inner;
     h = h * 1000003u ^ (size_t)k.outer;
     h = h * 1000003u ^ (size_t)k.ld;
-    h = h * 1000003u ^ (size_t)(k.box0 * 4096 + k.box1 * 2 + k.mn);
+    h = h * 1000003u ^ (size_t)(k.box0 * 4096 + k.box1);
     return h;
   }
 };
 
-// 2D fp32 map: dims {inner, outer}, row stride ld elements, OOB zero fill; K-major
-// operands use SWIZZLE_128B, MN-major ones SWIZZLE_128B_ATOM_32B (UMMA BASE32B).
-static CUtensorMap make_map(const float* ptr, int64_t inner, int64_t outer, int64_t ld, int box0, int box1,
-                            int mn) {
+// 2D fp16 map: dims {inner, outer}, row stride ld elements, OOB zero fill, SWIZZLE_128B
+// (the inner box extent is always 64 elements = 128 B).
+static CUtensorMap make_map(const __half* ptr, int64_t inner, int64_t outer, int64_t ld, int box0, int box1) {
   static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
   static std::mutex mu;
-  MapKey key{ptr, inner, outer, ld, box0, box1, mn};
+  MapKey key{ptr, inner, outer, ld, box0, box1};
   {
     std::lock_guard<std::mutex> g(mu);
     auto it = cache.find(key);
@@ -419,12 +545,11 @@ static CUtensorMap make_map(const float* ptr, int64_t inner, int64_t outer, int6
   if (!fn) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
   CUtensorMap m;
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
   cuuint32_t box[2] = {(cuuint32_t)box0, (cuuint32_t)box1};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)ptr, dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, mn ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (void*)ptr, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   std::lock_guard<std::mutex> g(mu);
@@ -437,19 +562,55 @@ static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
 // Operand majors: A(m,k) = p[m*si + k*sj]; K-major iff sj == 1.
 static bool op_ok(const Operand& o) {
-  if (!o.hi || !o.lo) return false;
+  if (o.f32 || !o.hi || !o.lo || !o.sc) return false;
   if (!aligned16(o.hi) || !aligned16(o.lo)) return false;
   const int64_t ld = o.sj == 1 ? o.si : (o.si == 1 ? o.sj : -1);
-  return ld > 0 && (ld % 4) == 0 && (o.sj == 1 || o.si == 1);
+  return ld > 0 && (ld % 8) == 0 && (o.sj == 1 || o.si == 1);
 }
 
 bool gemm_tc_supported(const GemmArgs& g) {
   if (g.M < 64 || g.N < 8) return false;
   for (int s = 0; s < g.nseg; ++s) {
-    if (g.seg[s].K < 8) return false;
+    if (g.seg[s].K < 16) return false;
     if (!op_ok(g.seg[s].A) || !op_ok(g.seg[s].B)) return false;
+    // MN-major operands are staged in 64-wide chunks: the narrow (N <= 32) tile
+    // takes K-major B only
+    if (g.N <= 32 && g.seg[s].B.si != 1) return false;
   }
   return true;
+}
+
+// Tensor maps and segment geometry shared by the 1-CTA and 2-CTA launchers.
+// A rows per CTA = TC_BM; B box rows = bbox (BN, or BN/2 for the CTA pair).
+static void fill_args(const GemmArgs& g, int bbox, TcMaps& maps, TcArgs& a) {
+  a.M = g.M;
+  a.N = g.N;
+  a.nseg = g.nseg;
+  a.kb_total = 0;
+  for (int s = 0; s < 2; ++s) {
+    a.asc[s] = s < g.nseg ? g.seg[s].A.sc : nullptr;
+    a.bsc[s] = s < g.nseg ? g.seg[s].B.sc : nullptr;
+  }
+  for (int s = 0; s < g.nseg; ++s) {
+    const GemmSeg& sg = g.seg[s];
+    const bool akm = sg.A.sj == 1, bkm = sg.B.si == 1;  // B(k,n) = p[k*si + n*sj]: K-major iff si == 1
+    a.a[s].kmajor = akm;
+    a.b[s].kmajor = bkm;
+    a.kb[s] = (sg.K + TC_BK - 1) / TC_BK;
+    a.kb_total += a.kb[s];
+    const int64_t lda = akm ? sg.A.si : sg.A.sj;
+    const int64_t ldb = bkm ? sg.B.sj : sg.B.si;
+    for (int h = 0; h < 2; ++h) {
+      const __half* pa = h ? sg.A.lo : sg.A.hi;
+      const __half* pb = h ? sg.B.lo : sg.B.hi;
+      maps.m[s][h] = akm ? make_map(pa, sg.K, g.M, lda, TC_BK, TC_BM) : make_map(pa, g.M, sg.K, lda, 64, TC_BK);
+      maps.m[s][2 + h] = bkm ? make_map(pb, sg.K, g.N, ldb, TC_BK, bbox) : make_map(pb, g.N, sg.K, ldb, 64, TC_BK);
+    }
+  }
+  if (g.nseg < 2) a.kb[1] = 0;
+  a.epi = g.epi;
+  a.skip = g.skip;
+  a.lower_only = g.lower_only;
 }
 
 template <int BN, int STAGES>
@@ -462,30 +623,7 @@ static int launch_tc(cv_ctx* ctx, const GemmArgs& g, int splits, float* ext_part
   }
   TcMaps maps;
   TcArgs a{};
-  a.M = g.M;
-  a.N = g.N;
-  a.nseg = g.nseg;
-  a.kb_total = 0;
-  for (int s = 0; s < g.nseg; ++s) {
-    const GemmSeg& sg = g.seg[s];
-    const bool akm = sg.A.sj == 1, bkm = sg.B.si == 1;  // B(k,n) = p[k*si + n*sj]: K-major iff si == 1
-    a.a[s].kmajor = akm;
-    a.b[s].kmajor = bkm;
-    a.kb[s] = (sg.K + TC_BK - 1) / TC_BK;
-    a.kb_total += a.kb[s];
-    const int64_t lda = akm ? sg.A.si : sg.A.sj;
-    const int64_t ldb = bkm ? sg.B.sj : sg.B.si;
-    for (int h = 0; h < 2; ++h) {
-      const float* pa = h ? sg.A.lo : sg.A.hi;
-      const float* pb = h ? sg.B.lo : sg.B.hi;
-      maps.m[s][h] = akm ? make_map(pa, sg.K, g.M, lda, TC_BK, TC_BM, 0) : make_map(pa, g.M, sg.K, lda, 32, TC_BK, 1);
-      maps.m[s][2 + h] = bkm ? make_map(pb, sg.K, g.N, ldb, TC_BK, BN, 0) : make_map(pb, g.N, sg.K, ldb, 32, TC_BK, 1);
-    }
-  }
-  if (g.nseg < 2) a.kb[1] = 0;
-  a.epi = g.epi;
-  a.skip = g.skip;
-  a.lower_only = g.lower_only;
+  fill_args(g, BN, maps, a);
   a.kb_per_split = (a.kb_total + splits - 1) / splits;
   splits = (a.kb_total + a.kb_per_split - 1) / a.kb_per_split;
   a.splits = splits;

@@ -1,6 +1,7 @@
 // Internal (non-ABI) structures of curvopt_b200.
 #pragma once
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 #include <map>
@@ -11,13 +12,18 @@
 
 namespace cv {
 
+struct Scale;  // common.cuh: {int e; float amax;}
+
 // ---------------------------------------------------------------------------
-// Logical operand views.  X(i, j) = hi[i*si + j*sj] + lo[i*si + j*sj].
+// Logical operand views.  X(i, j) = (hi[i*si + j*sj] + lo[i*si + j*sj]) * 2^-sc->e
+// (scaled fp16 split, common.cuh), or plain fp32 f32[i*si + j*sj] (SIMT only).
 // ---------------------------------------------------------------------------
 struct Operand {
-  const float* hi = nullptr;
-  const float* lo = nullptr;
+  const __half* hi = nullptr;
+  const __half* lo = nullptr;
   int64_t si = 0, sj = 0;
+  const Scale* sc = nullptr;
+  const float* f32 = nullptr;   // plain fp32 operand (hi/lo unused)
 };
 
 struct GemmSeg {
@@ -35,22 +41,38 @@ enum EpiMode : int {
   EPI_ACCUM = 5,       // out += alpha * acc                      (Cholesky trailing update)
 };
 
+// Rigorous bound on |accumulator| used to pick a split output's exponent:
+// sum_t k[t] * (*x[t]) * (*y[t]), the x / y being amax slots of the inputs.
+struct AccBound {
+  int n = 0;
+  float k[4] = {0.f, 0.f, 0.f, 0.f};
+  const float* x[4] = {nullptr, nullptr, nullptr, nullptr};
+  const float* y[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+
 struct Epilogue {
   int mode = EPI_STORE;
   int act = 0;                   // CV_ACT_*
-  float* out = nullptr;          // fp32 output (EPI_STORE)
-  float* out_hi = nullptr;       // split outputs
-  float* out_lo = nullptr;
+  float* out = nullptr;          // fp32 output (EPI_STORE / GRAM / ACCUM)
+  __half* out_hi = nullptr;      // split outputs
+  __half* out_lo = nullptr;
+  Scale* out_sc = nullptr;       // exponent written by the producer, amax accumulated
+  int out_unit = 0;              // the output carries a ones column: its scale covers 1.0
+  AccBound bound;                // bound on |acc| (split outputs)
   int64_t ld = 0;
-  const float* mask_hi = nullptr;  // stored activation a (hi/lo) at [m, n] for act'
-  const float* mask_lo = nullptr;
+  const __half* mask_hi = nullptr;  // stored activation a (split) at [m, n] for act'
+  const __half* mask_lo = nullptr;
+  const Scale* mask_sc = nullptr;
   int64_t mask_ld = 0;
   float* raw = nullptr;          // optional: pre-mask value (fp32), ld raw_ld
   int64_t raw_ld = 0;
+  float* raw_amax = nullptr;     // optional: max |raw|
   const float* P = nullptr;      // EPI_HVP tanh: pre-mask G W^T from linearize
   int64_t P_ld = 0;
+  const float* P_amax = nullptr;
   const float* dz = nullptr;     // EPI_HVP tanh: pre-mask tangent from the JVP
   int64_t dz_ld = 0;
+  const float* dz_amax = nullptr;
   int mask_div = 1;              // mask row = m / mask_div (row lane: k rows per example)
   const float* sa = nullptr;     // EPI_GRAM: b x b activation Gram, ld sa_ld
   int64_t sa_ld = 0;
@@ -69,9 +91,10 @@ struct GemmArgs {
 };
 
 struct SplitBuf {
-  float* hi = nullptr;
-  float* lo = nullptr;
+  __half* hi = nullptr;
+  __half* lo = nullptr;
   int64_t ld = 0;
+  Scale* sc = nullptr;
 };
 
 // Caching device allocator: exact-size free lists, never returns memory to the
@@ -100,6 +123,8 @@ struct cv_ctx {
   void* nccl = nullptr;          // ncclComm_t
   double* red_ws = nullptr;      // reduction partials: kRedBlocks * 8 doubles
   double* scal_ws = nullptr;     // scratch scalars (64 doubles)
+  float* amax_ws = nullptr;      // split.cu: per-block maxima (2 x 148 x 16 floats)
+  unsigned* amax_counter = nullptr;  // split.cu: last-block counter (returns to 0 after each pass)
   int64_t launches = 0;
 };
 
@@ -112,9 +137,22 @@ struct cv_snap {
   int act = 0, loss = 0;
   int bl = 0, bg = 0;             // local / global batch
   int c = 0;
+  // Scale slots (device, one array; common.cuh).  Linearization slots are zeroed
+  // by cv_linearize, the per-product block [prod_sc, prod_sc + n_prod) by the
+  // split of every product input.
+  cv::Scale* scales = nullptr;
+  int n_scales = 0;
+  cv::Scale* w_sc = nullptr;      // [L] linearization weights, per layer block
+  cv::Scale* v_sc = nullptr;      // [L] product input, per layer block
+  cv::Scale* gout_sc = nullptr;   // G[L-1] (fp32 amax) and its split
+  cv::Scale* U_sc = nullptr;      // product cotangent U (fp32 amax) and its split
+  cv::Scale* U2_sc = nullptr;     // U2 amax
+  cv::Scale* prod_sc = nullptr;   // start of the per-product block
+  int n_prod = 0;
+  cv::Scale* scratch_sc = nullptr;  // [8] row lane / tests
   // weights of the linearization point, split, flat layout
-  float* w_hi = nullptr;
-  float* w_lo = nullptr;
+  __half* w_hi = nullptr;
+  __half* w_lo = nullptr;
   // augmented activations: acts[0] = [X | 1], acts[l] = [a_l | 1]; b x ld(n_l)
   std::vector<cv::SplitBuf> acts;
   // loss state
@@ -126,25 +164,29 @@ struct cv_snap {
   // G[l] for hidden layers (l < L-1): b x ld(n_{l+1}); P[l] = G[l+1] W^T pre-mask (tanh)
   std::vector<cv::SplitBuf> G;
   std::vector<float*> P;
+  std::vector<cv::Scale*> P_sc;   // amax of P[l]
   // per-product scratch
-  float* v_hi = nullptr;          // split of the product input (d)
-  float* v_lo = nullptr;
+  __half* v_hi = nullptr;         // split of the product input (d)
+  __half* v_lo = nullptr;
   std::vector<cv::SplitBuf> da;   // tangents of acts[l+1], zero column at n
   std::vector<float*> dz;         // pre-mask tangents (tanh HVP)
+  std::vector<cv::Scale*> dz_sc;  // amax of dz[l]
   std::vector<cv::SplitBuf> gs;   // backward scratch (ping-pong size L-1)
   float* U = nullptr;             // b x c cotangent
-  float* U2 = nullptr;            // b x c (HVP last-layer dz)
+  float* U2 = nullptr;            // b x c (backprojection cotangent)
   float* skinny_ws = nullptr;     // partial sums for skinny weight-gradient kernels
   int64_t skinny_ws_elems = 0;
-  // tensor-core output layer (tc_out): the c-wide operands padded to cp columns
-  // (16-byte rows for TMA), split: last-layer [W; b] (wl), per-product [V; Vb] (vl),
-  // cotangent U and G[L-1] (gout).  cp == c when the SIMT skinny kernels are used.
+  // tensor-core output layer (tc_out): the c-wide operands stored transposed and
+  // padded (c -> cp rows, K contiguous, 16-byte rows) so TMA reads them K-major:
+  // last-layer [W; b]^T (wl, ld ldw), per-product [V; Vb]^T (vl), cotangents U^T and
+  // G[L-1]^T (ld ldb).  cp == c when the SIMT skinny kernels are used.
   int tc_out = 0, cp = 0;
   int tc_dx = 0;  // output-layer backward on tensor cores (default: bandwidth kernel)
-  float* wl_hi = nullptr; float* wl_lo = nullptr;
-  float* vl_hi = nullptr; float* vl_lo = nullptr;
-  float* U_hi = nullptr; float* U_lo = nullptr;
-  float* gout_hi = nullptr; float* gout_lo = nullptr;
+  int64_t ldw = 0, ldb = 0;
+  __half* wl_hi = nullptr; __half* wl_lo = nullptr;
+  __half* vl_hi = nullptr; __half* vl_lo = nullptr;
+  __half* U_hi = nullptr; __half* U_lo = nullptr;
+  __half* gout_hi = nullptr; __half* gout_lo = nullptr;
   // row lane (lazily built)
   float* seeds = nullptr;         // b x c x c  (H_z^{1/2})
   float* pinv = nullptr;          // b x c x c
@@ -173,28 +215,33 @@ void allreduce_f32(cv_ctx* ctx, float* buf, int64_t n);
 void allreduce_f64(cv_ctx* ctx, double* buf, int64_t n);
 void check_launch(cv_ctx* ctx);
 
-// mlp.cu
-void split_vec(cv_ctx* ctx, const float* x, float* hi, float* lo, int64_t n, const int* skip);
+// split.cu: scaled fp16 splits with exact amax (two passes)
+void amax_into(cv_ctx* ctx, const float* x, int64_t n, Scale* slot);  // slot->amax = max|x|
+void split_flat(cv_ctx* ctx, const float* x, int64_t d, const std::vector<int64_t>& off, __half* hi, __half* lo,
+                Scale* sc, Scale* zero_sc, int n_zero, const int* skip);
 void split_rows(cv_ctx* ctx, const float* src, int64_t lds, int rows, int cols, const SplitBuf& dst, int ones);
-void set_ones_col(cv_ctx* ctx, const SplitBuf& b, int rows, int col);
+void split_mat(cv_ctx* ctx, const float* src, int64_t lds, int rows, int cols, __half* hi, __half* lo, int64_t ldd,
+               int trans, Scale* sc, int amax_ready, const int* skip);
 void set_col_value(cv_ctx* ctx, const SplitBuf& b, int rows, int col, float v);
 void gather_rows(cv_ctx* ctx, const SplitBuf& b, int rows, int cols, float* out);  // out = hi + lo
+
+// mlp.cu
 void mlp_linearize(cv_ctx* ctx, cv_snap* s, double* loss_out, float* grad_out);
 void pad_last_weights(cv_ctx* ctx, cv_snap* s);
-void mlp_ggn(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, float* out, const int* skip);
-void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, float* out, const int* skip);
-void mlp_jvp(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, float* out_bc);
+void mlp_ggn(cv_ctx* ctx, cv_snap* s, const float* v, float* out, const int* skip);
+void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* v, float* out, const int* skip);
+void mlp_jvp(cv_ctx* ctx, cv_snap* s, const float* v, float* out_bc);
 void mlp_vjp(cv_ctx* ctx, cv_snap* s, const float* U, float* out);
 void mlp_loss_at(cv_ctx* ctx, cv_snap* s, const float* w, double* loss_out);
 
-using MatvecFn = void (*)(cv_ctx*, cv_snap*, const float*, const float*, float*, const int*);
+using MatvecFn = void (*)(cv_ctx*, cv_snap*, const float*, float*, const int*);
 inline MatvecFn matvec_fn(int kind) { return kind == CV_KIND_HESSIAN ? mlp_hvp : mlp_ggn; }
 
 // vec.cu
 void scale_scalar(cv_ctx* ctx, double* x, double s);
 void cg_solve(cv_ctx* ctx, cv_snap* s, int kind, const float* g, double lam, double tol, int maxiter,
               int stab, const float* precond, double floor, const float* x0, float* x, cv_cg_stats* stats);
-void rademacher(cv_ctx* ctx, uint64_t seed, uint64_t counter, int64_t n, float* out, float* hi, float* lo);
+void rademacher(cv_ctx* ctx, uint64_t seed, uint64_t counter, int64_t n, float* out);
 void hutchinson(cv_ctx* ctx, cv_snap* s, int kind, uint64_t seed, uint64_t counter, int n_probes, float* diag,
                 double* trace);
 void power_iter(cv_ctx* ctx, cv_snap* s, int kind, uint64_t seed, uint64_t counter, int iters, double* eig);

@@ -8,6 +8,10 @@
 //   vjp       [gW;gb]_l = A_l^T G_l                       (models.py:274-285)
 //   hvp       [gW;gb]_l = A_l^T dG + [da_{l-1}|0]^T G_l   (models.py:287-307)
 // so biases never need their own epilogue and the bias gradient is the extra row.
+//
+// Every GEMM operand is a scaled fp16 pair (common.cuh).  Split outputs take their
+// exponent from a bound on |acc| built from the inputs' amax slots (AccBound):
+// for a segment with reduction depth K, |sum_k A_mk B_kn| <= K amax(A) amax(B).
 #include "common.cuh"
 #include "internal.h"
 #include "epilogue.cuh"
@@ -15,55 +19,21 @@
 
 namespace cv {
 
-int64_t ld_for(int n) { return ((int64_t)n + 1 + 3) / 4 * 4; }
-
-// ---------------------------------------------------------------------------
-// elementwise helpers
-// ---------------------------------------------------------------------------
-__global__ void k_split_vec(const float* __restrict__ x, float* __restrict__ hi, float* __restrict__ lo,
-                            int64_t n, const int* skip) {
-  if (skip_if(skip)) return;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    float h, l;
-    split2(x[i], h, l);
-    hi[i] = h;
-    lo[i] = l;
-  }
-}
-
-// dst[r, 0:cols] = split(src[r, 0:cols]); dst[r, cols] = (1, 0) when ones.
-__global__ void k_split_rows(const float* __restrict__ src, int64_t lds, int rows, int cols,
-                             float* __restrict__ hi, float* __restrict__ lo, int64_t ldd, int ones) {
-  const int64_t total = (int64_t)rows * (cols + 1);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / (cols + 1);
-    const int c = (int)(i - r * (cols + 1));
-    if (c == cols) {
-      if (ones) { hi[r * ldd + c] = 1.f; lo[r * ldd + c] = 0.f; }
-      continue;
-    }
-    float h, l;
-    split2(src[r * lds + c], h, l);
-    hi[r * ldd + c] = h;
-    lo[r * ldd + c] = l;
-  }
-}
-
-__global__ void k_set_col(float* hi, float* lo, int64_t ld, int rows, int col, float v) {
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
-    hi[(int64_t)r * ld + col] = v;
-    lo[(int64_t)r * ld + col] = 0.f;
-  }
-}
+// leading dimension of a b x (n + 1) split activation: 16-byte rows for TMA
+int64_t ld_for(int n) { return ((int64_t)n + 1 + 7) / 8 * 8; }
 
 static int grid_for(int64_t n, int threads = 256) {
   int64_t g = (n + threads - 1) / threads;
   return (int)(g < 1 ? 1 : (g > 148 * 16 ? 148 * 16 : g));
 }
 
-void split_vec(cv_ctx* ctx, const float* x, float* hi, float* lo, int64_t n, const int* skip) {
-  k_split_vec<<<grid_for(n), 256, 0, ctx->stream>>>(x, hi, lo, n, skip);
-  ctx->launches++;
+static const float* am(const Scale* sc) { return &sc->amax; }
+
+static void bound_add(AccBound& b, float k, const Scale* x, const Scale* y) {
+  b.k[b.n] = k;
+  b.x[b.n] = am(x);
+  b.y[b.n] = am(y);
+  ++b.n;
 }
 
 // ---------------------------------------------------------------------------
@@ -73,8 +43,9 @@ void split_vec(cv_ctx* ctx, const float* x, float* hi, float* lo, int64_t n, con
 __global__ void __launch_bounds__(256) k_loss_rows(const float* __restrict__ logits, int rows, int c, int loss,
                                                    const int64_t* __restrict__ yi, const float* __restrict__ yf,
                                                    float* probs, float* gout, float inv_b, double* partial,
-                                                   int write_state) {
+                                                   int write_state, float* gout_amax) {
   double part[1] = {0.0};
+  float amax = 0.f;
   for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < rows; m += gridDim.x * blockDim.x) {
     const float* z = logits + (int64_t)m * c;
     if (loss == CV_LOSS_CE) {
@@ -88,7 +59,9 @@ __global__ void __launch_bounds__(256) k_loss_rows(const float* __restrict__ log
         for (int j = 0; j < c; ++j) {
           const double p = exp((double)z[j] - mx) / se;
           probs[(int64_t)m * c + j] = (float)p;
-          gout[(int64_t)m * c + j] = (float)((p - (j == y ? 1.0 : 0.0)) * inv_b);
+          const float g = (float)((p - (j == y ? 1.0 : 0.0)) * inv_b);
+          gout[(int64_t)m * c + j] = g;
+          amax = fmaxf(amax, fabsf(g));
         }
       }
     } else {
@@ -96,11 +69,17 @@ __global__ void __launch_bounds__(256) k_loss_rows(const float* __restrict__ log
       for (int j = 0; j < c; ++j) {
         const double r = (double)z[j] - (double)yf[(int64_t)m * c + j];
         s += r * r;
-        if (write_state) gout[(int64_t)m * c + j] = (float)(r * inv_b);
+        if (write_state) {
+          const float g = (float)(r * inv_b);
+          gout[(int64_t)m * c + j] = g;
+          amax = fmaxf(amax, fabsf(g));
+        }
       }
       part[0] += 0.5 * s;
     }
   }
+  amax = warp_max_f(amax);
+  if ((threadIdx.x & 31) == 0 && write_state) atomic_amax(gout_amax, amax);
   block_sum<1>(part);
   if (threadIdx.x == 0) partial[blockIdx.x] = part[0];
 }
@@ -115,24 +94,22 @@ __global__ void k_finalize_sum(const double* partial, int nblk, double scale, do
 }
 
 // ---------------------------------------------------------------------------
-// Tensor-core output layer helpers (tc_out): padded split copies of the c-wide
-// operands and the row-wise post-processing of the JVP partials.
+// Tensor-core output layer helpers (tc_out)
 // ---------------------------------------------------------------------------
-// rows x c (ld ld_src) -> rows x cp split, zero padded; from (hi, lo) or from plain fp32
-__global__ void k_pad_split(const float* hi, const float* lo, const float* plain, int64_t ld_src, int rows, int c,
-                            int cp, float* ohi, float* olo, const int* skip) {
+// (rows x c, ld c) split block -> transposed, padded (cp x ldo) split, same exponent
+__global__ void k_pad_t(const __half* hi, const __half* lo, int rows, int c, int cp, int64_t ldo, __half* ohi,
+                        __half* olo, const int* skip) {
   if (skip_if(skip)) return;
-  const int64_t total = (int64_t)rows * cp;
+  const int64_t total = (int64_t)cp * rows;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / cp;
-    const int j = (int)(i - r * cp);
-    float h = 0.f, l = 0.f;
+    const int64_t j = i / rows, r = i - j * rows;
+    __half h = __float2half_rn(0.f), l = h;
     if (j < c) {
-      if (plain) split2(plain[r * ld_src + j], h, l);
-      else { h = hi[r * ld_src + j]; l = lo[r * ld_src + j]; }
+      h = hi[r * c + j];
+      l = lo[r * c + j];
     }
-    ohi[i] = h;
-    olo[i] = l;
+    ohi[j * ldo + r] = h;
+    olo[j * ldo + r] = l;
   }
 }
 
@@ -140,108 +117,129 @@ __global__ void k_pad_split(const float* hi, const float* lo, const float* plain
 // the logits tangent (POST_LOGITS) or U = H_z(z) * scale (models.py:199-204)
 template <int CM>
 __global__ void k_out_reduce(const float* part, int splits, int rows, int c, int post, int loss, const float* probs,
-                             float scale, float* out_plain, float* ohi, float* olo, int cp, const int* skip) {
+                             float scale, float* out, float* out_amax, const int* skip) {
   if (skip_if(skip)) return;
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= rows) return;
-  float t[CM];
+  float amax = 0.f;
+  if (m < rows) {
+    float t[CM];
 #pragma unroll
-  for (int j = 0; j < CM; ++j) t[j] = 0.f;
-  for (int z = 0; z < splits; ++z) {
-    const float* p = part + ((int64_t)z * rows + m) * c;
-#pragma unroll
-    for (int j = 0; j < CM; ++j)
-      if (j < c) t[j] += p[j];
-  }
-  if (post == 1) {
-    if (loss == CV_LOSS_CE) {
-      const float* p = probs + (int64_t)m * c;
-      float pt = 0.f;
+    for (int j = 0; j < CM; ++j) t[j] = 0.f;
+    for (int z = 0; z < splits; ++z) {
+      const float* p = part + ((int64_t)z * rows + m) * c;
 #pragma unroll
       for (int j = 0; j < CM; ++j)
-        if (j < c) pt = fmaf(p[j], t[j], pt);
-#pragma unroll
-      for (int j = 0; j < CM; ++j)
-        if (j < c) t[j] = (p[j] * t[j] - p[j] * pt) * scale;
-    } else {
-#pragma unroll
-      for (int j = 0; j < CM; ++j) t[j] *= scale;
+        if (j < c) t[j] += p[j];
     }
-  }
-  if (out_plain)
+    if (post == 1) {
+      if (loss == CV_LOSS_CE) {
+        const float* p = probs + (int64_t)m * c;
+        float pt = 0.f;
 #pragma unroll
-    for (int j = 0; j < CM; ++j)
-      if (j < c) out_plain[(int64_t)m * c + j] = t[j];
-  if (ohi)
+        for (int j = 0; j < CM; ++j)
+          if (j < c) pt = fmaf(p[j], t[j], pt);
 #pragma unroll
-    for (int j = 0; j < CM; ++j)
-      if (j < cp) {
-        float h = 0.f, l = 0.f;
-        if (j < c) split2(t[j], h, l);
-        ohi[(int64_t)m * cp + j] = h;
-        olo[(int64_t)m * cp + j] = l;
+        for (int j = 0; j < CM; ++j)
+          if (j < c) t[j] = (p[j] * t[j] - p[j] * pt) * scale;
+      } else {
+#pragma unroll
+        for (int j = 0; j < CM; ++j) t[j] *= scale;
       }
+    }
+#pragma unroll
+    for (int j = 0; j < CM; ++j)
+      if (j < c) {
+        out[(int64_t)m * c + j] = t[j];
+        amax = fmaxf(amax, fabsf(t[j]));
+      }
+  }
+  amax = warp_max_f(amax);
+  if ((threadIdx.x & 31) == 0 && out_amax) atomic_amax(out_amax, amax);
 }
 
 // ---------------------------------------------------------------------------
 // Host orchestration
 // ---------------------------------------------------------------------------
-static void launch_skinny_rows(cv_ctx* ctx, const SkinnyRowsArgs& a) { skinny_rows(ctx, a); }
-static void launch_skinny_dx(cv_ctx* ctx, const SkinnyDxArgs& a) { skinny_dx(ctx, a); }
-static void launch_skinny_dw(cv_ctx* ctx, cv_snap* s, SkinnyDwArgs a) { skinny_dw(ctx, a, s->skinny_ws, s->skinny_ws_elems); }
+static Operand mk_op(const __half* hi, const __half* lo, int64_t si, int64_t sj, const Scale* sc) {
+  Operand o;
+  o.hi = hi;
+  o.lo = lo;
+  o.si = si;
+  o.sj = sj;
+  o.sc = sc;
+  return o;
+}
+static Operand op_rows(const SplitBuf& b) { return mk_op(b.hi, b.lo, b.ld, 1, b.sc); }   // X(m,k)=buf[m,k]
+static Operand op_trans(const SplitBuf& b) { return mk_op(b.hi, b.lo, 1, b.ld, b.sc); }  // X(m,k)=buf[k,m]
+// layer block [W; b] (rows x nout, row-major): B(k, n) = W[k, n]  /  B(k, n) = W[n, k]
+static Operand op_wblock(const __half* hi, const __half* lo, int nout, const Scale* sc) {
+  return mk_op(hi, lo, nout, 1, sc);
+}
+static Operand op_wT(const __half* hi, const __half* lo, int nout, const Scale* sc) { return mk_op(hi, lo, 1, nout, sc); }
 
-// Operand views --------------------------------------------------------------
-static Operand op_rows(const SplitBuf& b) { return Operand{b.hi, b.lo, b.ld, 1}; }          // X(m,k)=buf[m,k]
-static Operand op_trans(const SplitBuf& b) { return Operand{b.hi, b.lo, 1, b.ld}; }         // X(m,k)=buf[k,m]
-static Operand op_wblock(const float* hi, const float* lo, int nout) { return Operand{hi, lo, nout, 1}; }
-static Operand op_wT(const float* hi, const float* lo, int nout) { return Operand{hi, lo, 1, nout}; }
+static void split_epi(Epilogue& e, const SplitBuf& out) {
+  e.out_hi = out.hi;
+  e.out_lo = out.lo;
+  e.ld = out.ld;
+  e.out_sc = out.sc;
+}
+static void mask_epi(Epilogue& e, const SplitBuf& a) {
+  e.mask_hi = a.hi;
+  e.mask_lo = a.lo;
+  e.mask_ld = a.ld;
+  e.mask_sc = a.sc;
+}
 
-// last-layer block of a split flat vector -> padded split copy (tc_out)
-static void pad_last(cv_ctx* ctx, cv_snap* s, const float* hi, const float* lo, float* ohi, float* olo,
+// last-layer block of a split flat vector -> transposed padded split (tc_out)
+static void pad_last(cv_ctx* ctx, cv_snap* s, const __half* hi, const __half* lo, __half* ohi, __half* olo,
                      const int* skip) {
   const int l = s->L - 1;
   const int rows = s->dims[l] + 1;
-  k_pad_split<<<grid_for((int64_t)rows * s->cp), 256, 0, ctx->stream>>>(hi + s->off[l], lo + s->off[l], nullptr, s->c,
-                                                                         rows, s->c, s->cp, ohi, olo, skip);
+  k_pad_t<<<grid_for((int64_t)rows * s->cp), 256, 0, ctx->stream>>>(hi + s->off[l], lo + s->off[l], rows, s->c, s->cp,
+                                                                     s->ldw, ohi, olo, skip);
   ctx->launches++;
 }
 
 void pad_last_weights(cv_ctx* ctx, cv_snap* s) { pad_last(ctx, s, s->w_hi, s->w_lo, s->wl_hi, s->wl_lo, nullptr); }
 
-// the split (ld cp) form of a b x c cotangent: U / G[L-1] map to their resident
-// splits, any other (plain, ld c) matrix is split into U_hi / U_lo
-static void cot_split(cv_ctx* ctx, cv_snap* s, const float* U, const float** hi, const float** lo, const int* skip) {
-  if (U == s->gout) { *hi = s->gout_hi; *lo = s->gout_lo; return; }
-  if (U != s->U) {
-    k_pad_split<<<grid_for((int64_t)s->bl * s->cp), 256, 0, ctx->stream>>>(nullptr, nullptr, U, s->c, s->bl, s->c,
-                                                                           s->cp, s->U_hi, s->U_lo, skip);
-    ctx->launches++;
+// The transposed split (cp x ldb) of a b x c cotangent whose amax slot is valid:
+// G[L-1] keeps its resident split, anything else is split into U_hi / U_lo.
+static const Scale* cot_split(cv_ctx* ctx, cv_snap* s, const float* U, Scale* usc, const __half** hi,
+                              const __half** lo, const int* skip) {
+  if (U == s->gout) {
+    *hi = s->gout_hi;
+    *lo = s->gout_lo;
+    return s->gout_sc;
   }
+  split_mat(ctx, U, s->c, s->bl, s->c, s->U_hi, s->U_lo, s->ldb, 1, usc, 1, skip);
   *hi = s->U_hi;
   *lo = s->U_lo;
+  return usc;
 }
 
-void mlp_forward_layer(cv_ctx* ctx, cv_snap* s, int l, const SplitBuf& in, const float* whi, const float* wlo,
-                       const SplitBuf& out) {
+void mlp_forward_layer(cv_ctx* ctx, cv_snap* s, int l, const SplitBuf& in, const __half* whi, const __half* wlo,
+                       const Scale* wsc, const SplitBuf& out) {
   GemmArgs g;
   g.M = s->bl;
   g.N = s->dims[l + 1];
   g.nseg = 1;
-  g.seg[0] = GemmSeg{op_rows(in), op_wblock(whi + s->off[l], wlo + s->off[l], s->dims[l + 1]), s->dims[l] + 1};
+  g.seg[0] = GemmSeg{op_rows(in), op_wblock(whi + s->off[l], wlo + s->off[l], s->dims[l + 1], wsc + l), s->dims[l] + 1};
   g.epi.mode = EPI_SPLIT_ACT;
   g.epi.act = s->act;
-  g.epi.out_hi = out.hi;
-  g.epi.out_lo = out.lo;
-  g.epi.ld = out.ld;
+  split_epi(g.epi, out);
+  g.epi.out_unit = 1;
+  bound_add(g.epi.bound, (float)(s->dims[l] + 1), in.sc, wsc + l);
   gemm(ctx, g);
+  // the ones column of the next layer's augmented input (covered by the scale)
+  set_col_value(ctx, out, s->bl, s->dims[l + 1], 1.f);
 }
 
 // logits = A_{L-1} [W; b]  (skinny)
-void mlp_output_layer(cv_ctx* ctx, cv_snap* s, const SplitBuf& in, const float* whi, const float* wlo,
-                      float* logits) {
+void mlp_output_layer(cv_ctx* ctx, cv_snap* s, const SplitBuf& in, const __half* whi, const __half* wlo,
+                      const Scale* wsc, float* logits) {
   const int l = s->L - 1;
   if (s->tc_out) {
-    const float *bh = s->wl_hi, *bl = s->wl_lo;
+    const __half *bh = s->wl_hi, *bl = s->wl_lo;
     if (whi != s->w_hi) {  // another parameter point (loss_at): pad its last block
       pad_last(ctx, s, whi, wlo, s->vl_hi, s->vl_lo, nullptr);
       bh = s->vl_hi;
@@ -251,7 +249,7 @@ void mlp_output_layer(cv_ctx* ctx, cv_snap* s, const SplitBuf& in, const float* 
     g.M = s->bl;
     g.N = s->c;
     g.nseg = 1;
-    g.seg[0] = GemmSeg{op_rows(in), Operand{bh, bl, s->cp, 1}, s->dims[l] + 1};
+    g.seg[0] = GemmSeg{op_rows(in), mk_op(bh, bl, 1, s->ldw, wsc + l), s->dims[l] + 1};
     g.epi.mode = EPI_STORE;
     g.epi.out = logits;
     g.epi.ld = s->c;
@@ -262,38 +260,35 @@ void mlp_output_layer(cv_ctx* ctx, cv_snap* s, const SplitBuf& in, const float* 
   a.rows = s->bl;
   a.c = s->c;
   a.nseg = 1;
-  a.seg[0] = SkinnySeg{in.hi, in.lo, in.ld, whi + s->off[l], wlo + s->off[l], s->c, s->dims[l] + 1};
+  a.seg[0] = SkinnySeg{in.hi, in.lo, in.ld, in.sc, whi + s->off[l], wlo + s->off[l], s->c, wsc + l, s->dims[l] + 1};
   a.post = POST_LOGITS;
   a.loss = s->loss;
   a.out = logits;
-  launch_skinny_rows(ctx, a);
+  skinny_rows(ctx, a);
 }
 
-// Loss value (+ optionally probs / G[L-1]) from logits; *loss_out = global mean.
 void mlp_loss(cv_ctx* ctx, cv_snap* s, const float* logits, int write_state, double* loss_out);
 
 // G_prev = (U W_l^T) * act'(a_l) for the output layer (l = L-1), skinny K = c.
-static void skinny_backward(cv_ctx* ctx, cv_snap* s, const float* U, const float* whi, const float* wlo,
-                            const SplitBuf& out, float* raw, const int* skip) {
+static void skinny_backward(cv_ctx* ctx, cv_snap* s, const float* U, Scale* usc, const __half* whi, const __half* wlo,
+                            const Scale* wsc, const SplitBuf& out, float* raw, Scale* raw_sc, const int* skip) {
   const int l = s->L - 1;
-  if (s->tc_out && s->tc_dx) {
-    const float *uh, *ul;
-    cot_split(ctx, s, U, &uh, &ul, skip);
+  if (s->tc_out && s->tc_dx && whi == s->w_hi) {
+    const __half *uh, *ul;
+    const Scale* uc = cot_split(ctx, s, U, usc, &uh, &ul, skip);
     GemmArgs g;
     g.M = s->bl;
     g.N = s->dims[l];
     g.nseg = 1;
-    g.seg[0] = GemmSeg{Operand{uh, ul, s->cp, 1}, Operand{s->wl_hi, s->wl_lo, 1, s->cp}, s->c};
+    g.seg[0] = GemmSeg{mk_op(uh, ul, 1, s->ldb, uc), mk_op(s->wl_hi, s->wl_lo, s->ldw, 1, wsc + l), s->c};
     g.epi.mode = EPI_SPLIT_MASK;
     g.epi.act = s->act;
-    g.epi.out_hi = out.hi;
-    g.epi.out_lo = out.lo;
-    g.epi.ld = out.ld;
-    g.epi.mask_hi = s->acts[l].hi;
-    g.epi.mask_lo = s->acts[l].lo;
-    g.epi.mask_ld = s->acts[l].ld;
+    split_epi(g.epi, out);
+    mask_epi(g.epi, s->acts[l]);
     g.epi.raw = raw;
     g.epi.raw_ld = out.ld;
+    g.epi.raw_amax = raw_sc ? &raw_sc->amax : nullptr;
+    bound_add(g.epi.bound, (float)s->c, uc, wsc + l);
     g.skip = skip;
     gemm(ctx, g);
     return;
@@ -306,38 +301,36 @@ static void skinny_backward(cv_ctx* ctx, cv_snap* s, const float* U, const float
   a.U[0] = U;
   a.w_hi[0] = whi + s->off[l];
   a.w_lo[0] = wlo + s->off[l];
+  a.w_sc[0] = wsc + l;
   a.epi.mode = EPI_SPLIT_MASK;
   a.epi.act = s->act;
-  a.epi.out_hi = out.hi;
-  a.epi.out_lo = out.lo;
-  a.epi.ld = out.ld;
-  a.epi.mask_hi = s->acts[l].hi;
-  a.epi.mask_lo = s->acts[l].lo;
-  a.epi.mask_ld = s->acts[l].ld;
+  split_epi(a.epi, out);
+  mask_epi(a.epi, s->acts[l]);
   a.epi.raw = raw;
   a.epi.raw_ld = out.ld;
+  a.epi.raw_amax = raw_sc ? &raw_sc->amax : nullptr;
+  bound_add(a.epi.bound, (float)s->c, usc, wsc + l);
   a.skip = skip;
-  launch_skinny_dx(ctx, a);
+  skinny_dx(ctx, a);
 }
 
 // G_prev = (G_l W_l^T) * act'(a_l), hidden layer l >= 1
-static void hidden_backward(cv_ctx* ctx, cv_snap* s, int l, const SplitBuf& Gl, const float* whi,
-                            const float* wlo, const SplitBuf& out, float* raw, const int* skip) {
+static void hidden_backward(cv_ctx* ctx, cv_snap* s, int l, const SplitBuf& Gl, const __half* whi,
+                            const __half* wlo, const Scale* wsc, const SplitBuf& out, float* raw, Scale* raw_sc,
+                            const int* skip) {
   GemmArgs g;
   g.M = s->bl;
   g.N = s->dims[l];
   g.nseg = 1;
-  g.seg[0] = GemmSeg{op_rows(Gl), op_wT(whi + s->off[l], wlo + s->off[l], s->dims[l + 1]), s->dims[l + 1]};
+  g.seg[0] = GemmSeg{op_rows(Gl), op_wT(whi + s->off[l], wlo + s->off[l], s->dims[l + 1], wsc + l), s->dims[l + 1]};
   g.epi.mode = EPI_SPLIT_MASK;
   g.epi.act = s->act;
-  g.epi.out_hi = out.hi;
-  g.epi.out_lo = out.lo;
-  g.epi.ld = out.ld;
-  g.epi.mask_hi = s->acts[l].hi;
-  g.epi.mask_lo = s->acts[l].lo;
-  g.epi.mask_ld = s->acts[l].ld;
+  split_epi(g.epi, out);
+  mask_epi(g.epi, s->acts[l]);
   g.epi.raw = raw;
   g.epi.raw_ld = out.ld;
+  g.epi.raw_amax = raw_sc ? &raw_sc->amax : nullptr;
+  bound_add(g.epi.bound, (float)s->dims[l + 1], Gl.sc, wsc + l);
   g.skip = skip;
   gemm(ctx, g);
 }
@@ -349,8 +342,8 @@ static void weight_grad(cv_ctx* ctx, cv_snap* s, int l, const SplitBuf& G1, cons
   g.M = s->dims[l] + 1;
   g.N = s->dims[l + 1];
   g.nseg = A2 ? 2 : 1;
-  g.seg[0] = GemmSeg{op_trans(s->acts[l]), Operand{G1.hi, G1.lo, G1.ld, 1}, s->bl};
-  if (A2) g.seg[1] = GemmSeg{op_trans(*A2), Operand{G2->hi, G2->lo, G2->ld, 1}, s->bl};
+  g.seg[0] = GemmSeg{op_trans(s->acts[l]), mk_op(G1.hi, G1.lo, G1.ld, 1, G1.sc), s->bl};
+  if (A2) g.seg[1] = GemmSeg{op_trans(*A2), mk_op(G2->hi, G2->lo, G2->ld, 1, G2->sc), s->bl};
   g.epi.mode = EPI_STORE;
   g.epi.out = out + s->off[l];
   g.epi.ld = s->dims[l + 1];
@@ -358,19 +351,21 @@ static void weight_grad(cv_ctx* ctx, cv_snap* s, int l, const SplitBuf& G1, cons
   gemm(ctx, g);
 }
 
-static void skinny_weight_grad(cv_ctx* ctx, cv_snap* s, const float* U, const SplitBuf* A2, const float* U2,
-                               float* out, const int* skip) {
+// last layer: [gW; gb] = A^T U (+ A2^T U2)
+static void skinny_weight_grad(cv_ctx* ctx, cv_snap* s, const float* U, Scale* usc, const SplitBuf* A2,
+                               const float* U2, Scale* u2sc, float* out, const int* skip) {
   const int l = s->L - 1;
   if (s->tc_out) {
-    const float *uh, *ul, *u2h = nullptr, *u2l = nullptr;
-    cot_split(ctx, s, U, &uh, &ul, skip);
-    if (A2) cot_split(ctx, s, U2, &u2h, &u2l, skip);
+    const __half *uh, *ul, *u2h = nullptr, *u2l = nullptr;
+    const Scale* uc = cot_split(ctx, s, U, usc, &uh, &ul, skip);
+    const Scale* u2c = nullptr;
+    if (A2) u2c = cot_split(ctx, s, U2, u2sc, &u2h, &u2l, skip);
     GemmArgs g;
     g.M = s->dims[l] + 1;
     g.N = s->c;
     g.nseg = A2 ? 2 : 1;
-    g.seg[0] = GemmSeg{op_trans(s->acts[l]), Operand{uh, ul, s->cp, 1}, s->bl};
-    if (A2) g.seg[1] = GemmSeg{op_trans(*A2), Operand{u2h, u2l, s->cp, 1}, s->bl};
+    g.seg[0] = GemmSeg{op_trans(s->acts[l]), mk_op(uh, ul, 1, s->ldb, uc), s->bl};
+    if (A2) g.seg[1] = GemmSeg{op_trans(*A2), mk_op(u2h, u2l, 1, s->ldb, u2c), s->bl};
     g.epi.mode = EPI_STORE;
     g.epi.out = out + s->off[l];
     g.epi.ld = s->c;
@@ -383,78 +378,85 @@ static void skinny_weight_grad(cv_ctx* ctx, cv_snap* s, const float* U, const Sp
   a.M = s->dims[l] + 1;
   a.c = s->c;
   a.nseg = A2 ? 2 : 1;
-  a.a_hi[0] = s->acts[l].hi; a.a_lo[0] = s->acts[l].lo; a.lda[0] = s->acts[l].ld; a.U[0] = U;
-  if (A2) { a.a_hi[1] = A2->hi; a.a_lo[1] = A2->lo; a.lda[1] = A2->ld; a.U[1] = U2; }
+  a.a_hi[0] = s->acts[l].hi; a.a_lo[0] = s->acts[l].lo; a.lda[0] = s->acts[l].ld; a.a_sc[0] = s->acts[l].sc;
+  a.U[0] = U;
+  if (A2) { a.a_hi[1] = A2->hi; a.a_lo[1] = A2->lo; a.lda[1] = A2->ld; a.a_sc[1] = A2->sc; a.U[1] = U2; }
   a.out = out + s->off[l];
   a.skip = skip;
-  launch_skinny_dw(ctx, s, a);
+  skinny_dw(ctx, a, s->skinny_ws, s->skinny_ws_elems);
 }
 
 
 // Full linearization (models.py:337-396): acts, loss, probs, G, grad.
 void mlp_linearize(cv_ctx* ctx, cv_snap* s, double* loss_out, float* grad_out) {
   const int L = s->L;
-  for (int l = 0; l < L - 1; ++l) mlp_forward_layer(ctx, s, l, s->acts[l], s->w_hi, s->w_lo, s->acts[l + 1]);
-  mlp_output_layer(ctx, s, s->acts[L - 1], s->w_hi, s->w_lo, s->logits);
+  for (int l = 0; l < L - 1; ++l)
+    mlp_forward_layer(ctx, s, l, s->acts[l], s->w_hi, s->w_lo, s->w_sc, s->acts[l + 1]);
+  mlp_output_layer(ctx, s, s->acts[L - 1], s->w_hi, s->w_lo, s->w_sc, s->logits);
   mlp_loss(ctx, s, s->logits, 1, loss_out);
   // primal backward: G[l-1] = (G[l] W_l^T) * sp[l-1]   (models.py:378-381)
+  const bool tanh_ = s->act == CV_ACT_TANH;
   if (L >= 2) {
-    skinny_backward(ctx, s, s->gout, s->w_hi, s->w_lo, s->G[L - 2], s->act == CV_ACT_TANH ? s->P[L - 2] : nullptr,
-                    nullptr);
+    skinny_backward(ctx, s, s->gout, s->gout_sc, s->w_hi, s->w_lo, s->w_sc, s->G[L - 2],
+                    tanh_ ? s->P[L - 2] : nullptr, tanh_ ? s->P_sc[L - 2] : nullptr, nullptr);
     for (int l = L - 2; l >= 1; --l)
-      hidden_backward(ctx, s, l, s->G[l], s->w_hi, s->w_lo, s->G[l - 1],
-                      s->act == CV_ACT_TANH ? s->P[l - 1] : nullptr, nullptr);
+      hidden_backward(ctx, s, l, s->G[l], s->w_hi, s->w_lo, s->w_sc, s->G[l - 1], tanh_ ? s->P[l - 1] : nullptr,
+                      tanh_ ? s->P_sc[l - 1] : nullptr, nullptr);
   }
   if (grad_out) {
-    skinny_weight_grad(ctx, s, s->gout, nullptr, nullptr, grad_out, nullptr);
+    skinny_weight_grad(ctx, s, s->gout, s->gout_sc, nullptr, nullptr, nullptr, grad_out, nullptr);
     for (int l = L - 2; l >= 0; --l) weight_grad(ctx, s, l, s->G[l], nullptr, nullptr, grad_out, nullptr);
     if (ctx->nccl) allreduce_f32(ctx, grad_out, s->d);
   }
 }
 
+// split of a product input v into v_hi / v_lo (per-layer exponents); also
+// zeroes this product's amax slots
+static void split_input(cv_ctx* ctx, cv_snap* s, const float* v, const int* skip) {
+  split_flat(ctx, v, s->d, s->off, s->v_hi, s->v_lo, s->v_sc, s->prod_sc, s->n_prod, skip);
+}
+
 // JVP through the hidden layers: da[l] = act'(a_{l+1}) * (A_l V_l + da[l-1] W_l).
-static void jvp_hidden(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, bool keep_dz,
-                       const int* skip) {
+static void jvp_hidden(cv_ctx* ctx, cv_snap* s, bool keep_dz, const int* skip) {
   for (int l = 0; l < s->L - 1; ++l) {
     GemmArgs g;
     g.M = s->bl;
     g.N = s->dims[l + 1];
-    g.seg[0] = GemmSeg{op_rows(s->acts[l]), op_wblock(vhi + s->off[l], vlo + s->off[l], s->dims[l + 1]),
+    g.seg[0] = GemmSeg{op_rows(s->acts[l]),
+                       op_wblock(s->v_hi + s->off[l], s->v_lo + s->off[l], s->dims[l + 1], s->v_sc + l),
                        s->dims[l] + 1};
     g.nseg = 1;
+    bound_add(g.epi.bound, (float)(s->dims[l] + 1), s->acts[l].sc, s->v_sc + l);
     if (l > 0) {
-      g.seg[1] = GemmSeg{op_rows(s->da[l - 1]), op_wblock(s->w_hi + s->off[l], s->w_lo + s->off[l], s->dims[l + 1]),
-                         s->dims[l]};
+      g.seg[1] = GemmSeg{op_rows(s->da[l - 1]),
+                         op_wblock(s->w_hi + s->off[l], s->w_lo + s->off[l], s->dims[l + 1], s->w_sc + l), s->dims[l]};
       g.nseg = 2;
+      bound_add(g.epi.bound, (float)s->dims[l], s->da[l - 1].sc, s->w_sc + l);
     }
     g.epi.mode = EPI_SPLIT_MASK;
     g.epi.act = s->act;
-    g.epi.out_hi = s->da[l].hi;
-    g.epi.out_lo = s->da[l].lo;
-    g.epi.ld = s->da[l].ld;
-    g.epi.mask_hi = s->acts[l + 1].hi;
-    g.epi.mask_lo = s->acts[l + 1].lo;
-    g.epi.mask_ld = s->acts[l + 1].ld;
+    split_epi(g.epi, s->da[l]);
+    mask_epi(g.epi, s->acts[l + 1]);
     g.epi.raw = keep_dz ? s->dz[l] : nullptr;
     g.epi.raw_ld = s->da[l].ld;
+    g.epi.raw_amax = keep_dz ? &s->dz_sc[l]->amax : nullptr;
     g.skip = skip;
     gemm(ctx, g);
   }
 }
 
 // Output tangent with fused H_z: U = H_z(J v) * scale (post HZ) or raw J v (logits).
-static void jvp_out(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, int post, float scale,
-                    float* out, const int* skip) {
+static void jvp_out(cv_ctx* ctx, cv_snap* s, int post, float scale, float* out, float* out_amax, const int* skip) {
   const int l = s->L - 1;
   if (s->tc_out) {
-    pad_last(ctx, s, vhi, vlo, s->vl_hi, s->vl_lo, skip);
+    pad_last(ctx, s, s->v_hi, s->v_lo, s->vl_hi, s->vl_lo, skip);
     GemmArgs g;
     g.M = s->bl;
     g.N = s->c;
     g.nseg = 1;
-    g.seg[0] = GemmSeg{op_rows(s->acts[l]), Operand{s->vl_hi, s->vl_lo, s->cp, 1}, s->dims[l] + 1};
+    g.seg[0] = GemmSeg{op_rows(s->acts[l]), mk_op(s->vl_hi, s->vl_lo, 1, s->ldw, s->v_sc + l), s->dims[l] + 1};
     if (l > 0) {
-      g.seg[1] = GemmSeg{op_rows(s->da[l - 1]), Operand{s->wl_hi, s->wl_lo, s->cp, 1}, s->dims[l]};
+      g.seg[1] = GemmSeg{op_rows(s->da[l - 1]), mk_op(s->wl_hi, s->wl_lo, 1, s->ldw, s->w_sc + l), s->dims[l]};
       g.nseg = 2;
     }
     g.skip = skip;
@@ -463,12 +465,10 @@ static void jvp_out(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo,
     const bool hz = post == POST_HZ;
     if (s->c <= 16)
       k_out_reduce<16><<<(s->bl + 127) / 128, 128, 0, ctx->stream>>>(part, splits, s->bl, s->c, hz, s->loss, s->probs,
-                                                                    scale, out, hz ? s->U_hi : nullptr,
-                                                                    hz ? s->U_lo : nullptr, s->cp, skip);
+                                                                    scale, out, out_amax, skip);
     else
       k_out_reduce<32><<<(s->bl + 127) / 128, 128, 0, ctx->stream>>>(part, splits, s->bl, s->c, hz, s->loss, s->probs,
-                                                                    scale, out, hz ? s->U_hi : nullptr,
-                                                                    hz ? s->U_lo : nullptr, s->cp, skip);
+                                                                    scale, out, out_amax, skip);
     ctx->launches++;
     ctx->pool.put(part);
     return;
@@ -476,12 +476,12 @@ static void jvp_out(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo,
   SkinnyRowsArgs a{};
   a.rows = s->bl;
   a.c = s->c;
-  a.seg[0] = SkinnySeg{s->acts[l].hi, s->acts[l].lo, s->acts[l].ld, vhi + s->off[l], vlo + s->off[l], s->c,
-                       s->dims[l] + 1};
+  a.seg[0] = SkinnySeg{s->acts[l].hi, s->acts[l].lo, s->acts[l].ld, s->acts[l].sc, s->v_hi + s->off[l],
+                       s->v_lo + s->off[l], s->c, s->v_sc + l, s->dims[l] + 1};
   a.nseg = 1;
   if (l > 0) {
-    a.seg[1] = SkinnySeg{s->da[l - 1].hi, s->da[l - 1].lo, s->da[l - 1].ld, s->w_hi + s->off[l], s->w_lo + s->off[l],
-                         s->c, s->dims[l]};
+    a.seg[1] = SkinnySeg{s->da[l - 1].hi, s->da[l - 1].lo, s->da[l - 1].ld, s->da[l - 1].sc, s->w_hi + s->off[l],
+                         s->w_lo + s->off[l], s->c, s->w_sc + l, s->dims[l]};
     a.nseg = 2;
   }
   a.post = post;
@@ -489,107 +489,110 @@ static void jvp_out(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo,
   a.probs = s->probs;
   a.scale = scale;
   a.out = out;
+  a.out_amax = out_amax;
   a.skip = skip;
-  launch_skinny_rows(ctx, a);
+  skinny_rows(ctx, a);
 }
 
-// sum_i J_i^T U_i (no 1/b) into out (models.py:274-285).
-static void vjp_from(cv_ctx* ctx, cv_snap* s, const float* U, float* out, const int* skip) {
+// sum_i J_i^T U_i (no 1/b) into out (models.py:274-285); usc->amax = max|U|.
+static void vjp_from(cv_ctx* ctx, cv_snap* s, const float* U, Scale* usc, float* out, const int* skip) {
   const int L = s->L;
-  skinny_weight_grad(ctx, s, U, nullptr, nullptr, out, skip);
+  skinny_weight_grad(ctx, s, U, usc, nullptr, nullptr, nullptr, out, skip);
   if (L >= 2) {
-    int cur = 0;
-    skinny_backward(ctx, s, U, s->w_hi, s->w_lo, s->gs[L - 2], nullptr, skip);
-    (void)cur;
+    skinny_backward(ctx, s, U, usc, s->w_hi, s->w_lo, s->w_sc, s->gs[L - 2], nullptr, nullptr, skip);
     for (int l = L - 2; l >= 0; --l) {
       weight_grad(ctx, s, l, s->gs[l], nullptr, nullptr, out, skip);
-      if (l > 0) hidden_backward(ctx, s, l, s->gs[l], s->w_hi, s->w_lo, s->gs[l - 1], nullptr, skip);
+      if (l > 0) hidden_backward(ctx, s, l, s->gs[l], s->w_hi, s->w_lo, s->w_sc, s->gs[l - 1], nullptr, nullptr, skip);
     }
   }
 }
 
-// GGN product (1/b) J^T H_z J v (curvature.py:109-110); v given split.
-void mlp_ggn(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, float* out, const int* skip) {
-  jvp_hidden(ctx, s, vhi, vlo, false, skip);
-  jvp_out(ctx, s, vhi, vlo, POST_HZ, 1.0f / (float)s->bg, s->U, skip);
-  vjp_from(ctx, s, s->U, out, skip);
+// GGN product (1/b) J^T H_z J v (curvature.py:109-110).
+void mlp_ggn(cv_ctx* ctx, cv_snap* s, const float* v, float* out, const int* skip) {
+  split_input(ctx, s, v, skip);
+  jvp_hidden(ctx, s, false, skip);
+  jvp_out(ctx, s, POST_HZ, 1.0f / (float)s->bg, s->U, &s->U_sc->amax, skip);
+  vjp_from(ctx, s, s->U, s->U_sc, out, skip);
   if (ctx->nccl) allreduce_f32(ctx, out, s->d);
 }
 
-void mlp_jvp(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, float* out_bc) {
-  jvp_hidden(ctx, s, vhi, vlo, false, nullptr);
-  jvp_out(ctx, s, vhi, vlo, POST_LOGITS, 1.f, out_bc, nullptr);
+void mlp_jvp(cv_ctx* ctx, cv_snap* s, const float* v, float* out_bc) {
+  split_input(ctx, s, v, nullptr);
+  jvp_hidden(ctx, s, false, nullptr);
+  jvp_out(ctx, s, POST_LOGITS, 1.f, out_bc, nullptr, nullptr);
 }
 
 void mlp_vjp(cv_ctx* ctx, cv_snap* s, const float* U, float* out) {
-  vjp_from(ctx, s, U, out, nullptr);
+  cudaMemsetAsync(s->prod_sc, 0, sizeof(Scale) * s->n_prod, ctx->stream);
+  amax_into(ctx, U, (int64_t)s->bl * s->c, s->U_sc);
+  vjp_from(ctx, s, U, s->U_sc, out, nullptr);
   if (ctx->nccl) allreduce_f32(ctx, out, s->d);
 }
 
+// HVP backward epilogue for the layer below l: (dG W^T + G V^T) * sp [+ tanh P spp dz]
+static void hvp_epi(cv_snap* s, Epilogue& e, int l) {
+  e.mode = EPI_HVP;
+  e.act = s->act;
+  split_epi(e, s->gs[l - 1]);
+  mask_epi(e, s->acts[l]);
+  if (s->act == CV_ACT_TANH) {
+    e.P = s->P[l - 1];
+    e.P_ld = s->gs[l - 1].ld;
+    e.P_amax = &s->P_sc[l - 1]->amax;
+    e.dz = s->dz[l - 1];
+    e.dz_ld = s->da[l - 1].ld;
+    e.dz_amax = &s->dz_sc[l - 1]->amax;
+  }
+}
+
 // Exact Hessian-vector product (models.py:287-307), forward-over-reverse.
-void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, float* out, const int* skip) {
+void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* v, float* out, const int* skip) {
   const int L = s->L;
   const bool tanh_ = s->act == CV_ACT_TANH;
-  jvp_hidden(ctx, s, vhi, vlo, tanh_, skip);
+  split_input(ctx, s, v, skip);
+  jvp_hidden(ctx, s, tanh_, skip);
   // dG_{L-1} = H_z dz_{L-1} / b
-  jvp_out(ctx, s, vhi, vlo, POST_HZ, 1.0f / (float)s->bg, s->U, skip);
+  jvp_out(ctx, s, POST_HZ, 1.0f / (float)s->bg, s->U, &s->U_sc->amax, skip);
   // last layer: [gW; gb] = A^T dG + [da|0]^T G_{L-1}
-  skinny_weight_grad(ctx, s, s->U, L >= 2 ? &s->da[L - 2] : nullptr, s->gout, out, skip);
+  skinny_weight_grad(ctx, s, s->U, s->U_sc, L >= 2 ? &s->da[L - 2] : nullptr, s->gout, s->gout_sc, out, skip);
   if (L >= 2) {
     // dG_{L-2} = (dG W^T + G_{L-1} V^T) * sp + [tanh] P * spp * dz
     const int l = L - 1;
     if (s->tc_out && s->tc_dx) {
-      // vl holds this product's padded last block (written by jvp_out)
+      // U's split was made by skinny_weight_grad, vl by jvp_out
       GemmArgs g;
       g.M = s->bl;
       g.N = s->dims[l];
       g.nseg = 2;
-      g.seg[0] = GemmSeg{Operand{s->U_hi, s->U_lo, s->cp, 1}, Operand{s->wl_hi, s->wl_lo, 1, s->cp}, s->c};
-      g.seg[1] = GemmSeg{Operand{s->gout_hi, s->gout_lo, s->cp, 1}, Operand{s->vl_hi, s->vl_lo, 1, s->cp}, s->c};
-      g.epi.mode = EPI_HVP;
-      g.epi.act = s->act;
-      g.epi.out_hi = s->gs[l - 1].hi;
-      g.epi.out_lo = s->gs[l - 1].lo;
-      g.epi.ld = s->gs[l - 1].ld;
-      g.epi.mask_hi = s->acts[l].hi;
-      g.epi.mask_lo = s->acts[l].lo;
-      g.epi.mask_ld = s->acts[l].ld;
-      if (tanh_) {
-        g.epi.P = s->P[l - 1];
-        g.epi.P_ld = s->gs[l - 1].ld;
-        g.epi.dz = s->dz[l - 1];
-        g.epi.dz_ld = s->da[l - 1].ld;
-      }
+      g.seg[0] = GemmSeg{mk_op(s->U_hi, s->U_lo, 1, s->ldb, s->U_sc), mk_op(s->wl_hi, s->wl_lo, s->ldw, 1, s->w_sc + l),
+                         s->c};
+      g.seg[1] = GemmSeg{mk_op(s->gout_hi, s->gout_lo, 1, s->ldb, s->gout_sc),
+                         mk_op(s->vl_hi, s->vl_lo, s->ldw, 1, s->v_sc + l), s->c};
+      hvp_epi(s, g.epi, l);
+      bound_add(g.epi.bound, (float)s->c, s->U_sc, s->w_sc + l);
+      bound_add(g.epi.bound, (float)s->c, s->gout_sc, s->v_sc + l);
       g.skip = skip;
       gemm(ctx, g);
+    } else {
+      SkinnyDxArgs a{};
+      a.rows = s->bl;
+      a.n = s->dims[l];
+      a.c = s->c;
+      a.nseg = 2;
+      a.U[0] = s->U;
+      a.w_hi[0] = s->w_hi + s->off[l];
+      a.w_lo[0] = s->w_lo + s->off[l];
+      a.w_sc[0] = s->w_sc + l;
+      a.U[1] = s->gout;
+      a.w_hi[1] = s->v_hi + s->off[l];
+      a.w_lo[1] = s->v_lo + s->off[l];
+      a.w_sc[1] = s->v_sc + l;
+      hvp_epi(s, a.epi, l);
+      bound_add(a.epi.bound, (float)s->c, s->U_sc, s->w_sc + l);
+      bound_add(a.epi.bound, (float)s->c, s->gout_sc, s->v_sc + l);
+      a.skip = skip;
+      skinny_dx(ctx, a);
     }
-    SkinnyDxArgs a{};
-    a.rows = s->bl;
-    a.n = s->dims[l];
-    a.c = s->c;
-    a.nseg = 2;
-    a.U[0] = s->U;
-    a.w_hi[0] = s->w_hi + s->off[l];
-    a.w_lo[0] = s->w_lo + s->off[l];
-    a.U[1] = s->gout;
-    a.w_hi[1] = vhi + s->off[l];
-    a.w_lo[1] = vlo + s->off[l];
-    a.epi.mode = EPI_HVP;
-    a.epi.act = s->act;
-    a.epi.out_hi = s->gs[l - 1].hi;
-    a.epi.out_lo = s->gs[l - 1].lo;
-    a.epi.ld = s->gs[l - 1].ld;
-    a.epi.mask_hi = s->acts[l].hi;
-    a.epi.mask_lo = s->acts[l].lo;
-    a.epi.mask_ld = s->acts[l].ld;
-    if (tanh_) {
-      a.epi.P = s->P[l - 1];
-      a.epi.P_ld = s->gs[l - 1].ld;
-      a.epi.dz = s->dz[l - 1];
-      a.epi.dz_ld = s->da[l - 1].ld;
-    }
-    a.skip = skip;
-    if (!(s->tc_out && s->tc_dx)) launch_skinny_dx(ctx, a);
     for (int h = L - 2; h >= 0; --h) {
       weight_grad(ctx, s, h, s->gs[h], h > 0 ? &s->da[h - 1] : nullptr, h > 0 ? &s->G[h] : nullptr, out, skip);
       if (h > 0) {
@@ -597,24 +600,15 @@ void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, float*
         g.M = s->bl;
         g.N = s->dims[h];
         g.nseg = 2;
-        g.seg[0] = GemmSeg{op_rows(s->gs[h]), op_wT(s->w_hi + s->off[h], s->w_lo + s->off[h], s->dims[h + 1]),
+        g.seg[0] = GemmSeg{op_rows(s->gs[h]),
+                           op_wT(s->w_hi + s->off[h], s->w_lo + s->off[h], s->dims[h + 1], s->w_sc + h),
                            s->dims[h + 1]};
-        g.seg[1] = GemmSeg{op_rows(s->G[h]), op_wT(vhi + s->off[h], vlo + s->off[h], s->dims[h + 1]),
+        g.seg[1] = GemmSeg{op_rows(s->G[h]),
+                           op_wT(s->v_hi + s->off[h], s->v_lo + s->off[h], s->dims[h + 1], s->v_sc + h),
                            s->dims[h + 1]};
-        g.epi.mode = EPI_HVP;
-        g.epi.act = s->act;
-        g.epi.out_hi = s->gs[h - 1].hi;
-        g.epi.out_lo = s->gs[h - 1].lo;
-        g.epi.ld = s->gs[h - 1].ld;
-        g.epi.mask_hi = s->acts[h].hi;
-        g.epi.mask_lo = s->acts[h].lo;
-        g.epi.mask_ld = s->acts[h].ld;
-        if (tanh_) {
-          g.epi.P = s->P[h - 1];
-          g.epi.P_ld = s->gs[h - 1].ld;
-          g.epi.dz = s->dz[h - 1];
-          g.epi.dz_ld = s->da[h - 1].ld;
-        }
+        hvp_epi(s, g.epi, h);
+        bound_add(g.epi.bound, (float)s->dims[h + 1], s->gs[h].sc, s->w_sc + h);
+        bound_add(g.epi.bound, (float)s->dims[h + 1], s->G[h].sc, s->v_sc + h);
         g.skip = skip;
         gemm(ctx, g);
       }
@@ -626,13 +620,9 @@ void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* vhi, const float* vlo, float*
 void mlp_loss(cv_ctx* ctx, cv_snap* s, const float* logits, int write_state, double* loss_out) {
   const int nblk = 64;
   k_loss_rows<<<nblk, 256, 0, ctx->stream>>>(logits, s->bl, s->c, s->loss, s->y_i, s->y_f, s->probs, s->gout,
-                                             1.0f / (float)s->bg, ctx->red_ws, write_state);
-  if (write_state && s->tc_out) {
-    k_pad_split<<<grid_for((int64_t)s->bl * s->cp), 256, 0, ctx->stream>>>(nullptr, nullptr, s->gout, s->c, s->bl,
-                                                                           s->c, s->cp, s->gout_hi, s->gout_lo,
-                                                                           nullptr);
-    ctx->launches++;
-  }
+                                             1.0f / (float)s->bg, ctx->red_ws, write_state, &s->gout_sc->amax);
+  if (write_state && s->tc_out)
+    split_mat(ctx, s->gout, s->c, s->bl, s->c, s->gout_hi, s->gout_lo, s->ldb, 1, s->gout_sc, 1, nullptr);
   const double scale = 1.0 / (double)s->bg;
   k_finalize_sum<<<1, 32, 0, ctx->stream>>>(ctx->red_ws, nblk, ctx->nccl ? 1.0 : scale, loss_out);
   ctx->launches += 2;
@@ -645,46 +635,16 @@ void mlp_loss(cv_ctx* ctx, cv_snap* s, const float* logits, int write_state, dou
 // Loss at another parameter point on the snapshot batch (curvature.py:82-84).
 void mlp_loss_at(cv_ctx* ctx, cv_snap* s, const float* w, double* loss_out) {
   // split w into the product scratch (v_hi / v_lo) and run a forward pass on the
-  // tangent scratch buffers (da[]) -- no product is in flight concurrently.
-  split_vec(ctx, w, s->v_hi, s->v_lo, s->d, nullptr);
+  // backward scratch buffers (gs[]) -- no product is in flight concurrently.
+  split_input(ctx, s, w, nullptr);
   const int L = s->L;
   const SplitBuf* in = &s->acts[0];
   for (int l = 0; l < L - 1; ++l) {
-    mlp_forward_layer(ctx, s, l, *in, s->v_hi, s->v_lo, s->gs[l]);
-    // gs[l] needs the ones column for the next layer's bias
-    k_set_col<<<grid_for(s->bl), 256, 0, ctx->stream>>>(s->gs[l].hi, s->gs[l].lo, s->gs[l].ld, s->bl,
-                                                          s->dims[l + 1], 1.f);
-    ctx->launches++;
+    mlp_forward_layer(ctx, s, l, *in, s->v_hi, s->v_lo, s->v_sc, s->gs[l]);
     in = &s->gs[l];
   }
-  mlp_output_layer(ctx, s, *in, s->v_hi, s->v_lo, s->U);
+  mlp_output_layer(ctx, s, *in, s->v_hi, s->v_lo, s->v_sc, s->U);
   mlp_loss(ctx, s, s->U, 0, loss_out);
-}
-
-void set_col_value(cv_ctx* ctx, const SplitBuf& b, int rows, int col, float v) {
-  k_set_col<<<grid_for(rows), 256, 0, ctx->stream>>>(b.hi, b.lo, b.ld, rows, col, v);
-  ctx->launches++;
-}
-
-void set_ones_col(cv_ctx* ctx, const SplitBuf& b, int rows, int col) { set_col_value(ctx, b, rows, col, 1.f); }
-
-__global__ void k_gather_rows(const float* hi, const float* lo, int64_t ld, int rows, int cols, float* out) {
-  const int64_t total = (int64_t)rows * cols;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / cols, c = i - r * cols;
-    out[i] = hi[r * ld + c] + lo[r * ld + c];
-  }
-}
-
-void gather_rows(cv_ctx* ctx, const SplitBuf& b, int rows, int cols, float* out) {
-  k_gather_rows<<<grid_for((int64_t)rows * cols), 256, 0, ctx->stream>>>(b.hi, b.lo, b.ld, rows, cols, out);
-  ctx->launches++;
-}
-
-void split_rows(cv_ctx* ctx, const float* src, int64_t lds, int rows, int cols, const SplitBuf& dst, int ones) {
-  k_split_rows<<<grid_for((int64_t)rows * (cols + 1)), 256, 0, ctx->stream>>>(src, lds, rows, cols, dst.hi, dst.lo,
-                                                                               dst.ld, ones);
-  ctx->launches++;
 }
 
 }  // namespace cv

@@ -118,18 +118,6 @@ __global__ void k_hz_roots(const float* logits, const int64_t* yi, const float* 
   }
 }
 
-// D0 rows (i, a) = seeds[i, a, :], split into an m x ld(c) buffer
-__global__ void k_seed_rows(const float* seeds, int m, int c, float* hi, float* lo, int64_t ld) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)m * c; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e / c;
-    const int j = (int)(e - r * c);
-    float h, l;
-    split2(seeds[e], h, l);
-    hi[r * ld + j] = h;
-    lo[r * ld + j] = l;
-  }
-}
-
 // cot[i, a] = sum_j seeds[i, a, j] u[i, j]  (curvature.py:58-59)
 __global__ void k_seed_apply(const float* seeds, const float* u, int b, int c, float* out) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -168,6 +156,24 @@ void row_rhs(cv_ctx* ctx, cv_snap* s, float* rhs) {
   cudaMemcpyAsync(rhs, s->rhs, sizeof(float) * s->bl * s->c, cudaMemcpyDeviceToDevice, ctx->stream);
 }
 
+static Operand sop(const SplitBuf& b, bool trans) {
+  Operand o;
+  o.hi = b.hi;
+  o.lo = b.lo;
+  o.si = trans ? 1 : b.ld;
+  o.sj = trans ? b.ld : 1;
+  o.sc = b.sc;
+  return o;
+}
+
+static Operand f32op(const float* p, int64_t si, int64_t sj) {
+  Operand o;
+  o.f32 = p;
+  o.si = si;
+  o.sj = sj;
+  return o;
+}
+
 static void ensure_gram(cv_ctx* ctx, cv_snap* s) {
   if (s->row_state & 2) return;
   ensure_seeds(ctx, s);
@@ -181,12 +187,13 @@ static void ensure_gram(cv_ctx* ctx, cv_snap* s) {
   const int64_t ldD = ld_for(wmax);
   SplitBuf D[2];
   for (int k = 0; k < 2; ++k) {
-    D[k].hi = snap_alloc(s, m * ldD);
-    D[k].lo = snap_alloc(s, m * ldD);
+    D[k].hi = (__half*)snap_alloc(s, (m * ldD + 1) / 2);
+    D[k].lo = (__half*)snap_alloc(s, (m * ldD + 1) / 2);
     D[k].ld = ldD;
+    D[k].sc = s->scratch_sc + k;
   }
-  k_seed_rows<<<1024, 256, 0, ctx->stream>>>(s->seeds, (int)m, c, D[0].hi, D[0].lo, ldD);
-  ctx->launches++;
+  // D0 rows (i, a) = seeds[i, a, :]  (exact amax, two passes)
+  split_mat(ctx, s->seeds, c, (int)m, c, D[0].hi, D[0].lo, ldD, 0, D[0].sc, 0, nullptr);
   int cur = 0;
   for (int l = L - 1; l >= 0; --l) {
     const int nout = s->dims[l + 1];
@@ -195,8 +202,7 @@ static void ensure_gram(cv_ctx* ctx, cv_snap* s) {
     g.M = b;
     g.N = b;
     g.nseg = 1;
-    g.seg[0] = GemmSeg{Operand{s->acts[l].hi, s->acts[l].lo, s->acts[l].ld, 1},
-                       Operand{s->acts[l].hi, s->acts[l].lo, 1, s->acts[l].ld}, s->dims[l] + 1};
+    g.seg[0] = GemmSeg{sop(s->acts[l], false), sop(s->acts[l], true), s->dims[l] + 1};
     g.epi.mode = EPI_STORE;
     g.epi.out = sa;
     g.epi.ld = b;
@@ -206,7 +212,7 @@ static void ensure_gram(cv_ctx* ctx, cv_snap* s) {
     h.M = (int)m;
     h.N = (int)m;
     h.nseg = 1;
-    h.seg[0] = GemmSeg{Operand{D[cur].hi, D[cur].lo, ldD, 1}, Operand{D[cur].hi, D[cur].lo, 1, ldD}, nout};
+    h.seg[0] = GemmSeg{sop(D[cur], false), sop(D[cur], true), nout};
     h.epi.mode = EPI_GRAM;
     h.epi.out = s->gram;
     h.epi.ld = m;
@@ -217,21 +223,33 @@ static void ensure_gram(cv_ctx* ctx, cv_snap* s) {
     gemm(ctx, h);
     if (l > 0) {
       // D <- (D W_l^T) * act'(a_l) broadcast over the k rows of each example
+      cudaMemsetAsync(D[cur ^ 1].sc, 0, sizeof(Scale), ctx->stream);
       GemmArgs q;
       q.M = (int)m;
       q.N = s->dims[l];
       q.nseg = 1;
-      q.seg[0] = GemmSeg{Operand{D[cur].hi, D[cur].lo, ldD, 1},
-                         Operand{s->w_hi + s->off[l], s->w_lo + s->off[l], 1, nout}, nout};
+      Operand wt;
+      wt.hi = s->w_hi + s->off[l];
+      wt.lo = s->w_lo + s->off[l];
+      wt.si = 1;
+      wt.sj = nout;
+      wt.sc = s->w_sc + l;
+      q.seg[0] = GemmSeg{sop(D[cur], false), wt, nout};
       q.epi.mode = EPI_SPLIT_MASK;
       q.epi.act = s->act;
       q.epi.out_hi = D[cur ^ 1].hi;
       q.epi.out_lo = D[cur ^ 1].lo;
+      q.epi.out_sc = D[cur ^ 1].sc;
       q.epi.ld = ldD;
       q.epi.mask_hi = s->acts[l].hi;
       q.epi.mask_lo = s->acts[l].lo;
+      q.epi.mask_sc = s->acts[l].sc;
       q.epi.mask_ld = s->acts[l].ld;
       q.epi.mask_div = c;
+      q.epi.bound.n = 1;
+      q.epi.bound.k[0] = (float)nout;
+      q.epi.bound.x[0] = &D[cur].sc->amax;
+      q.epi.bound.y[0] = &(s->w_sc + l)->amax;
       gemm(ctx, q);
       cur ^= 1;
     }
@@ -409,7 +427,7 @@ int row_solve_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, flo
     p.M = rest;
     p.N = nb;
     p.nseg = 1;
-    p.seg[0] = GemmSeg{Operand{A21, nullptr, m, 1}, Operand{dblk, nullptr, 1, nb}, nb};
+    p.seg[0] = GemmSeg{f32op(A21, m, 1), f32op(dblk, 1, nb), nb};
     p.epi.mode = EPI_STORE;
     p.epi.out = A21;
     p.epi.ld = m;
@@ -419,7 +437,7 @@ int row_solve_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, flo
     u.M = rest;
     u.N = rest;
     u.nseg = 1;
-    u.seg[0] = GemmSeg{Operand{A21, nullptr, m, 1}, Operand{A21, nullptr, 1, m}, nb};
+    u.seg[0] = GemmSeg{f32op(A21, m, 1), f32op(A21, 1, m), nb};
     u.epi.mode = EPI_ACCUM;
     u.epi.alpha = -1.f;
     u.epi.out = s->chol + (int64_t)(j0 + nb) * m + (j0 + nb);

@@ -1,7 +1,8 @@
 // Output-layer kernels (c = output width <= 32).  All three are HBM-bound streams
 // over one b x n activation/tangent matrix, so they are written for bandwidth:
-// 128-bit loads/stores, the tiny c-wide operand staged in shared memory, several
-// rows or columns per thread in flight, deterministic fixed-order reductions.
+// wide loads/stores, the tiny c-wide operand staged in shared memory or
+// registers, several rows or columns per thread in flight, deterministic
+// fixed-order reductions.  Activations arrive as scaled fp16 pairs (common.cuh).
 //   skinny_rows : last-layer JVP + fused H_z (models.py:243-255, 199-204)
 //   skinny_dw   : last-layer [gW; gb] = A^T U (models.py:280-281)
 //   skinny_dx   : G = (U W^T) * act'(a) (models.py:282-284, 378-381)
@@ -12,10 +13,22 @@
 
 namespace cv {
 
-CV_DEV float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+union H4 {
+  uint2 u;
+  __half h[4];
+};
+
+// 4 consecutive split elements (8-byte aligned) -> fp32
+CV_DEV void ld_join4(const __half* hi, const __half* lo, float inv, float (&x)[4]) {
+  H4 a, b;
+  a.u = *reinterpret_cast<const uint2*>(hi);
+  b.u = *reinterpret_cast<const uint2*>(lo);
+#pragma unroll
+  for (int t = 0; t < 4; ++t) x[t] = (__half2float(a.h[t]) + __half2float(b.h[t])) * inv;
+}
 
 // ---------------------------------------------------------------------------
-// rows: one warp per RPW rows, lanes stride K in float4 steps, B^T chunk in smem
+// rows: one warp per RPW rows, lanes stride K in 4-element steps, B^T chunk in smem
 // ---------------------------------------------------------------------------
 template <int CM, int RPW>
 __global__ void __launch_bounds__(256) k_rows(SkinnyRowsArgs a) {
@@ -31,6 +44,7 @@ __global__ void __launch_bounds__(256) k_rows(SkinnyRowsArgs a) {
     for (int j = 0; j < CM; ++j) acc[r][j] = 0.f;
   for (int s = 0; s < a.nseg; ++s) {
     const SkinnySeg g = a.seg[s];
+    const float ainv = pow2f(-g.a_sc->e), binv = pow2f(-g.b_sc->e);
     for (int k0 = 0; k0 < g.K; k0 += RK) {
       const int kmax = min(RK, g.K - k0);
       __syncthreads();
@@ -39,7 +53,7 @@ __global__ void __launch_bounds__(256) k_rows(SkinnyRowsArgs a) {
         float v = 0.f;
         if (kk < kmax && j < a.c) {
           const int64_t idx = (int64_t)(k0 + kk) * g.ldb + j;
-          v = g.b_hi[idx] + g.b_lo[idx];
+          v = join16(g.b_hi[idx], g.b_lo[idx], binv);
         }
         Bt[j][kk] = v;
       }
@@ -50,14 +64,13 @@ __global__ void __launch_bounds__(256) k_rows(SkinnyRowsArgs a) {
         for (int r = 0; r < RPW; ++r) {
           const int m = m0 + r;
           if (m < a.rows) {
-            const float* ph = g.a_hi + (int64_t)m * g.lda + k0 + kk;
-            const float* pl = g.a_lo + (int64_t)m * g.lda + k0 + kk;
-            if (kk + 3 < kmax) {
-              const float4 h = ld4(ph), l = ld4(pl);
-              av[r][0] = h.x + l.x; av[r][1] = h.y + l.y; av[r][2] = h.z + l.z; av[r][3] = h.w + l.w;
+            const __half* ph = g.a_hi + (int64_t)m * g.lda + k0 + kk;
+            const __half* pl = g.a_lo + (int64_t)m * g.lda + k0 + kk;
+            if (kk + 3 < kmax && al8(ph) && al8(pl)) {
+              ld_join4(ph, pl, ainv, av[r]);
             } else {
 #pragma unroll
-              for (int t = 0; t < 4; ++t) av[r][t] = kk + t < kmax ? ph[t] + pl[t] : 0.f;
+              for (int t = 0; t < 4; ++t) av[r][t] = kk + t < kmax ? join16(ph[t], pl[t], ainv) : 0.f;
             }
           } else {
 #pragma unroll
@@ -74,6 +87,7 @@ __global__ void __launch_bounds__(256) k_rows(SkinnyRowsArgs a) {
       }
     }
   }
+  float amax = 0.f;
 #pragma unroll
   for (int r = 0; r < RPW; ++r) {
 #pragma unroll
@@ -84,8 +98,9 @@ __global__ void __launch_bounds__(256) k_rows(SkinnyRowsArgs a) {
 #pragma unroll
     for (int j = 0; j < CM; ++j)
       if (j == lane) t = acc[r][j];
+    float o;
     if (a.post == POST_LOGITS || a.loss == CV_LOSS_MSE) {
-      if (lane < a.c) a.out[(int64_t)m * a.c + lane] = a.post == POST_LOGITS ? t : t * a.scale;
+      o = a.post == POST_LOGITS ? t : t * a.scale;
     } else {
       // H_z T = p*T - p*(p.T)  (softmax-CE, per example)
       const float* p = a.probs + (int64_t)m * a.c;
@@ -93,12 +108,16 @@ __global__ void __launch_bounds__(256) k_rows(SkinnyRowsArgs a) {
 #pragma unroll
       for (int j = 0; j < CM; ++j)
         if (j < a.c) pt = fmaf(p[j], acc[r][j], pt);
-      if (lane < a.c) {
-        const float pj = p[lane];
-        a.out[(int64_t)m * a.c + lane] = (pj * t - pj * pt) * a.scale;
-      }
+      const float pj = lane < a.c ? p[lane] : 0.f;
+      o = (pj * t - pj * pt) * a.scale;
+    }
+    if (lane < a.c) {
+      a.out[(int64_t)m * a.c + lane] = o;
+      amax = fmaxf(amax, fabsf(o));
     }
   }
+  amax = warp_max_f(amax);
+  if (lane == 0 && a.out_amax) atomic_amax(a.out_amax, amax);
 }
 
 void skinny_rows(cv_ctx* ctx, const SkinnyRowsArgs& a) {
@@ -114,9 +133,9 @@ void skinny_rows(cv_ctx* ctx, const SkinnyRowsArgs& a) {
 
 // ---------------------------------------------------------------------------
 // dx: thread = 4 adjacent columns with their W^T entries held in registers; a
-// warp covers 128 contiguous columns of a row (512-byte coalesced accesses); the
-// block walks 32-row tiles (U rows staged in smem) and issues the R activation
-// loads of a row group before any of its stores.
+// warp covers 128 contiguous columns of a row (coalesced accesses); the block
+// walks 32-row tiles (U rows staged in smem) and issues the R activation loads of
+// a row group before any of its stores.
 // ---------------------------------------------------------------------------
 template <int C, int NSEG, bool TANH>
 __global__ void __launch_bounds__(128) k_dx(SkinnyDxArgs a) {
@@ -129,21 +148,26 @@ __global__ void __launch_bounds__(128) k_dx(SkinnyDxArgs a) {
   const bool colok = nb < a.n;
   float w[NSEG][C][4];
 #pragma unroll
-  for (int s = 0; s < NSEG; ++s)
+  for (int s = 0; s < NSEG; ++s) {
+    const float winv = pow2f(-a.w_sc[s]->e);
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const bool ok = nb + t < a.n;
       const int64_t base = (int64_t)(nb + t) * a.c;
 #pragma unroll
-      for (int j = 0; j < C; ++j) w[s][j][t] = (ok && j < a.c) ? a.w_hi[s][base + j] + a.w_lo[s][base + j] : 0.f;
+      for (int j = 0; j < C; ++j)
+        w[s][j][t] = (ok && j < a.c) ? join16(a.w_hi[s][base + j], a.w_lo[s][base + j], winv) : 0.f;
     }
+  }
   const Epilogue& e = a.epi;
-  constexpr bool tanh_ = TANH;
-  const bool fast = (e.mode == EPI_SPLIT_MASK || (e.mode == EPI_HVP && !tanh_)) && e.mask_div == 1 &&
-                    al16(e.out_hi) && al16(e.out_lo) && al16(e.mask_hi) && (!tanh_ || al16(e.mask_lo)) &&
+  const EpiRt rt = epi_prepare(e);
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) epi_publish(e, rt);
+  const bool fast = (e.mode == EPI_SPLIT_MASK || (e.mode == EPI_HVP && !TANH)) && e.mask_div == 1 &&
+                    al8(e.out_hi) && al8(e.out_lo) && al8(e.mask_hi) && (!TANH || al8(e.mask_lo)) &&
                     (e.ld & 3) == 0 && (e.mask_ld & 3) == 0 && (!e.raw || (al16(e.raw) && (e.raw_ld & 3) == 0));
   const bool full = nb + 4 <= a.n;
   const int tiles = (a.rows + RT - 1) / RT;
+  float amax = 0.f, ramax = 0.f;
   for (int tile = blockIdx.y; tile < tiles; tile += gridDim.y) {
     const int m0 = tile * RT;
     __syncthreads();
@@ -153,15 +177,15 @@ __global__ void __launch_bounds__(128) k_dx(SkinnyDxArgs a) {
     }
     __syncthreads();
     if (!colok) continue;
-    float4 mh[R], ml[TANH ? R : 1];
+    uint2 mh[R], ml[TANH ? R : 1];
     if (fast) {
 #pragma unroll
       for (int i = 0; i < R; ++i) {
         const int m = m0 + warp + 4 * i;
         if (m < a.rows && full) {
           const int64_t mo = (int64_t)m * e.mask_ld + nb;
-          mh[i] = ld4(e.mask_hi + mo);
-          if constexpr (TANH) ml[i] = ld4(e.mask_lo + mo);
+          mh[i] = *reinterpret_cast<const uint2*>(e.mask_hi + mo);
+          if constexpr (TANH) ml[i] = *reinterpret_cast<const uint2*>(e.mask_lo + mo);
         }
       }
     }
@@ -181,22 +205,41 @@ __global__ void __launch_bounds__(128) k_dx(SkinnyDxArgs a) {
           v[3] = fmaf(u, w[s][j][3], v[3]);
         }
       if (fast && full) {
-        float av[4] = {mh[i].x, mh[i].y, mh[i].z, mh[i].w};
-        if constexpr (TANH) { av[0] += ml[i].x; av[1] += ml[i].y; av[2] += ml[i].z; av[3] += ml[i].w; }
-        if (e.raw) *reinterpret_cast<float4*>(e.raw + (int64_t)m * e.raw_ld + nb) = make_float4(v[0], v[1], v[2], v[3]);
-        float h[4], l[4];
+        H4 hh;
+        hh.u = mh[i];
+        float av[4];
+        if constexpr (TANH) {
+          H4 ll;
+          ll.u = ml[i];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) split2(v[t] * act_deriv(TANH ? CV_ACT_TANH : CV_ACT_RELU, av[t]), h[t], l[t]);
+          for (int t = 0; t < 4; ++t) av[t] = (__half2float(hh.h[t]) + __half2float(ll.h[t])) * rt.mask_inv;
+        } else {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) av[t] = __half2float(hh.h[t]);
+        }
+        if (e.raw) {
+          *reinterpret_cast<float4*>(e.raw + (int64_t)m * e.raw_ld + nb) = make_float4(v[0], v[1], v[2], v[3]);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) ramax = fmaxf(ramax, fabsf(v[t]));
+        }
+        H4 oh, ol;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float x = v[t] * act_deriv(TANH ? CV_ACT_TANH : CV_ACT_RELU, av[t]);
+          amax = fmaxf(amax, fabsf(x));
+          split16(x, rt.out_s, oh.h[t], ol.h[t]);
+        }
         const int64_t o = (int64_t)m * e.ld + nb;
-        *reinterpret_cast<float4*>(e.out_hi + o) = make_float4(h[0], h[1], h[2], h[3]);
-        *reinterpret_cast<float4*>(e.out_lo + o) = make_float4(l[0], l[1], l[2], l[3]);
-      } else if (!(full && epi_applyV<4>(e, m, nb, v))) {
+        *reinterpret_cast<uint2*>(e.out_hi + o) = oh.u;
+        *reinterpret_cast<uint2*>(e.out_lo + o) = ol.u;
+      } else {
 #pragma unroll
         for (int t = 0; t < 4; ++t)
-          if (nb + t < a.n) epi_apply(e, m, nb + t, v[t]);
+          if (nb + t < a.n) epi_apply(e, rt, m, nb + t, v[t], amax, ramax);
       }
     }
   }
+  epi_flush_amax(e, amax, ramax);
 }
 
 template <int C, int NSEG>
@@ -236,9 +279,11 @@ __global__ void __launch_bounds__(128) k_dw_partial(SkinnyDwArgs a) {
     for (int j = 0; j < CM; ++j) acc[t][j] = 0.f;
   const bool full = m + 3 < a.M;
   for (int s = 0; s < a.nseg; ++s) {
-    const float* ah = a.a_hi[s];
-    const float* al = a.a_lo[s];
+    const __half* ah = a.a_hi[s];
+    const __half* al = a.a_lo[s];
     const int64_t lda = a.lda[s];
+    const float inv = pow2f(-a.a_sc[s]->e);
+    const bool vec = full && (lda & 3) == 0 && al8(ah) && al8(al);
     for (int k0 = kb; k0 < ke; k0 += KT) {
       const int kn = min(KT, ke - k0);
       __syncthreads();
@@ -252,12 +297,11 @@ __global__ void __launch_bounds__(128) k_dw_partial(SkinnyDwArgs a) {
       for (int kk = 0; kk < kn; ++kk) {
         const int64_t o = (int64_t)(k0 + kk) * lda + m;
         float x[4];
-        if (full) {
-          const float4 h = ld4(ah + o), l = ld4(al + o);
-          x[0] = h.x + l.x; x[1] = h.y + l.y; x[2] = h.z + l.z; x[3] = h.w + l.w;
+        if (vec) {
+          ld_join4(ah + o, al + o, inv, x);
         } else {
 #pragma unroll
-          for (int t = 0; t < 4; ++t) x[t] = m + t < a.M ? ah[o + t] + al[o + t] : 0.f;
+          for (int t = 0; t < 4; ++t) x[t] = m + t < a.M ? join16(ah[o + t], al[o + t], inv) : 0.f;
         }
 #pragma unroll
         for (int j = 0; j < CM; ++j) {

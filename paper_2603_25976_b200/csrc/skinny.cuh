@@ -5,8 +5,8 @@
 namespace cv {
 
 struct SkinnySeg {
-  const float* a_hi; const float* a_lo; int64_t lda;  // A: rows x K row-major (split)
-  const float* b_hi; const float* b_lo; int64_t ldb;  // B: K x c row-major (split)
+  const __half* a_hi; const __half* a_lo; int64_t lda; const Scale* a_sc;  // A: rows x K row-major (split)
+  const __half* b_hi; const __half* b_lo; int64_t ldb; const Scale* b_sc;  // B: K x c row-major (split)
   int K;
 };
 
@@ -21,6 +21,7 @@ struct SkinnyRowsArgs {
   const float* probs;     // rows x c (POST_HZ, ce)
   float scale;            // POST_HZ: 1/b_global
   float* out;             // rows x c
+  float* out_amax;        // optional: max |out|
   const int* skip;
 };
 
@@ -28,15 +29,15 @@ struct SkinnyRowsArgs {
 struct SkinnyDxArgs {
   int rows, n, c, nseg;
   const float* U[2];
-  const float* w_hi[2]; const float* w_lo[2];
-  Epilogue epi;
+  const __half* w_hi[2]; const __half* w_lo[2]; const Scale* w_sc[2];
+  Epilogue epi;           // split output; epi.bound covers c * amax(U_s) * amax(W_s)
   const int* skip;
 };
 
 // out[m, j] = sum_s sum_k A_s[k, m] U_s[k, j]   (m < M = n + 1, ld c)
 struct SkinnyDwArgs {
   int rows, M, c, nseg, ksplit;
-  const float* a_hi[2]; const float* a_lo[2]; int64_t lda[2];
+  const __half* a_hi[2]; const __half* a_lo[2]; int64_t lda[2]; const Scale* a_sc[2];
   const float* U[2];
   float* partial;   // ksplit x M x c
   float* out;       // M x c

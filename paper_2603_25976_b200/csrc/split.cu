@@ -1,0 +1,242 @@
+// Scaled fp16 splits (common.cuh) of fp32 inputs, with the exact amax.
+//
+// Each split is two launches: an amax pass whose last block to finish reduces
+// the per-block maxima and publishes {e, amax} into the tensor's Scale slot
+// (max is order independent, so the result is deterministic), then the split
+// pass.  Used for everything whose scale cannot come from a GEMM bound: the
+// product inputs (CG directions, probes, loss_at points), the input batch, the
+// weights, and the c-wide cotangents of the output layer.
+#include "common.cuh"
+#include "internal.h"
+
+namespace cv {
+
+constexpr int SP_NB = 2 * 148, SP_NT = 256, SP_MAXL = 16;
+
+struct OffTab {
+  int64_t off[SP_MAXL + 1];
+  int L;
+};
+
+CV_DEV float block_max(float v, float* sh) {
+  v = warp_max_f(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  float r = 0.f;
+  if (threadIdx.x < 32) {
+    r = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.f;
+    r = warp_max_f(r);
+  }
+  return r;  // valid in thread 0
+}
+
+// last block of the grid? (after every block wrote its partials)
+CV_DEV bool last_block(unsigned* counter) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  return last;
+}
+
+// per-layer amax of a flat vector; the last block publishes sc[l] and zeroes zero_sc
+__global__ void __launch_bounds__(SP_NT) k_flat_amax(const float* __restrict__ x, OffTab t, float* part,
+                                                     unsigned* counter, Scale* sc, Scale* zero_sc, int n_zero,
+                                                     const int* skip) {
+  if (skip_if(skip)) return;
+  __shared__ float sh[SP_NT / 32];
+  for (int l = 0; l < t.L; ++l) {
+    float m = 0.f;
+    for (int64_t i = t.off[l] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < t.off[l + 1];
+         i += (int64_t)gridDim.x * blockDim.x)
+      m = fmaxf(m, fabsf(x[i]));
+    m = block_max(m, sh);
+    if (threadIdx.x == 0) part[blockIdx.x * SP_MAXL + l] = m;
+  }
+  if (!last_block(counter)) return;
+  for (int l = 0; l < t.L; ++l) {
+    float m = 0.f;
+    for (int b = threadIdx.x; b < gridDim.x; b += blockDim.x) m = fmaxf(m, part[b * SP_MAXL + l]);
+    m = block_max(m, sh);
+    if (threadIdx.x == 0) {
+      sc[l].amax = m;
+      sc[l].e = exp_for_bound(m);
+    }
+  }
+  for (int i = threadIdx.x; i < n_zero; i += blockDim.x) {
+    zero_sc[i].e = 0;
+    zero_sc[i].amax = 0.f;
+  }
+  if (threadIdx.x == 0) *counter = 0;
+}
+
+__global__ void __launch_bounds__(SP_NT) k_flat_split(const float* __restrict__ x, OffTab t, const Scale* sc,
+                                                      __half* __restrict__ hi, __half* __restrict__ lo,
+                                                      const int* skip) {
+  if (skip_if(skip)) return;
+  for (int l = 0; l < t.L; ++l) {
+    const float s = pow2f(sc[l].e);
+    const int64_t b = t.off[l], e = t.off[l + 1];
+    int64_t b8 = (b + 7) & ~(int64_t)7;  // 8-aligned body (16-byte half stores)
+    if (b8 > e) b8 = e;
+    const int64_t e8 = b8 + ((e - b8) & ~(int64_t)7);
+    for (int64_t i = b + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (b8 < e ? b8 : e);
+         i += (int64_t)gridDim.x * blockDim.x)
+      split16(x[i], s, hi[i], lo[i]);
+    for (int64_t q = b8 / 8 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < e8 / 8;
+         q += (int64_t)gridDim.x * blockDim.x) {
+      const float4 a = *reinterpret_cast<const float4*>(x + 8 * q);
+      const float4 c = *reinterpret_cast<const float4*>(x + 8 * q + 4);
+      union { uint4 u; __half h[8]; } H, Lo;
+      const float v[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) split16(v[k], s, H.h[k], Lo.h[k]);
+      *reinterpret_cast<uint4*>(hi + 8 * q) = H.u;
+      *reinterpret_cast<uint4*>(lo + 8 * q) = Lo.u;
+    }
+    for (int64_t i = (e8 > b8 ? e8 : b8) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e;
+         i += (int64_t)gridDim.x * blockDim.x)
+      if (i >= b8) split16(x[i], s, hi[i], lo[i]);
+  }
+}
+
+static unsigned* counter_of(cv_ctx* ctx) { return ctx->amax_counter; }
+static float* part_of(cv_ctx* ctx) { return ctx->amax_ws; }
+
+void split_flat(cv_ctx* ctx, const float* x, int64_t d, const std::vector<int64_t>& off, __half* hi, __half* lo,
+                Scale* sc, Scale* zero_sc, int n_zero, const int* skip) {
+  const int L = (int)off.size();
+  for (int l0 = 0; l0 < L; l0 += SP_MAXL) {
+    OffTab t;
+    t.L = L - l0 < SP_MAXL ? L - l0 : SP_MAXL;
+    for (int l = 0; l <= t.L; ++l) t.off[l] = l0 + l < L ? off[l0 + l] : d;
+    const bool last = l0 + t.L >= L;
+    k_flat_amax<<<SP_NB, SP_NT, 0, ctx->stream>>>(x, t, part_of(ctx), counter_of(ctx), sc + l0,
+                                                  last ? zero_sc : nullptr, last ? n_zero : 0, skip);
+    k_flat_split<<<SP_NB, SP_NT, 0, ctx->stream>>>(x, t, sc + l0, hi, lo, skip);
+    ctx->launches += 2;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 2-D splits: [rows x cols] fp32 (ld lds) -> split (ld ldd), optionally
+// transposed (dst[j, i]) and with a ones column at `cols` (augmented activations)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(SP_NT) k_mat_amax(const float* __restrict__ x, int64_t lds, int rows, int cols,
+                                                    float floor_, float* part, unsigned* counter, Scale* sc,
+                                                    const int* skip) {
+  if (skip_if(skip)) return;
+  __shared__ float sh[SP_NT / 32];
+  const int64_t total = (int64_t)rows * cols;
+  float m = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i - r * cols;
+    m = fmaxf(m, fabsf(x[r * lds + c]));
+  }
+  m = block_max(m, sh);
+  if (threadIdx.x == 0) part[blockIdx.x * SP_MAXL] = m;
+  if (!last_block(counter)) return;
+  m = 0.f;
+  for (int b = threadIdx.x; b < gridDim.x; b += blockDim.x) m = fmaxf(m, part[b * SP_MAXL]);
+  m = block_max(m, sh);
+  if (threadIdx.x == 0) {
+    m = fmaxf(m, floor_);
+    sc->amax = m;
+    sc->e = exp_for_bound(m);
+    *counter = 0;
+  }
+}
+
+// publish e from an amax accumulated by the producer
+__global__ void k_scale_from_amax(Scale* sc, float floor_, const int* skip) {
+  if (skip_if(skip)) return;
+  const float m = fmaxf(sc->amax, floor_);
+  sc->amax = m;
+  sc->e = exp_for_bound(m);
+}
+
+__global__ void __launch_bounds__(SP_NT) k_mat_split(const float* __restrict__ x, int64_t lds, int rows, int cols,
+                                                     int out_rows, int out_cols, int trans, int ones,
+                                                     const Scale* sc, __half* __restrict__ hi,
+                                                     __half* __restrict__ lo, int64_t ldd, const int* skip) {
+  if (skip_if(skip)) return;
+  const float s = pow2f(sc->e);
+  // destination index space: out_rows x out_cols (padding written as zero)
+  const int64_t total = (int64_t)out_rows * out_cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / out_cols, c = i - r * out_cols;  // destination (r, c)
+    const int64_t sr = trans ? c : r, sc_ = trans ? r : c;  // source (row, col)
+    float v = 0.f;
+    if (sr < rows && sc_ < cols) v = x[sr * lds + sc_];
+    else if (ones && sr < rows && sc_ == cols) v = 1.f;
+    split16(v, s, hi[r * ldd + c], lo[r * ldd + c]);
+  }
+}
+
+static int grid_for(int64_t n) {
+  int64_t g = (n + SP_NT - 1) / SP_NT;
+  return (int)(g < 1 ? 1 : (g > 148 * 8 ? 148 * 8 : g));
+}
+
+void amax_into(cv_ctx* ctx, const float* x, int64_t n, Scale* slot) {
+  k_mat_amax<<<SP_NB, SP_NT, 0, ctx->stream>>>(x, n, 1, (int)n, 0.f, part_of(ctx), counter_of(ctx), slot, nullptr);
+  ctx->launches++;
+}
+
+void split_rows(cv_ctx* ctx, const float* src, int64_t lds, int rows, int cols, const SplitBuf& dst, int ones) {
+  k_mat_amax<<<SP_NB, SP_NT, 0, ctx->stream>>>(src, lds, rows, cols, ones ? 1.f : 0.f, part_of(ctx),
+                                               counter_of(ctx), dst.sc, nullptr);
+  const int oc = ones ? cols + 1 : cols;
+  k_mat_split<<<grid_for((int64_t)rows * oc), SP_NT, 0, ctx->stream>>>(src, lds, rows, cols, rows, oc, 0, ones, dst.sc,
+                                                                      dst.hi, dst.lo, dst.ld, nullptr);
+  ctx->launches += 2;
+}
+
+// src rows x cols -> (trans ? cols_pad x ldd : rows x ldd) split; amax_ready: sc->amax
+// already holds max|src| (accumulated by the producer)
+void split_mat(cv_ctx* ctx, const float* src, int64_t lds, int rows, int cols, __half* hi, __half* lo, int64_t ldd,
+               int trans, Scale* sc, int amax_ready, const int* skip) {
+  if (amax_ready) {
+    k_scale_from_amax<<<1, 1, 0, ctx->stream>>>(sc, 0.f, skip);
+  } else {
+    k_mat_amax<<<SP_NB, SP_NT, 0, ctx->stream>>>(src, lds, rows, cols, 0.f, part_of(ctx), counter_of(ctx), sc, skip);
+  }
+  const int orows = trans ? (int)((cols + 15) / 16 * 16) : rows;
+  const int ocols = trans ? rows : cols;
+  k_mat_split<<<grid_for((int64_t)orows * ocols), SP_NT, 0, ctx->stream>>>(src, lds, rows, cols, orows, ocols, trans, 0,
+                                                                          sc, hi, lo, ldd, skip);
+  ctx->launches += 2;
+}
+
+// column `col` of a split buffer := v (scaled by the buffer's exponent); amax covers |v|
+__global__ void k_set_col(__half* hi, __half* lo, int64_t ld, int rows, int col, float v, Scale* sc) {
+  const float s = pow2f(sc->e);
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
+    split16(v, s, hi[(int64_t)r * ld + col], lo[(int64_t)r * ld + col]);
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomic_amax(&sc->amax, fabsf(v));
+}
+
+void set_col_value(cv_ctx* ctx, const SplitBuf& b, int rows, int col, float v) {
+  k_set_col<<<grid_for(rows), SP_NT, 0, ctx->stream>>>(b.hi, b.lo, b.ld, rows, col, v, b.sc);
+  ctx->launches++;
+}
+
+__global__ void k_gather_rows(const __half* hi, const __half* lo, int64_t ld, int rows, int cols, const Scale* sc,
+                              float* out) {
+  const float inv = pow2f(-sc->e);
+  const int64_t total = (int64_t)rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i - r * cols;
+    out[i] = join16(hi[r * ld + c], lo[r * ld + c], inv);
+  }
+}
+
+void gather_rows(cv_ctx* ctx, const SplitBuf& b, int rows, int cols, float* out) {
+  k_gather_rows<<<grid_for((int64_t)rows * cols), SP_NT, 0, ctx->stream>>>(b.hi, b.lo, b.ld, rows, cols, b.sc, out);
+  ctx->launches++;
+}
+
+}  // namespace cv

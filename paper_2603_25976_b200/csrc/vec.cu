@@ -53,22 +53,12 @@ CV_DEV float rad(uint64_t seed, uint64_t counter, int64_t i) {
   return (splitmix(seed, counter + 1 + (uint64_t)i) >> 63) ? 1.f : -1.f;
 }
 
-__global__ void k_rademacher(uint64_t seed, uint64_t counter, int64_t n, float scale, float* out, float* hi,
-                             float* lo) {
-  GRID_STRIDE(i, n) {
-    const float z = rad(seed, counter, i) * scale;
-    if (out) out[i] = z;
-    if (hi) {
-      float h, l;
-      split2(z, h, l);
-      hi[i] = h;
-      lo[i] = l;
-    }
-  }
+__global__ void k_rademacher(uint64_t seed, uint64_t counter, int64_t n, float scale, float* out) {
+  GRID_STRIDE(i, n) out[i] = rad(seed, counter, i) * scale;
 }
 
-void rademacher(cv_ctx* ctx, uint64_t seed, uint64_t counter, int64_t n, float* out, float* hi, float* lo) {
-  k_rademacher<<<NB, NT, 0, ctx->stream>>>(seed, counter, n, 1.f, out, hi, lo);
+void rademacher(cv_ctx* ctx, uint64_t seed, uint64_t counter, int64_t n, float* out) {
+  k_rademacher<<<NB, NT, 0, ctx->stream>>>(seed, counter, n, 1.f, out);
   ctx->launches++;
 }
 
@@ -207,11 +197,12 @@ static float* snap_tmp(cv_snap* s, float** slot) {
 void hutchinson(cv_ctx* ctx, cv_snap* s, int kind, uint64_t seed, uint64_t counter, int n_probes, float* diag,
                 double* trace) {
   float* hz = snap_tmp(s, &s->tmp_d);
+  float* z = snap_tmp(s, &s->tmp_d2);
   MatvecFn mv = matvec_fn(kind);
   for (int j = 0; j < n_probes; ++j) {
     const uint64_t ctr = counter + (uint64_t)j * (uint64_t)s->d;
-    rademacher(ctx, seed, ctr, s->d, nullptr, s->v_hi, s->v_lo);
-    mv(ctx, s, s->v_hi, s->v_lo, hz, nullptr);
+    rademacher(ctx, seed, ctr, s->d, z);
+    mv(ctx, s, z, hz, nullptr);
     k_hutch_acc<<<NB, NT, 0, ctx->stream>>>(seed, ctr, hz, s->d, diag, j == 0, j == n_probes - 1,
                                             1.f / (float)n_probes, ctx->red_ws);
     ctx->launches++;
@@ -249,19 +240,9 @@ __global__ void k_pi_final(const double* ws, PiDev* st, double* norm_out) {
     *norm_out = nrm;
   }
 }
-__global__ void k_pi_next(const float* hv, const double* nrm, int64_t d, float* v, float* hi, float* lo,
-                          const int* skip) {
+__global__ void k_pi_next(const float* hv, const double* nrm, int64_t d, float* v, const int* skip) {
   if (skip_if(skip)) return;
-  const float inv = (float)(1.0 / *nrm);
-  GRID_STRIDE(i, d) {
-    const float x = (float)((double)hv[i] / *nrm);
-    (void)inv;
-    v[i] = x;
-    float h, l;
-    split2(x, h, l);
-    hi[i] = h;
-    lo[i] = l;
-  }
+  GRID_STRIDE(i, d) v[i] = (float)((double)hv[i] / *nrm);
 }
 __global__ void k_pi_out(const PiDev* st, double* out) { *out = st->result; }
 
@@ -272,14 +253,14 @@ void power_iter(cv_ctx* ctx, cv_snap* s, int kind, uint64_t seed, uint64_t count
   double* nrm = ctx->scal_ws + 4;
   k_pi_init<<<1, 1, 0, ctx->stream>>>(st);
   const float scale = (float)(1.0 / sqrt((double)s->d));
-  k_rademacher<<<NB, NT, 0, ctx->stream>>>(seed, counter, s->d, scale, v, s->v_hi, s->v_lo);
+  k_rademacher<<<NB, NT, 0, ctx->stream>>>(seed, counter, s->d, scale, v);
   ctx->launches += 2;
   MatvecFn mv = matvec_fn(kind);
   for (int it = 0; it < iters; ++it) {
-    mv(ctx, s, s->v_hi, s->v_lo, hv, &st->done);
+    mv(ctx, s, v, hv, &st->done);
     k_pi_reduce<<<NB, NT, 0, ctx->stream>>>(v, hv, s->d, ctx->red_ws, &st->done);
     k_pi_final<<<1, NT, 0, ctx->stream>>>(ctx->red_ws, st, nrm);
-    k_pi_next<<<NB, NT, 0, ctx->stream>>>(hv, nrm, s->d, v, s->v_hi, s->v_lo, &st->done);
+    k_pi_next<<<NB, NT, 0, ctx->stream>>>(hv, nrm, s->d, v, &st->done);
     ctx->launches += 3;
   }
   k_pi_out<<<1, 1, 0, ctx->stream>>>(st, eig);
@@ -318,14 +299,10 @@ __global__ void k_cg_init_final(const double* ws, CgDev* st) {
     st->gv_skip = st->done || !st->x0nz;
   }
 }
-// x = x0 (if any nonzero entry) else 0; split x for the warm-start product
-__global__ void k_cg_setup_x(const float* x0, const CgDev* st, int64_t d, float* x, float* hi, float* lo) {
+// x = x0 (if any nonzero entry) else 0
+__global__ void k_cg_setup_x(const float* x0, const CgDev* st, int64_t d, float* x) {
   const bool use = st->x0nz;
-  GRID_STRIDE(i, d) {
-    const float v = use ? x0[i] : 0.f;
-    x[i] = v;
-    if (use) { float h, l; split2(v, h, l); hi[i] = h; lo[i] = l; }
-  }
+  GRID_STRIDE(i, d) x[i] = use ? x0[i] : 0.f;
 }
 // r = g - (Ax + lam x) (warm) or g; partial ||r||^2
 __global__ void k_cg_r0(const float* g, const float* ax, const float* x, float lam, const CgDev* st, int64_t d,
@@ -353,17 +330,13 @@ __global__ void k_cg_r0_final(const double* ws, CgDev* st, double tol) {
 }
 // p = z = M^-1 r; rz = r.z
 __global__ void k_cg_p0(const float* r, const float* pre, float lam, float floor_, const CgDev* st, int64_t d,
-                        float* p, float* hi, float* lo, double* ws) {
+                        float* p, double* ws) {
   if (st->done) return;
   double t[1] = {0.0};
   GRID_STRIDE(i, d) {
     const float ri = r[i];
     const float z = minv_of(pre, i, lam, floor_) * ri;
     p[i] = z;
-    float h, l;
-    split2(z, h, l);
-    hi[i] = h;
-    lo[i] = l;
     t[0] += (double)ri * z;
   }
   write_partials<1>(ws, t);
@@ -471,18 +444,11 @@ __global__ void k_cg_update(float* x, float* r, const float* p, const float* ap,
   }
   write_partials<2>(ws, t);
 }
-// stabilising iteration: x += a p, split x for the explicit residual product
-__global__ void k_cg_xupdate(float* x, const float* p, const CgDev* st, int64_t d, float* hi, float* lo) {
+// stabilising iteration: x += a p (the explicit residual product follows)
+__global__ void k_cg_xupdate(float* x, const float* p, const CgDev* st, int64_t d) {
   if (st->done) return;
   const float a = (float)st->alpha;
-  GRID_STRIDE(i, d) {
-    const float v = x[i] + a * p[i];
-    x[i] = v;
-    float h, l;
-    split2(v, h, l);
-    hi[i] = h;
-    lo[i] = l;
-  }
+  GRID_STRIDE(i, d) x[i] += a * p[i];
 }
 // r = g - (Ax + lam x); partials ||r||^2, r.M^-1 r
 __global__ void k_cg_rstab(const float* g, const float* ax, const float* x, float* r, const float* pre, float lam,
@@ -516,9 +482,9 @@ __global__ void k_cg_r_final(const double* ws, CgDev* st, int k, int maxiter, in
     st->gv_skip = st->done;
   }
 }
-// p = M^-1 r + beta p, split p for the next product
+// p = M^-1 r + beta p
 __global__ void k_cg_pnext(const float* r, const float* pre, float lam, float floor_, const CgDev* st, int64_t d,
-                           float* p, float* hi, float* lo) {
+                           float* p) {
   if (st->done) return;
   const float beta = (float)st->alpha;
   const int64_t nq = d >> 2;
@@ -531,19 +497,9 @@ __global__ void k_cg_pnext(const float* r, const float* pre, float lam, float fl
     p4.z = minv_of(pre, i + 2, lam, floor_) * r4.z + beta * p4.z;
     p4.w = minv_of(pre, i + 3, lam, floor_) * r4.w + beta * p4.w;
     *reinterpret_cast<float4*>(p + i) = p4;
-    float4 h4, l4;
-    split2(p4.x, h4.x, l4.x); split2(p4.y, h4.y, l4.y); split2(p4.z, h4.z, l4.z); split2(p4.w, h4.w, l4.w);
-    *reinterpret_cast<float4*>(hi + i) = h4;
-    *reinterpret_cast<float4*>(lo + i) = l4;
   }
-  for (int64_t i = 4 * nq + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d; i += (int64_t)gridDim.x * blockDim.x) {
-    const float v = minv_of(pre, i, lam, floor_) * r[i] + beta * p[i];
-    p[i] = v;
-    float h, l;
-    split2(v, h, l);
-    hi[i] = h;
-    lo[i] = l;
-  }
+  for (int64_t i = 4 * nq + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = minv_of(pre, i, lam, floor_) * r[i] + beta * p[i];
 }
 __global__ void k_cg_finish(const CgDev* st, cv_cg_stats* out) {
   out->relres = st->relres;
@@ -572,33 +528,33 @@ void cg_solve(cv_ctx* ctx, cv_snap* s, int kind, const float* g, double lam, dou
   k_cg_init_final<<<1, NT, 0, sm>>>(ws, st);
   ctx->launches += 2;
   if (x0) {
-    k_cg_setup_x<<<NB, NT, 0, sm>>>(x0, st, d, x, s->v_hi, s->v_lo);
+    k_cg_setup_x<<<NB, NT, 0, sm>>>(x0, st, d, x);
     ctx->launches++;
-    mv(ctx, s, s->v_hi, s->v_lo, ap, &st->gv_skip);
+    mv(ctx, s, x, ap, &st->gv_skip);
   } else {
     cudaMemsetAsync(x, 0, sizeof(float) * d, sm);
   }
   k_cg_r0<<<NB, NT, 0, sm>>>(g, ap, x, flam, st, d, r, ws);
   k_cg_r0_final<<<1, NT, 0, sm>>>(ws, st, tol);
-  k_cg_p0<<<NB, NT, 0, sm>>>(r, precond, flam, ffl, st, d, p, s->v_hi, s->v_lo, ws);
+  k_cg_p0<<<NB, NT, 0, sm>>>(r, precond, flam, ffl, st, d, p, ws);
   k_cg_p0_final<<<1, NT, 0, sm>>>(ws, st);
   ctx->launches += 4;
   for (int k = 1; k <= maxiter; ++k) {
     const int is_stab = (stab > 0 && k % stab == 0) ? 1 : 0;
-    mv(ctx, s, s->v_hi, s->v_lo, ap, &st->done);
+    mv(ctx, s, p, ap, &st->done);
     k_cg_pap<<<NB, NT, 0, sm>>>(ap, p, flam, st, d, ws);
     k_cg_pap_final<<<1, NT, 0, sm>>>(ws, st, k, is_stab);
     ctx->launches += 2;
     if (is_stab) {
-      k_cg_xupdate<<<NB, NT, 0, sm>>>(x, p, st, d, s->v_hi, s->v_lo);
+      k_cg_xupdate<<<NB, NT, 0, sm>>>(x, p, st, d);
       ctx->launches++;
-      mv(ctx, s, s->v_hi, s->v_lo, ap, &st->gv_skip);
+      mv(ctx, s, x, ap, &st->gv_skip);
       k_cg_rstab<<<NB, NT, 0, sm>>>(g, ap, x, r, precond, flam, ffl, st, d, ws);
     } else {
       k_cg_update<<<NB, NT, 0, sm>>>(x, r, p, ap, precond, flam, ffl, st, d, ws);
     }
     k_cg_r_final<<<1, NT, 0, sm>>>(ws, st, k, maxiter, is_stab, tol);
-    k_cg_pnext<<<NB, NT, 0, sm>>>(r, precond, flam, ffl, st, d, p, s->v_hi, s->v_lo);
+    k_cg_pnext<<<NB, NT, 0, sm>>>(r, precond, flam, ffl, st, d, p);
     ctx->launches += 3;
   }
   k_cg_finish<<<1, 1, 0, sm>>>(st, stats);

@@ -78,12 +78,13 @@ def _gemm(engine, M, N, K, a_km, b_km, seed=0):
 
 @pytest.mark.parametrize("a_km", [1, 0])
 @pytest.mark.parametrize("b_km", [1, 0])
-@pytest.mark.parametrize("M,N,K", [(128, 128, 32), (256, 512, 96), (200, 300, 70), (1024, 1024, 1024)])
+@pytest.mark.parametrize("M,N,K", [(128, 128, 32), (256, 512, 96), (200, 300, 70), (200, 296, 72),
+                                   (1024, 1024, 1024), (8192, 1024, 785)])
 def test_gemm_unit(a_km, b_km, M, N, K):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    if (not a_km and M % 4) or (not b_km and N % 4) or (a_km and K % 4) or (b_km and K % 4):
-        pytest.skip("leading dimension not 16-byte aligned")
+    if (not a_km and M % 8) or (not b_km and N % 8) or (a_km and K % 8) or (b_km and K % 8):
+        pytest.skip("leading dimension not 16-byte aligned (fp16 rows)")
     out, ref = _gemm("tc", M, N, K, a_km, b_km)
     err = float((out.double() - ref).norm() / ref.norm())
     assert err < 1e-5, (err, out[:2, :4].tolist(), ref[:2, :4].tolist())
