@@ -42,28 +42,53 @@ CV_DEV bool last_block(unsigned* counter) {
   return last;
 }
 
-// per-layer amax of a flat vector; the last block publishes sc[l] and zeroes zero_sc
+// per-layer amax of a flat vector; the last block publishes sc[l] and zeroes zero_sc.
+// One grid-stride pass of 128-bit loads; a thread's indices only increase, so it
+// tracks its current layer and folds the running max into shared memory when the
+// layer changes (at most L times).
 __global__ void __launch_bounds__(SP_NT) k_flat_amax(const float* __restrict__ x, OffTab t, float* part,
                                                      unsigned* counter, Scale* sc, Scale* zero_sc, int n_zero,
                                                      const int* skip) {
   if (skip_if(skip)) return;
   __shared__ float sh[SP_NT / 32];
-  for (int l = 0; l < t.L; ++l) {
-    float m = 0.f;
-    for (int64_t i = t.off[l] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < t.off[l + 1];
-         i += (int64_t)gridDim.x * blockDim.x)
-      m = fmaxf(m, fabsf(x[i]));
-    m = block_max(m, sh);
-    if (threadIdx.x == 0) part[blockIdx.x * SP_MAXL + l] = m;
+  __shared__ int smax[SP_MAXL];
+  if (threadIdx.x < SP_MAXL) smax[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t d = t.off[t.L], base = t.off[0];
+  const int64_t n = d - base;
+  const int64_t lead = ((base + 3) & ~(int64_t)3) - base;  // elements before the first 16-byte boundary
+  int l = 0;
+  float m = 0.f;
+  auto take = [&](int64_t i, float v) {
+    if (i >= t.off[l + 1]) {
+      atomicMax(&smax[l], __float_as_int(m));
+      m = 0.f;
+      while (i >= t.off[l + 1]) ++l;
+    }
+    m = fmaxf(m, fabsf(v));
+  };
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = base + tid; i < base + (lead < n ? lead : n); i += nth) take(i, x[i]);
+  const int64_t q0 = (base + lead) / 4, q1 = (base + n) / 4;
+  for (int64_t q = q0 + tid; q < q1; q += nth) {
+    const float4 v = *reinterpret_cast<const float4*>(x + 4 * q);
+    take(4 * q, v.x);
+    take(4 * q + 1, v.y);
+    take(4 * q + 2, v.z);
+    take(4 * q + 3, v.w);
   }
+  for (int64_t i = (q1 * 4 > base + lead ? q1 * 4 : base + lead) + tid; i < d; i += nth) take(i, x[i]);
+  atomicMax(&smax[l], __float_as_int(m));
+  __syncthreads();
+  if (threadIdx.x < t.L) part[blockIdx.x * SP_MAXL + threadIdx.x] = __int_as_float(smax[threadIdx.x]);
   if (!last_block(counter)) return;
-  for (int l = 0; l < t.L; ++l) {
-    float m = 0.f;
-    for (int b = threadIdx.x; b < gridDim.x; b += blockDim.x) m = fmaxf(m, part[b * SP_MAXL + l]);
-    m = block_max(m, sh);
+  for (int l2 = 0; l2 < t.L; ++l2) {
+    float mm = 0.f;
+    for (int b = threadIdx.x; b < gridDim.x; b += blockDim.x) mm = fmaxf(mm, part[b * SP_MAXL + l2]);
+    mm = block_max(mm, sh);
     if (threadIdx.x == 0) {
-      sc[l].amax = m;
-      sc[l].e = exp_for_bound(m);
+      sc[l2].amax = mm;
+      sc[l2].e = exp_for_bound(mm);
     }
   }
   for (int i = threadIdx.x; i < n_zero; i += blockDim.x) {
@@ -130,11 +155,31 @@ __global__ void __launch_bounds__(SP_NT) k_mat_amax(const float* __restrict__ x,
                                                     const int* skip) {
   if (skip_if(skip)) return;
   __shared__ float sh[SP_NT / 32];
-  const int64_t total = (int64_t)rows * cols;
+  // one warp per row, lanes over columns (128-bit when the rows are aligned)
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool vec = (lds & 3) == 0 && ((uintptr_t)x & 15) == 0;
   float m = 0.f;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / cols, c = i - r * cols;
-    m = fmaxf(m, fabsf(x[r * lds + c]));
+  if (rows == 1) {  // flat vector: all threads over the columns
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+    const int64_t nq = vec ? cols / 4 : 0;
+    for (int64_t q = tid; q < nq; q += nth) {
+      const float4 v = *reinterpret_cast<const float4*>(x + 4 * q);
+      m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+    for (int64_t i = 4 * nq + tid; i < cols; i += nth) m = fmaxf(m, fabsf(x[i]));
+  } else {
+    for (int64_t r = warp; r < rows; r += nwarps) {
+      const float* row = x + r * lds;
+      int c0 = 0;
+      if (vec)
+        for (; c0 + 128 <= cols; c0 += 128) {
+          const float4 v = *reinterpret_cast<const float4*>(row + c0 + 4 * lane);
+          m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+        }
+      for (int c = c0 + lane; c < cols; c += 32) m = fmaxf(m, fabsf(row[c]));
+    }
   }
   m = block_max(m, sh);
   if (threadIdx.x == 0) part[blockIdx.x * SP_MAXL] = m;
@@ -164,15 +209,26 @@ __global__ void __launch_bounds__(SP_NT) k_mat_split(const float* __restrict__ x
                                                      __half* __restrict__ lo, int64_t ldd, const int* skip) {
   if (skip_if(skip)) return;
   const float s = pow2f(sc->e);
-  // destination index space: out_rows x out_cols (padding written as zero)
-  const int64_t total = (int64_t)out_rows * out_cols;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / out_cols, c = i - r * out_cols;  // destination (r, c)
-    const int64_t sr = trans ? c : r, sc_ = trans ? r : c;  // source (row, col)
-    float v = 0.f;
-    if (sr < rows && sc_ < cols) v = x[sr * lds + sc_];
-    else if (ones && sr < rows && sc_ == cols) v = 1.f;
-    split16(v, s, hi[r * ldd + c], lo[r * ldd + c]);
+  if (trans) {  // few long destination rows (c-wide cotangents): flat over elements
+    const int64_t total = (int64_t)out_rows * out_cols;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t r = i / out_cols, c = i - r * out_cols;
+      const float v = (c < rows && r < cols) ? x[c * lds + r] : 0.f;
+      split16(v, s, hi[r * ldd + c], lo[r * ldd + c]);
+    }
+    return;
+  }
+  // destination rows r (one warp each), lanes over columns c
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < out_rows; r += nwarps) {
+    for (int64_t c = lane; c < out_cols; c += 32) {
+      float v = 0.f;
+      if (r < rows && c < cols) v = x[r * lds + c];
+      else if (ones && r < rows && c == cols) v = 1.f;
+      split16(v, s, hi[r * ldd + c], lo[r * ldd + c]);
+    }
   }
 }
 
