@@ -143,6 +143,17 @@ CV_API int cv_norm_check(cv_ctx* ctx, const float* x, int64_t d, double* scal);
 CV_API int cv_gemm_test(cv_ctx* ctx, int engine, int M, int N, int K, const float* a, int64_t lda, int a_kmajor,
                         const float* b, int64_t ldb, int b_kmajor, float* out, int64_t ldo);
 
+/* Diagnostic: average time (ms) of one tensor-core GEMM of the given shape on
+ * resident random operands; mode 0 = fp32 store epilogue, 1 = split + ReLU-mask
+ * epilogue (the JVP / backward epilogue).  Tuning aid, not on any product path. */
+CV_API int cv_gemm_bench(cv_ctx* ctx, int M, int N, int K, int a_kmajor, int b_kmajor, int mode, int iters,
+                         float* ms_out);
+
+/* Test: two-segment tensor-core GEMM out = A.B + A.(s2 B), A M x K and B N x K
+ * (K-major, K % 8 == 0): the segments' scale exponents differ by ~log2(s2),
+ * exercising the accumulator rescaling between K segments. */
+CV_API int cv_gemm_test_seg2(cv_ctx* ctx, int M, int N, int K, const float* a, const float* b, float s2, float* out);
+
 /* ---- row lane ------------------------------------------------------------- */
 CV_API int64_t cv_row_dim(const cv_snap* snap);                        /* m = b * c */
 CV_API int cv_row_rhs(cv_snap* snap, float* rhs_out /* m */);

@@ -61,6 +61,8 @@ _SIGS = {
     "cv_norm_check": (C.c_int, [_P, _P, C.c_int64, _P]),
     "cv_gemm_test": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, _P, C.c_int64, C.c_int, _P, C.c_int64,
                                C.c_int, _P, C.c_int64]),
+    "cv_gemm_bench": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P]),
+    "cv_gemm_test_seg2": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, _P, _P, C.c_float, _P]),
     "cv_row_dim": (C.c_int64, [_P]),
     "cv_row_rhs": (C.c_int, [_P, _P]),
     "cv_row_gram": (C.c_int, [_P, _P]),

@@ -37,7 +37,9 @@ namespace cv {
 
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;                   // fp16 elements = 128 bytes = one SWIZZLE_128B row
-constexpr int TC_ZERO_BYTES = TC_BM * 128;  // all-zero K-major A tile for pure rescaling MMAs
+constexpr int TC_ZERO_BYTES = TC_BM * 32;   // all-zero K-major A tile (SWIZZLE_32B, K=16) for rescaling MMAs
+constexpr int TC_STG_BYTES = 2048;          // per epilogue warp: 32 rows x 16 cols, two fp16 planes or one fp32
+constexpr int TC_STG_TOTAL = 8 * TC_STG_BYTES;
 
 struct TcOperand {
   int kmajor;   // 1: K contiguous, 0: M/N contiguous
@@ -55,6 +57,8 @@ struct TcArgs {
   Epilogue epi;
   const int* skip;
   int lower_only;
+  int dbg;            // experiments: 1 = epilogue reads TMEM only
+  int tma_out;        // 0: per-thread stores; 1: fp16 split pair via TMA; 2: fp32 (out or partial) via TMA
   float* partial;     // split-K partials (nullptr: apply the epilogue directly)
   int tiles_m, tiles_n, splits;
 };
@@ -214,6 +218,30 @@ CV_DEV void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+CV_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+CV_DEV void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+CV_DEV void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+CV_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+CV_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+CV_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // product exponents and processing order of the K segments (larger S first)
 struct SegPlan {
   int S[2];
@@ -244,17 +272,139 @@ CV_DEV int vseg(const TcArgs& a, const SegPlan& p, int v, int& lkb) {
   return 1 - p.ord;
 }
 
+// descriptor of the zero tile: K-major SWIZZLE_32B, 32-byte rows (K = 16), 8-row atoms of 256 B
+CV_DEV uint64_t zero_desc(const uint8_t* z) { return umma_desc(smem_u32(z), 16, 256, 6); }
+
 // zero the rescaling tile (all threads), visible to the tensor core's async proxy
 CV_DEV void zero_tile_init(uint8_t* z) {
   for (int i = threadIdx.x; i < TC_ZERO_BYTES / 16; i += blockDim.x) reinterpret_cast<uint4*>(z)[i] = make_uint4(0, 0, 0, 0);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+struct TcMaps {
+  CUtensorMap m[2][4];  // [seg][A_hi, A_lo, B_hi, B_lo]
+  CUtensorMap o[2];     // TMA-store epilogue: fp16 {hi, lo} boxes {16, 32} SW32, or fp32 {16, 32(,1)} SW64
+};
+
+// Epilogue of one accumulator tile through shared memory and TMA stores (the
+// hot modes: split outputs with an optional ReLU mask, fp32 outputs and split-K
+// partials).  Each warp owns a 2 KB staging slot and walks its 32 rows in
+// 16-column steps: tcgen05.ld -> (mask tile loaded row-contiguously through the
+// slot) -> epilogue -> swizzled staging -> one elected lane issues the TMA
+// store(s).  Global traffic is full-row, and stores retire asynchronously.
+template <int BN>
+CV_DEV void tile_epilogue_tma(const TcArgs& a, const TcMaps& maps, const EpiRt& rt, uint32_t tacc, int m_base, int n0,
+                              int split, float inv, int q, int half, int lane, uint8_t* stg, float& amax) {
+  const int r0 = m_base + q * 32;  // this warp's first row
+  const int m = r0 + lane;
+  const uint32_t trow = tacc + ((uint32_t)(q * 32) << 16);
+  constexpr int NSUB = BN / 16;
+  constexpr int S0 = NSUB >= 2 ? NSUB / 2 : 1;
+  const int sb = half * S0, se = NSUB >= 2 ? (half + 1) * S0 : (half == 0 ? 1 : 0);
+  const Epilogue& e = a.epi;
+  const bool use_mask = a.tma_out == 1 && (e.mode == EPI_SPLIT_MASK || e.mode == EPI_HVP);
+  const bool relu_act = e.act == CV_ACT_RELU;
+  // this lane's share of a sub-tile's mask (rows lane/2 and lane/2 + 16, 8 columns),
+  // loaded one sub-tile ahead so the global latency overlaps the previous sub-tile
+  auto load_mask = [&](int nb, uint4 (&mv)[2]) {
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+      const int rr = (lane >> 1) + 16 * it, ch = lane & 1;
+      mv[it] = make_uint4(0, 0, 0, 0);
+      if (nb < a.N && r0 + rr < a.M && nb + 8 * ch < a.N)
+        mv[it] = *reinterpret_cast<const uint4*>(e.mask_hi + (int64_t)(r0 + rr) * e.mask_ld + nb + 8 * ch);
+    }
+  };
+  uint4 mcur[2], mnext[2];
+  if (use_mask) load_mask(n0 + sb * 16, mcur);
+#pragma unroll 1
+  for (int sbk = sb; sbk < se; ++sbk) {
+    const int nb = n0 + sbk * 16;
+    if (nb >= a.N) break;
+    if (use_mask && sbk + 1 < se) load_mask(nb + 16, mnext);
+    uint32_t r[16];
+    tmem_ld16(trow + sbk * 16, r);
+    float v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]) * inv;
+    // the slot must be free: the previous sub-tile's TMA store has read it
+    if (lane == 0) bulk_wait_read0();
+    __syncwarp();
+    if (a.tma_out == 1) {
+      // ---- split fp16 output (activations / tangents / cotangents) ----
+      float o[16];
+      if (use_mask) {
+        // stage the mask tile (rows r0..r0+31, cols nb..nb+15; ReLU: sign of hi) and
+        // read back this lane's row
+#pragma unroll
+        for (int it = 0; it < 2; ++it) {
+          const int rr = (lane >> 1) + 16 * it, ch = lane & 1;
+          *reinterpret_cast<uint4*>(stg + rr * 32 + 16 * (ch ^ ((rr >> 2) & 1))) = mcur[it];
+        }
+        __syncwarp();
+        H8 mk[2];
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) mk[ch].u = *reinterpret_cast<const uint4*>(stg + lane * 32 + 16 * (ch ^ ((lane >> 2) & 1)));
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) o[j] = v[j] * (__half2float(mk[j >> 3].h[j & 7]) > 0.f ? 1.f : 0.f);
+        mcur[0] = mnext[0];
+        mcur[1] = mnext[1];
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) o[j] = relu_act ? relu_f(v[j]) : tanhf(v[j]);
+      }
+      if (m < a.M)
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (nb + j < a.N) amax = fmaxf(amax, fabsf(o[j]));
+      H8 h0, h1, l0, l1;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        split16(o[j], rt.out_s, h0.h[j], l0.h[j]);
+        split16(o[8 + j], rt.out_s, h1.h[j], l1.h[j]);
+      }
+      const int sw = (lane >> 2) & 1;
+      *reinterpret_cast<uint4*>(stg + lane * 32 + 16 * (0 ^ sw)) = h0.u;
+      *reinterpret_cast<uint4*>(stg + lane * 32 + 16 * (1 ^ sw)) = h1.u;
+      *reinterpret_cast<uint4*>(stg + 1024 + lane * 32 + 16 * (0 ^ sw)) = l0.u;
+      *reinterpret_cast<uint4*>(stg + 1024 + lane * 32 + 16 * (1 ^ sw)) = l1.u;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(&maps.o[0], stg, nb, r0);
+        tma_store_2d(&maps.o[1], stg + 1024, nb, r0);
+        bulk_commit();
+      }
+    } else {
+      // ---- fp32 output / split-K partial: 32 rows x 64 B, SWIZZLE_64B ----
+      const int sw = (lane >> 1) & 3;
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch)
+        *reinterpret_cast<float4*>(stg + lane * 64 + 16 * (ch ^ sw)) =
+            make_float4(v[4 * ch], v[4 * ch + 1], v[4 * ch + 2], v[4 * ch + 3]);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        if (a.partial) tma_store_3d(&maps.o[0], stg, nb, r0, split);
+        else tma_store_2d(&maps.o[0], stg, nb, r0);
+        bulk_commit();
+      }
+    }
+  }
+}
+
 // The epilogue of one accumulator tile (TMEM -> registers -> fused epilogue), run by
 // 8 warps: warp w reads TMEM lane quadrant (w % 4), half = column half.
 template <int BN>
-CV_DEV void tile_epilogue(const TcArgs& a, const EpiRt& rt, uint32_t tacc, int m_base, int n0, int split, float inv,
-                          int q, int half, int lane) {
+CV_DEV void tile_epilogue(const TcArgs& a, const TcMaps& maps, const EpiRt& rt, uint32_t tacc, int m_base, int n0,
+                          int split, float inv, int q, int half, int lane, uint8_t* stg) {
+  if (a.tma_out && !a.dbg) {
+    float amax = 0.f, ramax = 0.f;
+    tile_epilogue_tma<BN>(a, maps, rt, tacc, m_base, n0, split, inv, q, half, lane, stg, amax);
+    if (!a.partial) epi_flush_amax(a.epi, amax, ramax);
+    return;
+  }
   const int m = m_base + q * 32 + lane;
   const uint32_t trow = tacc + ((uint32_t)(q * 32) << 16);
   constexpr int NCH = BN / 32;
@@ -264,6 +414,10 @@ CV_DEV void tile_epilogue(const TcArgs& a, const EpiRt& rt, uint32_t tacc, int m
   for (int c = half * C0; c < (NCH >= 2 ? (half + 1) * C0 : (half == 0 ? 1 : 0)); ++c) {
     uint32_t r[32];
     tmem_ld32(trow + c * 32, r);
+    if (a.dbg) {
+      if (r[0] == 0x7fffffff && r[31] == 1) amax += 1.f;
+      continue;
+    }
     if (m >= a.M) continue;
     const int nb = n0 + c * 32;
     float v[32];
@@ -294,16 +448,13 @@ CV_DEV void tile_epilogue(const TcArgs& a, const EpiRt& rt, uint32_t tacc, int m
 // ---------------------------------------------------------------------------
 // Kernel (1-CTA)
 // ---------------------------------------------------------------------------
-struct TcMaps {
-  CUtensorMap m[2][4];  // [seg][A_hi, A_lo, B_hi, B_lo]
-};
 
 template <int BN, int STAGES>
 struct TcCfg {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;  // 16 KB
   static constexpr int B_BYTES = BN * TC_BK * 2;     // 4 / 16 / 32 KB
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + TC_ZERO_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + TC_ZERO_BYTES + TC_STG_TOTAL + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered accumulator
   static constexpr int THREADS = 320;                          // w0 TMA, w1 MMA, w2..w9 epilogue
 };
@@ -340,7 +491,8 @@ __global__ void __launch_bounds__(320, 1) k_gemm_tc(const __grid_constant__ TcMa
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* zero = smem + STAGES * Cfg::STAGE_BYTES;
-  uint64_t* full = (uint64_t*)(zero + TC_ZERO_BYTES);
+  uint8_t* stg_all = zero + TC_ZERO_BYTES;
+  uint64_t* full = (uint64_t*)(stg_all + TC_STG_TOTAL);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -398,7 +550,7 @@ __global__ void __launch_bounds__(320, 1) k_gemm_tc(const __grid_constant__ TcMa
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ----------------
     int it = 0, acc_i = 0;
-    const uint64_t zdesc = op_desc(smem_u32(zero), 0, 0);
+    const uint64_t zdesc = zero_desc(zero);
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
       int m0, n0, kb0, nkb;
       if (!tc_work(a, w, TC_BM, BN, m0, n0, kb0, nkb)) continue;
@@ -444,12 +596,14 @@ __global__ void __launch_bounds__(320, 1) k_gemm_tc(const __grid_constant__ TcMa
       int lkb;
       const int last = vseg(a, plan, kb0 + nkb - 1, lkb);
       const float inv = plan.inv_a[last] * plan.inv_b[last];
-      tile_epilogue<BN>(a, rt, tmem + ab * BN, m0, n0, w / (a.tiles_m * a.tiles_n), inv, q, half, lane);
+      tile_epilogue<BN>(a, maps, rt, tmem + ab * BN, m0, n0, w / (a.tiles_m * a.tiles_n), inv, q, half, lane,
+                        stg_all + (warp - 2) * TC_STG_BYTES);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[ab]);
       ++acc_i;
     }
+    if (lane == 0) bulk_wait0();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -560,6 +714,84 @@ static CUtensorMap make_map(const __half* ptr, int64_t inner, int64_t outer, int
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
+// Output map of the TMA-store epilogue (rank 2 or 3), cached like the operand maps.
+struct OutKey {
+  const void* ptr;
+  int64_t d0, d1, d2, s1;
+  int fp16;
+  bool operator==(const OutKey& o) const {
+    return ptr == o.ptr && d0 == o.d0 && d1 == o.d1 && d2 == o.d2 && s1 == o.s1 && fp16 == o.fp16;
+  }
+};
+struct OutKeyHash {
+  size_t operator()(const OutKey& k) const {
+    size_t h = (size_t)k.ptr;
+    h = h * 1000003u ^ (size_t)k.d0;
+    h = h * 1000003u ^ (size_t)k.d1;
+    h = h * 1000003u ^ (size_t)k.d2;
+    h = h * 1000003u ^ (size_t)(k.s1 * 2 + k.fp16);
+    return h;
+  }
+};
+
+// fp16: dims {cols, rows}, row stride ld, box {16, 32}, SWIZZLE_32B.
+// fp32: dims {cols, rows (, slabs)}, box {16, 32 (, 1)}, SWIZZLE_64B.
+static CUtensorMap make_out_map(const void* ptr, int fp16, int64_t cols, int64_t rows, int64_t slabs, int64_t ld) {
+  static std::unordered_map<OutKey, CUtensorMap, OutKeyHash> cache;
+  static std::mutex mu;
+  OutKey key{ptr, cols, rows, slabs, ld, fp16};
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  auto fn = encode_fn();
+  if (!fn) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+  CUtensorMap m;
+  const int esz = fp16 ? 2 : 4;
+  const cuuint32_t rank = slabs > 1 ? 3 : 2;
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)slabs};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * esz, (cuuint64_t)ld * esz * rows};
+  cuuint32_t box[3] = {16, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(&m, fp16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, (void*)ptr, dims,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  fp16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (out) failed (" + std::to_string((int)r) + ")");
+  std::lock_guard<std::mutex> g(mu);
+  if (cache.size() > 4096) cache.clear();
+  cache.emplace(key, m);
+  return m;
+}
+
+// Choose the TMA-store epilogue when the mode and layout allow it.
+static void setup_out(const GemmArgs& g, TcMaps& maps, TcArgs& a, float* partial, int splits) {
+  static const int off = getenv("CURVOPT_TC_TMA_OUT") && getenv("CURVOPT_TC_TMA_OUT")[0] == '0';
+  a.tma_out = 0;
+  if (off || g.lower_only) return;
+  const Epilogue& e = g.epi;
+  if (partial) {
+    if ((g.N & 3) || !aligned16(partial)) return;
+    maps.o[0] = make_out_map(partial, 0, g.N, g.M, splits, g.N);
+    a.tma_out = 2;
+    return;
+  }
+  if (e.mode == EPI_STORE) {
+    if ((e.ld & 3) || !aligned16(e.out)) return;
+    maps.o[0] = make_out_map(e.out, 0, g.N, g.M, 1, e.ld);
+    a.tma_out = 2;
+    return;
+  }
+  const bool relu_mask = (e.mode == EPI_SPLIT_MASK || e.mode == EPI_HVP) && e.act == CV_ACT_RELU && !e.raw &&
+                         e.mask_div == 1 && (e.mask_ld & 7) == 0 && aligned16(e.mask_hi);
+  if (!(e.mode == EPI_SPLIT_ACT || relu_mask)) return;
+  if ((e.ld & 7) || !aligned16(e.out_hi) || !aligned16(e.out_lo)) return;
+  maps.o[0] = make_out_map(e.out_hi, 1, g.N, g.M, 1, e.ld);
+  maps.o[1] = make_out_map(e.out_lo, 1, g.N, g.M, 1, e.ld);
+  a.tma_out = 1;
+}
+
 // Operand majors: A(m,k) = p[m*si + k*sj]; K-major iff sj == 1.
 static bool op_ok(const Operand& o) {
   if (o.f32 || !o.hi || !o.lo || !o.sc) return false;
@@ -611,6 +843,8 @@ static void fill_args(const GemmArgs& g, int bbox, TcMaps& maps, TcArgs& a) {
   a.epi = g.epi;
   a.skip = g.skip;
   a.lower_only = g.lower_only;
+  static const int dbg = getenv("CURVOPT_DBG_EPI") ? atoi(getenv("CURVOPT_DBG_EPI")) : 0;
+  a.dbg = dbg;
 }
 
 template <int BN, int STAGES>
@@ -636,6 +870,7 @@ static int launch_tc(cv_ctx* ctx, const GemmArgs& g, int splits, float* ext_part
     part = (float*)ctx->pool.get(sizeof(float) * (size_t)splits * g.M * g.N);
     a.partial = part;
   }
+  setup_out(g, maps, a, a.partial, splits);
   const int work = a.tiles_m * a.tiles_n * splits;
   const int grid = work < ctx->sm_count ? work : ctx->sm_count;
   k_gemm_tc<BN, STAGES><<<grid, Cfg::THREADS, Cfg::SMEM, ctx->stream>>>(maps, a);
@@ -667,7 +902,7 @@ void gemm_tc(cv_ctx* ctx, const GemmArgs& g) {
     if (splits < 1) splits = 1;
   }
   if (g.N <= 32)
-    launch_tc<32, 5>(ctx, g, splits);
+    launch_tc<32, 4>(ctx, g, splits);
   else if (pair)
     launch_tc2<3>(ctx, g, splits);
   else if (wide)
@@ -688,7 +923,7 @@ int gemm_tc_partial(cv_ctx* ctx, const GemmArgs& g, float** partial) {
   const int kbs = (kb_total + splits - 1) / splits;
   splits = (kb_total + kbs - 1) / kbs;
   *partial = (float*)ctx->pool.get(sizeof(float) * (size_t)splits * g.M * g.N);
-  return launch_tc<32, 5>(ctx, g, splits, *partial);
+  return launch_tc<32, 4>(ctx, g, splits, *partial);
 }
 
 }  // namespace cv

@@ -16,7 +16,7 @@ struct Tc2Cfg {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;         // 16 KB: this CTA's 128 rows
   static constexpr int B_BYTES = (TC2_BN / 2) * TC_BK * 2;  // 16 KB: this CTA's 128 columns
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + TC_ZERO_BYTES + 1024 + 256;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + TC_ZERO_BYTES + TC_STG_TOTAL + 1024 + 256;
   static constexpr int TMEM_COLS = 2 * TC2_BN;
 };
 
@@ -65,7 +65,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* zero = smem + STAGES * Cfg::STAGE_BYTES;
-  uint64_t* full = (uint64_t*)(zero + TC_ZERO_BYTES);
+  uint8_t* stg_all = zero + TC_ZERO_BYTES;
+  uint64_t* full = (uint64_t*)(stg_all + TC_STG_TOTAL);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -129,7 +130,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   } else if (warp == 1 && lane == 0 && rank == 0) {
     // ---------------- MMA issuer (leader CTA) ----------------
     int it = 0, acc_i = 0;
-    const uint64_t zdesc = op_desc(smem_u32(zero), 0, 0);
+    const uint64_t zdesc = zero_desc(zero);
     for (int w = cluster; w < total; w += nclusters) {
       int mt0, n0, kb0, nkb;
       if (!tc_work(a, w, 2 * TC_BM, TC2_BN, mt0, n0, kb0, nkb)) continue;
@@ -176,13 +177,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       int lkb;
       const int last = vseg(a, plan, kb0 + nkb - 1, lkb);
       const float inv = plan.inv_a[last] * plan.inv_b[last];
-      tile_epilogue<TC2_BN>(a, rt, tmem + ab * TC2_BN, mt0 + rank * TC_BM, n0, w / (a.tiles_m * a.tiles_n), inv, q,
-                            half, lane);
+      tile_epilogue<TC2_BN>(a, maps, rt, tmem + ab * TC2_BN, mt0 + rank * TC_BM, n0, w / (a.tiles_m * a.tiles_n),
+                            inv, q, half, lane, stg_all + (warp - 2) * TC_STG_BYTES);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(tempty0[ab]);
       ++acc_i;
     }
+    if (lane == 0) bulk_wait0();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -214,6 +216,7 @@ static void launch_tc2(cv_ctx* ctx, const GemmArgs& g, int splits) {
     part = (float*)ctx->pool.get(sizeof(float) * (size_t)splits * g.M * g.N);
     a.partial = part;
   }
+  setup_out(g, maps, a, a.partial, splits);
   const int work = a.tiles_m * a.tiles_n * splits;
   const int pairs = ctx->sm_count / 2;
   const int grid = 2 * (work < pairs ? work : pairs);

@@ -88,3 +88,22 @@ def test_gemm_unit(a_km, b_km, M, N, K):
     out, ref = _gemm("tc", M, N, K, a_km, b_km)
     err = float((out.double() - ref).norm() / ref.norm())
     assert err < 1e-5, (err, out[:2, :4].tolist(), ref[:2, :4].tolist())
+
+
+@pytest.mark.parametrize("s2", [1.0, 2.0 ** -7, 2.0 ** 9, 2.0 ** -20, 2.0 ** 23, 2.0 ** -40])
+@pytest.mark.parametrize("M,N,K", [(256, 256, 512), (8192, 1024, 256), (200, 48, 72)])
+def test_two_segment_rescale(s2, M, N, K):
+    """Segments with exponents differing by up to 2^40 share one accumulator:
+    the larger-scale segment runs first and is rescaled (scale-input-d, plus
+    zero-operand MMAs beyond 2^15) before the second accumulates."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    rt = runtime()
+    g = torch.Generator(device="cuda").manual_seed(3)
+    A = torch.randn(M, K, device="cuda", generator=g)
+    B = torch.randn(N, K, device="cuda", generator=g)
+    out = torch.full((M, N), float("nan"), device="cuda")
+    rt.call("cv_gemm_test_seg2", rt.h, M, N, K, A.data_ptr(), B.data_ptr(), float(s2), out.data_ptr())
+    ref = (1.0 + s2) * (A.double() @ B.double().t())
+    err = float((out.double() - ref).norm() / ref.norm())
+    assert err < 2e-6, err
