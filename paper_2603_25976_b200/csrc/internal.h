@@ -149,6 +149,7 @@ struct cv_snap {
   cv::Scale* U2_sc = nullptr;     // U2 amax
   cv::Scale* prod_sc = nullptr;   // start of the per-product block
   int n_prod = 0;
+  int v_ready = 0;                // the next product input's scales were published by its producer
   cv::Scale* scratch_sc = nullptr;  // [8] row lane / tests
   // weights of the linearization point, split, flat layout
   __half* w_hi = nullptr;
@@ -219,6 +220,12 @@ void check_launch(cv_ctx* ctx);
 void amax_into(cv_ctx* ctx, const float* x, int64_t n, Scale* slot);  // slot->amax = max|x|
 void split_flat(cv_ctx* ctx, const float* x, int64_t d, const std::vector<int64_t>& off, __half* hi, __half* lo,
                 Scale* sc, Scale* zero_sc, int n_zero, const int* skip);
+void split_flat_apply(cv_ctx* ctx, const float* x, int64_t d, const std::vector<int64_t>& off, __half* hi,
+                      __half* lo, const Scale* sc, const int* skip);
+// p = M^-1 r + beta p with the per-layer amax of p published into sc (false: not fused, L > 16)
+bool cg_pnext_amax(cv_ctx* ctx, const float* r, const float* pre, float lam, float floor_, const double* beta,
+                   const int* done, float* p, int64_t d, const std::vector<int64_t>& off, Scale* sc, Scale* zero_sc,
+                   int n_zero);
 void split_rows(cv_ctx* ctx, const float* src, int64_t lds, int rows, int cols, const SplitBuf& dst, int ones);
 void split_mat(cv_ctx* ctx, const float* src, int64_t lds, int rows, int cols, __half* hi, __half* lo, int64_t ldd,
                int trans, Scale* sc, int amax_ready, const int* skip);

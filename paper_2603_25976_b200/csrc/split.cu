@@ -42,6 +42,29 @@ CV_DEV bool last_block(unsigned* counter) {
   return last;
 }
 
+// block maxima -> part; the grid's last block reduces them and publishes sc[l]
+// (and zeroes the zero_sc block of Scale slots).
+CV_DEV void flat_amax_finish(const OffTab& t, int* smax, float* sh, float* part, unsigned* counter, Scale* sc,
+                             Scale* zero_sc, int n_zero) {
+  __syncthreads();
+  if (threadIdx.x < t.L) part[blockIdx.x * SP_MAXL + threadIdx.x] = __int_as_float(smax[threadIdx.x]);
+  if (!last_block(counter)) return;
+  for (int l2 = 0; l2 < t.L; ++l2) {
+    float mm = 0.f;
+    for (int b = threadIdx.x; b < gridDim.x; b += blockDim.x) mm = fmaxf(mm, __ldcg(part + b * SP_MAXL + l2));
+    mm = block_max(mm, sh);
+    if (threadIdx.x == 0) {
+      sc[l2].amax = mm;
+      sc[l2].e = exp_for_bound(mm);
+    }
+  }
+  for (int i = threadIdx.x; i < n_zero; i += blockDim.x) {
+    zero_sc[i].e = 0;
+    zero_sc[i].amax = 0.f;
+  }
+  if (threadIdx.x == 0) *counter = 0;
+}
+
 // per-layer amax of a flat vector; the last block publishes sc[l] and zeroes zero_sc.
 // One grid-stride pass of 128-bit loads; a thread's indices only increase, so it
 // tracks its current layer and folds the running max into shared memory when the
@@ -79,23 +102,58 @@ __global__ void __launch_bounds__(SP_NT) k_flat_amax(const float* __restrict__ x
   }
   for (int64_t i = (q1 * 4 > base + lead ? q1 * 4 : base + lead) + tid; i < d; i += nth) take(i, x[i]);
   atomicMax(&smax[l], __float_as_int(m));
+  flat_amax_finish(t, smax, sh, part, counter, sc, zero_sc, n_zero);
+}
+
+// CG direction update fused with the per-layer amax of the next product input:
+// p = M^-1 r + beta p (solvers.py:111-112), then the last block publishes the
+// scales (the product's split pass follows without its own amax pass).
+__global__ void __launch_bounds__(SP_NT) k_cg_pnext_amax(const float* __restrict__ r, const float* __restrict__ pre,
+                                                         float lam, float floor_, const double* beta_p,
+                                                         const int* done, float* __restrict__ p, OffTab t,
+                                                         float* part, unsigned* counter, Scale* sc, Scale* zero_sc,
+                                                         int n_zero) {
+  if (*(volatile const int*)done) return;
+  __shared__ float sh[SP_NT / 32];
+  __shared__ int smax[SP_MAXL];
+  if (threadIdx.x < SP_MAXL) smax[threadIdx.x] = 0;
   __syncthreads();
-  if (threadIdx.x < t.L) part[blockIdx.x * SP_MAXL + threadIdx.x] = __int_as_float(smax[threadIdx.x]);
-  if (!last_block(counter)) return;
-  for (int l2 = 0; l2 < t.L; ++l2) {
-    float mm = 0.f;
-    for (int b = threadIdx.x; b < gridDim.x; b += blockDim.x) mm = fmaxf(mm, part[b * SP_MAXL + l2]);
-    mm = block_max(mm, sh);
-    if (threadIdx.x == 0) {
-      sc[l2].amax = mm;
-      sc[l2].e = exp_for_bound(mm);
+  const float beta = (float)*beta_p;
+  const int64_t d = t.off[t.L];
+  int l = 0;
+  float m = 0.f;
+  auto take = [&](int64_t i, float v) {
+    if (i >= t.off[l + 1]) {
+      atomicMax(&smax[l], __float_as_int(m));
+      m = 0.f;
+      while (i >= t.off[l + 1]) ++l;
     }
+    m = fmaxf(m, fabsf(v));
+  };
+  auto minv = [&](int64_t i) { return pre ? 1.f / (fmaxf(pre[i], floor_) + lam) : 1.f; };
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nq = d >> 2;
+  for (int64_t q = tid; q < nq; q += nth) {
+    const int64_t i = 4 * q;
+    const float4 r4 = *reinterpret_cast<const float4*>(r + i);
+    float4 p4 = *reinterpret_cast<const float4*>(p + i);
+    p4.x = minv(i) * r4.x + beta * p4.x;
+    p4.y = minv(i + 1) * r4.y + beta * p4.y;
+    p4.z = minv(i + 2) * r4.z + beta * p4.z;
+    p4.w = minv(i + 3) * r4.w + beta * p4.w;
+    *reinterpret_cast<float4*>(p + i) = p4;
+    take(i, p4.x);
+    take(i + 1, p4.y);
+    take(i + 2, p4.z);
+    take(i + 3, p4.w);
   }
-  for (int i = threadIdx.x; i < n_zero; i += blockDim.x) {
-    zero_sc[i].e = 0;
-    zero_sc[i].amax = 0.f;
+  for (int64_t i = 4 * nq + tid; i < d; i += nth) {
+    const float v = minv(i) * r[i] + beta * p[i];
+    p[i] = v;
+    take(i, v);
   }
-  if (threadIdx.x == 0) *counter = 0;
+  atomicMax(&smax[l], __float_as_int(m));
+  flat_amax_finish(t, smax, sh, part, counter, sc, zero_sc, n_zero);
 }
 
 __global__ void __launch_bounds__(SP_NT) k_flat_split(const float* __restrict__ x, OffTab t, const Scale* sc,
@@ -146,6 +204,31 @@ void split_flat(cv_ctx* ctx, const float* x, int64_t d, const std::vector<int64_
   }
 }
 
+static OffTab off_tab(const std::vector<int64_t>& off, int64_t d) {
+  OffTab t;
+  t.L = (int)off.size();
+  for (int l = 0; l < t.L; ++l) t.off[l] = off[l];
+  t.off[t.L] = d;
+  return t;
+}
+
+// split pass only (the scales were published by a fused producer)
+void split_flat_apply(cv_ctx* ctx, const float* x, int64_t d, const std::vector<int64_t>& off, __half* hi,
+                      __half* lo, const Scale* sc, const int* skip) {
+  k_flat_split<<<SP_NB, SP_NT, 0, ctx->stream>>>(x, off_tab(off, d), sc, hi, lo, skip);
+  ctx->launches++;
+}
+
+bool cg_pnext_amax(cv_ctx* ctx, const float* r, const float* pre, float lam, float floor_, const double* beta,
+                   const int* done, float* p, int64_t d, const std::vector<int64_t>& off, Scale* sc, Scale* zero_sc,
+                   int n_zero) {
+  if ((int)off.size() > SP_MAXL) return false;
+  k_cg_pnext_amax<<<SP_NB, SP_NT, 0, ctx->stream>>>(r, pre, lam, floor_, beta, done, p, off_tab(off, d), part_of(ctx),
+                                                    counter_of(ctx), sc, zero_sc, n_zero);
+  ctx->launches++;
+  return true;
+}
+
 // ---------------------------------------------------------------------------
 // 2-D splits: [rows x cols] fp32 (ld lds) -> split (ld ldd), optionally
 // transposed (dst[j, i]) and with a ones column at `cols` (augmented activations)
@@ -185,7 +268,7 @@ __global__ void __launch_bounds__(SP_NT) k_mat_amax(const float* __restrict__ x,
   if (threadIdx.x == 0) part[blockIdx.x * SP_MAXL] = m;
   if (!last_block(counter)) return;
   m = 0.f;
-  for (int b = threadIdx.x; b < gridDim.x; b += blockDim.x) m = fmaxf(m, part[b * SP_MAXL]);
+  for (int b = threadIdx.x; b < gridDim.x; b += blockDim.x) m = fmaxf(m, __ldcg(part + b * SP_MAXL));
   m = block_max(m, sh);
   if (threadIdx.x == 0) {
     m = fmaxf(m, floor_);
@@ -195,20 +278,15 @@ __global__ void __launch_bounds__(SP_NT) k_mat_amax(const float* __restrict__ x,
   }
 }
 
-// publish e from an amax accumulated by the producer
-__global__ void k_scale_from_amax(Scale* sc, float floor_, const int* skip) {
-  if (skip_if(skip)) return;
-  const float m = fmaxf(sc->amax, floor_);
-  sc->amax = m;
-  sc->e = exp_for_bound(m);
-}
-
 __global__ void __launch_bounds__(SP_NT) k_mat_split(const float* __restrict__ x, int64_t lds, int rows, int cols,
                                                      int out_rows, int out_cols, int trans, int ones,
-                                                     const Scale* sc, __half* __restrict__ hi,
+                                                     Scale* sc, int from_amax, __half* __restrict__ hi,
                                                      __half* __restrict__ lo, int64_t ldd, const int* skip) {
   if (skip_if(skip)) return;
-  const float s = pow2f(sc->e);
+  // from_amax: the producer accumulated max|x| in sc->amax; derive (and publish) e here
+  const int e = from_amax ? exp_for_bound(sc->amax) : sc->e;
+  if (from_amax && blockIdx.x == 0 && threadIdx.x == 0) sc->e = e;
+  const float s = pow2f(e);
   if (trans) {  // few long destination rows (c-wide cotangents): flat over elements
     const int64_t total = (int64_t)out_rows * out_cols;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -247,7 +325,7 @@ void split_rows(cv_ctx* ctx, const float* src, int64_t lds, int rows, int cols, 
                                                counter_of(ctx), dst.sc, nullptr);
   const int oc = ones ? cols + 1 : cols;
   k_mat_split<<<grid_for((int64_t)rows * oc), SP_NT, 0, ctx->stream>>>(src, lds, rows, cols, rows, oc, 0, ones, dst.sc,
-                                                                      dst.hi, dst.lo, dst.ld, nullptr);
+                                                                      0, dst.hi, dst.lo, dst.ld, nullptr);
   ctx->launches += 2;
 }
 
@@ -255,16 +333,15 @@ void split_rows(cv_ctx* ctx, const float* src, int64_t lds, int rows, int cols, 
 // already holds max|src| (accumulated by the producer)
 void split_mat(cv_ctx* ctx, const float* src, int64_t lds, int rows, int cols, __half* hi, __half* lo, int64_t ldd,
                int trans, Scale* sc, int amax_ready, const int* skip) {
-  if (amax_ready) {
-    k_scale_from_amax<<<1, 1, 0, ctx->stream>>>(sc, 0.f, skip);
-  } else {
+  if (!amax_ready) {
     k_mat_amax<<<SP_NB, SP_NT, 0, ctx->stream>>>(src, lds, rows, cols, 0.f, part_of(ctx), counter_of(ctx), sc, skip);
+    ctx->launches++;
   }
   const int orows = trans ? (int)((cols + 15) / 16 * 16) : rows;
   const int ocols = trans ? rows : cols;
   k_mat_split<<<grid_for((int64_t)orows * ocols), SP_NT, 0, ctx->stream>>>(src, lds, rows, cols, orows, ocols, trans, 0,
-                                                                          sc, hi, lo, ldd, skip);
-  ctx->launches += 2;
+                                                                          sc, amax_ready, hi, lo, ldd, skip);
+  ctx->launches++;
 }
 
 // column `col` of a split buffer := v (scaled by the buffer's exponent); amax covers |v|

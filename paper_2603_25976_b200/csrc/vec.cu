@@ -347,8 +347,14 @@ __global__ void k_cg_p0_final(const double* ws, CgDev* st) {
   sum_partials<1>(ws, t);
   if (threadIdx.x == 0) st->rz = t[0];
 }
-// Ap = Gv(p) + lam p (in place); partials p.Ap, max|p|, #nonfinite(p)
-__global__ void k_cg_pap(float* ap, const float* p, float lam, const CgDev* st, int64_t d, double* ws) {
+CV_DEV bool grid_last(unsigned* ctr);
+CV_DEV void pap_final_body(const double* ws, CgDev* st, int k, int stab);
+CV_DEV void r_final_body(const double* ws, CgDev* st, int k, int maxiter, int stab, double tol);
+
+// Ap = Gv(p) + lam p (in place); partials p.Ap, max|p|, #nonfinite(p); the last
+// block turns them into alpha and the termination flags (solvers.py:90-105)
+__global__ void k_cg_pap(float* ap, const float* p, float lam, CgDev* st, int64_t d, double* ws, unsigned* ctr, int k,
+                         int stab) {
   if (st->done) return;
   double t[3] = {0.0, 0.0, 0.0};
   auto body = [&](float pi, float& a) {
@@ -382,16 +388,27 @@ __global__ void k_cg_pap(float* ap, const float* p, float lam, const CgDev* st, 
     for (int w = 0; w < NT / 32; ++w) m = fmax(m, smx[w]);
     ws[blockIdx.x * 8 + 1] = m;
   }
+  if (grid_last(ctr)) pap_final_body(ws, st, k, stab);
 }
-__global__ void k_cg_pap_final(const double* ws, CgDev* st, int k, int stab) {
-  if (st->done) return;
+// grid's last block? (after every block wrote its partials; counter returns to 0)
+CV_DEV bool grid_last(unsigned* ctr) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ctr, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last && threadIdx.x == 0) *ctr = 0;
+  return last;
+}
+
+CV_DEV void pap_final_body(const double* ws, CgDev* st, int k, int stab) {
   double t[3];
   // sums of slots 0 and 2; max of slot 1
   double s0 = 0.0, s2 = 0.0, mx = 0.0;
   for (int b = threadIdx.x; b < NB; b += NT) {
-    s0 += ws[b * 8 + 0];
-    s2 += ws[b * 8 + 2];
-    mx = fmax(mx, ws[b * 8 + 1]);
+    s0 += __ldcg(ws + b * 8 + 0);
+    s2 += __ldcg(ws + b * 8 + 2);
+    mx = fmax(mx, __ldcg(ws + b * 8 + 1));
   }
   t[0] = s0; t[1] = 0.0; t[2] = s2;
   block_sum<3>(t);
@@ -416,7 +433,8 @@ __global__ void k_cg_pap_final(const double* ws, CgDev* st, int k, int stab) {
 }
 // plain iteration: x += a p; r -= a Ap; partials ||r||^2, r.M^-1 r
 __global__ void k_cg_update(float* x, float* r, const float* p, const float* ap, const float* pre, float lam,
-                            float floor_, const CgDev* st, int64_t d, double* ws) {
+                            float floor_, CgDev* st, int64_t d, double* ws, unsigned* ctr, int k, int maxiter,
+                            double tol) {
   if (st->done) return;
   const float a = (float)st->alpha;
   double t[2] = {0.0, 0.0};
@@ -443,6 +461,7 @@ __global__ void k_cg_update(float* x, float* r, const float* p, const float* ap,
     r[i] = ri;
   }
   write_partials<2>(ws, t);
+  if (grid_last(ctr)) r_final_body(ws, st, k, maxiter, 0, tol);
 }
 // stabilising iteration: x += a p (the explicit residual product follows)
 __global__ void k_cg_xupdate(float* x, const float* p, const CgDev* st, int64_t d) {
@@ -452,7 +471,8 @@ __global__ void k_cg_xupdate(float* x, const float* p, const CgDev* st, int64_t 
 }
 // r = g - (Ax + lam x); partials ||r||^2, r.M^-1 r
 __global__ void k_cg_rstab(const float* g, const float* ax, const float* x, float* r, const float* pre, float lam,
-                           float floor_, const CgDev* st, int64_t d, double* ws) {
+                           float floor_, CgDev* st, int64_t d, double* ws, unsigned* ctr, int k, int maxiter,
+                           double tol) {
   if (st->done) return;
   double t[2] = {0.0, 0.0};
   GRID_STRIDE(i, d) {
@@ -462,11 +482,15 @@ __global__ void k_cg_rstab(const float* g, const float* ax, const float* x, floa
     t[1] += (double)ri * (minv_of(pre, i, lam, floor_) * ri);
   }
   write_partials<2>(ws, t);
+  if (grid_last(ctr)) r_final_body(ws, st, k, maxiter, 1, tol);
 }
-__global__ void k_cg_r_final(const double* ws, CgDev* st, int k, int maxiter, int stab, double tol) {
-  if (st->done) return;
-  double t[2];
-  sum_partials<2>(ws, t);
+CV_DEV void r_final_body(const double* ws, CgDev* st, int k, int maxiter, int stab, double tol) {
+  double t[2] = {0.0, 0.0};
+  for (int b = threadIdx.x; b < NB; b += NT) {
+    t[0] += __ldcg(ws + b * 8 + 0);
+    t[1] += __ldcg(ws + b * 8 + 1);
+  }
+  block_sum<2>(t);
   if (threadIdx.x == 0) {
     if (stab) st->gv++;
     const double relres = sqrt(t[0]) / st->bnorm;
@@ -539,23 +563,29 @@ void cg_solve(cv_ctx* ctx, cv_snap* s, int kind, const float* g, double lam, dou
   k_cg_p0<<<NB, NT, 0, sm>>>(r, precond, flam, ffl, st, d, p, ws);
   k_cg_p0_final<<<1, NT, 0, sm>>>(ws, st);
   ctx->launches += 4;
+  unsigned* ctr = ctx->amax_counter + 1;
   for (int k = 1; k <= maxiter; ++k) {
     const int is_stab = (stab > 0 && k % stab == 0) ? 1 : 0;
     mv(ctx, s, p, ap, &st->done);
-    k_cg_pap<<<NB, NT, 0, sm>>>(ap, p, flam, st, d, ws);
-    k_cg_pap_final<<<1, NT, 0, sm>>>(ws, st, k, is_stab);
-    ctx->launches += 2;
+    k_cg_pap<<<NB, NT, 0, sm>>>(ap, p, flam, st, d, ws, ctr, k, is_stab);
+    ctx->launches++;
     if (is_stab) {
       k_cg_xupdate<<<NB, NT, 0, sm>>>(x, p, st, d);
       ctx->launches++;
       mv(ctx, s, x, ap, &st->gv_skip);
-      k_cg_rstab<<<NB, NT, 0, sm>>>(g, ap, x, r, precond, flam, ffl, st, d, ws);
+      k_cg_rstab<<<NB, NT, 0, sm>>>(g, ap, x, r, precond, flam, ffl, st, d, ws, ctr, k, maxiter, tol);
     } else {
-      k_cg_update<<<NB, NT, 0, sm>>>(x, r, p, ap, precond, flam, ffl, st, d, ws);
+      k_cg_update<<<NB, NT, 0, sm>>>(x, r, p, ap, precond, flam, ffl, st, d, ws, ctr, k, maxiter, tol);
     }
-    k_cg_r_final<<<1, NT, 0, sm>>>(ws, st, k, maxiter, is_stab, tol);
-    k_cg_pnext<<<NB, NT, 0, sm>>>(r, precond, flam, ffl, st, d, p);
-    ctx->launches += 3;
+    ctx->launches++;
+    if (k == maxiter) break;  // the direction of a last iteration is never used
+    // p <- M^-1 r + beta p, fused with the next product's input scales
+    if (cg_pnext_amax(ctx, r, precond, flam, ffl, &st->alpha, &st->done, p, d, s->off, s->v_sc, s->prod_sc, s->n_prod)) {
+      s->v_ready = 1;
+    } else {
+      k_cg_pnext<<<NB, NT, 0, sm>>>(r, precond, flam, ffl, st, d, p);
+      ctx->launches++;
+    }
   }
   k_cg_finish<<<1, 1, 0, sm>>>(st, stats);
   ctx->launches++;

@@ -45,3 +45,20 @@ tot = sum(v[1] for v in agg.values())
 print(f"step {wall:.3f} ms (events), kernel busy {busy/1000/N:.3f} ms/step, kernel sum {tot/1000/N:.3f} ms/step")
 for name, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:40]:
     print(f"{t/1000/N:8.3f} ms/step  {n/N:6.1f}/step  {t/n:8.1f} us  {name[:110]}")
+
+# gaps between consecutive kernels (GPU idle), largest first, for one step in the middle
+ev = sorted(((e.time_range.start, e.time_range.end, e.name) for e in evs), key=lambda t: t[0])
+gaps = []
+for (s0, e0, n0), (s1, e1, n1) in zip(ev, ev[1:]):
+    if s1 - e0 > 15:
+        gaps.append((s1 - e0, n0[:50], n1[:50]))
+gaps.sort(reverse=True)
+tot_gap = sum(g[0] for g in gaps)
+print(f"gaps > 15 us: {len(gaps)/N:.1f}/step, {tot_gap/1000/N:.3f} ms/step")
+import collections as _c
+agg2 = _c.defaultdict(lambda: [0, 0.0])
+for g, a, b in gaps:
+    agg2[(a, b)][0] += 1
+    agg2[(a, b)][1] += g
+for (a, b), (n, t) in sorted(agg2.items(), key=lambda kv: -kv[1][1])[:15]:
+    print(f"{t/1000/N:7.3f} ms/step {n/N:5.1f}/step  after {a}  before {b}")
