@@ -3,11 +3,43 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <math.h>
+#include <stdlib.h>
 #include <cuda_fp16.h>
 
 #define CV_DEV __device__ __forceinline__
 
+// Programmatic dependent launch: every kernel is launched with programmatic
+// stream serialization (launch_k) and starts by waiting for its predecessor grid
+// (full completion + memory flush, so RAW/WAR hazards are as with plain stream
+// order) and then allowing its own successor to be scheduled.  The successor's
+// launch and prologue thus overlap this kernel's tail instead of following it.
+#define CV_PDL_ENTRY()                                        \
+  do {                                                        \
+    asm volatile("griddepcontrol.wait;" ::: "memory");        \
+    asm volatile("griddepcontrol.launch_dependents;" :::);    \
+  } while (0)
+
 namespace cv {
+
+inline int pdl_enabled() {
+  static const int on = !(getenv("CURVOPT_PDL") && getenv("CURVOPT_PDL")[0] == '0');
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(cudaStream_t st, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, args...);
+}
 
 constexpr int kRedBlocks = 592;    // 4 x 148 SMs; fixed => deterministic reductions
 constexpr int kRedThreads = 256;

@@ -8,6 +8,7 @@
 namespace cv {
 
 __global__ void k_fill_split(__half* hi, __half* lo, int64_t n, uint32_t seed) {
+  CV_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     uint32_t h = (uint32_t)i * 2654435761u ^ seed;
     h ^= h >> 13;
@@ -19,6 +20,7 @@ __global__ void k_fill_split(__half* hi, __half* lo, int64_t n, uint32_t seed) {
 }
 
 __global__ void k_set_scale(Scale* sc, int n, float amax) {
+  CV_PDL_ENTRY();
   if (threadIdx.x < n) {
     sc[threadIdx.x].e = 0;
     sc[threadIdx.x].amax = amax;
@@ -44,10 +46,10 @@ extern "C" __attribute__((visibility("default"))) int cv_gemm_bench(cv_ctx* ctx,
     Scale* sc = (Scale*)ctx->pool.get(sizeof(Scale) * 4);
     __half *ahi = buf, *alo = ahi + na, *bhi = alo + na, *blo = bhi + nb, *mhi = blo + nb, *mlo = mhi + no,
            *ohi = mlo + no, *olo = ohi + no;
-    k_fill_split<<<1024, 256, 0, ctx->stream>>>(ahi, alo, na, 1u);
-    k_fill_split<<<1024, 256, 0, ctx->stream>>>(bhi, blo, nb, 2u);
-    k_fill_split<<<1024, 256, 0, ctx->stream>>>(mhi, mlo, no, 3u);
-    k_set_scale<<<1, 32, 0, ctx->stream>>>(sc, 4, 1024.f);
+    launch_k(ctx->stream, k_fill_split, 1024, 256, 0, ahi, alo, na, 1u);
+    launch_k(ctx->stream, k_fill_split, 1024, 256, 0, bhi, blo, nb, 2u);
+    launch_k(ctx->stream, k_fill_split, 1024, 256, 0, mhi, mlo, no, 3u);
+    launch_k(ctx->stream, k_set_scale, 1, 32, 0, sc, 4, 1024.f);
     GemmArgs g;
     g.M = M;
     g.N = N;
@@ -107,6 +109,7 @@ extern "C" __attribute__((visibility("default"))) int cv_gemm_bench(cv_ctx* ctx,
 
 namespace cv {
 __global__ void k_scale_copy(const float* x, float s, int64_t n, float* y) {
+  CV_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     y[i] = x[i] * s;
 }
@@ -126,7 +129,7 @@ extern "C" __attribute__((visibility("default"))) int cv_gemm_test_seg2(cv_ctx* 
     float* b2 = (float*)ctx->pool.get(sizeof(float) * (size_t)nb);
     Scale* sc = (Scale*)ctx->pool.get(sizeof(Scale) * 3);
     __half *ahi = buf, *alo = ahi + na, *bhi = alo + na, *blo = bhi + nb, *b2hi = blo + nb, *b2lo = b2hi + nb;
-    k_scale_copy<<<1024, 256, 0, ctx->stream>>>(b, s2, nb, b2);
+    launch_k(ctx->stream, k_scale_copy, 1024, 256, 0, b, s2, nb, b2);
     split_mat(ctx, a, K, M, K, ahi, alo, K, 0, sc, 0, nullptr);
     split_mat(ctx, b, K, N, K, bhi, blo, K, 0, sc + 1, 0, nullptr);
     split_mat(ctx, b2, K, N, K, b2hi, b2lo, K, 0, sc + 2, 0, nullptr);

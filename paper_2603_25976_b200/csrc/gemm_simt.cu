@@ -12,6 +12,7 @@ namespace cv {
 constexpr int SB_M = 64, SB_N = 64, SB_K = 16;
 
 __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs a) {
+  CV_PDL_ENTRY();
   if (skip_if(a.skip)) return;
   if (a.lower_only && (int)(blockIdx.x * SB_N) > (int)(blockIdx.y * SB_M + SB_M - 1)) return;
   __shared__ __align__(16) float As[SB_K][SB_M + 4];
@@ -77,7 +78,7 @@ __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs a) {
 void gemm_simt(cv_ctx* ctx, const GemmArgs& a) {
   if (a.M <= 0 || a.N <= 0) return;
   dim3 grid((a.N + SB_N - 1) / SB_N, (a.M + SB_M - 1) / SB_M);
-  k_gemm_simt<<<grid, 256, 0, ctx->stream>>>(a);
+  launch_k(ctx->stream, k_gemm_simt, grid, 256, 0, a);
   ctx->launches++;
 }
 

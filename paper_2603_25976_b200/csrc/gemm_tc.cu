@@ -486,6 +486,7 @@ CV_DEV void load_slab(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, bool 
 // mainloop of item i+1.
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(320, 1) k_gemm_tc(const __grid_constant__ TcMaps maps, const TcArgs a) {
+  CV_PDL_ENTRY();
   using Cfg = TcCfg<BN, STAGES>;
   if (skip_if(a.skip)) return;
   extern __shared__ uint8_t smem_raw[];
@@ -616,6 +617,7 @@ __global__ void __launch_bounds__(320, 1) k_gemm_tc(const __grid_constant__ TcMa
 // split-K reduction in fixed order, then the real epilogue
 __global__ void k_splitk_reduce(const float* partial, int splits, int M, int N, Epilogue epi, const int* skip,
                                 int lower_only) {
+  CV_PDL_ENTRY();
   if (skip_if(skip)) return;
   const EpiRt rt = epi_prepare(epi);
   if (blockIdx.x == 0 && threadIdx.x == 0) epi_publish(epi, rt);
@@ -873,10 +875,10 @@ static int launch_tc(cv_ctx* ctx, const GemmArgs& g, int splits, float* ext_part
   setup_out(g, maps, a, a.partial, splits);
   const int work = a.tiles_m * a.tiles_n * splits;
   const int grid = work < ctx->sm_count ? work : ctx->sm_count;
-  k_gemm_tc<BN, STAGES><<<grid, Cfg::THREADS, Cfg::SMEM, ctx->stream>>>(maps, a);
+  launch_k(ctx->stream, k_gemm_tc<BN, STAGES>, grid, Cfg::THREADS, Cfg::SMEM, maps, a);
   ctx->launches++;
   if (part) {
-    k_splitk_reduce<<<4 * ctx->sm_count, 256, 0, ctx->stream>>>(part, splits, g.M, g.N, g.epi, g.skip, g.lower_only);
+    launch_k(ctx->stream, k_splitk_reduce, 4 * ctx->sm_count, 256, 0, part, splits, g.M, g.N, g.epi, g.skip, g.lower_only);
     ctx->launches++;
     ctx->pool.put(part);  // stream-ordered reuse: later users enqueue after this kernel
   }

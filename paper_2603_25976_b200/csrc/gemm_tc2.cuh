@@ -60,6 +60,7 @@ CV_DEV void load_slab_2sm(uint8_t* dst, const CUtensorMap* map, uint32_t bar, bo
 template <int STAGES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     k_gemm_tc2(const __grid_constant__ TcMaps maps, const TcArgs a) {
+  CV_PDL_ENTRY();
   using Cfg = Tc2Cfg<STAGES>;
   if (skip_if(a.skip)) return;  // the flag is identical for both CTAs of the pair
   extern __shared__ uint8_t smem_raw[];
@@ -220,10 +221,10 @@ static void launch_tc2(cv_ctx* ctx, const GemmArgs& g, int splits) {
   const int work = a.tiles_m * a.tiles_n * splits;
   const int pairs = ctx->sm_count / 2;
   const int grid = 2 * (work < pairs ? work : pairs);
-  k_gemm_tc2<STAGES><<<grid, 320, Cfg::SMEM, ctx->stream>>>(maps, a);
+  launch_k(ctx->stream, k_gemm_tc2<STAGES>, grid, 320, Cfg::SMEM, maps, a);
   ctx->launches++;
   if (splits > 1) {
-    k_splitk_reduce<<<4 * ctx->sm_count, 256, 0, ctx->stream>>>(part, splits, g.M, g.N, g.epi, g.skip, g.lower_only);
+    launch_k(ctx->stream, k_splitk_reduce, 4 * ctx->sm_count, 256, 0, part, splits, g.M, g.N, g.epi, g.skip, g.lower_only);
     ctx->launches++;
     ctx->pool.put(part);
   }

@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(256) k_loss_rows(const float* __restrict__ log
                                                    const int64_t* __restrict__ yi, const float* __restrict__ yf,
                                                    float* probs, float* gout, float inv_b, double* partial,
                                                    int write_state, float* gout_amax) {
+  CV_PDL_ENTRY();
   double part[1] = {0.0};
   float amax = 0.f;
   for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < rows; m += gridDim.x * blockDim.x) {
@@ -86,6 +87,7 @@ __global__ void __launch_bounds__(256) k_loss_rows(const float* __restrict__ log
 
 // Sum nblk partials in fixed order, scale, store to *out (device double).
 __global__ void k_finalize_sum(const double* partial, int nblk, double scale, double* out) {
+  CV_PDL_ENTRY();
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int i = 0; i < nblk; ++i) s += partial[i];
@@ -99,6 +101,7 @@ __global__ void k_finalize_sum(const double* partial, int nblk, double scale, do
 // (rows x c, ld c) split block -> transposed, padded (cp x ldo) split, same exponent
 __global__ void k_pad_t(const __half* hi, const __half* lo, int rows, int c, int cp, int64_t ldo, __half* ohi,
                         __half* olo, const int* skip) {
+  CV_PDL_ENTRY();
   if (skip_if(skip)) return;
   const int64_t total = (int64_t)cp * rows;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -118,6 +121,7 @@ __global__ void k_pad_t(const __half* hi, const __half* lo, int rows, int c, int
 template <int CM>
 __global__ void k_out_reduce(const float* part, int splits, int rows, int c, int post, int loss, const float* probs,
                              float scale, float* out, float* out_amax, const int* skip) {
+  CV_PDL_ENTRY();
   if (skip_if(skip)) return;
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   float amax = 0.f;
@@ -195,7 +199,7 @@ static void pad_last(cv_ctx* ctx, cv_snap* s, const __half* hi, const __half* lo
                      const int* skip) {
   const int l = s->L - 1;
   const int rows = s->dims[l] + 1;
-  k_pad_t<<<grid_for((int64_t)rows * s->cp), 256, 0, ctx->stream>>>(hi + s->off[l], lo + s->off[l], rows, s->c, s->cp,
+  launch_k(ctx->stream, k_pad_t, grid_for((int64_t)rows * s->cp), 256, 0, hi + s->off[l], lo + s->off[l], rows, s->c, s->cp,
                                                                      s->ldw, ohi, olo, skip);
   ctx->launches++;
 }
@@ -469,10 +473,10 @@ static void jvp_out(cv_ctx* ctx, cv_snap* s, int post, float scale, float* out, 
     const int splits = gemm_tc_partial(ctx, g, &part);
     const bool hz = post == POST_HZ;
     if (s->c <= 16)
-      k_out_reduce<16><<<(s->bl + 127) / 128, 128, 0, ctx->stream>>>(part, splits, s->bl, s->c, hz, s->loss, s->probs,
+      launch_k(ctx->stream, k_out_reduce<16>, (s->bl + 127) / 128, 128, 0, part, splits, s->bl, s->c, hz, s->loss, s->probs,
                                                                     scale, out, out_amax, skip);
     else
-      k_out_reduce<32><<<(s->bl + 127) / 128, 128, 0, ctx->stream>>>(part, splits, s->bl, s->c, hz, s->loss, s->probs,
+      launch_k(ctx->stream, k_out_reduce<32>, (s->bl + 127) / 128, 128, 0, part, splits, s->bl, s->c, hz, s->loss, s->probs,
                                                                     scale, out, out_amax, skip);
     ctx->launches++;
     ctx->pool.put(part);
@@ -624,12 +628,12 @@ void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* v, float* out, const int* ski
 
 void mlp_loss(cv_ctx* ctx, cv_snap* s, const float* logits, int write_state, double* loss_out) {
   const int nblk = 64;
-  k_loss_rows<<<nblk, 256, 0, ctx->stream>>>(logits, s->bl, s->c, s->loss, s->y_i, s->y_f, s->probs, s->gout,
+  launch_k(ctx->stream, k_loss_rows, nblk, 256, 0, logits, s->bl, s->c, s->loss, s->y_i, s->y_f, s->probs, s->gout,
                                              1.0f / (float)s->bg, ctx->red_ws, write_state, &s->gout_sc->amax);
   if (write_state && s->tc_out)
     split_mat(ctx, s->gout, s->c, s->bl, s->c, s->gout_hi, s->gout_lo, s->ldb, 1, s->gout_sc, 1, nullptr);
   const double scale = 1.0 / (double)s->bg;
-  k_finalize_sum<<<1, 32, 0, ctx->stream>>>(ctx->red_ws, nblk, ctx->nccl ? 1.0 : scale, loss_out);
+  launch_k(ctx->stream, k_finalize_sum, 1, 32, 0, ctx->red_ws, nblk, ctx->nccl ? 1.0 : scale, loss_out);
   ctx->launches += 2;
   if (ctx->nccl) {
     allreduce_f64(ctx, loss_out, 1);

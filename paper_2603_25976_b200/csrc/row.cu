@@ -22,6 +22,7 @@ constexpr int CH_NB = 64;  // Cholesky block size
 template <int CM>
 __global__ void k_hz_roots(const float* logits, const int64_t* yi, const float* yf, int b, int c, int loss,
                            float* seeds, float* pinv, float* rhs) {
+  CV_PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= b) return;
   const size_t cc = (size_t)c * c;
@@ -120,6 +121,7 @@ __global__ void k_hz_roots(const float* logits, const int64_t* yi, const float* 
 
 // cot[i, a] = sum_j seeds[i, a, j] u[i, j]  (curvature.py:58-59)
 __global__ void k_seed_apply(const float* seeds, const float* u, int b, int c, float* out) {
+  CV_PDL_ENTRY();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= (int64_t)b * c) return;
   const int64_t i = e / c;
@@ -142,10 +144,10 @@ static void ensure_seeds(cv_ctx* ctx, cv_snap* s) {
   s->pinv = snap_alloc(s, (int64_t)b * c * c);
   s->rhs = snap_alloc(s, (int64_t)b * c);
   if (c <= 16)
-    k_hz_roots<16><<<(b + 63) / 64, 64, 0, ctx->stream>>>(s->logits, s->y_i, s->y_f, b, c, s->loss, s->seeds,
+    launch_k(ctx->stream, k_hz_roots<16>, (b + 63) / 64, 64, 0, s->logits, s->y_i, s->y_f, b, c, s->loss, s->seeds,
                                                           s->pinv, s->rhs);
   else
-    k_hz_roots<32><<<(b + 31) / 32, 32, 0, ctx->stream>>>(s->logits, s->y_i, s->y_f, b, c, s->loss, s->seeds,
+    launch_k(ctx->stream, k_hz_roots<32>, (b + 31) / 32, 32, 0, s->logits, s->y_i, s->y_f, b, c, s->loss, s->seeds,
                                                           s->pinv, s->rhs);
   ctx->launches++;
   s->row_state |= 1;
@@ -267,6 +269,7 @@ void row_gram(cv_ctx* ctx, cv_snap* s, float* gram_out) {
 // Blocked right-looking Cholesky, lower, in place on chol = gram + mu I.
 // ---------------------------------------------------------------------------
 __global__ void k_copy_add_diag(const float* src, float* dst, int64_t m, float mu) {
+  CV_PDL_ENTRY();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * m; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / m, j = e - i * m;
     dst[e] = src[e] + (i == j ? mu : 0.f);
@@ -277,6 +280,7 @@ __global__ void k_copy_add_diag(const float* src, float* dst, int64_t m, float m
 // and its inverse (fp32) into dinv[blk]; flag <- 1 if not positive definite.
 __global__ void __launch_bounds__(256) k_potrf_diag(float* A, int64_t lda, int j0, int nb, float* dinv_blk,
                                                     int* flag) {
+  CV_PDL_ENTRY();
   __shared__ double T[CH_NB][CH_NB + 1];
   __shared__ int bad;
   const int tid = threadIdx.x;
@@ -325,6 +329,7 @@ __global__ void __launch_bounds__(256) k_potrf_diag(float* A, int64_t lda, int j
 // forward substitution, one diagonal block: y_blk = Dinv (r_blk) ; then
 // r[j0+nb:] -= L[j0+nb:, blk] y_blk    (r, y in fp64)
 __global__ void k_trsv_fwd_diag(const float* dinv, int nb, int j0, double* r, double* y) {
+  CV_PDL_ENTRY();
   __shared__ double rb[CH_NB];
   const int t = threadIdx.x;
   if (t < nb) rb[t] = r[j0 + t];
@@ -336,6 +341,7 @@ __global__ void k_trsv_fwd_diag(const float* dinv, int nb, int j0, double* r, do
   }
 }
 __global__ void k_trsv_fwd_update(const float* A, int64_t lda, int64_t m, int j0, int nb, const double* y, double* r) {
+  CV_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int64_t row = j0 + nb + (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= m) return;
@@ -347,6 +353,7 @@ __global__ void k_trsv_fwd_update(const float* A, int64_t lda, int64_t m, int j0
 // backward: s_blk = L[j0+nb:, blk]^T v[j0+nb:]; v_blk = Dinv^T (y_blk - s_blk)
 __global__ void k_trsv_bwd_gather(const float* A, int64_t lda, int64_t m, int j0, int nb, const double* v,
                                   double* partial, int rows_per_block) {
+  CV_PDL_ENTRY();
   // partial[blockIdx.x * nb + k] = sum over this block's rows of A[row, j0+k] v[row]
   const int k = threadIdx.x;
   if (k >= nb) return;
@@ -357,6 +364,7 @@ __global__ void k_trsv_bwd_gather(const float* A, int64_t lda, int64_t m, int j0
 }
 __global__ void k_trsv_bwd_diag(const float* dinv, int nb, int j0, const double* y, const double* partial,
                                 int nparts, double* v) {
+  CV_PDL_ENTRY();
   __shared__ double rb[CH_NB];
   const int t = threadIdx.x;
   if (t < nb) {
@@ -373,6 +381,7 @@ __global__ void k_trsv_bwd_diag(const float* dinv, int nb, int j0, const double*
 }
 // r = rhs - (G + mu I) v, one warp per row, fp64 accumulation (refinement residual)
 __global__ void k_row_residual(const float* G, int64_t m, float mu, const float* rhs, const double* v, double* r) {
+  CV_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= m) return;
@@ -392,13 +401,16 @@ __global__ void k_row_residual(const float* G, int64_t m, float mu, const float*
 }
 
 __global__ void k_axpy_d(const double* x, double* y, int64_t n) {
+  CV_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) y[i] += x[i];
 }
 
 __global__ void k_f2d(const float* x, double* y, int64_t n) {
+  CV_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) y[i] = x[i];
 }
 __global__ void k_d2f(const double* x, float* y, int64_t n) {
+  CV_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) y[i] = (float)x[i];
 }
 
@@ -409,7 +421,7 @@ int row_solve_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, flo
   const int nblk = (int)((m + CH_NB - 1) / CH_NB);
   if (!s->dinv) s->dinv = snap_alloc(s, (int64_t)nblk * CH_NB * CH_NB);
   cudaStream_t st = ctx->stream;
-  k_copy_add_diag<<<4096, 256, 0, st>>>(s->gram, s->chol, m, (float)mu);
+  launch_k(st, k_copy_add_diag, 4096, 256, 0, s->gram, s->chol, m, (float)mu);
   int* flag = (int*)(ctx->scal_ws + 32);
   cudaMemsetAsync(flag, 0, sizeof(int), st);
   ctx->launches++;
@@ -417,7 +429,7 @@ int row_solve_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, flo
     const int j0 = bi * CH_NB;
     const int nb = (int)((m - j0) < CH_NB ? (m - j0) : CH_NB);
     float* dblk = s->dinv + (int64_t)bi * CH_NB * CH_NB;
-    k_potrf_diag<<<1, 256, 0, st>>>(s->chol, m, j0, nb, dblk, flag);
+    launch_k(st, k_potrf_diag, 1, 256, 0, s->chol, m, j0, nb, dblk, flag);
     ctx->launches++;
     const int rest = (int)(m - j0 - nb);
     if (rest <= 0) continue;
@@ -462,29 +474,29 @@ int row_solve_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, flo
     for (int bi = 0; bi < nblk; ++bi) {
       const int j0 = bi * CH_NB;
       const int nb = (int)((m - j0) < CH_NB ? (m - j0) : CH_NB);
-      k_trsv_fwd_diag<<<1, CH_NB, 0, st>>>(s->dinv + (int64_t)bi * CH_NB * CH_NB, nb, j0, r, y);
+      launch_k(st, k_trsv_fwd_diag, 1, CH_NB, 0, s->dinv + (int64_t)bi * CH_NB * CH_NB, nb, j0, r, y);
       const int64_t rest = m - j0 - nb;
-      if (rest > 0) k_trsv_fwd_update<<<(int)((rest + 7) / 8), 256, 0, st>>>(s->chol, m, m, j0, nb, y, r);
+      if (rest > 0) launch_k(st, k_trsv_fwd_update, (int)((rest + 7) / 8), 256, 0, s->chol, m, m, j0, nb, y, r);
     }
     for (int bi = nblk - 1; bi >= 0; --bi) {
       const int j0 = bi * CH_NB;
       const int nb = (int)((m - j0) < CH_NB ? (m - j0) : CH_NB);
       const int64_t rest = m - j0 - nb;
       const int nparts = (int)((rest + rpb - 1) / rpb);
-      if (nparts > 0) k_trsv_bwd_gather<<<nparts, CH_NB, 0, st>>>(s->chol, m, m, j0, nb, x, part, rpb);
-      k_trsv_bwd_diag<<<1, CH_NB, 0, st>>>(s->dinv + (int64_t)bi * CH_NB * CH_NB, nb, j0, y, part, nparts, x);
+      if (nparts > 0) launch_k(st, k_trsv_bwd_gather, nparts, CH_NB, 0, s->chol, m, m, j0, nb, x, part, rpb);
+      launch_k(st, k_trsv_bwd_diag, 1, CH_NB, 0, s->dinv + (int64_t)bi * CH_NB * CH_NB, nb, j0, y, part, nparts, x);
     }
     ctx->launches += 4 * nblk;
   };
-  k_f2d<<<256, 256, 0, st>>>(rhs, r, m);
+  launch_k(st, k_f2d, 256, 256, 0, rhs, r, m);
   tri_solve(v);
   for (int it = 0; it < 2; ++it) {
-    k_row_residual<<<(int)((m + 7) / 8), 256, 0, st>>>(s->gram, m, (float)mu, rhs, v, r);
+    launch_k(st, k_row_residual, (int)((m + 7) / 8), 256, 0, s->gram, m, (float)mu, rhs, v, r);
     tri_solve(dv);
-    k_axpy_d<<<256, 256, 0, st>>>(dv, v, m);
+    launch_k(st, k_axpy_d, 256, 256, 0, dv, v, m);
     ctx->launches += 2;
   }
-  k_d2f<<<256, 256, 0, st>>>(v, v_out, m);
+  launch_k(st, k_d2f, 256, 256, 0, v, v_out, m);
   ctx->launches += 2;
   ctx->pool.put(part);
   ctx->pool.put(r);
@@ -494,7 +506,7 @@ int row_solve_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, flo
 void row_backproject(cv_ctx* ctx, cv_snap* s, const float* v, float* out) {
   ensure_seeds(ctx, s);
   const int64_t m = (int64_t)s->bl * s->c;
-  k_seed_apply<<<(int)((m + 255) / 256), 256, 0, ctx->stream>>>(s->seeds, v, s->bl, s->c, s->U2);
+  launch_k(ctx->stream, k_seed_apply, (int)((m + 255) / 256), 256, 0, s->seeds, v, s->bl, s->c, s->U2);
   ctx->launches++;
   mlp_vjp(ctx, s, s->U2, out);
 }

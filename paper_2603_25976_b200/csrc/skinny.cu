@@ -32,6 +32,7 @@ CV_DEV void ld_join4(const __half* hi, const __half* lo, float inv, float (&x)[4
 // ---------------------------------------------------------------------------
 template <int CM, int RPW>
 __global__ void __launch_bounds__(256) k_rows(SkinnyRowsArgs a) {
+  CV_PDL_ENTRY();
   if (skip_if(a.skip)) return;
   constexpr int RK = 8192 / CM;  // K chunk: 32 KB of B^T
   __shared__ __align__(16) float Bt[CM][RK];
@@ -123,10 +124,10 @@ __global__ void __launch_bounds__(256) k_rows(SkinnyRowsArgs a) {
 void skinny_rows(cv_ctx* ctx, const SkinnyRowsArgs& a) {
   if (a.c <= 16) {
     constexpr int RPW = 4;
-    k_rows<16, RPW><<<(a.rows + 8 * RPW - 1) / (8 * RPW), 256, 0, ctx->stream>>>(a);
+    launch_k(ctx->stream, k_rows<16, RPW>, (a.rows + 8 * RPW - 1) / (8 * RPW), 256, 0, a);
   } else {
     constexpr int RPW = 2;
-    k_rows<32, RPW><<<(a.rows + 8 * RPW - 1) / (8 * RPW), 256, 0, ctx->stream>>>(a);
+    launch_k(ctx->stream, k_rows<32, RPW>, (a.rows + 8 * RPW - 1) / (8 * RPW), 256, 0, a);
   }
   ctx->launches++;
 }
@@ -139,6 +140,7 @@ void skinny_rows(cv_ctx* ctx, const SkinnyRowsArgs& a) {
 // ---------------------------------------------------------------------------
 template <int C, int NSEG, bool TANH>
 __global__ void __launch_bounds__(128) k_dx(SkinnyDxArgs a) {
+  CV_PDL_ENTRY();
   if (skip_if(a.skip)) return;
   constexpr int RT = 32;   // rows per tile
   constexpr int R = 8;     // rows per thread in flight
@@ -248,8 +250,8 @@ static void launch_dx(cv_ctx* ctx, const SkinnyDxArgs& a) {
   const int tiles = (a.rows + 31) / 32;
   int gy = (ctx->sm_count * 4 + gx - 1) / gx;  // ~4 resident 128-thread blocks per SM
   if (gy > tiles) gy = tiles;
-  if (a.epi.act == CV_ACT_TANH) k_dx<C, NSEG, true><<<dim3(gx, gy), 128, 0, ctx->stream>>>(a);
-  else k_dx<C, NSEG, false><<<dim3(gx, gy), 128, 0, ctx->stream>>>(a);
+  if (a.epi.act == CV_ACT_TANH) launch_k(ctx->stream, k_dx<C, NSEG, true>, dim3(gx, gy), 128, 0, a);
+  else launch_k(ctx->stream, k_dx<C, NSEG, false>, dim3(gx, gy), 128, 0, a);
 }
 
 void skinny_dx(cv_ctx* ctx, const SkinnyDxArgs& a) {
@@ -266,6 +268,7 @@ void skinny_dx(cv_ctx* ctx, const SkinnyDxArgs& a) {
 // ---------------------------------------------------------------------------
 template <int CM>
 __global__ void __launch_bounds__(128) k_dw_partial(SkinnyDwArgs a) {
+  CV_PDL_ENTRY();
   if (skip_if(a.skip)) return;
   constexpr int KT = 64;
   __shared__ float Us[KT][CM];
@@ -323,6 +326,7 @@ __global__ void __launch_bounds__(128) k_dw_partial(SkinnyDwArgs a) {
 }
 
 __global__ void k_dw_final(SkinnyDwArgs a) {
+  CV_PDL_ENTRY();
   if (skip_if(a.skip)) return;
   const int64_t total = (int64_t)a.M * a.c;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -342,10 +346,10 @@ void skinny_dw(cv_ctx* ctx, SkinnyDwArgs a, float* ws, int64_t ws_elems) {
   a.ksplit = ks;
   a.partial = ws;
   dim3 grid(mblocks, ks);
-  if (a.c <= 16) k_dw_partial<16><<<grid, 128, 0, ctx->stream>>>(a);
-  else k_dw_partial<32><<<grid, 128, 0, ctx->stream>>>(a);
+  if (a.c <= 16) launch_k(ctx->stream, k_dw_partial<16>, grid, 128, 0, a);
+  else launch_k(ctx->stream, k_dw_partial<32>, grid, 128, 0, a);
   const int64_t total = (int64_t)a.M * a.c;
-  k_dw_final<<<(int)((total + 255) / 256), 256, 0, ctx->stream>>>(a);
+  launch_k(ctx->stream, k_dw_final, (int)((total + 255) / 256), 256, 0, a);
   ctx->launches += 2;
 }
 

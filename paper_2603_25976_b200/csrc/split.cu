@@ -72,6 +72,7 @@ CV_DEV void flat_amax_finish(const OffTab& t, int* smax, float* sh, float* part,
 __global__ void __launch_bounds__(SP_NT) k_flat_amax(const float* __restrict__ x, OffTab t, float* part,
                                                      unsigned* counter, Scale* sc, Scale* zero_sc, int n_zero,
                                                      const int* skip) {
+  CV_PDL_ENTRY();
   if (skip_if(skip)) return;
   __shared__ float sh[SP_NT / 32];
   __shared__ int smax[SP_MAXL];
@@ -113,6 +114,7 @@ __global__ void __launch_bounds__(SP_NT) k_cg_pnext_amax(const float* __restrict
                                                          const int* done, float* __restrict__ p, OffTab t,
                                                          float* part, unsigned* counter, Scale* sc, Scale* zero_sc,
                                                          int n_zero) {
+  CV_PDL_ENTRY();
   if (*(volatile const int*)done) return;
   __shared__ float sh[SP_NT / 32];
   __shared__ int smax[SP_MAXL];
@@ -159,6 +161,7 @@ __global__ void __launch_bounds__(SP_NT) k_cg_pnext_amax(const float* __restrict
 __global__ void __launch_bounds__(SP_NT) k_flat_split(const float* __restrict__ x, OffTab t, const Scale* sc,
                                                       __half* __restrict__ hi, __half* __restrict__ lo,
                                                       const int* skip) {
+  CV_PDL_ENTRY();
   if (skip_if(skip)) return;
   for (int l = 0; l < t.L; ++l) {
     const float s = pow2f(sc[l].e);
@@ -197,9 +200,9 @@ void split_flat(cv_ctx* ctx, const float* x, int64_t d, const std::vector<int64_
     t.L = L - l0 < SP_MAXL ? L - l0 : SP_MAXL;
     for (int l = 0; l <= t.L; ++l) t.off[l] = l0 + l < L ? off[l0 + l] : d;
     const bool last = l0 + t.L >= L;
-    k_flat_amax<<<SP_NB, SP_NT, 0, ctx->stream>>>(x, t, part_of(ctx), counter_of(ctx), sc + l0,
+    launch_k(ctx->stream, k_flat_amax, SP_NB, SP_NT, 0, x, t, part_of(ctx), counter_of(ctx), sc + l0,
                                                   last ? zero_sc : nullptr, last ? n_zero : 0, skip);
-    k_flat_split<<<SP_NB, SP_NT, 0, ctx->stream>>>(x, t, sc + l0, hi, lo, skip);
+    launch_k(ctx->stream, k_flat_split, SP_NB, SP_NT, 0, x, t, sc + l0, hi, lo, skip);
     ctx->launches += 2;
   }
 }
@@ -215,7 +218,7 @@ static OffTab off_tab(const std::vector<int64_t>& off, int64_t d) {
 // split pass only (the scales were published by a fused producer)
 void split_flat_apply(cv_ctx* ctx, const float* x, int64_t d, const std::vector<int64_t>& off, __half* hi,
                       __half* lo, const Scale* sc, const int* skip) {
-  k_flat_split<<<SP_NB, SP_NT, 0, ctx->stream>>>(x, off_tab(off, d), sc, hi, lo, skip);
+  launch_k(ctx->stream, k_flat_split, SP_NB, SP_NT, 0, x, off_tab(off, d), sc, hi, lo, skip);
   ctx->launches++;
 }
 
@@ -223,7 +226,7 @@ bool cg_pnext_amax(cv_ctx* ctx, const float* r, const float* pre, float lam, flo
                    const int* done, float* p, int64_t d, const std::vector<int64_t>& off, Scale* sc, Scale* zero_sc,
                    int n_zero) {
   if ((int)off.size() > SP_MAXL) return false;
-  k_cg_pnext_amax<<<SP_NB, SP_NT, 0, ctx->stream>>>(r, pre, lam, floor_, beta, done, p, off_tab(off, d), part_of(ctx),
+  launch_k(ctx->stream, k_cg_pnext_amax, SP_NB, SP_NT, 0, r, pre, lam, floor_, beta, done, p, off_tab(off, d), part_of(ctx),
                                                     counter_of(ctx), sc, zero_sc, n_zero);
   ctx->launches++;
   return true;
@@ -236,6 +239,7 @@ bool cg_pnext_amax(cv_ctx* ctx, const float* r, const float* pre, float lam, flo
 __global__ void __launch_bounds__(SP_NT) k_mat_amax(const float* __restrict__ x, int64_t lds, int rows, int cols,
                                                     float floor_, float* part, unsigned* counter, Scale* sc,
                                                     const int* skip) {
+  CV_PDL_ENTRY();
   if (skip_if(skip)) return;
   __shared__ float sh[SP_NT / 32];
   // one warp per row, lanes over columns (128-bit when the rows are aligned)
@@ -282,6 +286,7 @@ __global__ void __launch_bounds__(SP_NT) k_mat_split(const float* __restrict__ x
                                                      int out_rows, int out_cols, int trans, int ones,
                                                      Scale* sc, int from_amax, __half* __restrict__ hi,
                                                      __half* __restrict__ lo, int64_t ldd, const int* skip) {
+  CV_PDL_ENTRY();
   if (skip_if(skip)) return;
   // from_amax: the producer accumulated max|x| in sc->amax; derive (and publish) e here
   const int e = from_amax ? exp_for_bound(sc->amax) : sc->e;
@@ -316,15 +321,15 @@ static int grid_for(int64_t n) {
 }
 
 void amax_into(cv_ctx* ctx, const float* x, int64_t n, Scale* slot) {
-  k_mat_amax<<<SP_NB, SP_NT, 0, ctx->stream>>>(x, n, 1, (int)n, 0.f, part_of(ctx), counter_of(ctx), slot, nullptr);
+  launch_k(ctx->stream, k_mat_amax, SP_NB, SP_NT, 0, x, n, 1, (int)n, 0.f, part_of(ctx), counter_of(ctx), slot, nullptr);
   ctx->launches++;
 }
 
 void split_rows(cv_ctx* ctx, const float* src, int64_t lds, int rows, int cols, const SplitBuf& dst, int ones) {
-  k_mat_amax<<<SP_NB, SP_NT, 0, ctx->stream>>>(src, lds, rows, cols, ones ? 1.f : 0.f, part_of(ctx),
+  launch_k(ctx->stream, k_mat_amax, SP_NB, SP_NT, 0, src, lds, rows, cols, ones ? 1.f : 0.f, part_of(ctx),
                                                counter_of(ctx), dst.sc, nullptr);
   const int oc = ones ? cols + 1 : cols;
-  k_mat_split<<<grid_for((int64_t)rows * oc), SP_NT, 0, ctx->stream>>>(src, lds, rows, cols, rows, oc, 0, ones, dst.sc,
+  launch_k(ctx->stream, k_mat_split, grid_for((int64_t)rows * oc), SP_NT, 0, src, lds, rows, cols, rows, oc, 0, ones, dst.sc,
                                                                       0, dst.hi, dst.lo, dst.ld, nullptr);
   ctx->launches += 2;
 }
@@ -334,18 +339,19 @@ void split_rows(cv_ctx* ctx, const float* src, int64_t lds, int rows, int cols, 
 void split_mat(cv_ctx* ctx, const float* src, int64_t lds, int rows, int cols, __half* hi, __half* lo, int64_t ldd,
                int trans, Scale* sc, int amax_ready, const int* skip) {
   if (!amax_ready) {
-    k_mat_amax<<<SP_NB, SP_NT, 0, ctx->stream>>>(src, lds, rows, cols, 0.f, part_of(ctx), counter_of(ctx), sc, skip);
+    launch_k(ctx->stream, k_mat_amax, SP_NB, SP_NT, 0, src, lds, rows, cols, 0.f, part_of(ctx), counter_of(ctx), sc, skip);
     ctx->launches++;
   }
   const int orows = trans ? (int)((cols + 15) / 16 * 16) : rows;
   const int ocols = trans ? rows : cols;
-  k_mat_split<<<grid_for((int64_t)orows * ocols), SP_NT, 0, ctx->stream>>>(src, lds, rows, cols, orows, ocols, trans, 0,
+  launch_k(ctx->stream, k_mat_split, grid_for((int64_t)orows * ocols), SP_NT, 0, src, lds, rows, cols, orows, ocols, trans, 0,
                                                                           sc, amax_ready, hi, lo, ldd, skip);
   ctx->launches++;
 }
 
 // column `col` of a split buffer := v (scaled by the buffer's exponent); amax covers |v|
 __global__ void k_set_col(__half* hi, __half* lo, int64_t ld, int rows, int col, float v, Scale* sc) {
+  CV_PDL_ENTRY();
   const float s = pow2f(sc->e);
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
     split16(v, s, hi[(int64_t)r * ld + col], lo[(int64_t)r * ld + col]);
@@ -353,12 +359,13 @@ __global__ void k_set_col(__half* hi, __half* lo, int64_t ld, int rows, int col,
 }
 
 void set_col_value(cv_ctx* ctx, const SplitBuf& b, int rows, int col, float v) {
-  k_set_col<<<grid_for(rows), SP_NT, 0, ctx->stream>>>(b.hi, b.lo, b.ld, rows, col, v, b.sc);
+  launch_k(ctx->stream, k_set_col, grid_for(rows), SP_NT, 0, b.hi, b.lo, b.ld, rows, col, v, b.sc);
   ctx->launches++;
 }
 
 __global__ void k_gather_rows(const __half* hi, const __half* lo, int64_t ld, int rows, int cols, const Scale* sc,
                               float* out) {
+  CV_PDL_ENTRY();
   const float inv = pow2f(-sc->e);
   const int64_t total = (int64_t)rows * cols;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -368,7 +375,7 @@ __global__ void k_gather_rows(const __half* hi, const __half* lo, int64_t ld, in
 }
 
 void gather_rows(cv_ctx* ctx, const SplitBuf& b, int rows, int cols, float* out) {
-  k_gather_rows<<<grid_for((int64_t)rows * cols), SP_NT, 0, ctx->stream>>>(b.hi, b.lo, b.ld, rows, cols, b.sc, out);
+  launch_k(ctx->stream, k_gather_rows, grid_for((int64_t)rows * cols), SP_NT, 0, b.hi, b.lo, b.ld, rows, cols, b.sc, out);
   ctx->launches++;
 }
 

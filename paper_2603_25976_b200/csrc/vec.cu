@@ -54,36 +54,40 @@ CV_DEV float rad(uint64_t seed, uint64_t counter, int64_t i) {
 }
 
 __global__ void k_rademacher(uint64_t seed, uint64_t counter, int64_t n, float scale, float* out) {
+  CV_PDL_ENTRY();
   GRID_STRIDE(i, n) out[i] = rad(seed, counter, i) * scale;
 }
 
 void rademacher(cv_ctx* ctx, uint64_t seed, uint64_t counter, int64_t n, float* out) {
-  k_rademacher<<<NB, NT, 0, ctx->stream>>>(seed, counter, n, 1.f, out);
+  launch_k(ctx->stream, k_rademacher, NB, NT, 0, seed, counter, n, 1.f, out);
   ctx->launches++;
 }
 
 // ---------------------------------------------------------------------------
 // small scalar utilities
 // ---------------------------------------------------------------------------
-__global__ void k_scale_scalar(double* x, double s) { *x *= s; }
+__global__ void k_scale_scalar(double* x, double s) {
+  CV_PDL_ENTRY(); *x *= s; }
 void scale_scalar(cv_ctx* ctx, double* x, double s) {
-  k_scale_scalar<<<1, 1, 0, ctx->stream>>>(x, s);
+  launch_k(ctx->stream, k_scale_scalar, 1, 1, 0, x, s);
   ctx->launches++;
 }
 
 __global__ void k_dot(const float* a, const float* b, int64_t n, double* ws) {
+  CV_PDL_ENTRY();
   double t[1] = {0.0};
   GRID_STRIDE(i, n) t[0] += (double)a[i] * (double)b[i];
   write_partials<1>(ws, t);
 }
 __global__ void k_dot_final(const double* ws, double* out) {
+  CV_PDL_ENTRY();
   double t[1];
   sum_partials<1>(ws, t);
   if (threadIdx.x == 0) *out = t[0];
 }
 void dot_into(cv_ctx* ctx, const float* a, const float* b, int64_t n, double* out) {
-  k_dot<<<NB, NT, 0, ctx->stream>>>(a, b, n, ctx->red_ws);
-  k_dot_final<<<1, NT, 0, ctx->stream>>>(ctx->red_ws, out);
+  launch_k(ctx->stream, k_dot, NB, NT, 0, a, b, n, ctx->red_ws);
+  launch_k(ctx->stream, k_dot_final, 1, NT, 0, ctx->red_ws, out);
   ctx->launches += 2;
 }
 
@@ -91,6 +95,7 @@ void dot_into(cv_ctx* ctx, const float* a, const float* b, int64_t n, double* ou
 // (method.py:345-357; the all-`scale` chain collapses to one coefficient)
 __global__ void k_apply_update(const float* w, const float* dir, float coef, int64_t d, float* upd, float* wn,
                                double* ws) {
+  CV_PDL_ENTRY();
   double t[3] = {0.0, 0.0, 0.0};
   GRID_STRIDE(i, d) {
     const float di = dir[i];
@@ -105,18 +110,20 @@ __global__ void k_apply_update(const float* w, const float* dir, float coef, int
   write_partials<3>(ws, t);
 }
 __global__ void k_apply_update_final(const double* ws, double* scal) {
+  CV_PDL_ENTRY();
   double t[3];
   sum_partials<3>(ws, t);
   if (threadIdx.x == 0) { scal[0] = sqrt(t[0]); scal[1] = t[1]; scal[2] = t[2]; }
 }
 void apply_update(cv_ctx* ctx, const float* w, const float* dir, double coef, int64_t d, float* upd, float* wn,
                   double* scal) {
-  k_apply_update<<<NB, NT, 0, ctx->stream>>>(w, dir, (float)coef, d, upd, wn, ctx->red_ws);
-  k_apply_update_final<<<1, NT, 0, ctx->stream>>>(ctx->red_ws, scal);
+  launch_k(ctx->stream, k_apply_update, NB, NT, 0, w, dir, (float)coef, d, upd, wn, ctx->red_ws);
+  launch_k(ctx->stream, k_apply_update_final, 1, NT, 0, ctx->red_ws, scal);
   ctx->launches += 2;
 }
 
 __global__ void k_norm_check(const float* x, int64_t d, double* ws) {
+  CV_PDL_ENTRY();
   double t[2] = {0.0, 0.0};
   GRID_STRIDE(i, d) {
     const float v = x[i];
@@ -126,18 +133,20 @@ __global__ void k_norm_check(const float* x, int64_t d, double* ws) {
   write_partials<2>(ws, t);
 }
 __global__ void k_norm_check_final(const double* ws, double* scal) {
+  CV_PDL_ENTRY();
   double t[2];
   sum_partials<2>(ws, t);
   if (threadIdx.x == 0) { scal[0] = t[0]; scal[1] = t[1]; }
 }
 void norm_check(cv_ctx* ctx, const float* x, int64_t d, double* scal) {
-  k_norm_check<<<NB, NT, 0, ctx->stream>>>(x, d, ctx->red_ws);
-  k_norm_check_final<<<1, NT, 0, ctx->stream>>>(ctx->red_ws, scal);
+  launch_k(ctx->stream, k_norm_check, NB, NT, 0, x, d, ctx->red_ws);
+  launch_k(ctx->stream, k_norm_check_final, 1, NT, 0, ctx->red_ws, scal);
   ctx->launches += 2;
 }
 
 // diag EMA (control.py:70-77) / floored store (method.py:407-408) + mean (method.py:409)
 __global__ void k_diag_ema(float* diag, const float* est, float beta, int64_t d, int mode, double* ws) {
+  CV_PDL_ENTRY();
   double t[1] = {0.0};
   GRID_STRIDE(i, d) {
     const float e = est[i];
@@ -148,15 +157,16 @@ __global__ void k_diag_ema(float* diag, const float* est, float beta, int64_t d,
   write_partials<1>(ws, t);
 }
 __global__ void k_mean_final(const double* ws, double inv_n, double* out) {
+  CV_PDL_ENTRY();
   double t[1];
   sum_partials<1>(ws, t);
   if (threadIdx.x == 0) *out = t[0] * inv_n;
 }
 void diag_ema(cv_ctx* ctx, float* diag, const float* est, double beta, int64_t d, int mode, double* mean) {
-  k_diag_ema<<<NB, NT, 0, ctx->stream>>>(diag, est, (float)beta, d, mode, ctx->red_ws);
+  launch_k(ctx->stream, k_diag_ema, NB, NT, 0, diag, est, (float)beta, d, mode, ctx->red_ws);
   ctx->launches++;
   if (mean) {
-    k_mean_final<<<1, NT, 0, ctx->stream>>>(ctx->red_ws, 1.0 / (double)d, mean);
+    launch_k(ctx->stream, k_mean_final, 1, NT, 0, ctx->red_ws, 1.0 / (double)d, mean);
     ctx->launches++;
   }
 }
@@ -167,6 +177,7 @@ void diag_ema(cv_ctx* ctx, float* diag, const float* est, double beta, int64_t d
 // ---------------------------------------------------------------------------
 __global__ void k_hutch_acc(uint64_t seed, uint64_t counter, const float* hz, int64_t d, float* diag, int first,
                             int last, float inv_n, double* ws) {
+  CV_PDL_ENTRY();
   double t[1] = {0.0};
   GRID_STRIDE(i, d) {
     const float z = rad(seed, counter, i);
@@ -181,6 +192,7 @@ __global__ void k_hutch_acc(uint64_t seed, uint64_t counter, const float* hz, in
   write_partials<1>(ws, t);
 }
 __global__ void k_trace_final(const double* ws, double inv_n, double* out, int first) {
+  CV_PDL_ENTRY();
   double t[1];
   sum_partials<1>(ws, t);
   if (threadIdx.x == 0) *out = (first ? 0.0 : *out) + t[0] * inv_n;
@@ -203,11 +215,11 @@ void hutchinson(cv_ctx* ctx, cv_snap* s, int kind, uint64_t seed, uint64_t count
     const uint64_t ctr = counter + (uint64_t)j * (uint64_t)s->d;
     rademacher(ctx, seed, ctr, s->d, z);
     mv(ctx, s, z, hz, nullptr);
-    k_hutch_acc<<<NB, NT, 0, ctx->stream>>>(seed, ctr, hz, s->d, diag, j == 0, j == n_probes - 1,
+    launch_k(ctx->stream, k_hutch_acc, NB, NT, 0, seed, ctr, hz, s->d, diag, j == 0, j == n_probes - 1,
                                             1.f / (float)n_probes, ctx->red_ws);
     ctx->launches++;
     if (trace) {
-      k_trace_final<<<1, NT, 0, ctx->stream>>>(ctx->red_ws, 1.0 / (double)n_probes, trace, j == 0);
+      launch_k(ctx->stream, k_trace_final, 1, NT, 0, ctx->red_ws, 1.0 / (double)n_probes, trace, j == 0);
       ctx->launches++;
     }
   }
@@ -218,8 +230,10 @@ void hutchinson(cv_ctx* ctx, cv_snap* s, int kind, uint64_t seed, uint64_t count
 // ---------------------------------------------------------------------------
 struct PiDev { double ray, result; int done; };
 
-__global__ void k_pi_init(PiDev* st) { st->ray = 0.0; st->result = 0.0; st->done = 0; }
+__global__ void k_pi_init(PiDev* st) {
+  CV_PDL_ENTRY(); st->ray = 0.0; st->result = 0.0; st->done = 0; }
 __global__ void k_pi_reduce(const float* v, const float* hv, int64_t d, double* ws, const int* skip) {
+  CV_PDL_ENTRY();
   if (skip_if(skip)) return;
   double t[2] = {0.0, 0.0};
   GRID_STRIDE(i, d) {
@@ -229,6 +243,7 @@ __global__ void k_pi_reduce(const float* v, const float* hv, int64_t d, double* 
   write_partials<2>(ws, t);
 }
 __global__ void k_pi_final(const double* ws, PiDev* st, double* norm_out) {
+  CV_PDL_ENTRY();
   if (st->done) return;
   double t[2];
   sum_partials<2>(ws, t);
@@ -241,29 +256,31 @@ __global__ void k_pi_final(const double* ws, PiDev* st, double* norm_out) {
   }
 }
 __global__ void k_pi_next(const float* hv, const double* nrm, int64_t d, float* v, const int* skip) {
+  CV_PDL_ENTRY();
   if (skip_if(skip)) return;
   GRID_STRIDE(i, d) v[i] = (float)((double)hv[i] / *nrm);
 }
-__global__ void k_pi_out(const PiDev* st, double* out) { *out = st->result; }
+__global__ void k_pi_out(const PiDev* st, double* out) {
+  CV_PDL_ENTRY(); *out = st->result; }
 
 void power_iter(cv_ctx* ctx, cv_snap* s, int kind, uint64_t seed, uint64_t counter, int iters, double* eig) {
   float* v = snap_tmp(s, &s->tmp_d);
   float* hv = snap_tmp(s, &s->tmp_d2);
   PiDev* st = (PiDev*)ctx->scal_ws;
   double* nrm = ctx->scal_ws + 4;
-  k_pi_init<<<1, 1, 0, ctx->stream>>>(st);
+  launch_k(ctx->stream, k_pi_init, 1, 1, 0, st);
   const float scale = (float)(1.0 / sqrt((double)s->d));
-  k_rademacher<<<NB, NT, 0, ctx->stream>>>(seed, counter, s->d, scale, v);
+  launch_k(ctx->stream, k_rademacher, NB, NT, 0, seed, counter, s->d, scale, v);
   ctx->launches += 2;
   MatvecFn mv = matvec_fn(kind);
   for (int it = 0; it < iters; ++it) {
     mv(ctx, s, v, hv, &st->done);
-    k_pi_reduce<<<NB, NT, 0, ctx->stream>>>(v, hv, s->d, ctx->red_ws, &st->done);
-    k_pi_final<<<1, NT, 0, ctx->stream>>>(ctx->red_ws, st, nrm);
-    k_pi_next<<<NB, NT, 0, ctx->stream>>>(hv, nrm, s->d, v, &st->done);
+    launch_k(ctx->stream, k_pi_reduce, NB, NT, 0, v, hv, s->d, ctx->red_ws, &st->done);
+    launch_k(ctx->stream, k_pi_final, 1, NT, 0, ctx->red_ws, st, nrm);
+    launch_k(ctx->stream, k_pi_next, NB, NT, 0, hv, nrm, s->d, v, &st->done);
     ctx->launches += 3;
   }
-  k_pi_out<<<1, 1, 0, ctx->stream>>>(st, eig);
+  launch_k(ctx->stream, k_pi_out, 1, 1, 0, st, eig);
   ctx->launches++;
 }
 
@@ -278,6 +295,7 @@ struct CgDev {
 };
 
 __global__ void k_cg_init(const float* g, const float* x0, int64_t d, double* ws) {
+  CV_PDL_ENTRY();
   double t[2] = {0.0, 0.0};
   GRID_STRIDE(i, d) {
     t[0] += (double)g[i] * g[i];
@@ -286,6 +304,7 @@ __global__ void k_cg_init(const float* g, const float* x0, int64_t d, double* ws
   write_partials<2>(ws, t);
 }
 __global__ void k_cg_init_final(const double* ws, CgDev* st) {
+  CV_PDL_ENTRY();
   double t[2];
   sum_partials<2>(ws, t);
   if (threadIdx.x == 0) {
@@ -301,12 +320,14 @@ __global__ void k_cg_init_final(const double* ws, CgDev* st) {
 }
 // x = x0 (if any nonzero entry) else 0
 __global__ void k_cg_setup_x(const float* x0, const CgDev* st, int64_t d, float* x) {
+  CV_PDL_ENTRY();
   const bool use = st->x0nz;
   GRID_STRIDE(i, d) x[i] = use ? x0[i] : 0.f;
 }
 // r = g - (Ax + lam x) (warm) or g; partial ||r||^2
 __global__ void k_cg_r0(const float* g, const float* ax, const float* x, float lam, const CgDev* st, int64_t d,
                         float* r, double* ws) {
+  CV_PDL_ENTRY();
   if (st->done) return;
   const bool warm = st->x0nz;
   double t[1] = {0.0};
@@ -318,6 +339,7 @@ __global__ void k_cg_r0(const float* g, const float* ax, const float* x, float l
   write_partials<1>(ws, t);
 }
 __global__ void k_cg_r0_final(const double* ws, CgDev* st, double tol) {
+  CV_PDL_ENTRY();
   if (st->done) return;
   double t[1];
   sum_partials<1>(ws, t);
@@ -331,6 +353,7 @@ __global__ void k_cg_r0_final(const double* ws, CgDev* st, double tol) {
 // p = z = M^-1 r; rz = r.z
 __global__ void k_cg_p0(const float* r, const float* pre, float lam, float floor_, const CgDev* st, int64_t d,
                         float* p, double* ws) {
+  CV_PDL_ENTRY();
   if (st->done) return;
   double t[1] = {0.0};
   GRID_STRIDE(i, d) {
@@ -342,6 +365,7 @@ __global__ void k_cg_p0(const float* r, const float* pre, float lam, float floor
   write_partials<1>(ws, t);
 }
 __global__ void k_cg_p0_final(const double* ws, CgDev* st) {
+  CV_PDL_ENTRY();
   if (st->done) return;
   double t[1];
   sum_partials<1>(ws, t);
@@ -355,6 +379,7 @@ CV_DEV void r_final_body(const double* ws, CgDev* st, int k, int maxiter, int st
 // block turns them into alpha and the termination flags (solvers.py:90-105)
 __global__ void k_cg_pap(float* ap, const float* p, float lam, CgDev* st, int64_t d, double* ws, unsigned* ctr, int k,
                          int stab) {
+  CV_PDL_ENTRY();
   if (st->done) return;
   double t[3] = {0.0, 0.0, 0.0};
   auto body = [&](float pi, float& a) {
@@ -435,6 +460,7 @@ CV_DEV void pap_final_body(const double* ws, CgDev* st, int k, int stab) {
 __global__ void k_cg_update(float* x, float* r, const float* p, const float* ap, const float* pre, float lam,
                             float floor_, CgDev* st, int64_t d, double* ws, unsigned* ctr, int k, int maxiter,
                             double tol) {
+  CV_PDL_ENTRY();
   if (st->done) return;
   const float a = (float)st->alpha;
   double t[2] = {0.0, 0.0};
@@ -465,6 +491,7 @@ __global__ void k_cg_update(float* x, float* r, const float* p, const float* ap,
 }
 // stabilising iteration: x += a p (the explicit residual product follows)
 __global__ void k_cg_xupdate(float* x, const float* p, const CgDev* st, int64_t d) {
+  CV_PDL_ENTRY();
   if (st->done) return;
   const float a = (float)st->alpha;
   GRID_STRIDE(i, d) x[i] += a * p[i];
@@ -473,6 +500,7 @@ __global__ void k_cg_xupdate(float* x, const float* p, const CgDev* st, int64_t 
 __global__ void k_cg_rstab(const float* g, const float* ax, const float* x, float* r, const float* pre, float lam,
                            float floor_, CgDev* st, int64_t d, double* ws, unsigned* ctr, int k, int maxiter,
                            double tol) {
+  CV_PDL_ENTRY();
   if (st->done) return;
   double t[2] = {0.0, 0.0};
   GRID_STRIDE(i, d) {
@@ -509,6 +537,7 @@ CV_DEV void r_final_body(const double* ws, CgDev* st, int k, int maxiter, int st
 // p = M^-1 r + beta p
 __global__ void k_cg_pnext(const float* r, const float* pre, float lam, float floor_, const CgDev* st, int64_t d,
                            float* p) {
+  CV_PDL_ENTRY();
   if (st->done) return;
   const float beta = (float)st->alpha;
   const int64_t nq = d >> 2;
@@ -526,6 +555,7 @@ __global__ void k_cg_pnext(const float* r, const float* pre, float lam, float fl
     p[i] = minv_of(pre, i, lam, floor_) * r[i] + beta * p[i];
 }
 __global__ void k_cg_finish(const CgDev* st, cv_cg_stats* out) {
+  CV_PDL_ENTRY();
   out->relres = st->relres;
   out->bnorm = st->bnorm;
   out->iterations = st->iters;
@@ -548,34 +578,34 @@ void cg_solve(cv_ctx* ctx, cv_snap* s, int kind, const float* g, double lam, dou
   const float flam = (float)lam, ffl = (float)floor;
   MatvecFn mv = matvec_fn(kind);
 
-  k_cg_init<<<NB, NT, 0, sm>>>(g, x0, d, ws);
-  k_cg_init_final<<<1, NT, 0, sm>>>(ws, st);
+  launch_k(sm, k_cg_init, NB, NT, 0, g, x0, d, ws);
+  launch_k(sm, k_cg_init_final, 1, NT, 0, ws, st);
   ctx->launches += 2;
   if (x0) {
-    k_cg_setup_x<<<NB, NT, 0, sm>>>(x0, st, d, x);
+    launch_k(sm, k_cg_setup_x, NB, NT, 0, x0, st, d, x);
     ctx->launches++;
     mv(ctx, s, x, ap, &st->gv_skip);
   } else {
     cudaMemsetAsync(x, 0, sizeof(float) * d, sm);
   }
-  k_cg_r0<<<NB, NT, 0, sm>>>(g, ap, x, flam, st, d, r, ws);
-  k_cg_r0_final<<<1, NT, 0, sm>>>(ws, st, tol);
-  k_cg_p0<<<NB, NT, 0, sm>>>(r, precond, flam, ffl, st, d, p, ws);
-  k_cg_p0_final<<<1, NT, 0, sm>>>(ws, st);
+  launch_k(sm, k_cg_r0, NB, NT, 0, g, ap, x, flam, st, d, r, ws);
+  launch_k(sm, k_cg_r0_final, 1, NT, 0, ws, st, tol);
+  launch_k(sm, k_cg_p0, NB, NT, 0, r, precond, flam, ffl, st, d, p, ws);
+  launch_k(sm, k_cg_p0_final, 1, NT, 0, ws, st);
   ctx->launches += 4;
   unsigned* ctr = ctx->amax_counter + 1;
   for (int k = 1; k <= maxiter; ++k) {
     const int is_stab = (stab > 0 && k % stab == 0) ? 1 : 0;
     mv(ctx, s, p, ap, &st->done);
-    k_cg_pap<<<NB, NT, 0, sm>>>(ap, p, flam, st, d, ws, ctr, k, is_stab);
+    launch_k(sm, k_cg_pap, NB, NT, 0, ap, p, flam, st, d, ws, ctr, k, is_stab);
     ctx->launches++;
     if (is_stab) {
-      k_cg_xupdate<<<NB, NT, 0, sm>>>(x, p, st, d);
+      launch_k(sm, k_cg_xupdate, NB, NT, 0, x, p, st, d);
       ctx->launches++;
       mv(ctx, s, x, ap, &st->gv_skip);
-      k_cg_rstab<<<NB, NT, 0, sm>>>(g, ap, x, r, precond, flam, ffl, st, d, ws, ctr, k, maxiter, tol);
+      launch_k(sm, k_cg_rstab, NB, NT, 0, g, ap, x, r, precond, flam, ffl, st, d, ws, ctr, k, maxiter, tol);
     } else {
-      k_cg_update<<<NB, NT, 0, sm>>>(x, r, p, ap, precond, flam, ffl, st, d, ws, ctr, k, maxiter, tol);
+      launch_k(sm, k_cg_update, NB, NT, 0, x, r, p, ap, precond, flam, ffl, st, d, ws, ctr, k, maxiter, tol);
     }
     ctx->launches++;
     if (k == maxiter) break;  // the direction of a last iteration is never used
@@ -583,11 +613,11 @@ void cg_solve(cv_ctx* ctx, cv_snap* s, int kind, const float* g, double lam, dou
     if (cg_pnext_amax(ctx, r, precond, flam, ffl, &st->alpha, &st->done, p, d, s->off, s->v_sc, s->prod_sc, s->n_prod)) {
       s->v_ready = 1;
     } else {
-      k_cg_pnext<<<NB, NT, 0, sm>>>(r, precond, flam, ffl, st, d, p);
+      launch_k(sm, k_cg_pnext, NB, NT, 0, r, precond, flam, ffl, st, d, p);
       ctx->launches++;
     }
   }
-  k_cg_finish<<<1, 1, 0, sm>>>(st, stats);
+  launch_k(sm, k_cg_finish, 1, 1, 0, st, stats);
   ctx->launches++;
 }
 
