@@ -92,6 +92,12 @@ int cv_ctx_destroy(cv_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   try { nccl_destroy(ctx); } catch (...) {}
+  if (ctx->side) {
+    cudaStreamSynchronize(ctx->side);
+    cudaStreamDestroy(ctx->side);
+    cudaEventDestroy(ctx->ev_fork);
+    cudaEventDestroy(ctx->ev_join);
+  }
   ctx->pool.release_all();
   delete ctx;
   return CV_OK;

@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs a) {
 void gemm_simt(cv_ctx* ctx, const GemmArgs& a) {
   if (a.M <= 0 || a.N <= 0) return;
   dim3 grid((a.N + SB_N - 1) / SB_N, (a.M + SB_M - 1) / SB_M);
-  launch_k(ctx->stream, k_gemm_simt, grid, 256, 0, a);
+  launch_k(a.stream ? a.stream : ctx->stream, k_gemm_simt, grid, 256, 0, a);
   ctx->launches++;
 }
 

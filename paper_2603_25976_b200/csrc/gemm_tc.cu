@@ -874,43 +874,93 @@ static int launch_tc(cv_ctx* ctx, const GemmArgs& g, int splits, float* ext_part
   }
   setup_out(g, maps, a, a.partial, splits);
   const int work = a.tiles_m * a.tiles_n * splits;
-  const int grid = work < ctx->sm_count ? work : ctx->sm_count;
-  launch_k(ctx->stream, k_gemm_tc<BN, STAGES>, grid, Cfg::THREADS, Cfg::SMEM, maps, a);
+  const int sms = g.max_ctas > 0 && g.max_ctas < ctx->sm_count ? g.max_ctas : ctx->sm_count;
+  const int grid = work < sms ? work : sms;
+  cudaStream_t st = g.stream ? g.stream : ctx->stream;
+  launch_k(st, k_gemm_tc<BN, STAGES>, grid, Cfg::THREADS, Cfg::SMEM, maps, a);
   ctx->launches++;
   if (part) {
-    launch_k(ctx->stream, k_splitk_reduce, 4 * ctx->sm_count, 256, 0, part, splits, g.M, g.N, g.epi, g.skip, g.lower_only);
+    launch_k(st, k_splitk_reduce, 4 * ctx->sm_count, 256, 0, part, splits, g.M, g.N, g.epi, g.skip, g.lower_only);
     ctx->launches++;
-    ctx->pool.put(part);  // stream-ordered reuse: later users enqueue after this kernel
+    if (st != ctx->stream) ctx->deferred.push_back(part);  // reused only after the join
+    else ctx->pool.put(part);  // stream-ordered reuse: later users enqueue after this kernel
   }
   return splits;
 }
 
 #include "gemm_tc2.cuh"
 
-void gemm_tc(cv_ctx* ctx, const GemmArgs& g) {
+// Tile configuration and split-K factor of a GEMM on `sms` SMs.
+struct TcPlan {
+  int kind;  // 0: <32,4>, 1: 2-CTA 256x256, 2: <256,2>, 3: <128,3>
+  int tiles, kb_total, splits;
+};
+
+static TcPlan tc_plan_kind(const GemmArgs& g, int sms, int kind) {
+  TcPlan p;
+  p.kind = kind;
+  const int bn = kind == 0 ? 32 : (kind == 3 ? 128 : 256);
+  const int bm = kind == 1 ? 256 : TC_BM;
+  p.tiles = ((g.M + bm - 1) / bm) * ((g.N + bn - 1) / bn);
+  const int slots = kind == 1 ? sms / 2 : sms;  // concurrent work items
+  p.kb_total = 0;
+  for (int s = 0; s < g.nseg; ++s) p.kb_total += (g.seg[s].K + TC_BK - 1) / TC_BK;
+  // split K when the tile grid cannot fill the machine (weight-gradient GEMMs: M, N ~ 1e3, K = batch)
+  p.splits = 1;
+  if (g.epi.mode == EPI_STORE && p.tiles < slots) {
+    p.splits = slots / p.tiles;
+    if (p.splits > p.kb_total / 4) p.splits = p.kb_total / 4;
+    if (p.splits < 1) p.splits = 1;
+  }
+  return p;
+}
+
+// relative time of a plan: rounds of work items x k-blocks per item (+ fill/epilogue),
+// per SM; a 2-CTA tile costs each SM what a 1-CTA 128 x 256 tile does
+static double plan_time(const TcPlan& p, int sms) {
+  const int slots = p.kind == 1 ? sms / 2 : sms;
+  const int items = p.tiles * p.splits;
+  const int rounds = (items + slots - 1) / slots;
+  const double item_kb = (double)((p.kb_total + p.splits - 1) / p.splits);
+  const double pen = p.kind == 2 ? 1.3 : (p.kind == 3 ? 1.2 : 1.0);  // 2-stage ring / narrower tile (measured)
+  const double per_kb = p.kind == 3 ? 0.5 : 1.0;                        // 128 x 128 tile: half the MMA work
+  return rounds * (item_kb * per_kb * pen + 4.0);
+}
+
+static TcPlan tc_plan(const GemmArgs& g, int sms) {
   static const int force_bn = getenv("CURVOPT_TC_BN") ? atoi(getenv("CURVOPT_TC_BN")) : 0;
   static const int use_2sm = getenv("CURVOPT_TC_2SM") ? atoi(getenv("CURVOPT_TC_2SM")) : 1;
+  static const int force_kind = getenv("CURVOPT_TC_KIND") ? atoi(getenv("CURVOPT_TC_KIND")) : -1;
+  if (g.N <= 32) return tc_plan_kind(g, sms, 0);
+  if (force_kind >= 1 && force_kind <= 3) return tc_plan_kind(g, sms, force_kind);
   const bool pair = use_2sm && !force_bn && g.M >= 256 && g.N >= 256;
   const bool wide = force_bn ? force_bn == 256 : g.N >= 512;
-  const int tiles = pair ? ((g.M + 255) / 256) * ((g.N + 255) / 256) * 2
-                         : (wide ? (g.N + 255) / 256 : (g.N + 127) / 128) * ((g.M + TC_BM - 1) / TC_BM);
-  int kb_total = 0;
-  for (int s = 0; s < g.nseg; ++s) kb_total += (g.seg[s].K + TC_BK - 1) / TC_BK;
-  // split K when the tile grid cannot fill the machine (weight-gradient GEMMs: M, N ~ 1e3, K = batch)
-  int splits = 1;
-  if (g.epi.mode == EPI_STORE && tiles < ctx->sm_count) {
-    splits = ctx->sm_count / tiles;
-    if (splits > kb_total / 4) splits = kb_total / 4;
-    if (splits < 1) splits = 1;
+  TcPlan best = tc_plan_kind(g, sms, pair ? 1 : (wide ? 2 : 3));
+  if (g.epi.mode == EPI_STORE && !force_bn) {
+    // split-K weight gradients: the tile shape that wastes the least of the M edge
+    for (int k = 1; k <= 3; ++k) {
+      if (k == 1 && !pair) continue;
+      const TcPlan c = tc_plan_kind(g, sms, k);
+      if (plan_time(c, sms) < plan_time(best, sms)) best = c;
+    }
   }
-  if (g.N <= 32)
-    launch_tc<32, 4>(ctx, g, splits);
-  else if (pair)
-    launch_tc2<3>(ctx, g, splits);
-  else if (wide)
-    launch_tc<256, 2>(ctx, g, splits);
-  else
-    launch_tc<128, 3>(ctx, g, splits);
+  return best;
+}
+
+double gemm_tc_estimate(const cv_ctx* ctx, const GemmArgs& g, int ctas) {
+  (void)ctx;
+  return plan_time(tc_plan(g, ctas), ctas);
+}
+
+void gemm_tc(cv_ctx* ctx, const GemmArgs& g) {
+  const int sms = g.max_ctas > 0 && g.max_ctas < ctx->sm_count ? g.max_ctas : ctx->sm_count;
+  const TcPlan p = tc_plan(g, sms);
+  switch (p.kind) {
+    case 0: launch_tc<32, 4>(ctx, g, p.splits); break;
+    case 1: launch_tc2<3>(ctx, g, p.splits); break;
+    case 2: launch_tc<256, 2>(ctx, g, p.splits); break;
+    default: launch_tc<128, 3>(ctx, g, p.splits); break;
+  }
 }
 
 // Narrow (N <= 32) GEMM returning raw split-K partials [splits][M][N]: the output

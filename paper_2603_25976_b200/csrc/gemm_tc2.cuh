@@ -219,13 +219,16 @@ static void launch_tc2(cv_ctx* ctx, const GemmArgs& g, int splits) {
   }
   setup_out(g, maps, a, a.partial, splits);
   const int work = a.tiles_m * a.tiles_n * splits;
-  const int pairs = ctx->sm_count / 2;
+  const int sms = g.max_ctas > 0 && g.max_ctas < ctx->sm_count ? g.max_ctas : ctx->sm_count;
+  const int pairs = sms / 2;
   const int grid = 2 * (work < pairs ? work : pairs);
-  launch_k(ctx->stream, k_gemm_tc2<STAGES>, grid, 320, Cfg::SMEM, maps, a);
+  cudaStream_t st = g.stream ? g.stream : ctx->stream;
+  launch_k(st, k_gemm_tc2<STAGES>, grid, 320, Cfg::SMEM, maps, a);
   ctx->launches++;
   if (splits > 1) {
-    launch_k(ctx->stream, k_splitk_reduce, 4 * ctx->sm_count, 256, 0, part, splits, g.M, g.N, g.epi, g.skip, g.lower_only);
+    launch_k(st, k_splitk_reduce, 4 * ctx->sm_count, 256, 0, part, splits, g.M, g.N, g.epi, g.skip, g.lower_only);
     ctx->launches++;
-    ctx->pool.put(part);
+    if (st != ctx->stream) ctx->deferred.push_back(part);  // reused only after the join
+    else ctx->pool.put(part);
   }
 }

@@ -88,6 +88,8 @@ struct GemmArgs {
   Epilogue epi;
   const int* skip = nullptr;     // device flag: kernel returns immediately when != 0
   int lower_only = 0;            // only tiles intersecting the lower triangle (m >= n)
+  cudaStream_t stream = nullptr; // nullptr: the context stream
+  int max_ctas = 0;              // > 0: cap on the persistent grid (SM share when co-scheduled)
 };
 
 struct SplitBuf {
@@ -126,6 +128,9 @@ struct cv_ctx {
   float* amax_ws = nullptr;      // split.cu: per-block maxima (2 x 148 x 16 floats)
   unsigned* amax_counter = nullptr;  // split.cu: last-block counter (returns to 0 after each pass)
   int64_t launches = 0;
+  cudaStream_t side = nullptr;   // second stream for co-scheduled independent GEMMs
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  std::vector<void*> deferred;   // side-stream scratch, returned to the pool after the join
 };
 
 struct cv_snap {
@@ -209,6 +214,13 @@ void gemm_simt(cv_ctx* ctx, const GemmArgs& a);
 bool gemm_tc_supported(const GemmArgs& a);
 void gemm_tc(cv_ctx* ctx, const GemmArgs& a);
 void gemm(cv_ctx* ctx, const GemmArgs& a);  // engine dispatch
+// two independent GEMMs at once: a on the context stream, b on the side stream,
+// the SMs split between them by estimated time; returns when both are enqueued
+// (the context stream waits for b)
+void gemm_pair(cv_ctx* ctx, GemmArgs a, GemmArgs b);
+double gemm_tc_estimate(const cv_ctx* ctx, const GemmArgs& g, int ctas);  // relative time on `ctas` SMs
+cudaStream_t side_fork(cv_ctx* ctx);  // side stream ordered after the context stream's current work
+void side_join(cv_ctx* ctx);          // context stream waits for the side stream
 int gemm_tc_partial(cv_ctx* ctx, const GemmArgs& g, float** partial);  // N <= 32, raw split-K partials
 
 // runtime.cu

@@ -319,9 +319,9 @@ static void skinny_backward(cv_ctx* ctx, cv_snap* s, const float* U, Scale* usc,
 }
 
 // G_prev = (G_l W_l^T) * act'(a_l), hidden layer l >= 1
-static void hidden_backward(cv_ctx* ctx, cv_snap* s, int l, const SplitBuf& Gl, const __half* whi,
-                            const __half* wlo, const Scale* wsc, const SplitBuf& out, float* raw, Scale* raw_sc,
-                            const int* skip) {
+static GemmArgs hidden_backward_args(cv_snap* s, int l, const SplitBuf& Gl, const __half* whi, const __half* wlo,
+                                     const Scale* wsc, const SplitBuf& out, float* raw, Scale* raw_sc,
+                                     const int* skip) {
   GemmArgs g;
   g.M = s->bl;
   g.N = s->dims[l];
@@ -336,12 +336,12 @@ static void hidden_backward(cv_ctx* ctx, cv_snap* s, int l, const SplitBuf& Gl, 
   g.epi.raw_amax = raw_sc ? &raw_sc->amax : nullptr;
   bound_add(g.epi.bound, (float)s->dims[l + 1], Gl.sc, wsc + l);
   g.skip = skip;
-  gemm(ctx, g);
+  return g;
 }
 
 // [gW; gb]_l = A_l^T G (+ A2^T G2), written into out + off[l] (hidden layers).
-static void weight_grad(cv_ctx* ctx, cv_snap* s, int l, const SplitBuf& G1, const SplitBuf* A2,
-                        const SplitBuf* G2, float* out, const int* skip) {
+static GemmArgs weight_grad_args(cv_snap* s, int l, const SplitBuf& G1, const SplitBuf* A2, const SplitBuf* G2,
+                                 float* out, const int* skip) {
   GemmArgs g;
   g.M = s->dims[l] + 1;
   g.N = s->dims[l + 1];
@@ -352,12 +352,12 @@ static void weight_grad(cv_ctx* ctx, cv_snap* s, int l, const SplitBuf& G1, cons
   g.epi.out = out + s->off[l];
   g.epi.ld = s->dims[l + 1];
   g.skip = skip;
-  gemm(ctx, g);
+  return g;
 }
 
 // last layer: [gW; gb] = A^T U (+ A2^T U2)
 static void skinny_weight_grad(cv_ctx* ctx, cv_snap* s, const float* U, Scale* usc, const SplitBuf* A2,
-                               const float* U2, Scale* u2sc, float* out, const int* skip) {
+                               const float* U2, Scale* u2sc, float* out, const int* skip, bool side = false) {
   const int l = s->L - 1;
   if (s->tc_out) {
     const __half *uh, *ul, *u2h = nullptr, *u2l = nullptr;
@@ -374,6 +374,12 @@ static void skinny_weight_grad(cv_ctx* ctx, cv_snap* s, const float* U, Scale* u
     g.epi.out = out + s->off[l];
     g.epi.ld = s->c;
     g.skip = skip;
+    static const int cosched = !(getenv("CURVOPT_COSCHED") && getenv("CURVOPT_COSCHED")[0] == '0');
+    if (side && cosched && ctx->engine != CV_ENGINE_SIMT && gemm_tc_supported(g)) {
+      // beside the output-layer backward (the caller joins the side stream)
+      g.stream = side_fork(ctx);
+      g.max_ctas = 48;
+    }
     gemm(ctx, g);
     return;
   }
@@ -398,20 +404,23 @@ void mlp_linearize(cv_ctx* ctx, cv_snap* s, double* loss_out, float* grad_out) {
     mlp_forward_layer(ctx, s, l, s->acts[l], s->w_hi, s->w_lo, s->w_sc, s->acts[l + 1]);
   mlp_output_layer(ctx, s, s->acts[L - 1], s->w_hi, s->w_lo, s->w_sc, s->logits);
   mlp_loss(ctx, s, s->logits, 1, loss_out);
-  // primal backward: G[l-1] = (G[l] W_l^T) * sp[l-1]   (models.py:378-381)
+  // primal backward: G[l-1] = (G[l] W_l^T) * sp[l-1]   (models.py:378-381), with the
+  // weight gradient of layer l co-scheduled beside the backward GEMM of layer l
   const bool tanh_ = s->act == CV_ACT_TANH;
+  if (grad_out) skinny_weight_grad(ctx, s, s->gout, s->gout_sc, nullptr, nullptr, nullptr, grad_out, nullptr);
   if (L >= 2) {
     skinny_backward(ctx, s, s->gout, s->gout_sc, s->w_hi, s->w_lo, s->w_sc, s->G[L - 2],
                     tanh_ ? s->P[L - 2] : nullptr, tanh_ ? s->P_sc[L - 2] : nullptr, nullptr);
-    for (int l = L - 2; l >= 1; --l)
-      hidden_backward(ctx, s, l, s->G[l], s->w_hi, s->w_lo, s->w_sc, s->G[l - 1], tanh_ ? s->P[l - 1] : nullptr,
-                      tanh_ ? s->P_sc[l - 1] : nullptr, nullptr);
+    for (int l = L - 2; l >= 1; --l) {
+      const GemmArgs dx = hidden_backward_args(s, l, s->G[l], s->w_hi, s->w_lo, s->w_sc, s->G[l - 1],
+                                               tanh_ ? s->P[l - 1] : nullptr, tanh_ ? s->P_sc[l - 1] : nullptr,
+                                               nullptr);
+      if (grad_out) gemm_pair(ctx, dx, weight_grad_args(s, l, s->G[l], nullptr, nullptr, grad_out, nullptr));
+      else gemm(ctx, dx);
+    }
+    if (grad_out) gemm(ctx, weight_grad_args(s, 0, s->G[0], nullptr, nullptr, grad_out, nullptr));
   }
-  if (grad_out) {
-    skinny_weight_grad(ctx, s, s->gout, s->gout_sc, nullptr, nullptr, nullptr, grad_out, nullptr);
-    for (int l = L - 2; l >= 0; --l) weight_grad(ctx, s, l, s->G[l], nullptr, nullptr, grad_out, nullptr);
-    if (ctx->nccl) allreduce_f32(ctx, grad_out, s->d);
-  }
+  if (grad_out && ctx->nccl) allreduce_f32(ctx, grad_out, s->d);
 }
 
 // split of a product input v into v_hi / v_lo (per-layer exponents); also
@@ -506,14 +515,20 @@ static void jvp_out(cv_ctx* ctx, cv_snap* s, int post, float scale, float* out, 
 // sum_i J_i^T U_i (no 1/b) into out (models.py:274-285); usc->amax = max|U|.
 static void vjp_from(cv_ctx* ctx, cv_snap* s, const float* U, Scale* usc, float* out, const int* skip) {
   const int L = s->L;
-  skinny_weight_grad(ctx, s, U, usc, nullptr, nullptr, nullptr, out, skip);
+  skinny_weight_grad(ctx, s, U, usc, nullptr, nullptr, nullptr, out, skip, true);
   if (L >= 2) {
     skinny_backward(ctx, s, U, usc, s->w_hi, s->w_lo, s->w_sc, s->gs[L - 2], nullptr, nullptr, skip);
     for (int l = L - 2; l >= 0; --l) {
-      weight_grad(ctx, s, l, s->gs[l], nullptr, nullptr, out, skip);
-      if (l > 0) hidden_backward(ctx, s, l, s->gs[l], s->w_hi, s->w_lo, s->w_sc, s->gs[l - 1], nullptr, nullptr, skip);
+      const GemmArgs dw = weight_grad_args(s, l, s->gs[l], nullptr, nullptr, out, skip);
+      if (l > 0)
+        gemm_pair(ctx, hidden_backward_args(s, l, s->gs[l], s->w_hi, s->w_lo, s->w_sc, s->gs[l - 1], nullptr, nullptr,
+                                            skip),
+                  dw);
+      else
+        gemm(ctx, dw);
     }
   }
+  side_join(ctx);
 }
 
 // GGN product (1/b) J^T H_z J v (curvature.py:109-110).
@@ -603,7 +618,8 @@ void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* v, float* out, const int* ski
       skinny_dx(ctx, a);
     }
     for (int h = L - 2; h >= 0; --h) {
-      weight_grad(ctx, s, h, s->gs[h], h > 0 ? &s->da[h - 1] : nullptr, h > 0 ? &s->G[h] : nullptr, out, skip);
+      const GemmArgs dw =
+          weight_grad_args(s, h, s->gs[h], h > 0 ? &s->da[h - 1] : nullptr, h > 0 ? &s->G[h] : nullptr, out, skip);
       if (h > 0) {
         GemmArgs g;
         g.M = s->bl;
@@ -619,7 +635,9 @@ void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* v, float* out, const int* ski
         bound_add(g.epi.bound, (float)s->dims[h + 1], s->gs[h].sc, s->w_sc + h);
         bound_add(g.epi.bound, (float)s->dims[h + 1], s->G[h].sc, s->v_sc + h);
         g.skip = skip;
-        gemm(ctx, g);
+        gemm_pair(ctx, g, dw);
+      } else {
+        gemm(ctx, dw);
       }
     }
   }

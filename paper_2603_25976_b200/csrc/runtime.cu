@@ -138,6 +138,64 @@ void check_launch(cv_ctx* ctx) {
 // GEMM engine dispatch: tensor-core (tcgen05, 3xTF32) where the operand
 // geometry allows TMA, exact-fp32 SIMT otherwise.
 // ---------------------------------------------------------------------------
+static void ensure_side(cv_ctx* ctx) {
+  if (ctx->side) return;
+  if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess)
+    throw std::runtime_error("CUDA: cannot create the side stream");
+}
+
+cudaStream_t side_fork(cv_ctx* ctx) {
+  ensure_side(ctx);
+  cudaEventRecord(ctx->ev_fork, ctx->stream);
+  cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
+  return ctx->side;
+}
+
+void side_join(cv_ctx* ctx) {
+  if (!ctx->side) return;
+  cudaEventRecord(ctx->ev_join, ctx->side);
+  cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0);
+  for (void* p : ctx->deferred) ctx->pool.put(p);
+  ctx->deferred.clear();
+}
+
+void gemm_pair(cv_ctx* ctx, GemmArgs a, GemmArgs b) {
+  static const int off = getenv("CURVOPT_COSCHED") && getenv("CURVOPT_COSCHED")[0] == '0';
+  const bool tc = ctx->engine != CV_ENGINE_SIMT && gemm_tc_supported(a) && gemm_tc_supported(b);
+  if (off || !tc) {
+    gemm(ctx, a);
+    gemm(ctx, b);
+    return;
+  }
+  ensure_side(ctx);
+  // SM split minimising the slower of the two (even counts: CTA pairs)
+  const int sms = ctx->sm_count;
+  int best = sms / 2;
+  double best_t = 1e300;
+  for (int ca = 16; ca <= sms - 16; ca += 2) {
+    const double ta = gemm_tc_estimate(ctx, a, ca), tb = gemm_tc_estimate(ctx, b, sms - ca);
+    const double t = ta > tb ? ta : tb;
+    if (t < best_t) {
+      best_t = t;
+      best = ca;
+    }
+  }
+  a.max_ctas = best;
+  b.max_ctas = sms - best;
+  a.stream = ctx->stream;
+  b.stream = ctx->side;
+  cudaEventRecord(ctx->ev_fork, ctx->stream);
+  cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
+  gemm(ctx, b);
+  gemm(ctx, a);
+  cudaEventRecord(ctx->ev_join, ctx->side);
+  cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0);
+  for (void* p : ctx->deferred) ctx->pool.put(p);  // later users are ordered after the join
+  ctx->deferred.clear();
+}
+
 void gemm(cv_ctx* ctx, const GemmArgs& a) {
   if (ctx->engine != CV_ENGINE_SIMT && gemm_tc_supported(a)) {
     gemm_tc(ctx, a);
