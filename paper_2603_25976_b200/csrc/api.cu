@@ -246,12 +246,20 @@ int cv_linearize(cv_ctx* ctx, int n_layers, const int* dims, int act, int loss, 
       s->gout_hi = alloc_h(s, s->cp * s->ldb);
       s->gout_lo = alloc_h(s, s->cp * s->ldb);
     }
+    if (L >= 2 && c <= 16 && ctx->engine != CV_ENGINE_SIMT) {
+      s->wl_f32 = alloc_f(s, (int64_t)(dims[L - 1] + 1) * c);
+      s->head_groups_max = 2 * ((dims[L - 1] + 127) / 128);
+      s->head_part = alloc_f(s, (int64_t)s->head_groups_max * b * c);
+    }
   } catch (...) {
     for (void* p : s->owned) ctx->pool.put(p);
     delete s;
     throw;
   }
   split_flat(ctx, w, s->d, s->off, s->w_hi, s->w_lo, s->w_sc, nullptr, 0, nullptr);
+  if (s->wl_f32)
+    cudaMemcpyAsync(s->wl_f32, w + s->off[L - 1], sizeof(float) * (size_t)(dims[L - 1] + 1) * c,
+                    cudaMemcpyDeviceToDevice, ctx->stream);
   if (s->tc_out) pad_last_weights(ctx, s);
   split_rows(ctx, X, dims[0], b, dims[0], s->acts[0], 1);
   for (int l = 0; l + 1 < L; ++l) set_col_value(ctx, s->da[l], b, dims[l + 1], 0.f);

@@ -39,7 +39,8 @@ constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;                   // fp16 elements = 128 bytes = one SWIZZLE_128B row
 constexpr int TC_ZERO_BYTES = TC_BM * 32;   // all-zero K-major A tile (SWIZZLE_32B, K=16) for rescaling MMAs
 constexpr int TC_STG_BYTES = 2048;          // per epilogue warp: 32 rows x 16 cols, two fp16 planes or one fp32
-constexpr int TC_STG_TOTAL = 8 * TC_STG_BYTES;
+constexpr int TC_HSTG_BYTES = 1280;        // per epilogue warp: the fused head's W / V rows of one sub-tile (16 x 10 x 2 fp32)
+constexpr int TC_STG_TOTAL = 8 * (TC_STG_BYTES + TC_HSTG_BYTES);
 
 struct TcOperand {
   int kmajor;   // 1: K contiguous, 0: M/N contiguous
@@ -286,6 +287,105 @@ struct TcMaps {
   CUtensorMap o[2];     // TMA-store epilogue: fp16 {hi, lo} boxes {16, 32} SW32, or fp32 {16, 32(,1)} SW64
 };
 
+CV_DEV float4 lds4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+CV_DEV void sts4(uint32_t addr, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
+// Fused output-layer head, c = 10: the W and V rows of a 16-column sub-tile (2 x 160
+// contiguous fp32, 16-byte aligned) are fetched cooperatively by the warp (lane l
+// holds float4 l, l+32, l+64 of the 80), one sub-tile ahead, and staged in the warp's
+// smem slot, from which every lane reads them as broadcasts.
+CV_DEV void head_fetch10(const Epilogue& e, int nb, int N, int lane, float4 (&hf)[3]) {
+  const int64_t lim = (int64_t)N * 10;  // valid floats of the W / V row blocks
+#pragma unroll
+  for (int u = 0; u < 3; ++u) {
+    const int idx = lane + 32 * u;
+    hf[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (idx < 80 && nb < N) {
+      const float* base = idx < 40 ? e.head_w : e.head_v;
+      const int64_t o = (int64_t)nb * 10 + 4 * (idx % 40);
+      if (o + 4 <= lim) {
+        hf[u] = __ldg(reinterpret_cast<const float4*>(base + o));
+      } else {
+        float t[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int i = 0; i < 4; ++i)
+          if (o + i < lim) t[i] = __ldg(base + o + i);
+        hf[u] = make_float4(t[0], t[1], t[2], t[3]);
+      }
+    }
+  }
+}
+
+CV_DEV void head_stage10(uint32_t hs, int lane, const float4 (&hf)[3]) {
+#pragma unroll
+  for (int u = 0; u < 3; ++u)
+    if (lane + 32 * u < 80) sts4(hs + 16 * (lane + 32 * u), hf[u]);
+}
+
+// d = a * b + c on two fp32 lanes at once (sm_100 FFMA2)
+CV_DEV float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+
+// hacc[k] += sum_j a[j] V[j, k] + t[j] W[j, k] over the staged sub-tile (k pairs on FFMA2)
+CV_DEV void head_acc10(uint32_t hs, const float (&av)[16], const float (&t)[16], float (&hacc)[16]) {
+  float2 h[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) h[k] = make_float2(hacc[2 * k], hacc[2 * k + 1]);
+#pragma unroll
+  for (int j0 = 0; j0 < 16; j0 += 2) {
+    float2 w[10], v[10];
+#pragma unroll
+    for (int u = 0; u < 5; ++u) {
+      const float4 a = lds4(hs + 4 * (j0 * 10) + 16 * u);
+      const float4 b = lds4(hs + 640 + 4 * (j0 * 10) + 16 * u);
+      w[2 * u] = make_float2(a.x, a.y);
+      w[2 * u + 1] = make_float2(a.z, a.w);
+      v[2 * u] = make_float2(b.x, b.y);
+      v[2 * u + 1] = make_float2(b.z, b.w);
+    }
+#pragma unroll
+    for (int jj = 0; jj < 2; ++jj) {
+      const float2 tt = make_float2(t[j0 + jj], t[j0 + jj]);
+      const float2 aa = make_float2(av[j0 + jj], av[j0 + jj]);
+#pragma unroll
+      for (int k = 0; k < 5; ++k) h[k] = ffma2(aa, v[jj * 5 + k], ffma2(tt, w[jj * 5 + k], h[k]));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    hacc[2 * k] = h[k].x;
+    hacc[2 * k + 1] = h[k].y;
+  }
+}
+
+// any other head width (<= 16): direct broadcast loads from global
+CV_DEV void head_acc_generic(const Epilogue& e, int nb, int N, const float (&av)[16], const float (&t)[16],
+                             float (&hacc)[16]) {
+  const int hc = e.head_c;
+  const float* wr = e.head_w + (int64_t)nb * hc;
+  const float* vr = e.head_v + (int64_t)nb * hc;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    if (nb + j >= N) break;
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (k < hc) hacc[k] = fmaf(av[j], __ldg(vr + j * hc + k), fmaf(t[j], __ldg(wr + j * hc + k), hacc[k]));
+  }
+}
+
 // Epilogue of one accumulator tile through shared memory and TMA stores (the
 // hot modes: split outputs with an optional ReLU mask, fp32 outputs and split-K
 // partials).  Each warp owns a 2 KB staging slot and walks its 32 rows in
@@ -294,7 +394,8 @@ struct TcMaps {
 // store(s).  Global traffic is full-row, and stores retire asynchronously.
 template <int BN>
 CV_DEV void tile_epilogue_tma(const TcArgs& a, const TcMaps& maps, const EpiRt& rt, uint32_t tacc, int m_base, int n0,
-                              int split, float inv, int q, int half, int lane, uint8_t* stg, float& amax) {
+                              int split, float inv, int q, int half, int lane, uint8_t* stg, uint8_t* hstg,
+                              float& amax) {
   const int r0 = m_base + q * 32;  // this warp's first row
   const int m = r0 + lane;
   const uint32_t trow = tacc + ((uint32_t)(q * 32) << 16);
@@ -304,24 +405,38 @@ CV_DEV void tile_epilogue_tma(const TcArgs& a, const TcMaps& maps, const EpiRt& 
   const Epilogue& e = a.epi;
   const bool use_mask = a.tma_out == 1 && (e.mode == EPI_SPLIT_MASK || e.mode == EPI_HVP);
   const bool relu_act = e.act == CV_ACT_RELU;
+  const bool head = use_mask && e.head_part != nullptr;
+  const bool head10 = head && e.head_c == 10 && !(((uintptr_t)e.head_w | (uintptr_t)e.head_v) & 15);
+  const bool store = !(head && e.head_only);
+  const uint32_t hs = smem_u32(hstg);
+  float4 hf[3];
+  if (head10) head_fetch10(e, n0 + sb * 16, a.N, lane, hf);
   // this lane's share of a sub-tile's mask (rows lane/2 and lane/2 + 16, 8 columns),
-  // loaded one sub-tile ahead so the global latency overlaps the previous sub-tile
-  auto load_mask = [&](int nb, uint4 (&mv)[2]) {
+  // loaded one sub-tile ahead so the global latency overlaps the previous sub-tile;
+  // the head also needs the low plane (the activation value, not just its sign)
+  auto load_mask = [&](int nb, uint4 (&mv)[2], uint4 (&ml)[2]) {
 #pragma unroll
     for (int it = 0; it < 2; ++it) {
       const int rr = (lane >> 1) + 16 * it, ch = lane & 1;
       mv[it] = make_uint4(0, 0, 0, 0);
-      if (nb < a.N && r0 + rr < a.M && nb + 8 * ch < a.N)
-        mv[it] = *reinterpret_cast<const uint4*>(e.mask_hi + (int64_t)(r0 + rr) * e.mask_ld + nb + 8 * ch);
+      ml[it] = make_uint4(0, 0, 0, 0);
+      if (nb < a.N && r0 + rr < a.M && nb + 8 * ch < a.N) {
+        const int64_t o = (int64_t)(r0 + rr) * e.mask_ld + nb + 8 * ch;
+        mv[it] = *reinterpret_cast<const uint4*>(e.mask_hi + o);
+        if (head) ml[it] = *reinterpret_cast<const uint4*>(e.mask_lo + o);
+      }
     }
   };
-  uint4 mcur[2], mnext[2];
-  if (use_mask) load_mask(n0 + sb * 16, mcur);
+  uint4 mcur[2], mnext[2], lcur[2], lnext[2];
+  float hacc[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) hacc[k] = 0.f;
+  if (use_mask) load_mask(n0 + sb * 16, mcur, lcur);
 #pragma unroll 1
   for (int sbk = sb; sbk < se; ++sbk) {
     const int nb = n0 + sbk * 16;
     if (nb >= a.N) break;
-    if (use_mask && sbk + 1 < se) load_mask(nb + 16, mnext);
+    if (use_mask && sbk + 1 < se) load_mask(nb + 16, mnext, lnext);
     uint32_t r[16];
     tmem_ld16(trow + sbk * 16, r);
     float v[16];
@@ -340,20 +455,42 @@ CV_DEV void tile_epilogue_tma(const TcArgs& a, const TcMaps& maps, const EpiRt& 
         for (int it = 0; it < 2; ++it) {
           const int rr = (lane >> 1) + 16 * it, ch = lane & 1;
           *reinterpret_cast<uint4*>(stg + rr * 32 + 16 * (ch ^ ((rr >> 2) & 1))) = mcur[it];
+          if (head) *reinterpret_cast<uint4*>(stg + 1024 + rr * 32 + 16 * (ch ^ ((rr >> 2) & 1))) = lcur[it];
         }
         __syncwarp();
-        H8 mk[2];
+        H8 mk[2], ml[2];
 #pragma unroll
-        for (int ch = 0; ch < 2; ++ch) mk[ch].u = *reinterpret_cast<const uint4*>(stg + lane * 32 + 16 * (ch ^ ((lane >> 2) & 1)));
+        for (int ch = 0; ch < 2; ++ch) {
+          mk[ch].u = *reinterpret_cast<const uint4*>(stg + lane * 32 + 16 * (ch ^ ((lane >> 2) & 1)));
+          if (head) ml[ch].u = *reinterpret_cast<const uint4*>(stg + 1024 + lane * 32 + 16 * (ch ^ ((lane >> 2) & 1)));
+        }
         __syncwarp();
 #pragma unroll
         for (int j = 0; j < 16; ++j) o[j] = v[j] * (__half2float(mk[j >> 3].h[j & 7]) > 0.f ? 1.f : 0.f);
+        if (head) {
+          float av[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            av[j] = (__half2float(mk[j >> 3].h[j & 7]) + __half2float(ml[j >> 3].h[j & 7])) * rt.mask_inv;
+          if (head10) {
+            head_stage10(hs, lane, hf);
+            __syncwarp();
+            if (sbk + 1 < se) head_fetch10(e, nb + 16, a.N, lane, hf);
+            head_acc10(hs, av, o, hacc);
+            __syncwarp();  // the slot is rewritten by the next sub-tile
+          } else {
+            head_acc_generic(e, nb, a.N, av, o, hacc);
+          }
+        }
         mcur[0] = mnext[0];
         mcur[1] = mnext[1];
+        lcur[0] = lnext[0];
+        lcur[1] = lnext[1];
       } else {
 #pragma unroll
         for (int j = 0; j < 16; ++j) o[j] = relu_act ? relu_f(v[j]) : tanhf(v[j]);
       }
+      if (!store) continue;
       if (m < a.M)
 #pragma unroll
         for (int j = 0; j < 16; ++j)
@@ -392,16 +529,24 @@ CV_DEV void tile_epilogue_tma(const TcArgs& a, const TcMaps& maps, const EpiRt& 
       }
     }
   }
+  if (head && m < a.M) {
+    // group = column half of this tile; fixed-order reduction in k_out_reduce
+    const int grp = (n0 / BN) * 2 + half;
+    float* dst = e.head_part + ((int64_t)grp * a.M + m) * e.head_c;
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (k < e.head_c) dst[k] = hacc[k];
+  }
 }
 
 // The epilogue of one accumulator tile (TMEM -> registers -> fused epilogue), run by
 // 8 warps: warp w reads TMEM lane quadrant (w % 4), half = column half.
 template <int BN>
 CV_DEV void tile_epilogue(const TcArgs& a, const TcMaps& maps, const EpiRt& rt, uint32_t tacc, int m_base, int n0,
-                          int split, float inv, int q, int half, int lane, uint8_t* stg) {
+                          int split, float inv, int q, int half, int lane, uint8_t* stg, uint8_t* hstg) {
   if (a.tma_out && !a.dbg) {
     float amax = 0.f, ramax = 0.f;
-    tile_epilogue_tma<BN>(a, maps, rt, tacc, m_base, n0, split, inv, q, half, lane, stg, amax);
+    tile_epilogue_tma<BN>(a, maps, rt, tacc, m_base, n0, split, inv, q, half, lane, stg, hstg, amax);
     if (!a.partial) epi_flush_amax(a.epi, amax, ramax);
     return;
   }
@@ -598,7 +743,7 @@ __global__ void __launch_bounds__(320, 1) k_gemm_tc(const __grid_constant__ TcMa
       const int last = vseg(a, plan, kb0 + nkb - 1, lkb);
       const float inv = plan.inv_a[last] * plan.inv_b[last];
       tile_epilogue<BN>(a, maps, rt, tmem + ab * BN, m0, n0, w / (a.tiles_m * a.tiles_n), inv, q, half, lane,
-                        stg_all + (warp - 2) * TC_STG_BYTES);
+                        stg_all + (warp - 2) * TC_STG_BYTES, stg_all + 8 * TC_STG_BYTES + (warp - 2) * TC_HSTG_BYTES);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[ab]);
@@ -873,6 +1018,7 @@ static int launch_tc(cv_ctx* ctx, const GemmArgs& g, int splits, float* ext_part
     a.partial = part;
   }
   setup_out(g, maps, a, a.partial, splits);
+  if (g.epi.head_part && a.tma_out != 1) throw std::runtime_error("fused output head needs the TMA split epilogue");
   const int work = a.tiles_m * a.tiles_n * splits;
   const int sms = g.max_ctas > 0 && g.max_ctas < ctx->sm_count ? g.max_ctas : ctx->sm_count;
   const int grid = work < sms ? work : sms;
@@ -950,6 +1096,24 @@ static TcPlan tc_plan(const GemmArgs& g, int sms) {
 double gemm_tc_estimate(const cv_ctx* ctx, const GemmArgs& g, int ctas) {
   (void)ctx;
   return plan_time(tc_plan(g, ctas), ctas);
+}
+
+// Number of column groups of the fused output-layer head this GEMM would write
+// (tile_epilogue_tma), or 0 when the GEMM cannot carry the head (engine, layout,
+// epilogue mode or tile plan); the caller then runs the output layer separately.
+int gemm_tc_head_groups(const cv_ctx* ctx, const GemmArgs& g) {
+  static const int off = getenv("CURVOPT_HEAD") && getenv("CURVOPT_HEAD")[0] == '0';
+  static const int tma_off = getenv("CURVOPT_TC_TMA_OUT") && getenv("CURVOPT_TC_TMA_OUT")[0] == '0';
+  if (off || tma_off || ctx->engine == CV_ENGINE_SIMT || !gemm_tc_supported(g) || g.lower_only) return 0;
+  const Epilogue& e = g.epi;
+  if (e.mode != EPI_SPLIT_MASK || e.act != CV_ACT_RELU || e.raw || e.mask_div != 1 || (e.mask_ld & 7) ||
+      !aligned16(e.mask_hi) || !aligned16(e.mask_lo) || (e.ld & 7) || !aligned16(e.out_hi) || !aligned16(e.out_lo))
+    return 0;
+  const int sms = g.max_ctas > 0 && g.max_ctas < ctx->sm_count ? g.max_ctas : ctx->sm_count;
+  const TcPlan p = tc_plan(g, sms);
+  if (p.kind == 0 || p.splits > 1) return 0;
+  const int bn = p.kind == 3 ? 128 : 256;
+  return 2 * ((g.N + bn - 1) / bn);
 }
 
 void gemm_tc(cv_ctx* ctx, const GemmArgs& g) {

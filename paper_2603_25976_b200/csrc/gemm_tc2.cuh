@@ -179,7 +179,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       const int last = vseg(a, plan, kb0 + nkb - 1, lkb);
       const float inv = plan.inv_a[last] * plan.inv_b[last];
       tile_epilogue<TC2_BN>(a, maps, rt, tmem + ab * TC2_BN, mt0 + rank * TC_BM, n0, w / (a.tiles_m * a.tiles_n),
-                            inv, q, half, lane, stg_all + (warp - 2) * TC_STG_BYTES);
+                            inv, q, half, lane, stg_all + (warp - 2) * TC_STG_BYTES,
+                            stg_all + 8 * TC_STG_BYTES + (warp - 2) * TC_HSTG_BYTES);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(tempty0[ab]);
@@ -218,6 +219,7 @@ static void launch_tc2(cv_ctx* ctx, const GemmArgs& g, int splits) {
     a.partial = part;
   }
   setup_out(g, maps, a, a.partial, splits);
+  if (g.epi.head_part && a.tma_out != 1) throw std::runtime_error("fused output head needs the TMA split epilogue");
   const int work = a.tiles_m * a.tiles_n * splits;
   const int sms = g.max_ctas > 0 && g.max_ctas < ctx->sm_count ? g.max_ctas : ctx->sm_count;
   const int pairs = sms / 2;

@@ -79,6 +79,16 @@ struct Epilogue {
   int kdiv = 1;                  // EPI_GRAM: rows per example
   int first = 0;                 // EPI_GRAM: overwrite instead of accumulate
   float alpha = 1.f;             // EPI_ACCUM
+  // Fused output-layer JVP ("head", EPI_SPLIT_MASK on the last hidden layer only):
+  // each epilogue thread accumulates, over its row m and its column half,
+  //   head_part[g][m][:hc] = sum_n a(m, n) Vh[n, :] + t(m, n) Wh[n, :]
+  // with a = the stored activation (mask operand), t = the masked tangent; a
+  // fixed-order reduction over the groups g adds the bias row (models.py:243-255).
+  const float* head_w = nullptr;   // N x hc fp32 (output layer W rows)
+  const float* head_v = nullptr;   // N x hc fp32 (the product's V rows)
+  float* head_part = nullptr;      // [groups][M][hc]
+  int head_c = 0;
+  int head_only = 0;               // skip the split tangent store (GGN: the head is its only consumer)
 };
 
 struct GemmArgs {
@@ -193,6 +203,11 @@ struct cv_snap {
   __half* vl_hi = nullptr; __half* vl_lo = nullptr;
   __half* U_hi = nullptr; __half* U_lo = nullptr;
   __half* gout_hi = nullptr; __half* gout_lo = nullptr;
+  // fused output-layer head (EPI head_*): fp32 copy of the last layer's [W; b] block
+  // ((n+1) x c) and the per-group partials of the output tangent
+  float* wl_f32 = nullptr;
+  float* head_part = nullptr;
+  int head_groups_max = 0;
   // row lane (lazily built)
   float* seeds = nullptr;         // b x c x c  (H_z^{1/2})
   float* pinv = nullptr;          // b x c x c
@@ -222,6 +237,7 @@ double gemm_tc_estimate(const cv_ctx* ctx, const GemmArgs& g, int ctas);  // rel
 cudaStream_t side_fork(cv_ctx* ctx);  // side stream ordered after the context stream's current work
 void side_join(cv_ctx* ctx);          // context stream waits for the side stream
 int gemm_tc_partial(cv_ctx* ctx, const GemmArgs& g, float** partial);  // N <= 32, raw split-K partials
+int gemm_tc_head_groups(const cv_ctx* ctx, const GemmArgs& g);          // 0: no fused output-layer head
 
 // runtime.cu
 void allreduce_f32(cv_ctx* ctx, float* buf, int64_t n);

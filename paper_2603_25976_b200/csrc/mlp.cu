@@ -116,25 +116,67 @@ __global__ void k_pad_t(const __half* hi, const __half* lo, int rows, int c, int
   }
 }
 
-// out-layer JVP: sum the split-K partials of z = J v per row, then either store
-// the logits tangent (POST_LOGITS) or U = H_z(z) * scale (models.py:199-204)
+// out-layer JVP: sum the split-K / head-group partials of z = J v per row (+ the
+// bias row), then either store the logits tangent (POST_LOGITS) or
+// U = H_z(z) * scale (models.py:199-204).  A block owns 128 rows: the partial
+// slabs [z][rows][c] are read coalesced (each thread sums fixed element positions
+// over z in fixed order), then rows are finished from shared memory.
 template <int CM>
-__global__ void k_out_reduce(const float* part, int splits, int rows, int c, int post, int loss, const float* probs,
-                             float scale, float* out, float* out_amax, const int* skip) {
+__global__ void __launch_bounds__(128) k_out_reduce(const float* part, int splits, int rows, int c, int post, int loss,
+                                                    const float* probs, float scale, float* out, float* out_amax,
+                                                    const int* skip, const float* bias) {
   CV_PDL_ENTRY();
   if (skip_if(skip)) return;
-  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  constexpr int RB = 32;             // rows per block
+  constexpr int PT = RB * CM / 128;  // element positions per thread
+  __shared__ float tile[RB * CM];
+  const int m0 = blockIdx.x * RB;
+  const int nrows = min(RB, rows - m0);
+  const int nel = nrows * c;
+  float acc[PT];
+#pragma unroll
+  for (int u = 0; u < PT; ++u) {
+    const int e = threadIdx.x + 128 * u;
+    acc[u] = (bias && e < nel) ? bias[e % c] : 0.f;
+  }
+  // four slabs' loads in flight before their (fixed-order) adds
+  int z = 0;
+  for (; z + 4 <= splits; z += 4) {
+    float x[4][PT];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float* p = part + ((int64_t)(z + i) * rows + m0) * c;
+#pragma unroll
+      for (int u = 0; u < PT; ++u) {
+        const int e = threadIdx.x + 128 * u;
+        x[i][u] = e < nel ? p[e] : 0.f;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int u = 0; u < PT; ++u) acc[u] += x[i][u];
+  }
+  for (; z < splits; ++z) {
+    const float* p = part + ((int64_t)z * rows + m0) * c;
+#pragma unroll
+    for (int u = 0; u < PT; ++u) {
+      const int e = threadIdx.x + 128 * u;
+      if (e < nel) acc[u] += p[e];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < PT; ++u) {
+    const int e = threadIdx.x + 128 * u;
+    if (e < nel) tile[e] = acc[u];
+  }
+  __syncthreads();
+  const int r = threadIdx.x, m = m0 + r;
   float amax = 0.f;
-  if (m < rows) {
+  if (r < nrows) {
     float t[CM];
 #pragma unroll
-    for (int j = 0; j < CM; ++j) t[j] = 0.f;
-    for (int z = 0; z < splits; ++z) {
-      const float* p = part + ((int64_t)z * rows + m) * c;
-#pragma unroll
-      for (int j = 0; j < CM; ++j)
-        if (j < c) t[j] += p[j];
-    }
+    for (int j = 0; j < CM; ++j) t[j] = j < c ? tile[r * c + j] : 0.f;
     if (post == 1) {
       if (loss == CV_LOSS_CE) {
         const float* p = probs + (int64_t)m * c;
@@ -153,10 +195,12 @@ __global__ void k_out_reduce(const float* part, int splits, int rows, int c, int
 #pragma unroll
     for (int j = 0; j < CM; ++j)
       if (j < c) {
-        out[(int64_t)m * c + j] = t[j];
+        tile[r * c + j] = t[j];
         amax = fmaxf(amax, fabsf(t[j]));
       }
   }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nel; e += 128) out[(int64_t)m0 * c + e] = tile[e];  // coalesced
   amax = warp_max_f(amax);
   if ((threadIdx.x & 31) == 0 && out_amax) atomic_amax(out_amax, amax);
 }
@@ -435,7 +479,13 @@ static void split_input(cv_ctx* ctx, cv_snap* s, const float* v, const int* skip
 }
 
 // JVP through the hidden layers: da[l] = act'(a_{l+1}) * (A_l V_l + da[l-1] W_l).
-static void jvp_hidden(cv_ctx* ctx, cv_snap* s, bool keep_dz, const int* skip) {
+// With v (the fp32 product input) the last hidden GEMM also carries the output
+// layer's JVP in its epilogue (Epilogue::head_*): returns the number of partial
+// groups it leaves in s->head_part (0: not fused, jvp_out runs the output layer).
+// head_only: da[L-2] has no other consumer (GGN / JVP) and is not stored.
+static int jvp_hidden(cv_ctx* ctx, cv_snap* s, bool keep_dz, const int* skip, const float* v = nullptr,
+                      bool head_only = false) {
+  int groups = 0;
   for (int l = 0; l < s->L - 1; ++l) {
     GemmArgs g;
     g.M = s->bl;
@@ -459,13 +509,38 @@ static void jvp_hidden(cv_ctx* ctx, cv_snap* s, bool keep_dz, const int* skip) {
     g.epi.raw_ld = s->da[l].ld;
     g.epi.raw_amax = keep_dz ? &s->dz_sc[l]->amax : nullptr;
     g.skip = skip;
+    if (v && s->head_part && l == s->L - 2) {
+      g.epi.head_w = s->wl_f32;
+      g.epi.head_v = v + s->off[l + 1];
+      g.epi.head_c = s->c;
+      g.epi.head_part = s->head_part;
+      g.epi.head_only = head_only;
+      groups = gemm_tc_head_groups(ctx, g);
+      if (groups <= 0 || groups > s->head_groups_max) {
+        groups = 0;
+        g.epi.head_part = nullptr;
+        g.epi.head_only = 0;
+      }
+    }
     gemm(ctx, g);
   }
+  return groups;
 }
 
 // Output tangent with fused H_z: U = H_z(J v) * scale (post HZ) or raw J v (logits).
-static void jvp_out(cv_ctx* ctx, cv_snap* s, int post, float scale, float* out, float* out_amax, const int* skip) {
+static void jvp_out(cv_ctx* ctx, cv_snap* s, int post, float scale, float* out, float* out_amax, const int* skip,
+                    int head_groups = 0, const float* v = nullptr) {
   const int l = s->L - 1;
+  if (head_groups > 0) {
+    // the last hidden GEMM left per-group partials of z = J v: add the bias row
+    // [Vb]_{L-1} and reduce in fixed order (+ H_z)
+    if (s->tc_out && s->tc_dx) pad_last(ctx, s, s->v_hi, s->v_lo, s->vl_hi, s->vl_lo, skip);  // vl for the HVP backward
+    const float* bias = v + s->off[l] + (int64_t)s->dims[l] * s->c;
+    launch_k(ctx->stream, k_out_reduce<16>, (s->bl + 31) / 32, 128, 0, (const float*)s->head_part, head_groups, s->bl,
+             s->c, post == POST_HZ ? 1 : 0, s->loss, (const float*)s->probs, scale, out, out_amax, skip, bias);
+    ctx->launches++;
+    return;
+  }
   if (s->tc_out) {
     pad_last(ctx, s, s->v_hi, s->v_lo, s->vl_hi, s->vl_lo, skip);
     GemmArgs g;
@@ -482,11 +557,11 @@ static void jvp_out(cv_ctx* ctx, cv_snap* s, int post, float scale, float* out, 
     const int splits = gemm_tc_partial(ctx, g, &part);
     const bool hz = post == POST_HZ;
     if (s->c <= 16)
-      launch_k(ctx->stream, k_out_reduce<16>, (s->bl + 127) / 128, 128, 0, part, splits, s->bl, s->c, hz, s->loss, s->probs,
-                                                                    scale, out, out_amax, skip);
+      launch_k(ctx->stream, k_out_reduce<16>, (s->bl + 31) / 32, 128, 0, part, splits, s->bl, s->c, hz, s->loss, s->probs,
+                                                                    scale, out, out_amax, skip, (const float*)nullptr);
     else
-      launch_k(ctx->stream, k_out_reduce<32>, (s->bl + 127) / 128, 128, 0, part, splits, s->bl, s->c, hz, s->loss, s->probs,
-                                                                    scale, out, out_amax, skip);
+      launch_k(ctx->stream, k_out_reduce<32>, (s->bl + 31) / 32, 128, 0, part, splits, s->bl, s->c, hz, s->loss, s->probs,
+                                                                    scale, out, out_amax, skip, (const float*)nullptr);
     ctx->launches++;
     ctx->pool.put(part);
     return;
@@ -534,16 +609,16 @@ static void vjp_from(cv_ctx* ctx, cv_snap* s, const float* U, Scale* usc, float*
 // GGN product (1/b) J^T H_z J v (curvature.py:109-110).
 void mlp_ggn(cv_ctx* ctx, cv_snap* s, const float* v, float* out, const int* skip) {
   split_input(ctx, s, v, skip);
-  jvp_hidden(ctx, s, false, skip);
-  jvp_out(ctx, s, POST_HZ, 1.0f / (float)s->bg, s->U, &s->U_sc->amax, skip);
+  const int hg = jvp_hidden(ctx, s, false, skip, v, true);
+  jvp_out(ctx, s, POST_HZ, 1.0f / (float)s->bg, s->U, &s->U_sc->amax, skip, hg, v);
   vjp_from(ctx, s, s->U, s->U_sc, out, skip);
   if (ctx->nccl) allreduce_f32(ctx, out, s->d);
 }
 
 void mlp_jvp(cv_ctx* ctx, cv_snap* s, const float* v, float* out_bc) {
   split_input(ctx, s, v, nullptr);
-  jvp_hidden(ctx, s, false, nullptr);
-  jvp_out(ctx, s, POST_LOGITS, 1.f, out_bc, nullptr, nullptr);
+  const int hg = jvp_hidden(ctx, s, false, nullptr, v, true);
+  jvp_out(ctx, s, POST_LOGITS, 1.f, out_bc, nullptr, nullptr, hg, v);
 }
 
 void mlp_vjp(cv_ctx* ctx, cv_snap* s, const float* U, float* out) {
@@ -574,9 +649,9 @@ void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* v, float* out, const int* ski
   const int L = s->L;
   const bool tanh_ = s->act == CV_ACT_TANH;
   split_input(ctx, s, v, skip);
-  jvp_hidden(ctx, s, tanh_, skip);
+  const int hg = jvp_hidden(ctx, s, tanh_, skip, v, false);
   // dG_{L-1} = H_z dz_{L-1} / b
-  jvp_out(ctx, s, POST_HZ, 1.0f / (float)s->bg, s->U, &s->U_sc->amax, skip);
+  jvp_out(ctx, s, POST_HZ, 1.0f / (float)s->bg, s->U, &s->U_sc->amax, skip, hg, v);
   // last layer: [gW; gb] = A^T dG + [da|0]^T G_{L-1}
   skinny_weight_grad(ctx, s, s->U, s->U_sc, L >= 2 ? &s->da[L - 2] : nullptr, s->gout, s->gout_sc, out, skip);
   if (L >= 2) {
