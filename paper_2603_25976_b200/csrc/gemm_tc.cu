@@ -486,6 +486,7 @@ CV_DEV void tile_epilogue_tma(const TcArgs& a, const TcMaps& maps, const EpiRt& 
         mcur[1] = mnext[1];
         lcur[0] = lnext[0];
         lcur[1] = lnext[1];
+
       } else {
 #pragma unroll
         for (int j = 0; j < 16; ++j) o[j] = relu_act ? relu_f(v[j]) : tanhf(v[j]);
@@ -537,6 +538,24 @@ CV_DEV void tile_epilogue_tma(const TcArgs& a, const TcMaps& maps, const EpiRt& 
     for (int k = 0; k < 16; ++k)
       if (k < e.head_c) dst[k] = hacc[k];
   }
+}
+
+// Bulk L2 prefetch of the mask rows (and, for the fused head, the low plane) an
+// epilogue warp will read for its next tile: issued before the warp waits for the
+// accumulator, so the tile's mainloop hides the DRAM latency of the mask stream.
+template <int BN>
+CV_DEV void epi_prefetch_mask(const TcArgs& a, int m_base, int n0, int q, int half, int lane) {
+  const Epilogue& e = a.epi;
+  if (!(a.tma_out == 1 && (e.mode == EPI_SPLIT_MASK || e.mode == EPI_HVP))) return;
+  const int m = m_base + q * 32 + lane;
+  const int c0 = n0 + half * (BN / 2);
+  int cols = a.N - c0 < BN / 2 ? a.N - c0 : BN / 2;
+  cols &= ~7;
+  if (m >= a.M || cols <= 0) return;
+  const int64_t o = (int64_t)m * e.mask_ld + c0;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(e.mask_hi + o), "r"(cols * 2) : "memory");
+  if (e.head_part)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(e.mask_lo + o), "r"(cols * 2) : "memory");
 }
 
 // The epilogue of one accumulator tile (TMEM -> registers -> fused epilogue), run by
@@ -737,6 +756,7 @@ __global__ void __launch_bounds__(320, 1) k_gemm_tc(const __grid_constant__ TcMa
       int m0, n0, kb0, nkb;
       if (!tc_work(a, w, TC_BM, BN, m0, n0, kb0, nkb)) continue;
       const int ab = acc_i & 1;
+      epi_prefetch_mask<BN>(a, m0, n0, q, half, lane);
       mbar_wait(&tfull[ab], (acc_i >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       int lkb;

@@ -173,6 +173,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       int mt0, n0, kb0, nkb;
       if (!tc_work(a, w, 2 * TC_BM, TC2_BN, mt0, n0, kb0, nkb)) continue;
       const int ab = acc_i & 1;
+      epi_prefetch_mask<TC2_BN>(a, mt0 + rank * TC_BM, n0, q, half, lane);
       mbar_wait(&tfull[ab], (acc_i >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       int lkb;

@@ -244,6 +244,101 @@ __global__ void __launch_bounds__(128) k_dx(SkinnyDxArgs a) {
   epi_flush_amax(e, amax, ramax);
 }
 
+// dx, wide variant for the hot case (one segment, ReLU mask, c <= 10, n <= 1024,
+// 16-byte rows): a thread owns 8 adjacent columns (128-bit mask loads and split
+// stores), the n/8 threads of a row span it, a 256-thread block covers 256/(n/8)
+// rows per pass and DXW_R passes per chunk.  W^T is staged once per block in
+// shared memory as [c][n]; the chunk's mask loads are issued before its U rows are
+// staged, and each W row read from smem feeds all DXW_R rows of the thread.
+constexpr int DXW_R = 4;
+constexpr int DXW_C = 10;
+__global__ void __launch_bounds__(256) k_dx_wide(SkinnyDxArgs a) {
+  CV_PDL_ENTRY();
+  if (skip_if(a.skip)) return;
+  extern __shared__ __align__(16) float dxw_smem[];
+  float* Wt = dxw_smem;                    // [DXW_C][n]
+  const int tpr = a.n >> 3;                // threads per row
+  const int rpp = 256 / tpr;               // rows per pass
+  const int rows_chunk = rpp * DXW_R;
+  float* Us = Wt + DXW_C * a.n;            // [rows_chunk][DXW_C]
+  const int t = threadIdx.x;
+  const int rl = t / tpr, col = (t - rl * tpr) * 8;
+  const bool act = rl < rpp;
+  {
+    const float winv = pow2f(-a.w_sc[0]->e);
+    for (int i = t; i < DXW_C * a.n; i += 256) {
+      const int j = i / a.n, n = i - j * a.n;
+      const int64_t idx = (int64_t)n * a.c + j;
+      Wt[i] = j < a.c ? join16(a.w_hi[0][idx], a.w_lo[0][idx], winv) : 0.f;
+    }
+  }
+  const Epilogue& e = a.epi;
+  const EpiRt rt = epi_prepare(e);
+  if (blockIdx.x == 0 && threadIdx.x == 0) epi_publish(e, rt);
+  float amax = 0.f;
+  const int chunks = (a.rows + rows_chunk - 1) / rows_chunk;
+  for (int ch = blockIdx.x; ch < chunks; ch += gridDim.x) {
+    const int m0 = ch * rows_chunk;
+    uint4 mk[DXW_R];
+#pragma unroll
+    for (int i = 0; i < DXW_R; ++i) {
+      const int m = m0 + i * rpp + rl;
+      mk[i] = make_uint4(0, 0, 0, 0);
+      if (act && m < a.rows) mk[i] = __ldg(reinterpret_cast<const uint4*>(e.mask_hi + (int64_t)m * e.mask_ld + col));
+    }
+    __syncthreads();  // W staged / the previous chunk's readers of Us are done
+    for (int i = t; i < rows_chunk * DXW_C; i += 256) {
+      const int r = i / DXW_C, j = i - r * DXW_C;
+      Us[i] = (m0 + r < a.rows && j < a.c) ? a.U[0][(int64_t)(m0 + r) * a.c + j] : 0.f;
+    }
+    __syncthreads();
+    if (!act) continue;
+    float v[DXW_R][8];
+#pragma unroll
+    for (int i = 0; i < DXW_R; ++i)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[i][q] = 0.f;
+#pragma unroll
+    for (int j = 0; j < DXW_C; ++j) {
+      const float4 w0 = *reinterpret_cast<const float4*>(Wt + j * a.n + col);
+      const float4 w1 = *reinterpret_cast<const float4*>(Wt + j * a.n + col + 4);
+      const float w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+      for (int i = 0; i < DXW_R; ++i) {
+        const float u = Us[(i * rpp + rl) * DXW_C + j];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[i][q] = fmaf(u, w[q], v[i][q]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < DXW_R; ++i) {
+      const int m = m0 + i * rpp + rl;
+      if (m >= a.rows) break;
+      H8 hm, oh, ol;
+      hm.u = mk[i];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float x = __half2float(hm.h[q]) > 0.f ? v[i][q] : 0.f;
+        amax = fmaxf(amax, fabsf(x));
+        split16(x, rt.out_s, oh.h[q], ol.h[q]);
+      }
+      const int64_t o = (int64_t)m * e.ld + col;
+      *reinterpret_cast<uint4*>(e.out_hi + o) = oh.u;
+      *reinterpret_cast<uint4*>(e.out_lo + o) = ol.u;
+    }
+  }
+  float ramax = 0.f;
+  epi_flush_amax(e, amax, ramax);
+}
+
+static bool dx_wide_ok(const SkinnyDxArgs& a) {
+  static const int off = getenv("CURVOPT_DX_WIDE") && getenv("CURVOPT_DX_WIDE")[0] == '0';
+  const Epilogue& e = a.epi;
+  return !off && a.nseg == 1 && a.c <= DXW_C && (a.n & 7) == 0 && a.n <= 1024 && a.n >= 64 &&
+         e.mode == EPI_SPLIT_MASK && e.act == CV_ACT_RELU && !e.raw && e.mask_div == 1 && (e.ld & 7) == 0 &&
+         (e.mask_ld & 7) == 0 && !(((uintptr_t)e.out_hi | (uintptr_t)e.out_lo | (uintptr_t)e.mask_hi) & 15);
+}
+
 template <int C, int NSEG>
 static void launch_dx(cv_ctx* ctx, const SkinnyDxArgs& a) {
   const int gx = (a.n + 127) / 128;
@@ -255,6 +350,20 @@ static void launch_dx(cv_ctx* ctx, const SkinnyDxArgs& a) {
 }
 
 void skinny_dx(cv_ctx* ctx, const SkinnyDxArgs& a) {
+  if (dx_wide_ok(a)) {
+    const int rows_chunk = (256 / (a.n >> 3)) * DXW_R;
+    const size_t smem = sizeof(float) * ((size_t)DXW_C * a.n + (size_t)rows_chunk * DXW_C);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_dx_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      attr = true;
+    }
+    int grid = (a.rows + rows_chunk - 1) / rows_chunk;
+    if (grid > 2 * ctx->sm_count) grid = 2 * ctx->sm_count;
+    launch_k(ctx->stream, k_dx_wide, grid, 256, smem, a);
+    ctx->launches++;
+    return;
+  }
   const bool two = a.nseg > 1;
   if (a.c == 10) two ? launch_dx<10, 2>(ctx, a) : launch_dx<10, 1>(ctx, a);
   else if (a.c <= 16) two ? launch_dx<16, 2>(ctx, a) : launch_dx<16, 1>(ctx, a);
