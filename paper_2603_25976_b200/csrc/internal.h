@@ -135,7 +135,7 @@ struct cv_ctx {
   void* nccl = nullptr;          // ncclComm_t
   double* red_ws = nullptr;      // reduction partials: kRedBlocks * 8 doubles
   double* scal_ws = nullptr;     // scratch scalars (64 doubles)
-  float* amax_ws = nullptr;      // split.cu: per-block maxima (2 x 148 x 16 floats)
+  float* amax_ws = nullptr;      // split.cu: per-block maxima (4 x 148 x 16 floats)
   unsigned* amax_counter = nullptr;  // split.cu: last-block counter (returns to 0 after each pass)
   int64_t launches = 0;
   cudaStream_t side = nullptr;   // second stream for co-scheduled independent GEMMs

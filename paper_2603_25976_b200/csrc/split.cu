@@ -11,7 +11,7 @@
 
 namespace cv {
 
-constexpr int SP_NB = 2 * 148, SP_NT = 256, SP_MAXL = 16;
+constexpr int SP_NB = 4 * 148, SP_NT = 256, SP_MAXL = 16;  // grid: 16 B x 151K threads in flight per stream
 
 struct OffTab {
   int64_t off[SP_MAXL + 1];
@@ -135,14 +135,25 @@ __global__ void __launch_bounds__(SP_NT) k_cg_pnext_amax(const float* __restrict
   auto minv = [&](int64_t i) { return pre ? 1.f / (fmaxf(pre[i], floor_) + lam) : 1.f; };
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
   const int64_t nq = d >> 2;
+  const bool pre4 = pre && !((uintptr_t)pre & 15);
   for (int64_t q = tid; q < nq; q += nth) {
     const int64_t i = 4 * q;
     const float4 r4 = *reinterpret_cast<const float4*>(r + i);
     float4 p4 = *reinterpret_cast<const float4*>(p + i);
-    p4.x = minv(i) * r4.x + beta * p4.x;
-    p4.y = minv(i + 1) * r4.y + beta * p4.y;
-    p4.z = minv(i + 2) * r4.z + beta * p4.z;
-    p4.w = minv(i + 3) * r4.w + beta * p4.w;
+    float4 m4 = make_float4(1.f, 1.f, 1.f, 1.f);
+    if (pre4) {
+      m4 = *reinterpret_cast<const float4*>(pre + i);
+      m4.x = 1.f / (fmaxf(m4.x, floor_) + lam);
+      m4.y = 1.f / (fmaxf(m4.y, floor_) + lam);
+      m4.z = 1.f / (fmaxf(m4.z, floor_) + lam);
+      m4.w = 1.f / (fmaxf(m4.w, floor_) + lam);
+    } else if (pre) {
+      m4 = make_float4(minv(i), minv(i + 1), minv(i + 2), minv(i + 3));
+    }
+    p4.x = m4.x * r4.x + beta * p4.x;
+    p4.y = m4.y * r4.y + beta * p4.y;
+    p4.z = m4.z * r4.z + beta * p4.z;
+    p4.w = m4.w * r4.w + beta * p4.w;
     *reinterpret_cast<float4*>(p + i) = p4;
     take(i, p4.x);
     take(i + 1, p4.y);

@@ -7,6 +7,8 @@
 
 #include <float.h>
 
+#include <type_traits>
+
 namespace cv {
 
 constexpr int NB = kRedBlocks, NT = kRedThreads;
@@ -34,6 +36,43 @@ CV_DEV void write_partials(double* ws, double (&t)[NV]) {
 
 CV_DEV float4 ld4g(const float* p) { return *reinterpret_cast<const float4*>(p); }
 
+// W consecutive floats (W = 4: one 128-bit access) -- the vector kernels below are
+// written once as body(W, i) and run on 4-element groups plus a scalar tail, so
+// every thread keeps 16 bytes per stream in flight (what HBM needs at this grid).
+template <int W>
+struct Vf {
+  float v[W];
+};
+template <int W>
+CV_DEV Vf<W> ldv(const float* p) {
+  Vf<W> r;
+  if constexpr (W == 4) {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    r.v[0] = a.x; r.v[1] = a.y; r.v[2] = a.z; r.v[3] = a.w;
+  } else {
+    r.v[0] = *p;
+  }
+  return r;
+}
+template <int W>
+CV_DEV void stv(float* p, const Vf<W>& r) {
+  if constexpr (W == 4) *reinterpret_cast<float4*>(p) = make_float4(r.v[0], r.v[1], r.v[2], r.v[3]);
+  else *p = r.v[0];
+}
+using W4 = std::integral_constant<int, 4>;
+using W1 = std::integral_constant<int, 1>;
+CV_DEV bool al16p(const void* a, const void* b = nullptr, const void* c = nullptr, const void* d = nullptr) {
+  return (((uintptr_t)a | (uintptr_t)b | (uintptr_t)c | (uintptr_t)d) & 15) == 0;
+}
+// grid-stride over 4-element groups (when `al`), then the scalar tail
+template <typename F>
+CV_DEV void vec_for(int64_t n, bool al, F&& body) {
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, st = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nq = al ? (n >> 2) : 0;
+  for (int64_t q = t0; q < nq; q += st) body(W4{}, 4 * q);
+  for (int64_t i = 4 * nq + t0; i < n; i += st) body(W1{}, i);
+}
+
 CV_DEV float minv_of(const float* pre, int64_t i, float lam, float floor_) {
   return pre ? 1.f / (fmaxf(pre[i], floor_) + lam) : 1.f;
 }
@@ -55,7 +94,13 @@ CV_DEV float rad(uint64_t seed, uint64_t counter, int64_t i) {
 
 __global__ void k_rademacher(uint64_t seed, uint64_t counter, int64_t n, float scale, float* out) {
   CV_PDL_ENTRY();
-  GRID_STRIDE(i, n) out[i] = rad(seed, counter, i) * scale;
+  vec_for(n, al16p(out), [&](auto W_, int64_t i) {
+    constexpr int W = decltype(W_)::value;
+    Vf<W> o;
+#pragma unroll
+    for (int j = 0; j < W; ++j) o.v[j] = rad(seed, counter, i + j) * scale;
+    stv<W>(out + i, o);
+  });
 }
 
 void rademacher(cv_ctx* ctx, uint64_t seed, uint64_t counter, int64_t n, float* out) {
@@ -76,7 +121,12 @@ void scale_scalar(cv_ctx* ctx, double* x, double s) {
 __global__ void k_dot(const float* a, const float* b, int64_t n, double* ws) {
   CV_PDL_ENTRY();
   double t[1] = {0.0};
-  GRID_STRIDE(i, n) t[0] += (double)a[i] * (double)b[i];
+  vec_for(n, al16p(a, b), [&](auto W_, int64_t i) {
+    constexpr int W = decltype(W_)::value;
+    const Vf<W> x = ldv<W>(a + i), y = ldv<W>(b + i);
+#pragma unroll
+    for (int j = 0; j < W; ++j) t[0] += (double)x.v[j] * (double)y.v[j];
+  });
   write_partials<1>(ws, t);
 }
 __global__ void k_dot_final(const double* ws, double* out) {
@@ -97,16 +147,24 @@ __global__ void k_apply_update(const float* w, const float* dir, float coef, int
                                double* ws) {
   CV_PDL_ENTRY();
   double t[3] = {0.0, 0.0, 0.0};
-  GRID_STRIDE(i, d) {
-    const float di = dir[i];
-    const float u = di * coef;
-    const float x = w[i] + u;
-    upd[i] = u;
-    wn[i] = x;
-    t[0] += (double)u * u;
-    t[1] += (!isfinite(di) || !isfinite(u) || !isfinite(x)) ? 1.0 : 0.0;
-    t[2] += (double)di * di;
-  }
+  vec_for(d, al16p(w, dir, upd, wn), [&](auto W_, int64_t i) {
+    constexpr int W = decltype(W_)::value;
+    const Vf<W> dv = ldv<W>(dir + i), wv = ldv<W>(w + i);
+    Vf<W> uv, xv;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      const float di = dv.v[j];
+      const float u = di * coef;
+      const float x = wv.v[j] + u;
+      uv.v[j] = u;
+      xv.v[j] = x;
+      t[0] += (double)u * u;
+      t[1] += (!isfinite(di) || !isfinite(u) || !isfinite(x)) ? 1.0 : 0.0;
+      t[2] += (double)di * di;
+    }
+    stv<W>(upd + i, uv);
+    stv<W>(wn + i, xv);
+  });
   write_partials<3>(ws, t);
 }
 __global__ void k_apply_update_final(const double* ws, double* scal) {
@@ -125,11 +183,15 @@ void apply_update(cv_ctx* ctx, const float* w, const float* dir, double coef, in
 __global__ void k_norm_check(const float* x, int64_t d, double* ws) {
   CV_PDL_ENTRY();
   double t[2] = {0.0, 0.0};
-  GRID_STRIDE(i, d) {
-    const float v = x[i];
-    t[0] += (double)v * v;
-    t[1] += isfinite(v) ? 0.0 : 1.0;
-  }
+  vec_for(d, al16p(x), [&](auto W_, int64_t i) {
+    constexpr int W = decltype(W_)::value;
+    const Vf<W> xv = ldv<W>(x + i);
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      t[0] += (double)xv.v[j] * xv.v[j];
+      t[1] += isfinite(xv.v[j]) ? 0.0 : 1.0;
+    }
+  });
   write_partials<2>(ws, t);
 }
 __global__ void k_norm_check_final(const double* ws, double* scal) {
@@ -148,12 +210,19 @@ void norm_check(cv_ctx* ctx, const float* x, int64_t d, double* scal) {
 __global__ void k_diag_ema(float* diag, const float* est, float beta, int64_t d, int mode, double* ws) {
   CV_PDL_ENTRY();
   double t[1] = {0.0};
-  GRID_STRIDE(i, d) {
-    const float e = est[i];
-    const float v = mode == 0 ? fmaxf(beta * diag[i] + (1.f - beta) * e, 0.f) : fmaxf(e, 0.f);
-    diag[i] = v;
-    t[0] += v;
-  }
+  vec_for(d, al16p(diag, est), [&](auto W_, int64_t i) {
+    constexpr int W = decltype(W_)::value;
+    const Vf<W> ev = ldv<W>(est + i);
+    Vf<W> dv = ldv<W>(diag + i);
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      const float e = ev.v[j];
+      const float v = mode == 0 ? fmaxf(beta * dv.v[j] + (1.f - beta) * e, 0.f) : fmaxf(e, 0.f);
+      dv.v[j] = v;
+      t[0] += v;
+    }
+    stv<W>(diag + i, dv);
+  });
   write_partials<1>(ws, t);
 }
 __global__ void k_mean_final(const double* ws, double inv_n, double* out) {
@@ -179,16 +248,21 @@ __global__ void k_hutch_acc(uint64_t seed, uint64_t counter, const float* hz, in
                             int last, float inv_n, double* ws) {
   CV_PDL_ENTRY();
   double t[1] = {0.0};
-  GRID_STRIDE(i, d) {
-    const float z = rad(seed, counter, i);
-    const float zh = z * hz[i];
-    t[0] += (double)zh;
-    if (diag) {
-      float a = first ? zh : diag[i] + zh;
+  vec_for(d, al16p(hz, diag), [&](auto W_, int64_t i) {
+    constexpr int W = decltype(W_)::value;
+    const Vf<W> hv = ldv<W>(hz + i);
+    Vf<W> dv;
+    if (diag && !first) dv = ldv<W>(diag + i);
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      const float zh = rad(seed, counter, i + j) * hv.v[j];
+      t[0] += (double)zh;
+      float a = first ? zh : dv.v[j] + zh;
       if (last) a *= inv_n;
-      diag[i] = a;
+      dv.v[j] = a;
     }
-  }
+    if (diag) stv<W>(diag + i, dv);
+  });
   write_partials<1>(ws, t);
 }
 __global__ void k_trace_final(const double* ws, double inv_n, double* out, int first) {
@@ -236,10 +310,15 @@ __global__ void k_pi_reduce(const float* v, const float* hv, int64_t d, double* 
   CV_PDL_ENTRY();
   if (skip_if(skip)) return;
   double t[2] = {0.0, 0.0};
-  GRID_STRIDE(i, d) {
-    t[0] += (double)v[i] * hv[i];
-    t[1] += (double)hv[i] * hv[i];
-  }
+  vec_for(d, al16p(v, hv), [&](auto W_, int64_t i) {
+    constexpr int W = decltype(W_)::value;
+    const Vf<W> a = ldv<W>(v + i), h = ldv<W>(hv + i);
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      t[0] += (double)a.v[j] * h.v[j];
+      t[1] += (double)h.v[j] * h.v[j];
+    }
+  });
   write_partials<2>(ws, t);
 }
 __global__ void k_pi_final(const double* ws, PiDev* st, double* norm_out) {
@@ -258,7 +337,14 @@ __global__ void k_pi_final(const double* ws, PiDev* st, double* norm_out) {
 __global__ void k_pi_next(const float* hv, const double* nrm, int64_t d, float* v, const int* skip) {
   CV_PDL_ENTRY();
   if (skip_if(skip)) return;
-  GRID_STRIDE(i, d) v[i] = (float)((double)hv[i] / *nrm);
+  const double nr = *nrm;
+  vec_for(d, al16p(hv, v), [&](auto W_, int64_t i) {
+    constexpr int W = decltype(W_)::value;
+    Vf<W> a = ldv<W>(hv + i);
+#pragma unroll
+    for (int j = 0; j < W; ++j) a.v[j] = (float)((double)a.v[j] / nr);
+    stv<W>(v + i, a);
+  });
 }
 __global__ void k_pi_out(const PiDev* st, double* out) {
   CV_PDL_ENTRY(); *out = st->result; }
@@ -297,10 +383,17 @@ struct CgDev {
 __global__ void k_cg_init(const float* g, const float* x0, int64_t d, double* ws) {
   CV_PDL_ENTRY();
   double t[2] = {0.0, 0.0};
-  GRID_STRIDE(i, d) {
-    t[0] += (double)g[i] * g[i];
-    if (x0) t[1] += x0[i] != 0.f ? 1.0 : 0.0;
-  }
+  vec_for(d, al16p(g, x0), [&](auto W_, int64_t i) {
+    constexpr int W = decltype(W_)::value;
+    const Vf<W> gv = ldv<W>(g + i);
+    Vf<W> xv;
+    if (x0) xv = ldv<W>(x0 + i);
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      t[0] += (double)gv.v[j] * gv.v[j];
+      if (x0) t[1] += xv.v[j] != 0.f ? 1.0 : 0.0;
+    }
+  });
   write_partials<2>(ws, t);
 }
 __global__ void k_cg_init_final(const double* ws, CgDev* st) {
@@ -322,7 +415,15 @@ __global__ void k_cg_init_final(const double* ws, CgDev* st) {
 __global__ void k_cg_setup_x(const float* x0, const CgDev* st, int64_t d, float* x) {
   CV_PDL_ENTRY();
   const bool use = st->x0nz;
-  GRID_STRIDE(i, d) x[i] = use ? x0[i] : 0.f;
+  vec_for(d, al16p(x0, x), [&](auto W_, int64_t i) {
+    constexpr int W = decltype(W_)::value;
+    Vf<W> a;
+    if (use) a = ldv<W>(x0 + i);
+    else
+#pragma unroll
+      for (int j = 0; j < W; ++j) a.v[j] = 0.f;
+    stv<W>(x + i, a);
+  });
 }
 // r = g - (Ax + lam x) (warm) or g; partial ||r||^2
 __global__ void k_cg_r0(const float* g, const float* ax, const float* x, float lam, const CgDev* st, int64_t d,
@@ -331,11 +432,18 @@ __global__ void k_cg_r0(const float* g, const float* ax, const float* x, float l
   if (st->done) return;
   const bool warm = st->x0nz;
   double t[1] = {0.0};
-  GRID_STRIDE(i, d) {
-    const float v = warm ? g[i] - (ax[i] + lam * x[i]) : g[i];
-    r[i] = v;
-    t[0] += (double)v * v;
-  }
+  vec_for(d, al16p(g, ax, x, r), [&](auto W_, int64_t i) {
+    constexpr int W = decltype(W_)::value;
+    Vf<W> v = ldv<W>(g + i);
+    if (warm) {
+      const Vf<W> av = ldv<W>(ax + i), xv = ldv<W>(x + i);
+#pragma unroll
+      for (int j = 0; j < W; ++j) v.v[j] = v.v[j] - (av.v[j] + lam * xv.v[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < W; ++j) t[0] += (double)v.v[j] * v.v[j];
+    stv<W>(r + i, v);
+  });
   write_partials<1>(ws, t);
 }
 __global__ void k_cg_r0_final(const double* ws, CgDev* st, double tol) {
@@ -356,12 +464,19 @@ __global__ void k_cg_p0(const float* r, const float* pre, float lam, float floor
   CV_PDL_ENTRY();
   if (st->done) return;
   double t[1] = {0.0};
-  GRID_STRIDE(i, d) {
-    const float ri = r[i];
-    const float z = minv_of(pre, i, lam, floor_) * ri;
-    p[i] = z;
-    t[0] += (double)ri * z;
-  }
+  vec_for(d, al16p(r, pre, p), [&](auto W_, int64_t i) {
+    constexpr int W = decltype(W_)::value;
+    const Vf<W> rv = ldv<W>(r + i);
+    Vf<W> mv, z;
+    if (pre) mv = ldv<W>(pre + i);
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      const float mi = pre ? 1.f / (fmaxf(mv.v[j], floor_) + lam) : 1.f;
+      z.v[j] = mi * rv.v[j];
+      t[0] += (double)rv.v[j] * z.v[j];
+    }
+    stv<W>(p + i, z);
+  });
   write_partials<1>(ws, t);
 }
 __global__ void k_cg_p0_final(const double* ws, CgDev* st) {
@@ -494,7 +609,14 @@ __global__ void k_cg_xupdate(float* x, const float* p, const CgDev* st, int64_t 
   CV_PDL_ENTRY();
   if (st->done) return;
   const float a = (float)st->alpha;
-  GRID_STRIDE(i, d) x[i] += a * p[i];
+  vec_for(d, al16p(x, p), [&](auto W_, int64_t i) {
+    constexpr int W = decltype(W_)::value;
+    Vf<W> xv = ldv<W>(x + i);
+    const Vf<W> pv = ldv<W>(p + i);
+#pragma unroll
+    for (int j = 0; j < W; ++j) xv.v[j] += a * pv.v[j];
+    stv<W>(x + i, xv);
+  });
 }
 // r = g - (Ax + lam x); partials ||r||^2, r.M^-1 r
 __global__ void k_cg_rstab(const float* g, const float* ax, const float* x, float* r, const float* pre, float lam,
@@ -503,12 +625,21 @@ __global__ void k_cg_rstab(const float* g, const float* ax, const float* x, floa
   CV_PDL_ENTRY();
   if (st->done) return;
   double t[2] = {0.0, 0.0};
-  GRID_STRIDE(i, d) {
-    const float ri = g[i] - (ax[i] + lam * x[i]);
-    r[i] = ri;
-    t[0] += (double)ri * ri;
-    t[1] += (double)ri * (minv_of(pre, i, lam, floor_) * ri);
-  }
+  vec_for(d, al16p(g, ax, x, r) && al16p(pre), [&](auto W_, int64_t i) {
+    constexpr int W = decltype(W_)::value;
+    const Vf<W> gv = ldv<W>(g + i), av = ldv<W>(ax + i), xv = ldv<W>(x + i);
+    Vf<W> mv, rv;
+    if (pre) mv = ldv<W>(pre + i);
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      const float ri = gv.v[j] - (av.v[j] + lam * xv.v[j]);
+      rv.v[j] = ri;
+      const float mi = pre ? 1.f / (fmaxf(mv.v[j], floor_) + lam) : 1.f;
+      t[0] += (double)ri * ri;
+      t[1] += (double)ri * (mi * ri);
+    }
+    stv<W>(r + i, rv);
+  });
   write_partials<2>(ws, t);
   if (grid_last(ctr)) r_final_body(ws, st, k, maxiter, 1, tol);
 }
