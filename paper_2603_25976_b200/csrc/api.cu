@@ -98,6 +98,12 @@ int cv_ctx_destroy(cv_ctx* ctx) {
     cudaEventDestroy(ctx->ev_fork);
     cudaEventDestroy(ctx->ev_join);
   }
+  if (ctx->side2) {
+    cudaStreamSynchronize(ctx->side2);
+    cudaStreamDestroy(ctx->side2);
+    cudaEventDestroy(ctx->ev_fork2);
+    cudaEventDestroy(ctx->ev_join2);
+  }
   ctx->pool.release_all();
   delete ctx;
   return CV_OK;

@@ -1048,7 +1048,8 @@ static int launch_tc(cv_ctx* ctx, const GemmArgs& g, int splits, float* ext_part
   if (part) {
     launch_k(st, k_splitk_reduce, 4 * ctx->sm_count, 256, 0, part, splits, g.M, g.N, g.epi, g.skip, g.lower_only);
     ctx->launches++;
-    if (st != ctx->stream) ctx->deferred.push_back(part);  // reused only after the join
+    if (st == ctx->side2 && st) ctx->deferred2.push_back(part);
+    else if (st != ctx->stream) ctx->deferred.push_back(part);  // reused only after the join
     else ctx->pool.put(part);  // stream-ordered reuse: later users enqueue after this kernel
   }
   return splits;

@@ -231,7 +231,8 @@ static void launch_tc2(cv_ctx* ctx, const GemmArgs& g, int splits) {
   if (splits > 1) {
     launch_k(st, k_splitk_reduce, 4 * ctx->sm_count, 256, 0, part, splits, g.M, g.N, g.epi, g.skip, g.lower_only);
     ctx->launches++;
-    if (st != ctx->stream) ctx->deferred.push_back(part);  // reused only after the join
+    if (st == ctx->side2 && st) ctx->deferred2.push_back(part);
+    else if (st != ctx->stream) ctx->deferred.push_back(part);  // reused only after the join
     else ctx->pool.put(part);
   }
 }

@@ -141,6 +141,9 @@ struct cv_ctx {
   cudaStream_t side = nullptr;   // second stream for co-scheduled independent GEMMs
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<void*> deferred;   // side-stream scratch, returned to the pool after the join
+  cudaStream_t side2 = nullptr;  // third stream: the output layer's weight gradient beside the pair
+  cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
+  std::vector<void*> deferred2;  // side2 scratch, returned after side_join
 };
 
 struct cv_snap {
@@ -235,7 +238,8 @@ void gemm(cv_ctx* ctx, const GemmArgs& a);  // engine dispatch
 void gemm_pair(cv_ctx* ctx, GemmArgs a, GemmArgs b);
 double gemm_tc_estimate(const cv_ctx* ctx, const GemmArgs& g, int ctas);  // relative time on `ctas` SMs
 cudaStream_t side_fork(cv_ctx* ctx);  // side stream ordered after the context stream's current work
-void side_join(cv_ctx* ctx);          // context stream waits for the side stream
+cudaStream_t side2_fork(cv_ctx* ctx); // third stream, same ordering; joined by side_join
+void side_join(cv_ctx* ctx);          // context stream waits for the side streams
 int gemm_tc_partial(cv_ctx* ctx, const GemmArgs& g, float** partial);  // N <= 32, raw split-K partials
 int gemm_tc_head_groups(const cv_ctx* ctx, const GemmArgs& g);          // 0: no fused output-layer head
 

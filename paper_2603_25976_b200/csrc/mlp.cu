@@ -419,10 +419,11 @@ static void skinny_weight_grad(cv_ctx* ctx, cv_snap* s, const float* U, Scale* u
     g.epi.ld = s->c;
     g.skip = skip;
     static const int cosched = !(getenv("CURVOPT_COSCHED") && getenv("CURVOPT_COSCHED")[0] == '0');
-    if (side && cosched && ctx->engine != CV_ENGINE_SIMT && gemm_tc_supported(g)) {
+    static const int side_ctas = getenv("CURVOPT_DWL_CTAS") ? atoi(getenv("CURVOPT_DWL_CTAS")) : 48;
+    if (side && cosched && side_ctas > 0 && ctx->engine != CV_ENGINE_SIMT && gemm_tc_supported(g)) {
       // beside the output-layer backward (the caller joins the side stream)
-      g.stream = side_fork(ctx);
-      g.max_ctas = 48;
+      g.stream = side2_fork(ctx);
+      g.max_ctas = side_ctas;
     }
     gemm(ctx, g);
     return;

@@ -153,7 +153,25 @@ cudaStream_t side_fork(cv_ctx* ctx) {
   return ctx->side;
 }
 
+cudaStream_t side2_fork(cv_ctx* ctx) {
+  if (!ctx->side2) {
+    if (cudaStreamCreateWithFlags(&ctx->side2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_fork2, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_join2, cudaEventDisableTiming) != cudaSuccess)
+      throw std::runtime_error("CUDA: cannot create the second side stream");
+  }
+  cudaEventRecord(ctx->ev_fork2, ctx->stream);
+  cudaStreamWaitEvent(ctx->side2, ctx->ev_fork2, 0);
+  return ctx->side2;
+}
+
 void side_join(cv_ctx* ctx) {
+  if (ctx->side2) {
+    cudaEventRecord(ctx->ev_join2, ctx->side2);
+    cudaStreamWaitEvent(ctx->stream, ctx->ev_join2, 0);
+    for (void* p : ctx->deferred2) ctx->pool.put(p);
+    ctx->deferred2.clear();
+  }
   if (!ctx->side) return;
   cudaEventRecord(ctx->ev_join, ctx->side);
   cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0);

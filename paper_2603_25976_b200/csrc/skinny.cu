@@ -244,87 +244,98 @@ __global__ void __launch_bounds__(128) k_dx(SkinnyDxArgs a) {
   epi_flush_amax(e, amax, ramax);
 }
 
-// dx, wide variant for the hot case (one segment, ReLU mask, c <= 10, n <= 1024,
-// 16-byte rows): a thread owns 8 adjacent columns (128-bit mask loads and split
-// stores), the n/8 threads of a row span it, a 256-thread block covers 256/(n/8)
-// rows per pass and DXW_R passes per chunk.  W^T is staged once per block in
-// shared memory as [c][n]; the chunk's mask loads are issued before its U rows are
-// staged, and each W row read from smem feeds all DXW_R rows of the thread.
-constexpr int DXW_R = 4;
+// dx, streaming variant for the hot case (one segment, ReLU mask, c <= 10, n <= 1024,
+// 16-byte rows): a thread owns 4 adjacent columns with their W entries in
+// registers, n/4 threads span a row, and each block streams a contiguous range of
+// rows: the block's U rows are staged in shared memory once (one barrier), the
+// 64-bit mask loads of DXW_R rows are in flight ahead of their use, the split
+// output leaves as two 64-bit stores per row.
+constexpr int DXW_R = 8;
 constexpr int DXW_C = 10;
-__global__ void __launch_bounds__(256) k_dx_wide(SkinnyDxArgs a) {
+
+// d = a * b + c on two fp32 lanes (sm_100 FFMA2)
+CV_DEV float2 ffma2_dx(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__global__ void __launch_bounds__(256, 2) k_dx_wide(SkinnyDxArgs a, int rows_per_block) {
   CV_PDL_ENTRY();
   if (skip_if(a.skip)) return;
-  extern __shared__ __align__(16) float dxw_smem[];
-  float* Wt = dxw_smem;                    // [DXW_C][n]
-  const int tpr = a.n >> 3;                // threads per row
-  const int rpp = 256 / tpr;               // rows per pass
-  const int rows_chunk = rpp * DXW_R;
-  float* Us = Wt + DXW_C * a.n;            // [rows_chunk][DXW_C]
-  const int t = threadIdx.x;
-  const int rl = t / tpr, col = (t - rl * tpr) * 8;
-  const bool act = rl < rpp;
+  const int tpr = a.n >> 2;               // threads per row (<= 256)
+  const int rpp = 256 / tpr;              // rows per pass
+  const int rl = threadIdx.x / tpr, col = (threadIdx.x - rl * tpr) * 4;
+  float w[DXW_C][4];
   {
     const float winv = pow2f(-a.w_sc[0]->e);
-    for (int i = t; i < DXW_C * a.n; i += 256) {
-      const int j = i / a.n, n = i - j * a.n;
-      const int64_t idx = (int64_t)n * a.c + j;
-      Wt[i] = j < a.c ? join16(a.w_hi[0][idx], a.w_lo[0][idx], winv) : 0.f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t base = (int64_t)(col + q) * a.c;
+#pragma unroll
+      for (int j = 0; j < DXW_C; ++j)
+        w[j][q] = j < a.c ? join16(a.w_hi[0][base + j], a.w_lo[0][base + j], winv) : 0.f;
     }
   }
   const Epilogue& e = a.epi;
   const EpiRt rt = epi_prepare(e);
   if (blockIdx.x == 0 && threadIdx.x == 0) epi_publish(e, rt);
   float amax = 0.f;
-  const int chunks = (a.rows + rows_chunk - 1) / rows_chunk;
-  for (int ch = blockIdx.x; ch < chunks; ch += gridDim.x) {
-    const int m0 = ch * rows_chunk;
-    uint4 mk[DXW_R];
+  const int r_begin = blockIdx.x * rows_per_block;
+  const int r_end = min(a.rows, r_begin + rows_per_block);
+  // the block's mask rows are one contiguous range: pull it toward L2 in bulk first
+  if (threadIdx.x < 8 && r_end > r_begin) {
+    const char* mb = reinterpret_cast<const char*>(e.mask_hi + (int64_t)r_begin * e.mask_ld);
+    const int64_t bytes = ((int64_t)(r_end - r_begin) * e.mask_ld * 2) & ~(int64_t)15;
+    const int64_t chunk = ((bytes / 8) + 15) & ~(int64_t)15;
+    const int64_t o = chunk * threadIdx.x;
+    const int64_t len = o >= bytes ? 0 : (bytes - o < chunk ? bytes - o : chunk);
+    if (len > 0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(mb + o), "r"((unsigned)len) : "memory");
+  }
+  // the block's U rows (contiguous) staged once: every later U read is a smem broadcast
+  extern __shared__ __align__(16) float Us[];
+  for (int i = threadIdx.x; i < (r_end - r_begin) * a.c; i += blockDim.x) Us[i] = a.U[0][(int64_t)r_begin * a.c + i];
+  __syncthreads();
+  if (rl >= rpp) return;
+  for (int r0 = r_begin + rl; r0 < r_end; r0 += rpp * DXW_R) {
+    uint2 mk[DXW_R];
 #pragma unroll
     for (int i = 0; i < DXW_R; ++i) {
-      const int m = m0 + i * rpp + rl;
-      mk[i] = make_uint4(0, 0, 0, 0);
-      if (act && m < a.rows) mk[i] = __ldg(reinterpret_cast<const uint4*>(e.mask_hi + (int64_t)m * e.mask_ld + col));
+      const int m = r0 + i * rpp;
+      mk[i] = make_uint2(0, 0);
+      if (m < r_end) mk[i] = __ldg(reinterpret_cast<const uint2*>(e.mask_hi + (int64_t)m * e.mask_ld + col));
     }
-    __syncthreads();  // W staged / the previous chunk's readers of Us are done
-    for (int i = t; i < rows_chunk * DXW_C; i += 256) {
-      const int r = i / DXW_C, j = i - r * DXW_C;
-      Us[i] = (m0 + r < a.rows && j < a.c) ? a.U[0][(int64_t)(m0 + r) * a.c + j] : 0.f;
-    }
-    __syncthreads();
-    if (!act) continue;
-    float v[DXW_R][8];
 #pragma unroll
-    for (int i = 0; i < DXW_R; ++i)
+    for (int i = 0; i < DXW_R; ++i) {
+      const int m = r0 + i * rpp;
+      if (m >= r_end) break;
+      float u[DXW_C];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) v[i][q] = 0.f;
+      for (int j = 0; j < DXW_C; ++j) u[j] = j < a.c ? Us[(m - r_begin) * a.c + j] : 0.f;
+      // column pairs on FFMA2
+      float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-    for (int j = 0; j < DXW_C; ++j) {
-      const float4 w0 = *reinterpret_cast<const float4*>(Wt + j * a.n + col);
-      const float4 w1 = *reinterpret_cast<const float4*>(Wt + j * a.n + col + 4);
-      const float w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-#pragma unroll
-      for (int i = 0; i < DXW_R; ++i) {
-        const float u = Us[(i * rpp + rl) * DXW_C + j];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) v[i][q] = fmaf(u, w[q], v[i][q]);
+      for (int j = 0; j < DXW_C; ++j) {
+        const float2 uu = make_float2(u[j], u[j]);
+        acc[0] = ffma2_dx(uu, make_float2(w[j][0], w[j][1]), acc[0]);
+        acc[1] = ffma2_dx(uu, make_float2(w[j][2], w[j][3]), acc[1]);
       }
-    }
-#pragma unroll
-    for (int i = 0; i < DXW_R; ++i) {
-      const int m = m0 + i * rpp + rl;
-      if (m >= a.rows) break;
-      H8 hm, oh, ol;
+      const float vv[4] = {acc[0].x, acc[0].y, acc[1].x, acc[1].y};
+      H4 hm, oh, ol;
       hm.u = mk[i];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float x = __half2float(hm.h[q]) > 0.f ? v[i][q] : 0.f;
+      for (int q = 0; q < 4; ++q) {
+        const float v = vv[q];
+        const float x = __half2float(hm.h[q]) > 0.f ? v : 0.f;
         amax = fmaxf(amax, fabsf(x));
         split16(x, rt.out_s, oh.h[q], ol.h[q]);
       }
       const int64_t o = (int64_t)m * e.ld + col;
-      *reinterpret_cast<uint4*>(e.out_hi + o) = oh.u;
-      *reinterpret_cast<uint4*>(e.out_lo + o) = ol.u;
+      *reinterpret_cast<uint2*>(e.out_hi + o) = oh.u;
+      *reinterpret_cast<uint2*>(e.out_lo + o) = ol.u;
     }
   }
   float ramax = 0.f;
@@ -351,16 +362,10 @@ static void launch_dx(cv_ctx* ctx, const SkinnyDxArgs& a) {
 
 void skinny_dx(cv_ctx* ctx, const SkinnyDxArgs& a) {
   if (dx_wide_ok(a)) {
-    const int rows_chunk = (256 / (a.n >> 3)) * DXW_R;
-    const size_t smem = sizeof(float) * ((size_t)DXW_C * a.n + (size_t)rows_chunk * DXW_C);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_dx_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-      attr = true;
-    }
-    int grid = (a.rows + rows_chunk - 1) / rows_chunk;
-    if (grid > 2 * ctx->sm_count) grid = 2 * ctx->sm_count;
-    launch_k(ctx->stream, k_dx_wide, grid, 256, smem, a);
+    // contiguous row ranges, 2 resident 256-thread blocks per SM
+    const int blocks = 2 * ctx->sm_count;
+    const int rpb = (a.rows + blocks - 1) / blocks;
+    launch_k(ctx->stream, k_dx_wide, (a.rows + rpb - 1) / rpb, 256, sizeof(float) * (size_t)rpb * a.c, a, rpb);
     ctx->launches++;
     return;
   }
