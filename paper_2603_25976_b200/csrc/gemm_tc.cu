@@ -25,6 +25,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
 #include <mutex>
 #include <stdexcept>
 #include <unordered_map>
@@ -1061,7 +1062,10 @@ static int launch_tc(cv_ctx* ctx, const GemmArgs& g, int splits, float* ext_part
 struct TcPlan {
   int kind;  // 0: <32,4>, 1: 2-CTA 256x256, 2: <256,2>, 3: <128,3>
   int tiles, kb_total, splits;
+  int M, N;
 };
+
+static double plan_time(const TcPlan& p, int sms);
 
 static TcPlan tc_plan_kind(const GemmArgs& g, int sms, int kind) {
   TcPlan p;
@@ -1073,11 +1077,23 @@ static TcPlan tc_plan_kind(const GemmArgs& g, int sms, int kind) {
   p.kb_total = 0;
   for (int s = 0; s < g.nseg; ++s) p.kb_total += (g.seg[s].K + TC_BK - 1) / TC_BK;
   // split K when the tile grid cannot fill the machine (weight-gradient GEMMs: M, N ~ 1e3, K = batch)
+  p.M = g.M;
+  p.N = g.N;
   p.splits = 1;
   if (g.epi.mode == EPI_STORE && p.tiles < slots) {
-    p.splits = slots / p.tiles;
-    if (p.splits > p.kb_total / 4) p.splits = p.kb_total / 4;
-    if (p.splits < 1) p.splits = 1;
+    // the split-K factor whose rounds of items fill the slots best (incl. the partials' round trip)
+    double best = 1e300;
+    int bs = 1;
+    const int smax = p.kb_total / 4 < 32 ? p.kb_total / 4 : 32;
+    for (int sp = 1; sp <= smax; ++sp) {
+      p.splits = sp;
+      const double t = plan_time(p, sms);
+      if (t < best) {
+        best = t;
+        bs = sp;
+      }
+    }
+    p.splits = bs;
   }
   return p;
 }
@@ -1091,7 +1107,10 @@ static double plan_time(const TcPlan& p, int sms) {
   const double item_kb = (double)((p.kb_total + p.splits - 1) / p.splits);
   const double pen = p.kind == 2 ? 1.3 : (p.kind == 3 ? 1.2 : 1.0);  // 2-stage ring / narrower tile (measured)
   const double per_kb = p.kind == 3 ? 0.5 : 1.0;                        // 128 x 128 tile: half the MMA work
-  return rounds * (item_kb * per_kb * pen + 4.0);
+  // split-K partials: written once and read once by the fixed-order reduce (units of
+  // ~1.2 us, one 256x256x64 3xFP16 k-block on a CTA pair, at ~6.5 TB/s)
+  const double red = p.splits > 1 ? (double)(p.splits + 1) * p.M * p.N * 4.0 / 7.8e6 + 2.0 : 0.0;
+  return rounds * (item_kb * per_kb * pen + 4.0) + red;
 }
 
 static TcPlan tc_plan(const GemmArgs& g, int sms) {
@@ -1140,6 +1159,11 @@ int gemm_tc_head_groups(const cv_ctx* ctx, const GemmArgs& g) {
 void gemm_tc(cv_ctx* ctx, const GemmArgs& g) {
   const int sms = g.max_ctas > 0 && g.max_ctas < ctx->sm_count ? g.max_ctas : ctx->sm_count;
   const TcPlan p = tc_plan(g, sms);
+  static const int dbg_plan = getenv("CURVOPT_DEBUG_PLAN") ? 1 : 0;
+  if (dbg_plan)
+    fprintf(stderr, "[plan] M=%d N=%d K=%d nseg=%d mode=%d sms=%d -> kind=%d tiles=%d splits=%d est=%.1f\n", g.M, g.N,
+            g.seg[0].K + (g.nseg > 1 ? g.seg[1].K : 0), g.nseg, g.epi.mode, sms, p.kind, p.tiles, p.splits,
+            plan_time(p, sms));
   switch (p.kind) {
     case 0: launch_tc<32, 4>(ctx, g, p.splits); break;
     case 1: launch_tc2<3>(ctx, g, p.splits); break;

@@ -384,10 +384,13 @@ static GemmArgs hidden_backward_args(cv_snap* s, int l, const SplitBuf& Gl, cons
 }
 
 // [gW; gb]_l = A_l^T G (+ A2^T G2), written into out + off[l] (hidden layers).
+// no_bias: the GEMM covers the W rows only (M = n_l) and the bias row is the
+// column sum of G (bias_colsum) -- when n_l is a multiple of the 256-row tile the
+// ones row would otherwise cost a whole extra row of tiles.
 static GemmArgs weight_grad_args(cv_snap* s, int l, const SplitBuf& G1, const SplitBuf* A2, const SplitBuf* G2,
-                                 float* out, const int* skip) {
+                                 float* out, const int* skip, bool no_bias = false) {
   GemmArgs g;
-  g.M = s->dims[l] + 1;
+  g.M = s->dims[l] + (no_bias ? 0 : 1);
   g.N = s->dims[l + 1];
   g.nseg = A2 ? 2 : 1;
   g.seg[0] = GemmSeg{op_trans(s->acts[l]), mk_op(G1.hi, G1.lo, G1.ld, 1, G1.sc), s->bl};
@@ -397,6 +400,59 @@ static GemmArgs weight_grad_args(cv_snap* s, int l, const SplitBuf& G1, const Sp
   g.epi.ld = s->dims[l + 1];
   g.skip = skip;
   return g;
+}
+
+// gb_l = sum over the batch rows of G_l (models.py:280-281), from its split pair:
+// row-chunk partials, then a fixed-order reduction.  Runs on the second side stream
+// beside the weight-gradient / backward GEMM pair (joined by side_join).
+constexpr int CS_RCH = 256;
+__global__ void __launch_bounds__(128) k_colsum_part(const __half* hi, const __half* lo, int64_t ld, const Scale* sc,
+                                                     int rows, int cols, float* part, const int* skip) {
+  CV_PDL_ENTRY();
+  if (skip_if(skip)) return;
+  const int c8 = (blockIdx.x * 128 + threadIdx.x) * 8;
+  if (c8 >= cols) return;
+  const int rpc = (rows + gridDim.y - 1) / gridDim.y;
+  const int r0 = blockIdx.y * rpc, r1 = min(rows, r0 + rpc);
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+  for (int r = r0; r < r1; ++r) {
+    H8 h, l;
+    h.u = __ldg(reinterpret_cast<const uint4*>(hi + (int64_t)r * ld + c8));
+    l.u = __ldg(reinterpret_cast<const uint4*>(lo + (int64_t)r * ld + c8));
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] += __half2float(h.h[q]) + __half2float(l.h[q]);
+  }
+  const float inv = pow2f(-sc->e);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) part[(int64_t)blockIdx.y * cols + c8 + q] = acc[q] * inv;
+}
+__global__ void k_colsum_final(const float* part, int nch, int cols, float* out, const int* skip) {
+  CV_PDL_ENTRY();
+  if (skip_if(skip)) return;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  double t = 0.0;
+  for (int z = 0; z < nch; ++z) t += part[(int64_t)z * cols + c];
+  out[c] = (float)t;
+}
+
+static bool bias_apart(cv_ctx* ctx, cv_snap* s, int l) {
+  static const int off = !(getenv("CURVOPT_BIAS_APART") && getenv("CURVOPT_BIAS_APART")[0] == '1');  // opt-in
+  const int n = s->dims[l], N = s->dims[l + 1];
+  return !off && ctx->engine != CV_ENGINE_SIMT && n % 256 == 0 && N % 8 == 0;
+}
+
+static void bias_colsum(cv_ctx* ctx, cv_snap* s, int l, const SplitBuf& G, float* out, const int* skip) {
+  const int N = s->dims[l + 1];
+  cudaStream_t st = side2_fork(ctx);
+  float* part = (float*)ctx->pool.get(sizeof(float) * (size_t)CS_RCH * N);
+  launch_k(st, k_colsum_part, dim3((N / 8 + 127) / 128, CS_RCH), 128, 0, (const __half*)G.hi, (const __half*)G.lo,
+           G.ld, (const Scale*)G.sc, s->bl, N, part, skip);
+  launch_k(st, k_colsum_final, (N + 255) / 256, 256, 0, (const float*)part, CS_RCH, N,
+           out + s->off[l] + (int64_t)s->dims[l] * N, skip);
+  ctx->launches += 2;
+  ctx->deferred2.push_back(part);
 }
 
 // last layer: [gW; gb] = A^T U (+ A2^T U2)
@@ -460,10 +516,20 @@ void mlp_linearize(cv_ctx* ctx, cv_snap* s, double* loss_out, float* grad_out) {
       const GemmArgs dx = hidden_backward_args(s, l, s->G[l], s->w_hi, s->w_lo, s->w_sc, s->G[l - 1],
                                                tanh_ ? s->P[l - 1] : nullptr, tanh_ ? s->P_sc[l - 1] : nullptr,
                                                nullptr);
-      if (grad_out) gemm_pair(ctx, dx, weight_grad_args(s, l, s->G[l], nullptr, nullptr, grad_out, nullptr));
-      else gemm(ctx, dx);
+      if (grad_out) {
+        const bool nb = bias_apart(ctx, s, l);
+        if (nb) bias_colsum(ctx, s, l, s->G[l], grad_out, nullptr);
+        gemm_pair(ctx, dx, weight_grad_args(s, l, s->G[l], nullptr, nullptr, grad_out, nullptr, nb));
+      } else {
+        gemm(ctx, dx);
+      }
     }
-    if (grad_out) gemm(ctx, weight_grad_args(s, 0, s->G[0], nullptr, nullptr, grad_out, nullptr));
+    if (grad_out) {
+      const bool nb = bias_apart(ctx, s, 0);
+      if (nb) bias_colsum(ctx, s, 0, s->G[0], grad_out, nullptr);
+      gemm(ctx, weight_grad_args(s, 0, s->G[0], nullptr, nullptr, grad_out, nullptr, nb));
+    }
+    side_join(ctx);
   }
   if (grad_out && ctx->nccl) allreduce_f32(ctx, grad_out, s->d);
 }
@@ -595,7 +661,9 @@ static void vjp_from(cv_ctx* ctx, cv_snap* s, const float* U, Scale* usc, float*
   if (L >= 2) {
     skinny_backward(ctx, s, U, usc, s->w_hi, s->w_lo, s->w_sc, s->gs[L - 2], nullptr, nullptr, skip);
     for (int l = L - 2; l >= 0; --l) {
-      const GemmArgs dw = weight_grad_args(s, l, s->gs[l], nullptr, nullptr, out, skip);
+      const bool nb = bias_apart(ctx, s, l);
+      if (nb) bias_colsum(ctx, s, l, s->gs[l], out, skip);
+      const GemmArgs dw = weight_grad_args(s, l, s->gs[l], nullptr, nullptr, out, skip, nb);
       if (l > 0)
         gemm_pair(ctx, hidden_backward_args(s, l, s->gs[l], s->w_hi, s->w_lo, s->w_sc, s->gs[l - 1], nullptr, nullptr,
                                             skip),
@@ -694,8 +762,10 @@ void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* v, float* out, const int* ski
       skinny_dx(ctx, a);
     }
     for (int h = L - 2; h >= 0; --h) {
-      const GemmArgs dw =
-          weight_grad_args(s, h, s->gs[h], h > 0 ? &s->da[h - 1] : nullptr, h > 0 ? &s->G[h] : nullptr, out, skip);
+      const bool nb = bias_apart(ctx, s, h);
+      if (nb) bias_colsum(ctx, s, h, s->gs[h], out, skip);  // the [da|0] segment adds nothing to the bias row
+      const GemmArgs dw = weight_grad_args(s, h, s->gs[h], h > 0 ? &s->da[h - 1] : nullptr, h > 0 ? &s->G[h] : nullptr,
+                                           out, skip, nb);
       if (h > 0) {
         GemmArgs g;
         g.M = s->bl;
@@ -717,6 +787,7 @@ void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* v, float* out, const int* ski
       }
     }
   }
+  side_join(ctx);
   if (ctx->nccl) allreduce_f32(ctx, out, s->d);
 }
 
