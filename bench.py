@@ -89,7 +89,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -120,6 +120,16 @@ class ClockSampler:
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.rows)}
+
+
+def product_traffic():
+    """DRAM bytes of one GGN product from the committed ncu --set full capture
+    (scratch/product_traffic.py -> profiles/r1b_product_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1b_product_traffic.json")) as f:
+            return float(json.load(f)["dram_bytes_per_product"])
+    except Exception:
+        return None
 
 
 def measured_peaks():
@@ -323,7 +333,9 @@ def run_ours(args, rank, world):
             "gv_per_s": gv_per_s, "gv_per_step": gv_total / args.steps,
             "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak if peak else None, "traffic": None,
+                         "frac": achieved / peak if peak else None, "traffic": product_traffic(),
+                         "traffic_source": "profiles/r1b_product_traffic.json (ncu --set full, DRAM read+write "
+                                           "bytes summed over the product's kernels, cold-cache replay)",
                          "unit_of_work": f"one GGN product at b={bl}: {flops / 1e9:.1f} GFLOP useful, "
                                          f"{gv_ms:.3f} ms avg over {n_gv} (CUDA events)",
                          "peak_source": peak_note},
