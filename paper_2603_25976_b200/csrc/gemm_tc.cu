@@ -1080,7 +1080,12 @@ static TcPlan tc_plan_kind(const GemmArgs& g, int sms, int kind) {
   p.M = g.M;
   p.N = g.N;
   p.splits = 1;
-  if (g.epi.mode == EPI_STORE && p.tiles < slots) {
+  // split-K when the tiles cannot fill the slots (weight gradients: K = batch; every GEMM
+  // at the per-rank batch of a data-parallel run); the fixed-order reduce applies any
+  // element-wise epilogue
+  const bool splittable = !g.lower_only && (g.epi.mode == EPI_STORE || g.epi.mode == EPI_SPLIT_ACT ||
+                                            g.epi.mode == EPI_SPLIT_MASK || g.epi.mode == EPI_HVP);
+  if (splittable && p.tiles < slots) {
     // the split-K factor whose rounds of items fill the slots best (incl. the partials' round trip)
     double best = 1e300;
     int bs = 1;
@@ -1122,8 +1127,10 @@ static TcPlan tc_plan(const GemmArgs& g, int sms) {
   const bool pair = use_2sm && !force_bn && g.M >= 256 && g.N >= 256;
   const bool wide = force_bn ? force_bn == 256 : g.N >= 512;
   TcPlan best = tc_plan_kind(g, sms, pair ? 1 : (wide ? 2 : 3));
-  if (g.epi.mode == EPI_STORE && !force_bn) {
-    // split-K weight gradients: the tile shape that wastes the least of the M edge
+  const int slots = best.kind == 1 ? sms / 2 : sms;
+  if ((g.epi.mode == EPI_STORE || best.tiles < slots) && !force_bn) {
+    // split-K weight gradients and under-filled grids: the tile shape that wastes the
+    // least of the edges / fills the slots best
     for (int k = 1; k <= 3; ++k) {
       if (k == 1 && !pair) continue;
       const TcPlan c = tc_plan_kind(g, sms, k);

@@ -6,7 +6,7 @@ import paper_2603_25976_b200 as P
 from torch.profiler import profile, ProfilerActivity
 m = P.Model(784, (1024, 1024), 10, "relu")
 w = P.init_params(m, P.Rng(0)).to_device()
-r = P.Rng(1); b = 8192
+r = P.Rng(1); b = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 X = torch.from_numpy(r.normal(b*784).reshape(b,784).astype(np.float32)).cuda()
 y = torch.from_numpy(r.integers(b,10)).cuda()
 snap = P.make_snapshot("ggn_ce", m, w, P.Batch(X, y, "ce"))
