@@ -1118,7 +1118,45 @@ static double plan_time(const TcPlan& p, int sms) {
   return rounds * (item_kb * per_kb * pen + 4.0) + red;
 }
 
+static TcPlan tc_plan_search(const GemmArgs& g, int sms);
+
+// Plans depend only on the GEMM's geometry and SM budget: memoised, so the
+// co-scheduling split search (gemm_pair) and every launch stay off the host's
+// critical path.
+struct PlanKey {
+  int M, N, K0, K1, nseg, mode, lower, sms;
+  bool operator==(const PlanKey& o) const {
+    return M == o.M && N == o.N && K0 == o.K0 && K1 == o.K1 && nseg == o.nseg && mode == o.mode &&
+           lower == o.lower && sms == o.sms;
+  }
+};
+struct PlanKeyHash {
+  size_t operator()(const PlanKey& k) const {
+    size_t h = (size_t)k.M * 1000003u ^ (size_t)k.N;
+    h = h * 1000003u ^ (size_t)k.K0;
+    h = h * 1000003u ^ (size_t)k.K1;
+    h = h * 1000003u ^ (size_t)(k.nseg * 64 + k.mode * 2 + k.lower);
+    return h * 1000003u ^ (size_t)k.sms;
+  }
+};
+
 static TcPlan tc_plan(const GemmArgs& g, int sms) {
+  static std::unordered_map<PlanKey, TcPlan, PlanKeyHash> cache;
+  static std::mutex mu;
+  const PlanKey key{g.M, g.N, g.seg[0].K, g.nseg > 1 ? g.seg[1].K : 0, g.nseg, g.epi.mode, g.lower_only, sms};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  const TcPlan p = tc_plan_search(g, sms);
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache.size() > 65536) cache.clear();
+  cache.emplace(key, p);
+  return p;
+}
+
+static TcPlan tc_plan_search(const GemmArgs& g, int sms) {
   static const int force_bn = getenv("CURVOPT_TC_BN") ? atoi(getenv("CURVOPT_TC_BN")) : 0;
   static const int use_2sm = getenv("CURVOPT_TC_2SM") ? atoi(getenv("CURVOPT_TC_2SM")) : 1;
   static const int force_kind = getenv("CURVOPT_TC_KIND") ? atoi(getenv("CURVOPT_TC_KIND")) : -1;
