@@ -295,19 +295,24 @@ __global__ void __launch_bounds__(256, 2) k_dx_wide(SkinnyDxArgs a, int rows_per
     const int64_t len = o >= bytes ? 0 : (bytes - o < chunk ? bytes - o : chunk);
     if (len > 0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(mb + o), "r"((unsigned)len) : "memory");
   }
+  // mask loads of a batch of DXW_R rows (double buffered: batch b+1 is in flight while b is computed)
+  auto load_batch = [&](int r0, uint2 (&mk)[DXW_R]) {
+#pragma unroll
+    for (int i = 0; i < DXW_R; ++i) {
+      const int m = r0 + i * rpp;
+      mk[i] = make_uint2(0, 0);
+      if (rl < rpp && m < r_end) mk[i] = __ldg(reinterpret_cast<const uint2*>(e.mask_hi + (int64_t)m * e.mask_ld + col));
+    }
+  };
+  uint2 mcur[DXW_R], mnext[DXW_R];
+  load_batch(r_begin + rl, mcur);
   // the block's U rows (contiguous) staged once: every later U read is a smem broadcast
   extern __shared__ __align__(16) float Us[];
   for (int i = threadIdx.x; i < (r_end - r_begin) * a.c; i += blockDim.x) Us[i] = a.U[0][(int64_t)r_begin * a.c + i];
   __syncthreads();
   if (rl >= rpp) return;
   for (int r0 = r_begin + rl; r0 < r_end; r0 += rpp * DXW_R) {
-    uint2 mk[DXW_R];
-#pragma unroll
-    for (int i = 0; i < DXW_R; ++i) {
-      const int m = r0 + i * rpp;
-      mk[i] = make_uint2(0, 0);
-      if (m < r_end) mk[i] = __ldg(reinterpret_cast<const uint2*>(e.mask_hi + (int64_t)m * e.mask_ld + col));
-    }
+    if (r0 + rpp * DXW_R < r_end) load_batch(r0 + rpp * DXW_R, mnext);
 #pragma unroll
     for (int i = 0; i < DXW_R; ++i) {
       const int m = r0 + i * rpp;
@@ -325,7 +330,7 @@ __global__ void __launch_bounds__(256, 2) k_dx_wide(SkinnyDxArgs a, int rows_per
       }
       const float vv[4] = {acc[0].x, acc[0].y, acc[1].x, acc[1].y};
       H4 hm, oh, ol;
-      hm.u = mk[i];
+      hm.u = mcur[i];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const float v = vv[q];
@@ -337,6 +342,8 @@ __global__ void __launch_bounds__(256, 2) k_dx_wide(SkinnyDxArgs a, int rows_per
       *reinterpret_cast<uint2*>(e.out_hi + o) = oh.u;
       *reinterpret_cast<uint2*>(e.out_lo + o) = ol.u;
     }
+#pragma unroll
+    for (int i = 0; i < DXW_R; ++i) mcur[i] = mnext[i];
   }
   float ramax = 0.f;
   epi_flush_amax(e, amax, ramax);
