@@ -412,19 +412,18 @@ CV_DEV void tile_epilogue_tma(const TcArgs& a, const TcMaps& maps, const EpiRt& 
   const uint32_t hs = smem_u32(hstg);
   float4 hf[3];
   if (head10) head_fetch10(e, n0 + sb * 16, a.N, lane, hf);
-  // this lane's share of a sub-tile's mask (rows lane/2 and lane/2 + 16, 8 columns),
-  // loaded one sub-tile ahead so the global latency overlaps the previous sub-tile;
-  // the head also needs the low plane (the activation value, not just its sign)
+  // this lane's row of a sub-tile's mask (16 columns = one 32-byte sector), loaded one
+  // sub-tile ahead so the global latency overlaps the previous sub-tile; the head also
+  // needs the low plane (the activation value, not just its sign)
   auto load_mask = [&](int nb, uint4 (&mv)[2], uint4 (&ml)[2]) {
 #pragma unroll
-    for (int it = 0; it < 2; ++it) {
-      const int rr = (lane >> 1) + 16 * it, ch = lane & 1;
-      mv[it] = make_uint4(0, 0, 0, 0);
-      ml[it] = make_uint4(0, 0, 0, 0);
-      if (nb < a.N && r0 + rr < a.M && nb + 8 * ch < a.N) {
-        const int64_t o = (int64_t)(r0 + rr) * e.mask_ld + nb + 8 * ch;
-        mv[it] = *reinterpret_cast<const uint4*>(e.mask_hi + o);
-        if (head) ml[it] = *reinterpret_cast<const uint4*>(e.mask_lo + o);
+    for (int ch = 0; ch < 2; ++ch) {
+      mv[ch] = make_uint4(0, 0, 0, 0);
+      ml[ch] = make_uint4(0, 0, 0, 0);
+      if (m < a.M && nb + 8 * ch < a.N) {
+        const int64_t o = (int64_t)m * e.mask_ld + nb + 8 * ch;
+        mv[ch] = *reinterpret_cast<const uint4*>(e.mask_hi + o);
+        if (head) ml[ch] = *reinterpret_cast<const uint4*>(e.mask_lo + o);
       }
     }
   };
@@ -443,29 +442,16 @@ CV_DEV void tile_epilogue_tma(const TcArgs& a, const TcMaps& maps, const EpiRt& 
     float v[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]) * inv;
-    // the slot must be free: the previous sub-tile's TMA store has read it
-    if (lane == 0) bulk_wait_read0();
-    __syncwarp();
     if (a.tma_out == 1) {
       // ---- split fp16 output (activations / tangents / cotangents) ----
       float o[16];
       if (use_mask) {
-        // stage the mask tile (rows r0..r0+31, cols nb..nb+15; ReLU: sign of hi) and
-        // read back this lane's row
-#pragma unroll
-        for (int it = 0; it < 2; ++it) {
-          const int rr = (lane >> 1) + 16 * it, ch = lane & 1;
-          *reinterpret_cast<uint4*>(stg + rr * 32 + 16 * (ch ^ ((rr >> 2) & 1))) = mcur[it];
-          if (head) *reinterpret_cast<uint4*>(stg + 1024 + rr * 32 + 16 * (ch ^ ((rr >> 2) & 1))) = lcur[it];
-        }
-        __syncwarp();
         H8 mk[2], ml[2];
 #pragma unroll
         for (int ch = 0; ch < 2; ++ch) {
-          mk[ch].u = *reinterpret_cast<const uint4*>(stg + lane * 32 + 16 * (ch ^ ((lane >> 2) & 1)));
-          if (head) ml[ch].u = *reinterpret_cast<const uint4*>(stg + 1024 + lane * 32 + 16 * (ch ^ ((lane >> 2) & 1)));
+          mk[ch].u = mcur[ch];
+          ml[ch].u = lcur[ch];
         }
-        __syncwarp();
 #pragma unroll
         for (int j = 0; j < 16; ++j) o[j] = v[j] * (__half2float(mk[j >> 3].h[j & 7]) > 0.f ? 1.f : 0.f);
         if (head) {
@@ -503,6 +489,10 @@ CV_DEV void tile_epilogue_tma(const TcArgs& a, const TcMaps& maps, const EpiRt& 
         split16(o[j], rt.out_s, h0.h[j], l0.h[j]);
         split16(o[8 + j], rt.out_s, h1.h[j], l1.h[j]);
       }
+      // the slot must be free: the previous sub-tile's TMA store has read it (waited
+      // only now, so that read overlaps this sub-tile's TMEM load and math)
+      if (lane == 0) bulk_wait_read0();
+      __syncwarp();
       const int sw = (lane >> 2) & 1;
       *reinterpret_cast<uint4*>(stg + lane * 32 + 16 * (0 ^ sw)) = h0.u;
       *reinterpret_cast<uint4*>(stg + lane * 32 + 16 * (1 ^ sw)) = h1.u;
@@ -517,6 +507,8 @@ CV_DEV void tile_epilogue_tma(const TcArgs& a, const TcMaps& maps, const EpiRt& 
       }
     } else {
       // ---- fp32 output / split-K partial: 32 rows x 64 B, SWIZZLE_64B ----
+      if (lane == 0) bulk_wait_read0();
+      __syncwarp();
       const int sw = (lane >> 1) & 3;
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch)
@@ -1060,7 +1052,7 @@ static int launch_tc(cv_ctx* ctx, const GemmArgs& g, int splits, float* ext_part
 
 // Tile configuration and split-K factor of a GEMM on `sms` SMs.
 struct TcPlan {
-  int kind;  // 0: <32,4>, 1: 2-CTA 256x256, 2: <256,2>, 3: <128,3>
+  int kind;  // 0: <32,4>, 1: 2-CTA 256x256, 2: <256,2>, 3: <128,3>, 4: 2-CTA 256x128
   int tiles, kb_total, splits;
   int M, N;
 };
@@ -1070,10 +1062,10 @@ static double plan_time(const TcPlan& p, int sms);
 static TcPlan tc_plan_kind(const GemmArgs& g, int sms, int kind) {
   TcPlan p;
   p.kind = kind;
-  const int bn = kind == 0 ? 32 : (kind == 3 ? 128 : 256);
-  const int bm = kind == 1 ? 256 : TC_BM;
+  const int bn = kind == 0 ? 32 : ((kind == 3 || kind == 4) ? 128 : 256);
+  const int bm = (kind == 1 || kind == 4) ? 256 : TC_BM;
   p.tiles = ((g.M + bm - 1) / bm) * ((g.N + bn - 1) / bn);
-  const int slots = kind == 1 ? sms / 2 : sms;  // concurrent work items
+  const int slots = (kind == 1 || kind == 4) ? sms / 2 : sms;  // concurrent work items
   p.kb_total = 0;
   for (int s = 0; s < g.nseg; ++s) p.kb_total += (g.seg[s].K + TC_BK - 1) / TC_BK;
   // split K when the tile grid cannot fill the machine (weight-gradient GEMMs: M, N ~ 1e3, K = batch)
@@ -1106,12 +1098,14 @@ static TcPlan tc_plan_kind(const GemmArgs& g, int sms, int kind) {
 // relative time of a plan: rounds of work items x k-blocks per item (+ fill/epilogue),
 // per SM; a 2-CTA tile costs each SM what a 1-CTA 128 x 256 tile does
 static double plan_time(const TcPlan& p, int sms) {
-  const int slots = p.kind == 1 ? sms / 2 : sms;
+  const int slots = (p.kind == 1 || p.kind == 4) ? sms / 2 : sms;
   const int items = p.tiles * p.splits;
   const int rounds = (items + slots - 1) / slots;
   const double item_kb = (double)((p.kb_total + p.splits - 1) / p.splits);
-  const double pen = p.kind == 2 ? 1.3 : (p.kind == 3 ? 1.2 : 1.0);  // 2-stage ring / narrower tile (measured)
-  const double per_kb = p.kind == 3 ? 0.5 : 1.0;                        // 128 x 128 tile: half the MMA work
+  // 2-stage ring / narrower tiles (measured on B200: the 2-CTA 256x128 tile streams at ~0.7x
+  // the 256x256 rate, so it is only reachable by CURVOPT_TC_KIND=4)
+  const double pen = p.kind == 2 ? 1.3 : (p.kind == 3 ? 1.2 : (p.kind == 4 ? 1.4 : 1.0));
+  const double per_kb = (p.kind == 3 || p.kind == 4) ? 0.5 : 1.0;      // 128-wide tiles: half the MMA work
   // split-K partials: written once and read once by the fixed-order reduce (units of
   // ~1.2 us, one 256x256x64 3xFP16 k-block on a CTA pair, at ~6.5 TB/s)
   const double red = p.splits > 1 ? (double)(p.splits + 1) * p.M * p.N * 4.0 / 7.8e6 + 2.0 : 0.0;
@@ -1161,7 +1155,7 @@ static TcPlan tc_plan_search(const GemmArgs& g, int sms) {
   static const int use_2sm = getenv("CURVOPT_TC_2SM") ? atoi(getenv("CURVOPT_TC_2SM")) : 1;
   static const int force_kind = getenv("CURVOPT_TC_KIND") ? atoi(getenv("CURVOPT_TC_KIND")) : -1;
   if (g.N <= 32) return tc_plan_kind(g, sms, 0);
-  if (force_kind >= 1 && force_kind <= 3) return tc_plan_kind(g, sms, force_kind);
+  if (force_kind >= 1 && force_kind <= 4) return tc_plan_kind(g, sms, force_kind);
   const bool pair = use_2sm && !force_bn && g.M >= 256 && g.N >= 256;
   const bool wide = force_bn ? force_bn == 256 : g.N >= 512;
   TcPlan best = tc_plan_kind(g, sms, pair ? 1 : (wide ? 2 : 3));
@@ -1197,7 +1191,7 @@ int gemm_tc_head_groups(const cv_ctx* ctx, const GemmArgs& g) {
   const int sms = g.max_ctas > 0 && g.max_ctas < ctx->sm_count ? g.max_ctas : ctx->sm_count;
   const TcPlan p = tc_plan(g, sms);
   if (p.kind == 0 || p.splits > 1) return 0;
-  const int bn = p.kind == 3 ? 128 : 256;
+  const int bn = (p.kind == 3 || p.kind == 4) ? 128 : 256;
   return 2 * ((g.N + bn - 1) / bn);
 }
 
@@ -1211,7 +1205,8 @@ void gemm_tc(cv_ctx* ctx, const GemmArgs& g) {
             plan_time(p, sms));
   switch (p.kind) {
     case 0: launch_tc<32, 4>(ctx, g, p.splits); break;
-    case 1: launch_tc2<3>(ctx, g, p.splits); break;
+    case 1: launch_tc2<3, 256>(ctx, g, p.splits); break;
+    case 4: launch_tc2<4, 128>(ctx, g, p.splits); break;
     case 2: launch_tc<256, 2>(ctx, g, p.splits); break;
     default: launch_tc<128, 3>(ctx, g, p.splits); break;
   }

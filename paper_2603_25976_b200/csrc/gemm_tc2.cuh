@@ -9,12 +9,11 @@
 // epilogue warps release the accumulator on the leader's "tempty" barrier.
 // Persistent over work items, TMEM double buffered (2 x 256 columns).
 
-constexpr int TC2_BN = 256;
-
-template <int STAGES>
+// TC2_BN = tile width of the pair: 256 (each CTA stages 128 B columns) or 128 (64).
+template <int STAGES, int TC2_BN>
 struct Tc2Cfg {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;         // 16 KB: this CTA's 128 rows
-  static constexpr int B_BYTES = (TC2_BN / 2) * TC_BK * 2;  // 16 KB: this CTA's 128 columns
+  static constexpr int B_BYTES = (TC2_BN / 2) * TC_BK * 2;  // 16 / 8 KB: this CTA's 128 / 64 columns
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + TC_ZERO_BYTES + TC_STG_TOTAL + 1024 + 256;
   static constexpr int TMEM_COLS = 2 * TC2_BN;
@@ -57,11 +56,11 @@ CV_DEV void load_slab_2sm(uint8_t* dst, const CUtensorMap* map, uint32_t bar, bo
   }
 }
 
-template <int STAGES>
+template <int STAGES, int TC2_BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     k_gemm_tc2(const __grid_constant__ TcMaps maps, const TcArgs a) {
   CV_PDL_ENTRY();
-  using Cfg = Tc2Cfg<STAGES>;
+  using Cfg = Tc2Cfg<STAGES, TC2_BN>;
   if (skip_if(a.skip)) return;  // the flag is identical for both CTAs of the pair
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -198,12 +197,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   }
 }
 
-template <int STAGES>
+template <int STAGES, int TC2_BN>
 static void launch_tc2(cv_ctx* ctx, const GemmArgs& g, int splits) {
-  using Cfg = Tc2Cfg<STAGES>;
+  using Cfg = Tc2Cfg<STAGES, TC2_BN>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_gemm_tc2<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    cudaFuncSetAttribute(k_gemm_tc2<STAGES, TC2_BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     attr_set = true;
   }
   TcMaps maps;
@@ -226,7 +225,7 @@ static void launch_tc2(cv_ctx* ctx, const GemmArgs& g, int splits) {
   const int pairs = sms / 2;
   const int grid = 2 * (work < pairs ? work : pairs);
   cudaStream_t st = g.stream ? g.stream : ctx->stream;
-  launch_k(st, k_gemm_tc2<STAGES>, grid, 320, Cfg::SMEM, maps, a);
+  launch_k(st, k_gemm_tc2<STAGES, TC2_BN>, grid, 320, Cfg::SMEM, maps, a);
   ctx->launches++;
   if (splits > 1) {
     launch_k(st, k_splitk_reduce, 4 * ctx->sm_count, 256, 0, part, splits, g.M, g.N, g.epi, g.skip, g.lower_only);
