@@ -204,6 +204,13 @@ int cv_linearize(cv_ctx* ctx, int n_layers, const int* dims, int act, int loss, 
     s->v_hi = alloc_h(s, s->d);
     s->v_lo = alloc_h(s, s->d);
     for (int l = 0; l < L; ++l) s->acts.push_back(alloc_split(s, b, dims[l], acts_sc + l));
+    s->bits_buf.assign(L, nullptr);
+    if (act == CV_ACT_RELU && ctx->engine != CV_ENGINE_SIMT)
+      for (int l = 1; l < L; ++l) {
+        const int64_t ldw = ((dims[l] + 15) / 16 + 7) / 8 * 8;
+        s->bits_buf[l] = (uint16_t*)ctx->pool.get(sizeof(uint16_t) * (size_t)b * ldw);
+        s->owned.push_back(s->bits_buf[l]);
+      }
     s->logits = alloc_f(s, (int64_t)b * c);
     s->probs = alloc_f(s, (int64_t)b * c);
     s->gout = alloc_f(s, (int64_t)b * c);

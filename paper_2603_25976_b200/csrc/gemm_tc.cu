@@ -393,7 +393,9 @@ CV_DEV void head_acc_generic(const Epilogue& e, int nb, int N, const float (&av)
 // 16-column steps: tcgen05.ld -> (mask tile loaded row-contiguously through the
 // slot) -> epilogue -> swizzled staging -> one elected lane issues the TMA
 // store(s).  Global traffic is full-row, and stores retire asynchronously.
-template <int BN>
+// BITS: the ReLU mask comes as packed bits (Epilogue::mask_bits), compiled as its own
+// copy so the fp16-mask prefetch registers and the bit words are never live together.
+template <int BN, bool BITS>
 CV_DEV void tile_epilogue_tma(const TcArgs& a, const TcMaps& maps, const EpiRt& rt, uint32_t tacc, int m_base, int n0,
                               int split, float inv, int q, int half, int lane, uint8_t* stg, uint8_t* hstg,
                               float& amax) {
@@ -409,6 +411,21 @@ CV_DEV void tile_epilogue_tma(const TcArgs& a, const TcMaps& maps, const EpiRt& 
   const bool head = use_mask && e.head_part != nullptr;
   const bool head10 = head && e.head_c == 10 && !(((uintptr_t)e.head_w | (uintptr_t)e.head_v) & 15);
   const bool store = !(head && e.head_only);
+  // packed ReLU bits: the lane's words for all sub-tiles of its half in one go
+  const bool use_bits = BITS;
+  // up to 8 16-bit words (one per sub-tile) as a 128-bit shift register in 4 registers
+  uint64_t wq0 = 0, wq1 = 0;
+  if (use_bits) {
+#pragma unroll
+    for (int i = 0; i < (NSUB >= 2 ? NSUB / 2 : 1) && i < 8; ++i) {
+      const int nb = n0 + (sb + i) * 16;
+      const uint64_t wd =
+          (m < a.M && nb < a.N && sb + i < se) ? (uint64_t)e.mask_bits[(int64_t)m * e.mbits_ld + nb / 16] : 0ull;
+      if (i < 4) wq0 |= wd << (16 * i);
+      else wq1 |= wd << (16 * (i - 4));
+    }
+  }
+  const bool use_hi = use_mask && !use_bits;
   const uint32_t hs = smem_u32(hstg);
   float4 hf[3];
   if (head10) head_fetch10(e, n0 + sb * 16, a.N, lane, hf);
@@ -431,12 +448,12 @@ CV_DEV void tile_epilogue_tma(const TcArgs& a, const TcMaps& maps, const EpiRt& 
   float hacc[16];
 #pragma unroll
   for (int k = 0; k < 16; ++k) hacc[k] = 0.f;
-  if (use_mask) load_mask(n0 + sb * 16, mcur, lcur);
+  if (use_hi) load_mask(n0 + sb * 16, mcur, lcur);
 #pragma unroll 1
   for (int sbk = sb; sbk < se; ++sbk) {
     const int nb = n0 + sbk * 16;
     if (nb >= a.N) break;
-    if (use_mask && sbk + 1 < se) load_mask(nb + 16, mnext, lnext);
+    if (use_hi && sbk + 1 < se) load_mask(nb + 16, mnext, lnext);
     uint32_t r[16];
     tmem_ld16(trow + sbk * 16, r);
     float v[16];
@@ -445,7 +462,13 @@ CV_DEV void tile_epilogue_tma(const TcArgs& a, const TcMaps& maps, const EpiRt& 
     if (a.tma_out == 1) {
       // ---- split fp16 output (activations / tangents / cotangents) ----
       float o[16];
-      if (use_mask) {
+      if (use_bits) {
+        const uint32_t wd = (uint32_t)(wq0 & 0xFFFFu);
+        wq0 = (wq0 >> 16) | (wq1 << 48);
+        wq1 >>= 16;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) o[j] = ((wd >> j) & 1u) ? v[j] : 0.f;
+      } else if (use_mask) {
         H8 mk[2], ml[2];
 #pragma unroll
         for (int ch = 0; ch < 2; ++ch) {
@@ -488,6 +511,16 @@ CV_DEV void tile_epilogue_tma(const TcArgs& a, const TcMaps& maps, const EpiRt& 
       for (int j = 0; j < 8; ++j) {
         split16(o[j], rt.out_s, h0.h[j], l0.h[j]);
         split16(o[8 + j], rt.out_s, h1.h[j], l1.h[j]);
+      }
+      if (e.bits_out && m < a.M) {
+        // packed ReLU sign bits of the stored hi plane (what the hi-mask consumers test)
+        uint32_t wd = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          wd |= (__half2float(h0.h[j]) > 0.f ? 1u : 0u) << j;
+          wd |= (__half2float(h1.h[j]) > 0.f ? 1u : 0u) << (8 + j);
+        }
+        e.bits_out[(int64_t)m * e.bits_out_ld + nb / 16] = (uint16_t)wd;
       }
       // the slot must be free: the previous sub-tile's TMA store has read it (waited
       // only now, so that read overlaps this sub-tile's TMEM load and math)
@@ -540,6 +573,7 @@ template <int BN>
 CV_DEV void epi_prefetch_mask(const TcArgs& a, int m_base, int n0, int q, int half, int lane) {
   const Epilogue& e = a.epi;
   if (!(a.tma_out == 1 && (e.mode == EPI_SPLIT_MASK || e.mode == EPI_HVP))) return;
+  if (e.mask_bits && e.act == CV_ACT_RELU && !e.head_part && e.mask_div == 1) return;  // packed bits: no row stream
   const int m = m_base + q * 32 + lane;
   const int c0 = n0 + half * (BN / 2);
   int cols = a.N - c0 < BN / 2 ? a.N - c0 : BN / 2;
@@ -558,7 +592,11 @@ CV_DEV void tile_epilogue(const TcArgs& a, const TcMaps& maps, const EpiRt& rt, 
                           int split, float inv, int q, int half, int lane, uint8_t* stg, uint8_t* hstg) {
   if (a.tma_out && !a.dbg) {
     float amax = 0.f, ramax = 0.f;
-    tile_epilogue_tma<BN>(a, maps, rt, tacc, m_base, n0, split, inv, q, half, lane, stg, hstg, amax);
+    const Epilogue& e = a.epi;
+    const bool bits = a.tma_out == 1 && (e.mode == EPI_SPLIT_MASK || e.mode == EPI_HVP) && e.act == CV_ACT_RELU &&
+                      !e.head_part && e.mask_bits != nullptr && e.mask_div == 1;
+    if (bits) tile_epilogue_tma<BN, true>(a, maps, rt, tacc, m_base, n0, split, inv, q, half, lane, stg, hstg, amax);
+    else tile_epilogue_tma<BN, false>(a, maps, rt, tacc, m_base, n0, split, inv, q, half, lane, stg, hstg, amax);
     if (!a.partial) epi_flush_amax(a.epi, amax, ramax);
     return;
   }
@@ -925,6 +963,20 @@ static CUtensorMap make_out_map(const void* ptr, int fp16, int64_t cols, int64_t
   return m;
 }
 
+// The TMA-store epilogue a GEMM's output allows without split-K partials:
+// 0 none (per-thread stores), 1 fp16 split pair, 2 fp32 (mirrors setup_out).
+static int tma_out_mode(const GemmArgs& g) {
+  static const int off = getenv("CURVOPT_TC_TMA_OUT") && getenv("CURVOPT_TC_TMA_OUT")[0] == '0';
+  if (off || g.lower_only) return 0;
+  const Epilogue& e = g.epi;
+  if (e.mode == EPI_STORE) return ((e.ld & 3) || !aligned16(e.out)) ? 0 : 2;
+  const bool relu_mask = (e.mode == EPI_SPLIT_MASK || e.mode == EPI_HVP) && e.act == CV_ACT_RELU && !e.raw &&
+                         e.mask_div == 1 && (e.mask_ld & 7) == 0 && aligned16(e.mask_hi);
+  if (!(e.mode == EPI_SPLIT_ACT || relu_mask)) return 0;
+  if ((e.ld & 7) || !aligned16(e.out_hi) || !aligned16(e.out_lo)) return 0;
+  return 1;
+}
+
 // Choose the TMA-store epilogue when the mode and layout allow it.
 static void setup_out(const GemmArgs& g, TcMaps& maps, TcArgs& a, float* partial, int splits) {
   static const int off = getenv("CURVOPT_TC_TMA_OUT") && getenv("CURVOPT_TC_TMA_OUT")[0] == '0';
@@ -1193,6 +1245,13 @@ int gemm_tc_head_groups(const cv_ctx* ctx, const GemmArgs& g) {
   if (p.kind == 0 || p.splits > 1) return 0;
   const int bn = (p.kind == 3 || p.kind == 4) ? 128 : 256;
   return 2 * ((g.N + bn - 1) / bn);
+}
+
+bool gemm_tc_tma_split(const cv_ctx* ctx, const GemmArgs& g) {
+  if (ctx->engine == CV_ENGINE_SIMT || !gemm_tc_supported(g) || tma_out_mode(g) != 1) return false;
+  const int sms = g.max_ctas > 0 && g.max_ctas < ctx->sm_count ? g.max_ctas : ctx->sm_count;
+  const TcPlan p = tc_plan(g, sms);
+  return p.kind != 0 && p.splits == 1;
 }
 
 void gemm_tc(cv_ctx* ctx, const GemmArgs& g) {

@@ -89,6 +89,12 @@ struct Epilogue {
   float* head_part = nullptr;      // [groups][M][hc]
   int head_c = 0;
   int head_only = 0;               // skip the split tangent store (GGN: the head is its only consumer)
+  // ReLU mask as packed bits (SplitBuf::bits): consumers read 2 bytes per 16 columns
+  // instead of the 32-byte fp16 row; producers (EPI_SPLIT_ACT) write them
+  const uint16_t* mask_bits = nullptr;
+  int64_t mbits_ld = 0;
+  uint16_t* bits_out = nullptr;
+  int64_t bits_out_ld = 0;
 };
 
 struct GemmArgs {
@@ -107,6 +113,10 @@ struct SplitBuf {
   __half* lo = nullptr;
   int64_t ld = 0;
   Scale* sc = nullptr;
+  // ReLU activations: packed sign bits (bit k of word j of row m = hi[m, 16 j + k] > 0),
+  // written by the forward epilogue; nullptr when not available (consumers read hi)
+  uint16_t* bits = nullptr;
+  int64_t bits_ld = 0;  // words per row (multiple of 8)
 };
 
 // Caching device allocator: exact-size free lists, never returns memory to the
@@ -174,6 +184,8 @@ struct cv_snap {
   __half* w_lo = nullptr;
   // augmented activations: acts[0] = [X | 1], acts[l] = [a_l | 1]; b x ld(n_l)
   std::vector<cv::SplitBuf> acts;
+  std::vector<uint16_t*> bits_buf;  // [L] packed ReLU bits of acts[l] (l >= 1), see SplitBuf::bits
+  int64_t bits_ld_max = 0;
   // loss state
   float* logits = nullptr;        // b x c
   float* probs = nullptr;         // b x c (ce)
@@ -242,6 +254,7 @@ cudaStream_t side2_fork(cv_ctx* ctx); // third stream, same ordering; joined by 
 void side_join(cv_ctx* ctx);          // context stream waits for the side streams
 int gemm_tc_partial(cv_ctx* ctx, const GemmArgs& g, float** partial);  // N <= 32, raw split-K partials
 int gemm_tc_head_groups(const cv_ctx* ctx, const GemmArgs& g);          // 0: no fused output-layer head
+bool gemm_tc_tma_split(const cv_ctx* ctx, const GemmArgs& g);           // runs the TMA split epilogue (bits producer)
 
 // runtime.cu
 void allreduce_f32(cv_ctx* ctx, float* buf, int64_t n);

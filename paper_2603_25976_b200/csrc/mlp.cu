@@ -236,6 +236,8 @@ static void mask_epi(Epilogue& e, const SplitBuf& a) {
   e.mask_lo = a.lo;
   e.mask_ld = a.ld;
   e.mask_sc = a.sc;
+  e.mask_bits = a.bits;
+  e.mbits_ld = a.bits_ld;
 }
 
 // last-layer block of a split flat vector -> transposed padded split (tc_out)
@@ -265,8 +267,10 @@ static const Scale* cot_split(cv_ctx* ctx, cv_snap* s, const float* U, Scale* us
   return usc;
 }
 
-void mlp_forward_layer(cv_ctx* ctx, cv_snap* s, int l, const SplitBuf& in, const __half* whi, const __half* wlo,
-                       const Scale* wsc, const SplitBuf& out) {
+// bits: packed ReLU sign-bit buffer of `out` (linearization only); returns whether the
+// GEMM's epilogue wrote it
+bool mlp_forward_layer(cv_ctx* ctx, cv_snap* s, int l, const SplitBuf& in, const __half* whi, const __half* wlo,
+                       const Scale* wsc, const SplitBuf& out, uint16_t* bits = nullptr) {
   GemmArgs g;
   g.M = s->bl;
   g.N = s->dims[l + 1];
@@ -277,9 +281,17 @@ void mlp_forward_layer(cv_ctx* ctx, cv_snap* s, int l, const SplitBuf& in, const
   split_epi(g.epi, out);
   g.epi.out_unit = 1;
   bound_add(g.epi.bound, (float)(s->dims[l] + 1), in.sc, wsc + l);
+  bool wrote = false;
+  static const int bits_on = !(getenv("CURVOPT_MASK_BITS") && getenv("CURVOPT_MASK_BITS")[0] == '0');
+  if (bits && bits_on && s->act == CV_ACT_RELU && gemm_tc_tma_split(ctx, g)) {
+    g.epi.bits_out = bits;
+    g.epi.bits_out_ld = ((s->dims[l + 1] + 15) / 16 + 7) / 8 * 8;
+    wrote = true;
+  }
   gemm(ctx, g);
   // the ones column of the next layer's augmented input (covered by the scale)
   set_col_value(ctx, out, s->bl, s->dims[l + 1], 1.f);
+  return wrote;
 }
 
 // logits = A_{L-1} [W; b]  (skinny)
@@ -502,7 +514,12 @@ static void skinny_weight_grad(cv_ctx* ctx, cv_snap* s, const float* U, Scale* u
 void mlp_linearize(cv_ctx* ctx, cv_snap* s, double* loss_out, float* grad_out) {
   const int L = s->L;
   for (int l = 0; l < L - 1; ++l)
-    mlp_forward_layer(ctx, s, l, s->acts[l], s->w_hi, s->w_lo, s->w_sc, s->acts[l + 1]);
+  {
+    SplitBuf& o = s->acts[l + 1];
+    const bool wrote = mlp_forward_layer(ctx, s, l, s->acts[l], s->w_hi, s->w_lo, s->w_sc, o, s->bits_buf[l + 1]);
+    o.bits = wrote ? s->bits_buf[l + 1] : nullptr;
+    o.bits_ld = wrote ? ((s->dims[l + 1] + 15) / 16 + 7) / 8 * 8 : 0;
+  }
   mlp_output_layer(ctx, s, s->acts[L - 1], s->w_hi, s->w_lo, s->w_sc, s->logits);
   mlp_loss(ctx, s, s->logits, 1, loss_out);
   // primal backward: G[l-1] = (G[l] W_l^T) * sp[l-1]   (models.py:378-381), with the

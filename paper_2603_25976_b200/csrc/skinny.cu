@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(256, 2) k_dx_wide(SkinnyDxArgs a, int rows_per
   const int r_begin = blockIdx.x * rows_per_block;
   const int r_end = min(a.rows, r_begin + rows_per_block);
   // the block's mask rows are one contiguous range: pull it toward L2 in bulk first
-  if (threadIdx.x < 8 && r_end > r_begin) {
+  if (threadIdx.x < 8 && r_end > r_begin && !e.mask_bits) {
     const char* mb = reinterpret_cast<const char*>(e.mask_hi + (int64_t)r_begin * e.mask_ld);
     const int64_t bytes = ((int64_t)(r_end - r_begin) * e.mask_ld * 2) & ~(int64_t)15;
     const int64_t chunk = ((bytes / 8) + 15) & ~(int64_t)15;
@@ -296,12 +296,17 @@ __global__ void __launch_bounds__(256, 2) k_dx_wide(SkinnyDxArgs a, int rows_per
     if (len > 0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(mb + o), "r"((unsigned)len) : "memory");
   }
   // mask loads of a batch of DXW_R rows (double buffered: batch b+1 is in flight while b is computed)
+  // (packed ReLU bits when the forward wrote them: 2 bytes per 16 columns instead of 32)
+  const bool bits = e.mask_bits != nullptr;
   auto load_batch = [&](int r0, uint2 (&mk)[DXW_R]) {
 #pragma unroll
     for (int i = 0; i < DXW_R; ++i) {
       const int m = r0 + i * rpp;
       mk[i] = make_uint2(0, 0);
-      if (rl < rpp && m < r_end) mk[i] = __ldg(reinterpret_cast<const uint2*>(e.mask_hi + (int64_t)m * e.mask_ld + col));
+      if (rl < rpp && m < r_end) {
+        if (bits) mk[i].x = (uint32_t)__ldg(e.mask_bits + (int64_t)m * e.mbits_ld + (col >> 4));  // shifted at use
+        else mk[i] = __ldg(reinterpret_cast<const uint2*>(e.mask_hi + (int64_t)m * e.mask_ld + col));
+      }
     }
   };
   uint2 mcur[DXW_R], mnext[DXW_R];
@@ -334,7 +339,8 @@ __global__ void __launch_bounds__(256, 2) k_dx_wide(SkinnyDxArgs a, int rows_per
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const float v = vv[q];
-        const float x = __half2float(hm.h[q]) > 0.f ? v : 0.f;
+        const bool on = bits ? ((mcur[i].x >> ((col & 15) + q)) & 1u) != 0u : __half2float(hm.h[q]) > 0.f;
+        const float x = on ? v : 0.f;
         amax = fmaxf(amax, fabsf(x));
         split16(x, rt.out_s, oh.h[q], ol.h[q]);
       }
@@ -369,10 +375,13 @@ static void launch_dx(cv_ctx* ctx, const SkinnyDxArgs& a) {
 
 void skinny_dx(cv_ctx* ctx, const SkinnyDxArgs& a) {
   if (dx_wide_ok(a)) {
+    static const int dx_bits = !(getenv("CURVOPT_DX_BITS") && getenv("CURVOPT_DX_BITS")[0] == '0');
+    SkinnyDxArgs b = a;
+    if (!dx_bits) b.epi.mask_bits = nullptr;
     // contiguous row ranges, 2 resident 256-thread blocks per SM
     const int blocks = 2 * ctx->sm_count;
     const int rpb = (a.rows + blocks - 1) / blocks;
-    launch_k(ctx->stream, k_dx_wide, (a.rows + rpb - 1) / rpb, 256, sizeof(float) * (size_t)rpb * a.c, a, rpb);
+    launch_k(ctx->stream, k_dx_wide, (a.rows + rpb - 1) / rpb, 256, sizeof(float) * (size_t)rpb * a.c, b, rpb);
     ctx->launches++;
     return;
   }
