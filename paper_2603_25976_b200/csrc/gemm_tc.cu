@@ -25,6 +25,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <mutex>
 #include <stdexcept>
@@ -1269,6 +1270,121 @@ void gemm_tc(cv_ctx* ctx, const GemmArgs& g) {
     case 2: launch_tc<256, 2>(ctx, g, p.splits); break;
     default: launch_tc<128, 3>(ctx, g, p.splits); break;
   }
+}
+
+// Two independent GEMMs in one persistent 2-CTA launch (k_gemm_tc2x2): the work items
+// of both (a: whole tiles; b: split-K items of about a's k-depth) are assigned to the
+// clusters longest-first, each to the least loaded cluster, so neither GEMM's last wave
+// leaves SMs idle and no static SM split is needed.  Returns false when either GEMM
+// does not run on the 256x256 2-CTA tiles.
+bool gemm_tc_pair_fused(cv_ctx* ctx, const GemmArgs& ga, const GemmArgs& gb) {
+  // opt-in (CURVOPT_PAIR_FUSED=1): measured at C3 it ties or trails the SM-split co-schedule,
+  // because the persistent pair holds every SM and the output layer's weight gradient can
+  // no longer run beside it
+  static const int off = !(getenv("CURVOPT_PAIR_FUSED") && getenv("CURVOPT_PAIR_FUSED")[0] == '1');
+  if (off || ctx->engine == CV_ENGINE_SIMT || !gemm_tc_supported(ga) || !gemm_tc_supported(gb)) return false;
+  if (ga.lower_only || gb.lower_only || ga.epi.head_part || gb.epi.head_part) return false;
+  const int sms = ctx->sm_count, C = sms / 2;
+  const TcPlan pa = tc_plan(ga, sms);
+  if (pa.kind != 1 || pa.splits != 1 || gb.M < 256 || gb.N < 256) return false;  // b: 2-CTA tiles, own split-K
+  using Cfg = Tc2Cfg<3, 256>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_gemm_tc2x2<3, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    attr_set = true;
+  }
+  TcMaps2 maps;
+  TcArgs2 args;
+  memset(&args, 0, sizeof(args));
+  const GemmArgs* gs[2] = {&ga, &gb};
+  float* part[2] = {nullptr, nullptr};
+  int kb_item_a = 0;
+  for (int i = 0; i < 2; ++i) {
+    const GemmArgs& g = *gs[i];
+    TcArgs& a = args.a[i];
+    fill_args(g, 128, maps.m[i], a);
+    int splits = 1;
+    if (i == 1 && g.epi.mode == EPI_STORE) {
+      // split-K items of about a's depth / bdiv (smaller items fill the last round),
+      // bounded by 4 k-blocks per item and 32 splits
+      static const int bdiv = getenv("CURVOPT_PAIR_BDIV") ? atoi(getenv("CURVOPT_PAIR_BDIV")) : 1;
+      const int target = std::max(4, kb_item_a / std::max(1, bdiv));
+      splits = (a.kb_total + target / 2) / target;
+      if (splits > a.kb_total / 4) splits = a.kb_total / 4;
+      if (splits > 32) splits = 32;
+      if (splits < 1) splits = 1;
+    }
+    a.kb_per_split = (a.kb_total + splits - 1) / splits;
+    splits = (a.kb_total + a.kb_per_split - 1) / a.kb_per_split;
+    a.splits = splits;
+    a.tiles_m = (g.M + 2 * TC_BM - 1) / (2 * TC_BM);
+    a.tiles_n = (g.N + 256 - 1) / 256;
+    if (i == 0) kb_item_a = a.kb_per_split;
+    if (splits > 1) {
+      part[i] = (float*)ctx->pool.get(sizeof(float) * (size_t)splits * g.M * g.N);
+      a.partial = part[i];
+    }
+    setup_out(g, maps.m[i], a, a.partial, splits);
+  }
+  // LPT schedule, cached by geometry
+  std::vector<int> key = {C};
+  for (int i = 0; i < 2; ++i) {
+    const TcArgs& a = args.a[i];
+    key.insert(key.end(), {a.M, a.N, a.kb[0], a.kb[1], a.kb_per_split, a.splits, a.tiles_m, a.tiles_n});
+  }
+  int* dsched = nullptr;
+  int ld = 0;
+  auto it = ctx->pair_sched.find(key);
+  if (it != ctx->pair_sched.end()) {
+    dsched = it->second.first;
+    ld = it->second.second;
+  } else {
+    struct It {
+      int cost, code;
+    };
+    std::vector<It> items;
+    for (int i = 0; i < 2; ++i) {
+      const TcArgs& a = args.a[i];
+      const int tiles = a.tiles_m * a.tiles_n, total = tiles * a.splits;
+      for (int w = 0; w < total; ++w) {
+        const int split = w / tiles;
+        const int kb0 = split * a.kb_per_split;
+        const int nkb = std::min(a.kb_total, kb0 + a.kb_per_split) - kb0;
+        items.push_back({nkb + 2, (i << 24) | w});  // + fill / epilogue
+      }
+    }
+    std::stable_sort(items.begin(), items.end(), [](const It& x, const It& y) { return x.cost > y.cost; });
+    std::vector<std::vector<int>> lists(C);
+    std::vector<long long> load(C, 0);
+    for (const It& x : items) {
+      int best = 0;
+      for (int c = 1; c < C; ++c)
+        if (load[c] < load[best]) best = c;
+      load[best] += x.cost;
+      lists[best].push_back(x.code);
+    }
+    size_t mx = 0;
+    for (auto& l : lists) mx = std::max(mx, l.size());
+    ld = (int)mx + 1;
+    std::vector<int> h((size_t)C * ld, -1);
+    for (int c = 0; c < C; ++c)
+      for (size_t j = 0; j < lists[c].size(); ++j) h[(size_t)c * ld + j] = lists[c][j];
+    dsched = (int*)ctx->pool.get(sizeof(int) * h.size());
+    cudaMemcpyAsync(dsched, h.data(), sizeof(int) * h.size(), cudaMemcpyHostToDevice, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);  // once per geometry: the host buffer dies here
+    ctx->pair_sched[key] = {dsched, ld};
+  }
+  launch_k(ctx->stream, k_gemm_tc2x2<3, 256>, 2 * C, 320, Cfg::SMEM, maps, args, (const int*)dsched, ld);
+  ctx->launches++;
+  for (int i = 0; i < 2; ++i) {
+    if (!part[i]) continue;
+    const GemmArgs& g = *gs[i];
+    launch_k(ctx->stream, k_splitk_reduce, 4 * ctx->sm_count, 256, 0, (const float*)part[i], args.a[i].splits, g.M,
+             g.N, g.epi, g.skip, g.lower_only);
+    ctx->launches++;
+    ctx->pool.put(part[i]);
+  }
+  return true;
 }
 
 // Narrow (N <= 32) GEMM returning raw split-K partials [splits][M][N]: the output

@@ -154,6 +154,7 @@ struct cv_ctx {
   cudaStream_t side2 = nullptr;  // third stream: the output layer's weight gradient beside the pair
   cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
   std::vector<void*> deferred2;  // side2 scratch, returned after side_join
+  std::map<std::vector<int>, std::pair<int*, int>> pair_sched;  // gemm_pair LPT schedules (device, row length)
 };
 
 struct cv_snap {
@@ -248,6 +249,7 @@ void gemm(cv_ctx* ctx, const GemmArgs& a);  // engine dispatch
 // the SMs split between them by estimated time; returns when both are enqueued
 // (the context stream waits for b)
 void gemm_pair(cv_ctx* ctx, GemmArgs a, GemmArgs b);
+bool gemm_tc_pair_fused(cv_ctx* ctx, const GemmArgs& a, const GemmArgs& b);  // one scheduled launch (false: not eligible)
 double gemm_tc_estimate(const cv_ctx* ctx, const GemmArgs& g, int ctas);  // relative time on `ctas` SMs
 cudaStream_t side_fork(cv_ctx* ctx);  // side stream ordered after the context stream's current work
 cudaStream_t side2_fork(cv_ctx* ctx); // third stream, same ordering; joined by side_join

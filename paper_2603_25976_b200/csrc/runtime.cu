@@ -187,6 +187,7 @@ void gemm_pair(cv_ctx* ctx, GemmArgs a, GemmArgs b) {
     gemm(ctx, b);
     return;
   }
+  if (gemm_tc_pair_fused(ctx, a, b)) return;
   ensure_side(ctx);
   // SM split minimising the slower of the two (even counts: CTA pairs)
   const int sms = ctx->sm_count;
