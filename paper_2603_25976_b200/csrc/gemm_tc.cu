@@ -1130,7 +1130,7 @@ static TcPlan tc_plan_kind(const GemmArgs& g, int sms, int kind) {
   // element-wise epilogue
   const bool splittable = !g.lower_only && (g.epi.mode == EPI_STORE || g.epi.mode == EPI_SPLIT_ACT ||
                                             g.epi.mode == EPI_SPLIT_MASK || g.epi.mode == EPI_HVP);
-  if (splittable && p.tiles < slots) {
+  if (splittable && p.tiles < slots && !g.unsplit) {
     // the split-K factor whose rounds of items fill the slots best (incl. the partials' round trip)
     double best = 1e300;
     int bs = 1;
@@ -1171,10 +1171,10 @@ static TcPlan tc_plan_search(const GemmArgs& g, int sms);
 // co-scheduling split search (gemm_pair) and every launch stay off the host's
 // critical path.
 struct PlanKey {
-  int M, N, K0, K1, nseg, mode, lower, sms;
+  int M, N, K0, K1, nseg, mode, lower, sms, unsplit;
   bool operator==(const PlanKey& o) const {
     return M == o.M && N == o.N && K0 == o.K0 && K1 == o.K1 && nseg == o.nseg && mode == o.mode &&
-           lower == o.lower && sms == o.sms;
+           lower == o.lower && sms == o.sms && unsplit == o.unsplit;
   }
 };
 struct PlanKeyHash {
@@ -1183,14 +1183,15 @@ struct PlanKeyHash {
     h = h * 1000003u ^ (size_t)k.K0;
     h = h * 1000003u ^ (size_t)k.K1;
     h = h * 1000003u ^ (size_t)(k.nseg * 64 + k.mode * 2 + k.lower);
-    return h * 1000003u ^ (size_t)k.sms;
+    return (h * 1000003u ^ (size_t)k.sms) * 2 + (size_t)k.unsplit;
   }
 };
 
 static TcPlan tc_plan(const GemmArgs& g, int sms) {
   static std::unordered_map<PlanKey, TcPlan, PlanKeyHash> cache;
   static std::mutex mu;
-  const PlanKey key{g.M, g.N, g.seg[0].K, g.nseg > 1 ? g.seg[1].K : 0, g.nseg, g.epi.mode, g.lower_only, sms};
+  const PlanKey key{g.M, g.N, g.seg[0].K, g.nseg > 1 ? g.seg[1].K : 0, g.nseg, g.epi.mode, g.lower_only, sms,
+                    g.unsplit};
   {
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find(key);

@@ -106,6 +106,7 @@ struct GemmArgs {
   int lower_only = 0;            // only tiles intersecting the lower triangle (m >= n)
   cudaStream_t stream = nullptr; // nullptr: the context stream
   int max_ctas = 0;              // > 0: cap on the persistent grid (SM share when co-scheduled)
+  int unsplit = 0;               // plan without split-K (the fused output head needs whole tiles)
 };
 
 struct SplitBuf {
