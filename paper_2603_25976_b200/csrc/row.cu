@@ -346,7 +346,18 @@ __global__ void k_trsv_fwd_update(const float* A, int64_t lda, int64_t m, int j0
   const int64_t row = j0 + nb + (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= m) return;
   double s = 0.0;
-  for (int k = lane; k < nb; k += 32) s += (double)A[row * lda + j0 + k] * y[j0 + k];
+  const float* Ar = A + row * lda + j0;
+  if ((nb & 127) == 0 && !(((uintptr_t)Ar) & 15)) {
+    // 128-bit loads, all of a lane's loads independent (nb / 128 in flight)
+#pragma unroll 4
+    for (int k = lane * 4; k < nb; k += 128) {
+      const float4 a = *reinterpret_cast<const float4*>(Ar + k);
+      s += (double)a.x * y[j0 + k] + (double)a.y * y[j0 + k + 1] + (double)a.z * y[j0 + k + 2] +
+           (double)a.w * y[j0 + k + 3];
+    }
+  } else {
+    for (int k = lane; k < nb; k += 32) s += (double)Ar[k] * y[j0 + k];
+  }
   s = warp_sum(s);
   if (lane == 0) r[row] -= s;
 }
@@ -358,8 +369,18 @@ __global__ void k_trsv_bwd_gather(const float* A, int64_t lda, int64_t m, int j0
   const int k = threadIdx.x;
   if (k >= nb) return;
   const int64_t r0 = j0 + nb + (int64_t)blockIdx.x * rows_per_block;
+  const int64_t r1 = r0 + rows_per_block < m ? r0 + rows_per_block : m;
+  // 8 independent accumulators: 8 row loads in flight per thread
+  double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  int64_t row = r0;
+  for (; row + 8 <= r1; row += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] += (double)A[(row + u) * lda + j0 + k] * v[row + u];
+  }
+  for (; row < r1; ++row) acc[0] += (double)A[row * lda + j0 + k] * v[row];
   double s = 0.0;
-  for (int64_t row = r0; row < r0 + rows_per_block && row < m; ++row) s += (double)A[row * lda + j0 + k] * v[row];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) s += acc[u];
   partial[blockIdx.x * nb + k] = s;
 }
 __global__ void k_trsv_bwd_diag(const float* dinv, int nb, int j0, const double* y, const double* partial,
@@ -379,6 +400,86 @@ __global__ void k_trsv_bwd_diag(const float* dinv, int nb, int j0, const double*
     v[j0 + t] = s;
   }
 }
+// Panel forms of the two substitutions (TS_NB = 512 columns = 8 diagonal 64-blocks per
+// launch): one CTA walks the panel's 64-blocks with their precomputed inverses (fp64
+// right-hand sides in shared memory), so a triangular solve is 2 x m/512 dependent
+// launches instead of 4 x m/64.
+constexpr int TS_NB = 512;
+
+// forward: y[j0 : j0+nbp] from r (the panel rows of r are consumed in smem)
+__global__ void __launch_bounds__(TS_NB) k_trsv_fwd_panel(const float* A, int64_t lda, const float* dinv, int j0,
+                                                          int nbp, const double* r, double* y) {
+  CV_PDL_ENTRY();
+  __shared__ double rb[TS_NB];
+  __shared__ double yb[CH_NB];
+  const int t = threadIdx.x;
+  if (t < nbp) rb[t] = r[j0 + t];
+  __syncthreads();
+  for (int s0 = 0; s0 < nbp; s0 += CH_NB) {
+    const int nb = nbp - s0 < CH_NB ? nbp - s0 : CH_NB;
+    const float* D = dinv + (int64_t)((j0 + s0) / CH_NB) * CH_NB * CH_NB;
+    if (t < nb) {
+      double acc = 0.0;
+      for (int k = 0; k <= t; ++k) acc += (double)D[t * nb + k] * rb[s0 + k];
+      yb[t] = acc;
+      y[j0 + s0 + t] = acc;
+    }
+    __syncthreads();
+    // later rows of the panel: rb[i] -= L[i, s0 : s0+nb] yb
+    const int i = s0 + nb + t;
+    if (i < nbp) {
+      const float* Li = A + (int64_t)(j0 + i) * lda + j0 + s0;
+      double acc = 0.0;
+      for (int k = 0; k < nb; ++k) acc += (double)Li[k] * yb[k];
+      rb[i] -= acc;
+    }
+    __syncthreads();
+  }
+}
+
+// backward: v[j0 : j0+nbp] from y and the gathered partials L[below, panel]^T v[below]
+__global__ void __launch_bounds__(TS_NB) k_trsv_bwd_panel(const float* A, int64_t lda, const float* dinv, int j0,
+                                                          int nbp, const double* y, const double* partial, int nparts,
+                                                          double* v) {
+  CV_PDL_ENTRY();
+  __shared__ double rb[TS_NB];
+  __shared__ double xb[TS_NB];
+  __shared__ double red[8][CH_NB];
+  const int t = threadIdx.x;
+  if (t < nbp) {
+    double acc = 0.0;
+    for (int p = 0; p < nparts; ++p) acc += partial[(int64_t)p * nbp + t];
+    rb[t] = y[j0 + t] - acc;
+  }
+  __syncthreads();
+  const int nsub = (nbp + CH_NB - 1) / CH_NB;
+  for (int sb = nsub - 1; sb >= 0; --sb) {
+    const int s0 = sb * CH_NB;
+    const int nb = nbp - s0 < CH_NB ? nbp - s0 : CH_NB;
+    // rb[s0 + k] -= sum over the panel's later rows i of L[i, s0 + k] x[i]  (8 row groups)
+    const int k = t & (CH_NB - 1), grp = t / CH_NB;
+    double acc = 0.0;
+    if (k < nb)
+      for (int i = s0 + nb + grp; i < nbp; i += 8) acc += (double)A[(int64_t)(j0 + i) * lda + j0 + s0 + k] * xb[i];
+    red[grp][k] = acc;
+    __syncthreads();
+    if (t < nb) {
+      double s = rb[s0 + t];
+      for (int g2 = 0; g2 < 8; ++g2) s -= red[g2][t];
+      rb[s0 + t] = s;
+    }
+    __syncthreads();
+    const float* D = dinv + (int64_t)((j0 + s0) / CH_NB) * CH_NB * CH_NB;
+    if (t < nb) {
+      double s = 0.0;
+      for (int kk = t; kk < nb; ++kk) s += (double)D[kk * nb + t] * rb[s0 + kk];  // Dinv^T
+      xb[s0 + t] = s;
+      v[j0 + s0 + t] = s;
+    }
+    __syncthreads();
+  }
+}
+
 // r = rhs - (G + mu I) v, one warp per row, fp64 accumulation (refinement residual)
 __global__ void k_row_residual(const float* G, int64_t m, float mu, const float* rhs, const double* v, double* r) {
   CV_PDL_ENTRY();
@@ -511,26 +612,29 @@ int row_solve_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, flo
   double* y = r + m;
   double* v = r + 2 * m;
   double* dv = r + 3 * m;
-  const int rpb = 256;
+  const int rpb = 64;
   const int nparts_max = (int)((m + rpb - 1) / rpb);
-  double* part = (double*)ctx->pool.get(sizeof(double) * (size_t)nparts_max * CH_NB);
+  double* part = (double*)ctx->pool.get(sizeof(double) * (size_t)nparts_max * TS_NB);
   auto tri_solve = [&](double* x) {  // r -> x = (L L^T)^-1 r   (r is consumed)
-    for (int bi = 0; bi < nblk; ++bi) {
-      const int j0 = bi * CH_NB;
-      const int nb = (int)((m - j0) < CH_NB ? (m - j0) : CH_NB);
-      launch_k(st, k_trsv_fwd_diag, 1, CH_NB, 0, s->dinv + (int64_t)bi * CH_NB * CH_NB, nb, j0, r, y);
-      const int64_t rest = m - j0 - nb;
-      if (rest > 0) launch_k(st, k_trsv_fwd_update, (int)((rest + 7) / 8), 256, 0, s->chol, m, m, j0, nb, y, r);
+    const int npan = (int)((m + TS_NB - 1) / TS_NB);
+    for (int pi = 0; pi < npan; ++pi) {
+      const int j0 = pi * TS_NB;
+      const int nbp = (int)((m - j0) < TS_NB ? (m - j0) : TS_NB);
+      launch_k(st, k_trsv_fwd_panel, 1, TS_NB, 0, (const float*)s->chol, m, (const float*)s->dinv, j0, nbp,
+               (const double*)r, y);
+      const int64_t rest = m - j0 - nbp;
+      if (rest > 0) launch_k(st, k_trsv_fwd_update, (int)((rest + 7) / 8), 256, 0, s->chol, m, m, j0, nbp, y, r);
     }
-    for (int bi = nblk - 1; bi >= 0; --bi) {
-      const int j0 = bi * CH_NB;
-      const int nb = (int)((m - j0) < CH_NB ? (m - j0) : CH_NB);
-      const int64_t rest = m - j0 - nb;
+    for (int pi = npan - 1; pi >= 0; --pi) {
+      const int j0 = pi * TS_NB;
+      const int nbp = (int)((m - j0) < TS_NB ? (m - j0) : TS_NB);
+      const int64_t rest = m - j0 - nbp;
       const int nparts = (int)((rest + rpb - 1) / rpb);
-      if (nparts > 0) launch_k(st, k_trsv_bwd_gather, nparts, CH_NB, 0, s->chol, m, m, j0, nb, x, part, rpb);
-      launch_k(st, k_trsv_bwd_diag, 1, CH_NB, 0, s->dinv + (int64_t)bi * CH_NB * CH_NB, nb, j0, y, part, nparts, x);
+      if (nparts > 0) launch_k(st, k_trsv_bwd_gather, nparts, TS_NB, 0, s->chol, m, m, j0, nbp, x, part, rpb);
+      launch_k(st, k_trsv_bwd_panel, 1, TS_NB, 0, (const float*)s->chol, m, (const float*)s->dinv, j0, nbp,
+               (const double*)y, (const double*)part, nparts, x);
     }
-    ctx->launches += 4 * nblk;
+    ctx->launches += 4 * npan;
   };
   launch_k(st, k_f2d, 256, 256, 0, rhs, r, m);
   tri_solve(v);
