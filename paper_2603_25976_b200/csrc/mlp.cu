@@ -472,6 +472,13 @@ static void skinny_weight_grad(cv_ctx* ctx, cv_snap* s, const float* U, Scale* u
                                const float* U2, Scale* u2sc, float* out, const int* skip, bool side = false) {
   const int l = s->L - 1;
   if (s->tc_out) {
+    static const int cosched = !(getenv("CURVOPT_COSCHED") && getenv("CURVOPT_COSCHED")[0] == '0');
+    static const int side_ctas = getenv("CURVOPT_DWL_CTAS") ? atoi(getenv("CURVOPT_DWL_CTAS")) : 48;
+    // beside the output-layer backward: the cotangent split and the GEMM both go to the
+    // second side stream (the caller joins it); not with tc_dx, whose backward reuses U's split
+    const bool on_side = side && cosched && side_ctas > 0 && ctx->engine != CV_ENGINE_SIMT && !s->tc_dx;
+    cudaStream_t main_stream = ctx->stream;
+    if (on_side) ctx->stream = side2_fork(ctx);
     const __half *uh, *ul, *u2h = nullptr, *u2l = nullptr;
     const Scale* uc = cot_split(ctx, s, U, usc, &uh, &ul, skip);
     const Scale* u2c = nullptr;
@@ -486,14 +493,12 @@ static void skinny_weight_grad(cv_ctx* ctx, cv_snap* s, const float* U, Scale* u
     g.epi.out = out + s->off[l];
     g.epi.ld = s->c;
     g.skip = skip;
-    static const int cosched = !(getenv("CURVOPT_COSCHED") && getenv("CURVOPT_COSCHED")[0] == '0');
-    static const int side_ctas = getenv("CURVOPT_DWL_CTAS") ? atoi(getenv("CURVOPT_DWL_CTAS")) : 48;
-    if (side && cosched && side_ctas > 0 && ctx->engine != CV_ENGINE_SIMT && gemm_tc_supported(g)) {
-      // beside the output-layer backward (the caller joins the side stream)
-      g.stream = side2_fork(ctx);
+    if (on_side && gemm_tc_supported(g)) {
+      g.stream = ctx->stream;
       g.max_ctas = side_ctas;
     }
     gemm(ctx, g);
+    ctx->stream = main_stream;
     return;
   }
   SkinnyDwArgs a{};
