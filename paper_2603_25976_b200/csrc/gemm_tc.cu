@@ -410,7 +410,9 @@ CV_DEV void tile_epilogue_tma(const TcArgs& a, const TcMaps& maps, const EpiRt& 
   const bool use_mask = a.tma_out == 1 && (e.mode == EPI_SPLIT_MASK || e.mode == EPI_HVP);
   const bool relu_act = e.act == CV_ACT_RELU;
   const bool head = use_mask && e.head_part != nullptr;
-  const bool head10 = head && e.head_c == 10 && !(((uintptr_t)e.head_w | (uintptr_t)e.head_v) & 15);
+  // forward variant (EPI_SPLIT_ACT): logits partials sum_n act(z)(m, n) W[n, :]
+  const bool head_fwd = !use_mask && a.tma_out == 1 && e.mode == EPI_SPLIT_ACT && e.head_part != nullptr;
+  const bool head10 = (head || head_fwd) && e.head_c == 10 && !(((uintptr_t)e.head_w | (uintptr_t)e.head_v) & 15);
   const bool store = !(head && e.head_only);
   // packed ReLU bits: the lane's words for all sub-tiles of its half in one go
   const bool use_bits = BITS;
@@ -501,6 +503,20 @@ CV_DEV void tile_epilogue_tma(const TcArgs& a, const TcMaps& maps, const EpiRt& 
       } else {
 #pragma unroll
         for (int j = 0; j < 16; ++j) o[j] = relu_act ? relu_f(v[j]) : tanhf(v[j]);
+        if (head_fwd) {
+          float zero[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) zero[j] = 0.f;
+          if (head10) {
+            head_stage10(hs, lane, hf);
+            __syncwarp();
+            if (sbk + 1 < se) head_fetch10(e, nb + 16, a.N, lane, hf);
+            head_acc10(hs, zero, o, hacc);
+            __syncwarp();
+          } else {
+            head_acc_generic(e, nb, a.N, zero, o, hacc);
+          }
+        }
       }
       if (!store) continue;
       if (m < a.M)
@@ -557,7 +573,7 @@ CV_DEV void tile_epilogue_tma(const TcArgs& a, const TcMaps& maps, const EpiRt& 
       }
     }
   }
-  if (head && m < a.M) {
+  if ((head || head_fwd) && m < a.M) {
     // group = column half of this tile; fixed-order reduction in k_out_reduce
     const int grp = (n0 / BN) * 2 + half;
     float* dst = e.head_part + ((int64_t)grp * a.M + m) * e.head_c;
@@ -1239,9 +1255,10 @@ int gemm_tc_head_groups(const cv_ctx* ctx, const GemmArgs& g) {
   static const int tma_off = getenv("CURVOPT_TC_TMA_OUT") && getenv("CURVOPT_TC_TMA_OUT")[0] == '0';
   if (off || tma_off || ctx->engine == CV_ENGINE_SIMT || !gemm_tc_supported(g) || g.lower_only) return 0;
   const Epilogue& e = g.epi;
-  if (e.mode != EPI_SPLIT_MASK || e.act != CV_ACT_RELU || e.raw || e.mask_div != 1 || (e.mask_ld & 7) ||
-      !aligned16(e.mask_hi) || !aligned16(e.mask_lo) || (e.ld & 7) || !aligned16(e.out_hi) || !aligned16(e.out_lo))
-    return 0;
+  const bool jvp_head = e.mode == EPI_SPLIT_MASK && e.act == CV_ACT_RELU && !e.raw && e.mask_div == 1 &&
+                        !(e.mask_ld & 7) && aligned16(e.mask_hi) && aligned16(e.mask_lo);
+  const bool fwd_head = e.mode == EPI_SPLIT_ACT && !e.head_only;
+  if (!(jvp_head || fwd_head) || (e.ld & 7) || !aligned16(e.out_hi) || !aligned16(e.out_lo)) return 0;
   const int sms = g.max_ctas > 0 && g.max_ctas < ctx->sm_count ? g.max_ctas : ctx->sm_count;
   const TcPlan p = tc_plan(g, sms);
   if (p.kind == 0 || p.splits > 1) return 0;

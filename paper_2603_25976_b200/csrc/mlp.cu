@@ -269,8 +269,12 @@ static const Scale* cot_split(cv_ctx* ctx, cv_snap* s, const float* U, Scale* us
 
 // bits: packed ReLU sign-bit buffer of `out` (linearization only); returns whether the
 // GEMM's epilogue wrote it
+// head_groups: when non-null and this is the last hidden layer, the output layer's
+// logits are accumulated in the GEMM's epilogue (partials in s->head_part; the count is
+// returned, 0 when the GEMM cannot carry the head)
 bool mlp_forward_layer(cv_ctx* ctx, cv_snap* s, int l, const SplitBuf& in, const __half* whi, const __half* wlo,
-                       const Scale* wsc, const SplitBuf& out, uint16_t* bits = nullptr) {
+                       const Scale* wsc, const SplitBuf& out, uint16_t* bits = nullptr, int* head_groups = nullptr,
+                       const float* head_wf = nullptr) {
   GemmArgs g;
   g.M = s->bl;
   g.N = s->dims[l + 1];
@@ -281,6 +285,25 @@ bool mlp_forward_layer(cv_ctx* ctx, cv_snap* s, int l, const SplitBuf& in, const
   split_epi(g.epi, out);
   g.epi.out_unit = 1;
   bound_add(g.epi.bound, (float)(s->dims[l] + 1), in.sc, wsc + l);
+  if (head_groups) {
+    *head_groups = 0;
+    if (s->head_part && head_wf && l == s->L - 2) {
+      g.epi.head_w = head_wf;
+      g.epi.head_v = head_wf;  // unused by the forward head (zero activation tangent)
+      g.epi.head_c = s->c;
+      g.epi.head_part = s->head_part;
+      g.unsplit = 1;
+      const int gr = gemm_tc_head_groups(ctx, g);
+      if (gr > 0 && gr <= s->head_groups_max) {
+        *head_groups = gr;
+      } else {
+        g.epi.head_w = g.epi.head_v = nullptr;
+        g.epi.head_part = nullptr;
+        g.epi.head_c = 0;
+        g.unsplit = 0;
+      }
+    }
+  }
   bool wrote = false;
   static const int bits_on = !(getenv("CURVOPT_MASK_BITS") && getenv("CURVOPT_MASK_BITS")[0] == '0');
   if (bits && bits_on && s->act == CV_ACT_RELU && gemm_tc_tma_split(ctx, g)) {
@@ -518,14 +541,25 @@ static void skinny_weight_grad(cv_ctx* ctx, cv_snap* s, const float* U, Scale* u
 // Full linearization (models.py:337-396): acts, loss, probs, G, grad.
 void mlp_linearize(cv_ctx* ctx, cv_snap* s, double* loss_out, float* grad_out) {
   const int L = s->L;
+  int head_groups = 0;
+  static const int fwd_head = !(getenv("CURVOPT_FWD_HEAD") && getenv("CURVOPT_FWD_HEAD")[0] == '0');
   for (int l = 0; l < L - 1; ++l)
   {
     SplitBuf& o = s->acts[l + 1];
-    const bool wrote = mlp_forward_layer(ctx, s, l, s->acts[l], s->w_hi, s->w_lo, s->w_sc, o, s->bits_buf[l + 1]);
+    const bool wrote = mlp_forward_layer(ctx, s, l, s->acts[l], s->w_hi, s->w_lo, s->w_sc, o, s->bits_buf[l + 1],
+                                         fwd_head ? &head_groups : nullptr, s->wl_f32);
     o.bits = wrote ? s->bits_buf[l + 1] : nullptr;
     o.bits_ld = wrote ? ((s->dims[l + 1] + 15) / 16 + 7) / 8 * 8 : 0;
   }
-  mlp_output_layer(ctx, s, s->acts[L - 1], s->w_hi, s->w_lo, s->w_sc, s->logits);
+  if (head_groups > 0) {
+    // logits = sum of the head partials + the bias row, in fixed order (models.py:357)
+    const float* bias = s->wl_f32 + (int64_t)s->dims[L - 1] * s->c;
+    launch_k(ctx->stream, k_out_reduce<16>, (s->bl + 31) / 32, 128, 0, (const float*)s->head_part, head_groups, s->bl,
+             s->c, 0, s->loss, (const float*)s->probs, 1.f, s->logits, (float*)nullptr, (const int*)nullptr, bias);
+    ctx->launches++;
+  } else {
+    mlp_output_layer(ctx, s, s->acts[L - 1], s->w_hi, s->w_lo, s->w_sc, s->logits);
+  }
   mlp_loss(ctx, s, s->logits, 1, loss_out);
   // primal backward: G[l-1] = (G[l] W_l^T) * sp[l-1]   (models.py:378-381), with the
   // weight gradient of layer l co-scheduled beside the backward GEMM of layer l
@@ -833,15 +867,28 @@ void mlp_loss(cv_ctx* ctx, cv_snap* s, const float* logits, int write_state, dou
 // Loss at another parameter point on the snapshot batch (curvature.py:82-84).
 void mlp_loss_at(cv_ctx* ctx, cv_snap* s, const float* w, double* loss_out) {
   // split w into the product scratch (v_hi / v_lo) and run a forward pass on the
-  // backward scratch buffers (gs[]) -- no product is in flight concurrently.
+  // backward scratch buffers (gs[]) -- no product is in flight concurrently.  The
+  // logits take the same path as the linearization's (fused head or output GEMM), so
+  // loss_before and loss_after share their rounding and rho's difference stays exact.
   split_input(ctx, s, w, nullptr);
   const int L = s->L;
   const SplitBuf* in = &s->acts[0];
+  int head_groups = 0;
+  static const int fwd_head = !(getenv("CURVOPT_FWD_HEAD") && getenv("CURVOPT_FWD_HEAD")[0] == '0');
+  const float* wl = w + s->off[L - 1];
   for (int l = 0; l < L - 1; ++l) {
-    mlp_forward_layer(ctx, s, l, *in, s->v_hi, s->v_lo, s->v_sc, s->gs[l]);
+    mlp_forward_layer(ctx, s, l, *in, s->v_hi, s->v_lo, s->v_sc, s->gs[l], nullptr, fwd_head ? &head_groups : nullptr,
+                      wl);
     in = &s->gs[l];
   }
-  mlp_output_layer(ctx, s, *in, s->v_hi, s->v_lo, s->v_sc, s->U);
+  if (head_groups > 0) {
+    const float* bias = wl + (int64_t)s->dims[L - 1] * s->c;
+    launch_k(ctx->stream, k_out_reduce<16>, (s->bl + 31) / 32, 128, 0, (const float*)s->head_part, head_groups, s->bl,
+             s->c, 0, s->loss, (const float*)s->probs, 1.f, s->U, (float*)nullptr, (const int*)nullptr, bias);
+    ctx->launches++;
+  } else {
+    mlp_output_layer(ctx, s, *in, s->v_hi, s->v_lo, s->v_sc, s->U);
+  }
   mlp_loss(ctx, s, s->U, 0, loss_out);
 }
 
