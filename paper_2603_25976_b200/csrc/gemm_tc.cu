@@ -529,6 +529,14 @@ CV_DEV void tile_epilogue_tma(const TcArgs& a, const TcMaps& maps, const EpiRt& 
         split16(o[j], rt.out_s, h0.h[j], l0.h[j]);
         split16(o[8 + j], rt.out_s, h1.h[j], l1.h[j]);
       }
+      if (e.out_unit && nb + 16 >= a.N && m < a.M) {
+        // the ones column of the augmented activation [a | 1] (column N, past the TMA box)
+        __half oh, ol;
+        split16(1.f, rt.out_s, oh, ol);
+        e.out_hi[(int64_t)m * e.ld + a.N] = oh;
+        e.out_lo[(int64_t)m * e.ld + a.N] = ol;
+        amax = fmaxf(amax, 1.f);
+      }
       if (e.bits_out && m < a.M) {
         // packed ReLU sign bits of the stored hi plane (what the hi-mask consumers test)
         uint32_t wd = 0;

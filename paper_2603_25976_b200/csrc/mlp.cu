@@ -311,9 +311,10 @@ bool mlp_forward_layer(cv_ctx* ctx, cv_snap* s, int l, const SplitBuf& in, const
     g.epi.bits_out_ld = ((s->dims[l + 1] + 15) / 16 + 7) / 8 * 8;
     wrote = true;
   }
+  const bool tma_epi = gemm_tc_tma_split(ctx, g);  // that epilogue also writes the ones column
   gemm(ctx, g);
   // the ones column of the next layer's augmented input (covered by the scale)
-  set_col_value(ctx, out, s->bl, s->dims[l + 1], 1.f);
+  if (!tma_epi) set_col_value(ctx, out, s->bl, s->dims[l + 1], 1.f);
   return wrote;
 }
 
