@@ -203,7 +203,7 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     W = min(args.warmup, 1)
-    sps, times, gv = cpu_oracle_run(max_seconds=min(180.0, 20.0 * max(args.steps, 1)), max_steps=args.steps,
+    sps, times, gv = cpu_oracle_run(max_seconds=min(90.0, 20.0 * max(args.steps, 1)), max_steps=args.steps,
                                     warmup=W)
     sample = (f"{len(times)} full C3 planned steps (after {W} warm-up) of the numpy/OpenBLAS f64 oracle restating "
               f"curvopt Method.step; {cores_used()} BLAS threads")
@@ -351,8 +351,8 @@ def run_ours(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
