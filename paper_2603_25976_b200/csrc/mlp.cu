@@ -364,7 +364,8 @@ static void skinny_backward(cv_ctx* ctx, cv_snap* s, const float* U, Scale* usc,
     g.M = s->bl;
     g.N = s->dims[l];
     g.nseg = 1;
-    g.seg[0] = GemmSeg{mk_op(uh, ul, 1, s->ldb, uc), mk_op(s->wl_hi, s->wl_lo, s->ldw, 1, wsc + l), s->c};
+    // K = cp: the transposed, padded operands carry zero rows c..cp-1 (the tcgen05 K step is 16)
+    g.seg[0] = GemmSeg{mk_op(uh, ul, 1, s->ldb, uc), mk_op(s->wl_hi, s->wl_lo, s->ldw, 1, wsc + l), s->cp};
     g.epi.mode = EPI_SPLIT_MASK;
     g.epi.act = s->act;
     split_epi(g.epi, out);
@@ -792,9 +793,9 @@ void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* v, float* out, const int* ski
       g.N = s->dims[l];
       g.nseg = 2;
       g.seg[0] = GemmSeg{mk_op(s->U_hi, s->U_lo, 1, s->ldb, s->U_sc), mk_op(s->wl_hi, s->wl_lo, s->ldw, 1, s->w_sc + l),
-                         s->c};
+                         s->cp};
       g.seg[1] = GemmSeg{mk_op(s->gout_hi, s->gout_lo, 1, s->ldb, s->gout_sc),
-                         mk_op(s->vl_hi, s->vl_lo, s->ldw, 1, s->v_sc + l), s->c};
+                         mk_op(s->vl_hi, s->vl_lo, s->ldw, 1, s->v_sc + l), s->cp};
       hvp_epi(s, g.epi, l);
       bound_add(g.epi.bound, (float)s->c, s->U_sc, s->w_sc + l);
       bound_add(g.epi.bound, (float)s->c, s->gout_sc, s->v_sc + l);
