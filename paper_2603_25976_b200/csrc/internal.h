@@ -276,7 +276,7 @@ bool cg_pnext_amax(cv_ctx* ctx, const float* r, const float* pre, float lam, flo
                    int n_zero);
 void split_rows(cv_ctx* ctx, const float* src, int64_t lds, int rows, int cols, const SplitBuf& dst, int ones);
 void split_mat(cv_ctx* ctx, const float* src, int64_t lds, int rows, int cols, __half* hi, __half* lo, int64_t ldd,
-               int trans, Scale* sc, int amax_ready, const int* skip);
+               int trans, Scale* sc, int amax_ready, const int* skip, int pad_cols = 0);
 void set_col_value(cv_ctx* ctx, const SplitBuf& b, int rows, int col, float v);
 void gather_rows(cv_ctx* ctx, const SplitBuf& b, int rows, int cols, float* out);  // out = hi + lo
 

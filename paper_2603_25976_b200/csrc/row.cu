@@ -195,7 +195,8 @@ static void ensure_gram(cv_ctx* ctx, cv_snap* s) {
     D[k].sc = s->scratch_sc + k;
   }
   // D0 rows (i, a) = seeds[i, a, :]  (exact amax, two passes)
-  split_mat(ctx, s->seeds, c, (int)m, c, D[0].hi, D[0].lo, ldD, 0, D[0].sc, 0, nullptr);
+  // (zero columns c..15: the output layer's Gram term runs on the tensor engine with K = 16)
+  split_mat(ctx, s->seeds, c, (int)m, c, D[0].hi, D[0].lo, ldD, 0, D[0].sc, 0, nullptr, ldD >= 16 ? 16 : 0);
   int cur = 0;
   for (int l = L - 1; l >= 0; --l) {
     const int nout = s->dims[l + 1];
@@ -214,7 +215,7 @@ static void ensure_gram(cv_ctx* ctx, cv_snap* s) {
     h.M = (int)m;
     h.N = (int)m;
     h.nseg = 1;
-    h.seg[0] = GemmSeg{sop(D[cur], false), sop(D[cur], true), nout};
+    h.seg[0] = GemmSeg{sop(D[cur], false), sop(D[cur], true), (l == L - 1 && nout < 16 && ldD >= 16) ? 16 : nout};
     h.epi.mode = EPI_GRAM;
     h.epi.out = s->gram;
     h.epi.ld = m;

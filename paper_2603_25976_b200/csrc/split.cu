@@ -348,13 +348,13 @@ void split_rows(cv_ctx* ctx, const float* src, int64_t lds, int rows, int cols, 
 // src rows x cols -> (trans ? cols_pad x ldd : rows x ldd) split; amax_ready: sc->amax
 // already holds max|src| (accumulated by the producer)
 void split_mat(cv_ctx* ctx, const float* src, int64_t lds, int rows, int cols, __half* hi, __half* lo, int64_t ldd,
-               int trans, Scale* sc, int amax_ready, const int* skip) {
+               int trans, Scale* sc, int amax_ready, const int* skip, int pad_cols) {
   if (!amax_ready) {
     launch_k(ctx->stream, k_mat_amax, SP_NB, SP_NT, 0, src, lds, rows, cols, 0.f, part_of(ctx), counter_of(ctx), sc, skip);
     ctx->launches++;
   }
   const int orows = trans ? (int)((cols + 15) / 16 * 16) : rows;
-  const int ocols = trans ? rows : cols;
+  const int ocols = trans ? rows : (pad_cols > cols ? pad_cols : cols);  // zero columns up to pad_cols
   launch_k(ctx->stream, k_mat_split, grid_for((int64_t)orows * ocols), SP_NT, 0, src, lds, rows, cols, orows, ocols, trans, 0,
                                                                           sc, amax_ready, hi, lo, ldd, skip);
   ctx->launches++;
