@@ -16,6 +16,7 @@ Prints ONE JSON line (rank 0).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -250,6 +251,11 @@ def run_ours(args, rank, world):
     stream = torch.cuda.current_stream()
     gv_total = 0
     launches0 = rt.launches()
+    # no cyclic-GC pause inside the timed regions (a full collection of the interpreter's
+    # heap is tens of ms, which the step's single host sync would expose as GPU idle)
+    gc.collect()
+    gc.freeze()
+    gc.disable()
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     infos = []
@@ -293,6 +299,7 @@ def run_ours(args, rank, world):
     d2h = w.dim * 4 + 16 * 8 + 48
     e2e = {"value": args.steps / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 
+    gc.enable()
     # ---- roofline of the dominant unit: the GGN product (its GEMMs), timed live ----
     snap = P.make_snapshot("ggn_ce", model, w, dev_batches[0])
     v = torch.randn(w.dim, device=dev)

@@ -1,6 +1,8 @@
 """Per-phase device time of C3 planned steps: linearize (make_snapshot), solve, rest (CUDA events)."""
 import sys; sys.path.insert(0, ".")
 import numpy as np, torch
+import gc, os
+if os.environ.get("NO_GC"): gc.disable()
 import bench
 import paper_2603_25976_b200 as P
 import paper_2603_25976_b200.method as M
