@@ -138,9 +138,19 @@ void check_launch(cv_ctx* ctx) {
 // GEMM engine dispatch: tensor-core (tcgen05, 3xTF32) where the operand
 // geometry allows TMA, exact-fp32 SIMT otherwise.
 // ---------------------------------------------------------------------------
+// side-stream priority: CURVOPT_SIDE_PRIO = 0 (default, same as a default stream) or
+// "hi" (the device's greatest priority)
+static int side_priority() {
+  const char* e = getenv("CURVOPT_SIDE_PRIO");
+  if (!e || strcmp(e, "hi") != 0) return 0;
+  int least = 0, greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  return greatest;
+}
+
 static void ensure_side(cv_ctx* ctx) {
   if (ctx->side) return;
-  if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+  if (cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, side_priority()) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess)
     throw std::runtime_error("CUDA: cannot create the side stream");
@@ -155,7 +165,7 @@ cudaStream_t side_fork(cv_ctx* ctx) {
 
 cudaStream_t side2_fork(cv_ctx* ctx) {
   if (!ctx->side2) {
-    if (cudaStreamCreateWithFlags(&ctx->side2, cudaStreamNonBlocking) != cudaSuccess ||
+    if (cudaStreamCreateWithPriority(&ctx->side2, cudaStreamNonBlocking, side_priority()) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_fork2, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_join2, cudaEventDisableTiming) != cudaSuccess)
       throw std::runtime_error("CUDA: cannot create the second side stream");
