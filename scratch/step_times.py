@@ -10,7 +10,7 @@ w = P.init_params(model, P.Rng(0)).to_device(dev)
 hb = bench.make_batches(4, bench.GLOBAL_B, 0, 1)
 db = [P.Batch(torch.from_numpy(X).to(dev), torch.from_numpy(y).to(dev), "ce", global_size=bench.GLOBAL_B) for X, y in hb]
 st = meth.init(w, 0)
-for i in range(25):
+for i in range(int(sys.argv[1]) if len(sys.argv) > 1 else 25):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter(); e0.record()
