@@ -261,7 +261,7 @@ int cv_linearize(cv_ctx* ctx, int n_layers, const int* dims, int act, int loss, 
     }
     if (L >= 2 && c <= 16 && ctx->engine != CV_ENGINE_SIMT) {
       s->wl_f32 = alloc_f(s, (int64_t)(dims[L - 1] + 1) * c);
-      s->head_groups_max = 2 * ((dims[L - 1] + 127) / 128);
+      s->head_groups_max = 2 * ((dims[L - 1] + 63) / 64);  // narrowest head tile: 64 columns
       s->head_part = alloc_f(s, (int64_t)s->head_groups_max * b * c);
     }
   } catch (...) {

@@ -1129,7 +1129,7 @@ static int launch_tc(cv_ctx* ctx, const GemmArgs& g, int splits, float* ext_part
 
 // Tile configuration and split-K factor of a GEMM on `sms` SMs.
 struct TcPlan {
-  int kind;  // 0: <32,4>, 1: 2-CTA 256x256, 2: <256,2>, 3: <128,3>, 4: 2-CTA 256x128
+  int kind;  // 0: <32,4>, 1: 2-CTA 256x256, 2: <256,2>, 3: <128,3>, 4: 2-CTA 256x128, 5: <64,4>
   int tiles, kb_total, splits;
   int M, N;
 };
@@ -1139,7 +1139,7 @@ static double plan_time(const TcPlan& p, int sms);
 static TcPlan tc_plan_kind(const GemmArgs& g, int sms, int kind) {
   TcPlan p;
   p.kind = kind;
-  const int bn = kind == 0 ? 32 : ((kind == 3 || kind == 4) ? 128 : 256);
+  const int bn = kind == 0 ? 32 : (kind == 5 ? 64 : ((kind == 3 || kind == 4) ? 128 : 256));
   const int bm = (kind == 1 || kind == 4) ? 256 : TC_BM;
   p.tiles = ((g.M + bm - 1) / bm) * ((g.N + bn - 1) / bn);
   const int slots = (kind == 1 || kind == 4) ? sms / 2 : sms;  // concurrent work items
@@ -1181,8 +1181,8 @@ static double plan_time(const TcPlan& p, int sms) {
   const double item_kb = (double)((p.kb_total + p.splits - 1) / p.splits);
   // 2-stage ring / narrower tiles (measured on B200: the 2-CTA 256x128 tile streams at ~0.7x
   // the 256x256 rate, so it is only reachable by CURVOPT_TC_KIND=4)
-  const double pen = p.kind == 2 ? 1.3 : (p.kind == 3 ? 1.2 : (p.kind == 4 ? 1.4 : 1.0));
-  const double per_kb = (p.kind == 3 || p.kind == 4) ? 0.5 : 1.0;      // 128-wide tiles: half the MMA work
+  const double pen = p.kind == 2 ? 1.3 : (p.kind == 3 ? 1.2 : (p.kind == 4 ? 1.4 : (p.kind == 5 ? 1.6 : 1.0)));
+  const double per_kb = (p.kind == 3 || p.kind == 4) ? 0.5 : (p.kind == 5 ? 0.25 : 1.0);  // narrower tiles: less MMA work
   // split-K partials: written once and read once by the fixed-order reduce (units of
   // ~1.2 us, one 256x256x64 3xFP16 k-block on a CTA pair, at ~6.5 TB/s)
   const double red = p.splits > 1 ? (double)(p.splits + 1) * p.M * p.N * 4.0 / 7.8e6 + 2.0 : 0.0;
@@ -1233,7 +1233,7 @@ static TcPlan tc_plan_search(const GemmArgs& g, int sms) {
   static const int use_2sm = getenv("CURVOPT_TC_2SM") ? atoi(getenv("CURVOPT_TC_2SM")) : 1;
   static const int force_kind = getenv("CURVOPT_TC_KIND") ? atoi(getenv("CURVOPT_TC_KIND")) : -1;
   if (g.N <= 32) return tc_plan_kind(g, sms, 0);
-  if (force_kind >= 1 && force_kind <= 4) return tc_plan_kind(g, sms, force_kind);
+  if (force_kind >= 1 && force_kind <= 5) return tc_plan_kind(g, sms, force_kind);
   const bool pair = use_2sm && !force_bn && g.M >= 256 && g.N >= 256;
   const bool wide = force_bn ? force_bn == 256 : g.N >= 512;
   TcPlan best = tc_plan_kind(g, sms, pair ? 1 : (wide ? 2 : 3));
@@ -1241,7 +1241,7 @@ static TcPlan tc_plan_search(const GemmArgs& g, int sms) {
   if ((g.epi.mode == EPI_STORE || best.tiles < slots) && !force_bn) {
     // split-K weight gradients and under-filled grids: the tile shape that wastes the
     // least of the edges / fills the slots best
-    for (int k = 1; k <= 3; ++k) {
+    for (int k : {1, 2, 3, 5}) {  // (kind 5, 128x64: only for grids the wider tiles cannot fill)
       if (k == 1 && !pair) continue;
       const TcPlan c = tc_plan_kind(g, sms, k);
       if (plan_time(c, sms) < plan_time(best, sms)) best = c;
@@ -1270,7 +1270,7 @@ int gemm_tc_head_groups(const cv_ctx* ctx, const GemmArgs& g) {
   const int sms = g.max_ctas > 0 && g.max_ctas < ctx->sm_count ? g.max_ctas : ctx->sm_count;
   const TcPlan p = tc_plan(g, sms);
   if (p.kind == 0 || p.splits > 1) return 0;
-  const int bn = (p.kind == 3 || p.kind == 4) ? 128 : 256;
+  const int bn = p.kind == 5 ? 64 : ((p.kind == 3 || p.kind == 4) ? 128 : 256);
   return 2 * ((g.N + bn - 1) / bn);
 }
 
@@ -1294,6 +1294,7 @@ void gemm_tc(cv_ctx* ctx, const GemmArgs& g) {
     case 1: launch_tc2<3, 256>(ctx, g, p.splits); break;
     case 4: launch_tc2<4, 128>(ctx, g, p.splits); break;
     case 2: launch_tc<256, 2>(ctx, g, p.splits); break;
+    case 5: launch_tc<64, 4>(ctx, g, p.splits); break;
     default: launch_tc<128, 3>(ctx, g, p.splits); break;
   }
 }
