@@ -211,6 +211,8 @@ void gemm_pair(cv_ctx* ctx, GemmArgs a, GemmArgs b) {
       best = ca;
     }
   }
+  static const int force_split = getenv("CURVOPT_PAIR_SPLIT") ? atoi(getenv("CURVOPT_PAIR_SPLIT")) : 0;
+  if (force_split >= 16 && force_split <= sms - 16) best = force_split & ~1;  // experiments
   a.max_ctas = best;
   b.max_ctas = sms - best;
   a.stream = ctx->stream;
