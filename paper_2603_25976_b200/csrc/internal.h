@@ -264,6 +264,21 @@ void allreduce_f32(cv_ctx* ctx, float* buf, int64_t n);
 void allreduce_f64(cv_ctx* ctx, double* buf, int64_t n);
 void check_launch(cv_ctx* ctx);
 
+// per-layer offset table of a flat parameter-space vector (kernel argument)
+constexpr int kOffTabMax = 16;
+struct OffTab {
+  int64_t off[kOffTabMax + 1];
+  int L;
+};
+inline OffTab make_off_tab(const std::vector<int64_t>& off, int64_t d) {
+  OffTab t;
+  t.L = (int)off.size();
+  for (int l = 0; l < t.L; ++l) t.off[l] = off[l];
+  t.off[t.L] = d;
+  return t;
+}
+constexpr int kAmaxWsFloats = 4 * 148 * kOffTabMax;  // amax_ws block maxima; kOffTabMax floats follow
+
 // split.cu: scaled fp16 splits with exact amax (two passes)
 void amax_into(cv_ctx* ctx, const float* x, int64_t n, Scale* slot);  // slot->amax = max|x|
 void split_flat(cv_ctx* ctx, const float* x, int64_t d, const std::vector<int64_t>& off, __half* hi, __half* lo,
@@ -274,6 +289,12 @@ void split_flat_apply(cv_ctx* ctx, const float* x, int64_t d, const std::vector<
 bool cg_pnext_amax(cv_ctx* ctx, const float* r, const float* pre, float lam, float floor_, const double* beta,
                    const int* done, float* p, int64_t d, const std::vector<int64_t>& off, Scale* sc, Scale* zero_sc,
                    int n_zero);
+// the same direction update fused with the split of p into (hi, lo): the scale is taken
+// from the bound mr[l] + |beta| * sc[l].amax (mr: per-layer max|M^-1 r| of the update
+// kernel, sc[l].amax: the amax of the previous direction), then sc[l] = {e, amax(p)}
+void cg_pnext_split(cv_ctx* ctx, const float* r, const float* pre, float lam, float floor_, const double* beta,
+                    const int* done, float* p, int64_t d, const std::vector<int64_t>& off, const float* mr,
+                    Scale* sc, Scale* zero_sc, int n_zero, __half* hi, __half* lo);
 void split_rows(cv_ctx* ctx, const float* src, int64_t lds, int rows, int cols, const SplitBuf& dst, int ones);
 void split_mat(cv_ctx* ctx, const float* src, int64_t lds, int rows, int cols, __half* hi, __half* lo, int64_t ldd,
                int trans, Scale* sc, int amax_ready, const int* skip, int pad_cols = 0);

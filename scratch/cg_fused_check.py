@@ -1,4 +1,4 @@
-"""5 C3 planned steps; prints a hash of the final weights and the StepInfo rows (compare CURVOPT_CG_FUSED=0/1)."""
+"""5 C3 planned steps; prints a hash of the final weights and the StepInfo rows (compare CURVOPT_CG_SPLIT_FUSED=0/1)."""
 import sys, hashlib; sys.path.insert(0, ".")
 import numpy as np, torch
 import bench

@@ -2,7 +2,8 @@
 
 * The row lane's two-level Cholesky with tensor-core trailing updates (512-column panels)
   only engages for m = b*c > 512; here m = 2560 (5 panels).
-* Opt-in engine variants (the scheduled pair launch, the 2-CTA 256x128 tile) are read
+* Opt-in engine variants (the scheduled pair launch, the 2-CTA 256x128 tile, the CG
+  direction update with the fused split) are read
   from the environment once per process, so each runs in a subprocess against the oracle.
 """
 
@@ -94,3 +95,14 @@ def test_opt_in_engine_variants_vs_oracle(env):
     err = float([ln for ln in out.stdout.splitlines() if ln.startswith("ERR")][-1].split()[1])
     print(env, err)
     assert err < 1e-4
+
+
+def test_cg_split_fused_variant():
+    """CURVOPT_CG_SPLIT_FUSED=1 (direction update writes the next product's split with a
+    bound-derived exponent): the CG parity tests, stabilised and preconditioned cases
+    included, pass unchanged."""
+    out = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-q",
+                          "-m", "gpu", "-k", "cg_solve", "-p", "no:cacheprovider"],
+                         env={**os.environ, "CURVOPT_CG_SPLIT_FUSED": "1"}, capture_output=True, text=True,
+                         timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
