@@ -706,9 +706,7 @@ CV_DEV void load_slab(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, bool 
 // mainloop of item i+1.
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(320, 1) k_gemm_tc(const __grid_constant__ TcMaps maps, const TcArgs a) {
-  CV_PDL_ENTRY();
   using Cfg = TcCfg<BN, STAGES>;
-  if (skip_if(a.skip)) return;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* zero = smem + STAGES * Cfg::STAGE_BYTES;
@@ -745,9 +743,13 @@ __global__ void __launch_bounds__(320, 1) k_gemm_tc(const __grid_constant__ TcMa
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  const SegPlan plan = seg_plan(a);
+  // the setup above touches no data of earlier kernels: it overlaps the predecessor's tail
+  CV_PDL_ENTRY();
+  const bool skipped = skip_if(a.skip);
+  const SegPlan plan = skipped ? SegPlan{} : seg_plan(a);
 
-  if (warp == 0 && lane == 0) {
+  if (skipped) {
+  } else if (warp == 0 && lane == 0) {
     // ---------------- TMA producer ----------------
     int it = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x) {

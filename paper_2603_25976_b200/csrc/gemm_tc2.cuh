@@ -78,7 +78,6 @@ CV_DEV bool tc2_item(const TcArgs* args, const int* sched, int sched_ld, int clu
 template <int STAGES, int TC2_BN, int NG>
 CV_DEV void tc2_body(const TcMaps* maps, const TcArgs* args, const int* sched, int sched_ld) {
   using Cfg = Tc2Cfg<STAGES, TC2_BN>;
-  if (skip_if(args[0].skip)) return;  // identical for every GEMM of the launch and both CTAs
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* zero = smem + STAGES * Cfg::STAGE_BYTES;
@@ -118,11 +117,15 @@ CV_DEV void tc2_body(const TcMaps* maps, const TcArgs* args, const int* sched, i
   cluster_sync_all();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // the setup above touches no data of earlier kernels: it overlaps the predecessor's tail
+  CV_PDL_ENTRY();
+  const bool skipped = skip_if(args[0].skip);  // identical for every GEMM of the launch and both CTAs
   SegPlan plan[NG];
 #pragma unroll
-  for (int gg = 0; gg < NG; ++gg) plan[gg] = seg_plan(args[gg]);
+  for (int gg = 0; gg < NG; ++gg) plan[gg] = skipped ? SegPlan{} : seg_plan(args[gg]);
 
-  if (warp == 0 && lane == 0) {
+  if (skipped) {
+  } else if (warp == 0 && lane == 0) {
     // ---------------- TMA producer (both CTAs) ----------------
     int it = 0, g, w;
     for (int item = 0; tc2_item<NG>(args, sched, sched_ld, cluster, nclusters, item, g, w); ++item) {
@@ -227,7 +230,6 @@ CV_DEV void tc2_body(const TcMaps* maps, const TcArgs* args, const int* sched, i
 template <int STAGES, int TC2_BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     k_gemm_tc2(const __grid_constant__ TcMaps maps, const TcArgs a) {
-  CV_PDL_ENTRY();
   tc2_body<STAGES, TC2_BN, 1>(&maps, &a, nullptr, 0);
 }
 
@@ -244,7 +246,6 @@ template <int STAGES, int TC2_BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     k_gemm_tc2x2(const __grid_constant__ TcMaps2 maps, const __grid_constant__ TcArgs2 args, const int* sched,
                  int sched_ld) {
-  CV_PDL_ENTRY();
   tc2_body<STAGES, TC2_BN, 2>(maps.m, args.a, sched, sched_ld);
 }
 

@@ -264,8 +264,6 @@ CV_DEV float2 ffma2_dx(float2 a, float2 b, float2 c) {
   return d;
 }
 __global__ void __launch_bounds__(256, 2) k_dx_wide(SkinnyDxArgs a, int rows_per_block) {
-  CV_PDL_ENTRY();
-  if (skip_if(a.skip)) return;
   const int tpr = a.n >> 2;               // threads per row (<= 256)
   const int rpp = 256 / tpr;              // rows per pass
   const int rl = threadIdx.x / tpr, col = (threadIdx.x - rl * tpr) * 4;
@@ -280,6 +278,10 @@ __global__ void __launch_bounds__(256, 2) k_dx_wide(SkinnyDxArgs a, int rows_per
         w[j][q] = j < a.c ? join16(a.w_hi[0][base + j], a.w_lo[0][base + j], winv) : 0.f;
     }
   }
+  // the weights (and their scale) are the linearization's: loaded before the wait, so
+  // they overlap the predecessor's tail
+  CV_PDL_ENTRY();
+  if (skip_if(a.skip)) return;
   const Epilogue& e = a.epi;
   const EpiRt rt = epi_prepare(e);
   if (blockIdx.x == 0 && threadIdx.x == 0) epi_publish(e, rt);
