@@ -6,6 +6,8 @@
 //   skinny_rows : last-layer JVP + fused H_z (models.py:243-255, 199-204)
 //   skinny_dw   : last-layer [gW; gb] = A^T U (models.py:280-281)
 //   skinny_dx   : G = (U W^T) * act'(a) (models.py:282-284, 378-381)
+#include <type_traits>
+
 #include "common.cuh"
 #include "epilogue.cuh"
 #include "internal.h"
@@ -252,6 +254,7 @@ __global__ void __launch_bounds__(128) k_dx(SkinnyDxArgs a) {
 // output leaves as two 64-bit stores per row.
 constexpr int DXW_R = 8;
 constexpr int DXW_C = 10;
+// two resident 256-thread blocks per SM (a three-block bound spills: measured slower)
 
 // d = a * b + c on two fp32 lanes (sm_100 FFMA2)
 CV_DEV float2 ffma2_dx(float2 a, float2 b, float2 c) {
@@ -263,19 +266,31 @@ CV_DEV float2 ffma2_dx(float2 a, float2 b, float2 c) {
       : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
   return d;
 }
+// RPP: rows per pass (256 / (n / 4)) when known at compile time (n = 1024: 1), else 0.
+// Everything row-invariant (parameters, base pointers, the mask bit offset) is hoisted
+// out of the row loop, U rows are staged at a fixed stride of DXW_C (zero-padded) so a
+// row's coefficients are five 64-bit shared loads, and the split runs on half2 pairs
+// (same rounding as split16).
+template <int RPP, bool BITS>
 __global__ void __launch_bounds__(256, 2) k_dx_wide(SkinnyDxArgs a, int rows_per_block) {
-  const int tpr = a.n >> 2;               // threads per row (<= 256)
-  const int rpp = 256 / tpr;              // rows per pass
+  const int tpr = a.n >> 2;                     // threads per row (<= 256)
+  const int rpp = RPP > 0 ? RPP : 256 / tpr;    // rows per pass
   const int rl = threadIdx.x / tpr, col = (threadIdx.x - rl * tpr) * 4;
-  float w[DXW_C][4];
+  float2 w01[DXW_C], w23[DXW_C];
   {
     const float winv = pow2f(-a.w_sc[0]->e);
+    float w[4][DXW_C];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int64_t base = (int64_t)(col + q) * a.c;
 #pragma unroll
       for (int j = 0; j < DXW_C; ++j)
-        w[j][q] = j < a.c ? join16(a.w_hi[0][base + j], a.w_lo[0][base + j], winv) : 0.f;
+        w[q][j] = j < a.c ? join16(a.w_hi[0][base + j], a.w_lo[0][base + j], winv) : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < DXW_C; ++j) {
+      w01[j] = make_float2(w[0][j], w[1][j]);
+      w23[j] = make_float2(w[2][j], w[3][j]);
     }
   }
   // the weights (and their scale) are the linearization's: loaded before the wait, so
@@ -288,8 +303,9 @@ __global__ void __launch_bounds__(256, 2) k_dx_wide(SkinnyDxArgs a, int rows_per
   float amax = 0.f;
   const int r_begin = blockIdx.x * rows_per_block;
   const int r_end = min(a.rows, r_begin + rows_per_block);
+  constexpr bool bits = BITS;
   // the block's mask rows are one contiguous range: pull it toward L2 in bulk first
-  if (threadIdx.x < 8 && r_end > r_begin && !e.mask_bits) {
+  if (threadIdx.x < 8 && r_end > r_begin && !bits) {
     const char* mb = reinterpret_cast<const char*>(e.mask_hi + (int64_t)r_begin * e.mask_ld);
     const int64_t bytes = ((int64_t)(r_end - r_begin) * e.mask_ld * 2) & ~(int64_t)15;
     const int64_t chunk = ((bytes / 8) + 15) & ~(int64_t)15;
@@ -297,58 +313,100 @@ __global__ void __launch_bounds__(256, 2) k_dx_wide(SkinnyDxArgs a, int rows_per
     const int64_t len = o >= bytes ? 0 : (bytes - o < chunk ? bytes - o : chunk);
     if (len > 0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(mb + o), "r"((unsigned)len) : "memory");
   }
+  // row-invariant addressing: 2-byte elements in both mask forms (packed-bit words, mask halves)
+  const int64_t mrow = 2 * (bits ? e.mbits_ld : e.mask_ld);
+  const char* mbase = bits ? reinterpret_cast<const char*>(e.mask_bits + (col >> 4))
+                           : reinterpret_cast<const char*>(e.mask_hi + col);
+  const int bsh = col & 15;
+  const int64_t ld = e.ld;
+  __half* const ohb = e.out_hi + col;
+  __half* const olb = e.out_lo + col;
+  const float out_s = rt.out_s;
   // mask loads of a batch of DXW_R rows (double buffered: batch b+1 is in flight while b is computed)
-  // (packed ReLU bits when the forward wrote them: 2 bytes per 16 columns instead of 32)
-  const bool bits = e.mask_bits != nullptr;
-  auto load_batch = [&](int r0, uint2 (&mk)[DXW_R]) {
+  using MaskT = typename std::conditional<BITS, uint32_t, uint2>::type;
+  auto load_batch = [&](int r0, MaskT (&mk)[DXW_R]) {
+    const char* p = mbase + (int64_t)r0 * mrow;
 #pragma unroll
     for (int i = 0; i < DXW_R; ++i) {
-      const int m = r0 + i * rpp;
-      mk[i] = make_uint2(0, 0);
-      if (rl < rpp && m < r_end) {
-        if (bits) mk[i].x = (uint32_t)__ldg(e.mask_bits + (int64_t)m * e.mbits_ld + (col >> 4));  // shifted at use
-        else mk[i] = __ldg(reinterpret_cast<const uint2*>(e.mask_hi + (int64_t)m * e.mask_ld + col));
+      mk[i] = MaskT{};
+      if (rl < rpp && r0 + i * rpp < r_end) {
+        const char* q = p + (int64_t)i * rpp * mrow;
+        if constexpr (BITS) mk[i] = __ldg(reinterpret_cast<const uint16_t*>(q));  // shifted at use
+        else mk[i] = __ldg(reinterpret_cast<const uint2*>(q));
       }
     }
   };
-  uint2 mcur[DXW_R], mnext[DXW_R];
+  MaskT mcur[DXW_R], mnext[DXW_R];
   load_batch(r_begin + rl, mcur);
-  // the block's U rows (contiguous) staged once: every later U read is a smem broadcast
+  // the block's U rows (contiguous) staged once at stride DXW_C: every later U read is a
+  // 64-bit smem broadcast
   extern __shared__ __align__(16) float Us[];
-  for (int i = threadIdx.x; i < (r_end - r_begin) * a.c; i += blockDim.x) Us[i] = a.U[0][(int64_t)r_begin * a.c + i];
+  {
+    const int nr = r_end - r_begin, c = a.c;
+    const float* Ug = a.U[0] + (int64_t)r_begin * c;
+    for (int i = threadIdx.x; i < nr * DXW_C; i += blockDim.x) {
+      const int rr = i / DXW_C, j = i - rr * DXW_C;
+      Us[i] = j < c ? Ug[rr * c + j] : 0.f;
+    }
+  }
   __syncthreads();
   if (rl >= rpp) return;
+  const int64_t ostep = (int64_t)rpp * ld;
   for (int r0 = r_begin + rl; r0 < r_end; r0 += rpp * DXW_R) {
     if (r0 + rpp * DXW_R < r_end) load_batch(r0 + rpp * DXW_R, mnext);
-#pragma unroll
-    for (int i = 0; i < DXW_R; ++i) {
-      const int m = r0 + i * rpp;
-      if (m >= r_end) break;
-      float u[DXW_C];
-#pragma unroll
-      for (int j = 0; j < DXW_C; ++j) u[j] = j < a.c ? Us[(m - r_begin) * a.c + j] : 0.f;
+    const float* ub = Us + (r0 - r_begin) * DXW_C;
+    __half* oh = ohb + (int64_t)r0 * ld;
+    __half* ol = olb + (int64_t)r0 * ld;
+    const int cnt = (r_end - r0 + rpp - 1) / rpp;
+    auto row = [&](int i) {
+      const float2* u2 = reinterpret_cast<const float2*>(ub + i * rpp * DXW_C);
       // column pairs on FFMA2
-      float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int j = 0; j < DXW_C; ++j) {
-        const float2 uu = make_float2(u[j], u[j]);
-        acc[0] = ffma2_dx(uu, make_float2(w[j][0], w[j][1]), acc[0]);
-        acc[1] = ffma2_dx(uu, make_float2(w[j][2], w[j][3]), acc[1]);
+      for (int jj = 0; jj < DXW_C / 2; ++jj) {
+        const float2 uu = u2[jj];
+        const float2 ux = make_float2(uu.x, uu.x), uy = make_float2(uu.y, uu.y);
+        acc0 = ffma2_dx(ux, w01[2 * jj], acc0);
+        acc1 = ffma2_dx(ux, w23[2 * jj], acc1);
+        acc0 = ffma2_dx(uy, w01[2 * jj + 1], acc0);
+        acc1 = ffma2_dx(uy, w23[2 * jj + 1], acc1);
       }
-      const float vv[4] = {acc[0].x, acc[0].y, acc[1].x, acc[1].y};
-      H4 hm, oh, ol;
-      hm.u = mcur[i];
+      float x[4];
+      if constexpr (BITS) {
+        const uint32_t wd = mcur[i] >> bsh;
+        x[0] = (wd & 1u) ? acc0.x : 0.f;
+        x[1] = (wd & 2u) ? acc0.y : 0.f;
+        x[2] = (wd & 4u) ? acc1.x : 0.f;
+        x[3] = (wd & 8u) ? acc1.y : 0.f;
+      } else {
+        H4 hm;
+        hm.u = mcur[i];
+        x[0] = __half2float(hm.h[0]) > 0.f ? acc0.x : 0.f;
+        x[1] = __half2float(hm.h[1]) > 0.f ? acc0.y : 0.f;
+        x[2] = __half2float(hm.h[2]) > 0.f ? acc1.x : 0.f;
+        x[3] = __half2float(hm.h[3]) > 0.f ? acc1.y : 0.f;
+      }
+      amax = fmaxf(amax, fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])), fmaxf(fabsf(x[2]), fabsf(x[3]))));
+      // split16 on pairs: hi = rn(x s), lo = rn(x s - hi)
+      const float s0 = x[0] * out_s, s1 = x[1] * out_s, s2 = x[2] * out_s, s3 = x[3] * out_s;
+      const __half2 h01 = __floats2half2_rn(s0, s1), h23 = __floats2half2_rn(s2, s3);
+      const float2 b01 = __half22float2(h01), b23 = __half22float2(h23);
+      const __half2 l01 = __floats2half2_rn(s0 - b01.x, s1 - b01.y), l23 = __floats2half2_rn(s2 - b23.x, s3 - b23.y);
+      uint2 hv, lv;
+      hv.x = *reinterpret_cast<const uint32_t*>(&h01);
+      hv.y = *reinterpret_cast<const uint32_t*>(&h23);
+      lv.x = *reinterpret_cast<const uint32_t*>(&l01);
+      lv.y = *reinterpret_cast<const uint32_t*>(&l23);
+      *reinterpret_cast<uint2*>(oh + i * ostep) = hv;
+      *reinterpret_cast<uint2*>(ol + i * ostep) = lv;
+    };
+    if (cnt >= DXW_R) {  // full batch: rows unrolled without predicates (cross-row ILP)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float v = vv[q];
-        const bool on = bits ? ((mcur[i].x >> ((col & 15) + q)) & 1u) != 0u : __half2float(hm.h[q]) > 0.f;
-        const float x = on ? v : 0.f;
-        amax = fmaxf(amax, fabsf(x));
-        split16(x, rt.out_s, oh.h[q], ol.h[q]);
-      }
-      const int64_t o = (int64_t)m * e.ld + col;
-      *reinterpret_cast<uint2*>(e.out_hi + o) = oh.u;
-      *reinterpret_cast<uint2*>(e.out_lo + o) = ol.u;
+      for (int i = 0; i < DXW_R; ++i) row(i);
+    } else {
+#pragma unroll
+      for (int i = 0; i < DXW_R; ++i)
+        if (i < cnt) row(i);
     }
 #pragma unroll
     for (int i = 0; i < DXW_R; ++i) mcur[i] = mnext[i];
@@ -383,7 +441,13 @@ void skinny_dx(cv_ctx* ctx, const SkinnyDxArgs& a) {
     // contiguous row ranges, 2 resident 256-thread blocks per SM
     const int blocks = 2 * ctx->sm_count;
     const int rpb = (a.rows + blocks - 1) / blocks;
-    launch_k(ctx->stream, k_dx_wide, (a.rows + rpb - 1) / rpb, 256, sizeof(float) * (size_t)rpb * a.c, b, rpb);
+    const size_t smem = sizeof(float) * (size_t)rpb * DXW_C;
+    const int grid = (a.rows + rpb - 1) / rpb;
+    const bool bt = b.epi.mask_bits != nullptr;
+    if (a.n == 1024) bt ? launch_k(ctx->stream, k_dx_wide<1, true>, grid, 256, smem, b, rpb)
+                        : launch_k(ctx->stream, k_dx_wide<1, false>, grid, 256, smem, b, rpb);
+    else bt ? launch_k(ctx->stream, k_dx_wide<0, true>, grid, 256, smem, b, rpb)
+            : launch_k(ctx->stream, k_dx_wide<0, false>, grid, 256, smem, b, rpb);
     ctx->launches++;
     return;
   }
