@@ -125,9 +125,9 @@ class ClockSampler:
 
 def product_traffic():
     """DRAM bytes of one GGN product from the committed ncu --set full capture
-    (scratch/product_traffic.py -> profiles/r1b_product_traffic.json), or None."""
+    (scratch/product_traffic.py -> profiles/r1c_product_traffic.json), or None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r1b_product_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r1c_product_traffic.json")) as f:
             return float(json.load(f)["dram_bytes_per_product"])
     except Exception:
         return None
@@ -341,7 +341,7 @@ def run_ours(args, rank, world):
             "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak if peak else None, "traffic": product_traffic(),
-                         "traffic_source": "profiles/r1b_product_traffic.json (ncu --set full, DRAM read+write "
+                         "traffic_source": "profiles/r1c_product_traffic.json (ncu --set full, DRAM read+write "
                                            "bytes summed over the product's kernels, cold-cache replay)",
                          "unit_of_work": f"one GGN product at b={bl}: {flops / 1e9:.1f} GFLOP useful, "
                                          f"{gv_ms:.3f} ms avg over {n_gv} (CUDA events)",
