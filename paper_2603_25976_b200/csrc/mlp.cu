@@ -125,26 +125,34 @@ template <int CM>
 __global__ void __launch_bounds__(128) k_out_reduce(const float* part, int splits, int rows, int c, int post, int loss,
                                                     const float* probs, float scale, float* out, float* out_amax,
                                                     const int* skip, const float* bias) {
-  CV_PDL_ENTRY();
-  if (skip_if(skip)) return;
   constexpr int RB = 32;             // rows per block
   constexpr int PT = RB * CM / 128;  // element positions per thread
+  constexpr int SB = 8;              // slabs in flight
   __shared__ float tile[RB * CM];
   const int m0 = blockIdx.x * RB;
   const int nrows = min(RB, rows - m0);
   const int nel = nrows * c;
+  // bias and probabilities come from the linearization / the product input: loaded before
+  // the wait for the partials' producer
   float acc[PT];
 #pragma unroll
   for (int u = 0; u < PT; ++u) {
     const int e = threadIdx.x + 128 * u;
     acc[u] = (bias && e < nel) ? bias[e % c] : 0.f;
   }
-  // four slabs' loads in flight before their (fixed-order) adds
-  int z = 0;
-  for (; z + 4 <= splits; z += 4) {
-    float x[4][PT];
+  const int r = threadIdx.x, m = m0 + r;
+  float pr[CM];
+  const bool hz_ce = post == 1 && loss == CV_LOSS_CE;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+  for (int j = 0; j < CM; ++j) pr[j] = (hz_ce && r < nrows && j < c) ? probs[(int64_t)m * c + j] : 0.f;
+  CV_PDL_ENTRY();
+  if (skip_if(skip)) return;
+  // SB slabs' loads in flight before their (fixed-order) adds
+  int z = 0;
+  for (; z + SB <= splits; z += SB) {
+    float x[SB][PT];
+#pragma unroll
+    for (int i = 0; i < SB; ++i) {
       const float* p = part + ((int64_t)(z + i) * rows + m0) * c;
 #pragma unroll
       for (int u = 0; u < PT; ++u) {
@@ -153,7 +161,7 @@ __global__ void __launch_bounds__(128) k_out_reduce(const float* part, int split
       }
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < SB; ++i)
 #pragma unroll
       for (int u = 0; u < PT; ++u) acc[u] += x[i][u];
   }
@@ -171,7 +179,6 @@ __global__ void __launch_bounds__(128) k_out_reduce(const float* part, int split
     if (e < nel) tile[e] = acc[u];
   }
   __syncthreads();
-  const int r = threadIdx.x, m = m0 + r;
   float amax = 0.f;
   if (r < nrows) {
     float t[CM];
@@ -179,7 +186,7 @@ __global__ void __launch_bounds__(128) k_out_reduce(const float* part, int split
     for (int j = 0; j < CM; ++j) t[j] = j < c ? tile[r * c + j] : 0.f;
     if (post == 1) {
       if (loss == CV_LOSS_CE) {
-        const float* p = probs + (int64_t)m * c;
+        const float* p = pr;
         float pt = 0.f;
 #pragma unroll
         for (int j = 0; j < CM; ++j)
