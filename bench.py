@@ -133,6 +133,33 @@ def product_traffic():
         return None
 
 
+# the tensor-core launches of one C3 product in the committed capture's order
+_GEMM_ROLES = [("JVP0 X V0, mask bits", 8192, 1024, 785), ("JVP1 [A1|da0][V1;W1] + fused output JVP", 8192, 1024, 2049),
+               ("dW1 weight gradient, split-K, side stream (SM share)", 1025, 1024, 8192),
+               ("dX1 backward, mask bits (SM share)", 8192, 1024, 1024), ("dW0 weight gradient, split-K", 785, 1024, 8192)]
+
+
+def gemm_launch_rooflines(peak):
+    """Per-launch tensor roofline of the product's GEMMs from the committed ncu --set full
+    capture (cold-cache serialised replay: co-scheduled launches replay on their SM share)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1c_product_traffic.json")) as f:
+            kern = json.load(f)["kernels"]
+    except Exception:
+        return None
+    tc2 = [k for k in kern if "k_gemm_tc2" in k["kernel"]]
+    if len(tc2) != len(_GEMM_ROLES):
+        return None
+    out = []
+    for k, (role, m, n, kk) in zip(tc2, _GEMM_ROLES):
+        tf = 2.0 * m * n * kk / (k["us"] * 1e-6) / 1e12
+        out.append({"launch": role, "useful_gflop": round(2.0 * m * n * kk / 1e9, 2), "us": k["us"],
+                    "tflops": round(tf, 1), "frac": round(tf / peak, 3) if peak else None,
+                    "tensor_pipe_pct": k.get("tensor_pipe_pct"),
+                    "dram_bytes": k["dram_read_B"] + k["dram_write_B"]})
+    return out
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -345,7 +372,8 @@ def run_ours(args, rank, world):
                                            "bytes summed over the product's kernels, cold-cache replay)",
                          "unit_of_work": f"one GGN product at b={bl}: {flops / 1e9:.1f} GFLOP useful, "
                                          f"{gv_ms:.3f} ms avg over {n_gv} (CUDA events)",
-                         "peak_source": peak_note},
+                         "peak_source": peak_note,
+                         "per_launch_ncu": gemm_launch_rooflines(peak) if bl == 8192 else None},
             "engine": os.environ.get("CURVOPT_ENGINE", "auto")}
     if world == 1 and not args.no_cpu:
         sps_cpu, times, gv = cpu_oracle_run(max_seconds=15.0, max_steps=3, warmup=0)
