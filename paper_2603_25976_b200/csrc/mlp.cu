@@ -505,7 +505,7 @@ static void skinny_weight_grad(cv_ctx* ctx, cv_snap* s, const float* U, Scale* u
   const int l = s->L - 1;
   if (s->tc_out) {
     static const int cosched = !(getenv("CURVOPT_COSCHED") && getenv("CURVOPT_COSCHED")[0] == '0');
-    static const int side_ctas = getenv("CURVOPT_DWL_CTAS") ? atoi(getenv("CURVOPT_DWL_CTAS")) : 64;
+    static const int side_ctas = getenv("CURVOPT_DWL_CTAS") ? atoi(getenv("CURVOPT_DWL_CTAS")) : 128;
     // beside the output-layer backward: the cotangent split and the GEMM both go to the
     // second side stream (the caller joins it); not with tc_dx, whose backward reuses U's split
     const bool on_side = side && cosched && side_ctas > 0 && ctx->engine != CV_ENGINE_SIMT && !s->tc_dx;
