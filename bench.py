@@ -92,10 +92,15 @@ class ClockSampler:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
                                           "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.first = threading.Event()
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # nvidia-smi needs a moment to start: enter the timed region only once it samples
+            # (a short timed region could otherwise see no sample at all)
+            self.first.wait(timeout=5.0)
         except Exception:
             self.proc = None
+        self.start_idx = len(self.rows)
         return self
 
     def _read(self):
@@ -103,6 +108,7 @@ class ClockSampler:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 7:
                 self.rows.append(parts)
+                self.first.set()
 
     def __exit__(self, *a):
         if self.proc is not None:
@@ -113,8 +119,11 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        # samples taken inside the timed region (else the one just before it)
+        rows = self.rows[self.start_idx:] or self.rows[-1:]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        self.rows = rows
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
