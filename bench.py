@@ -134,9 +134,9 @@ class ClockSampler:
 
 def product_traffic():
     """DRAM bytes of one GGN product from the committed ncu --set full capture
-    (scratch/product_traffic.py -> profiles/r1c_product_traffic.json), or None."""
+    (scratch/product_traffic.py -> profiles/r1d_product_traffic.json), or None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r1c_product_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r1d_product_traffic.json")) as f:
             return float(json.load(f)["dram_bytes_per_product"])
     except Exception:
         return None
@@ -152,7 +152,7 @@ def gemm_launch_rooflines(peak):
     """Per-launch tensor roofline of the product's GEMMs from the committed ncu --set full
     capture (cold-cache serialised replay: co-scheduled launches replay on their SM share)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r1c_product_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r1d_product_traffic.json")) as f:
             kern = json.load(f)["kernels"]
     except Exception:
         return None
@@ -377,7 +377,7 @@ def run_ours(args, rank, world):
             "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak if peak else None, "traffic": product_traffic(),
-                         "traffic_source": "profiles/r1c_product_traffic.json (ncu --set full, DRAM read+write "
+                         "traffic_source": "profiles/r1d_product_traffic.json (ncu --set full, DRAM read+write "
                                            "bytes summed over the product's kernels, cold-cache replay)",
                          "unit_of_work": f"one GGN product at b={bl}: {flops / 1e9:.1f} GFLOP useful, "
                                          f"{gv_ms:.3f} ms avg over {n_gv} (CUDA events)",
