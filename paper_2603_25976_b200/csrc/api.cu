@@ -204,6 +204,10 @@ int cv_linearize(cv_ctx* ctx, int n_layers, const int* dims, int act, int loss, 
     s->v_hi = alloc_h(s, s->d);
     s->v_lo = alloc_h(s, s->d);
     for (int l = 0; l < L; ++l) s->acts.push_back(alloc_split(s, b, dims[l], acts_sc + l));
+    // the weight and input splits go to the GPU before the remaining allocations: that host
+    // work no longer leaves the device idle at the start of every step
+    split_flat(ctx, w, s->d, s->off, s->w_hi, s->w_lo, s->w_sc, nullptr, 0, nullptr);
+    split_rows(ctx, X, dims[0], b, dims[0], s->acts[0], 1);
     s->bits_buf.assign(L, nullptr);
     if (act == CV_ACT_RELU && ctx->engine != CV_ENGINE_SIMT)
       for (int l = 1; l < L; ++l) {
@@ -269,12 +273,10 @@ int cv_linearize(cv_ctx* ctx, int n_layers, const int* dims, int act, int loss, 
     delete s;
     throw;
   }
-  split_flat(ctx, w, s->d, s->off, s->w_hi, s->w_lo, s->w_sc, nullptr, 0, nullptr);
   if (s->wl_f32)
     cudaMemcpyAsync(s->wl_f32, w + s->off[L - 1], sizeof(float) * (size_t)(dims[L - 1] + 1) * c,
                     cudaMemcpyDeviceToDevice, ctx->stream);
   if (s->tc_out) pad_last_weights(ctx, s);
-  split_rows(ctx, X, dims[0], b, dims[0], s->acts[0], 1);
   for (int l = 0; l + 1 < L; ++l) set_col_value(ctx, s->da[l], b, dims[l + 1], 0.f);
   mlp_linearize(ctx, s, loss_out, grad_out);
   *snap = s;
