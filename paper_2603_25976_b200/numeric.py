@@ -8,6 +8,8 @@ whichever side the operands live; mixing sides is a ContractError.
 
 from __future__ import annotations
 
+import functools
+import math
 from dataclasses import dataclass
 from typing import Any
 
@@ -22,8 +24,17 @@ def _is_torch(x) -> bool:
     return type(x).__module__.startswith("torch")
 
 
+@functools.lru_cache(maxsize=256)
+def _layout_size(layout: Layout) -> int:
+    return int(sum(math.prod(int(n) for n in shape) for _, shape in layout))
+
+
 def layout_size(layout: Layout) -> int:
-    return int(sum(int(np.prod(shape, dtype=np.int64)) for _, shape in layout))
+    """Total element count of a layout (cached: every ParamVector validates against it)."""
+    try:
+        return _layout_size(layout)
+    except TypeError:  # unhashable (list-based) layout
+        return int(sum(math.prod(int(n) for n in shape) for _, shape in layout))
 
 
 @dataclass(frozen=True)
