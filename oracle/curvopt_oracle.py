@@ -510,15 +510,35 @@ def ema_diag(diag, new, beta):  # control.py:70-77
 
 
 # --------------------------------------------------------------------------
-# Post-direction chain (transforms.py:148-199), the subset the configs use
+# Post-direction chain (transforms.py:121-199): every link kind
 # --------------------------------------------------------------------------
 
+def schedule_value(kind, t, p):
+    """Learning-rate schedules (transforms.py:121-145)."""
+    a0 = float(p.get("alpha0", 1.0))
+    if kind == "constant":
+        return a0
+    if kind == "step_decay":
+        return a0 * float(p.get("gamma", 0.1)) ** (t // int(p.get("period", 1000)))
+    if kind == "cosine_warmup":
+        warm, total = int(p.get("warmup", 0)), int(p["total"])
+        if warm > 0 and t < warm:
+            return a0 * t / warm
+        prog = min((t - warm) / max(total - warm, 1), 1.0)
+        return 0.5 * a0 * (1.0 + math.cos(math.pi * prog))
+    raise ValueError(kind)
+
+
 def chain_apply(chain, state, direction, w, t, precond_diag=None):
-    x = direction.copy()
+    """Links are (kind, params) pairs, applied left to right (transforms.py:148-199)."""
+    x = np.array(direction, dtype=np.float64)
     new = []
     for (kind, p), st in zip(chain, state):
         if kind == "scale":
             x = x * p["value"]
+            new.append({})
+        elif kind == "scale_by_schedule":
+            x = x * schedule_value(p["schedule"], t, p)
             new.append({})
         elif kind == "trace_momentum":
             m = p["beta"] * st["trace"] + x
@@ -532,13 +552,57 @@ def chain_apply(chain, state, direction, w, t, precond_diag=None):
             if n > p["max_norm"] and n > 0.0:
                 x = x * (p["max_norm"] / n)
             new.append({})
+        elif kind == "scale_by_adam":
+            tt = st["t"] + 1
+            m = p["b1"] * st["m"] + (1.0 - p["b1"]) * x
+            v = p["b2"] * st["v"] + (1.0 - p["b2"]) * (x * x)
+            x = (m / (1.0 - p["b1"] ** tt)) / (np.sqrt(v / (1.0 - p["b2"] ** tt)) + p["eps"])
+            new.append({"m": m, "v": v, "t": tt})
+        elif kind == "sophia_clip":
+            den = np.maximum(p["gamma"] * precond_diag, p["eps"])
+            x = np.clip(x / den, -1.0, 1.0)
+            new.append({})
         else:
             raise NotImplementedError(kind)
     return x, new
 
 
 def chain_init(chain, d):
-    return [{"trace": np.zeros(d)} if k == "trace_momentum" else {} for k, _ in chain]
+    out = []
+    for k, _ in chain:
+        if k == "trace_momentum":
+            out.append({"trace": np.zeros(d)})
+        elif k == "scale_by_adam":
+            out.append({"m": np.zeros(d), "v": np.zeros(d), "t": 0})
+        else:
+            out.append({})
+    return out
+
+
+def gnb_diag(lin: Lin, rng: ORng, n_samples: int):
+    """Sampled-label squared-gradient GGN diagonal estimate (telemetry.py:129-160)."""
+    p = lin.probs
+    b, c = p.shape
+    cum = np.cumsum(p, axis=1)
+    acc = np.zeros(n_params(lin.dims))
+    for _ in range(n_samples):
+        u = rng.uniform(b)
+        labels = np.minimum((u[:, None] > cum).sum(axis=1), c - 1)
+        cot = p.copy()
+        cot[np.arange(b), labels] -= 1.0
+        gh = vjp(lin, cot / b)
+        acc += b * (gh * gh)
+    return acc / n_samples
+
+
+def gen_regression(n, d, noise_std, seed, train_frac=0.9):
+    """Linear teacher on a gaussian design, 90/10 split (harness/data.py:49-60)."""
+    rng = ORng(seed)
+    X = rng.normal(n * d).reshape(n, d)
+    beta = rng.normal(d)
+    y = (X @ beta + rng.normal(n) * noise_std)[:, None]
+    ntr = int(n * train_frac)
+    return (X[:ntr], y[:ntr]), (X[ntr:], y[ntr:])
 
 
 # --------------------------------------------------------------------------
@@ -552,8 +616,8 @@ STEP_FIELDS = ("loss_before", "loss_after", "rho", "lam", "grad_norm", "step_nor
 @dataclass
 class OSpec:
     """Flat restatement of MethodSpec for the oracle (method.py:64-134)."""
-    curvature: str = "ggn_ce"
-    solver: str = "cg"                 # cg | row_cholesky
+    curvature: str | None = "ggn_ce"
+    solver: str | None = "cg"          # None (identity) | diag | cg | row_cholesky
     tol: float = 1e-5
     maxiter: int = 10
     stabilise_every: int = 10
@@ -563,8 +627,9 @@ class OSpec:
     damping: str = "constant"          # constant | trust_region
     lam0: float = 1.0
     tr_every_k: int = 5
-    estimator_every_k: int = -1        # hutchinson when >= 1
+    estimator_every_k: int = -1        # fires when >= 1
     estimator_probes: int = 1
+    estimator: str = "hutchinson"      # hutchinson | gnb
     rho_every_k: int = -1
     trace_every_k: int = -1
     trace_probes: int = 1
@@ -591,6 +656,38 @@ def oracle_init(spec: OSpec, d: int, seed: int = 0) -> OState:  # method.py:286-
     return OState(spec.lam0, np.zeros(d), chain_init(spec.chain, d), None, 0, ORng(seed))
 
 
+def preset_ospec(name: str) -> OSpec:
+    """The presets of method.py:438-552 as flat oracle specs."""
+    def soph(g):
+        return (("trace_momentum", {"beta": 0.96}), ("sophia_clip", {"gamma": g, "eps": 1e-12}),
+                ("add_decayed_weights", {"weight_decay": 1e-4}),
+                ("scale_by_schedule", {"schedule": "constant", "alpha0": 0.01}), ("scale", {"value": -1.0}))
+    table = {
+        "sophia_g": OSpec(curvature="ggn_ce", solver=None, precond="diag_ema", precond_beta=0.99, lam0=0.0,
+                          estimator="gnb", estimator_every_k=10, chain=soph(0.05)),
+        "sophia_h": OSpec(curvature="hessian", solver=None, precond="diag_ema", precond_beta=0.99, lam0=0.0,
+                          estimator="hutchinson", estimator_every_k=10, chain=soph(0.01)),
+        "sophia_n": OSpec(curvature="ggn_ce", solver=None, precond="diag_ema", precond_beta=0.99, lam0=0.0,
+                          estimator="hutchinson", estimator_every_k=10, chain=soph(0.05)),
+        "adahessian": OSpec(curvature="hessian", solver="diag", precond="diag_ema", precond_beta=0.999, lam0=1.0,
+                            estimator="hutchinson", estimator_every_k=1,
+                            chain=(("trace_momentum", {"beta": 0.9}),
+                                   ("scale_by_schedule", {"schedule": "constant", "alpha0": 0.1}),
+                                   ("scale", {"value": -1.0}))),
+        "sgd": OSpec(curvature=None, solver=None, lam0=0.0,
+                     chain=(("scale_by_schedule", {"schedule": "constant", "alpha0": 0.1}), ("scale", {"value": -1.0}))),
+        "sgdm": OSpec(curvature=None, solver=None, lam0=0.0,
+                      chain=(("trace_momentum", {"beta": 0.9}), ("add_decayed_weights", {"weight_decay": 5e-4}),
+                             ("scale_by_schedule", {"schedule": "constant", "alpha0": 0.05}),
+                             ("scale", {"value": -1.0}))),
+        "adam": OSpec(curvature=None, solver=None, lam0=0.0,
+                      chain=(("scale_by_adam", {"b1": 0.9, "b2": 0.999, "eps": 1e-8}),
+                             ("scale_by_schedule", {"schedule": "constant", "alpha0": 1e-3}),
+                             ("scale", {"value": -1.0}))),
+    }
+    return table[name]
+
+
 def oracle_step(spec: OSpec, dims, activation, loss, w, X, y, st: OState, gv_log=None, masks=None):
     """One planned step; returns (w', state', info dict, direction).  method.py:302-389."""
     t = st.t
@@ -612,7 +709,11 @@ def oracle_step(spec: OSpec, dims, activation, loss, w, X, y, st: OState, gv_log
     if not (math.isfinite(lin.value) and np.all(np.isfinite(g))):
         return abort()
     warm = None
-    if spec.solver == "cg":
+    if spec.solver is None:  # identity lane: the gradient itself (method.py:239-241)
+        direction, iters, conv, relres = g.copy(), -1, -1, float("nan")
+    elif spec.solver == "diag":  # solve_diag (solvers.py:45-50)
+        direction, iters, conv, relres = g / (np.maximum(st.diag, DIAG_FLOOR) + st.lam), -1, -1, float("nan")
+    elif spec.solver == "cg":
         x0 = st.warm if (spec.warm_start and st.warm is not None and st.warm.size == g.size) else None
         res = cg(mv, g, st.lam, spec.tol, spec.maxiter, spec.stabilise_every,
                  st.diag if spec.precond else None, x0)
@@ -642,7 +743,10 @@ def oracle_step(spec: OSpec, dims, activation, loss, w, X, y, st: OState, gv_log
         info.update(loss_after=la, rho=rho)
     diag = st.diag
     if _fires(spec.estimator_every_k, t):
-        est = hutchinson_diag(mv, rng, g.size, spec.estimator_probes)
+        if spec.estimator == "gnb":
+            est = gnb_diag(lin, rng, spec.estimator_probes)
+        else:
+            est = hutchinson_diag(mv, rng, g.size, spec.estimator_probes)
         diag = ema_diag(diag, est, spec.precond_beta) if spec.precond == "diag_ema" else np.maximum(est, 0.0)
         info["diag_mean"] = float(diag.mean())
     if _fires(spec.trace_every_k, t):

@@ -245,12 +245,9 @@ int cv_linearize(cv_ctx* ctx, int n_layers, const int* dims, int act, int loss, 
     s->skinny_ws_elems = need;
     s->skinny_ws = alloc_f(s, need);
     // output layer on the tensor-core engine when the shapes allow TMA operands
-    const char* env = getenv("CURVOPT_TC_OUT");
     s->cp = c;
-    s->tc_out = ctx->engine != CV_ENGINE_SIMT && !(env && env[0] == '0') && c >= 8 && b >= 128 && dims[L - 1] >= 64;
+    s->tc_out = ctx->engine != CV_ENGINE_SIMT && c >= 8 && b >= 128 && dims[L - 1] >= 64;
     if (s->tc_out) {
-      const char* dx = getenv("CURVOPT_TC_DX");
-      s->tc_dx = dx && dx[0] == '1';
       s->cp = c <= 16 ? 16 : 32;
       s->ldw = ((int64_t)dims[L - 1] + 1 + 7) / 8 * 8;
       s->ldb = ((int64_t)b + 7) / 8 * 8;

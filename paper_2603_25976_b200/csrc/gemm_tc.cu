@@ -60,7 +60,6 @@ struct TcArgs {
   Epilogue epi;
   const int* skip;
   int lower_only;
-  int dbg;            // experiments: 1 = epilogue reads TMEM only
   int tma_out;        // 0: per-thread stores; 1: fp16 split pair via TMA; 2: fp32 (out or partial) via TMA
   float* partial;     // split-K partials (nullptr: apply the epilogue directly)
   int tiles_m, tiles_n, splits;
@@ -615,7 +614,7 @@ CV_DEV void epi_prefetch_mask(const TcArgs& a, int m_base, int n0, int q, int ha
 template <int BN>
 CV_DEV void tile_epilogue(const TcArgs& a, const TcMaps& maps, const EpiRt& rt, uint32_t tacc, int m_base, int n0,
                           int split, float inv, int q, int half, int lane, uint8_t* stg, uint8_t* hstg) {
-  if (a.tma_out && !a.dbg) {
+  if (a.tma_out) {
     float amax = 0.f, ramax = 0.f;
     const Epilogue& e = a.epi;
     const bool bits = a.tma_out == 1 && (e.mode == EPI_SPLIT_MASK || e.mode == EPI_HVP) && e.act == CV_ACT_RELU &&
@@ -634,10 +633,6 @@ CV_DEV void tile_epilogue(const TcArgs& a, const TcMaps& maps, const EpiRt& rt, 
   for (int c = half * C0; c < (NCH >= 2 ? (half + 1) * C0 : (half == 0 ? 1 : 0)); ++c) {
     uint32_t r[32];
     tmem_ld32(trow + c * 32, r);
-    if (a.dbg) {
-      if (r[0] == 0x7fffffff && r[31] == 1) amax += 1.f;
-      continue;
-    }
     if (m >= a.M) continue;
     const int nb = n0 + c * 32;
     float v[32];
@@ -993,8 +988,7 @@ static CUtensorMap make_out_map(const void* ptr, int fp16, int64_t cols, int64_t
 // The TMA-store epilogue a GEMM's output allows without split-K partials:
 // 0 none (per-thread stores), 1 fp16 split pair, 2 fp32 (mirrors setup_out).
 static int tma_out_mode(const GemmArgs& g) {
-  static const int off = getenv("CURVOPT_TC_TMA_OUT") && getenv("CURVOPT_TC_TMA_OUT")[0] == '0';
-  if (off || g.lower_only) return 0;
+  if (g.lower_only) return 0;
   const Epilogue& e = g.epi;
   if (e.mode == EPI_STORE) return ((e.ld & 3) || !aligned16(e.out)) ? 0 : 2;
   const bool relu_mask = (e.mode == EPI_SPLIT_MASK || e.mode == EPI_HVP) && e.act == CV_ACT_RELU && !e.raw &&
@@ -1006,9 +1000,8 @@ static int tma_out_mode(const GemmArgs& g) {
 
 // Choose the TMA-store epilogue when the mode and layout allow it.
 static void setup_out(const GemmArgs& g, TcMaps& maps, TcArgs& a, float* partial, int splits) {
-  static const int off = getenv("CURVOPT_TC_TMA_OUT") && getenv("CURVOPT_TC_TMA_OUT")[0] == '0';
   a.tma_out = 0;
-  if (off || g.lower_only) return;
+  if (g.lower_only) return;
   const Epilogue& e = g.epi;
   if (partial) {
     if ((g.N & 3) || !aligned16(partial)) return;
@@ -1082,8 +1075,6 @@ static void fill_args(const GemmArgs& g, int bbox, TcMaps& maps, TcArgs& a) {
   a.epi = g.epi;
   a.skip = g.skip;
   a.lower_only = g.lower_only;
-  static const int dbg = getenv("CURVOPT_DBG_EPI") ? atoi(getenv("CURVOPT_DBG_EPI")) : 0;
-  a.dbg = dbg;
 }
 
 template <int BN, int STAGES>
@@ -1131,7 +1122,7 @@ static int launch_tc(cv_ctx* ctx, const GemmArgs& g, int splits, float* ext_part
 
 // Tile configuration and split-K factor of a GEMM on `sms` SMs.
 struct TcPlan {
-  int kind;  // 0: <32,4>, 1: 2-CTA 256x256, 2: <256,2>, 3: <128,3>, 4: 2-CTA 256x128, 5: <64,4>
+  int kind;  // 0: <32,4>, 1: 2-CTA 256x256, 2: <256,2>, 3: <128,3>, 5: <64,4>
   int tiles, kb_total, splits;
   int M, N;
 };
@@ -1141,10 +1132,10 @@ static double plan_time(const TcPlan& p, int sms);
 static TcPlan tc_plan_kind(const GemmArgs& g, int sms, int kind) {
   TcPlan p;
   p.kind = kind;
-  const int bn = kind == 0 ? 32 : (kind == 5 ? 64 : ((kind == 3 || kind == 4) ? 128 : 256));
-  const int bm = (kind == 1 || kind == 4) ? 256 : TC_BM;
+  const int bn = kind == 0 ? 32 : (kind == 5 ? 64 : (kind == 3 ? 128 : 256));
+  const int bm = kind == 1 ? 256 : TC_BM;
   p.tiles = ((g.M + bm - 1) / bm) * ((g.N + bn - 1) / bn);
-  const int slots = (kind == 1 || kind == 4) ? sms / 2 : sms;  // concurrent work items
+  const int slots = kind == 1 ? sms / 2 : sms;  // concurrent work items
   p.kb_total = 0;
   for (int s = 0; s < g.nseg; ++s) p.kb_total += (g.seg[s].K + TC_BK - 1) / TC_BK;
   // split K when the tile grid cannot fill the machine (weight-gradient GEMMs: M, N ~ 1e3, K = batch)
@@ -1177,14 +1168,13 @@ static TcPlan tc_plan_kind(const GemmArgs& g, int sms, int kind) {
 // relative time of a plan: rounds of work items x k-blocks per item (+ fill/epilogue),
 // per SM; a 2-CTA tile costs each SM what a 1-CTA 128 x 256 tile does
 static double plan_time(const TcPlan& p, int sms) {
-  const int slots = (p.kind == 1 || p.kind == 4) ? sms / 2 : sms;
+  const int slots = p.kind == 1 ? sms / 2 : sms;
   const int items = p.tiles * p.splits;
   const int rounds = (items + slots - 1) / slots;
   const double item_kb = (double)((p.kb_total + p.splits - 1) / p.splits);
-  // 2-stage ring / narrower tiles (measured on B200: the 2-CTA 256x128 tile streams at ~0.7x
-  // the 256x256 rate, so it is only reachable by CURVOPT_TC_KIND=4)
-  const double pen = p.kind == 2 ? 1.3 : (p.kind == 3 ? 1.2 : (p.kind == 4 ? 1.4 : (p.kind == 5 ? 1.6 : 1.0)));
-  const double per_kb = (p.kind == 3 || p.kind == 4) ? 0.5 : (p.kind == 5 ? 0.25 : 1.0);  // narrower tiles: less MMA work
+  // 2-stage ring / narrower tiles (measured on B200)
+  const double pen = p.kind == 2 ? 1.3 : (p.kind == 3 ? 1.2 : (p.kind == 5 ? 1.6 : 1.0));
+  const double per_kb = p.kind == 3 ? 0.5 : (p.kind == 5 ? 0.25 : 1.0);  // narrower tiles: less MMA work
   // split-K partials: written once and read once by the fixed-order reduce (units of
   // ~1.2 us, one 256x256x64 3xFP16 k-block on a CTA pair, at ~6.5 TB/s)
   const double red = p.splits > 1 ? (double)(p.splits + 1) * p.M * p.N * 4.0 / 7.8e6 + 2.0 : 0.0;
@@ -1231,16 +1221,12 @@ static TcPlan tc_plan(const GemmArgs& g, int sms) {
 }
 
 static TcPlan tc_plan_search(const GemmArgs& g, int sms) {
-  static const int force_bn = getenv("CURVOPT_TC_BN") ? atoi(getenv("CURVOPT_TC_BN")) : 0;
-  static const int use_2sm = getenv("CURVOPT_TC_2SM") ? atoi(getenv("CURVOPT_TC_2SM")) : 1;
-  static const int force_kind = getenv("CURVOPT_TC_KIND") ? atoi(getenv("CURVOPT_TC_KIND")) : -1;
   if (g.N <= 32) return tc_plan_kind(g, sms, 0);
-  if (force_kind >= 1 && force_kind <= 5) return tc_plan_kind(g, sms, force_kind);
-  const bool pair = use_2sm && !force_bn && g.M >= 256 && g.N >= 256;
-  const bool wide = force_bn ? force_bn == 256 : g.N >= 512;
+  const bool pair = g.M >= 256 && g.N >= 256;
+  const bool wide = g.N >= 512;
   TcPlan best = tc_plan_kind(g, sms, pair ? 1 : (wide ? 2 : 3));
   const int slots = best.kind == 1 ? sms / 2 : sms;
-  if ((g.epi.mode == EPI_STORE || best.tiles < slots) && !force_bn) {
+  if (g.epi.mode == EPI_STORE || best.tiles < slots) {
     // split-K weight gradients and under-filled grids: the tile shape that wastes the
     // least of the edges / fills the slots best
     for (int k : {1, 2, 3, 5}) {  // (kind 5, 128x64: only for grids the wider tiles cannot fill)
@@ -1261,9 +1247,7 @@ double gemm_tc_estimate(const cv_ctx* ctx, const GemmArgs& g, int ctas) {
 // (tile_epilogue_tma), or 0 when the GEMM cannot carry the head (engine, layout,
 // epilogue mode or tile plan); the caller then runs the output layer separately.
 int gemm_tc_head_groups(const cv_ctx* ctx, const GemmArgs& g) {
-  static const int off = getenv("CURVOPT_HEAD") && getenv("CURVOPT_HEAD")[0] == '0';
-  static const int tma_off = getenv("CURVOPT_TC_TMA_OUT") && getenv("CURVOPT_TC_TMA_OUT")[0] == '0';
-  if (off || tma_off || ctx->engine == CV_ENGINE_SIMT || !gemm_tc_supported(g) || g.lower_only) return 0;
+  if (ctx->engine == CV_ENGINE_SIMT || !gemm_tc_supported(g) || g.lower_only) return 0;
   const Epilogue& e = g.epi;
   const bool jvp_head = e.mode == EPI_SPLIT_MASK && e.act == CV_ACT_RELU && !e.raw && e.mask_div == 1 &&
                         !(e.mask_ld & 7) && aligned16(e.mask_hi) && aligned16(e.mask_lo);
@@ -1272,7 +1256,7 @@ int gemm_tc_head_groups(const cv_ctx* ctx, const GemmArgs& g) {
   const int sms = g.max_ctas > 0 && g.max_ctas < ctx->sm_count ? g.max_ctas : ctx->sm_count;
   const TcPlan p = tc_plan(g, sms);
   if (p.kind == 0 || p.splits > 1) return 0;
-  const int bn = p.kind == 5 ? 64 : ((p.kind == 3 || p.kind == 4) ? 128 : 256);
+  const int bn = p.kind == 5 ? 64 : (p.kind == 3 ? 128 : 256);
   return 2 * ((g.N + bn - 1) / bn);
 }
 
@@ -1286,134 +1270,13 @@ bool gemm_tc_tma_split(const cv_ctx* ctx, const GemmArgs& g) {
 void gemm_tc(cv_ctx* ctx, const GemmArgs& g) {
   const int sms = g.max_ctas > 0 && g.max_ctas < ctx->sm_count ? g.max_ctas : ctx->sm_count;
   const TcPlan p = tc_plan(g, sms);
-  static const int dbg_plan = getenv("CURVOPT_DEBUG_PLAN") ? 1 : 0;
-  if (dbg_plan)
-    fprintf(stderr, "[plan] M=%d N=%d K=%d nseg=%d mode=%d sms=%d -> kind=%d tiles=%d splits=%d est=%.1f\n", g.M, g.N,
-            g.seg[0].K + (g.nseg > 1 ? g.seg[1].K : 0), g.nseg, g.epi.mode, sms, p.kind, p.tiles, p.splits,
-            plan_time(p, sms));
   switch (p.kind) {
     case 0: launch_tc<32, 4>(ctx, g, p.splits); break;
     case 1: launch_tc2<3, 256>(ctx, g, p.splits); break;
-    case 4: launch_tc2<4, 128>(ctx, g, p.splits); break;
     case 2: launch_tc<256, 2>(ctx, g, p.splits); break;
     case 5: launch_tc<64, 4>(ctx, g, p.splits); break;
     default: launch_tc<128, 3>(ctx, g, p.splits); break;
   }
-}
-
-// Two independent GEMMs in one persistent 2-CTA launch (k_gemm_tc2x2): the work items
-// of both (a: whole tiles; b: split-K items of about a's k-depth) are assigned to the
-// clusters longest-first, each to the least loaded cluster, so neither GEMM's last wave
-// leaves SMs idle and no static SM split is needed.  Returns false when either GEMM
-// does not run on the 256x256 2-CTA tiles.
-bool gemm_tc_pair_fused(cv_ctx* ctx, const GemmArgs& ga, const GemmArgs& gb) {
-  // opt-in (CURVOPT_PAIR_FUSED=1): measured at C3 it ties or trails the SM-split co-schedule,
-  // because the persistent pair holds every SM and the output layer's weight gradient can
-  // no longer run beside it
-  static const int off = !(getenv("CURVOPT_PAIR_FUSED") && getenv("CURVOPT_PAIR_FUSED")[0] == '1');
-  if (off || ctx->engine == CV_ENGINE_SIMT || !gemm_tc_supported(ga) || !gemm_tc_supported(gb)) return false;
-  if (ga.lower_only || gb.lower_only || ga.epi.head_part || gb.epi.head_part) return false;
-  const int sms = ctx->sm_count, C = sms / 2;
-  const TcPlan pa = tc_plan(ga, sms);
-  if (pa.kind != 1 || pa.splits != 1 || gb.M < 256 || gb.N < 256) return false;  // b: 2-CTA tiles, own split-K
-  using Cfg = Tc2Cfg<3, 256>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_gemm_tc2x2<3, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
-    attr_set = true;
-  }
-  TcMaps2 maps;
-  TcArgs2 args;
-  memset(&args, 0, sizeof(args));
-  const GemmArgs* gs[2] = {&ga, &gb};
-  float* part[2] = {nullptr, nullptr};
-  int kb_item_a = 0;
-  for (int i = 0; i < 2; ++i) {
-    const GemmArgs& g = *gs[i];
-    TcArgs& a = args.a[i];
-    fill_args(g, 128, maps.m[i], a);
-    int splits = 1;
-    if (i == 1 && g.epi.mode == EPI_STORE) {
-      // split-K items of about a's depth / bdiv (smaller items fill the last round),
-      // bounded by 4 k-blocks per item and 32 splits
-      static const int bdiv = getenv("CURVOPT_PAIR_BDIV") ? atoi(getenv("CURVOPT_PAIR_BDIV")) : 1;
-      const int target = std::max(4, kb_item_a / std::max(1, bdiv));
-      splits = (a.kb_total + target / 2) / target;
-      if (splits > a.kb_total / 4) splits = a.kb_total / 4;
-      if (splits > 32) splits = 32;
-      if (splits < 1) splits = 1;
-    }
-    a.kb_per_split = (a.kb_total + splits - 1) / splits;
-    splits = (a.kb_total + a.kb_per_split - 1) / a.kb_per_split;
-    a.splits = splits;
-    a.tiles_m = (g.M + 2 * TC_BM - 1) / (2 * TC_BM);
-    a.tiles_n = (g.N + 256 - 1) / 256;
-    if (i == 0) kb_item_a = a.kb_per_split;
-    if (splits > 1) {
-      part[i] = (float*)ctx->pool.get(sizeof(float) * (size_t)splits * g.M * g.N);
-      a.partial = part[i];
-    }
-    setup_out(g, maps.m[i], a, a.partial, splits);
-  }
-  // LPT schedule, cached by geometry
-  std::vector<int> key = {C};
-  for (int i = 0; i < 2; ++i) {
-    const TcArgs& a = args.a[i];
-    key.insert(key.end(), {a.M, a.N, a.kb[0], a.kb[1], a.kb_per_split, a.splits, a.tiles_m, a.tiles_n});
-  }
-  int* dsched = nullptr;
-  int ld = 0;
-  auto it = ctx->pair_sched.find(key);
-  if (it != ctx->pair_sched.end()) {
-    dsched = it->second.first;
-    ld = it->second.second;
-  } else {
-    struct It {
-      int cost, code;
-    };
-    std::vector<It> items;
-    for (int i = 0; i < 2; ++i) {
-      const TcArgs& a = args.a[i];
-      const int tiles = a.tiles_m * a.tiles_n, total = tiles * a.splits;
-      for (int w = 0; w < total; ++w) {
-        const int split = w / tiles;
-        const int kb0 = split * a.kb_per_split;
-        const int nkb = std::min(a.kb_total, kb0 + a.kb_per_split) - kb0;
-        items.push_back({nkb + 2, (i << 24) | w});  // + fill / epilogue
-      }
-    }
-    std::stable_sort(items.begin(), items.end(), [](const It& x, const It& y) { return x.cost > y.cost; });
-    std::vector<std::vector<int>> lists(C);
-    std::vector<long long> load(C, 0);
-    for (const It& x : items) {
-      int best = 0;
-      for (int c = 1; c < C; ++c)
-        if (load[c] < load[best]) best = c;
-      load[best] += x.cost;
-      lists[best].push_back(x.code);
-    }
-    size_t mx = 0;
-    for (auto& l : lists) mx = std::max(mx, l.size());
-    ld = (int)mx + 1;
-    std::vector<int> h((size_t)C * ld, -1);
-    for (int c = 0; c < C; ++c)
-      for (size_t j = 0; j < lists[c].size(); ++j) h[(size_t)c * ld + j] = lists[c][j];
-    dsched = (int*)ctx->pool.get(sizeof(int) * h.size());
-    cudaMemcpyAsync(dsched, h.data(), sizeof(int) * h.size(), cudaMemcpyHostToDevice, ctx->stream);
-    cudaStreamSynchronize(ctx->stream);  // once per geometry: the host buffer dies here
-    ctx->pair_sched[key] = {dsched, ld};
-  }
-  launch_k(ctx->stream, k_gemm_tc2x2<3, 256>, 2 * C, 320, Cfg::SMEM, maps, args, (const int*)dsched, ld);
-  ctx->launches++;
-  for (int i = 0; i < 2; ++i) {
-    if (!part[i]) continue;
-    const GemmArgs& g = *gs[i];
-    launch_k(ctx->stream, k_splitk_reduce, 4 * ctx->sm_count, 256, 0, (const float*)part[i], args.a[i].splits, g.M,
-             g.N, g.epi, g.skip, g.lower_only);
-    ctx->launches++;
-    ctx->pool.put(part[i]);
-  }
-  return true;
 }
 
 // Narrow (N <= 32) GEMM returning raw split-K partials [splits][M][N]: the output

@@ -56,27 +56,14 @@ CV_DEV void load_slab_2sm(uint8_t* dst, const CUtensorMap* map, uint32_t bar, bo
   }
 }
 
-// Work item i of this cluster: GEMM g, work index w (tile + split x tiles).  One GEMM:
-// round robin over its items.  A scheduled pair (NG = 2): the host's LPT list for the
-// cluster, entries (g << 24) | w, terminated by -1.
-template <int NG>
-CV_DEV bool tc2_item(const TcArgs* args, const int* sched, int sched_ld, int cluster, int nclusters, int i, int& g,
-                     int& w) {
-  if constexpr (NG == 1) {
-    g = 0;
-    w = cluster + i * nclusters;
-    return w < args[0].tiles_m * args[0].tiles_n * args[0].splits;
-  } else {
-    const int v = sched[cluster * sched_ld + i];
-    if (v < 0) return false;
-    g = v >> 24;
-    w = v & 0xFFFFFF;
-    return true;
-  }
+// Work item i of this cluster: round robin over the GEMM's items.
+CV_DEV bool tc2_item(const TcArgs& a, int cluster, int nclusters, int i, int& w) {
+  w = cluster + i * nclusters;
+  return w < a.tiles_m * a.tiles_n * a.splits;
 }
 
-template <int STAGES, int TC2_BN, int NG>
-CV_DEV void tc2_body(const TcMaps* maps, const TcArgs* args, const int* sched, int sched_ld) {
+template <int STAGES, int TC2_BN>
+CV_DEV void tc2_body(const TcMaps& mp, const TcArgs& a) {
   using Cfg = Tc2Cfg<STAGES, TC2_BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -103,9 +90,8 @@ CV_DEV void tc2_body(const TcMaps* maps, const TcArgs* args, const int* sched, i
         mbar_init(&tempty[b], 16);  // 8 epilogue warps x 2 CTAs
       }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      for (int gg = 0; gg < NG; ++gg)
-        for (int sg = 0; sg < args[gg].nseg; ++sg)
-          for (int q = 0; q < 4; ++q) tma_prefetch(&maps[gg].m[sg][q]);
+      for (int sg = 0; sg < a.nseg; ++sg)
+        for (int q = 0; q < 4; ++q) tma_prefetch(&mp.m[sg][q]);
     }
   } else if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -119,18 +105,14 @@ CV_DEV void tc2_body(const TcMaps* maps, const TcArgs* args, const int* sched, i
   const uint32_t tmem = *tmem_slot;
   // the setup above touches no data of earlier kernels: it overlaps the predecessor's tail
   CV_PDL_ENTRY();
-  const bool skipped = skip_if(args[0].skip);  // identical for every GEMM of the launch and both CTAs
-  SegPlan plan[NG];
-#pragma unroll
-  for (int gg = 0; gg < NG; ++gg) plan[gg] = skipped ? SegPlan{} : seg_plan(args[gg]);
+  const bool skipped = skip_if(a.skip);  // identical for both CTAs
+  const SegPlan plan = skipped ? SegPlan{} : seg_plan(a);
 
   if (skipped) {
   } else if (warp == 0 && lane == 0) {
     // ---------------- TMA producer (both CTAs) ----------------
-    int it = 0, g, w;
-    for (int item = 0; tc2_item<NG>(args, sched, sched_ld, cluster, nclusters, item, g, w); ++item) {
-      const TcArgs& a = args[g];
-      const TcMaps& mp = maps[g];
+    int it = 0, w;
+    for (int item = 0; tc2_item(a, cluster, nclusters, item, w); ++item) {
       int mt0, n0, kb0, nkb;
       if (!tc_work(a, w, 2 * TC_BM, TC2_BN, mt0, n0, kb0, nkb)) continue;
       const int m0 = mt0 + rank * TC_BM;         // this CTA's A rows
@@ -139,7 +121,7 @@ CV_DEV void tc2_body(const TcMaps* maps, const TcArgs* args, const int* sched, i
         const int s = it % STAGES;
         if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
         int lkb;
-        const int sg = vseg(a, plan[g], kb0 + i, lkb);
+        const int sg = vseg(a, plan, kb0 + i, lkb);
         const int k0 = lkb * TC_BK;
         uint8_t* st = smem + s * Cfg::STAGE_BYTES;
         if (rank == 0) mbar_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
@@ -153,10 +135,9 @@ CV_DEV void tc2_body(const TcMaps* maps, const TcArgs* args, const int* sched, i
     }
   } else if (warp == 1 && lane == 0 && rank == 0) {
     // ---------------- MMA issuer (leader CTA) ----------------
-    int it = 0, acc_i = 0, g, w;
+    int it = 0, acc_i = 0, w;
     const uint64_t zdesc = zero_desc(zero);
-    for (int item = 0; tc2_item<NG>(args, sched, sched_ld, cluster, nclusters, item, g, w); ++item) {
-      const TcArgs& a = args[g];
+    for (int item = 0; tc2_item(a, cluster, nclusters, item, w); ++item) {
       int mt0, n0, kb0, nkb;
       if (!tc_work(a, w, 2 * TC_BM, TC2_BN, mt0, n0, kb0, nkb)) continue;
       const int ab = acc_i & 1;
@@ -169,8 +150,8 @@ CV_DEV void tc2_body(const TcMaps* maps, const TcArgs* args, const int* sched, i
         mbar_wait(&full[s], (it / STAGES) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         int lkb;
-        const int sg = vseg(a, plan[g], kb0 + i, lkb);
-        const int shift = (prev >= 0 && prev != sg) ? plan[g].S[prev] - plan[g].S[sg] : 0;
+        const int sg = vseg(a, plan, kb0 + i, lkb);
+        const int shift = (prev >= 0 && prev != sg) ? plan.S[prev] - plan.S[sg] : 0;
         prev = sg;
         const int amn = a.a[sg].kmajor ? 0 : 1, bmn = a.b[sg].kmajor ? 0 : 1;
         const uint32_t idesc = f16_idesc(2 * TC_BM, TC2_BN, amn, bmn);
@@ -190,15 +171,10 @@ CV_DEV void tc2_body(const TcMaps* maps, const TcArgs* args, const int* sched, i
     // ---------------- epilogue (both CTAs) ----------------
     const int q = warp & 3, half = (warp - 2) >> 2;
     const uint32_t tempty0[2] = {mapa_rank(&tempty[0], 0), mapa_rank(&tempty[1], 0)};
-    EpiRt rt[NG];
-#pragma unroll
-    for (int gg = 0; gg < NG; ++gg) {
-      rt[gg] = epi_prepare(args[gg].epi);
-      if (blockIdx.x == 0 && warp == 2 && lane == 0 && !args[gg].partial) epi_publish(args[gg].epi, rt[gg]);
-    }
-    int acc_i = 0, g, w;
-    for (int item = 0; tc2_item<NG>(args, sched, sched_ld, cluster, nclusters, item, g, w); ++item) {
-      const TcArgs& a = args[g];
+    const EpiRt rt = epi_prepare(a.epi);
+    if (blockIdx.x == 0 && warp == 2 && lane == 0 && !a.partial) epi_publish(a.epi, rt);
+    int acc_i = 0, w;
+    for (int item = 0; tc2_item(a, cluster, nclusters, item, w); ++item) {
       int mt0, n0, kb0, nkb;
       if (!tc_work(a, w, 2 * TC_BM, TC2_BN, mt0, n0, kb0, nkb)) continue;
       const int ab = acc_i & 1;
@@ -206,9 +182,9 @@ CV_DEV void tc2_body(const TcMaps* maps, const TcArgs* args, const int* sched, i
       mbar_wait(&tfull[ab], (acc_i >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       int lkb;
-      const int last = vseg(a, plan[g], kb0 + nkb - 1, lkb);
-      const float inv = plan[g].inv_a[last] * plan[g].inv_b[last];
-      tile_epilogue<TC2_BN>(a, maps[g], rt[g], tmem + ab * TC2_BN, mt0 + rank * TC_BM, n0,
+      const int last = vseg(a, plan, kb0 + nkb - 1, lkb);
+      const float inv = plan.inv_a[last] * plan.inv_b[last];
+      tile_epilogue<TC2_BN>(a, mp, rt, tmem + ab * TC2_BN, mt0 + rank * TC_BM, n0,
                             w / (a.tiles_m * a.tiles_n), inv, q, half, lane, stg_all + (warp - 2) * TC_STG_BYTES,
                             stg_all + 8 * TC_STG_BYTES + (warp - 2) * TC_HSTG_BYTES);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -229,24 +205,8 @@ CV_DEV void tc2_body(const TcMaps* maps, const TcArgs* args, const int* sched, i
 
 template <int STAGES, int TC2_BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
-    k_gemm_tc2(const __grid_constant__ TcMaps maps, const TcArgs a) {
-  tc2_body<STAGES, TC2_BN, 1>(&maps, &a, nullptr, 0);
-}
-
-// Two independent GEMMs in one persistent launch, the work items of both spread over
-// the clusters by the host's longest-processing-time-first schedule (gemm_pair).
-struct TcMaps2 {
-  TcMaps m[2];
-};
-struct TcArgs2 {
-  TcArgs a[2];
-};
-
-template <int STAGES, int TC2_BN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
-    k_gemm_tc2x2(const __grid_constant__ TcMaps2 maps, const __grid_constant__ TcArgs2 args, const int* sched,
-                 int sched_ld) {
-  tc2_body<STAGES, TC2_BN, 2>(maps.m, args.a, sched, sched_ld);
+    k_gemm_tc2(const __grid_constant__ TcMaps maps, const __grid_constant__ TcArgs a) {
+  tc2_body<STAGES, TC2_BN>(maps, a);
 }
 
 template <int STAGES, int TC2_BN>

@@ -155,7 +155,6 @@ struct cv_ctx {
   cudaStream_t side2 = nullptr;  // third stream: the output layer's weight gradient beside the pair
   cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
   std::vector<void*> deferred2;  // side2 scratch, returned after side_join
-  std::map<std::vector<int>, std::pair<int*, int>> pair_sched;  // gemm_pair LPT schedules (device, row length)
 };
 
 struct cv_snap {
@@ -214,7 +213,6 @@ struct cv_snap {
   // last-layer [W; b]^T (wl, ld ldw), per-product [V; Vb]^T (vl), cotangents U^T and
   // G[L-1]^T (ld ldb).  cp == c when the SIMT skinny kernels are used.
   int tc_out = 0, cp = 0;
-  int tc_dx = 0;  // output-layer backward on tensor cores (default: bandwidth kernel)
   int64_t ldw = 0, ldb = 0;
   __half* wl_hi = nullptr; __half* wl_lo = nullptr;
   __half* vl_hi = nullptr; __half* vl_lo = nullptr;
@@ -250,11 +248,21 @@ void gemm(cv_ctx* ctx, const GemmArgs& a);  // engine dispatch
 // the SMs split between them by estimated time; returns when both are enqueued
 // (the context stream waits for b)
 void gemm_pair(cv_ctx* ctx, GemmArgs a, GemmArgs b);
-bool gemm_tc_pair_fused(cv_ctx* ctx, const GemmArgs& a, const GemmArgs& b);  // one scheduled launch (false: not eligible)
 double gemm_tc_estimate(const cv_ctx* ctx, const GemmArgs& g, int ctas);  // relative time on `ctas` SMs
 cudaStream_t side_fork(cv_ctx* ctx);  // side stream ordered after the context stream's current work
 cudaStream_t side2_fork(cv_ctx* ctx); // third stream, same ordering; joined by side_join
 void side_join(cv_ctx* ctx);          // context stream waits for the side streams
+// Enqueue on another stream for a scope: restores the context stream on exit, and on an
+// exception also joins the side streams so no forked work is left unjoined.
+struct StreamSwap {
+  cv_ctx* c;
+  cudaStream_t prev;
+  int exc;
+  StreamSwap(cv_ctx* ctx, cudaStream_t s);
+  ~StreamSwap();
+  StreamSwap(const StreamSwap&) = delete;
+  StreamSwap& operator=(const StreamSwap&) = delete;
+};
 int gemm_tc_partial(cv_ctx* ctx, const GemmArgs& g, float** partial);  // N <= 32, raw split-K partials
 int gemm_tc_head_groups(const cv_ctx* ctx, const GemmArgs& g);          // 0: no fused output-layer head
 bool gemm_tc_tma_split(const cv_ctx* ctx, const GemmArgs& g);           // runs the TMA split epilogue (bits producer)
@@ -289,12 +297,6 @@ void split_flat_apply(cv_ctx* ctx, const float* x, int64_t d, const std::vector<
 bool cg_pnext_amax(cv_ctx* ctx, const float* r, const float* pre, float lam, float floor_, const double* beta,
                    const int* done, float* p, int64_t d, const std::vector<int64_t>& off, Scale* sc, Scale* zero_sc,
                    int n_zero);
-// the same direction update fused with the split of p into (hi, lo): the scale is taken
-// from the bound mr[l] + |beta| * sc[l].amax (mr: per-layer max|M^-1 r| of the update
-// kernel, sc[l].amax: the amax of the previous direction), then sc[l] = {e, amax(p)}
-void cg_pnext_split(cv_ctx* ctx, const float* r, const float* pre, float lam, float floor_, const double* beta,
-                    const int* done, float* p, int64_t d, const std::vector<int64_t>& off, const float* mr,
-                    Scale* sc, Scale* zero_sc, int n_zero, __half* hi, __half* lo);
 void split_rows(cv_ctx* ctx, const float* src, int64_t lds, int rows, int cols, const SplitBuf& dst, int ones);
 void split_mat(cv_ctx* ctx, const float* src, int64_t lds, int rows, int cols, __half* hi, __half* lo, int64_t ldd,
                int trans, Scale* sc, int amax_ready, const int* skip, int pad_cols = 0);

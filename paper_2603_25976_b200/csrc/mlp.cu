@@ -312,8 +312,7 @@ bool mlp_forward_layer(cv_ctx* ctx, cv_snap* s, int l, const SplitBuf& in, const
     }
   }
   bool wrote = false;
-  static const int bits_on = !(getenv("CURVOPT_MASK_BITS") && getenv("CURVOPT_MASK_BITS")[0] == '0');
-  if (bits && bits_on && s->act == CV_ACT_RELU && gemm_tc_tma_split(ctx, g)) {
+  if (bits && s->act == CV_ACT_RELU && gemm_tc_tma_split(ctx, g)) {
     g.epi.bits_out = bits;
     g.epi.bits_out_ld = ((s->dims[l + 1] + 15) / 16 + 7) / 8 * 8;
     wrote = true;
@@ -364,27 +363,6 @@ void mlp_loss(cv_ctx* ctx, cv_snap* s, const float* logits, int write_state, dou
 static void skinny_backward(cv_ctx* ctx, cv_snap* s, const float* U, Scale* usc, const __half* whi, const __half* wlo,
                             const Scale* wsc, const SplitBuf& out, float* raw, Scale* raw_sc, const int* skip) {
   const int l = s->L - 1;
-  if (s->tc_out && s->tc_dx && whi == s->w_hi) {
-    const __half *uh, *ul;
-    const Scale* uc = cot_split(ctx, s, U, usc, &uh, &ul, skip);
-    GemmArgs g;
-    g.M = s->bl;
-    g.N = s->dims[l];
-    g.nseg = 1;
-    // K = cp: the transposed, padded operands carry zero rows c..cp-1 (the tcgen05 K step is 16)
-    g.seg[0] = GemmSeg{mk_op(uh, ul, 1, s->ldb, uc), mk_op(s->wl_hi, s->wl_lo, s->ldw, 1, wsc + l), s->cp};
-    g.epi.mode = EPI_SPLIT_MASK;
-    g.epi.act = s->act;
-    split_epi(g.epi, out);
-    mask_epi(g.epi, s->acts[l]);
-    g.epi.raw = raw;
-    g.epi.raw_ld = out.ld;
-    g.epi.raw_amax = raw_sc ? &raw_sc->amax : nullptr;
-    bound_add(g.epi.bound, (float)s->c, uc, wsc + l);
-    g.skip = skip;
-    gemm(ctx, g);
-    return;
-  }
   SkinnyDxArgs a{};
   a.rows = s->bl;
   a.n = s->dims[l];
@@ -427,14 +405,12 @@ static GemmArgs hidden_backward_args(cv_snap* s, int l, const SplitBuf& Gl, cons
   return g;
 }
 
-// [gW; gb]_l = A_l^T G (+ A2^T G2), written into out + off[l] (hidden layers).
-// no_bias: the GEMM covers the W rows only (M = n_l) and the bias row is the
-// column sum of G (bias_colsum) -- when n_l is a multiple of the 256-row tile the
-// ones row would otherwise cost a whole extra row of tiles.
+// [gW; gb]_l = A_l^T G (+ A2^T G2), written into out + off[l] (hidden layers); the
+// ones column of A_l makes the bias gradient the GEMM's last row.
 static GemmArgs weight_grad_args(cv_snap* s, int l, const SplitBuf& G1, const SplitBuf* A2, const SplitBuf* G2,
-                                 float* out, const int* skip, bool no_bias = false) {
+                                 float* out, const int* skip) {
   GemmArgs g;
-  g.M = s->dims[l] + (no_bias ? 0 : 1);
+  g.M = s->dims[l] + 1;
   g.N = s->dims[l + 1];
   g.nseg = A2 ? 2 : 1;
   g.seg[0] = GemmSeg{op_trans(s->acts[l]), mk_op(G1.hi, G1.lo, G1.ld, 1, G1.sc), s->bl};
@@ -446,71 +422,16 @@ static GemmArgs weight_grad_args(cv_snap* s, int l, const SplitBuf& G1, const Sp
   return g;
 }
 
-// gb_l = sum over the batch rows of G_l (models.py:280-281), from its split pair:
-// row-chunk partials, then a fixed-order reduction.  Runs on the second side stream
-// beside the weight-gradient / backward GEMM pair (joined by side_join).
-constexpr int CS_RCH = 256;
-__global__ void __launch_bounds__(128) k_colsum_part(const __half* hi, const __half* lo, int64_t ld, const Scale* sc,
-                                                     int rows, int cols, float* part, const int* skip) {
-  CV_PDL_ENTRY();
-  if (skip_if(skip)) return;
-  const int c8 = (blockIdx.x * 128 + threadIdx.x) * 8;
-  if (c8 >= cols) return;
-  const int rpc = (rows + gridDim.y - 1) / gridDim.y;
-  const int r0 = blockIdx.y * rpc, r1 = min(rows, r0 + rpc);
-  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll 4
-  for (int r = r0; r < r1; ++r) {
-    H8 h, l;
-    h.u = __ldg(reinterpret_cast<const uint4*>(hi + (int64_t)r * ld + c8));
-    l.u = __ldg(reinterpret_cast<const uint4*>(lo + (int64_t)r * ld + c8));
-#pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] += __half2float(h.h[q]) + __half2float(l.h[q]);
-  }
-  const float inv = pow2f(-sc->e);
-#pragma unroll
-  for (int q = 0; q < 8; ++q) part[(int64_t)blockIdx.y * cols + c8 + q] = acc[q] * inv;
-}
-__global__ void k_colsum_final(const float* part, int nch, int cols, float* out, const int* skip) {
-  CV_PDL_ENTRY();
-  if (skip_if(skip)) return;
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= cols) return;
-  double t = 0.0;
-  for (int z = 0; z < nch; ++z) t += part[(int64_t)z * cols + c];
-  out[c] = (float)t;
-}
-
-static bool bias_apart(cv_ctx* ctx, cv_snap* s, int l) {
-  static const int off = !(getenv("CURVOPT_BIAS_APART") && getenv("CURVOPT_BIAS_APART")[0] == '1');  // opt-in
-  const int n = s->dims[l], N = s->dims[l + 1];
-  return !off && ctx->engine != CV_ENGINE_SIMT && n % 256 == 0 && N % 8 == 0;
-}
-
-static void bias_colsum(cv_ctx* ctx, cv_snap* s, int l, const SplitBuf& G, float* out, const int* skip) {
-  const int N = s->dims[l + 1];
-  cudaStream_t st = side2_fork(ctx);
-  float* part = (float*)ctx->pool.get(sizeof(float) * (size_t)CS_RCH * N);
-  launch_k(st, k_colsum_part, dim3((N / 8 + 127) / 128, CS_RCH), 128, 0, (const __half*)G.hi, (const __half*)G.lo,
-           G.ld, (const Scale*)G.sc, s->bl, N, part, skip);
-  launch_k(st, k_colsum_final, (N + 255) / 256, 256, 0, (const float*)part, CS_RCH, N,
-           out + s->off[l] + (int64_t)s->dims[l] * N, skip);
-  ctx->launches += 2;
-  ctx->deferred2.push_back(part);
-}
-
 // last layer: [gW; gb] = A^T U (+ A2^T U2)
 static void skinny_weight_grad(cv_ctx* ctx, cv_snap* s, const float* U, Scale* usc, const SplitBuf* A2,
                                const float* U2, Scale* u2sc, float* out, const int* skip, bool side = false) {
   const int l = s->L - 1;
   if (s->tc_out) {
-    static const int cosched = !(getenv("CURVOPT_COSCHED") && getenv("CURVOPT_COSCHED")[0] == '0');
-    static const int side_ctas = getenv("CURVOPT_DWL_CTAS") ? atoi(getenv("CURVOPT_DWL_CTAS")) : 128;
     // beside the output-layer backward: the cotangent split and the GEMM both go to the
-    // second side stream (the caller joins it); not with tc_dx, whose backward reuses U's split
-    const bool on_side = side && cosched && side_ctas > 0 && ctx->engine != CV_ENGINE_SIMT && !s->tc_dx;
-    cudaStream_t main_stream = ctx->stream;
-    if (on_side) ctx->stream = side2_fork(ctx);
+    // second side stream (the caller joins it) on 128 CTAs (measured best at C3)
+    constexpr int side_ctas = 128;
+    const bool on_side = side && ctx->engine != CV_ENGINE_SIMT;
+    StreamSwap swap(ctx, on_side ? side2_fork(ctx) : ctx->stream);
     const __half *uh, *ul, *u2h = nullptr, *u2l = nullptr;
     const Scale* uc = cot_split(ctx, s, U, usc, &uh, &ul, skip);
     const Scale* u2c = nullptr;
@@ -530,7 +451,6 @@ static void skinny_weight_grad(cv_ctx* ctx, cv_snap* s, const float* U, Scale* u
       g.max_ctas = side_ctas;
     }
     gemm(ctx, g);
-    ctx->stream = main_stream;
     return;
   }
   SkinnyDwArgs a{};
@@ -551,12 +471,10 @@ static void skinny_weight_grad(cv_ctx* ctx, cv_snap* s, const float* U, Scale* u
 void mlp_linearize(cv_ctx* ctx, cv_snap* s, double* loss_out, float* grad_out) {
   const int L = s->L;
   int head_groups = 0;
-  static const int fwd_head = !(getenv("CURVOPT_FWD_HEAD") && getenv("CURVOPT_FWD_HEAD")[0] == '0');
-  for (int l = 0; l < L - 1; ++l)
-  {
+  for (int l = 0; l < L - 1; ++l) {
     SplitBuf& o = s->acts[l + 1];
     const bool wrote = mlp_forward_layer(ctx, s, l, s->acts[l], s->w_hi, s->w_lo, s->w_sc, o, s->bits_buf[l + 1],
-                                         fwd_head ? &head_groups : nullptr, s->wl_f32);
+                                         &head_groups, s->wl_f32);
     o.bits = wrote ? s->bits_buf[l + 1] : nullptr;
     o.bits_ld = wrote ? ((s->dims[l + 1] + 15) / 16 + 7) / 8 * 8 : 0;
   }
@@ -582,18 +500,12 @@ void mlp_linearize(cv_ctx* ctx, cv_snap* s, double* loss_out, float* grad_out) {
                                                tanh_ ? s->P[l - 1] : nullptr, tanh_ ? s->P_sc[l - 1] : nullptr,
                                                nullptr);
       if (grad_out) {
-        const bool nb = bias_apart(ctx, s, l);
-        if (nb) bias_colsum(ctx, s, l, s->G[l], grad_out, nullptr);
-        gemm_pair(ctx, dx, weight_grad_args(s, l, s->G[l], nullptr, nullptr, grad_out, nullptr, nb));
+        gemm_pair(ctx, dx, weight_grad_args(s, l, s->G[l], nullptr, nullptr, grad_out, nullptr));
       } else {
         gemm(ctx, dx);
       }
     }
-    if (grad_out) {
-      const bool nb = bias_apart(ctx, s, 0);
-      if (nb) bias_colsum(ctx, s, 0, s->G[0], grad_out, nullptr);
-      gemm(ctx, weight_grad_args(s, 0, s->G[0], nullptr, nullptr, grad_out, nullptr, nb));
-    }
+    if (grad_out) gemm(ctx, weight_grad_args(s, 0, s->G[0], nullptr, nullptr, grad_out, nullptr));
     side_join(ctx);
   }
   if (grad_out && ctx->nccl) allreduce_f32(ctx, grad_out, s->d);
@@ -602,10 +514,6 @@ void mlp_linearize(cv_ctx* ctx, cv_snap* s, double* loss_out, float* grad_out) {
 // split of a product input v into v_hi / v_lo (per-layer exponents); also
 // zeroes this product's amax slots
 static void split_input(cv_ctx* ctx, cv_snap* s, const float* v, const int* skip) {
-  if (s->v_ready == 2) {  // split and scales written by the CG direction update itself
-    s->v_ready = 0;
-    return;
-  }
   if (s->v_ready) {  // scales already published (and slots zeroed) by the fused CG update
     split_flat_apply(ctx, v, s->d, s->off, s->v_hi, s->v_lo, s->v_sc, skip);
     s->v_ready = 0;
@@ -672,7 +580,6 @@ static void jvp_out(cv_ctx* ctx, cv_snap* s, int post, float scale, float* out, 
   if (head_groups > 0) {
     // the last hidden GEMM left per-group partials of z = J v: add the bias row
     // [Vb]_{L-1} and reduce in fixed order (+ H_z)
-    if (s->tc_out && s->tc_dx) pad_last(ctx, s, s->v_hi, s->v_lo, s->vl_hi, s->vl_lo, skip);  // vl for the HVP backward
     const float* bias = v + s->off[l] + (int64_t)s->dims[l] * s->c;
     launch_k(ctx->stream, k_out_reduce<16>, (s->bl + 31) / 32, 128, 0, (const float*)s->head_part, head_groups, s->bl,
              s->c, post == POST_HZ ? 1 : 0, s->loss, (const float*)s->probs, scale, out, out_amax, skip, bias);
@@ -732,9 +639,7 @@ static void vjp_from(cv_ctx* ctx, cv_snap* s, const float* U, Scale* usc, float*
   if (L >= 2) {
     skinny_backward(ctx, s, U, usc, s->w_hi, s->w_lo, s->w_sc, s->gs[L - 2], nullptr, nullptr, skip);
     for (int l = L - 2; l >= 0; --l) {
-      const bool nb = bias_apart(ctx, s, l);
-      if (nb) bias_colsum(ctx, s, l, s->gs[l], out, skip);
-      const GemmArgs dw = weight_grad_args(s, l, s->gs[l], nullptr, nullptr, out, skip, nb);
+      const GemmArgs dw = weight_grad_args(s, l, s->gs[l], nullptr, nullptr, out, skip);
       if (l > 0)
         gemm_pair(ctx, hidden_backward_args(s, l, s->gs[l], s->w_hi, s->w_lo, s->w_sc, s->gs[l - 1], nullptr, nullptr,
                                             skip),
@@ -797,22 +702,7 @@ void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* v, float* out, const int* ski
   if (L >= 2) {
     // dG_{L-2} = (dG W^T + G_{L-1} V^T) * sp + [tanh] P * spp * dz
     const int l = L - 1;
-    if (s->tc_out && s->tc_dx) {
-      // U's split was made by skinny_weight_grad, vl by jvp_out
-      GemmArgs g;
-      g.M = s->bl;
-      g.N = s->dims[l];
-      g.nseg = 2;
-      g.seg[0] = GemmSeg{mk_op(s->U_hi, s->U_lo, 1, s->ldb, s->U_sc), mk_op(s->wl_hi, s->wl_lo, s->ldw, 1, s->w_sc + l),
-                         s->cp};
-      g.seg[1] = GemmSeg{mk_op(s->gout_hi, s->gout_lo, 1, s->ldb, s->gout_sc),
-                         mk_op(s->vl_hi, s->vl_lo, s->ldw, 1, s->v_sc + l), s->cp};
-      hvp_epi(s, g.epi, l);
-      bound_add(g.epi.bound, (float)s->c, s->U_sc, s->w_sc + l);
-      bound_add(g.epi.bound, (float)s->c, s->gout_sc, s->v_sc + l);
-      g.skip = skip;
-      gemm(ctx, g);
-    } else {
+    {
       SkinnyDxArgs a{};
       a.rows = s->bl;
       a.n = s->dims[l];
@@ -833,10 +723,8 @@ void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* v, float* out, const int* ski
       skinny_dx(ctx, a);
     }
     for (int h = L - 2; h >= 0; --h) {
-      const bool nb = bias_apart(ctx, s, h);
-      if (nb) bias_colsum(ctx, s, h, s->gs[h], out, skip);  // the [da|0] segment adds nothing to the bias row
       const GemmArgs dw = weight_grad_args(s, h, s->gs[h], h > 0 ? &s->da[h - 1] : nullptr, h > 0 ? &s->G[h] : nullptr,
-                                           out, skip, nb);
+                                           out, skip);
       if (h > 0) {
         GemmArgs g;
         g.M = s->bl;
@@ -887,11 +775,9 @@ void mlp_loss_at(cv_ctx* ctx, cv_snap* s, const float* w, double* loss_out) {
   const int L = s->L;
   const SplitBuf* in = &s->acts[0];
   int head_groups = 0;
-  static const int fwd_head = !(getenv("CURVOPT_FWD_HEAD") && getenv("CURVOPT_FWD_HEAD")[0] == '0');
   const float* wl = w + s->off[L - 1];
   for (int l = 0; l < L - 1; ++l) {
-    mlp_forward_layer(ctx, s, l, *in, s->v_hi, s->v_lo, s->v_sc, s->gs[l], nullptr, fwd_head ? &head_groups : nullptr,
-                      wl);
+    mlp_forward_layer(ctx, s, l, *in, s->v_hi, s->v_lo, s->v_sc, s->gs[l], nullptr, &head_groups, wl);
     in = &s->gs[l];
   }
   if (head_groups > 0) {

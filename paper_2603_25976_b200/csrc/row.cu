@@ -533,8 +533,7 @@ int row_solve_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, flo
   // (all but O(m^2 CH_NBO) of the m^3/3 flops) runs on the tensor-core engine with L21
   // as a scaled fp16 pair.  The fp64 iterative refinement below absorbs the split's
   // rounding (cf. the 1e-6 lane-equivalence bound, tests/test_solvers.py:216-236).
-  static const int nbo_env = getenv("CURVOPT_CHOL_NBO") ? atoi(getenv("CURVOPT_CHOL_NBO")) : 512;
-  const int NBO = nbo_env >= CH_NB ? nbo_env / CH_NB * CH_NB : CH_NB;
+  constexpr int NBO = 512;  // panel width (a multiple of CH_NB)
   const bool tc = ctx->engine != CV_ENGINE_SIMT && m > NBO;
   __half* l21h = nullptr;
   __half* l21l = nullptr;

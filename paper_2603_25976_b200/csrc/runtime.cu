@@ -4,6 +4,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <exception>
 #include <stdexcept>
 
 #include "common.cuh"
@@ -138,19 +139,9 @@ void check_launch(cv_ctx* ctx) {
 // GEMM engine dispatch: tensor-core (tcgen05, 3xTF32) where the operand
 // geometry allows TMA, exact-fp32 SIMT otherwise.
 // ---------------------------------------------------------------------------
-// side-stream priority: CURVOPT_SIDE_PRIO = 0 (default, same as a default stream) or
-// "hi" (the device's greatest priority)
-static int side_priority() {
-  const char* e = getenv("CURVOPT_SIDE_PRIO");
-  if (!e || strcmp(e, "hi") != 0) return 0;
-  int least = 0, greatest = 0;
-  cudaDeviceGetStreamPriorityRange(&least, &greatest);
-  return greatest;
-}
-
 static void ensure_side(cv_ctx* ctx) {
   if (ctx->side) return;
-  if (cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, side_priority()) != cudaSuccess ||
+  if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess)
     throw std::runtime_error("CUDA: cannot create the side stream");
@@ -165,7 +156,7 @@ cudaStream_t side_fork(cv_ctx* ctx) {
 
 cudaStream_t side2_fork(cv_ctx* ctx) {
   if (!ctx->side2) {
-    if (cudaStreamCreateWithPriority(&ctx->side2, cudaStreamNonBlocking, side_priority()) != cudaSuccess ||
+    if (cudaStreamCreateWithFlags(&ctx->side2, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_fork2, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_join2, cudaEventDisableTiming) != cudaSuccess)
       throw std::runtime_error("CUDA: cannot create the second side stream");
@@ -189,15 +180,27 @@ void side_join(cv_ctx* ctx) {
   ctx->deferred.clear();
 }
 
+StreamSwap::StreamSwap(cv_ctx* ctx, cudaStream_t s) : c(ctx), prev(ctx->stream), exc(std::uncaught_exceptions()) {
+  ctx->stream = s;
+}
+
+StreamSwap::~StreamSwap() {
+  c->stream = prev;
+  if (std::uncaught_exceptions() > exc) {
+    try {
+      side_join(c);
+    } catch (...) {
+    }
+  }
+}
+
 void gemm_pair(cv_ctx* ctx, GemmArgs a, GemmArgs b) {
-  static const int off = getenv("CURVOPT_COSCHED") && getenv("CURVOPT_COSCHED")[0] == '0';
   const bool tc = ctx->engine != CV_ENGINE_SIMT && gemm_tc_supported(a) && gemm_tc_supported(b);
-  if (off || !tc) {
+  if (!tc) {
     gemm(ctx, a);
     gemm(ctx, b);
     return;
   }
-  if (gemm_tc_pair_fused(ctx, a, b)) return;
   ensure_side(ctx);
   // SM split minimising the slower of the two (even counts: CTA pairs)
   const int sms = ctx->sm_count;
@@ -211,8 +214,6 @@ void gemm_pair(cv_ctx* ctx, GemmArgs a, GemmArgs b) {
       best = ca;
     }
   }
-  static const int force_split = getenv("CURVOPT_PAIR_SPLIT") ? atoi(getenv("CURVOPT_PAIR_SPLIT")) : 0;
-  if (force_split >= 16 && force_split <= sms - 16) best = force_split & ~1;  // experiments
   a.max_ctas = best;
   b.max_ctas = sms - best;
   a.stream = ctx->stream;
@@ -232,8 +233,6 @@ void gemm(cv_ctx* ctx, const GemmArgs& a) {
     gemm_tc(ctx, a);
     return;
   }
-  if (ctx->engine == CV_ENGINE_TC && getenv("CURVOPT_TC_STRICT"))
-    throw std::runtime_error("tensor-core engine requested but GEMM shape unsupported");
   gemm_simt(ctx, a);
 }
 

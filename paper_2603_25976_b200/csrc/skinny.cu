@@ -416,9 +416,8 @@ __global__ void __launch_bounds__(256, 2) k_dx_wide(SkinnyDxArgs a, int rows_per
 }
 
 static bool dx_wide_ok(const SkinnyDxArgs& a) {
-  static const int off = getenv("CURVOPT_DX_WIDE") && getenv("CURVOPT_DX_WIDE")[0] == '0';
   const Epilogue& e = a.epi;
-  return !off && a.nseg == 1 && a.c <= DXW_C && (a.n & 7) == 0 && a.n <= 1024 && a.n >= 64 &&
+  return a.nseg == 1 && a.c <= DXW_C && (a.n & 7) == 0 && a.n <= 1024 && a.n >= 64 &&
          e.mode == EPI_SPLIT_MASK && e.act == CV_ACT_RELU && !e.raw && e.mask_div == 1 && (e.ld & 7) == 0 &&
          (e.mask_ld & 7) == 0 && !(((uintptr_t)e.out_hi | (uintptr_t)e.out_lo | (uintptr_t)e.mask_hi) & 15);
 }
@@ -435,9 +434,7 @@ static void launch_dx(cv_ctx* ctx, const SkinnyDxArgs& a) {
 
 void skinny_dx(cv_ctx* ctx, const SkinnyDxArgs& a) {
   if (dx_wide_ok(a)) {
-    static const int dx_bits = !(getenv("CURVOPT_DX_BITS") && getenv("CURVOPT_DX_BITS")[0] == '0');
-    SkinnyDxArgs b = a;
-    if (!dx_bits) b.epi.mask_bits = nullptr;
+    const SkinnyDxArgs& b = a;
     // contiguous row ranges, 2 resident 256-thread blocks per SM
     const int blocks = 2 * ctx->sm_count;
     const int rpb = (a.rows + blocks - 1) / blocks;

@@ -40,7 +40,7 @@ CV_DEV bool last_block(unsigned* counter) {
 // block maxima -> part; the grid's last block reduces them and publishes sc[l]
 // (and zeroes the zero_sc block of Scale slots).
 CV_DEV void flat_amax_finish(const OffTab& t, int* smax, float* sh, float* part, unsigned* counter, Scale* sc,
-                             Scale* zero_sc, int n_zero, const int* e_fixed = nullptr) {
+                             Scale* zero_sc, int n_zero) {
   __syncthreads();
   if (threadIdx.x < t.L) part[blockIdx.x * SP_MAXL + threadIdx.x] = __int_as_float(smax[threadIdx.x]);
   if (!last_block(counter)) return;
@@ -50,7 +50,7 @@ CV_DEV void flat_amax_finish(const OffTab& t, int* smax, float* sh, float* part,
     mm = block_max(mm, sh);
     if (threadIdx.x == 0) {
       sc[l2].amax = mm;
-      sc[l2].e = e_fixed ? e_fixed[l2] : exp_for_bound(mm);
+      sc[l2].e = exp_for_bound(mm);
     }
   }
   for (int i = threadIdx.x; i < n_zero; i += blockDim.x) {
@@ -164,88 +164,6 @@ __global__ void __launch_bounds__(SP_NT) k_cg_pnext_amax(const float* __restrict
   flat_amax_finish(t, smax, sh, part, counter, sc, zero_sc, n_zero);
 }
 
-// k_cg_pnext_amax fused with the split of the new direction: every block derives the
-// same per-layer exponent from the bound |M^-1 r + beta p| <= mr[l] + |beta| amax(p_old)
-// (mr: the update kernel's per-layer max|M^-1 r|; the (1 + 2^-20) slack covers the fp32
-// rounding of the direction), splits p as it is produced, and the last block publishes
-// sc[l] = {that exponent, the true amax of p} (the next bound's amax(p_old)).  The bound
-// is at most a factor (1 + |beta| amax_old / amax_new) above amax(p): the exponent is
-// exact or one binade low, so the split keeps its range guarantee and loses at most one
-// bit of the 22 it carries.
-__global__ void __launch_bounds__(SP_NT) k_cg_pnext_split(const float* __restrict__ r, const float* __restrict__ pre,
-                                                          float lam, float floor_, const double* beta_p,
-                                                          const int* done, float* __restrict__ p, OffTab t,
-                                                          const float* mr, float* part, unsigned* counter, Scale* sc,
-                                                          Scale* zero_sc, int n_zero, __half* __restrict__ hi,
-                                                          __half* __restrict__ lo) {
-  CV_PDL_ENTRY();
-  if (*(volatile const int*)done) return;
-  __shared__ float sh[SP_NT / 32];
-  __shared__ int smax[SP_MAXL], se[SP_MAXL];
-  __shared__ float ssc[SP_MAXL];
-  const float beta = (float)*beta_p;
-  if (threadIdx.x < SP_MAXL) {
-    smax[threadIdx.x] = 0;
-    if (threadIdx.x < t.L) {
-      // every block reads sc before its partials count towards the last block's publish
-      const float B = (__ldcg(mr + threadIdx.x) + fabsf(beta) * __ldcg(&sc[threadIdx.x].amax)) * (1.f + 0x1p-20f);
-      const int e = exp_for_bound(B);
-      se[threadIdx.x] = e;
-      ssc[threadIdx.x] = pow2f(e);
-    }
-  }
-  __syncthreads();
-  const int64_t d = t.off[t.L];
-  int l = 0;
-  float m = 0.f;
-  auto take = [&](int64_t i, float v) {
-    if (i >= t.off[l + 1]) {
-      atomicMax(&smax[l], __float_as_int(m));
-      m = 0.f;
-      while (i >= t.off[l + 1]) ++l;
-    }
-    m = fmaxf(m, fabsf(v));
-    return ssc[l];
-  };
-  auto minv = [&](int64_t i) { return pre ? 1.f / (fmaxf(pre[i], floor_) + lam) : 1.f; };
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
-  const int64_t nq = d >> 2;
-  const bool pre4 = pre && !((uintptr_t)pre & 15);
-  for (int64_t q = tid; q < nq; q += nth) {
-    const int64_t i = 4 * q;
-    const float4 r4 = *reinterpret_cast<const float4*>(r + i);
-    float4 p4 = *reinterpret_cast<const float4*>(p + i);
-    float4 m4 = make_float4(1.f, 1.f, 1.f, 1.f);
-    if (pre4) {
-      m4 = *reinterpret_cast<const float4*>(pre + i);
-      m4.x = 1.f / (fmaxf(m4.x, floor_) + lam);
-      m4.y = 1.f / (fmaxf(m4.y, floor_) + lam);
-      m4.z = 1.f / (fmaxf(m4.z, floor_) + lam);
-      m4.w = 1.f / (fmaxf(m4.w, floor_) + lam);
-    } else if (pre) {
-      m4 = make_float4(minv(i), minv(i + 1), minv(i + 2), minv(i + 3));
-    }
-    p4.x = m4.x * r4.x + beta * p4.x;
-    p4.y = m4.y * r4.y + beta * p4.y;
-    p4.z = m4.z * r4.z + beta * p4.z;
-    p4.w = m4.w * r4.w + beta * p4.w;
-    *reinterpret_cast<float4*>(p + i) = p4;
-    union { uint2 u; __half h[4]; } H, Lo;
-    split16(p4.x, take(i, p4.x), H.h[0], Lo.h[0]);
-    split16(p4.y, take(i + 1, p4.y), H.h[1], Lo.h[1]);
-    split16(p4.z, take(i + 2, p4.z), H.h[2], Lo.h[2]);
-    split16(p4.w, take(i + 3, p4.w), H.h[3], Lo.h[3]);
-    *reinterpret_cast<uint2*>(hi + i) = H.u;
-    *reinterpret_cast<uint2*>(lo + i) = Lo.u;
-  }
-  for (int64_t i = 4 * nq + tid; i < d; i += nth) {
-    const float v = minv(i) * r[i] + beta * p[i];
-    p[i] = v;
-    split16(v, take(i, v), hi[i], lo[i]);
-  }
-  atomicMax(&smax[l], __float_as_int(m));
-  flat_amax_finish(t, smax, sh, part, counter, sc, zero_sc, n_zero, se);
-}
 
 __global__ void __launch_bounds__(SP_NT) k_flat_split(const float* __restrict__ x, OffTab t, const Scale* sc,
                                                       __half* __restrict__ hi, __half* __restrict__ lo,
@@ -315,13 +233,6 @@ bool cg_pnext_amax(cv_ctx* ctx, const float* r, const float* pre, float lam, flo
   return true;
 }
 
-void cg_pnext_split(cv_ctx* ctx, const float* r, const float* pre, float lam, float floor_, const double* beta,
-                    const int* done, float* p, int64_t d, const std::vector<int64_t>& off, const float* mr,
-                    Scale* sc, Scale* zero_sc, int n_zero, __half* hi, __half* lo) {
-  launch_k(ctx->stream, k_cg_pnext_split, SP_NB, SP_NT, 0, r, pre, lam, floor_, beta, done, p, off_tab(off, d), mr,
-           part_of(ctx), counter_of(ctx), sc, zero_sc, n_zero, hi, lo);
-  ctx->launches++;
-}
 
 // ---------------------------------------------------------------------------
 // 2-D splits: [rows x cols] fp32 (ld lds) -> split (ld ldd), optionally

@@ -572,38 +572,20 @@ CV_DEV void pap_final_body(const double* ws, CgDev* st, int k, int stab) {
     st->gv_skip = st->done || !stab;
   }
 }
-// plain iteration: x += a p; r -= a Ap; partials ||r||^2, r.M^-1 r.  TRACK: also the
-// per-layer max|M^-1 r| (block maxima in mpart, reduced by the last block into mr) for
-// the bound-scaled split of the next direction (k_cg_pnext_split).
-template <bool TRACK>
+// plain iteration: x += a p; r -= a Ap; partials ||r||^2, r.M^-1 r
 __global__ void k_cg_update(float* x, float* r, const float* p, const float* ap, const float* pre, float lam,
                             float floor_, CgDev* st, int64_t d, double* ws, unsigned* ctr, int k, int maxiter,
-                            double tol, OffTab ot, float* mpart, float* mr) {
+                            double tol) {
   CV_PDL_ENTRY();
   if (st->done) return;
   const float a = (float)st->alpha;
   double t[2] = {0.0, 0.0};
-  __shared__ int smax[kOffTabMax];
-  if constexpr (TRACK) {
-    if (threadIdx.x < kOffTabMax) smax[threadIdx.x] = 0;
-    __syncthreads();
-  }
-  int l = 0;
-  float m = 0.f;
   auto body = [&](int64_t i, float& xi, float& ri, float pi, float api) {
     xi += a * pi;
     ri -= a * api;
     const float z = minv_of(pre, i, lam, floor_) * ri;
     t[0] += (double)ri * ri;
     t[1] += (double)ri * z;
-    if constexpr (TRACK) {
-      if (i >= ot.off[l + 1]) {
-        atomicMax(&smax[l], __float_as_int(m));
-        m = 0.f;
-        while (i >= ot.off[l + 1]) ++l;
-      }
-      m = fmaxf(m, fabsf(z));
-    }
   };
   const int64_t nq = d >> 2;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
@@ -621,30 +603,8 @@ __global__ void k_cg_update(float* x, float* r, const float* p, const float* ap,
     x[i] = xi;
     r[i] = ri;
   }
-  if constexpr (TRACK) {
-    atomicMax(&smax[l], __float_as_int(m));
-    __syncthreads();
-    if (threadIdx.x < ot.L) mpart[blockIdx.x * kOffTabMax + threadIdx.x] = __int_as_float(smax[threadIdx.x]);
-  }
   write_partials<2>(ws, t);
-  if (grid_last(ctr)) {
-    r_final_body(ws, st, k, maxiter, 0, tol);
-    if constexpr (TRACK) {
-      __shared__ float smx[NT / 32];
-      for (int l2 = 0; l2 < ot.L; ++l2) {
-        float mm = 0.f;
-        for (int b = threadIdx.x; b < NB; b += NT) mm = fmaxf(mm, __ldcg(mpart + b * kOffTabMax + l2));
-        mm = warp_max_f(mm);
-        if ((threadIdx.x & 31) == 0) smx[threadIdx.x >> 5] = mm;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          for (int w = 0; w < NT / 32; ++w) mm = fmaxf(mm, smx[w]);
-          mr[l2] = mm;
-        }
-        __syncthreads();
-      }
-    }
-  }
+  if (grid_last(ctr)) r_final_body(ws, st, k, maxiter, 0, tol);
 }
 // stabilising iteration: x += a p (the explicit residual product follows)
 __global__ void k_cg_xupdate(float* x, const float* p, const CgDev* st, int64_t d) {
@@ -767,14 +727,8 @@ void cg_solve(cv_ctx* ctx, cv_snap* s, int kind, const float* g, double lam, dou
   launch_k(sm, k_cg_p0_final, 1, NT, 0, ws, st);
   ctx->launches += 4;
   unsigned* ctr = ctx->amax_counter + 1;
-  // CURVOPT_CG_SPLIT_FUSED=1: the direction update also writes its split (bound-derived
-  // exponent); default: a separate split pass with the exact amax (no measured gain at C3)
-  static const bool split_fused = getenv("CURVOPT_CG_SPLIT_FUSED") && getenv("CURVOPT_CG_SPLIT_FUSED")[0] == '1';
-  const OffTab ot = make_off_tab(s->off, d);
-  float* mr = ctx->amax_ws + kAmaxWsFloats;
   for (int k = 1; k <= maxiter; ++k) {
     const int is_stab = (stab > 0 && k % stab == 0) ? 1 : 0;
-    bool fuse_split = false;
     mv(ctx, s, p, ap, &st->done);
     launch_k(sm, k_cg_pap, NB, NT, 0, ap, p, flam, st, d, ws, ctr, k, is_stab);
     ctx->launches++;
@@ -784,24 +738,10 @@ void cg_solve(cv_ctx* ctx, cv_snap* s, int kind, const float* g, double lam, dou
       mv(ctx, s, x, ap, &st->gv_skip);
       launch_k(sm, k_cg_rstab, NB, NT, 0, g, ap, x, r, precond, flam, ffl, st, d, ws, ctr, k, maxiter, tol);
     } else {
-      // the next direction's split rides on its update when the bound source (v_sc = the
-      // amax of this iteration's direction) was not overwritten by a stabilising product
-      fuse_split = split_fused && k < maxiter && (int)s->off.size() <= kOffTabMax;
-      if (fuse_split)
-        launch_k(sm, k_cg_update<true>, NB, NT, 0, x, r, p, ap, precond, flam, ffl, st, d, ws, ctr, k, maxiter, tol,
-                 ot, ctx->amax_ws, mr);
-      else
-        launch_k(sm, k_cg_update<false>, NB, NT, 0, x, r, p, ap, precond, flam, ffl, st, d, ws, ctr, k, maxiter, tol,
-                 ot, nullptr, nullptr);
+      launch_k(sm, k_cg_update, NB, NT, 0, x, r, p, ap, precond, flam, ffl, st, d, ws, ctr, k, maxiter, tol);
     }
     ctx->launches++;
     if (k == maxiter) break;  // the direction of a last iteration is never used
-    if (fuse_split) {
-      cg_pnext_split(ctx, r, precond, flam, ffl, &st->alpha, &st->done, p, d, s->off, mr, s->v_sc, s->prod_sc,
-                     s->n_prod, s->v_hi, s->v_lo);
-      s->v_ready = 2;
-      continue;
-    }
     // p <- M^-1 r + beta p, fused with the next product's input scales
     if (cg_pnext_amax(ctx, r, precond, flam, ffl, &st->alpha, &st->done, p, d, s->off, s->v_sc, s->prod_sc, s->n_prod)) {
       s->v_ready = 1;

@@ -32,7 +32,8 @@ from curvopt.models import Batch, Model, init_params, linearize  # noqa: E402
 from curvopt.control import TrustRegionConfig  # noqa: E402
 from curvopt.solvers import CgConfig, cg_solve, row_solve_cholesky  # noqa: E402
 from curvopt.telemetry import hutchinson_diag, hutchinson_trace, power_iter_top_eig  # noqa: E402
-from curvopt.transforms import scale  # noqa: E402
+from curvopt.transforms import (add_decayed_weights, chain_apply, chain_init, clip_global_norm,  # noqa: E402
+                                scale, scale_by_adam, scale_by_schedule, sophia_clip, trace_momentum)
 
 
 def save(name, **arrays):
@@ -252,8 +253,150 @@ def plan_cases():
     print("wrote plans.json")
 
 
+def primitive_tc_cases():
+    """Batch >= 128 and widths >= 64: every GEMM of the linearization, the GGN product and
+    the HVP runs on the tensor-core engine (M >= 64, 16-byte rows), and the output layer
+    takes the transposed tensor-core path (c >= 8, b >= 128)."""
+    out = {}
+    cfgs = [
+        ("relu_ce", Model(64, (96, 64), 10, "relu"), "ce", 128),
+        ("tanh_ce", Model(64, (96, 64), 10, "tanh"), "ce", 128),
+        ("relu_mse", Model(64, (128,), 8, "relu"), "mse", 192),
+        ("tanh_mse", Model(64, (64, 64), 8, "tanh"), "mse", 128),
+    ]
+    for name, m, loss, b in cfgs:
+        w = init_params(m, N.Rng(0))
+        batch = batch_for(m, b, loss)
+        lin = linearize(m, w, batch)
+        d = w.dim
+        v = w.like(N.Rng(2).normal(d))
+        U = N.Rng(3).normal(b * m.output_dim).reshape(b, m.output_dim)
+        kind = "ggn_ce" if loss == "ce" else "ggn_mse"
+        snap = make_snapshot(kind, m, w, batch)
+        hsnap = make_snapshot("hessian", m, w, batch)
+        cfg = CgConfig(tol=1e-5, maxiter=10, stabilise_every=3, warm_start=True)
+        res = cg_solve(snap.matvec, snap.grad, 0.5, cfg)
+        hres = cg_solve(hsnap.matvec, snap.grad, 2.0, cfg)
+        mv = lambda x: snap.matvec(w.like(x)).data  # noqa: E731
+        rng = N.Rng(5)
+        hd = hutchinson_diag(mv, rng, d, 2)
+        ht = hutchinson_trace(mv, rng, d, 2)
+        out.update({
+            f"{name}/dims": np.array(m.dims), f"{name}/act": np.array(m.activation),
+            f"{name}/loss": np.array(loss), f"{name}/w": w.data, f"{name}/X": batch.inputs,
+            f"{name}/y": batch.targets, f"{name}/v": v.data, f"{name}/U": U,
+            f"{name}/value": np.array(lin.loss), f"{name}/grad": lin.grad.data,
+            f"{name}/out": lin.out, f"{name}/jvp": lin.jvp(v), f"{name}/vjp": lin.vjp(U).data,
+            f"{name}/ggn": snap.matvec(v).data, f"{name}/hvp": hsnap.matvec(v).data,
+            f"{name}/cg_x": res.direction.data,
+            f"{name}/cg_stats": np.array([res.iterations, res.converged, res.final_relative_residual], dtype=np.float64),
+            f"{name}/hcg_x": hres.direction.data,
+            f"{name}/hcg_stats": np.array([hres.iterations, hres.converged, hres.final_relative_residual,
+                                           hres.negative_curvature], dtype=np.float64),
+            f"{name}/hutch_diag": hd, f"{name}/hutch_trace": np.array(ht),
+            f"{name}/loss_at": np.array(snap.loss_at(w.like(w.data + 0.01 * v.data))),
+        })
+    save("primitives_tc", **out)
+
+
+CHAINS = {
+    "sophia": lambda: (trace_momentum(0.96), sophia_clip(0.05, 1e-12), add_decayed_weights(1e-4),
+                       scale_by_schedule("constant", alpha0=0.01), scale(-1.0)),
+    "adam": lambda: (scale_by_adam(0.9, 0.999, 1e-8), scale_by_schedule("constant", alpha0=1e-3), scale(-1.0)),
+    "sgdm": lambda: (trace_momentum(0.9), add_decayed_weights(5e-4), scale_by_schedule("constant", alpha0=0.05),
+                     scale(-1.0)),
+    "clip_cos": lambda: (clip_global_norm(0.5), scale_by_schedule("cosine_warmup", alpha0=0.3, warmup=2, total=6),
+                         trace_momentum(0.5), clip_global_norm(0.05), scale(-2.0)),
+    "step_decay": lambda: (scale_by_schedule("step_decay", alpha0=0.2, gamma=0.5, period=2), scale(-1.0)),
+}
+
+
+def chain_cases():
+    """The reference's transform chains (transforms.py:148-199) over 4 steps of random
+    directions: update and the threaded state per step."""
+    out = {}
+    d = 3001
+    lay = (("w", (d,)),)
+    for name, mk in CHAINS.items():
+        chain = mk()
+        w = N.ParamVector(N.Rng(11).normal(d), lay)
+        pre = N.ParamVector(np.abs(N.Rng(12).normal(d)) * 1e-2, lay)
+        st = chain_init(chain, w)
+        for t in range(4):
+            direc = N.ParamVector(N.Rng(20 + t).normal(d) * (3.0 if t == 1 else 1.0), lay)
+            upd, st = chain_apply(chain, st, direc, w, t, precond_diag=pre)
+            out[f"{name}/upd{t}"] = upd.data
+            for i, s in enumerate(st):
+                for key, val in s.items():
+                    out[f"{name}/st{t}_{i}_{key}"] = np.asarray(val, dtype=np.float64)
+            w = w + upd
+        out[f"{name}/w0"] = N.Rng(11).normal(d)
+        out[f"{name}/pre"] = pre.data
+    save("chains", **out)
+
+
+def gnb_cases():
+    """Sampled-label GNB diagonal (telemetry.py:129-160) and the Sophia-G / AdaHessian /
+    Adam / SGDM presets over a few steps (device transform chains through Method.step)."""
+    from curvopt.method import make
+    from curvopt.telemetry import gnb_diag
+
+    out = {}
+    m = Model(64, (96, 64), 10, "relu")
+    w = init_params(m, N.Rng(0))
+    batch = batch_for(m, 128, "ce")
+    rng = N.Rng(7)
+    out["gnb/diag"] = gnb_diag(m, w, batch, rng, 3).data
+    out["gnb/rng_after"] = np.array([rng.counter], dtype=np.int64)
+    for preset in ("sophia_g", "sophia_h", "sophia_n", "adahessian", "adam", "sgdm", "sgd"):
+        meth = make(preset, m)
+        st = meth.init(w, 0)
+        ww = w
+        rows = []
+        for t in range(4):
+            ww, st, info = meth.step(ww, batch_for(m, 128, "ce", seed=1 + t), st)
+            rows.append(info.to_row())
+        out[f"{preset}/info"] = np.array(rows, dtype=np.float64)
+        out[f"{preset}/w_final"] = ww.data
+    save("gnb_presets", **out)
+
+
+def harness_cases():
+    """Synthetic regression + epoch batches of the cadence study (data.py:49-60,
+    run.py:174-192, bench.py:135-207): first batches and a short newton_cg run."""
+    from curvopt.harness.data import gen_regression
+    from curvopt.method import make
+
+    out = {}
+    train, test = gen_regression(n=2000, d=32, noise_std=0.1, seed=0)
+    out["reg/train_X_sum"] = np.array(train.X.sum())
+    out["reg/train_y"] = train.y[:50, 0].copy()
+    out["reg/test_n"] = np.array(test.n)
+    root = N.Rng(0)
+    m = Model(32, (64, 64), 1, "relu")
+    w = init_params(m, root.split())
+    batcher = EpochBatcher(train, 128, root.split())
+    meth = make("newton_cg", m, damping={"policy": "constant", "lam0": 1.0, "tr": None},
+                solver={"cg": {"maxiter": 3, "warm_start": True}}, telemetry={"rho_every_k": 2})
+    st = meth.init(w, seed=0)
+    rows = []
+    for t in range(6):
+        b = batcher.next()
+        if t == 0:
+            out["reg/batch0_idx_X"] = b.inputs[:4].copy()
+        w, st, info = meth.step(w, b, st)
+        rows.append(info.to_row())
+    out["newton_cg/info"] = np.array(rows, dtype=np.float64)
+    out["newton_cg/w_final"] = w.data
+    save("harness", **out)
+
+
 if __name__ == "__main__":
     rng_cases()
     primitive_cases()
     trajectory_cases()
     plan_cases()
+    primitive_tc_cases()
+    chain_cases()
+    gnb_cases()
+    harness_cases()
