@@ -20,6 +20,8 @@
  *   cv_row_solve_cholesky solvers.py:146-161
  *   cv_backproject        curvature.py:53-60 (scaled_row_transpose)
  *   cv_apply_update       method.py:345-357 (chain of scale links + w + update + norms)
+ *   cv_chain_apply        transforms.py:148-199 (chain_apply, every link kind) + method.py:345-357
+ *   cv_gnb_diag           telemetry.py:129-160 (gnb_diag, sampled-label GGN diagonal)
  *
  * Conventions
  *   - Every pointer argument is a DEVICE pointer owned by the caller, unless its
@@ -135,6 +137,43 @@ CV_API int cv_apply_update(cv_ctx* ctx, const float* w, const float* direction, 
                     float* update, float* w_next, double* scal);
 /* scal[0] = ||x||^2, scal[1] = #nonfinite(x) (device doubles). */
 CV_API int cv_norm_check(cv_ctx* ctx, const float* x, int64_t d, double* scal);
+
+/* One link of a post-direction transform chain (transforms.py:22-99).  Host-side
+ * scalars are pre-evaluated by the caller (schedules at step t, Adam bias
+ * corrections at the link's step count), so the device never sees t:
+ *   CV_LINK_SCALE                 p[0] = value (scale, or scale_by_schedule's value at t)
+ *   CV_LINK_TRACE_MOMENTUM        p[0] = beta;          state_in[0] = trace, state_out[0] = new trace
+ *   CV_LINK_ADD_DECAYED_WEIGHTS   p[0] = weight_decay   (reads w)
+ *   CV_LINK_CLIP_GLOBAL_NORM      p[0] = max_norm       (global ||x|| reduced on the device)
+ *   CV_LINK_SCALE_BY_ADAM         p[0..6] = b1, 1-b1, b2, 1-b2, eps, 1/(1-b1^t), 1/(1-b2^t);
+ *                                 state_in/out[0] = m, [1] = v
+ *   CV_LINK_SOPHIA_CLIP           p[0] = gamma, p[1] = eps (reads precond_diag)
+ * State outputs are fresh buffers (the caller keeps the old state for an aborted step). */
+enum {
+  CV_LINK_SCALE = 0,
+  CV_LINK_TRACE_MOMENTUM = 1,
+  CV_LINK_ADD_DECAYED_WEIGHTS = 2,
+  CV_LINK_SCALE_BY_ADAM = 3,
+  CV_LINK_SOPHIA_CLIP = 4,
+  CV_LINK_CLIP_GLOBAL_NORM = 5
+};
+typedef struct cv_link {
+  int32_t kind;
+  int32_t pad;
+  double p[7];
+  const float* state_in[2];
+  float* state_out[2];
+} cv_link;
+
+/* update = chain(direction); w_next = w + update; scal as cv_apply_update.
+ * links: host array of n_links; precond_diag nullable unless a sophia_clip link is present. */
+CV_API int cv_chain_apply(cv_ctx* ctx, int n_links, const cv_link* links, const float* direction, const float* w,
+                          const float* precond_diag, int64_t d, float* update, float* w_next, double* scal);
+
+/* GNB diagonal over n_samples label draws; draw r uses the uniforms counter + r*b_global + 1
+ * + row_offset + i for local row i (Rng.uniform(b_global), rows of this rank's shard). */
+CV_API int cv_gnb_diag(cv_snap* snap, uint64_t seed, uint64_t counter, int n_samples, int64_t row_offset,
+                       float* diag_out);
 
 /* ---- engine unit test ----------------------------------------------------- */
 /* out[M x N] (ld ldo) = A B with A, B given as fp32 (split inside): A(m,k) =

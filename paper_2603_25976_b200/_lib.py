@@ -30,6 +30,15 @@ class CgStats(C.Structure):
 
 CG_STATS_BYTES = C.sizeof(CgStats)
 
+LINK = {"scale": 0, "scale_by_schedule": 0, "trace_momentum": 1, "add_decayed_weights": 2, "scale_by_adam": 3,
+        "sophia_clip": 4, "clip_global_norm": 5}
+
+
+class CvLink(C.Structure):
+    """cv_link (include/curvopt_b200.h): one pre-evaluated transform link."""
+    _fields_ = [("kind", C.c_int32), ("pad", C.c_int32), ("p", C.c_double * 7), ("state_in", C.c_void_p * 2),
+                ("state_out", C.c_void_p * 2)]
+
 _P = C.c_void_p
 _SIGS = {
     "cv_version": (C.c_char_p, []),
@@ -59,6 +68,8 @@ _SIGS = {
     "cv_rho_terms": (C.c_int, [_P, C.c_int, _P, _P, _P, _P]),
     "cv_apply_update": (C.c_int, [_P, _P, _P, C.c_double, C.c_int64, _P, _P, _P]),
     "cv_norm_check": (C.c_int, [_P, _P, C.c_int64, _P]),
+    "cv_chain_apply": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, C.c_int64, _P, _P, _P]),
+    "cv_gnb_diag": (C.c_int, [_P, C.c_uint64, C.c_uint64, C.c_int, C.c_int64, _P]),
     "cv_gemm_test": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, _P, C.c_int64, C.c_int, _P, C.c_int64,
                                C.c_int, _P, C.c_int64]),
     "cv_gemm_bench": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P]),

@@ -37,6 +37,9 @@ struct CvError : std::runtime_error {
   } catch (const CvError& e) {                         \
     _ctx->err = e.what();                              \
     return e.code;                                     \
+  } catch (const std::invalid_argument& e) {           \
+    _ctx->err = e.what();                              \
+    return CV_E_CONTRACT;                              \
   } catch (const std::exception& e) {                  \
     _ctx->err = e.what();                              \
     return strstr(e.what(), "NCCL") ? CV_E_NCCL : CV_E_CUDA; \
@@ -399,6 +402,23 @@ int cv_apply_update(cv_ctx* ctx, const float* w, const float* direction, double 
 int cv_norm_check(cv_ctx* ctx, const float* x, int64_t d, double* scal) {
   CV_TRY(ctx)
   norm_check(_ctx, x, d, scal);
+  CV_CATCH
+}
+
+int cv_chain_apply(cv_ctx* ctx, int n_links, const cv_link* links, const float* direction, const float* w,
+                   const float* precond_diag, int64_t d, float* update, float* w_next, double* scal) {
+  CV_TRY(ctx)
+  contract(n_links >= 0 && (n_links == 0 || links), "chain links missing");
+  contract(direction && w && update && w_next && scal && d >= 1, "chain_apply needs direction, w and outputs");
+  chain_apply(_ctx, n_links, links, direction, w, precond_diag, d, update, w_next, scal);
+  CV_CATCH
+}
+
+int cv_gnb_diag(cv_snap* s, uint64_t seed, uint64_t counter, int n_samples, int64_t row_offset, float* diag_out) {
+  if (!s) return CV_E_CONTRACT;
+  CV_TRY(s->ctx)
+  contract(diag_out != nullptr, "gnb_diag needs an output");
+  gnb_diag(_ctx, s, seed, counter, n_samples, row_offset, diag_out);
   CV_CATCH
 }
 

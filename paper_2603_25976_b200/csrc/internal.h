@@ -328,4 +328,10 @@ void dot_into(cv_ctx* ctx, const float* a, const float* b, int64_t n, double* ou
 void apply_update(cv_ctx* ctx, const float* w, const float* dir, double coef, int64_t d, float* upd,
                   float* wn, double* scal);
 void norm_check(cv_ctx* ctx, const float* x, int64_t d, double* scal);
+
+// chain.cu
+void chain_apply(cv_ctx* ctx, int n_links, const cv_link* links, const float* dir, const float* w, const float* pre,
+                 int64_t d, float* upd, float* wn, double* scal);
+void gnb_diag(cv_ctx* ctx, cv_snap* s, uint64_t seed, uint64_t counter, int n_samples, int64_t row_offset,
+              float* diag);
 }  // namespace cv

@@ -43,13 +43,16 @@ class Batch:
     """Inputs plus targets (float matrix for mse, class indices for ce).
 
     `global_size` is the batch size the loss mean is taken over; it differs from
-    the local row count only for a rank's shard of a data-parallel batch.
+    the local row count only for a rank's shard of a data-parallel batch, whose
+    first row is row `row_offset` of the global batch (the per-row random streams,
+    e.g. gnb_diag's label draws, index the global batch).
     """
 
     inputs: object
     targets: object
     loss_kind: str
     global_size: int | None = None
+    row_offset: int = 0
     _dev: dict = field(default_factory=dict, repr=False, compare=False)
 
     def __post_init__(self):
@@ -92,6 +95,8 @@ class Batch:
             object.__setattr__(self, "global_size", int(b))
         elif self.global_size < b:
             raise ContractError("global_size smaller than the local shard")
+        if self.row_offset < 0 or self.row_offset + b > self.global_size:
+            raise ContractError("shard rows outside the global batch")
 
     @property
     def size(self) -> int:

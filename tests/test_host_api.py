@@ -95,7 +95,9 @@ def test_overrides_and_module_diff():
     assert P.module_diff(P.preset_spec("sophia_n"), P.preset_spec("sophia_h")) == ("curvature",)
 
 
+@pytest.mark.gpu
 def test_chain_apply_host_arrays():
+    """Host ParamVectors go through the device chain kernel (no CPU path)."""
     w = P.ParamVector(np.arange(4.0), (("w", (4,)),))
     d = w.like(np.ones(4))
     chain = (P.transforms.trace_momentum(0.5), P.transforms.clip_global_norm(1.0), P.transforms.scale(-2.0))
