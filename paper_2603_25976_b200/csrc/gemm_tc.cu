@@ -955,7 +955,9 @@ struct OutKeyHash {
 };
 
 // fp16: dims {cols, rows}, row stride ld, box {16, 32}, SWIZZLE_32B.
-// fp32: dims {cols, rows (, slabs)}, box {16, 32 (, 1)}, SWIZZLE_64B.
+// fp32: dims {cols, rows}, box {16, 32}, SWIZZLE_64B; split-K partials (slabs > 0):
+// dims {cols, rows, slabs}, box {16, 32, 1} -- rank 3 even for a single slab, since the
+// partial epilogue always issues the 3-D store.
 static CUtensorMap make_out_map(const void* ptr, int fp16, int64_t cols, int64_t rows, int64_t slabs, int64_t ld) {
   static std::unordered_map<OutKey, CUtensorMap, OutKeyHash> cache;
   static std::mutex mu;
@@ -969,8 +971,8 @@ static CUtensorMap make_out_map(const void* ptr, int fp16, int64_t cols, int64_t
   if (!fn) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
   CUtensorMap m;
   const int esz = fp16 ? 2 : 4;
-  const cuuint32_t rank = slabs > 1 ? 3 : 2;
-  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)slabs};
+  const cuuint32_t rank = slabs > 0 ? 3 : 2;
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)(slabs > 0 ? slabs : 1)};
   cuuint64_t strides[2] = {(cuuint64_t)ld * esz, (cuuint64_t)ld * esz * rows};
   cuuint32_t box[3] = {16, 32, 1};
   cuuint32_t estr[3] = {1, 1, 1};
@@ -1011,7 +1013,7 @@ static void setup_out(const GemmArgs& g, TcMaps& maps, TcArgs& a, float* partial
   }
   if (e.mode == EPI_STORE) {
     if ((e.ld & 3) || !aligned16(e.out)) return;
-    maps.o[0] = make_out_map(e.out, 0, g.N, g.M, 1, e.ld);
+    maps.o[0] = make_out_map(e.out, 0, g.N, g.M, 0, e.ld);
     a.tma_out = 2;
     return;
   }
@@ -1019,8 +1021,8 @@ static void setup_out(const GemmArgs& g, TcMaps& maps, TcArgs& a, float* partial
                          e.mask_div == 1 && (e.mask_ld & 7) == 0 && aligned16(e.mask_hi);
   if (!(e.mode == EPI_SPLIT_ACT || relu_mask)) return;
   if ((e.ld & 7) || !aligned16(e.out_hi) || !aligned16(e.out_lo)) return;
-  maps.o[0] = make_out_map(e.out_hi, 1, g.N, g.M, 1, e.ld);
-  maps.o[1] = make_out_map(e.out_lo, 1, g.N, g.M, 1, e.ld);
+  maps.o[0] = make_out_map(e.out_hi, 1, g.N, g.M, 0, e.ld);
+  maps.o[1] = make_out_map(e.out_lo, 1, g.N, g.M, 0, e.ld);
   a.tma_out = 1;
 }
 
