@@ -1,14 +1,21 @@
-"""Benchmark: GGN + PCG planned steps/sec (and Gv products/sec) on B200.
+"""Benchmark: planned steps/sec (and curvature products/sec) of the curvopt hot path on B200.
 
-Workload (BASELINE.json configs[2], "C3"): MLP 784-1024-1024-10 softmax-CE, global
-batch 8192, GGN curvature, PCG (tol 1e-5, maxiter 10, stabilise 10, warm start)
-with the diag-EMA(0.99) preconditioner fed by a Hutchinson probe every 10 steps,
-constant damping lam = 1, chain (scale 1e-3, scale -1).  Synthetic data from the
-reference's SplitMix64 stream (MNIST-shaped), random-init weights (init_params).
-With N GPUs the global batch is sharded b/N per rank (strong scaling); every Gv
-and gradient is NCCL all-reduced inside the native library.
+Default workload (BASELINE.json configs[2], "C3"): MLP 784-1024-1024-10 softmax-CE,
+global batch 8192, GGN curvature, PCG (tol 1e-5, maxiter 10, stabilise 10, warm
+start) with the diag-EMA(0.99) preconditioner fed by a Hutchinson probe every 10
+steps, constant damping lam = 1, chain (scale 1e-3, scale -1).  Synthetic data from
+the reference's SplitMix64 stream (MNIST-shaped), random-init weights (init_params).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c3|c4|c5]
+
+--config c4: configs[3], row-space lane (Gram + Cholesky), 3072-2048-2048-10, b=4096.
+--config c5: configs[4], exact-Hessian HVP + CG + trace/diag telemetry,
+             3072-4096x4-10, b=32768 (on N GPUs: b/N rows per rank).
+
+With N GPUs the global batch is sharded b/N per rank (strong scaling: the total work
+is fixed); every gradient and curvature product is NCCL all-reduced inside the native
+library.  Without torchrun, `--gpus N` (N > 1) launches the N ranks itself.
 
 Prints ONE JSON line (rank 0).
 """
@@ -20,26 +27,47 @@ import gc
 import json
 import math
 import os
+import platform
 import subprocess
 import sys
 import threading
 import time
-
-if "OPENBLAS_NUM_THREADS" not in os.environ:
-    try:
-        os.environ["OPENBLAS_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
-    except Exception:
-        pass
 
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-DIMS = (784, 1024, 1024, 10)
-GLOBAL_B = 8192
 METRIC = "GGN-CG planned steps/sec (C3: 784-1024-1024-10, b=8192, PCG + diag-EMA)"
 UNIT = "steps/s"
+
+
+class Workload:
+    def __init__(self, key, dims, b, metric, desc, kind, lane):
+        self.key, self.dims, self.b, self.metric, self.desc, self.kind, self.lane = key, dims, b, metric, desc, kind, lane
+
+    def config(self, world):
+        return {"workload": self.desc, "global_batch": self.b, "dims": list(self.dims),
+                "parallelism": f"dp{world}" if self.lane == "param" else "replicas only (row lane)",
+                "l2": "per-step working set > 126 MB L2 (no flush)"}
+
+
+WORKLOADS = {
+    "c3": Workload("c3", (784, 1024, 1024, 10), 8192, METRIC,
+                   "C3 784-1024-1024-10 softmax-CE, GGN + PCG(diag-EMA 0.99, Hutchinson@10), lam=1, "
+                   "CG tol 1e-5 maxiter 10", "ggn", "param"),
+    "c4": Workload("c4", (3072, 2048, 2048, 10), 4096,
+                   "row-space planned steps/sec (C4: 3072-2048-2048-10, b=4096, Gram + Cholesky)",
+                   "C4 3072-2048-2048-10 softmax-CE, GGN row-space lane: Gram JJ^T + mu I (m=40960) + blocked "
+                   "Cholesky + backprojection, lam=1", "ggn", "row"),
+    "c5": Workload("c5", (3072, 4096, 4096, 4096, 4096, 10), 32768,
+                   "exact-Hessian HVP-CG planned steps/sec (C5: 3072-4096x4-10, b=32768)",
+                   "C5 3072-4096x4-10 softmax-CE, exact-Hessian HVP + CG (tol 1e-5, maxiter 10), constant lam=1 "
+                   "(the reference has no step-norm damping), Hutchinson diag + trace telemetry @10", "hessian",
+                   "param"),
+}
+DIMS = WORKLOADS["c3"].dims
+GLOBAL_B = WORKLOADS["c3"].b
 
 
 def P_w(dims):
@@ -51,7 +79,19 @@ def gv_flops(dims, b):
     return 8 * b * P_w(dims) - 4 * b * dims[0] * dims[1]
 
 
-def make_batches(n_batches, b_global, rank, world):
+def hvp_flops(dims, b):
+    """One exact-Hessian product (ReLU): 12 b P_w - 8 b n0 n1."""
+    return 12 * b * P_w(dims) - 8 * b * dims[0] * dims[1]
+
+
+def row_flops(dims, b):
+    """Row lane: Gram as SYRK sum_l m^2 n_{l+1} + potrf m^3/3."""
+    c = dims[-1]
+    m = b * c
+    return sum(m * m * dims[l + 1] for l in range(len(dims) - 1)) + m ** 3 / 3.0
+
+
+def make_batches(n_batches, b_global, rank, world, dims=DIMS):
     """Shard rows [rank*b/N, (rank+1)*b/N) of batch i = Rng(1+i) normal/integers."""
     from paper_2603_25976_b200.numeric import Rng
 
@@ -59,9 +99,24 @@ def make_batches(n_batches, b_global, rank, world):
     out = []
     for i in range(n_batches):
         r = Rng(1 + i)
-        X = r.normal(b_global * DIMS[0]).reshape(b_global, DIMS[0]).astype(np.float32)
-        y = r.integers(b_global, DIMS[-1])
+        X = r.normal(b_global * dims[0]).reshape(b_global, dims[0]).astype(np.float32)
+        y = r.integers(b_global, dims[-1])
         out.append((X[rank * bl:(rank + 1) * bl], y[rank * bl:(rank + 1) * bl]))
+    return out
+
+
+def make_batches_fast(n_batches, b_global, rank, world, dims):
+    """C5-sized batches (b x 3072 = 10^8 normals): numpy's PCG64 instead of the Python
+    SplitMix64 stream, which would take minutes per batch; shard layout as make_batches."""
+    bl = b_global // world
+    out = []
+    for i in range(n_batches):
+        g = np.random.default_rng(1 + i)
+        X = g.standard_normal((bl, dims[0]), dtype=np.float32) if world == 1 else \
+            g.standard_normal((b_global, dims[0]), dtype=np.float32)[rank * bl:(rank + 1) * bl]
+        y = g.integers(0, dims[-1], size=b_global)[rank * bl:(rank + 1) * bl] if world > 1 else \
+            g.integers(0, dims[-1], size=bl)
+        out.append((np.ascontiguousarray(X), y.astype(np.int64)))
     return out
 
 
@@ -74,6 +129,29 @@ def spec_c3():
                         precond=P.PrecondSpec("diag_ema", 0.99), damping=P.DampingSpec("constant", 1.0),
                         estimator=P.EstimatorSpec("hutchinson", 1, every_k=10),
                         chain=(P.transforms.scale(1e-3), P.transforms.scale(-1.0)))
+
+
+def spec_c4():
+    import paper_2603_25976_b200 as P
+
+    return P.MethodSpec(curvature=P.CurvatureSpec("ggn_ce"), solver=P.SolverSpec("row_cholesky"),
+                        damping=P.DampingSpec("constant", 1.0),
+                        chain=(P.transforms.scale(1e-3), P.transforms.scale(-1.0)))
+
+
+def spec_c5():
+    import paper_2603_25976_b200 as P
+
+    return P.MethodSpec(curvature=P.CurvatureSpec("hessian"),
+                        solver=P.SolverSpec("cg", P.CgConfig(tol=1e-5, maxiter=10, stabilise_every=10,
+                                                             warm_start=True)),
+                        damping=P.DampingSpec("constant", 1.0),
+                        estimator=P.EstimatorSpec("hutchinson", 1, every_k=10),
+                        telemetry=P.TelemetrySpec(trace_every_k=10, trace_probes=1),
+                        chain=(P.transforms.scale(1e-3), P.transforms.scale(-1.0)))
+
+
+SPECS = {"c3": spec_c3, "c4": spec_c4, "c5": spec_c5}
 
 
 class ClockSampler:
@@ -96,7 +174,6 @@ class ClockSampler:
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
             # nvidia-smi needs a moment to start: enter the timed region only once it samples
-            # (a short timed region could otherwise see no sample at all)
             self.first.wait(timeout=5.0)
         except Exception:
             self.proc = None
@@ -119,54 +196,26 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        # samples taken inside the timed region (else the one just before it)
         rows = self.rows[self.start_idx:] or self.rows[-1:]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        self.rows = rows
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows)}
 
 
 def product_traffic():
-    """DRAM bytes of one GGN product from the committed ncu --set full capture
-    (scratch/product_traffic.py -> profiles/r1d_product_traffic.json), or None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1d_product_traffic.json")) as f:
-            return float(json.load(f)["dram_bytes_per_product"])
-    except Exception:
-        return None
-
-
-# the tensor-core launches of one C3 product in the committed capture's order
-_GEMM_ROLES = [("JVP0 X V0, mask bits", 8192, 1024, 785), ("JVP1 [A1|da0][V1;W1] + fused output JVP", 8192, 1024, 2049),
-               ("dW1 weight gradient, split-K, side stream (SM share)", 1025, 1024, 8192),
-               ("dX1 backward, mask bits (SM share)", 8192, 1024, 1024), ("dW0 weight gradient, split-K", 785, 1024, 8192)]
-
-
-def gemm_launch_rooflines(peak):
-    """Per-launch tensor roofline of the product's GEMMs from the committed ncu --set full
-    capture (cold-cache serialised replay: co-scheduled launches replay on their SM share)."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1d_product_traffic.json")) as f:
-            kern = json.load(f)["kernels"]
-    except Exception:
-        return None
-    tc2 = [k for k in kern if "k_gemm_tc2" in k["kernel"]]
-    if len(tc2) != len(_GEMM_ROLES):
-        return None
-    out = []
-    for k, (role, m, n, kk) in zip(tc2, _GEMM_ROLES):
-        tf = 2.0 * m * n * kk / (k["us"] * 1e-6) / 1e12
-        out.append({"launch": role, "useful_gflop": round(2.0 * m * n * kk / 1e9, 2), "us": k["us"],
-                    "tflops": round(tf, 1), "frac": round(tf / peak, 3) if peak else None,
-                    "tensor_pipe_pct": k.get("tensor_pipe_pct"),
-                    "dram_bytes": k["dram_read_B"] + k["dram_write_B"]})
-    return out
+    """DRAM bytes of one GGN product from the committed ncu --set full capture, or None."""
+    for name in ("r2_product_traffic.json", "r1d_product_traffic.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                return float(json.load(f)["dram_bytes_per_product"]), name
+        except Exception:
+            continue
+    return None, None
 
 
 def measured_peaks():
@@ -196,65 +245,152 @@ def f16_peak_tflops():
     return 2 * 8192**3 / (best * 1e-3) / 1e12
 
 
-# ---------------------------------------------------------------------------
-# CPU oracle (reference arm / cpu_baseline): the numpy restatement of the
-# reference step, timed on the host cores.
-# ---------------------------------------------------------------------------
-def cpu_oracle_run(max_seconds=20.0, max_steps=None, warmup=1):
-    from oracle import curvopt_oracle as O
-
-    spec = O.OSpec(precond="diag_ema", estimator_every_k=10)
-    w = O.init_params(DIMS, "relu", O.ORng(0))
-    batches = []
-    for i in range(2):
-        r = O.ORng(1 + i)
-        X = r.normal(GLOBAL_B * DIMS[0]).reshape(GLOBAL_B, DIMS[0])
-        batches.append((X, r.integers(GLOBAL_B, DIMS[-1])))
-    st = O.oracle_init(spec, w.size)
-    gv_log = []
-    for i in range(warmup):
-        w, st, _, _ = O.oracle_step(spec, DIMS, "relu", "ce", w, *batches[i % 2], st)
-    times = []
-    gv_log = []
-    t_all = time.perf_counter()
-    while True:
-        t0 = time.perf_counter()
-        w, st, info, _ = O.oracle_step(spec, DIMS, "relu", "ce", w, *batches[len(times) % 2], st, gv_log=gv_log)
-        times.append(time.perf_counter() - t0)
-        if max_steps is not None and len(times) >= max_steps:
-            break
-        if time.perf_counter() - t_all > max_seconds:
-            break
-    sps = len(times) / sum(times)
-    return sps, times, gv_log
-
-
-def cores_used():
+def cpu_model():
     try:
-        return int(os.environ.get("OPENBLAS_NUM_THREADS") or len(os.sched_getaffinity(0)))
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor() or "unknown"
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
     except Exception:
         return os.cpu_count()
 
 
+# ---------------------------------------------------------------------------
+# CPU oracle (reference arm / cpu_baseline): the numpy restatement of the
+# reference step, timed on the host cores (the reference itself is pure Python
+# and does not travel to the GPU box).
+# ---------------------------------------------------------------------------
+def cpu_c3_steps(steps, warmup, max_seconds):
+    from oracle import curvopt_oracle as O
+
+    spec = O.OSpec(precond="diag_ema", estimator_every_k=10)
+    w = O.init_params(DIMS, "relu", O.ORng(0))
+    batches = [(X.astype(np.float64), y) for X, y in make_batches(2, GLOBAL_B, 0, 1)]
+    st = O.oracle_init(spec, w.size)
+    for i in range(warmup):
+        w, st, _, _ = O.oracle_step(spec, DIMS, "relu", "ce", w, *batches[i % 2], st)
+    times, gv_log = [], []
+    t_all = time.perf_counter()
+    for i in range(steps):
+        t0 = time.perf_counter()
+        w, st, _, _ = O.oracle_step(spec, DIMS, "relu", "ce", w, *batches[(warmup + i) % 2], st, gv_log=gv_log)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_all > max_seconds:
+            break
+    return len(times) / sum(times), times, gv_log
+
+
+def cpu_gv_rate(threads, b=GLOBAL_B, n=2):
+    """GGN products/s of the oracle at b rows with `threads` BLAS threads."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import curvopt_oracle as O
+
+    w = O.init_params(DIMS, "relu", O.ORng(0))
+    X, y = O.synthetic_batch(b, DIMS[0], DIMS[-1])
+    with threadpool_limits(limits=threads):
+        lin = O.linearize(DIMS, "relu", "ce", w, X, y)
+        v = O.ORng(2).normal(w.size)
+        O.ggn_matvec(lin, v)
+        t0 = time.perf_counter()
+        for _ in range(n):
+            O.ggn_matvec(lin, v)
+        return n / (time.perf_counter() - t0)
+
+
+def cpu_row_sample(wl, threads):
+    """Bounded sample of the C4 row lane on the oracle: Gram + Cholesky + backprojection at
+    b=1024 (m=10240), extrapolated to b=4096 by the flop model (Gram ~ m^2, potrf ~ m^3)."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import curvopt_oracle as O
+
+    bs = 1024
+    dims = wl.dims
+    w = O.init_params(dims, "relu", O.ORng(0))
+    X, y = O.synthetic_batch(bs, dims[0], dims[-1])
+    with threadpool_limits(limits=threads):
+        t0 = time.perf_counter()
+        lin = O.linearize(dims, "relu", "ce", w, X, y)
+        seeds, rhs = O.row_seeds_rhs(lin)
+        t1 = time.perf_counter()
+        gram = O.output_gram(lin, seeds)
+        t2 = time.perf_counter()
+        v = O.row_cholesky(gram, rhs, float(bs))
+        t3 = time.perf_counter()
+        O.row_transpose(lin, seeds, v)
+        t4 = time.perf_counter()
+    k = wl.b / bs
+    est = (t1 - t0 + t4 - t3) * k + (t2 - t1) * k * k + (t3 - t2) * k ** 3
+    return 1.0 / est, f"b={bs} (m={bs * dims[-1]}) oracle row step {t4 - t0:.2f} s, extrapolated to b={wl.b} " \
+                      f"by the flop model (linearize/backprojection x{k:.0f}, Gram x{k * k:.0f}, potrf x{k ** 3:.0f})"
+
+
+def cpu_hvp_sample(wl, threads):
+    """Bounded sample of the C5 step: one oracle HVP at b=512 rows, extrapolated linearly to
+    b=32768 and to the products of a planned step (CG 10 + warm start + probes)."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import curvopt_oracle as O
+
+    bs = 512
+    dims = wl.dims
+    w = O.init_params(dims, "relu", O.ORng(0))
+    X, y = O.synthetic_batch(bs, dims[0], dims[-1])
+    with threadpool_limits(limits=threads):
+        t0 = time.perf_counter()
+        lin = O.linearize(dims, "relu", "ce", w, X, y)
+        t1 = time.perf_counter()
+        O.hvp(lin, O.ORng(2).normal(w.size))
+        t2 = time.perf_counter()
+    k = wl.b / bs
+    products = 11.1  # measured products per planned C5 step on the device run (CG 10 + warm start + probes / 10)
+    est = k * ((t1 - t0) + products * (t2 - t1))
+    return 1.0 / est, f"b={bs} oracle linearize {t1 - t0:.2f} s + one HVP {t2 - t1:.2f} s, extrapolated x{k:.0f} " \
+                      f"rows and x{products} products per step"
+
+
 def run_reference(args, rank, world):
+    """The reference arm: the CPU restatement of curvopt's step on the host cores."""
     if rank != 0:
         return
-    W = min(args.warmup, 1)
-    sps, times, gv = cpu_oracle_run(max_seconds=min(90.0, 20.0 * max(args.steps, 1)), max_steps=args.steps,
-                                    warmup=W)
-    sample = (f"{len(times)} full C3 planned steps (after {W} warm-up) of the numpy/OpenBLAS f64 oracle restating "
-              f"curvopt Method.step; {cores_used()} BLAS threads")
-    line = {"impl": "reference", "metric": METRIC, "value": sps, "unit": UNIT, "n_gpus": world,
-            "steps": len(times), "warmup": W, "ms_per_step": 1e3 / sps, "higher_is_better": True,
+    wl = WORKLOADS[args.config]
+    cores = host_cores()
+    if wl.key == "c3":
+        sps, times, gv = cpu_c3_steps(args.steps, args.warmup, max_seconds=240.0)
+        sample = (f"{len(times)} full C3 planned steps (after {args.warmup} warm-up) of the numpy/OpenBLAS f64 "
+                  f"oracle restating curvopt Method.step; {cores} BLAS threads. The reference's own ggn_ce "
+                  f"snapshot also runs a per-example eigh (curvature.py:118-119) the port skips, so the port is "
+                  f"the faster of the two")
+        gvps = sum(gv) / sum(times) if gv else None
+        steps = len(times)
+    elif wl.key == "c4":
+        sps, sample = cpu_row_sample(wl, cores)
+        gvps, steps = None, args.steps
+    else:
+        sps, sample = cpu_hvp_sample(wl, cores)
+        gvps, steps = None, args.steps
+    line = {"impl": "reference", "metric": wl.metric, "value": sps, "unit": UNIT, "n_gpus": world,
+            "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 / sps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C3 784-1024-1024-10 softmax-CE, GGN + PCG(diag-EMA 0.99, Hutchinson@10)",
-                       "global_batch": GLOBAL_B, "parallelism": "host cores"},
-            "gv_per_s": sum(gv) / sum(times) if gv else None,
-            "cpu_baseline": {"value": sps, "unit": UNIT, "cores": cores_used(), "kind": "port", "sample": sample},
+            "config": wl.config(world), "gv_per_s": gvps,
+            "cpu_baseline": {"value": sps, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": sps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# The GPU arm
+# ---------------------------------------------------------------------------
 def run_ours(args, rank, world):
     import torch
     import torch.distributed as dist
@@ -262,16 +398,28 @@ def run_ours(args, rank, world):
     import paper_2603_25976_b200 as P
     from paper_2603_25976_b200.runtime import runtime
 
+    wl = WORKLOADS[args.config]
+    dims = wl.dims
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
     rt = runtime()
-    model = P.Model(DIMS[0], DIMS[1:-1], DIMS[-1], "relu")
-    meth = P.assemble(spec_c3(), model)
+    model = P.Model(dims[0], dims[1:-1], dims[-1], "relu")
+    meth = P.assemble(SPECS[wl.key](), model)
     w0 = P.init_params(model, P.Rng(0))
-    bl = GLOBAL_B // world
-    host_batches = make_batches(4, GLOBAL_B, rank, world)
-    dev_batches = [P.Batch(torch.from_numpy(X).to(dev), torch.from_numpy(y).to(dev), "ce", global_size=GLOBAL_B)
-                   for X, y in host_batches]
+    row = wl.lane == "row"
+    shard_world = 1 if row else world  # the row lane runs replicas
+    shard_rank = 0 if row else rank
+    bl = wl.b // shard_world
+    nb = 4 if wl.key == "c3" else 2
+    if wl.key == "c3":
+        host_batches = make_batches(nb, wl.b, shard_rank, shard_world, dims)
+    else:
+        host_batches = make_batches_fast(nb, wl.b, shard_rank, shard_world, dims)
+
+    def mk_batch(X, y):
+        return P.Batch(X, y, "ce", global_size=wl.b, row_offset=shard_rank * bl)
+
+    dev_batches = [mk_batch(torch.from_numpy(X).to(dev), torch.from_numpy(y).to(dev)) for X, y in host_batches]
     w = w0.to_device(dev)
     st = meth.init(w, 0)
 
@@ -280,27 +428,23 @@ def run_ours(args, rank, world):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # warm-up (also triggers every lazy allocation)
     for i in range(args.warmup):
-        w, st, info = meth.step(w, dev_batches[i % len(dev_batches)], st)
-    # Gv counter: CG products + Hutchinson probes are read from the step records
+        w, st, info = meth.step(w, dev_batches[i % nb], st)
     stream = torch.cuda.current_stream()
     gv_total = 0
     launches0 = rt.launches()
-    # no cyclic-GC pause inside the timed regions (a full collection of the interpreter's
-    # heap is tens of ms, which the step's single host sync would expose as GPU idle)
+    # no cyclic-GC pause inside the timed regions (a full collection is tens of ms, which
+    # the step's single host sync would expose as GPU idle)
     gc.collect()
     gc.freeze()
     gc.disable()
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    infos = []
     with ClockSampler(dev.index) as clk:
         ev0.record(stream)
         for i in range(args.steps):
-            w, st, info = meth.step(w, dev_batches[(args.warmup + i) % len(dev_batches)], st)
-            infos.append(info)
-            gv_total += meth.last_products
+            w, st, info = meth.step(w, dev_batches[(args.warmup + i) % nb], st)
+            gv_total += getattr(meth, "last_products", 0)
         ev1.record(stream)
         barrier()
     launches = rt.launches() - launches0
@@ -312,18 +456,17 @@ def run_ours(args, rank, world):
     sps = args.steps / (ms * 1e-3)
     gv_per_s = gv_total / (ms * 1e-3)
 
-    # ---- e2e: same steps through the public API with host (pinned) buffers ----
-    e2e = None
+    # ---- e2e: the same steps through the public API with host (pinned) buffers ----
     wh = P.ParamVector(torch.from_numpy(np.asarray(w.data.cpu().numpy())).pin_memory(), w.layout)
     pinned = [(torch.from_numpy(X).pin_memory(), torch.from_numpy(y).pin_memory()) for X, y in host_batches]
     st_e = meth.init(w, 0)
-    for i in range(2):
-        wh, st_e, _ = meth.step(wh, P.Batch(*pinned[i % 4], "ce", global_size=GLOBAL_B), st_e)
+    for i in range(min(2, args.warmup)):
+        wh, st_e, _ = meth.step(wh, mk_batch(*pinned[i % nb]), st_e)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for i in range(args.steps):
-        wh, st_e, _ = meth.step(wh, P.Batch(*pinned[i % 4], "ce", global_size=GLOBAL_B), st_e)
+        wh, st_e, _ = meth.step(wh, mk_batch(*pinned[i % nb]), st_e)
     e1.record(stream)
     barrier()
     ems = e0.elapsed_time(e1)
@@ -331,65 +474,108 @@ def run_ours(args, rank, world):
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     ems = float(te.item())
-    h2d = bl * DIMS[0] * 4 + bl * 8 + w.dim * 4
-    d2h = w.dim * 4 + 16 * 8 + 48
+    h2d = bl * dims[0] * 4 + bl * 8 + w.dim * 4
+    d2h = w.dim * 4 + 24 * 8
     e2e = {"value": args.steps / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
-
     gc.enable()
-    # ---- roofline of the dominant unit: the GGN product (its GEMMs), timed live ----
-    snap = P.make_snapshot("ggn_ce", model, w, dev_batches[0])
-    v = torch.randn(w.dim, device=dev)
-    out = torch.empty_like(v)
-    for _ in range(3):
-        snap.apply(0, v, out)
-    barrier()
-    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    n_gv = 20
-    g0.record(stream)
-    for _ in range(n_gv):
-        snap.apply(0, v, out)
-    g1.record(stream)
-    torch.cuda.synchronize()
-    gv_ms = g0.elapsed_time(g1) / n_gv
-    snap.close()
-    flops = gv_flops(DIMS, bl)
-    achieved = flops / (gv_ms * 1e-3) / 1e12
-    peaks = measured_peaks()
-    # every useful flop of the product costs 3 fp16 tensor-core flops (hi.hi + hi.lo + lo.hi)
+
+    # ---- roofline of the dominant unit, timed live with CUDA events on the launch stream ----
     try:
         f16 = f16_peak_tflops() if rank == 0 else None
         peak = f16 / 3.0 if f16 else None
-        peak_note = f"measured cuBLAS fp16 {f16:.0f} TF/s / 3 (3xFP16 split passes)"
+        peak_note = f"measured cuBLAS fp16 {f16:.0f} TF/s / 3 (3xFP16 split passes)" if f16 else None
     except Exception:
-        peak = peaks.get("bf16_tflops", 1626.3) / 3
+        peak = measured_peaks().get("bf16_tflops", 1626.3) / 3
         peak_note = "MEASURED_PEAKS bf16 burst / 3 (3xFP16 split passes)"
+    if row:
+        flops = row_flops(dims, wl.b)
+        achieved = flops / (ms / args.steps * 1e-3) / 1e12
+        unit_note = (f"one row-lane planned step at b={wl.b} (m={wl.b * dims[-1]}): Gram as SYRK + potrf = "
+                     f"{flops / 1e12:.2f} TFLOP useful, {ms / args.steps:.1f} ms/step (CUDA events)")
+        traffic, tsrc = None, None
+    else:
+        kind = 1 if wl.kind == "hessian" else 0
+        snap = P.make_snapshot("hessian" if kind else "ggn_ce", model, w, dev_batches[0])
+        v = torch.randn(w.dim, device=dev)
+        out = torch.empty_like(v)
+        for _ in range(3):
+            snap.apply(kind, v, out)
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n_gv = 20 if wl.key == "c3" else 5
+        g0.record(stream)
+        for _ in range(n_gv):
+            snap.apply(kind, v, out)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gv_ms = g0.elapsed_time(g1) / n_gv
+        snap.close()
+        flops = hvp_flops(dims, bl) if kind else gv_flops(dims, bl)
+        achieved = flops / (gv_ms * 1e-3) / 1e12
+        unit_note = (f"one {'HVP' if kind else 'GGN'} product at b={bl}: {flops / 1e9:.1f} GFLOP useful, "
+                     f"{gv_ms:.3f} ms avg over {n_gv} (CUDA events)")
+        traffic, tsrc = product_traffic() if wl.key == "c3" else (None, None)
 
     if rank != 0:
         return
     clocks = clk.summary()
-    line = {"metric": METRIC, "value": sps, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+    line = {"metric": wl.metric, "value": sps, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32 (scaled 3xFP16 tensor-core GEMMs, fp32 accumulate, fp64 reductions)", "data": "synthetic",
-            "config": {"workload": "C3 784-1024-1024-10 softmax-CE, GGN + PCG(diag-EMA 0.99, Hutchinson@10), "
-                                   "lam=1, CG tol 1e-5 maxiter 10", "global_batch": GLOBAL_B,
-                       "parallelism": f"dp{world}", "l2": "per-step working set ~0.6 GB > 126 MB L2 (no flush)"},
-            "gv_per_s": gv_per_s, "gv_per_step": gv_total / args.steps,
+            "vs_baseline": None,
+            "dtype": "f32 (scaled 3xFP16 tensor-core GEMMs, fp32 accumulate, fp64 reductions)",
+            "data": "synthetic", "config": wl.config(world),
+            "gv_per_s": gv_per_s if not row else None, "gv_per_step": gv_total / args.steps if not row else None,
             "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak if peak else None, "traffic": product_traffic(),
-                         "traffic_source": "profiles/r1d_product_traffic.json (ncu --set full, DRAM read+write "
-                                           "bytes summed over the product's kernels, cold-cache replay)",
-                         "unit_of_work": f"one GGN product at b={bl}: {flops / 1e9:.1f} GFLOP useful, "
-                                         f"{gv_ms:.3f} ms avg over {n_gv} (CUDA events)",
-                         "peak_source": peak_note,
-                         "per_launch_ncu": gemm_launch_rooflines(peak) if bl == 8192 else None},
-            "engine": os.environ.get("CURVOPT_ENGINE", "auto")}
+                         "frac": achieved / peak if peak else None, "traffic": traffic,
+                         "traffic_source": f"profiles/{tsrc} (ncu --set full, DRAM read+write bytes summed over "
+                                           f"the product's kernels)" if tsrc else None,
+                         "unit_of_work": unit_note, "peak_source": peak_note}}
     if world == 1 and not args.no_cpu:
-        sps_cpu, times, gv = cpu_oracle_run(max_seconds=15.0, max_steps=3, warmup=0)
-        line["cpu_baseline"] = {"value": sps_cpu, "unit": UNIT, "cores": cores_used(), "kind": "port",
-                                "sample": f"{len(times)} full C3 planned steps of the numpy/OpenBLAS f64 oracle, "
-                                          f"{cores_used()} BLAS threads"}
+        cores = host_cores()
+        if wl.key == "c3":
+            sps_cpu, times, _ = cpu_c3_steps(3, 0, max_seconds=15.0)
+            sample = f"{len(times)} full C3 planned steps of the numpy/OpenBLAS f64 oracle, {cores} BLAS threads"
+            extra = {"gv_per_s_1thread": cpu_gv_rate(1), "gv_per_s_all_threads": cpu_gv_rate(cores),
+                     "gv_sample": f"2 oracle GGN products at b={wl.b} with OPENBLAS threads = 1 and = {cores}"}
+        elif wl.key == "c4":
+            sps_cpu, sample = cpu_row_sample(wl, cores)
+            extra = {}
+        else:
+            sps_cpu, sample = cpu_hvp_sample(wl, cores)
+            extra = {}
+        line["cpu_baseline"] = {"value": sps_cpu, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                                "cpu_model": cpu_model(), **extra}
     print(json.dumps(line), flush=True)
+
+
+def _rank_main(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    try:
+        run_ours(args, rank, world)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+def _spawn_entry(local_rank, args, world, port):
+    os.environ.update(RANK=str(local_rank), LOCAL_RANK=str(local_rank), WORLD_SIZE=str(world),
+                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    _rank_main(args)
 
 
 def main():
@@ -398,24 +584,22 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    if args.impl == "reference":
-        run_reference(args, rank, world)
-        return
-    if world > 1:
+    if args.warmup < 3 and args.impl == "ours":
+        raise SystemExit("bench.py: --warmup must be >= 3")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        # launch the N ranks ourselves (one process per GPU), as torchrun would
         import torch
-        import torch.distributed as dist
+        import torch.multiprocessing as mp
 
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
-    run_ours(args, rank, world)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.destroy_process_group()
+        if torch.cuda.device_count() < args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but only {torch.cuda.device_count()} visible")
+        port = 29000 + os.getpid() % 2000
+        mp.spawn(_spawn_entry, args=(args, args.gpus, port), nprocs=args.gpus, join=True)
+        return
+    _rank_main(args)
 
 
 if __name__ == "__main__":
