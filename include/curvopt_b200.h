@@ -84,8 +84,21 @@ typedef struct cv_cg_stats {
 } cv_cg_stats;
 
 /* ---- context ------------------------------------------------------------ */
-/* nccl_id: host pointer to a 128-byte ncclUniqueId (required when world > 1). */
+/* nccl_id: host pointer to a 128-byte ncclUniqueId.  world > 1 with nccl_id == NULL
+ * creates a context whose collectives go through an external communicator that the
+ * caller installs with cv_ctx_set_comm before the first call. */
 CV_API int cv_ctx_create(int device, int world, int rank, const void* nccl_id, cv_ctx** out);
+
+/* External communicator (instead of NCCL): called on the host, in enqueue order, for
+ * every collective of the context: in-place sum all-reduce of `count` elements of
+ * `dtype` (CV_DTYPE_*) at device pointer `buf`, ordered on `stream` (the work enqueued
+ * before it must be complete when the data is read; the result must be visible to work
+ * enqueued on `stream` afterwards -- a host-staged implementation synchronises the
+ * stream and copies back before returning).  Return 0 on success.  Lets a host runtime
+ * plug in its own transport (e.g. a gloo process group, several ranks on one GPU). */
+enum { CV_DTYPE_F32 = 0, CV_DTYPE_F64 = 1 };
+typedef int (*cv_comm_fn)(void* user, int dtype, void* buf, int64_t count, void* stream);
+CV_API int cv_ctx_set_comm(cv_ctx* ctx, cv_comm_fn fn, void* user);
 CV_API int cv_ctx_destroy(cv_ctx* ctx);
 CV_API int cv_ctx_set_stream(cv_ctx* ctx, void* cuda_stream);
 CV_API int cv_ctx_set_engine(cv_ctx* ctx, int engine);   /* CV_ENGINE_*: GEMM engine selection */

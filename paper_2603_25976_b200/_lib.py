@@ -40,10 +40,13 @@ class CvLink(C.Structure):
                 ("state_out", C.c_void_p * 2)]
 
 _P = C.c_void_p
+# cv_comm_fn: int (*)(void* user, int dtype, void* buf, int64_t count, void* stream)
+COMM_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p)
 _SIGS = {
     "cv_version": (C.c_char_p, []),
     "cv_ctx_create": (C.c_int, [C.c_int, C.c_int, C.c_int, _P, C.POINTER(_P)]),
     "cv_ctx_destroy": (C.c_int, [_P]),
+    "cv_ctx_set_comm": (C.c_int, [_P, COMM_FN, _P]),
     "cv_ctx_set_stream": (C.c_int, [_P, _P]),
     "cv_ctx_set_engine": (C.c_int, [_P, C.c_int]),
     "cv_last_error": (C.c_char_p, [_P]),

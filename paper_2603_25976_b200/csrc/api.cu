@@ -79,14 +79,22 @@ int cv_ctx_create(int device, int world, int rank, const void* nccl_id, cv_ctx**
   c->amax_counter = (unsigned*)c->pool.get(sizeof(unsigned) * 64);
   cudaMemsetAsync(c->amax_counter, 0, sizeof(unsigned) * 64, c->stream);
   if (world > 1) {
-    contract(nccl_id != nullptr, "world > 1 requires an NCCL unique id");
-    nccl_init(c, nccl_id);
+    if (nccl_id) nccl_init(c, nccl_id);  // else: cv_ctx_set_comm installs the communicator
   } else if (getenv("CURVOPT_FORCE_NCCL")) {
     // single-rank communicator: exercises the NCCL path of every product on one GPU
     char id[128];
     nccl_unique_id(id);
     nccl_init(c, id);
   }
+  CV_CATCH
+}
+
+int cv_ctx_set_comm(cv_ctx* ctx, cv_comm_fn fn, void* user) {
+  CV_TRY(ctx)
+  contract(_ctx->world > 1, "an external communicator needs world > 1");
+  contract(_ctx->nccl == nullptr, "the context already owns an NCCL communicator");
+  _ctx->comm_fn = fn;
+  _ctx->comm_user = user;
   CV_CATCH
 }
 
@@ -107,6 +115,11 @@ int cv_ctx_destroy(cv_ctx* ctx) {
     cudaEventDestroy(ctx->ev_fork2);
     cudaEventDestroy(ctx->ev_join2);
   }
+  if (ctx->comm) {
+    cudaStreamSynchronize(ctx->comm);
+    cudaStreamDestroy(ctx->comm);
+  }
+  for (cudaEvent_t e : ctx->comm_ev) cudaEventDestroy(e);
   ctx->pool.release_all();
   delete ctx;
   return CV_OK;

@@ -144,6 +144,10 @@ struct cv_ctx {
   std::string err;
   cv::Pool pool;
   void* nccl = nullptr;          // ncclComm_t
+  cv_comm_fn comm_fn = nullptr;  // external communicator (cv_ctx_set_comm), used instead of NCCL
+  void* comm_user = nullptr;
+  cudaStream_t comm = nullptr;   // NCCL stream of the per-layer (bucketed) gradient all-reduces
+  std::vector<cudaEvent_t> comm_ev;
   double* red_ws = nullptr;      // reduction partials: kRedBlocks * 8 doubles
   double* scal_ws = nullptr;     // scratch scalars (64 doubles)
   float* amax_ws = nullptr;      // split.cu: per-block maxima (4 x 148 x 16 floats)
@@ -247,7 +251,7 @@ void gemm(cv_ctx* ctx, const GemmArgs& a);  // engine dispatch
 // two independent GEMMs at once: a on the context stream, b on the side stream,
 // the SMs split between them by estimated time; returns when both are enqueued
 // (the context stream waits for b)
-void gemm_pair(cv_ctx* ctx, GemmArgs a, GemmArgs b);
+cudaStream_t gemm_pair(cv_ctx* ctx, GemmArgs a, GemmArgs b);  // returns the stream b ran on
 double gemm_tc_estimate(const cv_ctx* ctx, const GemmArgs& g, int ctas);  // relative time on `ctas` SMs
 cudaStream_t side_fork(cv_ctx* ctx);  // side stream ordered after the context stream's current work
 cudaStream_t side2_fork(cv_ctx* ctx); // third stream, same ordering; joined by side_join
@@ -268,8 +272,24 @@ int gemm_tc_head_groups(const cv_ctx* ctx, const GemmArgs& g);          // 0: no
 bool gemm_tc_tma_split(const cv_ctx* ctx, const GemmArgs& g);           // runs the TMA split epilogue (bits producer)
 
 // runtime.cu
+inline bool distributed(const cv_ctx* ctx) { return ctx->nccl != nullptr || ctx->comm_fn != nullptr; }
 void allreduce_f32(cv_ctx* ctx, float* buf, int64_t n);
 void allreduce_f64(cv_ctx* ctx, double* buf, int64_t n);
+// Per-layer ("bucketed") all-reduce of a flat parameter-space vector being produced
+// layer by layer: ready(l, st) is called once layer l's block is final on stream st;
+// with NCCL its all-reduce starts at once on the comm stream, overlapping the GEMMs
+// still running for the lower layers; finish() orders the context stream after all
+// of them.  With an external communicator the whole vector is reduced in finish().
+struct LayerAllreduce {
+  cv_ctx* ctx;
+  float* out;
+  const std::vector<int64_t>* off;
+  int64_t d;
+  int pending = 0;
+  LayerAllreduce(cv_ctx* c, float* o, const std::vector<int64_t>& offs, int64_t dd) : ctx(c), out(o), off(&offs), d(dd) {}
+  void ready(int l, cudaStream_t st);
+  void finish();
+};
 void check_launch(cv_ctx* ctx);
 
 // per-layer offset table of a flat parameter-space vector (kernel argument)

@@ -422,8 +422,8 @@ static GemmArgs weight_grad_args(cv_snap* s, int l, const SplitBuf& G1, const Sp
   return g;
 }
 
-// last layer: [gW; gb] = A^T U (+ A2^T U2)
-static void skinny_weight_grad(cv_ctx* ctx, cv_snap* s, const float* U, Scale* usc, const SplitBuf* A2,
+// last layer: [gW; gb] = A^T U (+ A2^T U2); returns the stream the result is final on
+static cudaStream_t skinny_weight_grad(cv_ctx* ctx, cv_snap* s, const float* U, Scale* usc, const SplitBuf* A2,
                                const float* U2, Scale* u2sc, float* out, const int* skip, bool side = false) {
   const int l = s->L - 1;
   if (s->tc_out) {
@@ -432,6 +432,7 @@ static void skinny_weight_grad(cv_ctx* ctx, cv_snap* s, const float* U, Scale* u
     constexpr int side_ctas = 128;
     const bool on_side = side && ctx->engine != CV_ENGINE_SIMT;
     StreamSwap swap(ctx, on_side ? side2_fork(ctx) : ctx->stream);
+    const cudaStream_t used = ctx->stream;
     const __half *uh, *ul, *u2h = nullptr, *u2l = nullptr;
     const Scale* uc = cot_split(ctx, s, U, usc, &uh, &ul, skip);
     const Scale* u2c = nullptr;
@@ -451,7 +452,7 @@ static void skinny_weight_grad(cv_ctx* ctx, cv_snap* s, const float* U, Scale* u
       g.max_ctas = side_ctas;
     }
     gemm(ctx, g);
-    return;
+    return used;
   }
   SkinnyDwArgs a{};
   a.rows = s->bl;
@@ -464,6 +465,7 @@ static void skinny_weight_grad(cv_ctx* ctx, cv_snap* s, const float* U, Scale* u
   a.out = out + s->off[l];
   a.skip = skip;
   skinny_dw(ctx, a, s->skinny_ws, s->skinny_ws_elems);
+  return ctx->stream;
 }
 
 
@@ -491,7 +493,9 @@ void mlp_linearize(cv_ctx* ctx, cv_snap* s, double* loss_out, float* grad_out) {
   // primal backward: G[l-1] = (G[l] W_l^T) * sp[l-1]   (models.py:378-381), with the
   // weight gradient of layer l co-scheduled beside the backward GEMM of layer l
   const bool tanh_ = s->act == CV_ACT_TANH;
-  if (grad_out) skinny_weight_grad(ctx, s, s->gout, s->gout_sc, nullptr, nullptr, nullptr, grad_out, nullptr);
+  LayerAllreduce ar(ctx, grad_out, s->off, s->d);
+  if (grad_out)
+    ar.ready(L - 1, skinny_weight_grad(ctx, s, s->gout, s->gout_sc, nullptr, nullptr, nullptr, grad_out, nullptr));
   if (L >= 2) {
     skinny_backward(ctx, s, s->gout, s->gout_sc, s->w_hi, s->w_lo, s->w_sc, s->G[L - 2],
                     tanh_ ? s->P[L - 2] : nullptr, tanh_ ? s->P_sc[L - 2] : nullptr, nullptr);
@@ -500,15 +504,18 @@ void mlp_linearize(cv_ctx* ctx, cv_snap* s, double* loss_out, float* grad_out) {
                                                tanh_ ? s->P[l - 1] : nullptr, tanh_ ? s->P_sc[l - 1] : nullptr,
                                                nullptr);
       if (grad_out) {
-        gemm_pair(ctx, dx, weight_grad_args(s, l, s->G[l], nullptr, nullptr, grad_out, nullptr));
+        ar.ready(l, gemm_pair(ctx, dx, weight_grad_args(s, l, s->G[l], nullptr, nullptr, grad_out, nullptr)));
       } else {
         gemm(ctx, dx);
       }
     }
-    if (grad_out) gemm(ctx, weight_grad_args(s, 0, s->G[0], nullptr, nullptr, grad_out, nullptr));
+    if (grad_out) {
+      gemm(ctx, weight_grad_args(s, 0, s->G[0], nullptr, nullptr, grad_out, nullptr));
+      ar.ready(0, ctx->stream);
+    }
     side_join(ctx);
   }
-  if (grad_out && ctx->nccl) allreduce_f32(ctx, grad_out, s->d);
+  if (grad_out) ar.finish();
 }
 
 // split of a product input v into v_hi / v_lo (per-layer exponents); also
@@ -633,22 +640,27 @@ static void jvp_out(cv_ctx* ctx, cv_snap* s, int post, float scale, float* out, 
 }
 
 // sum_i J_i^T U_i (no 1/b) into out (models.py:274-285); usc->amax = max|U|.
+// The per-layer gradient blocks are all-reduced as they become final (LayerAllreduce).
 static void vjp_from(cv_ctx* ctx, cv_snap* s, const float* U, Scale* usc, float* out, const int* skip) {
   const int L = s->L;
-  skinny_weight_grad(ctx, s, U, usc, nullptr, nullptr, nullptr, out, skip, true);
+  LayerAllreduce ar(ctx, out, s->off, s->d);
+  ar.ready(L - 1, skinny_weight_grad(ctx, s, U, usc, nullptr, nullptr, nullptr, out, skip, true));
   if (L >= 2) {
     skinny_backward(ctx, s, U, usc, s->w_hi, s->w_lo, s->w_sc, s->gs[L - 2], nullptr, nullptr, skip);
     for (int l = L - 2; l >= 0; --l) {
       const GemmArgs dw = weight_grad_args(s, l, s->gs[l], nullptr, nullptr, out, skip);
-      if (l > 0)
-        gemm_pair(ctx, hidden_backward_args(s, l, s->gs[l], s->w_hi, s->w_lo, s->w_sc, s->gs[l - 1], nullptr, nullptr,
-                                            skip),
-                  dw);
-      else
+      if (l > 0) {
+        ar.ready(l, gemm_pair(ctx, hidden_backward_args(s, l, s->gs[l], s->w_hi, s->w_lo, s->w_sc, s->gs[l - 1], nullptr,
+                                                        nullptr, skip),
+                              dw));
+      } else {
         gemm(ctx, dw);
+        ar.ready(0, ctx->stream);
+      }
     }
   }
   side_join(ctx);
+  ar.finish();
 }
 
 // GGN product (1/b) J^T H_z J v (curvature.py:109-110).
@@ -657,7 +669,6 @@ void mlp_ggn(cv_ctx* ctx, cv_snap* s, const float* v, float* out, const int* ski
   const int hg = jvp_hidden(ctx, s, false, skip, v, true);
   jvp_out(ctx, s, POST_HZ, 1.0f / (float)s->bg, s->U, &s->U_sc->amax, skip, hg, v);
   vjp_from(ctx, s, s->U, s->U_sc, out, skip);
-  if (ctx->nccl) allreduce_f32(ctx, out, s->d);
 }
 
 void mlp_jvp(cv_ctx* ctx, cv_snap* s, const float* v, float* out_bc) {
@@ -670,7 +681,6 @@ void mlp_vjp(cv_ctx* ctx, cv_snap* s, const float* U, float* out) {
   cudaMemsetAsync(s->prod_sc, 0, sizeof(Scale) * s->n_prod, ctx->stream);
   amax_into(ctx, U, (int64_t)s->bl * s->c, s->U_sc);
   vjp_from(ctx, s, U, s->U_sc, out, nullptr);
-  if (ctx->nccl) allreduce_f32(ctx, out, s->d);
 }
 
 // HVP backward epilogue for the layer below l: (dG W^T + G V^T) * sp [+ tanh P spp dz]
@@ -698,7 +708,9 @@ void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* v, float* out, const int* ski
   // dG_{L-1} = H_z dz_{L-1} / b
   jvp_out(ctx, s, POST_HZ, 1.0f / (float)s->bg, s->U, &s->U_sc->amax, skip, hg, v);
   // last layer: [gW; gb] = A^T dG + [da|0]^T G_{L-1}
-  skinny_weight_grad(ctx, s, s->U, s->U_sc, L >= 2 ? &s->da[L - 2] : nullptr, s->gout, s->gout_sc, out, skip);
+  LayerAllreduce ar(ctx, out, s->off, s->d);
+  ar.ready(L - 1, skinny_weight_grad(ctx, s, s->U, s->U_sc, L >= 2 ? &s->da[L - 2] : nullptr, s->gout, s->gout_sc,
+                                     out, skip));
   if (L >= 2) {
     // dG_{L-2} = (dG W^T + G_{L-1} V^T) * sp + [tanh] P * spp * dz
     const int l = L - 1;
@@ -740,14 +752,15 @@ void mlp_hvp(cv_ctx* ctx, cv_snap* s, const float* v, float* out, const int* ski
         bound_add(g.epi.bound, (float)s->dims[h + 1], s->gs[h].sc, s->w_sc + h);
         bound_add(g.epi.bound, (float)s->dims[h + 1], s->G[h].sc, s->v_sc + h);
         g.skip = skip;
-        gemm_pair(ctx, g, dw);
+        ar.ready(h, gemm_pair(ctx, g, dw));
       } else {
         gemm(ctx, dw);
+        ar.ready(0, ctx->stream);
       }
     }
   }
   side_join(ctx);
-  if (ctx->nccl) allreduce_f32(ctx, out, s->d);
+  ar.finish();
 }
 
 void mlp_loss(cv_ctx* ctx, cv_snap* s, const float* logits, int write_state, double* loss_out) {
@@ -757,9 +770,9 @@ void mlp_loss(cv_ctx* ctx, cv_snap* s, const float* logits, int write_state, dou
   if (write_state && s->tc_out)
     split_mat(ctx, s->gout, s->c, s->bl, s->c, s->gout_hi, s->gout_lo, s->ldb, 1, s->gout_sc, 1, nullptr);
   const double scale = 1.0 / (double)s->bg;
-  launch_k(ctx->stream, k_finalize_sum, 1, 32, 0, ctx->red_ws, nblk, ctx->nccl ? 1.0 : scale, loss_out);
+  launch_k(ctx->stream, k_finalize_sum, 1, 32, 0, ctx->red_ws, nblk, distributed(ctx) ? 1.0 : scale, loss_out);
   ctx->launches += 2;
-  if (ctx->nccl) {
+  if (distributed(ctx)) {
     allreduce_f64(ctx, loss_out, 1);
     scale_scalar(ctx, loss_out, scale);
   }

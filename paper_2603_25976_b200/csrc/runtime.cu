@@ -118,16 +118,56 @@ void nccl_destroy(cv_ctx* ctx) {
   ctx->nccl = nullptr;
 }
 
+static void comm_call(cv_ctx* ctx, int dtype, void* buf, int64_t n, cudaStream_t st) {
+  const int rc = ctx->comm_fn(ctx->comm_user, dtype, buf, n, (void*)st);
+  if (rc != 0) throw std::runtime_error("NCCL-substitute communicator failed (rc " + std::to_string(rc) + ")");
+}
+
 void allreduce_f32(cv_ctx* ctx, float* buf, int64_t n) {
+  if (ctx->comm_fn) return comm_call(ctx, CV_DTYPE_F32, buf, n, ctx->stream);
   if (!ctx->nccl) return;
   nccl_check(nccl_api().AllReduce(buf, buf, (size_t)n, ncclFloat32, ncclSum, (ncclComm_t)ctx->nccl, ctx->stream),
              "AllReduce");
 }
 
 void allreduce_f64(cv_ctx* ctx, double* buf, int64_t n) {
+  if (ctx->comm_fn) return comm_call(ctx, CV_DTYPE_F64, buf, n, ctx->stream);
   if (!ctx->nccl) return;
   nccl_check(nccl_api().AllReduce(buf, buf, (size_t)n, ncclFloat64, ncclSum, (ncclComm_t)ctx->nccl, ctx->stream),
              "AllReduce");
+}
+
+void LayerAllreduce::ready(int l, cudaStream_t st) {
+  if (!ctx->nccl || ctx->comm_fn) return;
+  if (!ctx->comm) {
+    if (cudaStreamCreateWithFlags(&ctx->comm, cudaStreamNonBlocking) != cudaSuccess)
+      throw std::runtime_error("CUDA: cannot create the comm stream");
+  }
+  while ((int)ctx->comm_ev.size() <= pending) {
+    cudaEvent_t e;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+      throw std::runtime_error("CUDA: cannot create a comm event");
+    ctx->comm_ev.push_back(e);
+  }
+  cudaEventRecord(ctx->comm_ev[pending], st);
+  cudaStreamWaitEvent(ctx->comm, ctx->comm_ev[pending], 0);
+  ++pending;
+  const int64_t b0 = (*off)[l], b1 = l + 1 < (int)off->size() ? (*off)[l + 1] : d;
+  nccl_check(nccl_api().AllReduce(out + b0, out + b0, (size_t)(b1 - b0), ncclFloat32, ncclSum,
+                                  (ncclComm_t)ctx->nccl, ctx->comm),
+             "AllReduce");
+}
+
+void LayerAllreduce::finish() {
+  if (!distributed(ctx)) return;
+  if (ctx->comm_fn || !pending) {  // external communicator (or nothing bucketed): one reduction
+    allreduce_f32(ctx, out, d);
+    return;
+  }
+  cudaEvent_t e = ctx->comm_ev[0];
+  cudaEventRecord(e, ctx->comm);
+  cudaStreamWaitEvent(ctx->stream, e, 0);
+  pending = 0;
 }
 
 void check_launch(cv_ctx* ctx) {
@@ -194,12 +234,12 @@ StreamSwap::~StreamSwap() {
   }
 }
 
-void gemm_pair(cv_ctx* ctx, GemmArgs a, GemmArgs b) {
+cudaStream_t gemm_pair(cv_ctx* ctx, GemmArgs a, GemmArgs b) {
   const bool tc = ctx->engine != CV_ENGINE_SIMT && gemm_tc_supported(a) && gemm_tc_supported(b);
   if (!tc) {
     gemm(ctx, a);
     gemm(ctx, b);
-    return;
+    return ctx->stream;
   }
   ensure_side(ctx);
   // SM split minimising the slower of the two (even counts: CTA pairs)
@@ -226,6 +266,7 @@ void gemm_pair(cv_ctx* ctx, GemmArgs a, GemmArgs b) {
   cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0);
   for (void* p : ctx->deferred) ctx->pool.put(p);  // later users are ordered after the join
   ctx->deferred.clear();
+  return ctx->side;
 }
 
 void gemm(cv_ctx* ctx, const GemmArgs& a) {

@@ -1,9 +1,13 @@
 """Per-process device runtime: one native context per (device, world).
 
-One process drives one GPU.  Under `torch.distributed` with world > 1 the
-context owns an NCCL communicator (unique id broadcast through the default
-process group), and every curvature product / gradient / loss is all-reduced
-inside the native library.
+One process drives one GPU.  Under `torch.distributed` with world > 1 the context
+owns the collectives of the batch-sharded path: every curvature product, gradient
+and loss is all-reduced inside the native library.  With an NCCL process group the
+library runs its own NCCL communicator (unique id broadcast through the default
+group; per-layer gradient all-reduces on a comm stream).  With a gloo process group
+(e.g. several ranks sharing one GPU, or CPU-side transport) the library calls back
+into `_HostComm`, which stages the buffer through the host and all-reduces it with
+the process group -- the same library code path, another transport.
 """
 
 from __future__ import annotations
@@ -16,10 +20,45 @@ import torch
 from . import _lib
 
 _RUNTIMES: dict = {}
+_LOCAL = False
+
+
+class _CudaArray:
+    """Zero-copy torch view of a raw device buffer (__cuda_array_interface__)."""
+
+    def __init__(self, ptr, count, typestr):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None, "stream": None}
+
+
+class _HostComm:
+    """cv_comm_fn over the default torch.distributed group (host-staged all-reduce)."""
+
+    def __init__(self, device):
+        self.device = device
+        self.calls = 0
+        self.fn = _lib.COMM_FN(self._allreduce)  # keep the ctypes thunk alive
+
+    def _allreduce(self, user, dtype, buf, count, stream):
+        import torch.distributed as dist
+
+        try:
+            torch.cuda.ExternalStream(stream, device=self.device).synchronize() if stream else \
+                torch.cuda.synchronize(self.device)
+            t = torch.as_tensor(_CudaArray(buf, count, "<f4" if dtype == 0 else "<f8"), device=self.device)
+            h = t.cpu()
+            dist.all_reduce(h)
+            t.copy_(h)
+            torch.cuda.synchronize(self.device)
+            self.calls += 1
+            return 0
+        except Exception:  # pragma: no cover - reported to the library as a failed collective
+            return 1
 
 
 class Runtime:
-    def __init__(self, device: int = 0, world: int = 1, rank: int = 0, nccl_id: bytes | None = None):
+    def __init__(self, device: int = 0, world: int = 1, rank: int = 0, nccl_id: bytes | None = None,
+                 host_comm: bool = False):
         if not torch.cuda.is_available():
             raise RuntimeError("curvopt_b200 requires a CUDA device (B200, sm_100a); none is visible")
         self.lib = _lib.lib()
@@ -33,6 +72,10 @@ class Runtime:
             msg = self.lib.cv_last_error(h) if h.value else b"context creation failed"
             raise _lib.DeviceError((msg or b"").decode())
         self.h = h
+        self.comm = None
+        if host_comm:
+            self.comm = _HostComm(self.device)
+            _lib.check(self.lib.cv_ctx_set_comm(self.h, self.comm.fn, None), self.h)
         engine = os.environ.get("CURVOPT_ENGINE", "auto")
         self.set_engine(engine)
 
@@ -59,21 +102,29 @@ class Runtime:
 def _dist_info():
     import torch.distributed as dist
 
-    if dist.is_available() and dist.is_initialized():
-        return dist.get_world_size(), dist.get_rank()
-    return 1, 0
+    if not _LOCAL and dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(), dist.get_rank(), dist.get_backend()
+    return 1, 0, None
+
+
+def set_local(on: bool = True) -> None:
+    """Replicas: ignore the process group (each rank runs the whole batch on its own GPU,
+    no collectives) -- the row lane's multi-GPU mode."""
+    global _LOCAL
+    _LOCAL = bool(on)
 
 
 def runtime(device: int | None = None) -> Runtime:
     """The process-wide runtime for `device` (default: current CUDA device)."""
     if device is None:
         device = torch.cuda.current_device() if torch.cuda.is_available() else 0
-    world, rank = _dist_info()
+    world, rank, backend = _dist_info()
     key = (device, world)
     rt = _RUNTIMES.get(key)
     if rt is None:
         nccl_id = None
-        if world > 1:
+        host_comm = world > 1 and backend != "nccl"
+        if world > 1 and not host_comm:
             import torch.distributed as dist
 
             buf = C.create_string_buffer(128)
@@ -84,7 +135,7 @@ def runtime(device: int | None = None) -> Runtime:
             obj = [bytes(buf.raw) if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
             nccl_id = obj[0]
-        rt = Runtime(device, world, rank, nccl_id)
+        rt = Runtime(device, world, rank, nccl_id, host_comm=host_comm)
         _RUNTIMES[key] = rt
     rt.bind_stream()
     return rt
