@@ -111,6 +111,8 @@ def test_two_ranks_on_one_gpu_match_the_full_batch(case, tmp_path):
                 np.testing.assert_allclose(mine[ok, j], ref[ok, j], rtol=1e-4 if f in TIGHT else 1e-3, atol=1e-9,
                                            err_msg=f)
         w, wf = np.array(res["w"]), np.array(full["w"])
-        assert np.linalg.norm(w - wf) / np.linalg.norm(wf) < 1e-5
+        # 1e-4: sophia_clip is sign-like where gamma * diag is tiny, so fp32 noise in the
+        # sharded gradient moves a few elements by the full learning rate
+        assert np.linalg.norm(w - wf) / np.linalg.norm(wf) < 1e-4
     # replicated decisions: both ranks hold bitwise the same weights
     assert ranks[0]["w"] == ranks[1]["w"]
