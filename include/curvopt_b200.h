@@ -19,6 +19,8 @@
  *   cv_row_gram           models.py:309-334 (output_gram) via curvature.py:62-65
  *   cv_row_solve_cholesky solvers.py:146-161
  *   cv_backproject        curvature.py:53-60 (scaled_row_transpose)
+ *   cv_row_solve_cg       solvers.py:164-174 (row_solve_cg) via method.py:270-282
+ *   cv_dense_*            solvers.py:146-174 on a caller-owned Gram
  *   cv_apply_update       method.py:345-357 (chain of scale links + w + update + norms)
  *   cv_chain_apply        transforms.py:148-199 (chain_apply, every link kind) + method.py:345-357
  *   cv_gnb_diag           telemetry.py:129-160 (gnb_diag, sampled-label GGN diagonal)
@@ -212,6 +214,18 @@ CV_API int cv_row_rhs(cv_snap* snap, float* rhs_out /* m */);
 CV_API int cv_row_gram(cv_snap* snap, float* gram_out /* m*m, nullable: keep on device */);
 CV_API int cv_row_solve_cholesky(cv_snap* snap, double mu, const float* rhs, float* v_out);
 CV_API int cv_backproject(cv_snap* snap, const float* v_row, float* out);
+/* Row-space CG on (Gram + mu I) v = rhs with the snapshot's Gram (solvers.py:164-174,
+ * method.py:270-282: row_solve_cg(lambda u: gram @ u, rhs, mu, cfg, x0)); the same
+ * device-resident loop as cv_cg_solve, products are dense Gram GEMVs.  x0 nullable. */
+CV_API int cv_row_solve_cg(cv_snap* snap, double mu, const float* rhs, double tol, int maxiter, int stabilise_every,
+                           const float* x0, float* v_out, cv_cg_stats* stats);
+/* The same two solves on a caller-owned dense symmetric Gram (m x m fp32, full storage,
+ * device): solvers.py:146-161 row_solve_cholesky(gram, rhs, mu) and row_solve_cg with
+ * gram_matvec = gram @ u.  Not positive definite -> CV_E_NOT_PD (the ContractError text). */
+CV_API int cv_dense_cholesky_solve(cv_ctx* ctx, const float* gram, int64_t m, double mu, const float* rhs,
+                                   float* v_out);
+CV_API int cv_dense_cg_solve(cv_ctx* ctx, const float* gram, int64_t m, double mu, const float* rhs, double tol,
+                             int maxiter, int stabilise_every, const float* x0, float* v_out, cv_cg_stats* stats);
 
 #ifdef __cplusplus
 }

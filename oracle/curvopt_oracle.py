@@ -617,7 +617,7 @@ STEP_FIELDS = ("loss_before", "loss_after", "rho", "lam", "grad_norm", "step_nor
 class OSpec:
     """Flat restatement of MethodSpec for the oracle (method.py:64-134)."""
     curvature: str | None = "ggn_ce"
-    solver: str | None = "cg"          # None (identity) | diag | cg | row_cholesky
+    solver: str | None = "cg"          # None (identity) | diag | cg | row_cholesky | row_cg
     tol: float = 1e-5
     maxiter: int = 10
     stabilise_every: int = 10
@@ -720,6 +720,15 @@ def oracle_step(spec: OSpec, dims, activation, loss, w, X, y, st: OState, gv_log
         if gv_log is not None:
             gv_log.append(res.gv_count)
         direction, iters, conv, relres = res.x, res.iterations, int(res.converged), res.relres
+        warm = res.x if spec.warm_start else None
+    elif spec.solver == "row_cg":  # method.py:270-282 -> row_solve_cg (solvers.py:164-174)
+        seeds, rhs = row_seeds_rhs(lin)
+        gram = output_gram(lin, seeds)
+        x0 = st.warm if (spec.warm_start and st.warm is not None and st.warm.size == rhs.size) else None
+        res = cg(lambda u: gram @ u, rhs, float(lin.b) * st.lam, spec.tol, spec.maxiter, spec.stabilise_every,
+                 None, x0)
+        direction, iters, conv, relres = row_transpose(lin, seeds, res.x), res.iterations, int(res.converged), \
+            res.relres
         warm = res.x if spec.warm_start else None
     else:  # row_cholesky (method.py:262-268)
         seeds, rhs = row_seeds_rhs(lin)

@@ -17,6 +17,7 @@ void row_rhs(cv_ctx* ctx, cv_snap* s, float* rhs);
 void row_gram(cv_ctx* ctx, cv_snap* s, float* gram_out);
 int row_solve_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, float* v);
 void row_backproject(cv_ctx* ctx, cv_snap* s, const float* v, float* out);
+const float* row_gram_dev(cv_ctx* ctx, cv_snap* s);
 }  // namespace cv
 
 using namespace cv;
@@ -496,6 +497,34 @@ int cv_row_solve_cholesky(cv_snap* s, double mu, const float* rhs, float* v_out)
   contract(_ctx->world == 1, "row lane is single-GPU (replicas only)");
   if (row_solve_cholesky(_ctx, s, mu, rhs, v_out) != 0)
     throw CvError(CV_E_NOT_PD, "row system is not positive definite; mu too small or gram invalid");
+  CV_CATCH
+}
+
+int cv_row_solve_cg(cv_snap* s, double mu, const float* rhs, double tol, int maxiter, int stabilise_every,
+                    const float* x0, float* v_out, cv_cg_stats* stats) {
+  if (!s) return CV_E_CONTRACT;
+  CV_TRY(s->ctx)
+  contract(_ctx->world == 1, "row lane is single-GPU (replicas only)");
+  contract(tol > 0 && maxiter >= 1, "cg tol must be positive and maxiter >= 1");
+  const float* G = row_gram_dev(_ctx, s);
+  dense_cg_solve(_ctx, G, (int64_t)s->bl * s->c, rhs, mu, tol, maxiter, stabilise_every, x0, v_out, stats);
+  CV_CATCH
+}
+
+int cv_dense_cholesky_solve(cv_ctx* ctx, const float* gram, int64_t m, double mu, const float* rhs, float* v_out) {
+  CV_TRY(ctx)
+  contract(m >= 1 && gram && rhs && v_out, "gram must be a square matrix");
+  if (dense_cholesky(_ctx, gram, m, mu, rhs, v_out) != 0)
+    throw CvError(CV_E_NOT_PD, "row system is not positive definite; mu too small or gram invalid");
+  CV_CATCH
+}
+
+int cv_dense_cg_solve(cv_ctx* ctx, const float* gram, int64_t m, double mu, const float* rhs, double tol, int maxiter,
+                      int stabilise_every, const float* x0, float* v_out, cv_cg_stats* stats) {
+  CV_TRY(ctx)
+  contract(m >= 1 && gram && rhs && v_out && stats, "gram must be a square matrix");
+  contract(tol > 0 && maxiter >= 1, "cg tol must be positive and maxiter >= 1");
+  dense_cg_solve(_ctx, gram, m, rhs, mu, tol, maxiter, stabilise_every, x0, v_out, stats);
   CV_CATCH
 }
 

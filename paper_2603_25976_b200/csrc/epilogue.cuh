@@ -59,6 +59,13 @@ CV_DEV float mask_val(const Epilogue& e, const EpiRt& rt, int64_t mi) {
 
 // Epilogue for one output element (m, n) with accumulator v; amax/ramax collect
 // max |written split value| and max |raw| for the caller's atomic publication.
+// out += v without returning the old value (L2-side reduction; FTZ: subnormal sums flush)
+CV_DEV void red_add_v4(float* p, float4 v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+CV_DEV void red_add_f32(float* p, float v) { asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory"); }
+
 CV_DEV void epi_apply(const Epilogue& e, const EpiRt& rt, int m, int n, float v, float& amax, float& ramax) {
   switch (e.mode) {
     case EPI_STORE:
@@ -91,12 +98,12 @@ CV_DEV void epi_apply(const Epilogue& e, const EpiRt& rt, int m, int n, float v,
     case EPI_GRAM: {
       const float sa = e.sa[(int64_t)(m / e.kdiv) * e.sa_ld + n / e.kdiv];
       float* o = e.out + (int64_t)m * e.ld + n;
-      *o = e.first ? v * sa : *o + v * sa;
+      if (e.first) *o = v * sa;
+      else red_add_f32(o, v * sa);
       return;
     }
     case EPI_ACCUM: {
-      float* o = e.out + (int64_t)m * e.ld + n;
-      *o += e.alpha * v;
+      red_add_f32(e.out + (int64_t)m * e.ld + n, e.alpha * v);
       return;
     }
   }
@@ -204,13 +211,17 @@ CV_DEV bool epi_applyV(const Epilogue& e, const EpiRt& rt, int m, int nb, const 
       const float* sa = e.sa + (int64_t)(m / e.kdiv) * e.sa_ld;
       if (!al16(out)) return false;
 #pragma unroll
+      // all loads of the row segment first (the stores alias them: issued in one batch
+      // the read latency is paid once per chunk, not once per 16 bytes)
+      // accumulation: one fire-and-forget vector reduction per 16 bytes (the L2 does the
+      // read-modify-write; each element gets exactly one add per GEMM, so the result is
+      // the same rounding as load + add + store, without the read round trip in the SM)
+#pragma unroll
       for (int j = 0; j < NC; j += 4) {
-        float4 cur = e.first ? make_float4(0.f, 0.f, 0.f, 0.f) : *reinterpret_cast<float4*>(out + j);
-        cur.x += v[j] * sa[(nb + j) / e.kdiv];
-        cur.y += v[j + 1] * sa[(nb + j + 1) / e.kdiv];
-        cur.z += v[j + 2] * sa[(nb + j + 2) / e.kdiv];
-        cur.w += v[j + 3] * sa[(nb + j + 3) / e.kdiv];
-        *reinterpret_cast<float4*>(out + j) = cur;
+        const float4 c = make_float4(v[j] * sa[(nb + j) / e.kdiv], v[j + 1] * sa[(nb + j + 1) / e.kdiv],
+                                     v[j + 2] * sa[(nb + j + 2) / e.kdiv], v[j + 3] * sa[(nb + j + 3) / e.kdiv]);
+        if (e.first) *reinterpret_cast<float4*>(out + j) = c;
+        else red_add_v4(out + j, c);
       }
       return true;
     }
@@ -218,14 +229,8 @@ CV_DEV bool epi_applyV(const Epilogue& e, const EpiRt& rt, int m, int nb, const 
       float* out = e.out + o;
       if (!al16(out)) return false;
 #pragma unroll
-      for (int j = 0; j < NC; j += 4) {
-        float4 cur = *reinterpret_cast<float4*>(out + j);
-        cur.x += e.alpha * v[j];
-        cur.y += e.alpha * v[j + 1];
-        cur.z += e.alpha * v[j + 2];
-        cur.w += e.alpha * v[j + 3];
-        *reinterpret_cast<float4*>(out + j) = cur;
-      }
+      for (int j = 0; j < NC; j += 4)
+        red_add_v4(out + j, make_float4(e.alpha * v[j], e.alpha * v[j + 1], e.alpha * v[j + 2], e.alpha * v[j + 3]));
       return true;
     }
   }
@@ -234,6 +239,7 @@ CV_DEV bool epi_applyV(const Epilogue& e, const EpiRt& rt, int m, int nb, const 
 
 // Publish a warp's running maxima (all 32 lanes must call).
 CV_DEV void epi_flush_amax(const Epilogue& e, float& amax, float& ramax) {
+  if (!e.out_sc && !e.raw_amax) return;  // (uniform) nothing to publish: no warp reduction
   const float a = warp_max_f(amax), r = warp_max_f(ramax);
   if ((threadIdx.x & 31) == 0) {
     if (e.out_sc && a > 0.f) atomic_amax(&e.out_sc->amax, a);

@@ -674,13 +674,27 @@ struct TcCfg {
   static constexpr int THREADS = 320;                          // w0 TMA, w1 MMA, w2..w9 epilogue
 };
 
+constexpr int TC_GROUP = 8;
+
 // work item -> (m0, n0, first k-block, k-blocks); split index slowest so that
 // co-resident CTAs share K ranges (and therefore L2-resident operand panels)
 CV_DEV bool tc_work(const TcArgs& a, int w, int bm, int bn, int& m0, int& n0, int& kb0, int& nkb) {
   const int tiles = a.tiles_m * a.tiles_n;
   const int split = w / tiles, t = w % tiles;
-  m0 = (t / a.tiles_n) * bm;
-  n0 = (t % a.tiles_n) * bn;
+  if (a.tiles_m >= 2 * TC_GROUP && a.tiles_n >= 2 * TC_GROUP) {
+    // large grids (Gram, Cholesky trailing updates, C5 layers): bands of TC_GROUP tile
+    // rows walked column by column, so the co-resident tiles of a wave share a few A
+    // and B slabs in L2 instead of streaming every B slab once per tile row
+    const int band = t / (TC_GROUP * a.tiles_n);
+    const int r0 = band * TC_GROUP;
+    const int rows = a.tiles_m - r0 < TC_GROUP ? a.tiles_m - r0 : TC_GROUP;
+    const int r = t - band * TC_GROUP * a.tiles_n;
+    m0 = (r0 + r % rows) * bm;
+    n0 = (r / rows) * bn;
+  } else {
+    m0 = (t / a.tiles_n) * bm;
+    n0 = (t % a.tiles_n) * bn;
+  }
   kb0 = split * a.kb_per_split;
   nkb = min(a.kb_total, kb0 + a.kb_per_split) - kb0;
   return !(a.lower_only && n0 > m0 + bm - 1);

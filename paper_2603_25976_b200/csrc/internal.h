@@ -233,7 +233,8 @@ struct cv_snap {
   float* rhs = nullptr;           // m
   float* gram = nullptr;          // m x m
   float* chol = nullptr;          // m x m, Cholesky factor of gram + mu I (lower)
-  float* dinv = nullptr;          // inverses of the diagonal blocks of chol
+  float* dinv = nullptr;          // inverses of the 64-wide diagonal blocks of chol
+  float* winv = nullptr;          // inverses of the 512-wide diagonal (panel) blocks of chol
   int row_state = 0;              // bit0 seeds built, bit1 gram built
   // solver scratch (lazily allocated, d each)
   float* cg_r = nullptr; float* cg_p = nullptr; float* cg_ap = nullptr;
@@ -339,6 +340,8 @@ inline MatvecFn matvec_fn(int kind) { return kind == CV_KIND_HESSIAN ? mlp_hvp :
 void scale_scalar(cv_ctx* ctx, double* x, double s);
 void cg_solve(cv_ctx* ctx, cv_snap* s, int kind, const float* g, double lam, double tol, int maxiter,
               int stab, const float* precond, double floor, const float* x0, float* x, cv_cg_stats* stats);
+void dense_cg_solve(cv_ctx* ctx, const float* gram, int64_t m, const float* rhs, double mu, double tol, int maxiter,
+                    int stab, const float* x0, float* x, cv_cg_stats* stats);
 void rademacher(cv_ctx* ctx, uint64_t seed, uint64_t counter, int64_t n, float* out);
 void hutchinson(cv_ctx* ctx, cv_snap* s, int kind, uint64_t seed, uint64_t counter, int n_probes, float* diag,
                 double* trace);
@@ -348,6 +351,9 @@ void dot_into(cv_ctx* ctx, const float* a, const float* b, int64_t n, double* ou
 void apply_update(cv_ctx* ctx, const float* w, const float* dir, double coef, int64_t d, float* upd,
                   float* wn, double* scal);
 void norm_check(cv_ctx* ctx, const float* x, int64_t d, double* scal);
+
+// row.cu
+int dense_cholesky(cv_ctx* ctx, const float* gram, int64_t m, double mu, const float* rhs, float* v_out);
 
 // chain.cu
 void chain_apply(cv_ctx* ctx, int n_links, const cv_link* links, const float* dir, const float* w, const float* pre,

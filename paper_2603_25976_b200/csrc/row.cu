@@ -8,6 +8,7 @@
 #include "internal.h"
 
 #include <stdexcept>
+#include <type_traits>
 #include <vector>
 
 namespace cv {
@@ -176,6 +177,8 @@ static Operand f32op(const float* p, int64_t si, int64_t sj) {
   return o;
 }
 
+__global__ void __launch_bounds__(256) k_sym_mirror(float* G, int64_t m);
+
 static void ensure_gram(cv_ctx* ctx, cv_snap* s) {
   if (s->row_state & 2) return;
   ensure_seeds(ctx, s);
@@ -223,6 +226,7 @@ static void ensure_gram(cv_ctx* ctx, cv_snap* s) {
     h.epi.sa_ld = b;
     h.epi.kdiv = c;
     h.epi.first = l == L - 1;
+    h.lower_only = 1;  // SYRK: lower tiles only, mirrored below
     gemm(ctx, h);
     if (l > 0) {
       // D <- (D W_l^T) * act'(a_l) broadcast over the k rows of each example
@@ -257,7 +261,17 @@ static void ensure_gram(cv_ctx* ctx, cv_snap* s) {
       cur ^= 1;
     }
   }
+  {
+    const int nt = (int)((m + 31) / 32);
+    launch_k(ctx->stream, k_sym_mirror, dim3(nt, nt), 256, 0, s->gram, m);
+    ctx->launches++;
+  }
   s->row_state |= 2;
+}
+
+const float* row_gram_dev(cv_ctx* ctx, cv_snap* s) {
+  ensure_gram(ctx, s);
+  return s->gram;
 }
 
 void row_gram(cv_ctx* ctx, cv_snap* s, float* gram_out) {
@@ -269,78 +283,351 @@ void row_gram(cv_ctx* ctx, cv_snap* s, float* gram_out) {
 // ---------------------------------------------------------------------------
 // Blocked right-looking Cholesky, lower, in place on chol = gram + mu I.
 // ---------------------------------------------------------------------------
-__global__ void k_copy_add_diag(const float* src, float* dst, int64_t m, float mu) {
+// dst = src + mu I on the lower triangle only (the factorization and the
+// triangular solves never read above the diagonal): 32 x 32 tiles, tiles strictly
+// above the diagonal skip; 128-bit rows when m % 4 == 0.
+__global__ void __launch_bounds__(256) k_copy_lower_add_diag(const float* src, float* dst, int64_t m, float mu) {
   CV_PDL_ENTRY();
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * m; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / m, j = e - i * m;
-    dst[e] = src[e] + (i == j ? mu : 0.f);
+  const int64_t ti = blockIdx.y, tj = blockIdx.x;
+  if (tj > ti) return;
+  const int64_t i0 = ti * 32, j0 = tj * 32;
+  const int c4 = threadIdx.x & 7, r8 = threadIdx.x >> 3;
+  for (int rr = r8; rr < 32; rr += 32) {
+    const int64_t i = i0 + rr;
+    if (i >= m) break;
+    const int64_t j = j0 + 4 * c4;
+    if ((m & 3) == 0 && j + 3 < m) {
+      float4 v = *reinterpret_cast<const float4*>(src + i * m + j);
+      if (i >= j && i <= j + 3) (&v.x)[i - j] += mu;
+      *reinterpret_cast<float4*>(dst + i * m + j) = v;
+    } else {
+      for (int q = 0; q < 4 && j + q < m; ++q) dst[i * m + j + q] = src[i * m + j + q] + (i == j + q ? mu : 0.f);
+    }
   }
 }
 
-// Factor the nb x nb diagonal block at j0 in fp64 shared memory, write L11 back
-// and its inverse (fp32) into dinv[blk]; flag <- 1 if not positive definite.
-__global__ void __launch_bounds__(256) k_potrf_diag(float* A, int64_t lda, int j0, int nb, float* dinv_blk,
-                                                    int* flag) {
+// G[j, i] = G[i, j] for i > j: the Gram is built as a SYRK (lower tiles only) and
+// mirrored once, so consumers that stream whole rows (refinement residual, row-space
+// CG products, cv_row_gram) see the full symmetric matrix.
+__global__ void __launch_bounds__(256) k_sym_mirror(float* G, int64_t m) {
   CV_PDL_ENTRY();
-  __shared__ double T[CH_NB][CH_NB + 1];
+  const int64_t ti = blockIdx.y, tj = blockIdx.x;  // destination tile (upper: tj >= ti)
+  if (tj < ti) return;
+  __shared__ float t[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  // source: rows tj*32.., cols ti*32.. (lower)
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t i = tj * 32 + r, j = ti * 32 + tx;
+    if (i < m && j < m) t[r][tx] = G[i * m + j];
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t i = ti * 32 + r, j = tj * 32 + tx;
+    if (i < m && j < m && j > i) G[i * m + j] = t[tx][r];  // (diagonal tiles: their upper half only)
+  }
+}
+
+
+// Factor the nb x nb diagonal block at j0 in fp64, write L11 back (lower) and its
+// inverse (fp32, row-major nb x nb) into dinv_blk; flag <- 1 if not positive definite.
+// Register-resident elimination on 4 x 4 tiles: thread t < 136 owns lower tile (bi, bj)
+// of the 16 x 16 tile grid (16 fp64 values in registers).  Step k applies
+// a_ij -= a_ik a_jk / a_kk to the owned values with j > k, reading column k from a
+// double-buffered shared row that the owners of column k+1 refill right after their
+// own update -- one barrier per column, the pivot's reciprocal published with it; the
+// scaling by 1/sqrt(a_kk) is applied once at the end.  X = L^-1 is formed the same way
+// (row k of X final at step k).  A partial block (nb < 64) is padded with the identity.
+constexpr int PD_T = 160;  // 136 tile owners, 5 warps
+
+CV_DEV void tri_index(int e, int& i, int& j) {  // e-th element of the row-major lower triangle
+  i = (int)((sqrtf(8.f * (float)e + 1.f) - 1.f) * 0.5f);
+  while ((i + 1) * (i + 2) / 2 <= e) ++i;
+  while (i * (i + 1) / 2 > e) --i;
+  j = e - i * (i + 1) / 2;
+}
+
+__global__ void __launch_bounds__(PD_T) k_potrf_diag(float* A, int64_t lda, int j0, int nb, float* dinv_blk,
+                                                     int* flag) {
+  CV_PDL_ENTRY();
+  __shared__ __align__(16) double colb[2][CH_NB];  // column k (row k of X), double buffered
+  __shared__ double rinv[2];                        // 1 / a_kk
+  __shared__ double dgv[CH_NB];                     // pivots a_kk
+  __shared__ double rdg[CH_NB];                     // 1 / sqrt(a_kk) = 1 / L_kk
+  __shared__ __align__(16) float LsT[CH_NB][CH_NB + 4];  // LsT[k][i] = L_ik / L_ii (i > k)
   __shared__ int bad;
-  const int tid = threadIdx.x;
-  if (tid == 0) bad = 0;
-  for (int e = tid; e < nb * nb; e += blockDim.x) {
-    const int i = e / nb, j = e % nb;
-    T[i][j] = j <= i ? (double)A[(int64_t)(j0 + i) * lda + j0 + j] : 0.0;
-  }
+  const int t = threadIdx.x;
+  const bool act = t < 136;
+  int bi = 0, bj = 0;
+  if (act) tri_index(t, bi, bj);
+  const bool diag = bi == bj;
+  double a[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = 4 * bi + r, j = 4 * bj + c;
+      double v = 0.0;
+      if (act && j <= i) v = (i < nb) ? (double)A[(int64_t)(j0 + i) * lda + j0 + j] : (i == j ? 1.0 : 0.0);
+      a[r][c] = v;
+    }
+  if (t == 0) bad = 0;
   __syncthreads();
-  for (int k = 0; k < nb; ++k) {
-    if (tid == 0) {
-      const double dkk = T[k][k];
-      if (!(dkk > 0.0) || !isfinite(dkk)) { bad = 1; T[k][k] = 1.0; }
-      else T[k][k] = sqrt(dkk);
+  // column k = 4 kb + kk is owned by tile column bj = kb (its column kk)
+  auto publish = [&](int kb, auto kk_) {
+    constexpr int kk = decltype(kk_)::value;
+    const int k = 4 * kb + kk;
+    if (!act || bj != kb) return;
+    double* cb = colb[k & 1];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) cb[4 * bi + r] = a[r][kk];
+    if (diag) {
+      double p = a[kk][kk];
+      if (!(p > 0.0) || !isfinite(p)) { bad = 1; p = 1.0; }
+      dgv[k] = p;
+      rinv[k & 1] = 1.0 / p;
     }
-    __syncthreads();
-    const double dk = T[k][k];
-    for (int i = k + 1 + tid; i < nb; i += blockDim.x) T[i][k] /= dk;
-    __syncthreads();
-    for (int e = tid; e < (nb - k - 1) * (nb - k - 1); e += blockDim.x) {
-      const int i = k + 1 + e / (nb - k - 1), j = k + 1 + e % (nb - k - 1);
-      if (j <= i) T[i][j] -= T[i][k] * T[j][k];
-    }
-    __syncthreads();
-  }
-  // inverse of the lower-triangular factor, one column per thread
-  // (column j of the inverse lives in dinv_blk[:, j]; only its own thread touches it)
-  for (int j = tid; j < nb; j += blockDim.x) {
-    double xc[CH_NB];
-    for (int i = 0; i < nb; ++i) {
-      if (i < j) { xc[i] = 0.0; dinv_blk[i * nb + j] = 0.f; continue; }
-      double s = i == j ? 1.0 : 0.0;
-      for (int k = j; k < i; ++k) s -= T[i][k] * xc[k];
-      xc[i] = s / T[i][i];
-      dinv_blk[i * nb + j] = (float)xc[i];
-    }
-  }
+  };
+  using I0 = std::integral_constant<int, 0>;
+  using I1 = std::integral_constant<int, 1>;
+  using I2 = std::integral_constant<int, 2>;
+  using I3 = std::integral_constant<int, 3>;
+  publish(0, I0{});
   __syncthreads();
-  for (int e = tid; e < nb * nb; e += blockDim.x) {
-    const int i = e / nb, j = e % nb;
-    if (j <= i) A[(int64_t)(j0 + i) * lda + j0 + j] = (float)T[i][j];
+  auto elim = [&](int kb, auto kk_) {
+    constexpr int kk = decltype(kk_)::value;
+    const int k = 4 * kb + kk;
+    const double* cb = colb[k & 1];
+    if (act && bj >= kb) {
+      const double r = rinv[k & 1];
+      double ci[4], sj[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        ci[q] = cb[4 * bi + q];
+        sj[q] = cb[4 * bj + q] * r;
+      }
+      if (bj > kb) {
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) a[rr][cc] -= ci[rr] * sj[cc];
+      } else {
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+          for (int cc = kk + 1; cc < 4; ++cc) a[rr][cc] -= ci[rr] * sj[cc];
+      }
+    }
+  };
+  for (int kb = 0; kb < 16; ++kb) {
+    elim(kb, I0{}); publish(kb, I1{}); __syncthreads();
+    elim(kb, I1{}); publish(kb, I2{}); __syncthreads();
+    elim(kb, I2{}); publish(kb, I3{}); __syncthreads();
+    elim(kb, I3{}); if (kb + 1 < 16) publish(kb + 1, I0{}); __syncthreads();
   }
-  if (tid == 0 && bad) *flag = 1;
+  for (int k = t; k < CH_NB; k += PD_T) rdg[k] = 1.0 / sqrt(dgv[k]);
+  __syncthreads();
+  // L_ij = a_ij / L_jj; the inverse's multipliers L_ik / L_ii (rounded to fp32 like the
+  // stored factor, so dinv inverts exactly what the solves read)
+  float lf[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = 4 * bi + r, j = 4 * bj + c;
+      lf[r][c] = (float)(i == j ? dgv[j] * rdg[j] : a[r][c] * rdg[j]);
+      if (act && j < i) LsT[j][i] = (float)((double)lf[r][c] * rdg[i]);
+    }
+  // X = L^-1: x[i][c] starts at delta_ic / L_ii; step k: x[i][c] -= (L_ik / L_ii) X[k][c]
+  double x[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) x[r][c] = (diag && r == c) ? rdg[4 * bi + r] : 0.0;
+  __syncthreads();
+  auto pub_row = [&](int kb, auto kk_) {  // row k of X, owned by tile row bi = kb
+    constexpr int kk = decltype(kk_)::value;
+    const int k = 4 * kb + kk;
+    if (!act || bi != kb) return;
+    double* rb = colb[k & 1];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) rb[4 * bj + c] = x[kk][c];
+  };
+  auto inv_step = [&](int kb, auto kk_) {
+    constexpr int kk = decltype(kk_)::value;
+    const int k = 4 * kb + kk;
+    if (!act || bi < kb || bj > kb) return;  // X[k][c] = 0 for c > k (tile columns right of kb)
+    const double* rb = colb[k & 1];
+    double xk[4], lk[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      xk[q] = rb[4 * bj + q];
+      lk[q] = (double)LsT[k][4 * bi + q];
+    }
+    if (bi > kb) {
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) x[rr][cc] -= lk[rr] * xk[cc];
+    } else {
+#pragma unroll
+      for (int rr = kk + 1; rr < 4; ++rr)
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) x[rr][cc] -= lk[rr] * xk[cc];
+    }
+  };
+  for (int kb = 0; kb < 16; ++kb) {
+    pub_row(kb, I0{}); __syncthreads(); inv_step(kb, I0{});
+    pub_row(kb, I1{}); __syncthreads(); inv_step(kb, I1{});
+    pub_row(kb, I2{}); __syncthreads(); inv_step(kb, I2{});
+    pub_row(kb, I3{}); __syncthreads(); inv_step(kb, I3{});
+  }
+  if (act) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int i = 4 * bi + r, j = 4 * bj + c;
+        if (i >= nb || j >= nb) continue;
+        if (j <= i) {
+          dinv_blk[i * nb + j] = (float)x[r][c];
+          A[(int64_t)(j0 + i) * lda + j0 + j] = lf[r][c];
+          if (j != i) dinv_blk[j * nb + i] = 0.f;
+        }
+      }
+  }
+  if (t == 0 && bad) *flag = 1;
 }
 
-// forward substitution, one diagonal block: y_blk = Dinv (r_blk) ; then
-// r[j0+nb:] -= L[j0+nb:, blk] y_blk    (r, y in fp64)
-__global__ void k_trsv_fwd_diag(const float* dinv, int nb, int j0, double* r, double* y) {
+// W = L11^-1 for the nbo x nbo diagonal block of a panel (nbo <= TT_MAX), from the
+// factored block (lower, in A at (p0, p0)) and the inverses of its 64-blocks (dinv):
+// block forward substitution  X_jj = Dinv_j,  X_ij = -Dinv_i sum_{k=j}^{i-1} L_ik X_kj.
+// Columns of the inverse are independent: each CTA owns TT_C columns (all inside one
+// 64-block j) and walks the block rows i > j with its column strip in shared memory.
+// W is row-major nbo x nbo, zero above the diagonal.
+constexpr int TT_C = 8;
+constexpr int TT_MAX = 512;
+// the (ib, kb) tiles a column strip walks, in order: L[ib][jb..ib-1], then Dinv_ib
+struct TtTile {
+  const float* p;
+  int64_t ld;
+  int rows, cols;
+};
+__global__ void __launch_bounds__(256) k_trtri_panel(const float* A, int64_t lda, const float* dinv, int p0, int nbo,
+                                                     float* W) {
   CV_PDL_ENTRY();
-  __shared__ double rb[CH_NB];
-  const int t = threadIdx.x;
-  if (t < nb) rb[t] = r[j0 + t];
+  __shared__ float X[TT_MAX][TT_C];
+  __shared__ __align__(16) float Lt[CH_NB][CH_NB + 4];
+  __shared__ float S[CH_NB][TT_C];
+  const int tid = threadIdx.x;
+  const int c0 = blockIdx.x * TT_C;
+  const int jb = c0 / CH_NB;
+  const int nsub = (nbo + CH_NB - 1) / CH_NB;
+  auto bsize = [&](int b) { return nbo - CH_NB * b < CH_NB ? nbo - CH_NB * b : CH_NB; };
+  const int nbj = bsize(jb);
+  const float* Dj = dinv + (int64_t)((p0 + CH_NB * jb) / CH_NB) * CH_NB * CH_NB;
+  for (int e = tid; e < CH_NB * TT_C; e += blockDim.x) {
+    const int r = e / TT_C, cc = e % TT_C, c = c0 + cc - CH_NB * jb;
+    X[CH_NB * jb + r][cc] = (r < nbj && c < nbj && c <= r) ? Dj[r * nbj + c] : 0.f;
+  }
+  // tile t of the walk: for ib = jb+1.., kb = jb..ib-1 (L tiles) then the Dinv_ib tile
+  auto tile_of = [&](int ib, int kb) {
+    TtTile t;
+    const int nbi = bsize(ib);
+    if (kb < ib) {
+      t.p = A + (int64_t)(p0 + CH_NB * ib) * lda + p0 + CH_NB * kb;
+      t.ld = lda;
+      t.rows = nbi;
+      t.cols = CH_NB;
+    } else {
+      t.p = dinv + (int64_t)((p0 + CH_NB * ib) / CH_NB) * CH_NB * CH_NB;
+      t.ld = nbi;
+      t.rows = nbi;
+      t.cols = nbi;
+    }
+    return t;
+  };
+  // register-staged prefetch of the next tile (4 x 16 bytes per thread, 128-bit when aligned)
+  float4 pre[4];
+  auto fetch = [&](const TtTile& t) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = tid + u * 256;  // float4 index in the 64 x 64 tile
+      const int rr = e / 16, c4 = (e % 16) * 4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (rr < t.rows) {
+        const float* src = t.p + (int64_t)rr * t.ld + c4;
+        if (c4 + 3 < t.cols && ((uintptr_t)src & 15) == 0) v = *reinterpret_cast<const float4*>(src);
+        else {
+          if (c4 < t.cols) v.x = src[0];
+          if (c4 + 1 < t.cols) v.y = src[1];
+          if (c4 + 2 < t.cols) v.z = src[2];
+          if (c4 + 3 < t.cols) v.w = src[3];
+        }
+      }
+      pre[u] = v;
+    }
+  };
+  auto commit = [&]() {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = tid + u * 256;
+      *reinterpret_cast<float4*>(&Lt[e / 16][(e % 16) * 4]) = pre[u];
+    }
+  };
+  int ib = jb + 1, kb = jb;
+  if (ib < nsub) fetch(tile_of(ib, kb));
   __syncthreads();
-  if (t < nb) {
-    double s = 0.0;
-    for (int k = 0; k <= t; ++k) s += (double)dinv[t * nb + k] * rb[k];
-    y[j0 + t] = s;
+  const int r = tid / 4, cq = (tid % 4) * (TT_C / 4);  // 64 rows x 4 column pairs
+  float acc[TT_C / 4] = {};
+  while (ib < nsub) {
+    commit();
+    __syncthreads();
+    // next tile in flight while this one is used
+    int nib = ib, nkb = kb + 1;
+    if (nkb > ib) { nib = ib + 1; nkb = jb; }
+    if (nib < nsub) fetch(tile_of(nib, nkb));
+    const int nbi = bsize(ib);
+    if (kb < ib) {
+#pragma unroll 8
+      for (int kk = 0; kk < CH_NB; ++kk) {
+        const float l = Lt[r][kk];
+#pragma unroll
+        for (int u = 0; u < TT_C / 4; ++u) acc[u] = fmaf(l, X[CH_NB * kb + kk][cq + u], acc[u]);
+      }
+      __syncthreads();
+      if (kb + 1 == ib) {  // S = sum_k L_ik X_kj complete
+#pragma unroll
+        for (int u = 0; u < TT_C / 4; ++u) {
+          S[r][cq + u] = acc[u];
+          acc[u] = 0.f;
+        }
+      }
+    } else {
+      // X_ib = -Dinv_ib S
+      float o[TT_C / 4] = {};
+      for (int kk = 0; kk <= r && kk < nbi; ++kk) {
+        const float dk = Lt[r][kk];
+#pragma unroll
+        for (int u = 0; u < TT_C / 4; ++u) o[u] = fmaf(dk, S[kk][cq + u], o[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < TT_C / 4; ++u) X[CH_NB * ib + r][cq + u] = r < nbi ? -o[u] : 0.f;
+      __syncthreads();
+    }
+    ib = nib;
+    kb = nkb;
+  }
+  __syncthreads();
+  for (int e = tid; e < nbo * TT_C; e += blockDim.x) {
+    const int rr = e / TT_C, cc = e % TT_C, c = c0 + cc;
+    if (c < nbo) W[(int64_t)rr * nbo + c] = rr < CH_NB * jb ? 0.f : X[rr][cc];
   }
 }
+
+// Triangular solves with the panel inverses W_p = L_pp^-1 (k_trtri_panel, kept per
+// panel): forward  y_p = W_p r_p,  r_below -= L21_p y_p;  backward  x_p = W_p^T (y_p -
+// L21_p^T x_below).  Every step is a GEMV spread over many CTAs (fp32 matrix, fp64
+// vectors), so a solve is ~5 short launches per 512-column panel.
 __global__ void k_trsv_fwd_update(const float* A, int64_t lda, int64_t m, int j0, int nb, const double* y, double* r) {
   CV_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
@@ -384,100 +671,52 @@ __global__ void k_trsv_bwd_gather(const float* A, int64_t lda, int64_t m, int j0
   for (int u = 0; u < 8; ++u) s += acc[u];
   partial[blockIdx.x * nb + k] = s;
 }
-__global__ void k_trsv_bwd_diag(const float* dinv, int nb, int j0, const double* y, const double* partial,
-                                int nparts, double* v) {
+// y[p0 + i] = sum_{j <= i} W[i, j] r[p0 + j]   (one warp per row of the lower W_p)
+__global__ void __launch_bounds__(256) k_tri_wgemv(const float* W, int nbo, int p0, const double* r, double* y) {
   CV_PDL_ENTRY();
-  __shared__ double rb[CH_NB];
-  const int t = threadIdx.x;
-  if (t < nb) {
-    double s = 0.0;
-    for (int p = 0; p < nparts; ++p) s += partial[p * nb + t];
-    rb[t] = y[j0 + t] - s;
-  }
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (i >= nbo) return;
+  double s = 0.0;
+  for (int j = lane; j <= i; j += 32) s += (double)W[(int64_t)i * nbo + j] * r[p0 + j];
+  s = warp_sum(s);
+  if (lane == 0) y[p0 + i] = s;
+}
+// t_i = y[p0 + i] - sum_b partial[b][i] (fixed order): 32 rows i per CTA, its 8 warps
+// stride over the partial blocks b and reduce in shared memory
+__global__ void __launch_bounds__(256) k_tri_bwd_reduce(const double* y, const double* partial, int nparts, int nbo,
+                                                        int p0, double* t) {
+  CV_PDL_ENTRY();
+  __shared__ double red[8][32];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + lane;
+  double s = 0.0;
+  if (i < nbo)
+    for (int b = wp; b < nparts; b += 8) s += partial[(int64_t)b * nbo + i];
+  red[wp][lane] = s;
   __syncthreads();
-  if (t < nb) {
-    double s = 0.0;
-    for (int k = t; k < nb; ++k) s += (double)dinv[k * nb + t] * rb[k];  // Dinv^T
-    v[j0 + t] = s;
+  if (wp == 0 && i < nbo) {
+    double a = 0.0;
+    for (int w = 0; w < 8; ++w) a += red[w][lane];
+    t[i] = y[p0 + i] - a;
   }
 }
-// Panel forms of the two substitutions (TS_NB = 512 columns = 8 diagonal 64-blocks per
-// launch): one CTA walks the panel's 64-blocks with their precomputed inverses (fp64
-// right-hand sides in shared memory), so a triangular solve is 2 x m/512 dependent
-// launches instead of 4 x m/64.
-constexpr int TS_NB = 512;
-
-// forward: y[j0 : j0+nbp] from r (the panel rows of r are consumed in smem)
-__global__ void __launch_bounds__(TS_NB) k_trsv_fwd_panel(const float* A, int64_t lda, const float* dinv, int j0,
-                                                          int nbp, const double* r, double* y) {
+// x[p0 + j] = sum_{i >= j} W[i, j] t_i: each CTA owns 32 columns j; its 8 warps stride
+// over the rows i and reduce in shared memory
+__global__ void __launch_bounds__(256) k_tri_wtgemv(const float* W, int nbo, int p0, const double* t, double* x) {
   CV_PDL_ENTRY();
-  __shared__ double rb[TS_NB];
-  __shared__ double yb[CH_NB];
-  const int t = threadIdx.x;
-  if (t < nbp) rb[t] = r[j0 + t];
+  __shared__ double red[8][32];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + lane;
+  double s = 0.0;
+  if (j < nbo)
+    for (int i = j + wp; i < nbo; i += 8) s += (double)W[(int64_t)i * nbo + j] * t[i];
+  red[wp][lane] = s;
   __syncthreads();
-  for (int s0 = 0; s0 < nbp; s0 += CH_NB) {
-    const int nb = nbp - s0 < CH_NB ? nbp - s0 : CH_NB;
-    const float* D = dinv + (int64_t)((j0 + s0) / CH_NB) * CH_NB * CH_NB;
-    if (t < nb) {
-      double acc = 0.0;
-      for (int k = 0; k <= t; ++k) acc += (double)D[t * nb + k] * rb[s0 + k];
-      yb[t] = acc;
-      y[j0 + s0 + t] = acc;
-    }
-    __syncthreads();
-    // later rows of the panel: rb[i] -= L[i, s0 : s0+nb] yb
-    const int i = s0 + nb + t;
-    if (i < nbp) {
-      const float* Li = A + (int64_t)(j0 + i) * lda + j0 + s0;
-      double acc = 0.0;
-      for (int k = 0; k < nb; ++k) acc += (double)Li[k] * yb[k];
-      rb[i] -= acc;
-    }
-    __syncthreads();
-  }
-}
-
-// backward: v[j0 : j0+nbp] from y and the gathered partials L[below, panel]^T v[below]
-__global__ void __launch_bounds__(TS_NB) k_trsv_bwd_panel(const float* A, int64_t lda, const float* dinv, int j0,
-                                                          int nbp, const double* y, const double* partial, int nparts,
-                                                          double* v) {
-  CV_PDL_ENTRY();
-  __shared__ double rb[TS_NB];
-  __shared__ double xb[TS_NB];
-  __shared__ double red[8][CH_NB];
-  const int t = threadIdx.x;
-  if (t < nbp) {
-    double acc = 0.0;
-    for (int p = 0; p < nparts; ++p) acc += partial[(int64_t)p * nbp + t];
-    rb[t] = y[j0 + t] - acc;
-  }
-  __syncthreads();
-  const int nsub = (nbp + CH_NB - 1) / CH_NB;
-  for (int sb = nsub - 1; sb >= 0; --sb) {
-    const int s0 = sb * CH_NB;
-    const int nb = nbp - s0 < CH_NB ? nbp - s0 : CH_NB;
-    // rb[s0 + k] -= sum over the panel's later rows i of L[i, s0 + k] x[i]  (8 row groups)
-    const int k = t & (CH_NB - 1), grp = t / CH_NB;
-    double acc = 0.0;
-    if (k < nb)
-      for (int i = s0 + nb + grp; i < nbp; i += 8) acc += (double)A[(int64_t)(j0 + i) * lda + j0 + s0 + k] * xb[i];
-    red[grp][k] = acc;
-    __syncthreads();
-    if (t < nb) {
-      double s = rb[s0 + t];
-      for (int g2 = 0; g2 < 8; ++g2) s -= red[g2][t];
-      rb[s0 + t] = s;
-    }
-    __syncthreads();
-    const float* D = dinv + (int64_t)((j0 + s0) / CH_NB) * CH_NB * CH_NB;
-    if (t < nb) {
-      double s = 0.0;
-      for (int kk = t; kk < nb; ++kk) s += (double)D[kk * nb + t] * rb[s0 + kk];  // Dinv^T
-      xb[s0 + t] = s;
-      v[j0 + s0 + t] = s;
-    }
-    __syncthreads();
+  if (wp == 0 && j < nbo) {
+    double a = 0.0;
+    for (int w = 0; w < 8; ++w) a += red[w][lane];
+    x[p0 + j] = a;
   }
 }
 
@@ -516,44 +755,54 @@ __global__ void k_d2f(const double* x, float* y, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) y[i] = (float)x[i];
 }
 
-int row_solve_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, float* v_out) {
-  ensure_gram(ctx, s);
-  const int64_t m = (int64_t)s->bl * s->c;
-  if (!s->chol) s->chol = snap_alloc(s, m * m);
-  const int nblk = (int)((m + CH_NB - 1) / CH_NB);
-  if (!s->dinv) s->dinv = snap_alloc(s, (int64_t)nblk * CH_NB * CH_NB);
+// (Gram + mu I) v = rhs for a dense symmetric m x m fp32 Gram (full storage) on the
+// device (solvers.py:146-161).  Workspace: chol (m x m, lower factor) and dinv
+// (inverses of the 64-blocks).  Returns 1 if the system is not positive definite.
+//
+// Two-level right-looking blocked Cholesky.  Each 512-column panel:
+//  (1) its 512 x 512 diagonal block is factored with the register-resident fp64
+//      64-block kernel (k_potrf_diag) and SIMT TRSM / updates confined to the block;
+//  (2) W = L11^-1 (k_trtri_panel);
+//  (3) the panel below the block, L21 = A21 W^T, is one tensor-core GEMM;
+//  (4) the trailing update A22 -= L21 L21^T (lower tiles) is one tensor-core GEMM.
+// All but O(m^2 x 512) of the m^3/3 flops run on the tensor engine (3xFP16 split
+// operands); fp64 triangular solves and two steps of fp64 iterative refinement
+// against the fp32 Gram absorb the split's rounding (cf. the 1e-6 lane-equivalence
+// bound, tests/test_solvers.py:216-236).  The SIMT engine (CV_ENGINE_SIMT) or a
+// system of one panel factors everything with exact-fp32 SIMT kernels.
+int dense_cholesky_solve(cv_ctx* ctx, const float* gram, int64_t m, double mu, const float* rhs, float* v_out,
+                         float* chol, float* dinv, float* winv, Scale* scr_sc) {
   cudaStream_t st = ctx->stream;
-  launch_k(st, k_copy_add_diag, 4096, 256, 0, s->gram, s->chol, m, (float)mu);
+  {
+    const int nt = (int)((m + 31) / 32);
+    launch_k(st, k_copy_lower_add_diag, dim3(nt, nt), 256, 0, gram, chol, m, (float)mu);
+  }
   int* flag = (int*)(ctx->scal_ws + 32);
   cudaMemsetAsync(flag, 0, sizeof(int), st);
   ctx->launches++;
-  // Two-level right-looking blocked Cholesky: panels of CH_NBO columns are factored
-  // with the 64-wide fp64 diagonal kernel, a SIMT triangular solve and SIMT updates
-  // confined to the panel; the trailing matrix update A22 -= L21 L21^T of each panel
-  // (all but O(m^2 CH_NBO) of the m^3/3 flops) runs on the tensor-core engine with L21
-  // as a scaled fp16 pair.  The fp64 iterative refinement below absorbs the split's
-  // rounding (cf. the 1e-6 lane-equivalence bound, tests/test_solvers.py:216-236).
-  constexpr int NBO = 512;  // panel width (a multiple of CH_NB)
+  constexpr int NBO = TT_MAX;  // panel width (a multiple of CH_NB)
   const bool tc = ctx->engine != CV_ENGINE_SIMT && m > NBO;
-  __half* l21h = nullptr;
-  __half* l21l = nullptr;
+  __half *l21h = nullptr, *l21l = nullptr, *wh = nullptr, *wl = nullptr;
   if (tc) {
     l21h = (__half*)ctx->pool.get(sizeof(__half) * (size_t)(m - NBO) * NBO);
     l21l = (__half*)ctx->pool.get(sizeof(__half) * (size_t)(m - NBO) * NBO);
+    wh = (__half*)ctx->pool.get(sizeof(__half) * (size_t)NBO * NBO);
+    wl = (__half*)ctx->pool.get(sizeof(__half) * (size_t)NBO * NBO);
   }
-  Scale* l21sc = s->scratch_sc + 2;
+  Scale* l21sc = scr_sc;
+  Scale* wsc = scr_sc + 1;
   for (int64_t p0 = 0; p0 < m; p0 += NBO) {
     const int nbo = (int)((m - p0) < NBO ? (m - p0) : NBO);
-    const int64_t pend = tc ? p0 + nbo : m;  // columns the in-panel updates cover
+    const int64_t pend = tc ? p0 + nbo : m;  // columns (and rows) the in-block updates cover
     for (int64_t j0 = p0; j0 < p0 + nbo; j0 += CH_NB) {
       const int bi = (int)(j0 / CH_NB);
       const int nb = (int)((m - j0) < CH_NB ? (m - j0) : CH_NB);
-      float* dblk = s->dinv + (int64_t)bi * CH_NB * CH_NB;
-      launch_k(st, k_potrf_diag, 1, 256, 0, s->chol, m, (int)j0, nb, dblk, flag);
+      float* dblk = dinv + (int64_t)bi * CH_NB * CH_NB;
+      launch_k(st, k_potrf_diag, 1, PD_T, 0, chol, m, (int)j0, nb, dblk, flag);
       ctx->launches++;
-      const int rest = (int)(m - j0 - nb);
+      const int rest = (int)(pend - j0 - nb);
       if (rest <= 0) continue;
-      float* A21 = s->chol + (int64_t)(j0 + nb) * m + j0;
+      float* A21 = chol + (int64_t)(j0 + nb) * m + j0;
       // A21 <- A21 * L11^-T
       GemmArgs p;
       p.M = rest;
@@ -564,25 +813,46 @@ int row_solve_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, flo
       p.epi.out = A21;
       p.epi.ld = m;
       gemm_simt(ctx, p);  // in place: one N tile per CTA row block
-      // A22 -= A21 A21^T, columns [j0+nb, pend) (lower part)
-      const int ncols = (int)(pend - j0 - nb);
-      if (ncols <= 0) continue;
+      // A22 -= A21 A21^T, lower part of [j0+nb, pend)^2
       GemmArgs u;
       u.M = rest;
-      u.N = ncols;
+      u.N = rest;
       u.nseg = 1;
       u.seg[0] = GemmSeg{f32op(A21, m, 1), f32op(A21, 1, m), nb};
       u.epi.mode = EPI_ACCUM;
       u.epi.alpha = -1.f;
-      u.epi.out = s->chol + (int64_t)(j0 + nb) * m + (j0 + nb);
+      u.epi.out = chol + (int64_t)(j0 + nb) * m + (j0 + nb);
       u.epi.ld = m;
       u.lower_only = 1;
       gemm_simt(ctx, u);
     }
+    // (2) W = L11^-1 (kept: the triangular solves below multiply by it)
+    float* W = winv + (p0 / NBO) * (int64_t)NBO * NBO;
+    launch_k(st, k_trtri_panel, (nbo + TT_C - 1) / TT_C, 256, 0, (const float*)chol, m, (const float*)dinv, (int)p0,
+             nbo, W);
+    ctx->launches++;
     const int rest2 = (int)(m - p0 - nbo);
     if (!tc || rest2 <= 0) continue;
-    // trailing update of the whole remaining matrix on the tensor cores
-    split_mat(ctx, s->chol + (p0 + nbo) * m + p0, m, rest2, nbo, l21h, l21l, nbo, 0, l21sc, 0, nullptr);
+    // (3) L21 = A21 W^T on the tensor cores (A21 split first; the GEMM writes fp32 L21 in place)
+    float* A21 = chol + (p0 + nbo) * m + p0;
+    split_mat(ctx, A21, m, rest2, nbo, l21h, l21l, nbo, 0, l21sc, 0, nullptr);
+    split_mat(ctx, W, nbo, nbo, nbo, wh, wl, nbo, 0, wsc, 0, nullptr);
+    {
+      Operand A, B;
+      A.hi = l21h; A.lo = l21l; A.sc = l21sc; A.si = nbo; A.sj = 1;  // A(i, k) = A21[i, k]
+      B.hi = wh; B.lo = wl; B.sc = wsc; B.si = 1; B.sj = nbo;        // B(k, j) = W[j, k]
+      GemmArgs t;
+      t.M = rest2;
+      t.N = nbo;
+      t.nseg = 1;
+      t.seg[0] = GemmSeg{A, B, nbo};
+      t.epi.mode = EPI_STORE;
+      t.epi.out = A21;
+      t.epi.ld = m;
+      gemm(ctx, t);
+    }
+    // (4) trailing update of the whole remaining matrix on the tensor cores
+    split_mat(ctx, A21, m, rest2, nbo, l21h, l21l, nbo, 0, l21sc, 0, nullptr);
     Operand A, B;
     A.hi = l21h; A.lo = l21l; A.sc = l21sc; A.si = nbo; A.sj = 1;  // A(i, k) = L21[i, k]
     B.hi = l21h; B.lo = l21l; B.sc = l21sc; B.si = 1; B.sj = nbo;  // B(k, j) = L21[j, k]
@@ -593,7 +863,7 @@ int row_solve_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, flo
     u.seg[0] = GemmSeg{A, B, nbo};
     u.epi.mode = EPI_ACCUM;
     u.epi.alpha = -1.f;
-    u.epi.out = s->chol + (p0 + nbo) * m + (p0 + nbo);
+    u.epi.out = chol + (p0 + nbo) * m + (p0 + nbo);
     u.epi.ld = m;
     u.lower_only = 1;
     gemm(ctx, u);
@@ -601,6 +871,8 @@ int row_solve_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, flo
   if (tc) {
     ctx->pool.put(l21h);
     ctx->pool.put(l21l);
+    ctx->pool.put(wh);
+    ctx->pool.put(wl);
   }
   int hflag = 0;
   cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
@@ -612,34 +884,43 @@ int row_solve_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, flo
   double* y = r + m;
   double* v = r + 2 * m;
   double* dv = r + 3 * m;
-  const int rpb = 64;
-  const int nparts_max = (int)((m + rpb - 1) / rpb);
-  double* part = (double*)ctx->pool.get(sizeof(double) * (size_t)nparts_max * TS_NB);
+  const int64_t nparts_max = 2 * ctx->sm_count;
+  double* part = (double*)ctx->pool.get(sizeof(double) * (size_t)(nparts_max + 1) * NBO);
+  double* tvec = part + nparts_max * NBO;
+  const int npan = (int)((m + NBO - 1) / NBO);
   auto tri_solve = [&](double* x) {  // r -> x = (L L^T)^-1 r   (r is consumed)
-    const int npan = (int)((m + TS_NB - 1) / TS_NB);
     for (int pi = 0; pi < npan; ++pi) {
-      const int j0 = pi * TS_NB;
-      const int nbp = (int)((m - j0) < TS_NB ? (m - j0) : TS_NB);
-      launch_k(st, k_trsv_fwd_panel, 1, TS_NB, 0, (const float*)s->chol, m, (const float*)s->dinv, j0, nbp,
-               (const double*)r, y);
-      const int64_t rest = m - j0 - nbp;
-      if (rest > 0) launch_k(st, k_trsv_fwd_update, (int)((rest + 7) / 8), 256, 0, s->chol, m, m, j0, nbp, y, r);
+      const int p0 = pi * NBO;
+      const int nbp = (int)((m - p0) < NBO ? (m - p0) : NBO);
+      const float* W = winv + (int64_t)pi * NBO * NBO;
+      launch_k(st, k_tri_wgemv, (nbp + 7) / 8, 256, 0, W, nbp, p0, (const double*)r, y);
+      const int64_t rest = m - p0 - nbp;
+      if (rest > 0) launch_k(st, k_trsv_fwd_update, (int)((rest + 7) / 8), 256, 0, chol, m, m, p0, nbp, y, r);
+      ctx->launches += rest > 0 ? 2 : 1;
     }
     for (int pi = npan - 1; pi >= 0; --pi) {
-      const int j0 = pi * TS_NB;
-      const int nbp = (int)((m - j0) < TS_NB ? (m - j0) : TS_NB);
-      const int64_t rest = m - j0 - nbp;
-      const int nparts = (int)((rest + rpb - 1) / rpb);
-      if (nparts > 0) launch_k(st, k_trsv_bwd_gather, nparts, TS_NB, 0, s->chol, m, m, j0, nbp, x, part, rpb);
-      launch_k(st, k_trsv_bwd_panel, 1, TS_NB, 0, (const float*)s->chol, m, (const float*)s->dinv, j0, nbp,
-               (const double*)y, (const double*)part, nparts, x);
+      const int p0 = pi * NBO;
+      const int nbp = (int)((m - p0) < NBO ? (m - p0) : NBO);
+      const float* W = winv + (int64_t)pi * NBO * NBO;
+      const int64_t rest = m - p0 - nbp;
+      int nparts = 0;
+      if (rest > 0) {
+        int64_t rpb = (rest + nparts_max - 1) / nparts_max;
+        if (rpb < 32) rpb = 32;
+        nparts = (int)((rest + rpb - 1) / rpb);
+        launch_k(st, k_trsv_bwd_gather, nparts, NBO, 0, chol, m, m, p0, nbp, (const double*)x, part, (int)rpb);
+        ctx->launches++;
+      }
+      launch_k(st, k_tri_bwd_reduce, (nbp + 31) / 32, 256, 0, (const double*)y, (const double*)part, nparts, nbp, p0,
+               tvec);
+      launch_k(st, k_tri_wtgemv, (nbp + 31) / 32, 256, 0, W, nbp, p0, (const double*)tvec, x);
+      ctx->launches += 2;
     }
-    ctx->launches += 4 * npan;
   };
   launch_k(st, k_f2d, 256, 256, 0, rhs, r, m);
   tri_solve(v);
   for (int it = 0; it < 2; ++it) {
-    launch_k(st, k_row_residual, (int)((m + 7) / 8), 256, 0, s->gram, m, (float)mu, rhs, v, r);
+    launch_k(st, k_row_residual, (int)((m + 7) / 8), 256, 0, gram, m, (float)mu, rhs, v, r);
     tri_solve(dv);
     launch_k(st, k_axpy_d, 256, 256, 0, dv, v, m);
     ctx->launches += 2;
@@ -649,6 +930,38 @@ int row_solve_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, flo
   ctx->pool.put(part);
   ctx->pool.put(r);
   return 0;
+}
+
+int row_solve_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, float* v_out) {
+  ensure_gram(ctx, s);
+  const int64_t m = (int64_t)s->bl * s->c;
+  if (!s->chol) s->chol = snap_alloc(s, m * m);
+  const int nblk = (int)((m + CH_NB - 1) / CH_NB);
+  if (!s->dinv) s->dinv = snap_alloc(s, (int64_t)nblk * CH_NB * CH_NB);
+  const int64_t npan = (m + TT_MAX - 1) / TT_MAX;
+  if (!s->winv) s->winv = snap_alloc(s, npan * TT_MAX * TT_MAX);
+  return dense_cholesky_solve(ctx, s->gram, m, mu, rhs, v_out, s->chol, s->dinv, s->winv, s->scratch_sc + 2);
+}
+
+int dense_cholesky(cv_ctx* ctx, const float* gram, int64_t m, double mu, const float* rhs, float* v_out) {
+  float* chol = (float*)ctx->pool.get(sizeof(float) * (size_t)(m * m));
+  const int64_t nblk = (m + CH_NB - 1) / CH_NB;
+  float* dinv = (float*)ctx->pool.get(sizeof(float) * (size_t)(nblk * CH_NB * CH_NB));
+  Scale* sc = (Scale*)ctx->pool.get(sizeof(Scale) * 4);
+  const int64_t npan = (m + TT_MAX - 1) / TT_MAX;
+  float* winv = (float*)ctx->pool.get(sizeof(float) * (size_t)(npan * TT_MAX * TT_MAX));
+  int rc = 1;
+  try {
+    rc = dense_cholesky_solve(ctx, gram, m, mu, rhs, v_out, chol, dinv, winv, sc);
+  } catch (...) {
+    ctx->pool.put(winv); ctx->pool.put(sc); ctx->pool.put(dinv); ctx->pool.put(chol);
+    throw;
+  }
+  ctx->pool.put(winv);
+  ctx->pool.put(sc);
+  ctx->pool.put(dinv);
+  ctx->pool.put(chol);
+  return rc;
 }
 
 void row_backproject(cv_ctx* ctx, cv_snap* s, const float* v, float* out) {

@@ -607,17 +607,222 @@ __global__ void k_cg_finish(const CgDev* st, cv_cg_stats* out) {
   out->x0_nonzero = st->x0nz;
 }
 
+// The operator of a parameter-space CG run: a snapshot's curvature product (the
+// direction update also publishes the next product's input scales).
+struct CgOperator {
+  int64_t d = 0;
+  cv_snap* s = nullptr;
+  MatvecFn mv = nullptr;
+  void apply(cv_ctx* ctx, const float* in, float* out, const int* skip) const { mv(ctx, s, in, out, skip); }
+};
+
+static void cg_run(cv_ctx* ctx, const CgOperator& op, const float* g, double lam, double tol, int maxiter, int stab,
+                   const float* precond, double floor, const float* x0, float* x, cv_cg_stats* stats, float* r,
+                   float* p, float* ap);
+
 void cg_solve(cv_ctx* ctx, cv_snap* s, int kind, const float* g, double lam, double tol, int maxiter, int stab,
               const float* precond, double floor, const float* x0, float* x, cv_cg_stats* stats) {
-  const int64_t d = s->d;
-  float* r = snap_tmp(s, &s->cg_r);
-  float* p = snap_tmp(s, &s->cg_p);
-  float* ap = snap_tmp(s, &s->cg_ap);
+  CgOperator op;
+  op.d = s->d;
+  op.s = s;
+  op.mv = matvec_fn(kind);
+  cg_run(ctx, op, g, lam, tol, maxiter, stab, precond, floor, x0, x, stats, snap_tmp(s, &s->cg_r),
+         snap_tmp(s, &s->cg_p), snap_tmp(s, &s->cg_ap));
+}
+
+// ---------------------------------------------------------------------------
+// Row-space CG on a dense Gram (solvers.py:164-174 with gram_matvec = gram @ u):
+// the same control flow and device-resident scalars as the parameter-space loop
+// (CgDev, pap_final_body, r_final_body), with the m-length vectors kept in fp64.
+// m = b*c is small (40,960 at C4), and the row systems are solved to few digits in
+// maxiter iterations, where fp32 residual recurrences drift from the f64 reference
+// by ~1e-4 (residual cancellation against |Gram| ~ 50x |rhs|); fp64 vectors track it.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_gram_gemv_d(const float* G, const double* x, int64_t m, double* y,
+                                                     const int* skip) {
+  CV_PDL_ENTRY();
+  if (skip && *skip) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * 8;
+  for (int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); row < m; row += nwarps) {
+    const float* g = G + row * m;
+    double s = 0.0;
+    if ((m & 3) == 0) {
+      for (int64_t k = lane * 4; k < m; k += 128) {
+        const float4 q = __ldcs(reinterpret_cast<const float4*>(g + k));
+        s += (double)q.x * x[k] + (double)q.y * x[k + 1] + (double)q.z * x[k + 2] + (double)q.w * x[k + 3];
+      }
+    } else {
+      for (int64_t k = lane; k < m; k += 32) s += (double)g[k] * x[k];
+    }
+    s = warp_sum(s);
+    if (lane == 0) y[row] = s;
+  }
+}
+#define DCG_FOR(i, n) for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
+__global__ void k_dcg_setup(const float* g, const float* x0, const CgDev* st, int64_t m, double* b, double* x) {
+  CV_PDL_ENTRY();
+  DCG_FOR(i, m) {
+    b[i] = g[i];
+    x[i] = st->x0nz ? (double)x0[i] : 0.0;
+  }
+}
+// r = b - (Ax + lam x) (warm) or b; partial ||r||^2
+__global__ void k_dcg_r0(const double* b, const double* ax, const double* x, double lam, const CgDev* st, int64_t m,
+                         double* r, double* ws) {
+  CV_PDL_ENTRY();
+  if (st->done) return;
+  double t[1] = {0.0};
+  DCG_FOR(i, m) {
+    const double v = st->x0nz ? b[i] - (ax[i] + lam * x[i]) : b[i];
+    r[i] = v;
+    t[0] += v * v;
+  }
+  write_partials<1>(ws, t);
+}
+__global__ void k_dcg_p0(const double* r, const CgDev* st, int64_t m, double* p, double* ws) {
+  CV_PDL_ENTRY();
+  if (st->done) return;
+  double t[1] = {0.0};
+  DCG_FOR(i, m) {
+    p[i] = r[i];
+    t[0] += r[i] * r[i];
+  }
+  write_partials<1>(ws, t);
+}
+__global__ void k_dcg_pap(double* ap, const double* p, double lam, CgDev* st, int64_t m, double* ws, unsigned* ctr,
+                          int k, int stab) {
+  CV_PDL_ENTRY();
+  if (st->done) return;
+  double t[3] = {0.0, 0.0, 0.0};
+  double mx = 0.0;
+  DCG_FOR(i, m) {
+    const double a = ap[i] + lam * p[i];
+    ap[i] = a;
+    t[0] += p[i] * a;
+    t[2] += isfinite(p[i]) ? 0.0 : 1.0;
+    mx = fmax(mx, fabs(p[i]));
+  }
+  write_partials<3>(ws, t);
+  __shared__ double smx[NT / 32];
+  mx = warp_max_d(mx);
+  if ((threadIdx.x & 31) == 0) smx[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double q = 0.0;
+    for (int w = 0; w < NT / 32; ++w) q = fmax(q, smx[w]);
+    ws[blockIdx.x * 8 + 1] = q;
+  }
+  if (grid_last(ctr)) pap_final_body(ws, st, k, stab);
+}
+__global__ void k_dcg_update(double* x, double* r, const double* p, const double* ap, CgDev* st, int64_t m, double* ws,
+                             unsigned* ctr, int k, int maxiter, double tol) {
+  CV_PDL_ENTRY();
+  if (st->done) return;
+  const double a = st->alpha;
+  double t[2] = {0.0, 0.0};
+  DCG_FOR(i, m) {
+    x[i] += a * p[i];
+    const double ri = r[i] - a * ap[i];
+    r[i] = ri;
+    t[0] += ri * ri;
+    t[1] += ri * ri;
+  }
+  write_partials<2>(ws, t);
+  if (grid_last(ctr)) r_final_body(ws, st, k, maxiter, 0, tol);
+}
+__global__ void k_dcg_xupdate(double* x, const double* p, const CgDev* st, int64_t m) {
+  CV_PDL_ENTRY();
+  if (st->done) return;
+  const double a = st->alpha;
+  DCG_FOR(i, m) x[i] += a * p[i];
+}
+__global__ void k_dcg_rstab(const double* b, const double* ax, const double* x, double* r, double lam, CgDev* st,
+                            int64_t m, double* ws, unsigned* ctr, int k, int maxiter, double tol) {
+  CV_PDL_ENTRY();
+  if (st->done) return;
+  double t[2] = {0.0, 0.0};
+  DCG_FOR(i, m) {
+    const double ri = b[i] - (ax[i] + lam * x[i]);
+    r[i] = ri;
+    t[0] += ri * ri;
+    t[1] += ri * ri;
+  }
+  write_partials<2>(ws, t);
+  if (grid_last(ctr)) r_final_body(ws, st, k, maxiter, 1, tol);
+}
+__global__ void k_dcg_pnext(const double* r, const CgDev* st, int64_t m, double* p) {
+  CV_PDL_ENTRY();
+  if (st->done) return;
+  const double beta = st->alpha;
+  DCG_FOR(i, m) p[i] = r[i] + beta * p[i];
+}
+__global__ void k_dcg_out(const double* x, int64_t m, float* out) {
+  CV_PDL_ENTRY();
+  DCG_FOR(i, m) out[i] = (float)x[i];
+}
+
+void dense_cg_solve(cv_ctx* ctx, const float* gram, int64_t m, const float* rhs, double mu, double tol, int maxiter,
+                    int stab, const float* x0, float* xout, cv_cg_stats* stats) {
+  CgDev* st = (CgDev*)(ctx->scal_ws + 8);
+  double* ws = ctx->red_ws;
+  cudaStream_t sm = ctx->stream;
+  unsigned* ctr = ctx->amax_counter + 1;
+  const int64_t ms = (m + 31) / 32 * 32;
+  double* buf = (double*)ctx->pool.get(sizeof(double) * (size_t)(5 * ms));
+  double *b = buf, *x = buf + ms, *r = buf + 2 * ms, *p = buf + 3 * ms, *ap = buf + 4 * ms;
+  const int64_t gb = (m + 7) / 8;
+  const int ggrid = (int)(gb < 16 * (int64_t)ctx->sm_count ? gb : 16 * (int64_t)ctx->sm_count);
+  auto A = [&](const double* in, double* out, const int* skip) {
+    launch_k(sm, k_gram_gemv_d, ggrid, 256, 0, gram, in, m, out, skip);
+    ctx->launches++;
+  };
+  launch_k(sm, k_cg_init, NB, NT, 0, rhs, x0, m, ws);
+  launch_k(sm, k_cg_init_final, 1, NT, 0, (const double*)ws, st);
+  launch_k(sm, k_dcg_setup, NB, NT, 0, rhs, x0, (const CgDev*)st, m, b, x);
+  ctx->launches += 3;
+  if (x0) A(x, ap, &st->gv_skip);
+  launch_k(sm, k_dcg_r0, NB, NT, 0, (const double*)b, (const double*)ap, (const double*)x, mu, (const CgDev*)st, m, r,
+           ws);
+  launch_k(sm, k_cg_r0_final, 1, NT, 0, (const double*)ws, st, tol);
+  launch_k(sm, k_dcg_p0, NB, NT, 0, (const double*)r, (const CgDev*)st, m, p, ws);
+  launch_k(sm, k_cg_p0_final, 1, NT, 0, (const double*)ws, st);
+  ctx->launches += 4;
+  for (int k = 1; k <= maxiter; ++k) {
+    const int is_stab = (stab > 0 && k % stab == 0) ? 1 : 0;
+    A(p, ap, &st->done);
+    launch_k(sm, k_dcg_pap, NB, NT, 0, ap, (const double*)p, mu, st, m, ws, ctr, k, is_stab);
+    ctx->launches++;
+    if (is_stab) {
+      launch_k(sm, k_dcg_xupdate, NB, NT, 0, x, (const double*)p, (const CgDev*)st, m);
+      A(x, ap, &st->gv_skip);
+      launch_k(sm, k_dcg_rstab, NB, NT, 0, (const double*)b, (const double*)ap, (const double*)x, r, mu, st, m, ws,
+               ctr, k, maxiter, tol);
+      ctx->launches += 2;
+    } else {
+      launch_k(sm, k_dcg_update, NB, NT, 0, x, r, (const double*)p, (const double*)ap, st, m, ws, ctr, k, maxiter,
+               tol);
+      ctx->launches++;
+    }
+    if (k == maxiter) break;
+    launch_k(sm, k_dcg_pnext, NB, NT, 0, (const double*)r, (const CgDev*)st, m, p);
+    ctx->launches++;
+  }
+  launch_k(sm, k_dcg_out, NB, NT, 0, (const double*)x, m, xout);
+  launch_k(sm, k_cg_finish, 1, 1, 0, (const CgDev*)st, stats);
+  ctx->launches += 2;
+  ctx->pool.put(buf);  // stream-ordered reuse
+}
+
+static void cg_run(cv_ctx* ctx, const CgOperator& op, const float* g, double lam, double tol, int maxiter, int stab,
+                   const float* precond, double floor, const float* x0, float* x, cv_cg_stats* stats, float* r,
+                   float* p, float* ap) {
+  const int64_t d = op.d;
+  cv_snap* s = op.s;
   CgDev* st = (CgDev*)(ctx->scal_ws + 8);
   double* ws = ctx->red_ws;
   cudaStream_t sm = ctx->stream;
   const float flam = (float)lam, ffl = (float)floor;
-  MatvecFn mv = matvec_fn(kind);
 
   launch_k(sm, k_cg_init, NB, NT, 0, g, x0, d, ws);
   launch_k(sm, k_cg_init_final, 1, NT, 0, ws, st);
@@ -625,7 +830,7 @@ void cg_solve(cv_ctx* ctx, cv_snap* s, int kind, const float* g, double lam, dou
   if (x0) {
     launch_k(sm, k_cg_setup_x, NB, NT, 0, x0, st, d, x);
     ctx->launches++;
-    mv(ctx, s, x, ap, &st->gv_skip);
+    op.apply(ctx, x, ap, &st->gv_skip);
   } else {
     cudaMemsetAsync(x, 0, sizeof(float) * d, sm);
   }
@@ -637,13 +842,13 @@ void cg_solve(cv_ctx* ctx, cv_snap* s, int kind, const float* g, double lam, dou
   unsigned* ctr = ctx->amax_counter + 1;
   for (int k = 1; k <= maxiter; ++k) {
     const int is_stab = (stab > 0 && k % stab == 0) ? 1 : 0;
-    mv(ctx, s, p, ap, &st->done);
+    op.apply(ctx, p, ap, &st->done);
     launch_k(sm, k_cg_pap, NB, NT, 0, ap, p, flam, st, d, ws, ctr, k, is_stab);
     ctx->launches++;
     if (is_stab) {
       launch_k(sm, k_cg_xupdate, NB, NT, 0, x, p, st, d);
       ctx->launches++;
-      mv(ctx, s, x, ap, &st->gv_skip);
+      op.apply(ctx, x, ap, &st->gv_skip);
       launch_k(sm, k_cg_rstab, NB, NT, 0, g, ap, x, r, precond, flam, ffl, st, d, ws, ctr, k, maxiter, tol);
     } else {
       launch_k(sm, k_cg_update, NB, NT, 0, x, r, p, ap, precond, flam, ffl, st, d, ws, ctr, k, maxiter, tol);
@@ -651,7 +856,8 @@ void cg_solve(cv_ctx* ctx, cv_snap* s, int kind, const float* g, double lam, dou
     ctx->launches++;
     if (k == maxiter) break;  // the direction of a last iteration is never used
     // p <- M^-1 r + beta p, fused with the next product's input scales
-    if (cg_pnext_amax(ctx, r, precond, flam, ffl, &st->alpha, &st->done, p, d, s->off, s->v_sc, s->prod_sc, s->n_prod)) {
+    if (s && cg_pnext_amax(ctx, r, precond, flam, ffl, &st->alpha, &st->done, p, d, s->off, s->v_sc, s->prod_sc,
+                           s->n_prod)) {
       s->v_ready = 1;
     } else {
       launch_k(sm, k_cg_pnext, NB, NT, 0, r, precond, flam, ffl, st, d, p);

@@ -79,6 +79,27 @@ class RowOps:
         s.rt.call("cv_row_solve_cholesky", s.h, float(mu), r.data_ptr(), out.data_ptr())
         return out
 
+    def gram_matvec(self, u):
+        """`gram @ u` (method.py:279) on the device."""
+        s = self._snap
+        u = torch.as_tensor(u, dtype=torch.float32, device=s.rt.device).contiguous().reshape(-1)
+        return self.gram() @ u
+
+    def solve_cg(self, mu: float, config, x0=None, stats=None):
+        """Row-space CG on (Gram + mu I) v = rhs (solvers.py:164-174), device resident.
+
+        Returns (v, stats) without synchronising; `stats` is a cv_cg_stats buffer."""
+        s = self._snap
+        out = torch.empty(self.m, dtype=torch.float32, device=s.rt.device)
+        st = torch.empty(_lib.CG_STATS_BYTES, dtype=torch.uint8, device=s.rt.device) if stats is None else stats
+        xx = None
+        if x0 is not None:
+            xx = torch.as_tensor(x0, dtype=torch.float32, device=s.rt.device).contiguous()
+        s.rt.bind_stream()
+        s.rt.call("cv_row_solve_cg", s.h, float(mu), self.rhs.data_ptr(), float(config.tol), int(config.maxiter),
+                  int(config.stabilise_every), _lib.ptr(xx), out.data_ptr(), st.data_ptr())
+        return out, st
+
     def scaled_row_transpose(self, u) -> ParamVector:
         s = self._snap
         u = torch.as_tensor(u, dtype=torch.float32, device=s.rt.device).contiguous().reshape(-1)

@@ -2,8 +2,9 @@
 
 `cg_solve` on a snapshot's matvec runs the whole (P)CG loop on the device
 (`cv_cg_solve`: fused vector kernels, fp64 scalars, on-device termination, no
-host round trip per iteration).  Any other operator (e.g. a dense row-space Gram
-for `row_solve_cg`) runs the same recurrence with torch device ops.
+host round trip per iteration).  The row-space solves run natively on a
+snapshot's or a caller's dense Gram (`cv_row_solve_cg`, `cv_dense_*`); only an
+arbitrary user callable runs the recurrence with torch device ops.
 """
 
 from __future__ import annotations
@@ -167,29 +168,65 @@ def _cg_generic(mv, rhs, lam, cfg: CgConfig, precond=None, x0=None):
     return x, cfg.maxiter, False, relres, False, gv
 
 
-def row_solve_cholesky(gram, rhs, mu: float, row=None):
-    """(gram + mu I) v = rhs (solvers.py:146-161).
-
-    With `row` (a snapshot's RowOps whose Gram this is) the factorisation runs in
-    the native blocked Cholesky; a not-PD system raises ContractError.
-    """
-    if row is not None:
-        return row.solve_cholesky(mu, rhs)
+def _dense_gram(gram, rhs):
     G = _as_t(gram)
-    r = _as_t(rhs, G)
+    if not G.is_cuda:
+        G = G.to("cuda")
+    G = G.to(torch.float32).contiguous()
+    r = torch.as_tensor(rhs).to(device=G.device, dtype=torch.float32).contiguous().reshape(-1) \
+        if _is_torch(rhs) else torch.from_numpy(np.ascontiguousarray(rhs, dtype=np.float32)).to(G.device).reshape(-1)
     if G.dim() != 2 or G.shape[0] != G.shape[1]:
         raise ContractError("gram must be a square matrix")
     if tuple(r.shape) != (G.shape[0],):
         raise ContractError("rhs length does not match gram")
-    A = G.double() + mu * torch.eye(G.shape[0], dtype=torch.float64, device=G.device)
-    L, info = torch.linalg.cholesky_ex(A)
-    if int(info) != 0:
-        raise ContractError("row system is not positive definite; mu too small or gram invalid")
-    return torch.cholesky_solve(r.double().unsqueeze(1), L).squeeze(1)
+    return G, r
+
+
+def row_solve_cholesky(gram, rhs, mu: float, row=None):
+    """(gram + mu I) v = rhs (solvers.py:146-161), native blocked Cholesky.
+
+    With `row` (a snapshot's RowOps whose Gram this is) the snapshot's resident Gram
+    is factored; otherwise the caller's dense Gram (`cv_dense_cholesky_solve`).  A
+    not-PD system raises ContractError.
+    """
+    if row is not None:
+        return row.solve_cholesky(mu, rhs)
+    from .runtime import runtime
+
+    rt = runtime()
+    G, r = _dense_gram(gram, rhs)
+    out = torch.empty_like(r)
+    rt.bind_stream()
+    rt.call("cv_dense_cholesky_solve", rt.h, G.data_ptr(), G.shape[0], float(mu), r.data_ptr(), out.data_ptr())
+    return out
 
 
 def row_solve_cg(gram_matvec, rhs, mu: float, config: CgConfig, x0=None):
-    """Row-space CG on (gram + mu I) v = rhs (solvers.py:164-174)."""
+    """Row-space CG on (gram + mu I) v = rhs (solvers.py:164-174).
+
+    `gram_matvec` may be a snapshot's `row.gram_matvec`, a dense Gram matrix, or
+    `lambda u: gram @ u` over one (the reference's own call, method.py:279: pass the
+    matrix to keep the loop on the device); any other callable runs the recurrence
+    with device ops that read the scalars back every iteration."""
+    from .runtime import runtime
+
+    owner = getattr(gram_matvec, "__self__", None)
+    gram = None
+    if owner is not None and getattr(gram_matvec, "__name__", "") == "gram_matvec":
+        gram = owner.gram()
+    elif _is_torch(gram_matvec) or isinstance(gram_matvec, np.ndarray):
+        gram = gram_matvec
+    if gram is not None:
+        rt = runtime()
+        G, r = _dense_gram(gram, rhs)
+        out = torch.empty_like(r)
+        st = torch.empty(_lib.CG_STATS_BYTES, dtype=torch.uint8, device=G.device)
+        xx = None if x0 is None else torch.as_tensor(x0).to(device=G.device, dtype=torch.float32).contiguous()
+        rt.bind_stream()
+        rt.call("cv_dense_cg_solve", rt.h, G.data_ptr(), G.shape[0], float(mu), r.data_ptr(), float(config.tol),
+                int(config.maxiter), int(config.stabilise_every), _lib.ptr(xx), out.data_ptr(), st.data_ptr())
+        s = read_cg_stats(st)
+        return out, int(s.iterations), bool(s.converged), float(s.relres)
     r = _as_t(rhs)
     x, it, conv, rel, _, _ = _cg_generic(lambda u: _as_t(gram_matvec(u), r), r, mu, config,
                                          x0=None if x0 is None else _as_t(x0, r))

@@ -391,6 +391,39 @@ def harness_cases():
     save("harness", **out)
 
 
+def rowcg_cases():
+    """The row-space CG lane (egn_mse_cg: method.py:270-282, solvers.py:164-174) over a
+    few steps of the lane-scaling workload (bench.py:67-82), warm-started from the
+    previous row-space solution; plus one row_solve_cg on a snapshot Gram."""
+    from curvopt.harness.data import gen_regression
+    from curvopt.method import make
+    from curvopt.solvers import row_solve_cg
+
+    out = {}
+    train, _ = gen_regression(n=2000, d=32, noise_std=0.1, seed=0)
+    root = N.Rng(0)
+    m = Model(32, (64, 64), 1, "relu")
+    w = init_params(m, root.split())
+    batcher = EpochBatcher(train, 96, root.split())
+    meth = make("egn_mse_cg", m)
+    st = meth.init(w, seed=0)
+    rows = []
+    for t in range(5):
+        b = batcher.next()
+        if t == 0:
+            snap = make_snapshot("ggn_mse", m, w, b)
+            gram = snap.row.gram()
+            v, it, conv, rr = row_solve_cg(lambda u: gram @ u, snap.row.rhs, 96.0,
+                                           CgConfig(tol=1e-5, maxiter=10, stabilise_every=10, warm_start=True))
+            out["solve/v"] = v
+            out["solve/stats"] = np.array([it, int(conv), rr])
+        w, st, info = meth.step(w, b, st)
+        rows.append(info.to_row())
+    out["egn_mse_cg/info"] = np.array(rows, dtype=np.float64)
+    out["egn_mse_cg/w_final"] = w.data
+    save("rowcg", **out)
+
+
 if __name__ == "__main__":
     rng_cases()
     primitive_cases()
@@ -400,3 +433,4 @@ if __name__ == "__main__":
     chain_cases()
     gnb_cases()
     harness_cases()
+    rowcg_cases()

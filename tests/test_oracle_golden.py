@@ -261,3 +261,25 @@ def test_regression_data_and_newton_cg_cadence_run(golden):
     rows, wf = _run(spec, dims, "relu", "mse", w, batches)
     _cmp_rows(rows, g["newton_cg/info"], tol=1e-8)
     assert rel(wf, g["newton_cg/w_final"]) < 1e-11
+
+
+def test_row_cg_lane_matches_reference(golden):
+    """egn_mse_cg (method.py:270-282 -> solvers.py:164-174): row-space CG on the Gram,
+    warm-started from the previous step's row-space solution."""
+    g = golden("rowcg")
+    (Xtr, ytr), _ = O.gen_regression(2000, 32, 0.1, 0)
+    root = O.ORng(0)
+    dims = (32, 64, 64, 1)
+    w = O.init_params(dims, "relu", root.split())
+    bat = O.Batcher(Xtr, ytr, 96, root.split())
+    batches = [bat.next() for _ in range(5)]
+    lin = O.linearize(dims, "relu", "mse", w, *batches[0])
+    seeds, rhs = O.row_seeds_rhs(lin)
+    gram = O.output_gram(lin, seeds)
+    res = O.cg(lambda u: gram @ u, rhs, 96.0)
+    assert rel(res.x, g["solve/v"]) < 1e-12
+    assert [res.iterations, int(res.converged)] == [int(x) for x in g["solve/stats"][:2]]
+    spec = O.OSpec(curvature="ggn_mse", solver="row_cg", maxiter=5)
+    rows, wf = _run(spec, dims, "relu", "mse", w, batches)
+    _cmp_rows(rows, g["egn_mse_cg/info"], tol=1e-8)
+    assert rel(wf, g["egn_mse_cg/w_final"]) < 1e-11
