@@ -328,151 +328,128 @@ __global__ void __launch_bounds__(256) k_sym_mirror(float* G, int64_t m) {
 }
 
 
-// Factor the nb x nb diagonal block at j0 in fp64, write L11 back (lower) and its
-// inverse (fp32, row-major nb x nb) into dinv_blk; flag <- 1 if not positive definite.
-// Register-resident elimination on 4 x 4 tiles: thread t < 136 owns lower tile (bi, bj)
-// of the 16 x 16 tile grid (16 fp64 values in registers).  Step k applies
-// a_ij -= a_ik a_jk / a_kk to the owned values with j > k, reading column k from a
-// double-buffered shared row that the owners of column k+1 refill right after their
-// own update -- one barrier per column, the pivot's reciprocal published with it; the
-// scaling by 1/sqrt(a_kk) is applied once at the end.  X = L^-1 is formed the same way
-// (row k of X final at step k).  A partial block (nb < 64) is padded with the identity.
-constexpr int PD_T = 160;  // 136 tile owners, 5 warps
+// ---------------------------------------------------------------------------
+// Diagonal (panel) block factorization.  The nbo x nbo diagonal block of a panel
+// (nbo <= 512) is factored by 64-row tiles: one launch per tile column j, whose CTAs
+// own the lower tiles (r, c), j < c <= r: CTA (r, c) forms L_rj = A_rj Dinv_j^T and
+// L_cj (64^3 SIMT micro-GEMMs from shared memory), applies A_rc -= L_rj L_cj^T in
+// place, and the CTA of the next diagonal tile (j+1, j+1) factors it at once
+// (potrf64).  Column j is only read during launch j, so CTAs never race; L goes to a
+// separate nbo x nbo block (Lblk) read by k_trtri_panel.  8 dependent launches per
+// 512-wide panel.
+// ---------------------------------------------------------------------------
+constexpr int PS_LD = CH_NB + 1;  // padded shared row (floats)
 
-CV_DEV void tri_index(int e, int& i, int& j) {  // e-th element of the row-major lower triangle
-  i = (int)((sqrtf(8.f * (float)e + 1.f) - 1.f) * 0.5f);
-  while ((i + 1) * (i + 2) / 2 <= e) ++i;
-  while (i * (i + 1) / 2 > e) --i;
-  j = e - i * (i + 1) / 2;
-}
+struct Potrf64Smem {
+  float colb[2][CH_NB];         // column k of the elimination (row k of X), double buffered
+  float dg[CH_NB];              // pivots
+  float Lsc[CH_NB][CH_NB + 1];  // Lsc[k][i] = L_ik / L_ii (i > k)
+  int bad;
+};
 
-__global__ void __launch_bounds__(PD_T) k_potrf_diag(float* A, int64_t lda, int j0, int nb, float* dinv_blk,
-                                                     int* flag) {
-  CV_PDL_ENTRY();
-  __shared__ __align__(16) double colb[2][CH_NB];  // column k (row k of X), double buffered
-  __shared__ double rinv[2];                        // 1 / a_kk
-  __shared__ double dgv[CH_NB];                     // pivots a_kk
-  __shared__ double rdg[CH_NB];                     // 1 / sqrt(a_kk) = 1 / L_kk
-  __shared__ __align__(16) float LsT[CH_NB][CH_NB + 4];  // LsT[k][i] = L_ik / L_ii (i > k)
-  __shared__ int bad;
-  const int t = threadIdx.x;
-  const bool act = t < 136;
-  int bi = 0, bj = 0;
-  if (act) tri_index(t, bi, bj);
-  const bool diag = bi == bj;
-  double a[4][4];
+// Cholesky of a 64 x 64 SPD block held as 4 x 4 fp32 tiles by a 256-thread CTA
+// (thread (ty, tx) = (tid / 16, tid % 16) owns tile (ty, tx); the lower tiles are
+// used).  Step k applies a_ij -= a_ik a_jk / a_kk to the owned values with j > k,
+// reading column k (final after step k-1) from a double-buffered shared row that the
+// owners of column k+1 refill right after their own update: one barrier per column;
+// the scaling by 1/sqrt(a_kk) is applied once at the end.  X = L^-1 is formed the
+// same way (row k of X final at step k).  fp32 (the fp64 iterative refinement of the
+// solve absorbs the factor's rounding).  Rows/cols >= nb must hold the identity.
+CV_DEV void potrf64(float (&a)[4][4], int ty, int tx, int nb, float* Lout, int64_t ldl, float* Xout,
+                    Potrf64Smem& sm, int* flag) {
+  const bool own = ty >= tx;
+  if (threadIdx.x == 0) sm.bad = 0;
+  // column k lives in tile column k / 4, its column k % 4
+  auto pub_col = [&](int kb, auto kk_) {
+    constexpr int kk = decltype(kk_)::value;
+    if (!own || tx != kb) return;
+    float* cb = sm.colb[(4 * kb + kk) & 1];
 #pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int i = 4 * bi + r, j = 4 * bj + c;
-      double v = 0.0;
-      if (act && j <= i) v = (i < nb) ? (double)A[(int64_t)(j0 + i) * lda + j0 + j] : (i == j ? 1.0 : 0.0);
-      a[r][c] = v;
-    }
-  if (t == 0) bad = 0;
-  __syncthreads();
-  // column k = 4 kb + kk is owned by tile column bj = kb (its column kk)
-  auto publish = [&](int kb, auto kk_) {
+    for (int r = 0; r < 4; ++r) cb[4 * ty + r] = a[r][kk];
+  };
+  auto elim = [&](int kb, auto kk_) {
     constexpr int kk = decltype(kk_)::value;
     const int k = 4 * kb + kk;
-    if (!act || bj != kb) return;
-    double* cb = colb[k & 1];
+    const float* cb = sm.colb[k & 1];
+    float piv = cb[k];
+    if (!(piv > 0.f) || !isfinite(piv)) piv = 1.f;  // (flagged below by the pivot's owner)
+    if (threadIdx.x == 0) sm.dg[k] = cb[k];
+    if (!own || tx < kb) return;
+    const float rp = 1.f / piv;
+    float ci[4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) cb[4 * bi + r] = a[r][kk];
-    if (diag) {
-      double p = a[kk][kk];
-      if (!(p > 0.0) || !isfinite(p)) { bad = 1; p = 1.0; }
-      dgv[k] = p;
-      rinv[k & 1] = 1.0 / p;
+    for (int r = 0; r < 4; ++r) ci[r] = cb[4 * ty + r];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (tx == kb && c <= kk) continue;
+      const float sj = cb[4 * tx + c] * rp;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) a[r][c] = fmaf(-ci[r], sj, a[r][c]);
     }
   };
   using I0 = std::integral_constant<int, 0>;
   using I1 = std::integral_constant<int, 1>;
   using I2 = std::integral_constant<int, 2>;
   using I3 = std::integral_constant<int, 3>;
-  publish(0, I0{});
+  pub_col(0, I0{});
   __syncthreads();
-  auto elim = [&](int kb, auto kk_) {
-    constexpr int kk = decltype(kk_)::value;
-    const int k = 4 * kb + kk;
-    const double* cb = colb[k & 1];
-    if (act && bj >= kb) {
-      const double r = rinv[k & 1];
-      double ci[4], sj[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        ci[q] = cb[4 * bi + q];
-        sj[q] = cb[4 * bj + q] * r;
-      }
-      if (bj > kb) {
-#pragma unroll
-        for (int rr = 0; rr < 4; ++rr)
-#pragma unroll
-          for (int cc = 0; cc < 4; ++cc) a[rr][cc] -= ci[rr] * sj[cc];
-      } else {
-#pragma unroll
-        for (int rr = 0; rr < 4; ++rr)
-#pragma unroll
-          for (int cc = kk + 1; cc < 4; ++cc) a[rr][cc] -= ci[rr] * sj[cc];
-      }
-    }
-  };
   for (int kb = 0; kb < 16; ++kb) {
-    elim(kb, I0{}); publish(kb, I1{}); __syncthreads();
-    elim(kb, I1{}); publish(kb, I2{}); __syncthreads();
-    elim(kb, I2{}); publish(kb, I3{}); __syncthreads();
-    elim(kb, I3{}); if (kb + 1 < 16) publish(kb + 1, I0{}); __syncthreads();
+    elim(kb, I0{}); pub_col(kb, I1{}); __syncthreads();
+    elim(kb, I1{}); pub_col(kb, I2{}); __syncthreads();
+    elim(kb, I2{}); pub_col(kb, I3{}); __syncthreads();
+    elim(kb, I3{}); if (kb + 1 < 16) pub_col(kb + 1, I0{}); __syncthreads();
   }
-  for (int k = t; k < CH_NB; k += PD_T) rdg[k] = 1.0 / sqrt(dgv[k]);
-  __syncthreads();
-  // L_ij = a_ij / L_jj; the inverse's multipliers L_ik / L_ii (rounded to fp32 like the
-  // stored factor, so dinv inverts exactly what the solves read)
-  float lf[4][4];
+  // L_ij = a_ij / sqrt(d_j) (i > j), L_jj = sqrt(d_j); Lsc[k][i] = L_ik / L_ii
+  float rs[4], rsi[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    float d = sm.dg[4 * tx + q];
+    if (!(d > 0.f) || !isfinite(d)) {
+      if (ty == tx) sm.bad = 1;
+      d = 1.f;
+    }
+    rs[q] = rsqrtf(d);
+    float di = sm.dg[4 * ty + q];
+    if (!(di > 0.f) || !isfinite(di)) di = 1.f;
+    rsi[q] = rsqrtf(di);
+  }
+  float l[4][4];
 #pragma unroll
   for (int r = 0; r < 4; ++r)
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      const int i = 4 * bi + r, j = 4 * bj + c;
-      lf[r][c] = (float)(i == j ? dgv[j] * rdg[j] : a[r][c] * rdg[j]);
-      if (act && j < i) LsT[j][i] = (float)((double)lf[r][c] * rdg[i]);
+      const bool dgl = ty == tx && r == c;
+      l[r][c] = (ty == tx && c > r) ? 0.f : (dgl ? 1.f / rs[c] : a[r][c] * rs[c]);
+      if (own && (ty > tx || r > c)) sm.Lsc[4 * tx + c][4 * ty + r] = l[r][c] * rsi[r];
     }
-  // X = L^-1: x[i][c] starts at delta_ic / L_ii; step k: x[i][c] -= (L_ik / L_ii) X[k][c]
-  double x[4][4];
+  // X = L^-1: x[i][c] = delta_ic / L_ii, then x[i][c] -= (L_ik / L_ii) X[k][c] for k < i
+  float x[4][4];
 #pragma unroll
   for (int r = 0; r < 4; ++r)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) x[r][c] = (diag && r == c) ? rdg[4 * bi + r] : 0.0;
+    for (int c = 0; c < 4; ++c) x[r][c] = (ty == tx && r == c) ? rsi[r] : 0.f;
   __syncthreads();
-  auto pub_row = [&](int kb, auto kk_) {  // row k of X, owned by tile row bi = kb
+  auto pub_row = [&](int kb, auto kk_) {
     constexpr int kk = decltype(kk_)::value;
-    const int k = 4 * kb + kk;
-    if (!act || bi != kb) return;
-    double* rb = colb[k & 1];
+    if (!own || ty != kb) return;
+    float* rb = sm.colb[(4 * kb + kk) & 1];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) rb[4 * bj + c] = x[kk][c];
+    for (int c = 0; c < 4; ++c) rb[4 * tx + c] = x[kk][c];
   };
   auto inv_step = [&](int kb, auto kk_) {
     constexpr int kk = decltype(kk_)::value;
     const int k = 4 * kb + kk;
-    if (!act || bi < kb || bj > kb) return;  // X[k][c] = 0 for c > k (tile columns right of kb)
-    const double* rb = colb[k & 1];
-    double xk[4], lk[4];
+    if (!own || ty < kb || tx > kb) return;  // X[k][c] = 0 for c > k
+    const float* rb = sm.colb[k & 1];
+    float xk[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      xk[q] = rb[4 * bj + q];
-      lk[q] = (double)LsT[k][4 * bi + q];
-    }
-    if (bi > kb) {
+    for (int c = 0; c < 4; ++c) xk[c] = rb[4 * tx + c];
 #pragma unroll
-      for (int rr = 0; rr < 4; ++rr)
+    for (int r = 0; r < 4; ++r) {
+      if (ty == kb && r <= kk) continue;
+      const float lk = sm.Lsc[k][4 * ty + r];
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) x[rr][cc] -= lk[rr] * xk[cc];
-    } else {
-#pragma unroll
-      for (int rr = kk + 1; rr < 4; ++rr)
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) x[rr][cc] -= lk[rr] * xk[cc];
+      for (int c = 0; c < 4; ++c) x[r][c] = fmaf(-lk, xk[c], x[r][c]);
     }
   };
   for (int kb = 0; kb < 16; ++kb) {
@@ -481,22 +458,154 @@ __global__ void __launch_bounds__(PD_T) k_potrf_diag(float* A, int64_t lda, int 
     pub_row(kb, I2{}); __syncthreads(); inv_step(kb, I2{});
     pub_row(kb, I3{}); __syncthreads(); inv_step(kb, I3{});
   }
-  if (act) {
+  if (own) {
 #pragma unroll
     for (int r = 0; r < 4; ++r)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const int i = 4 * bi + r, j = 4 * bj + c;
+        const int i = 4 * ty + r, j = 4 * tx + c;
         if (i >= nb || j >= nb) continue;
         if (j <= i) {
-          dinv_blk[i * nb + j] = (float)x[r][c];
-          A[(int64_t)(j0 + i) * lda + j0 + j] = lf[r][c];
-          if (j != i) dinv_blk[j * nb + i] = 0.f;
+          Xout[i * nb + j] = x[r][c];
+          Lout[(int64_t)i * ldl + j] = l[r][c];
+          if (j != i) Xout[j * nb + i] = 0.f;
         }
       }
   }
-  if (t == 0 && bad) *flag = 1;
+  __syncthreads();
+  if (threadIdx.x == 0 && sm.bad) *flag = 1;
 }
+
+// 64 x 64 tile (rows < rows_valid, cols < cols_valid, zero elsewhere) -> shared (ld PS_LD)
+CV_DEV void load_tile(float* dst, const float* src, int64_t ld, int rows_valid, int cols_valid) {
+  for (int e = threadIdx.x; e < CH_NB * CH_NB; e += blockDim.x) {
+    const int i = e >> 6, j = e & 63;
+    dst[i * PS_LD + j] = (i < rows_valid && j < cols_valid) ? src[(int64_t)i * ld + j] : 0.f;
+  }
+}
+// acc[r][c] (+)= sign * sum_k X[4ty+r][k] Y[4tx+c][k]   (X, Y in shared memory, ld PS_LD)
+CV_DEV void mm_xyt(const float* X, const float* Y, int ty, int tx, float (&acc)[4][4], float sign) {
+#pragma unroll 4
+  for (int k = 0; k < CH_NB; ++k) {
+    float xr[4], yr[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      xr[q] = X[(4 * ty + q) * PS_LD + k];
+      yr[q] = Y[(4 * tx + q) * PS_LD + k];
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[r][c] = fmaf(sign * xr[r], yr[c], acc[r][c]);
+  }
+}
+
+// First diagonal tile of a panel: factor A[p0.., p0..] (64 x 64, nb valid).
+__global__ void __launch_bounds__(256) k_potrf_diag(const float* A, int64_t lda, int nb, float* Lblk, int64_t ldl,
+                                                    float* dinv_blk, int* flag) {
+  CV_PDL_ENTRY();
+  __shared__ Potrf64Smem sm;
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+  float a[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = 4 * ty + r, j = 4 * tx + c;
+      a[r][c] = (i < nb && j < nb) ? A[(int64_t)i * lda + j] : (i == j ? 1.f : 0.f);
+    }
+  potrf64(a, ty, tx, nb, Lblk, ldl, dinv_blk, sm, flag);
+}
+
+// Launch j of a panel's diagonal-block factorization (see above).  blockIdx.x
+// enumerates the lower tiles (r, c), j < c <= r < nsub.
+__global__ void __launch_bounds__(256) k_panel_step(float* A, int64_t lda, int nbo, int j, float* Lblk,
+                                                    float* dinv, int* flag) {
+  CV_PDL_ENTRY();
+  extern __shared__ __align__(16) unsigned char psm[];
+  float* D = reinterpret_cast<float*>(psm);              // Dinv_j
+  float* T = D + CH_NB * PS_LD;                          // A_rj / A_cj staging
+  float* LR = T + CH_NB * PS_LD;
+  float* LC = LR + CH_NB * PS_LD;
+  Potrf64Smem& sm = *reinterpret_cast<Potrf64Smem*>(LC + CH_NB * PS_LD);
+  int e = blockIdx.x, r = j + 1;
+  while (e >= r - j) { e -= r - j; ++r; }
+  const int c = j + 1 + e;
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+  auto bsize = [&](int b) { return nbo - CH_NB * b < CH_NB ? nbo - CH_NB * b : CH_NB; };
+  const int nbj = bsize(j), nbr = bsize(r), nbc = bsize(c);
+  {
+    const float* Dj = dinv + (int64_t)j * CH_NB * CH_NB;
+    for (int q = threadIdx.x; q < CH_NB * CH_NB; q += blockDim.x) {
+      const int i = q >> 6, k = q & 63;
+      D[i * PS_LD + k] = (i < nbj && k < nbj) ? Dj[i * nbj + k] : 0.f;
+    }
+  }
+  // L_rj = A_rj Dinv_j^T
+  load_tile(T, A + (int64_t)CH_NB * r * lda + CH_NB * j, lda, nbr, nbj);
+  __syncthreads();
+  float acc[4][4] = {};
+  mm_xyt(T, D, ty, tx, acc, 1.f);
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) LR[(4 * ty + rr) * PS_LD + 4 * tx + cc] = acc[rr][cc];
+  if (c == j + 1) {  // one writer per L tile of column j
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const int i = 4 * ty + rr, k = 4 * tx + cc;
+        if (i < nbr && k < nbj) Lblk[(int64_t)(CH_NB * r + i) * nbo + CH_NB * j + k] = acc[rr][cc];
+      }
+  }
+  const float* LCp = LR;
+  if (c != r) {
+    __syncthreads();  // T reused
+    load_tile(T, A + (int64_t)CH_NB * c * lda + CH_NB * j, lda, nbc, nbj);
+    __syncthreads();
+    float acc2[4][4] = {};
+    mm_xyt(T, D, ty, tx, acc2, 1.f);
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) LC[(4 * ty + rr) * PS_LD + 4 * tx + cc] = acc2[rr][cc];
+    LCp = LC;
+  }
+  __syncthreads();
+  // A_rc -= L_rj L_cj^T
+  float* Arc = A + (int64_t)CH_NB * r * lda + CH_NB * c;
+  float u[4][4];
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      const int i = 4 * ty + rr, k = 4 * tx + cc;
+      u[rr][cc] = (i < nbr && k < nbc) ? Arc[(int64_t)i * lda + k] : 0.f;
+    }
+  mm_xyt(LR, LCp, ty, tx, u, -1.f);
+  if (r == c && r == j + 1) {
+    float a[4][4];
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const int i = 4 * ty + rr, k = 4 * tx + cc;
+        a[rr][cc] = (i < nbr && k < nbr) ? u[rr][cc] : (i == k ? 1.f : 0.f);
+      }
+    potrf64(a, ty, tx, nbr, Lblk + (int64_t)CH_NB * r * nbo + CH_NB * r, nbo, dinv + (int64_t)r * CH_NB * CH_NB, sm,
+            flag);
+  } else {
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const int i = 4 * ty + rr, k = 4 * tx + cc;
+        if (i < nbr && k < nbc) Arc[(int64_t)i * lda + k] = u[rr][cc];
+      }
+  }
+}
+constexpr int PS_SMEM = 4 * CH_NB * PS_LD * 4 + (int)sizeof(Potrf64Smem);
 
 // W = L11^-1 for the nbo x nbo diagonal block of a panel (nbo <= TT_MAX), from the
 // factored block (lower, in A at (p0, p0)) and the inverses of its 64-blocks (dinv):
@@ -781,7 +890,7 @@ int dense_cholesky_solve(cv_ctx* ctx, const float* gram, int64_t m, double mu, c
   cudaMemsetAsync(flag, 0, sizeof(int), st);
   ctx->launches++;
   constexpr int NBO = TT_MAX;  // panel width (a multiple of CH_NB)
-  const bool tc = ctx->engine != CV_ENGINE_SIMT && m > NBO;
+  const bool tc = m > NBO;     // (the GEMMs follow the context's engine selection)
   __half *l21h = nullptr, *l21l = nullptr, *wh = nullptr, *wl = nullptr;
   if (tc) {
     l21h = (__half*)ctx->pool.get(sizeof(__half) * (size_t)(m - NBO) * NBO);
@@ -791,48 +900,33 @@ int dense_cholesky_solve(cv_ctx* ctx, const float* gram, int64_t m, double mu, c
   }
   Scale* l21sc = scr_sc;
   Scale* wsc = scr_sc + 1;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_panel_step, cudaFuncAttributeMaxDynamicSharedMemorySize, PS_SMEM);
+    attr = true;
+  }
+  float* Lblk = (float*)ctx->pool.get(sizeof(float) * (size_t)NBO * NBO);
   for (int64_t p0 = 0; p0 < m; p0 += NBO) {
     const int nbo = (int)((m - p0) < NBO ? (m - p0) : NBO);
-    const int64_t pend = tc ? p0 + nbo : m;  // columns (and rows) the in-block updates cover
-    for (int64_t j0 = p0; j0 < p0 + nbo; j0 += CH_NB) {
-      const int bi = (int)(j0 / CH_NB);
-      const int nb = (int)((m - j0) < CH_NB ? (m - j0) : CH_NB);
-      float* dblk = dinv + (int64_t)bi * CH_NB * CH_NB;
-      launch_k(st, k_potrf_diag, 1, PD_T, 0, chol, m, (int)j0, nb, dblk, flag);
+    const int nsub = (nbo + CH_NB - 1) / CH_NB;
+    float* Ad = chol + p0 * m + p0;
+    float* dp = dinv + (p0 / CH_NB) * (int64_t)CH_NB * CH_NB;
+    // (1) the diagonal block: first tile, then one launch per tile column
+    launch_k(st, k_potrf_diag, 1, 256, 0, (const float*)Ad, m, nbo < CH_NB ? nbo : CH_NB, Lblk, (int64_t)nbo, dp,
+             flag);
+    ctx->launches++;
+    for (int j = 0; j + 1 < nsub; ++j) {
+      const int tiles = (nsub - j - 1) * (nsub - j) / 2;
+      launch_k(st, k_panel_step, tiles, 256, PS_SMEM, Ad, m, nbo, j, Lblk, dp, flag);
       ctx->launches++;
-      const int rest = (int)(pend - j0 - nb);
-      if (rest <= 0) continue;
-      float* A21 = chol + (int64_t)(j0 + nb) * m + j0;
-      // A21 <- A21 * L11^-T
-      GemmArgs p;
-      p.M = rest;
-      p.N = nb;
-      p.nseg = 1;
-      p.seg[0] = GemmSeg{f32op(A21, m, 1), f32op(dblk, 1, nb), nb};
-      p.epi.mode = EPI_STORE;
-      p.epi.out = A21;
-      p.epi.ld = m;
-      gemm_simt(ctx, p);  // in place: one N tile per CTA row block
-      // A22 -= A21 A21^T, lower part of [j0+nb, pend)^2
-      GemmArgs u;
-      u.M = rest;
-      u.N = rest;
-      u.nseg = 1;
-      u.seg[0] = GemmSeg{f32op(A21, m, 1), f32op(A21, 1, m), nb};
-      u.epi.mode = EPI_ACCUM;
-      u.epi.alpha = -1.f;
-      u.epi.out = chol + (int64_t)(j0 + nb) * m + (j0 + nb);
-      u.epi.ld = m;
-      u.lower_only = 1;
-      gemm_simt(ctx, u);
     }
     // (2) W = L11^-1 (kept: the triangular solves below multiply by it)
     float* W = winv + (p0 / NBO) * (int64_t)NBO * NBO;
-    launch_k(st, k_trtri_panel, (nbo + TT_C - 1) / TT_C, 256, 0, (const float*)chol, m, (const float*)dinv, (int)p0,
-             nbo, W);
+    launch_k(st, k_trtri_panel, (nbo + TT_C - 1) / TT_C, 256, 0, (const float*)Lblk, (int64_t)nbo,
+             (const float*)dp, 0, nbo, W);
     ctx->launches++;
     const int rest2 = (int)(m - p0 - nbo);
-    if (!tc || rest2 <= 0) continue;
+    if (rest2 <= 0) continue;
     // (3) L21 = A21 W^T on the tensor cores (A21 split first; the GEMM writes fp32 L21 in place)
     float* A21 = chol + (p0 + nbo) * m + p0;
     split_mat(ctx, A21, m, rest2, nbo, l21h, l21l, nbo, 0, l21sc, 0, nullptr);
@@ -868,6 +962,7 @@ int dense_cholesky_solve(cv_ctx* ctx, const float* gram, int64_t m, double mu, c
     u.lower_only = 1;
     gemm(ctx, u);
   }
+  ctx->pool.put(Lblk);
   if (tc) {
     ctx->pool.put(l21h);
     ctx->pool.put(l21l);
