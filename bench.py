@@ -12,6 +12,10 @@ the reference's SplitMix64 stream (MNIST-shaped), random-init weights (init_para
 --config c4: configs[3], row-space lane (Gram + Cholesky), 3072-2048-2048-10, b=4096.
 --config c5: configs[4], exact-Hessian HVP + CG + trace/diag telemetry,
              3072-4096x4-10, b=32768 (on N GPUs: b/N rows per rank).
+--config cadence: the paper's only published measurement of this path (PAPER.md
+             Table 3): newton_cg on MLP 512-1024-1024-1, b=256, constant damping,
+             CG maxiter 3, rho_every_k in {-1, 10, 5, 2, 1}, paired step timing
+             (harness.bench_cadence); value = median step ms with rho off.
 
 With N GPUs the global batch is sharded b/N per rank (strong scaling: the total work
 is fixed); every gradient and curvature product is NCCL all-reduced inside the native
@@ -152,6 +156,140 @@ def spec_c5():
 
 
 SPECS = {"c3": spec_c3, "c4": spec_c4, "c5": spec_c5}
+
+CADENCE_METRIC = ("newton_cg planned-step median ms, rho probes off (PAPER Table 3 workload: MLP 512-1024-1024-1, "
+                  "b=256, HVP + CG maxiter 3, constant damping)")
+CADENCE_KS = [-1, 10, 5, 2, 1]
+CADENCE_DIMS = (512, 1024, 1024, 1)
+
+
+def cadence_config(world):
+    return {"workload": "cadence study (bench.py:135-207): newton_cg, synth_regression n=20000 d=512, "
+                        "512-1024-1024-1 ReLU, b=256, constant lam=1, CG maxiter 3 warm start, "
+                        "rho_every_k in {-1,10,5,2,1}, paired timing, window 50",
+            "global_batch": 256, "dims": list(CADENCE_DIMS), "parallelism": f"replicas ({world})",
+            "l2": "working set < L2 (latency-bound step; the paper's protocol, no flush)"}
+
+
+def cpu_cadence_sample(steps, warmup, max_seconds=20.0):
+    """The oracle's newton_cg step (rho off) on the cadence workload: median ms."""
+    from oracle import curvopt_oracle as O
+
+    (Xtr, ytr), _ = O.gen_regression(20000, 512, 0.1, 0)
+    root = O.ORng(0)
+    w = O.init_params(CADENCE_DIMS, "relu", root.split())
+    bat = O.Batcher(Xtr, ytr, 256, root.split())
+    spec = O.OSpec(curvature="hessian", maxiter=3, rho_every_k=-1)
+    st = O.oracle_init(spec, w.size)
+    times = []
+    t_all = time.perf_counter()
+    for i in range(steps + warmup):
+        X, y = bat.next()
+        t0 = time.perf_counter()
+        w, st, _, _ = O.oracle_step(spec, CADENCE_DIMS, "relu", "mse", w, X, y, st)
+        if i >= warmup:
+            times.append((time.perf_counter() - t0) * 1e3)
+        if time.perf_counter() - t_all > max_seconds and len(times) >= 3:
+            break
+    return float(np.median(times)), len(times)
+
+
+def run_cadence(args, rank, world):
+    """The cadence study on the device (replicas: rank 0 reports)."""
+    import torch
+
+    import paper_2603_25976_b200 as P
+    from paper_2603_25976_b200 import harness as H
+    from paper_2603_25976_b200.runtime import runtime
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    rt = runtime()
+    window = min(50, args.steps)
+    H.bench_cadence(CADENCE_KS, steps=4, window=4, warmup=2)  # allocator / plan warm-up
+    launches0 = rt.launches()
+    gc.collect()
+    gc.disable()
+    t_wall = time.perf_counter()
+    with ClockSampler(dev.index) as clk:
+        rows = H.bench_cadence(CADENCE_KS, steps=args.steps, window=window, warmup=args.warmup)
+    wall = time.perf_counter() - t_wall
+    launches = rt.launches() - launches0
+    gc.enable()
+    table = [{"rho_every_k": k, "median_ms": med, "p90_ms": p90, "overhead_pct": ov,
+              "paper_median_ms": H.PAPER_TABLE3_MS[k][0], "paper_p90_ms": H.PAPER_TABLE3_MS[k][1]}
+             for k, med, p90, ov in rows]
+    med_off = rows[0][1]
+    # e2e: the rho-off setting through the public API with host buffers (pinned batch in,
+    # host parameters out every step), wall clock around the step as the protocol does
+    train, _ = H.gen_regression(20000, 512, 0.1, 0)
+    model = P.Model(512, (1024, 1024), 1, "relu")
+    meth = H.cadence_methods([-1], model)[-1]
+    root = P.Rng(0)
+    w = P.init_params(model, root.split())
+    w = P.ParamVector(torch.from_numpy(np.asarray(w.data, dtype=np.float32)).pin_memory(), w.layout)
+    bat = H.EpochBatcher(train, 256, root.split())
+    Xh = torch.from_numpy(np.ascontiguousarray(train.X, dtype=np.float32)).pin_memory()
+    yh = torch.from_numpy(np.ascontiguousarray(train.y, dtype=np.float32)).pin_memory()
+    st = meth.init(w, seed=0)
+    et = []
+    for t in range(args.steps + args.warmup):
+        idx = torch.from_numpy(np.ascontiguousarray(bat.next_indices(), dtype=np.int64))
+        b = P.Batch(Xh[idx].pin_memory(), yh[idx].pin_memory(), "mse")
+        t0 = time.perf_counter()
+        w, st, _ = meth.step(w, b, st)
+        et.append((time.perf_counter() - t0) * 1e3)
+    e2e_ms = H.timing_summary(et, args.warmup, window).median_ms
+    # roofline of the dominant unit: one HVP at b=256 (the step's products), CUDA events
+    wd = P.init_params(model, P.Rng(0)).to_device(dev)
+    Xd = torch.from_numpy(np.ascontiguousarray(train.X[:256], dtype=np.float32)).to(dev)
+    yd = torch.from_numpy(np.ascontiguousarray(train.y[:256], dtype=np.float32)).to(dev)
+    snap = P.make_snapshot("hessian", model, wd, P.Batch(Xd, yd, "mse"))
+    v = torch.randn(wd.dim, device=dev)
+    out = torch.empty_like(v)
+    for _ in range(5):
+        snap.apply(1, v, out)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record(stream)
+    for _ in range(50):
+        snap.apply(1, v, out)
+    g1.record(stream)
+    torch.cuda.synchronize()
+    hvp_ms = g0.elapsed_time(g1) / 50
+    snap.close()
+    flops = hvp_flops(CADENCE_DIMS, 256)
+    try:
+        peak = f16_peak_tflops() / 3.0
+        peak_note = "measured cuBLAS fp16 / 3 (3xFP16 split passes)"
+    except Exception:
+        peak = measured_peaks().get("bf16_tflops", 1626.3) / 3
+        peak_note = "MEASURED_PEAKS bf16 burst / 3"
+    achieved = flops / (hvp_ms * 1e-3) / 1e12
+    if rank != 0:
+        return
+    line = {"metric": CADENCE_METRIC, "value": med_off, "unit": "ms", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": med_off, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": med_off / H.PAPER_TABLE3_MS[-1][0],
+            "vs_baseline_note": "value / 0.84 ms (PAPER Table 3, RTX A4000 JAX, rho off; BASELINE.md row 1)",
+            "dtype": "f32 (scaled 3xFP16 tensor-core GEMMs, fp32 accumulate, fp64 reductions)",
+            "data": "synthetic (reference gen_regression)", "config": cadence_config(world), "cadence": table,
+            "wall_s_all_settings": wall,
+            "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": 256 * 512 * 4 + 256 * 4 + wd.dim * 4,
+                    "d2h_bytes_per_step": wd.dim * 4 + 24 * 8},
+            "gpu_launches": launches, "clocks": clk.summary(),
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None, "traffic_source": None,
+                         "unit_of_work": f"one HVP at b=256: {flops / 1e9:.2f} GFLOP useful, {hvp_ms * 1e3:.1f} us "
+                                         f"avg over 50 (CUDA events); launch/latency-bound at this size",
+                         "peak_source": peak_note}}
+    if not args.no_cpu:
+        med_cpu, n = cpu_cadence_sample(10, 2)
+        line["cpu_baseline"] = {"value": med_cpu, "unit": "ms", "cores": host_cores(), "kind": "port",
+                                "sample": f"{n} newton_cg steps (rho off) of the numpy/OpenBLAS f64 oracle, median",
+                                "cpu_model": cpu_model()}
+    print(json.dumps(line), flush=True)
 
 
 class ClockSampler:
@@ -362,6 +500,20 @@ def run_reference(args, rank, world):
     """The reference arm: the CPU restatement of curvopt's step on the host cores."""
     if rank != 0:
         return
+    if args.config == "cadence":
+        med, n = cpu_cadence_sample(args.steps, args.warmup, max_seconds=120.0)
+        cores = host_cores()
+        print(json.dumps({"impl": "reference", "metric": CADENCE_METRIC, "value": med, "unit": "ms",
+                          "n_gpus": world, "steps": n, "warmup": args.warmup, "ms_per_step": med,
+                          "higher_is_better": False, "scaling": "weak", "vs_baseline": med / 0.84,
+                          "dtype": "f64", "data": "synthetic (reference gen_regression)",
+                          "config": cadence_config(world),
+                          "cpu_baseline": {"value": med, "unit": "ms", "cores": cores, "kind": "port",
+                                           "sample": f"{n} newton_cg steps (rho off), oracle port, median",
+                                           "cpu_model": cpu_model()},
+                          "e2e": {"value": med, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+              flush=True)
+        return
     wl = WORKLOADS[args.config]
     cores = host_cores()
     if wl.key == "c3":
@@ -564,7 +716,10 @@ def _rank_main(args):
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         dist.init_process_group("nccl")
     try:
-        run_ours(args, rank, world)
+        if args.config == "cadence":
+            run_cadence(args, rank, world)
+        else:
+            run_ours(args, rank, world)
     finally:
         if world > 1:
             import torch.distributed as dist
@@ -584,7 +739,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="c3", choices=sorted(WORKLOADS) + ["cadence"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

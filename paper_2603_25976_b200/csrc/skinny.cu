@@ -123,14 +123,19 @@ __global__ void __launch_bounds__(256) k_rows(SkinnyRowsArgs a) {
   if (lane == 0 && a.out_amax) atomic_amax(a.out_amax, amax);
 }
 
+template <int CM, int RPW>
+static void launch_rows(cv_ctx* ctx, const SkinnyRowsArgs& a) {
+  launch_k(ctx->stream, k_rows<CM, RPW>, (a.rows + 8 * RPW - 1) / (8 * RPW), 256, 0, a);
+}
+
 void skinny_rows(cv_ctx* ctx, const SkinnyRowsArgs& a) {
-  if (a.c <= 16) {
-    constexpr int RPW = 4;
-    launch_k(ctx->stream, k_rows<16, RPW>, (a.rows + 8 * RPW - 1) / (8 * RPW), 256, 0, a);
-  } else {
-    constexpr int RPW = 2;
-    launch_k(ctx->stream, k_rows<32, RPW>, (a.rows + 8 * RPW - 1) / (8 * RPW), 256, 0, a);
-  }
+  // one row per warp unless that already gives >= 2 blocks per SM (small batches:
+  // every row in flight at once)
+  const bool many = (a.rows + 7) / 8 >= 2 * ctx->sm_count;
+  if (a.c == 1) many ? launch_rows<1, 4>(ctx, a) : launch_rows<1, 1>(ctx, a);
+  else if (a.c <= 4) many ? launch_rows<4, 4>(ctx, a) : launch_rows<4, 1>(ctx, a);
+  else if (a.c <= 16) many ? launch_rows<16, 4>(ctx, a) : launch_rows<16, 1>(ctx, a);
+  else many ? launch_rows<32, 2>(ctx, a) : launch_rows<32, 1>(ctx, a);
   ctx->launches++;
 }
 
@@ -449,7 +454,9 @@ void skinny_dx(cv_ctx* ctx, const SkinnyDxArgs& a) {
     return;
   }
   const bool two = a.nseg > 1;
-  if (a.c == 10) two ? launch_dx<10, 2>(ctx, a) : launch_dx<10, 1>(ctx, a);
+  if (a.c == 1) two ? launch_dx<1, 2>(ctx, a) : launch_dx<1, 1>(ctx, a);  // scalar regression output
+  else if (a.c <= 4) two ? launch_dx<4, 2>(ctx, a) : launch_dx<4, 1>(ctx, a);
+  else if (a.c == 10) two ? launch_dx<10, 2>(ctx, a) : launch_dx<10, 1>(ctx, a);
   else if (a.c <= 16) two ? launch_dx<16, 2>(ctx, a) : launch_dx<16, 1>(ctx, a);
   else two ? launch_dx<32, 2>(ctx, a) : launch_dx<32, 1>(ctx, a);
   ctx->launches++;
@@ -532,14 +539,16 @@ __global__ void k_dw_final(SkinnyDwArgs a) {
 void skinny_dw(cv_ctx* ctx, SkinnyDwArgs a, float* ws, int64_t ws_elems) {
   const int mblocks = (a.M + 511) / 512;
   int ks = (4 * ctx->sm_count + mblocks - 1) / mblocks;
-  const int max_by_rows = (a.rows + 63) / 64;
+  const int max_by_rows = (a.rows + 15) / 16;  // >= 16 rows per block: small batches still fill the SMs
   if (ks > max_by_rows) ks = max_by_rows;
   while (ks > 1 && (int64_t)ks * a.M * a.c > ws_elems) --ks;
   if (ks < 1) ks = 1;
   a.ksplit = ks;
   a.partial = ws;
   dim3 grid(mblocks, ks);
-  if (a.c <= 16) launch_k(ctx->stream, k_dw_partial<16>, grid, 128, 0, a);
+  if (a.c == 1) launch_k(ctx->stream, k_dw_partial<1>, grid, 128, 0, a);
+  else if (a.c <= 4) launch_k(ctx->stream, k_dw_partial<4>, grid, 128, 0, a);
+  else if (a.c <= 16) launch_k(ctx->stream, k_dw_partial<16>, grid, 128, 0, a);
   else launch_k(ctx->stream, k_dw_partial<32>, grid, 128, 0, a);
   const int64_t total = (int64_t)a.M * a.c;
   launch_k(ctx->stream, k_dw_final, (int)((total + 255) / 256), 256, 0, a);
