@@ -105,6 +105,13 @@ CV_API int cv_ctx_destroy(cv_ctx* ctx);
 CV_API int cv_ctx_set_stream(cv_ctx* ctx, void* cuda_stream);
 CV_API int cv_ctx_set_engine(cv_ctx* ctx, int engine);   /* CV_ENGINE_*: GEMM engine selection */
 CV_API const char* cv_last_error(const cv_ctx* ctx);
+/* CUDA-graph capture support: between begin and end every device buffer the library
+ * allocates (snapshots, solver scratch, split-K partials) comes from a fresh arena that
+ * the caller then owns with the captured graph (replays write into it, so it must not be
+ * shared with other work); cv_arena_free releases it once the graph is destroyed. */
+CV_API int cv_ctx_capture_begin(cv_ctx* ctx);
+CV_API int cv_ctx_capture_end(cv_ctx* ctx, void** arena_out);
+CV_API int cv_arena_free(cv_ctx* ctx, void* arena);
 CV_API int cv_nccl_unique_id(void* out128);               /* host buffer of 128 bytes */
 CV_API const char* cv_version(void);
 CV_API int64_t cv_kernel_launches(const cv_ctx* ctx);     /* kernels enqueued so far (instrumentation) */

@@ -50,6 +50,9 @@ _SIGS = {
     "cv_ctx_set_stream": (C.c_int, [_P, _P]),
     "cv_ctx_set_engine": (C.c_int, [_P, C.c_int]),
     "cv_last_error": (C.c_char_p, [_P]),
+    "cv_ctx_capture_begin": (C.c_int, [_P]),
+    "cv_ctx_capture_end": (C.c_int, [_P, C.POINTER(_P)]),
+    "cv_arena_free": (C.c_int, [_P, _P]),
     "cv_nccl_unique_id": (C.c_int, [_P]),
     "cv_kernel_launches": (C.c_int64, [_P]),
     "cv_linearize": (C.c_int, [_P, C.c_int, _P, C.c_int, C.c_int, _P, _P, _P, C.c_int, C.c_int,

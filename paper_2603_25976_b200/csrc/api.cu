@@ -140,6 +140,28 @@ int cv_ctx_set_engine(cv_ctx* ctx, int engine) {
 
 const char* cv_last_error(const cv_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
+int cv_ctx_capture_begin(cv_ctx* ctx) {
+  CV_TRY(ctx)
+  contract(_ctx->pool.redirected() == nullptr, "a graph capture is already open on this context");
+  _ctx->pool.redirect(new Pool());
+  CV_CATCH
+}
+
+int cv_ctx_capture_end(cv_ctx* ctx, void** arena_out) {
+  if (!ctx || !arena_out) return CV_E_CONTRACT;
+  Pool* a = ctx->pool.redirected();
+  ctx->pool.redirect(nullptr);
+  *arena_out = a;
+  return a ? CV_OK : CV_E_CONTRACT;
+}
+
+int cv_arena_free(cv_ctx* ctx, void* arena) {
+  if (!ctx) return CV_E_CONTRACT;
+  cudaSetDevice(ctx->device);
+  delete static_cast<Pool*>(arena);  // (after the graph that wrote into it is gone)
+  return CV_OK;
+}
+
 int64_t cv_kernel_launches(const cv_ctx* ctx) { return ctx ? ctx->launches : -1; }
 
 // ---------------------------------------------------------------------------

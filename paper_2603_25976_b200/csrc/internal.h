@@ -127,11 +127,17 @@ class Pool {
   void* get(size_t bytes);
   void put(void* p);
   void release_all();
+  bool owns(void* p) const { return live_.count(p) != 0; }
+  // While a CUDA graph is captured, allocations come from a separate arena the graph
+  // owns: its replays write into those blocks, which must never be handed to other work.
+  void redirect(Pool* arena) { redirect_ = arena; }
+  Pool* redirected() const { return redirect_; }
   ~Pool() { release_all(); }
 
  private:
   std::map<void*, size_t> live_;
   std::multimap<size_t, void*> free_;
+  Pool* redirect_ = nullptr;
 };
 
 }  // namespace cv
@@ -159,6 +165,7 @@ struct cv_ctx {
   cudaStream_t side2 = nullptr;  // third stream: the output layer's weight gradient beside the pair
   cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
   std::vector<void*> deferred2;  // side2 scratch, returned after side_join
+  bool side_live = false, side2_live = false;  // forked and not yet joined
 };
 
 struct cv_snap {

@@ -17,6 +17,7 @@ namespace cv {
 // Pool
 // ---------------------------------------------------------------------------
 void* Pool::get(size_t bytes) {
+  if (redirect_) return redirect_->get(bytes);
   bytes = (bytes + 255) / 256 * 256;
   if (bytes == 0) bytes = 256;
   auto it = free_.find(bytes);
@@ -42,6 +43,10 @@ void* Pool::get(size_t bytes) {
 
 void Pool::put(void* p) {
   if (!p) return;
+  if (redirect_ && redirect_->owns(p)) {
+    redirect_->put(p);
+    return;
+  }
   auto it = live_.find(p);
   if (it == live_.end()) return;
   free_.emplace(it->second, p);
@@ -191,6 +196,7 @@ cudaStream_t side_fork(cv_ctx* ctx) {
   ensure_side(ctx);
   cudaEventRecord(ctx->ev_fork, ctx->stream);
   cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
+  ctx->side_live = true;
   return ctx->side;
 }
 
@@ -203,19 +209,25 @@ cudaStream_t side2_fork(cv_ctx* ctx) {
   }
   cudaEventRecord(ctx->ev_fork2, ctx->stream);
   cudaStreamWaitEvent(ctx->side2, ctx->ev_fork2, 0);
+  ctx->side2_live = true;
   return ctx->side2;
 }
 
+// Joins only the side streams forked since the last join: a join of an idle side stream
+// would make a captured graph depend on work outside the capture.
 void side_join(cv_ctx* ctx) {
-  if (ctx->side2) {
+  if (ctx->side2 && ctx->side2_live) {
     cudaEventRecord(ctx->ev_join2, ctx->side2);
     cudaStreamWaitEvent(ctx->stream, ctx->ev_join2, 0);
-    for (void* p : ctx->deferred2) ctx->pool.put(p);
-    ctx->deferred2.clear();
+    ctx->side2_live = false;
   }
-  if (!ctx->side) return;
-  cudaEventRecord(ctx->ev_join, ctx->side);
-  cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0);
+  for (void* p : ctx->deferred2) ctx->pool.put(p);
+  ctx->deferred2.clear();
+  if (ctx->side && ctx->side_live) {
+    cudaEventRecord(ctx->ev_join, ctx->side);
+    cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0);
+    ctx->side_live = false;
+  }
   for (void* p : ctx->deferred) ctx->pool.put(p);
   ctx->deferred.clear();
 }
@@ -266,6 +278,7 @@ cudaStream_t gemm_pair(cv_ctx* ctx, GemmArgs a, GemmArgs b) {
   cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0);
   for (void* p : ctx->deferred) ctx->pool.put(p);  // later users are ordered after the join
   ctx->deferred.clear();
+  ctx->side_live = false;
   return ctx->side;
 }
 

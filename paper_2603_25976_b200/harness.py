@@ -127,8 +127,12 @@ class EpochBatcher:
         return idx
 
     def next(self) -> Batch:
-        idx = torch.from_numpy(np.ascontiguousarray(self.next_indices(), dtype=np.int64)).to(self.dd.X.device)
-        return Batch(self.dd.X.index_select(0, idx), self.dd.y.index_select(0, idx), self.dd.loss_kind)
+        hidx = np.ascontiguousarray(self.next_indices(), dtype=np.int64)
+        idx = torch.from_numpy(hidx).to(self.dd.X.device)
+        b = Batch(self.dd.X.index_select(0, idx), self.dd.y.index_select(0, idx), self.dd.loss_kind)
+        if self.dd.loss_kind == "ce":  # label-range contract from the host labels: no device read
+            b._dev["_ymax"] = int(self.dd.ds.y[hidx].max())
+        return b
 
 
 # -- run configuration and timing (run.py:31-110) -------------------------------------
