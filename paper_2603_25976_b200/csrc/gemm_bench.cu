@@ -6,6 +6,7 @@
 #include "internal.h"
 
 namespace cv {
+extern int g_force_kind, g_force_splits;
 
 __global__ void k_fill_split(__half* hi, __half* lo, int64_t n, uint32_t seed) {
   CV_PDL_ENTRY();
@@ -62,6 +63,10 @@ extern "C" __attribute__((visibility("default"))) int cv_gemm_bench(cv_ctx* ctx,
     g.seg[0].A = A;
     g.seg[0].B = B;
     g.seg[0].K = K;
+    // mode: bits 0-7 epilogue (0 store, 1 split+mask); bits 8-15 forced tile kind + 1
+    // (0: the planner's choice); bits 16-23 forced split-K factor (0: the kind's default)
+    const int fkind = ((mode >> 8) & 0xff) - 1, fsplit = (mode >> 16) & 0xff;
+    mode &= 0xff;
     if (mode == 1) {
       g.epi.mode = EPI_SPLIT_MASK;
       g.epi.act = CV_ACT_RELU;
@@ -83,6 +88,11 @@ extern "C" __attribute__((visibility("default"))) int cv_gemm_bench(cv_ctx* ctx,
       g.epi.ld = ldo;
     }
     if (!gemm_tc_supported(g)) throw std::runtime_error("unsupported shape");
+    g_force_kind = fkind;
+    g_force_splits = fsplit;
+    struct Reset {
+      ~Reset() { g_force_kind = -1; g_force_splits = 0; }
+    } reset;
     gemm_tc(ctx, g);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);

@@ -1283,9 +1283,16 @@ bool gemm_tc_tma_split(const cv_ctx* ctx, const GemmArgs& g) {
   return p.kind != 0 && p.splits == 1;
 }
 
+// cv_gemm_bench's plan override (tuning the planner's cost model; never set on a product path)
+int g_force_kind = -1, g_force_splits = 0;
+
 void gemm_tc(cv_ctx* ctx, const GemmArgs& g) {
   const int sms = g.max_ctas > 0 && g.max_ctas < ctx->sm_count ? g.max_ctas : ctx->sm_count;
-  const TcPlan p = tc_plan(g, sms);
+  TcPlan p = tc_plan(g, sms);
+  if (g_force_kind >= 0) {
+    p = tc_plan_kind(g, sms, g_force_kind);
+    if (g_force_splits > 0) p.splits = g_force_splits;
+  }
   switch (p.kind) {
     case 0: launch_tc<32, 4>(ctx, g, p.splits); break;
     case 1: launch_tc2<3, 256>(ctx, g, p.splits); break;
