@@ -1,0 +1,4 @@
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -5 > gpurun_out/r2_gputest.log
+timeout 600 python bench.py --steps 50 --warmup 10 --no-cpu > gpurun_out/r2_bench_c3.log 2>&1
+timeout 900 python bench.py --config c5 --steps 3 --warmup 3 --no-cpu > gpurun_out/r2_bench_c5.log 2>&1
+timeout 300 python scratch/small_gv.py > gpurun_out/r2_small_gv.log 2>&1
