@@ -241,7 +241,17 @@ static void ensure_gram(cv_ctx* ctx, cv_snap* s) {
       wt.si = 1;
       wt.sj = nout;
       wt.sc = s->w_sc + l;
-      q.seg[0] = GemmSeg{sop(D[cur], false), wt, nout};
+      int kq = nout;
+      if (l == L - 1 && s->tc_out && nout < 16 && ldD >= 16) {
+        // the output layer (K = c < 16): its transposed, zero-padded copy [W; b]^T (cp rows)
+        // with D's zero columns c..15 gives the tensor engine a K = 16 slab
+        wt.hi = s->wl_hi;
+        wt.lo = s->wl_lo;
+        wt.si = s->ldw;
+        wt.sj = 1;
+        kq = 16;
+      }
+      q.seg[0] = GemmSeg{sop(D[cur], false), wt, kq};
       q.epi.mode = EPI_SPLIT_MASK;
       q.epi.act = s->act;
       q.epi.out_hi = D[cur ^ 1].hi;
@@ -613,8 +623,8 @@ constexpr int PS_SMEM = 4 * CH_NB * PS_LD * 4 + (int)sizeof(Potrf64Smem);
 // Columns of the inverse are independent: each CTA owns TT_C columns (all inside one
 // 64-block j) and walks the block rows i > j with its column strip in shared memory.
 // W is row-major nbo x nbo, zero above the diagonal.
-constexpr int TT_C = 8;
-constexpr int TT_MAX = 512;
+constexpr int TT_C = 4;
+constexpr int TT_MAX = 1024;
 // the (ib, kb) tiles a column strip walks, in order: L[ib][jb..ib-1], then Dinv_ib
 struct TtTile {
   const float* p;
