@@ -638,7 +638,7 @@ CV_DEV void tile_epilogue(const TcArgs& a, const TcMaps& maps, const EpiRt& rt, 
     float v[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * inv;
-    const bool full_chunk = nb + 32 <= a.N && (!a.lower_only || nb + 31 <= m);
+    const bool full_chunk = nb + 32 <= a.N && (!a.lower_only || nb + 31 <= m + a.lower_only - 1);
     if (a.partial) {
       float* dst = a.partial + ((int64_t)split * a.M + m) * a.N + nb;
       if (full_chunk && al16(dst)) {
@@ -653,7 +653,7 @@ CV_DEV void tile_epilogue(const TcArgs& a, const TcMaps& maps, const EpiRt& rt, 
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const int n = nb + j;
-        if (n < a.N && (!a.lower_only || n <= m)) epi_apply(a.epi, rt, m, n, v[j], amax, ramax);
+        if (n < a.N && (!a.lower_only || n <= m + a.lower_only - 1)) epi_apply(a.epi, rt, m, n, v[j], amax, ramax);
       }
     }
   }
@@ -697,7 +697,7 @@ CV_DEV bool tc_work(const TcArgs& a, int w, int bm, int bn, int& m0, int& n0, in
   }
   kb0 = split * a.kb_per_split;
   nkb = min(a.kb_total, kb0 + a.kb_per_split) - kb0;
-  return !(a.lower_only && n0 > m0 + bm - 1);
+  return !(a.lower_only && n0 > m0 + bm - 1 + a.lower_only - 1);
 }
 
 // TMA of one operand slab: K-major = one box {64 K, rows}; MN-major = rows/64 boxes
@@ -877,7 +877,7 @@ __global__ void k_splitk_reduce(const float* partial, int splits, int M, int N, 
       float s = 0.f;
       for (int z = 0; z < splits; ++z) s += partial[(int64_t)z * total + i];
       const int m = (int)(i / N), n = (int)(i % N);
-      if (!lower_only || n <= m) epi_apply(epi, rt, m, n, s, amax, ramax);
+      if (!lower_only || n <= m + lower_only - 1) epi_apply(epi, rt, m, n, s, amax, ramax);
     }
   }
   epi_flush_amax(epi, amax, ramax);

@@ -103,7 +103,7 @@ struct GemmArgs {
   GemmSeg seg[2];
   Epilogue epi;
   const int* skip = nullptr;     // device flag: kernel returns immediately when != 0
-  int lower_only = 0;            // only tiles intersecting the lower triangle (m >= n)
+  int lower_only = 0;            // > 0: only the lower part n <= m + (lower_only - 1) (diagonal offset)
   cudaStream_t stream = nullptr; // nullptr: the context stream
   int max_ctas = 0;              // > 0: cap on the persistent grid (SM share when co-scheduled)
   int unsplit = 0;               // plan without split-K (the fused output head needs whole tiles)

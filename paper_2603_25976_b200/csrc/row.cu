@@ -169,14 +169,6 @@ static Operand sop(const SplitBuf& b, bool trans) {
   return o;
 }
 
-static Operand f32op(const float* p, int64_t si, int64_t sj) {
-  Operand o;
-  o.f32 = p;
-  o.si = si;
-  o.sj = sj;
-  return o;
-}
-
 __global__ void __launch_bounds__(256) k_sym_mirror(float* G, int64_t m);
 
 static void ensure_gram(cv_ctx* ctx, cv_snap* s) {
@@ -916,27 +908,34 @@ int dense_cholesky_solve(cv_ctx* ctx, const float* gram, int64_t m, double mu, c
     attr = true;
   }
   float* Lblk = (float*)ctx->pool.get(sizeof(float) * (size_t)NBO * NBO);
-  for (int64_t p0 = 0; p0 < m; p0 += NBO) {
+  // (1)+(2) the diagonal block of the panel at p0 (first tile, then one launch per tile
+  // column) and W = L11^-1 (kept: the triangular solves multiply by it), on stream `ds`
+  auto diag = [&](int64_t p0, cudaStream_t ds) {
     const int nbo = (int)((m - p0) < NBO ? (m - p0) : NBO);
     const int nsub = (nbo + CH_NB - 1) / CH_NB;
     float* Ad = chol + p0 * m + p0;
     float* dp = dinv + (p0 / CH_NB) * (int64_t)CH_NB * CH_NB;
-    // (1) the diagonal block: first tile, then one launch per tile column
-    launch_k(st, k_potrf_diag, 1, 256, 0, (const float*)Ad, m, nbo < CH_NB ? nbo : CH_NB, Lblk, (int64_t)nbo, dp,
+    launch_k(ds, k_potrf_diag, 1, 256, 0, (const float*)Ad, m, nbo < CH_NB ? nbo : CH_NB, Lblk, (int64_t)nbo, dp,
              flag);
-    ctx->launches++;
     for (int j = 0; j + 1 < nsub; ++j) {
       const int tiles = (nsub - j - 1) * (nsub - j) / 2;
-      launch_k(st, k_panel_step, tiles, 256, PS_SMEM, Ad, m, nbo, j, Lblk, dp, flag);
-      ctx->launches++;
+      launch_k(ds, k_panel_step, tiles, 256, PS_SMEM, Ad, m, nbo, j, Lblk, dp, flag);
     }
-    // (2) W = L11^-1 (kept: the triangular solves below multiply by it)
-    float* W = winv + (p0 / NBO) * (int64_t)NBO * NBO;
-    launch_k(st, k_trtri_panel, (nbo + TT_C - 1) / TT_C, 256, 0, (const float*)Lblk, (int64_t)nbo,
-             (const float*)dp, 0, nbo, W);
-    ctx->launches++;
+    launch_k(ds, k_trtri_panel, (nbo + TT_C - 1) / TT_C, 256, 0, (const float*)Lblk, (int64_t)nbo, (const float*)dp,
+             0, nbo, winv + (p0 / NBO) * (int64_t)NBO * NBO);
+    ctx->launches += nsub + 1;
+  };
+  // Look-ahead: once L21 of panel p is known, the diagonal block of panel p+1 is updated
+  // first (a small GEMM), then factored on a side stream while the rest of panel p's
+  // trailing update runs on the other SMs -- the latency-bound diagonal work hides under
+  // the tensor-core update instead of following it.
+  constexpr int kReserveSMs = 16;
+  diag(0, st);
+  for (int64_t p0 = 0; p0 < m; p0 += NBO) {
+    const int nbo = (int)((m - p0) < NBO ? (m - p0) : NBO);
     const int rest2 = (int)(m - p0 - nbo);
-    if (rest2 <= 0) continue;
+    if (rest2 <= 0) break;
+    float* W = winv + (p0 / NBO) * (int64_t)NBO * NBO;
     // (3) L21 = A21 W^T on the tensor cores (A21 split first; the GEMM writes fp32 L21 in place)
     float* A21 = chol + (p0 + nbo) * m + p0;
     split_mat(ctx, A21, m, rest2, nbo, l21h, l21l, nbo, 0, l21sc, 0, nullptr);
@@ -955,22 +954,43 @@ int dense_cholesky_solve(cv_ctx* ctx, const float* gram, int64_t m, double mu, c
       t.epi.ld = m;
       gemm(ctx, t);
     }
-    // (4) trailing update of the whole remaining matrix on the tensor cores
+    // (4) trailing update A22 -= L21 L21^T (lower) on the tensor cores, in two parts
     split_mat(ctx, A21, m, rest2, nbo, l21h, l21l, nbo, 0, l21sc, 0, nullptr);
-    Operand A, B;
-    A.hi = l21h; A.lo = l21l; A.sc = l21sc; A.si = nbo; A.sj = 1;  // A(i, k) = L21[i, k]
-    B.hi = l21h; B.lo = l21l; B.sc = l21sc; B.si = 1; B.sj = nbo;  // B(k, j) = L21[j, k]
-    GemmArgs u;
-    u.M = rest2;
-    u.N = rest2;
-    u.nseg = 1;
-    u.seg[0] = GemmSeg{A, B, nbo};
-    u.epi.mode = EPI_ACCUM;
-    u.epi.alpha = -1.f;
-    u.epi.out = chol + (p0 + nbo) * m + (p0 + nbo);
-    u.epi.ld = m;
-    u.lower_only = 1;
-    gemm(ctx, u);
+    const int64_t nx = p0 + nbo;  // the next panel
+    const int nb1 = rest2 < NBO ? rest2 : NBO;
+    auto update = [&](int64_t r0, int rows, int cols, int offset, int max_ctas) {
+      Operand A, B;
+      A.hi = l21h + (r0 - nx) * nbo; A.lo = l21l + (r0 - nx) * nbo; A.sc = l21sc; A.si = nbo; A.sj = 1;
+      B.hi = l21h; B.lo = l21l; B.sc = l21sc; B.si = 1; B.sj = nbo;  // B(k, j) = L21[j, k]
+      GemmArgs u;
+      u.M = rows;
+      u.N = cols;
+      u.nseg = 1;
+      u.seg[0] = GemmSeg{A, B, nbo};
+      u.epi.mode = EPI_ACCUM;
+      u.epi.alpha = -1.f;
+      u.epi.out = chol + r0 * m + nx;
+      u.epi.ld = m;
+      u.lower_only = offset + 1;  // lower part relative to the diagonal `offset` columns right
+      u.max_ctas = max_ctas;
+      gemm(ctx, u);
+    };
+    // (4a) the next panel's diagonal block
+    update(nx, nb1, nb1, 0, 0);
+    // look ahead only while the rest of the update outlasts the diagonal work (~1 ms on the
+    // reserved SMs); the last panels' small updates run on every SM
+    const double rows = (double)(rest2 - nb1), upd_ms = rows * ((double)rest2 - 0.5 * rows) * 2.0 * nbo / 4.5e11;
+    if (rest2 > nb1 && upd_ms > 1.0 && ctx->sm_count > 4 * kReserveSMs) {
+      // (4b) its factorization beside (4c) the rest of the update: rows below it, columns
+      // from it on (the lower part relative to the shifted diagonal)
+      cudaStream_t side = side_fork(ctx);
+      diag(nx, side);
+      update(nx + nb1, rest2 - nb1, rest2, nb1, ctx->sm_count - kReserveSMs);
+      side_join(ctx);
+    } else {
+      if (rest2 > nb1) update(nx + nb1, rest2 - nb1, rest2, nb1, 0);
+      diag(nx, st);
+    }
   }
   ctx->pool.put(Lblk);
   if (tc) {
