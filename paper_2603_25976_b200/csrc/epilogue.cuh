@@ -117,6 +117,10 @@ union H8 {
   uint4 u;
   __half h[8];
 };
+union H4 {
+  uint2 u;
+  __half h[4];
+};
 
 CV_DEV void split16x8(const float* x, float s, __half* hi, __half* lo) {
   H8 a, b;

@@ -883,6 +883,117 @@ __global__ void k_splitk_reduce(const float* partial, int splits, int M, int N, 
   epi_flush_amax(epi, amax, ramax);
 }
 
+// Split-K form of the fused output-layer JVP (the ReLU tangent GEMM of the last hidden
+// layer at batches too small for whole tiles to fill the machine): after the fixed-order
+// sum of the partials, one warp per (row, 128-column group) applies the mask, stores the
+// split tangent (unless head_only) and accumulates the group's share of the output
+// tangent, sum_n a(m, n) V[n, :] + t(m, n) W[n, :] (warp butterfly), into head_part.
+constexpr int kHeadGroupCols = 128;
+__global__ void __launch_bounds__(256) k_splitk_reduce_head(const float* partial, int splits, int M, int N,
+                                                            Epilogue epi, const int* skip) {
+  CV_PDL_ENTRY();
+  if (skip_if(skip)) return;
+  const EpiRt rt = epi_prepare(epi);
+  if (blockIdx.x == 0 && threadIdx.x == 0) epi_publish(epi, rt);
+  const int lane = threadIdx.x & 31;
+  const int groups = (N + kHeadGroupCols - 1) / kHeadGroupCols;
+  const int64_t total = (int64_t)M * N;
+  const int hc = epi.head_c;
+  const bool store = !epi.head_only;
+  __shared__ float hred[8][16 * 33];
+  float amax = 0.f;
+  for (int64_t wk = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); wk < (int64_t)M * groups;
+       wk += (int64_t)gridDim.x * 8) {
+    const int m = (int)(wk / groups), g = (int)(wk % groups);
+    const int n = g * kHeadGroupCols + 4 * lane;
+    float v[4] = {0.f, 0.f, 0.f, 0.f}, av[4] = {0.f, 0.f, 0.f, 0.f}, t[4] = {0.f, 0.f, 0.f, 0.f};
+    const bool full = n + 3 < N;
+    if (n < N) {
+      const int64_t o = (int64_t)m * N + n;
+      for (int z = 0; z < splits; ++z) {
+        if (full) {
+          const float4 q = *reinterpret_cast<const float4*>(partial + (int64_t)z * total + o);
+          v[0] += q.x; v[1] += q.y; v[2] += q.z; v[3] += q.w;
+        } else {
+          for (int j = 0; j < 4 && n + j < N; ++j) v[j] += partial[(int64_t)z * total + o + j];
+        }
+      }
+      if (full) {  // 8-byte mask loads and split stores (mask_ld, ld multiples of 8; n of 4)
+        H4 mh, ml, oh, ol;
+        mh.u = *reinterpret_cast<const uint2*>(epi.mask_hi + (int64_t)m * epi.mask_ld + n);
+        ml.u = *reinterpret_cast<const uint2*>(epi.mask_lo + (int64_t)m * epi.mask_ld + n);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float hi = __half2float(mh.h[j]);
+          av[j] = (hi + __half2float(ml.h[j])) * rt.mask_inv;
+          t[j] = hi > 0.f ? v[j] : 0.f;
+          split16(t[j], rt.out_s, oh.h[j], ol.h[j]);
+          amax = fmaxf(amax, fabsf(t[j]));
+        }
+        if (store) {
+          *reinterpret_cast<uint2*>(epi.out_hi + (int64_t)m * epi.ld + n) = oh.u;
+          *reinterpret_cast<uint2*>(epi.out_lo + (int64_t)m * epi.ld + n) = ol.u;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (n + j >= N) break;
+          const int64_t mi = (int64_t)m * epi.mask_ld + n + j;
+          const float hi = __half2float(epi.mask_hi[mi]);
+          av[j] = (hi + __half2float(epi.mask_lo[mi])) * rt.mask_inv;
+          t[j] = hi > 0.f ? v[j] : 0.f;
+          if (store) {
+            split16(t[j], rt.out_s, epi.out_hi[(int64_t)m * epi.ld + n + j], epi.out_lo[(int64_t)m * epi.ld + n + j]);
+            amax = fmaxf(amax, fabsf(t[j]));
+          }
+        }
+      }
+    }
+    float h[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) h[k] = 0.f;
+    if (hc == 10 && full && !(((uintptr_t)epi.head_v | (uintptr_t)epi.head_w) & 15)) {
+      // 4 columns x 10 outputs = 10 float4 per matrix, contiguous
+      const float4* vq = reinterpret_cast<const float4*>(epi.head_v + (int64_t)n * 10);
+      const float4* wq = reinterpret_cast<const float4*>(epi.head_w + (int64_t)n * 10);
+#pragma unroll
+      for (int u = 0; u < 10; ++u) {
+        const float4 vv = __ldg(vq + u), ww = __ldg(wq + u);
+        const float ve[4] = {vv.x, vv.y, vv.z, vv.w}, we[4] = {ww.x, ww.y, ww.z, ww.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int f = 4 * u + q, j = f / 10, k = f % 10;  // flat index over (column j, output k)
+          h[k] = fmaf(av[j], ve[q], fmaf(t[j], we[q], h[k]));
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (n + j >= N) break;
+        const float* vr = epi.head_v + (int64_t)(n + j) * hc;
+        const float* wr = epi.head_w + (int64_t)(n + j) * hc;
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if (k < hc) h[k] = fmaf(av[j], __ldg(vr + k), fmaf(t[j], __ldg(wr + k), h[k]));
+      }
+    }
+    // the warp's 32 lane partials per output: through shared memory, fixed order
+    float* red = hred[threadIdx.x >> 5];
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (k < hc) red[k * 33 + lane] = h[k];
+    __syncwarp();
+    if (lane < hc) {
+      float x = 0.f;
+      for (int l = 0; l < 32; ++l) x += red[lane * 33 + l];
+      epi.head_part[((int64_t)g * M + m) * hc + lane] = x;
+    }
+  }
+  float ramax = 0.f;
+  epi_flush_amax(epi, amax, ramax);
+}
+
 // ---------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------
@@ -1117,7 +1228,8 @@ static int launch_tc(cv_ctx* ctx, const GemmArgs& g, int splits, float* ext_part
     a.partial = part;
   }
   setup_out(g, maps, a, a.partial, splits);
-  if (g.epi.head_part && a.tma_out != 1) throw std::runtime_error("fused output head needs the TMA split epilogue");
+  if (g.epi.head_part && a.tma_out != 1 && !part)
+    throw std::runtime_error("fused output head needs the TMA split epilogue");
   const int work = a.tiles_m * a.tiles_n * splits;
   const int sms = g.max_ctas > 0 && g.max_ctas < ctx->sm_count ? g.max_ctas : ctx->sm_count;
   const int grid = work < sms ? work : sms;
@@ -1125,7 +1237,11 @@ static int launch_tc(cv_ctx* ctx, const GemmArgs& g, int splits, float* ext_part
   launch_k(st, k_gemm_tc<BN, STAGES>, grid, Cfg::THREADS, Cfg::SMEM, maps, a);
   ctx->launches++;
   if (part) {
-    launch_k(st, k_splitk_reduce, 4 * ctx->sm_count, 256, 0, part, splits, g.M, g.N, g.epi, g.skip, g.lower_only);
+    if (g.epi.head_part)
+      launch_k(st, k_splitk_reduce_head, 4 * ctx->sm_count, 256, 0, (const float*)part, splits, g.M, g.N, g.epi,
+               g.skip);
+    else
+      launch_k(st, k_splitk_reduce, 4 * ctx->sm_count, 256, 0, part, splits, g.M, g.N, g.epi, g.skip, g.lower_only);
     ctx->launches++;
     if (st == ctx->side2 && st) ctx->deferred2.push_back(part);
     else if (st != ctx->stream) ctx->deferred.push_back(part);  // reused only after the join
@@ -1262,7 +1378,8 @@ double gemm_tc_estimate(const cv_ctx* ctx, const GemmArgs& g, int ctas) {
 // Number of column groups of the fused output-layer head this GEMM would write
 // (tile_epilogue_tma), or 0 when the GEMM cannot carry the head (engine, layout,
 // epilogue mode or tile plan); the caller then runs the output layer separately.
-int gemm_tc_head_groups(const cv_ctx* ctx, const GemmArgs& g) {
+int gemm_tc_head_groups(const cv_ctx* ctx, const GemmArgs& g, int* via_reduce) {
+  if (via_reduce) *via_reduce = 0;
   if (ctx->engine == CV_ENGINE_SIMT || !gemm_tc_supported(g) || g.lower_only) return 0;
   const Epilogue& e = g.epi;
   const bool jvp_head = e.mode == EPI_SPLIT_MASK && e.act == CV_ACT_RELU && !e.raw && e.mask_div == 1 &&
@@ -1272,6 +1389,17 @@ int gemm_tc_head_groups(const cv_ctx* ctx, const GemmArgs& g) {
   const int sms = g.max_ctas > 0 && g.max_ctas < ctx->sm_count ? g.max_ctas : ctx->sm_count;
   const TcPlan p = tc_plan(g, sms);
   if (p.kind == 0 || p.splits > 1) return 0;
+  if (via_reduce && jvp_head && !g.epi.bits_out) {
+    // whole tiles that leave most of the machine idle (small batches): run split-K and
+    // form the head in the fixed-order reduction instead (k_splitk_reduce_head)
+    GemmArgs gs = g;
+    gs.unsplit = 0;
+    const TcPlan q = tc_plan(gs, sms);
+    if (q.kind != 0 && q.splits > 1 && plan_time(q, sms) < 0.6 * plan_time(p, sms)) {
+      *via_reduce = 1;
+      return (g.N + kHeadGroupCols - 1) / kHeadGroupCols;
+    }
+  }
   const int bn = p.kind == 5 ? 64 : (p.kind == 3 ? 128 : 256);
   return 2 * ((g.N + bn - 1) / bn);
 }

@@ -231,7 +231,8 @@ static void launch_tc2(cv_ctx* ctx, const GemmArgs& g, int splits) {
     a.partial = part;
   }
   setup_out(g, maps, a, a.partial, splits);
-  if (g.epi.head_part && a.tma_out != 1) throw std::runtime_error("fused output head needs the TMA split epilogue");
+  if (g.epi.head_part && a.tma_out != 1 && !part)
+    throw std::runtime_error("fused output head needs the TMA split epilogue");
   const int work = a.tiles_m * a.tiles_n * splits;
   const int sms = g.max_ctas > 0 && g.max_ctas < ctx->sm_count ? g.max_ctas : ctx->sm_count;
   const int pairs = sms / 2;
@@ -240,7 +241,11 @@ static void launch_tc2(cv_ctx* ctx, const GemmArgs& g, int splits) {
   launch_k(st, k_gemm_tc2<STAGES, TC2_BN>, grid, 320, Cfg::SMEM, maps, a);
   ctx->launches++;
   if (splits > 1) {
-    launch_k(st, k_splitk_reduce, 4 * ctx->sm_count, 256, 0, part, splits, g.M, g.N, g.epi, g.skip, g.lower_only);
+    if (g.epi.head_part)
+      launch_k(st, k_splitk_reduce_head, 4 * ctx->sm_count, 256, 0, (const float*)part, splits, g.M, g.N, g.epi,
+               g.skip);
+    else
+      launch_k(st, k_splitk_reduce, 4 * ctx->sm_count, 256, 0, part, splits, g.M, g.N, g.epi, g.skip, g.lower_only);
     ctx->launches++;
     if (st == ctx->side2 && st) ctx->deferred2.push_back(part);
     else if (st != ctx->stream) ctx->deferred.push_back(part);  // reused only after the join

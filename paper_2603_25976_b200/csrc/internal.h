@@ -276,7 +276,9 @@ struct StreamSwap {
   StreamSwap& operator=(const StreamSwap&) = delete;
 };
 int gemm_tc_partial(cv_ctx* ctx, const GemmArgs& g, float** partial);  // N <= 32, raw split-K partials
-int gemm_tc_head_groups(const cv_ctx* ctx, const GemmArgs& g);          // 0: no fused output-layer head
+// 0: no fused output-layer head; *via_reduce = 1: plan split-K (unsplit = 0) and the head
+// is formed in the split-K reduction
+int gemm_tc_head_groups(const cv_ctx* ctx, const GemmArgs& g, int* via_reduce = nullptr);
 bool gemm_tc_tma_split(const cv_ctx* ctx, const GemmArgs& g);           // runs the TMA split epilogue (bits producer)
 
 // runtime.cu

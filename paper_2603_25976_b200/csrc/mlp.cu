@@ -566,8 +566,10 @@ static int jvp_hidden(cv_ctx* ctx, cv_snap* s, bool keep_dz, const int* skip, co
       g.epi.head_c = s->c;
       g.epi.head_part = s->head_part;
       g.epi.head_only = head_only;
-      g.unsplit = 1;  // the head needs whole tiles: plan without split-K (small per-rank batches)
-      groups = gemm_tc_head_groups(ctx, g);
+      g.unsplit = 1;  // the head needs whole tiles (or a split-K head reduction, below)
+      int via_reduce = 0;
+      groups = gemm_tc_head_groups(ctx, g, &via_reduce);
+      if (via_reduce) g.unsplit = 0;
       if (groups <= 0 || groups > s->head_groups_max) {
         groups = 0;
         g.epi.head_part = nullptr;

@@ -15,10 +15,6 @@
 
 namespace cv {
 
-union H4 {
-  uint2 u;
-  __half h[4];
-};
 
 // 4 consecutive split elements (8-byte aligned) -> fp32
 CV_DEV void ld_join4(const __half* hi, const __half* lo, float inv, float (&x)[4]) {
