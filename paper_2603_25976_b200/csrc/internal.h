@@ -189,7 +189,7 @@ struct cv_snap {
   cv::Scale* U2_sc = nullptr;     // U2 amax
   cv::Scale* prod_sc = nullptr;   // start of the per-product block
   int n_prod = 0;
-  int v_ready = 0;                // the next product input's scales were published by its producer
+  int v_ready = 0;                // next product input: 1 scales published by its producer, 2 split written
   cv::Scale* scratch_sc = nullptr;  // [8] row lane / tests
   // weights of the linearization point, split, flat layout
   __half* w_hi = nullptr;

@@ -521,6 +521,10 @@ void mlp_linearize(cv_ctx* ctx, cv_snap* s, double* loss_out, float* grad_out) {
 // split of a product input v into v_hi / v_lo (per-layer exponents); also
 // zeroes this product's amax slots
 static void split_input(cv_ctx* ctx, cv_snap* s, const float* v, const int* skip) {
+  if (s->v_ready == 2) {  // the split itself was written by its producer (Rademacher probes)
+    s->v_ready = 0;
+    return;
+  }
   if (s->v_ready) {  // scales already published (and slots zeroed) by the fused CG update
     split_flat_apply(ctx, v, s->d, s->off, s->v_hi, s->v_lo, s->v_sc, skip);
     s->v_ready = 0;

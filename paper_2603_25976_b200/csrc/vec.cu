@@ -5,6 +5,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "vecutil.cuh"
+#include "epilogue.cuh"
 
 #include <float.h>
 #include <stdlib.h>
@@ -165,8 +166,58 @@ void diag_ema(cv_ctx* ctx, float* diag, const float* est, double beta, int64_t d
 // Hutchinson (telemetry.py:91-110): z regenerated from (seed, counter) in the
 // accumulation pass instead of being re-read.
 // ---------------------------------------------------------------------------
-__global__ void k_hutch_acc(uint64_t seed, uint64_t counter, const float* hz, int64_t d, float* diag, int first,
-                            int last, float inv_n, double* ws) {
+// A Rademacher probe (numeric.py:157-162) written straight as the product input's split:
+// z_i = +-1 is exact in the fp16 pair (hi = z 2^e, lo = 0, e = exp_for_bound(1), every
+// layer block's amax = 1: what the amax + split passes of an fp32 z would produce,
+// bit for bit); the signs are kept as packed bits for the accumulation pass, and fp32
+// values only for the output-layer block (the fused head and the bias row read those).
+// One thread per 32-element word.
+__global__ void k_rad_split(uint64_t seed, uint64_t counter, int64_t d, int64_t last_off, __half* hi, __half* lo,
+                            uint32_t* bits, float* zf, Scale* v_sc, int L, Scale* zero_sc, int n_zero) {
+  CV_PDL_ENTRY();
+  const int e = exp_for_bound(1.f);
+  if (blockIdx.x == 0) {
+    if (threadIdx.x < L) { v_sc[threadIdx.x].e = e; v_sc[threadIdx.x].amax = 1.f; }
+    if (threadIdx.x < n_zero) { zero_sc[threadIdx.x].e = 0; zero_sc[threadIdx.x].amax = 0.f; }
+  }
+  const __half hp = __float2half_rn(pow2f(e)), hn = __float2half_rn(-pow2f(e)), hz = __float2half_rn(0.f);
+  const int64_t words = (d + 31) / 32;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i0 = 32 * w;
+    uint32_t wd = 0;
+    if (i0 + 32 <= d && !(i0 & 7)) {
+      H8 h[4], z8;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) z8.h[j] = hz;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const bool pos = (splitmix(seed, counter + 1 + (uint64_t)(i0 + j)) >> 63) != 0;
+        wd |= (pos ? 1u : 0u) << j;
+        h[j >> 3].h[j & 7] = pos ? hp : hn;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        *reinterpret_cast<uint4*>(hi + i0 + 8 * q) = h[q].u;
+        *reinterpret_cast<uint4*>(lo + i0 + 8 * q) = z8.u;
+      }
+    } else {
+      for (int j = 0; j < 32 && i0 + j < d; ++j) {
+        const bool pos = (splitmix(seed, counter + 1 + (uint64_t)(i0 + j)) >> 63) != 0;
+        wd |= (pos ? 1u : 0u) << j;
+        hi[i0 + j] = pos ? hp : hn;
+        lo[i0 + j] = hz;
+      }
+    }
+    bits[w] = wd;
+    if (i0 + 32 > last_off)
+      for (int j = 0; j < 32 && i0 + j < d; ++j)
+        if (i0 + j >= last_off) zf[i0 + j] = ((wd >> j) & 1u) ? 1.f : -1.f;
+  }
+}
+
+// diag (+)= z * Hz / n with z from the probe's packed signs; partial sums of z.Hz
+__global__ void k_hutch_acc_bits(const uint32_t* bits, const float* hz, int64_t d, float* diag, int first, int last,
+                                 float inv_n, double* ws) {
   CV_PDL_ENTRY();
   double t[1] = {0.0};
   vec_for(d, al16p(hz, diag), [&](auto W_, int64_t i) {
@@ -174,9 +225,11 @@ __global__ void k_hutch_acc(uint64_t seed, uint64_t counter, const float* hz, in
     const Vf<W> hv = ldv<W>(hz + i);
     Vf<W> dv;
     if (diag && !first) dv = ldv<W>(diag + i);
+    // (W = 4 groups start at multiples of 4: their signs sit in one word)
+    const uint32_t wd = __ldg(bits + (i >> 5)) >> (i & 31);
 #pragma unroll
     for (int j = 0; j < W; ++j) {
-      const float zh = rad(seed, counter, i + j) * hv.v[j];
+      const float zh = ((wd >> j) & 1u) ? hv.v[j] : -hv.v[j];
       t[0] += (double)zh;
       float a = first ? zh : dv.v[j] + zh;
       if (last) a *= inv_n;
@@ -186,6 +239,7 @@ __global__ void k_hutch_acc(uint64_t seed, uint64_t counter, const float* hz, in
   });
   write_partials<1>(ws, t);
 }
+
 __global__ void k_trace_final(const double* ws, double inv_n, double* out, int first) {
   CV_PDL_ENTRY();
   double t[1];
@@ -205,19 +259,27 @@ void hutchinson(cv_ctx* ctx, cv_snap* s, int kind, uint64_t seed, uint64_t count
                 double* trace) {
   float* hz = snap_tmp(s, &s->tmp_d);
   float* z = snap_tmp(s, &s->tmp_d2);
+  uint32_t* zbits = (uint32_t*)ctx->pool.get(sizeof(uint32_t) * (size_t)((s->d + 31) / 32));
   MatvecFn mv = matvec_fn(kind);
+  const int64_t words = (s->d + 31) / 32;
+  const int rgrid = (int)(words / NT + 1 < 8 * (int64_t)ctx->sm_count ? words / NT + 1 : 8 * (int64_t)ctx->sm_count);
   for (int j = 0; j < n_probes; ++j) {
     const uint64_t ctr = counter + (uint64_t)j * (uint64_t)s->d;
-    rademacher(ctx, seed, ctr, s->d, z);
+    // the probe goes straight into the product input's split (no fp32 probe pass)
+    launch_k(ctx->stream, k_rad_split, rgrid, NT, 0, seed, ctr, s->d, s->off[s->L - 1], s->v_hi, s->v_lo, zbits, z,
+             s->v_sc, s->L, s->prod_sc, s->n_prod);
+    ctx->launches++;
+    s->v_ready = 2;
     mv(ctx, s, z, hz, nullptr);
-    launch_k(ctx->stream, k_hutch_acc, NB, NT, 0, seed, ctr, hz, s->d, diag, j == 0, j == n_probes - 1,
-                                            1.f / (float)n_probes, ctx->red_ws);
+    launch_k(ctx->stream, k_hutch_acc_bits, NB, NT, 0, (const uint32_t*)zbits, (const float*)hz, s->d, diag, j == 0,
+             j == n_probes - 1, 1.f / (float)n_probes, ctx->red_ws);
     ctx->launches++;
     if (trace) {
       launch_k(ctx->stream, k_trace_final, 1, NT, 0, ctx->red_ws, 1.0 / (double)n_probes, trace, j == 0);
       ctx->launches++;
     }
   }
+  ctx->pool.put(zbits);  // stream-ordered reuse
 }
 
 // ---------------------------------------------------------------------------

@@ -1,0 +1,3 @@
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_gates.py tests/test_gpu_graphs.py -x -q 2>&1 | tail -3 > gpurun_out/r2_gputest.log
+timeout 1200 ncu --profile-from-start off -k "regex:k_(flat|cg|norm|apply|rad|hutch|diag|chain|trace)" --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/r2_c5_vec.csv python scratch/c5_step.py > gpurun_out/r2_c5_step.log 2>&1
+python scratch/vec_sum.py gpurun_out/r2_c5_vec.csv > gpurun_out/r2_c5_vec_table.txt 2>&1
