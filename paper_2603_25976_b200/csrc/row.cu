@@ -624,7 +624,7 @@ struct TtTile {
   int rows, cols;
 };
 __global__ void __launch_bounds__(256) k_trtri_panel(const float* A, int64_t lda, const float* dinv, int p0, int nbo,
-                                                     float* W) {
+                                                     float* W, float* Wt) {
   CV_PDL_ENTRY();
   __shared__ float X[TT_MAX][TT_C];
   __shared__ __align__(16) float Lt[CH_NB][CH_NB + 4];
@@ -733,6 +733,11 @@ __global__ void __launch_bounds__(256) k_trtri_panel(const float* A, int64_t lda
     const int rr = e / TT_C, cc = e % TT_C, c = c0 + cc;
     if (c < nbo) W[(int64_t)rr * nbo + c] = rr < CH_NB * jb ? 0.f : X[rr][cc];
   }
+  // and W^T (row c = column c of W, contiguous): the backward solve reads it by rows
+  for (int e = tid; e < nbo * TT_C; e += blockDim.x) {
+    const int cc = e / nbo, rr = e % nbo, c = c0 + cc;
+    if (c < nbo) Wt[(int64_t)c * nbo + rr] = rr < CH_NB * jb ? 0.f : X[rr][cc];
+  }
 }
 
 // Triangular solves with the panel inverses W_p = L_pp^-1 (k_trtri_panel, kept per
@@ -812,23 +817,16 @@ __global__ void __launch_bounds__(256) k_tri_bwd_reduce(const double* y, const d
     t[i] = y[p0 + i] - a;
   }
 }
-// x[p0 + j] = sum_{i >= j} W[i, j] t_i: each CTA owns 32 columns j; its 8 warps stride
-// over the rows i and reduce in shared memory
-__global__ void __launch_bounds__(256) k_tri_wtgemv(const float* W, int nbo, int p0, const double* t, double* x) {
+// x[p0 + j] = sum_{i >= j} W[i, j] t_i = sum_{i >= j} Wt[j, i] t_i: one warp per row of W^T
+__global__ void __launch_bounds__(256) k_tri_wtgemv(const float* Wt, int nbo, int p0, const double* t, double* x) {
   CV_PDL_ENTRY();
-  __shared__ double red[8][32];
-  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  const int j = blockIdx.x * 32 + lane;
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (j >= nbo) return;
   double s = 0.0;
-  if (j < nbo)
-    for (int i = j + wp; i < nbo; i += 8) s += (double)W[(int64_t)i * nbo + j] * t[i];
-  red[wp][lane] = s;
-  __syncthreads();
-  if (wp == 0 && j < nbo) {
-    double a = 0.0;
-    for (int w = 0; w < 8; ++w) a += red[w][lane];
-    x[p0 + j] = a;
-  }
+  for (int i = j + lane; i < nbo; i += 32) s += (double)Wt[(int64_t)j * nbo + i] * t[i];
+  s = warp_sum(s);
+  if (lane == 0) x[p0 + j] = s;
 }
 
 // r = rhs - (G + mu I) v, one warp per row, fp64 accumulation (refinement residual)
@@ -893,6 +891,7 @@ int dense_cholesky_solve(cv_ctx* ctx, const float* gram, int64_t m, double mu, c
   ctx->launches++;
   constexpr int NBO = TT_MAX;  // panel width (a multiple of CH_NB)
   const bool tc = m > NBO;     // (the GEMMs follow the context's engine selection)
+  float* winvT = winv + ((m + NBO - 1) / NBO) * (int64_t)NBO * NBO;  // second half: the W^T of each panel
   __half *l21h = nullptr, *l21l = nullptr, *wh = nullptr, *wl = nullptr;
   if (tc) {
     l21h = (__half*)ctx->pool.get(sizeof(__half) * (size_t)(m - NBO) * NBO);
@@ -922,7 +921,7 @@ int dense_cholesky_solve(cv_ctx* ctx, const float* gram, int64_t m, double mu, c
       launch_k(ds, k_panel_step, tiles, 256, PS_SMEM, Ad, m, nbo, j, Lblk, dp, flag);
     }
     launch_k(ds, k_trtri_panel, (nbo + TT_C - 1) / TT_C, 256, 0, (const float*)Lblk, (int64_t)nbo, (const float*)dp,
-             0, nbo, winv + (p0 / NBO) * (int64_t)NBO * NBO);
+             0, nbo, winv + (p0 / NBO) * (int64_t)NBO * NBO, winvT + (p0 / NBO) * (int64_t)NBO * NBO);
     ctx->launches += nsub + 1;
   };
   // Look-ahead: once L21 of panel p is known, the diagonal block of panel p+1 is updated
@@ -1026,7 +1025,6 @@ int dense_cholesky_solve(cv_ctx* ctx, const float* gram, int64_t m, double mu, c
     for (int pi = npan - 1; pi >= 0; --pi) {
       const int p0 = pi * NBO;
       const int nbp = (int)((m - p0) < NBO ? (m - p0) : NBO);
-      const float* W = winv + (int64_t)pi * NBO * NBO;
       const int64_t rest = m - p0 - nbp;
       int nparts = 0;
       if (rest > 0) {
@@ -1038,7 +1036,8 @@ int dense_cholesky_solve(cv_ctx* ctx, const float* gram, int64_t m, double mu, c
       }
       launch_k(st, k_tri_bwd_reduce, (nbp + 31) / 32, 256, 0, (const double*)y, (const double*)part, nparts, nbp, p0,
                tvec);
-      launch_k(st, k_tri_wtgemv, (nbp + 31) / 32, 256, 0, W, nbp, p0, (const double*)tvec, x);
+      launch_k(st, k_tri_wtgemv, (nbp + 7) / 8, 256, 0, winvT + (int64_t)pi * NBO * NBO, nbp, p0,
+               (const double*)tvec, x);
       ctx->launches += 2;
     }
   };
@@ -1064,7 +1063,7 @@ int row_solve_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, flo
   const int nblk = (int)((m + CH_NB - 1) / CH_NB);
   if (!s->dinv) s->dinv = snap_alloc(s, (int64_t)nblk * CH_NB * CH_NB);
   const int64_t npan = (m + TT_MAX - 1) / TT_MAX;
-  if (!s->winv) s->winv = snap_alloc(s, npan * TT_MAX * TT_MAX);
+  if (!s->winv) s->winv = snap_alloc(s, 2 * npan * TT_MAX * TT_MAX);  // W and W^T per panel
   return dense_cholesky_solve(ctx, s->gram, m, mu, rhs, v_out, s->chol, s->dinv, s->winv, s->scratch_sc + 2);
 }
 
@@ -1074,7 +1073,7 @@ int dense_cholesky(cv_ctx* ctx, const float* gram, int64_t m, double mu, const f
   float* dinv = (float*)ctx->pool.get(sizeof(float) * (size_t)(nblk * CH_NB * CH_NB));
   Scale* sc = (Scale*)ctx->pool.get(sizeof(Scale) * 4);
   const int64_t npan = (m + TT_MAX - 1) / TT_MAX;
-  float* winv = (float*)ctx->pool.get(sizeof(float) * (size_t)(npan * TT_MAX * TT_MAX));
+  float* winv = (float*)ctx->pool.get(sizeof(float) * (size_t)(2 * npan * TT_MAX * TT_MAX));  // W and W^T
   int rc = 1;
   try {
     rc = dense_cholesky_solve(ctx, gram, m, mu, rhs, v_out, chol, dinv, winv, sc);
