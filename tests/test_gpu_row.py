@@ -132,3 +132,25 @@ def test_row_cholesky_m10240_direction_vs_oracle():
     print(f"m={b * dims[-1]}: direction vs oracle {e_dir:.2e}")
     assert e_dir < REL
     snap.close()
+
+
+def test_row_cholesky_lookahead_system_residual():
+    """m = 25,600 (b = 2560): large enough that the factorization runs the look-ahead
+    (the next panel's diagonal block factored on a side stream beside the trailing update)
+    and 1024-wide panels with a partial last panel; the solve must match an fp64 solve of
+    the same fp32 Gram (cuSOLVER as the checker)."""
+    dims, b = (256, 512, 512, 10), 2560
+    m = P.Model(dims[0], dims[1:-1], dims[-1], "relu")
+    w = P.init_params(m, P.Rng(0))
+    X, y = O.synthetic_batch(b, dims[0], dims[-1])
+    snap = P.make_snapshot("ggn_ce", m, w, P.Batch(X, y, "ce"))
+    mu = float(b)
+    v = snap.row.solve_cholesky(mu).double()
+    G = snap.row.gram().double()
+    G.diagonal().add_(mu)
+    ref = torch.linalg.solve(G, snap.row.rhs.double())
+    e = float(torch.linalg.vector_norm(v - ref) / torch.linalg.vector_norm(ref))
+    print(f"m={b * dims[-1]}: system {e:.2e}")
+    assert e < 1e-6
+    del G
+    snap.close()
