@@ -79,6 +79,7 @@ int cv_ctx_create(int device, int world, int rank, const void* nccl_id, cv_ctx**
   c->amax_ws = (float*)c->pool.get(sizeof(float) * (kAmaxWsFloats + kOffTabMax));  // split.cu SP_NB x SP_MAXL, mr
   c->amax_counter = (unsigned*)c->pool.get(sizeof(unsigned) * 64);
   cudaMemsetAsync(c->amax_counter, 0, sizeof(unsigned) * 64, c->stream);
+  if (const char* e = getenv("CURVOPT_SHARD_CG")) c->shard_cg = atoi(e) != 0;  // test hook (default: by size)
   if (world > 1) {
     if (nccl_id) nccl_init(c, nccl_id);  // else: cv_ctx_set_comm installs the communicator
   } else if (getenv("CURVOPT_FORCE_NCCL")) {

@@ -166,6 +166,8 @@ struct cv_ctx {
   cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
   std::vector<void*> deferred2;  // side2 scratch, returned after side_join
   bool side_live = false, side2_live = false;  // forked and not yet joined
+  int shard_cg = -1;             // CG vector sharding across ranks: -1 by size, 0 never, 1 always
+  int64_t shard_chunk = 0;       // while a sharded CG's product runs: owner chunk of the reduction
 };
 
 struct cv_snap {
@@ -285,6 +287,8 @@ bool gemm_tc_tma_split(const cv_ctx* ctx, const GemmArgs& g);           // runs 
 inline bool distributed(const cv_ctx* ctx) { return ctx->nccl != nullptr || ctx->comm_fn != nullptr; }
 void allreduce_f32(cv_ctx* ctx, float* buf, int64_t n);
 void allreduce_f64(cv_ctx* ctx, double* buf, int64_t n);
+void reduce_to_owners(cv_ctx* ctx, float* buf, int64_t b0, int64_t b1, int64_t chunk, cudaStream_t st);
+void allgather_f32(cv_ctx* ctx, float* buf, int64_t chunk);
 // Per-layer ("bucketed") all-reduce of a flat parameter-space vector being produced
 // layer by layer: ready(l, st) is called once layer l's block is final on stream st;
 // with NCCL its all-reduce starts at once on the comm stream, overlapping the GEMMs

@@ -4,6 +4,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <exception>
 #include <stdexcept>
 
@@ -70,6 +71,11 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
+                         cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -91,8 +97,13 @@ static NcclApi& nccl_api() {
   api.CommInitRank = (decltype(api.CommInitRank))dlsym(api.h, "ncclCommInitRank");
   api.CommDestroy = (decltype(api.CommDestroy))dlsym(api.h, "ncclCommDestroy");
   api.AllReduce = (decltype(api.AllReduce))dlsym(api.h, "ncclAllReduce");
+  api.Reduce = (decltype(api.Reduce))dlsym(api.h, "ncclReduce");
+  api.AllGather = (decltype(api.AllGather))dlsym(api.h, "ncclAllGather");
+  api.GroupStart = (decltype(api.GroupStart))dlsym(api.h, "ncclGroupStart");
+  api.GroupEnd = (decltype(api.GroupEnd))dlsym(api.h, "ncclGroupEnd");
   api.GetErrorString = (decltype(api.GetErrorString))dlsym(api.h, "ncclGetErrorString");
-  if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce)
+  if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.Reduce || !api.AllGather ||
+      !api.GroupStart || !api.GroupEnd)
     throw std::runtime_error("NCCL library lacks required symbols");
   return api;
 }
@@ -142,6 +153,40 @@ void allreduce_f64(cv_ctx* ctx, double* buf, int64_t n) {
              "AllReduce");
 }
 
+// Sharded CG (vec.cu cg_run_sharded): rank r owns [r*chunk, (r+1)*chunk) of every
+// parameter-space vector.  The block [b0, b1) of a summed product is reduced only onto
+// the ranks owning parts of it -- one ncclReduce per owner, grouped -- which moves the
+// bytes of a reduce-scatter instead of an all-reduce.  The external communicator only
+// sums, so there every rank receives the whole sum (same values on the owned range).
+void reduce_to_owners(cv_ctx* ctx, float* buf, int64_t b0, int64_t b1, int64_t chunk, cudaStream_t st) {
+  if (ctx->comm_fn) return comm_call(ctx, CV_DTYPE_F32, buf + b0, b1 - b0, st);
+  if (!ctx->nccl || b1 <= b0) return;
+  NcclApi& a = nccl_api();
+  nccl_check(a.GroupStart(), "GroupStart");
+  for (int r = (int)(b0 / chunk); r < ctx->world && (int64_t)r * chunk < b1; ++r) {
+    const int64_t s0 = std::max(b0, (int64_t)r * chunk), s1 = std::min(b1, (int64_t)(r + 1) * chunk);
+    if (s1 > s0)
+      nccl_check(a.Reduce(buf + s0, buf + s0, (size_t)(s1 - s0), ncclFloat32, ncclSum, r, (ncclComm_t)ctx->nccl, st),
+                 "Reduce");
+  }
+  nccl_check(a.GroupEnd(), "GroupEnd");
+}
+
+// buf holds world*chunk floats; rank r's chunk is valid on rank r; afterwards all are
+// valid everywhere.  The external communicator does it as a sum with zeros elsewhere.
+void allgather_f32(cv_ctx* ctx, float* buf, int64_t chunk) {
+  float* mine = buf + (int64_t)ctx->rank * chunk;
+  if (ctx->comm_fn) {
+    if (ctx->rank > 0) cudaMemsetAsync(buf, 0, sizeof(float) * (size_t)(mine - buf), ctx->stream);
+    const int64_t tail = (int64_t)(ctx->world - 1 - ctx->rank) * chunk;
+    if (tail > 0) cudaMemsetAsync(mine + chunk, 0, sizeof(float) * (size_t)tail, ctx->stream);
+    return comm_call(ctx, CV_DTYPE_F32, buf, (int64_t)ctx->world * chunk, ctx->stream);
+  }
+  if (!ctx->nccl) return;
+  nccl_check(nccl_api().AllGather(mine, buf, (size_t)chunk, ncclFloat32, (ncclComm_t)ctx->nccl, ctx->stream),
+             "AllGather");
+}
+
 void LayerAllreduce::ready(int l, cudaStream_t st) {
   if (!ctx->nccl || ctx->comm_fn) return;
   if (!ctx->comm) {
@@ -158,6 +203,7 @@ void LayerAllreduce::ready(int l, cudaStream_t st) {
   cudaStreamWaitEvent(ctx->comm, ctx->comm_ev[pending], 0);
   ++pending;
   const int64_t b0 = (*off)[l], b1 = l + 1 < (int)off->size() ? (*off)[l + 1] : d;
+  if (ctx->shard_chunk) return reduce_to_owners(ctx, out, b0, b1, ctx->shard_chunk, ctx->comm);
   nccl_check(nccl_api().AllReduce(out + b0, out + b0, (size_t)(b1 - b0), ncclFloat32, ncclSum,
                                   (ncclComm_t)ctx->nccl, ctx->comm),
              "AllReduce");
@@ -166,7 +212,8 @@ void LayerAllreduce::ready(int l, cudaStream_t st) {
 void LayerAllreduce::finish() {
   if (!distributed(ctx)) return;
   if (ctx->comm_fn || !pending) {  // external communicator (or nothing bucketed): one reduction
-    allreduce_f32(ctx, out, d);
+    if (ctx->shard_chunk) reduce_to_owners(ctx, out, 0, d, ctx->shard_chunk, ctx->stream);
+    else allreduce_f32(ctx, out, d);
     return;
   }
   cudaEvent_t e = ctx->comm_ev[0];

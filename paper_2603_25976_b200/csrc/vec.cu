@@ -379,20 +379,56 @@ __global__ void k_cg_init(const float* g, const float* x0, int64_t d, double* ws
   });
   write_partials<2>(ws, t);
 }
+// The control decisions, from the totals of a reduction (one thread).  The
+// replicated loop takes them in the last block of the reducing kernel; the sharded
+// loop after the all-reduce of the per-rank totals.
+CV_DEV void init_decide(double gg, double nz, CgDev* st) {
+  st->bnorm = sqrt(gg);
+  st->x0nz = nz > 0.0;
+  st->rz = st->alpha = st->rr = 0.0;
+  st->relres = 0.0;
+  st->iters = 0; st->conv = 0; st->neg = 0; st->gv = 0;
+  st->done = st->bnorm == 0.0;
+  if (st->done) { st->conv = 1; st->x0nz = 0; }
+  st->gv_skip = st->done || !st->x0nz;
+}
+CV_DEV void r0_decide(double rr, CgDev* st, double tol) {
+  if (st->x0nz) st->gv++;
+  st->relres = sqrt(rr) / st->bnorm;
+  if (st->relres <= tol) { st->done = 1; st->conv = 1; st->iters = 0; }
+  st->gv_skip = st->done;
+}
+CV_DEV void pap_decide(double pap, double mx, double nonfinite, CgDev* st, int k, int stab) {
+  st->gv++;
+  if (!isfinite(pap)) { st->done = 1; st->iters = k; st->conv = 0; }
+  else if (pap <= 0.0) { st->done = 1; st->iters = k; st->conv = 0; st->neg = 1; }
+  else {
+    const double alpha = st->rz / pap;
+    const bool step_ok = isfinite(alpha) && nonfinite == 0.0 && fabs((double)(float)alpha) * mx < (double)FLT_MAX;
+    if (!step_ok) { st->done = 1; st->iters = k; st->conv = 0; }
+    st->alpha = alpha;
+  }
+  st->gv_skip = st->done || !stab;
+}
+CV_DEV void r_decide(double rr, double rz_new, CgDev* st, int k, int maxiter, int stab, double tol) {
+  if (stab) st->gv++;
+  const double relres = sqrt(rr) / st->bnorm;
+  st->relres = relres;
+  if (!isfinite(relres)) { st->done = 1; st->iters = k; st->conv = 0; }
+  else if (relres <= tol) { st->done = 1; st->iters = k; st->conv = 1; }
+  else {
+    st->alpha = rz_new / st->rz;  // beta, consumed by k_cg_pnext
+    st->rz = rz_new;
+    if (k == maxiter) { st->done = 1; st->iters = maxiter; st->conv = 0; }
+  }
+  st->gv_skip = st->done;
+}
+
 __global__ void k_cg_init_final(const double* ws, CgDev* st) {
   CV_PDL_ENTRY();
   double t[2];
   sum_partials<2>(ws, t);
-  if (threadIdx.x == 0) {
-    st->bnorm = sqrt(t[0]);
-    st->x0nz = t[1] > 0.0;
-    st->rz = st->alpha = st->rr = 0.0;
-    st->relres = 0.0;
-    st->iters = 0; st->conv = 0; st->neg = 0; st->gv = 0;
-    st->done = st->bnorm == 0.0;
-    if (st->done) { st->conv = 1; st->x0nz = 0; }
-    st->gv_skip = st->done || !st->x0nz;
-  }
+  if (threadIdx.x == 0) init_decide(t[0], t[1], st);
 }
 // x = x0 (if any nonzero entry) else 0
 __global__ void k_cg_setup_x(const float* x0, const CgDev* st, int64_t d, float* x) {
@@ -434,12 +470,7 @@ __global__ void k_cg_r0_final(const double* ws, CgDev* st, double tol) {
   if (st->done) return;
   double t[1];
   sum_partials<1>(ws, t);
-  if (threadIdx.x == 0) {
-    if (st->x0nz) st->gv++;
-    st->relres = sqrt(t[0]) / st->bnorm;
-    if (st->relres <= tol) { st->done = 1; st->conv = 1; st->iters = 0; }
-    st->gv_skip = st->done;
-  }
+  if (threadIdx.x == 0) r0_decide(t[0], st, tol);
 }
 // p = z = M^-1 r; rz = r.z
 __global__ void k_cg_p0(const float* r, const float* pre, float lam, float floor_, const CgDev* st, int64_t d,
@@ -510,7 +541,7 @@ __global__ void k_cg_pap(float* ap, const float* p, float lam, CgDev* st, int64_
     for (int w = 0; w < NT / 32; ++w) m = fmax(m, smx[w]);
     ws[blockIdx.x * 8 + 1] = m;
   }
-  if (grid_last(ctr)) pap_final_body(ws, st, k, stab);
+  if (ctr && grid_last(ctr)) pap_final_body(ws, st, k, stab);
 }
 CV_DEV void pap_final_body(const double* ws, CgDev* st, int k, int stab) {
   double t[3];
@@ -529,17 +560,7 @@ CV_DEV void pap_final_body(const double* ws, CgDev* st, int k, int stab) {
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int w = 0; w < NT / 32; ++w) mx = fmax(mx, smx[w]);
-    st->gv++;
-    const double pap = t[0];
-    if (!isfinite(pap)) { st->done = 1; st->iters = k; st->conv = 0; }
-    else if (pap <= 0.0) { st->done = 1; st->iters = k; st->conv = 0; st->neg = 1; }
-    else {
-      const double alpha = st->rz / pap;
-      const bool step_ok = isfinite(alpha) && t[2] == 0.0 && fabs((double)(float)alpha) * mx < (double)FLT_MAX;
-      if (!step_ok) { st->done = 1; st->iters = k; st->conv = 0; }
-      st->alpha = alpha;
-    }
-    st->gv_skip = st->done || !stab;
+    pap_decide(t[0], mx, t[2], st, k, stab);
   }
 }
 // plain iteration: x += a p; r -= a Ap; partials ||r||^2, r.M^-1 r
@@ -574,7 +595,7 @@ __global__ void k_cg_update(float* x, float* r, const float* p, const float* ap,
     r[i] = ri;
   }
   write_partials<2>(ws, t);
-  if (grid_last(ctr)) r_final_body(ws, st, k, maxiter, 0, tol);
+  if (ctr && grid_last(ctr)) r_final_body(ws, st, k, maxiter, 0, tol);
 }
 // stabilising iteration: x += a p (the explicit residual product follows)
 __global__ void k_cg_xupdate(float* x, const float* p, const CgDev* st, int64_t d) {
@@ -613,7 +634,7 @@ __global__ void k_cg_rstab(const float* g, const float* ax, const float* x, floa
     stv<W>(r + i, rv);
   });
   write_partials<2>(ws, t);
-  if (grid_last(ctr)) r_final_body(ws, st, k, maxiter, 1, tol);
+  if (ctr && grid_last(ctr)) r_final_body(ws, st, k, maxiter, 1, tol);
 }
 CV_DEV void r_final_body(const double* ws, CgDev* st, int k, int maxiter, int stab, double tol) {
   double t[2] = {0.0, 0.0};
@@ -622,20 +643,7 @@ CV_DEV void r_final_body(const double* ws, CgDev* st, int k, int maxiter, int st
     t[1] += __ldcg(ws + b * 8 + 1);
   }
   block_sum<2>(t);
-  if (threadIdx.x == 0) {
-    if (stab) st->gv++;
-    const double relres = sqrt(t[0]) / st->bnorm;
-    st->relres = relres;
-    if (!isfinite(relres)) { st->done = 1; st->iters = k; st->conv = 0; }
-    else if (relres <= tol) { st->done = 1; st->iters = k; st->conv = 1; }
-    else {
-      const double rz_new = t[1];
-      st->alpha = rz_new / st->rz;  // beta, consumed by k_cg_pnext
-      st->rz = rz_new;
-      if (k == maxiter) { st->done = 1; st->iters = maxiter; st->conv = 0; }
-    }
-    st->gv_skip = st->done;
-  }
+  if (threadIdx.x == 0) r_decide(t[0], t[1], st, k, maxiter, stab, tol);
 }
 // p = M^-1 r + beta p
 __global__ void k_cg_pnext(const float* r, const float* pre, float lam, float floor_, const CgDev* st, int64_t d,
@@ -669,6 +677,53 @@ __global__ void k_cg_finish(const CgDev* st, cv_cg_stats* out) {
   out->x0_nonzero = st->x0nz;
 }
 
+// Sharded loop: reductions end in per-rank totals, all-reduced, then decided.
+template <int NV>
+__global__ void k_cgs_total(const double* ws, double* tot) {
+  CV_PDL_ENTRY();
+  double t[NV];
+  sum_partials<NV>(ws, t);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int v = 0; v < NV; ++v) tot[v] = t[v];
+}
+// p.Ap and #nonfinite summed; max|p| into this rank's slot (the sum-only all-reduce
+// then carries every rank's maximum)
+__global__ void k_cgs_pap_total(const double* ws, double* tot, int rank, int world) {
+  CV_PDL_ENTRY();
+  double t[3] = {0.0, 0.0, 0.0}, mx = 0.0;
+  for (int b = threadIdx.x; b < NB; b += NT) {
+    t[0] += ws[b * 8 + 0];
+    t[2] += ws[b * 8 + 2];
+    mx = fmax(mx, ws[b * 8 + 1]);
+  }
+  block_sum<3>(t);
+  __shared__ double smx[NT / 32];
+  mx = warp_max_d(mx);
+  if ((threadIdx.x & 31) == 0) smx[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < NT / 32; ++w) mx = fmax(mx, smx[w]);
+    tot[0] = t[0];
+    tot[1] = t[2];
+    for (int j = 0; j < world; ++j) tot[2 + j] = j == rank ? mx : 0.0;
+  }
+}
+enum { CGS_INIT, CGS_R0, CGS_P0, CGS_PAP, CGS_R };
+__global__ void k_cgs_decide(const double* tot, CgDev* st, int what, int k, int maxiter, int stab, double tol,
+                             int world) {
+  CV_PDL_ENTRY();
+  if (what == CGS_INIT) return init_decide(tot[0], tot[1], st);
+  if (st->done) return;
+  if (what == CGS_R0) r0_decide(tot[0], st, tol);
+  else if (what == CGS_P0) st->rz = tot[0];
+  else if (what == CGS_PAP) {
+    double mx = 0.0;
+    for (int j = 0; j < world; ++j) mx = fmax(mx, tot[2 + j]);
+    pap_decide(tot[0], mx, tot[1], st, k, stab);
+  } else r_decide(tot[0], tot[1], st, k, maxiter, stab, tol);
+}
+
 // The operator of a parameter-space CG run: a snapshot's curvature product (the
 // direction update also publishes the next product's input scales).
 struct CgOperator {
@@ -681,6 +736,19 @@ struct CgOperator {
 static void cg_run(cv_ctx* ctx, const CgOperator& op, const float* g, double lam, double tol, int maxiter, int stab,
                    const float* precond, double floor, const float* x0, float* x, cv_cg_stats* stats, float* r,
                    float* p, float* ap);
+static void cg_run_sharded(cv_ctx* ctx, const CgOperator& op, const float* g, double lam, double tol, int maxiter,
+                           int stab, const float* precond, double floor, const float* x0, float* x,
+                           cv_cg_stats* stats);
+
+// Shard the CG vectors across ranks once the replicated vector passes (13 x 4 d bytes
+// per iteration, ~0.15 ms at d = 8M) outweigh the sharded loop's extra launches and
+// scalar all-reduces (~30-40 us per iteration): C5 (d = 63M) shards, C3 (d = 1.9M)
+// stays replicated.
+constexpr int64_t kShardMinD = int64_t(1) << 23;
+static bool cg_sharded(const cv_ctx* ctx, int64_t d) {
+  if (!distributed(ctx) || ctx->shard_cg == 0) return false;
+  return ctx->shard_cg == 1 || (ctx->world > 1 && d >= kShardMinD);
+}
 
 void cg_solve(cv_ctx* ctx, cv_snap* s, int kind, const float* g, double lam, double tol, int maxiter, int stab,
               const float* precond, double floor, const float* x0, float* x, cv_cg_stats* stats) {
@@ -688,6 +756,7 @@ void cg_solve(cv_ctx* ctx, cv_snap* s, int kind, const float* g, double lam, dou
   op.d = s->d;
   op.s = s;
   op.mv = matvec_fn(kind);
+  if (cg_sharded(ctx, s->d)) return cg_run_sharded(ctx, op, g, lam, tol, maxiter, stab, precond, floor, x0, x, stats);
   cg_run(ctx, op, g, lam, tol, maxiter, stab, precond, floor, x0, x, stats, snap_tmp(s, &s->cg_r),
          snap_tmp(s, &s->cg_p), snap_tmp(s, &s->cg_ap));
 }
@@ -775,7 +844,7 @@ __global__ void k_dcg_pap(double* ap, const double* p, double lam, CgDev* st, in
     for (int w = 0; w < NT / 32; ++w) q = fmax(q, smx[w]);
     ws[blockIdx.x * 8 + 1] = q;
   }
-  if (grid_last(ctr)) pap_final_body(ws, st, k, stab);
+  if (ctr && grid_last(ctr)) pap_final_body(ws, st, k, stab);
 }
 __global__ void k_dcg_update(double* x, double* r, const double* p, const double* ap, CgDev* st, int64_t m, double* ws,
                              unsigned* ctr, int k, int maxiter, double tol) {
@@ -791,7 +860,7 @@ __global__ void k_dcg_update(double* x, double* r, const double* p, const double
     t[1] += ri * ri;
   }
   write_partials<2>(ws, t);
-  if (grid_last(ctr)) r_final_body(ws, st, k, maxiter, 0, tol);
+  if (ctr && grid_last(ctr)) r_final_body(ws, st, k, maxiter, 0, tol);
 }
 __global__ void k_dcg_xupdate(double* x, const double* p, const CgDev* st, int64_t m) {
   CV_PDL_ENTRY();
@@ -811,7 +880,7 @@ __global__ void k_dcg_rstab(const double* b, const double* ax, const double* x, 
     t[1] += ri * ri;
   }
   write_partials<2>(ws, t);
-  if (grid_last(ctr)) r_final_body(ws, st, k, maxiter, 1, tol);
+  if (ctr && grid_last(ctr)) r_final_body(ws, st, k, maxiter, 1, tol);
 }
 __global__ void k_dcg_pnext(const double* r, const CgDev* st, int64_t m, double* p) {
   CV_PDL_ENTRY();
@@ -928,6 +997,99 @@ static void cg_run(cv_ctx* ctx, const CgOperator& op, const float* g, double lam
   }
   launch_k(sm, k_cg_finish, 1, 1, 0, st, stats);
   ctx->launches++;
+}
+
+// Data-parallel CG with sharded vectors (world ranks, batch-sharded products).  Rank r
+// owns [r*chunk, (r+1)*chunk) of x, r, p and Ap: the summed product is reduced only onto
+// its owners (reduce_to_owners, per layer as the weight gradients finish), the update,
+// residual and direction passes run on d/world elements, each reduction is a few-double
+// all-reduce of per-rank totals followed by the replicated decision, and p (and x before
+// a stabilising product, and at the end) is all-gathered for the next product.  Same
+// recurrence and decisions as cg_run (solvers.py:60-114); only the summation order of
+// the dot products differs.
+static void cg_run_sharded(cv_ctx* ctx, const CgOperator& op, const float* g, double lam, double tol, int maxiter,
+                           int stab, const float* precond, double floor, const float* x0, float* x,
+                           cv_cg_stats* stats) {
+  const int64_t d = op.d;
+  const int W = ctx->world, R = ctx->rank;
+  const int64_t chunk = ((d + W - 1) / W + 63) / 64 * 64;  // 256-byte aligned shards
+  const int64_t lo = std::min(d, (int64_t)R * chunk);
+  const int64_t n = std::max<int64_t>(0, std::min(d, lo + chunk) - lo);
+  const int64_t dp = chunk * W;
+  CgDev* st = (CgDev*)(ctx->scal_ws + 8);
+  double* ws = ctx->red_ws;
+  cudaStream_t sm = ctx->stream;
+  const float flam = (float)lam, ffl = (float)floor;
+  float* buf = (float*)ctx->pool.get(sizeof(float) * 4 * dp);
+  double* tot = (double*)ctx->pool.get(sizeof(double) * (8 + W));
+  float *xs = buf, *r = buf + dp, *p = buf + 2 * dp, *ap = buf + 3 * dp;
+  cudaMemsetAsync(buf, 0, sizeof(float) * 4 * dp, sm);  // padding beyond d stays finite
+  const float* gl = g + lo;
+  const float* pre = precond ? precond + lo : nullptr;
+  float *xl = xs + lo, *rl = r + lo, *pl = p + lo, *apl = ap + lo;
+
+  auto decide = [&](int what, int nv, int k, int is_stab) {
+    allreduce_f64(ctx, tot, nv);
+    launch_k(sm, k_cgs_decide, 1, 1, 0, (const double*)tot, st, what, k, maxiter, is_stab, tol, W);
+    ctx->launches += 2;
+  };
+  auto product = [&](const float* in, const int* skip) {
+    ctx->shard_chunk = chunk;
+    try {
+      op.apply(ctx, in, ap, skip);
+    } catch (...) {
+      ctx->shard_chunk = 0;
+      throw;
+    }
+    ctx->shard_chunk = 0;
+  };
+
+  launch_k(sm, k_cg_init, NB, NT, 0, gl, x0 ? x0 + lo : nullptr, n, ws);
+  launch_k(sm, k_cgs_total<2>, 1, NT, 0, (const double*)ws, tot);
+  decide(CGS_INIT, 2, 0, 0);
+  if (x0) {
+    launch_k(sm, k_cg_setup_x, NB, NT, 0, x0, (const CgDev*)st, d, xs);  // whole x: the product's input
+    ctx->launches++;
+    product(xs, &st->gv_skip);
+  }
+  launch_k(sm, k_cg_r0, NB, NT, 0, gl, (const float*)apl, (const float*)xl, flam, (const CgDev*)st, n, rl, ws);
+  launch_k(sm, k_cgs_total<1>, 1, NT, 0, (const double*)ws, tot);
+  decide(CGS_R0, 1, 0, 0);
+  launch_k(sm, k_cg_p0, NB, NT, 0, (const float*)rl, pre, flam, ffl, (const CgDev*)st, n, pl, ws);
+  launch_k(sm, k_cgs_total<1>, 1, NT, 0, (const double*)ws, tot);
+  decide(CGS_P0, 1, 0, 0);
+  allgather_f32(ctx, p, chunk);
+  ctx->launches += 6;
+  for (int k = 1; k <= maxiter; ++k) {
+    const int is_stab = (stab > 0 && k % stab == 0) ? 1 : 0;
+    product(p, &st->done);
+    launch_k(sm, k_cg_pap, NB, NT, 0, apl, (const float*)pl, flam, st, n, ws, (unsigned*)nullptr, k, is_stab);
+    launch_k(sm, k_cgs_pap_total, 1, NT, 0, (const double*)ws, tot, R, W);
+    decide(CGS_PAP, 2 + W, k, is_stab);
+    if (is_stab) {
+      launch_k(sm, k_cg_xupdate, NB, NT, 0, xl, (const float*)pl, (const CgDev*)st, n);
+      allgather_f32(ctx, xs, chunk);
+      product(xs, &st->gv_skip);
+      launch_k(sm, k_cg_rstab, NB, NT, 0, gl, (const float*)apl, (const float*)xl, rl, pre, flam, ffl, st, n, ws,
+               (unsigned*)nullptr, k, maxiter, tol);
+    } else {
+      launch_k(sm, k_cg_update, NB, NT, 0, xl, rl, (const float*)pl, (const float*)apl, pre, flam, ffl, st, n, ws,
+               (unsigned*)nullptr, k, maxiter, tol);
+    }
+    launch_k(sm, k_cgs_total<2>, 1, NT, 0, (const double*)ws, tot);
+    decide(CGS_R, 2, k, is_stab);
+    ctx->launches += 4 + is_stab;
+    if (k == maxiter) break;
+    launch_k(sm, k_cg_pnext, NB, NT, 0, (const float*)rl, pre, flam, ffl, (const CgDev*)st, n, pl);
+    allgather_f32(ctx, p, chunk);
+    ctx->launches++;
+  }
+  allgather_f32(ctx, xs, chunk);
+  cudaMemcpyAsync(x, xs, sizeof(float) * d, cudaMemcpyDeviceToDevice, sm);
+  launch_k(sm, k_cg_finish, 1, 1, 0, (const CgDev*)st, stats);
+  ctx->launches++;
+  ctx->pool.put(buf);
+  ctx->pool.put(tot);
 }
 
 }  // namespace cv

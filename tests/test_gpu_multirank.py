@@ -67,13 +67,13 @@ if world > 1:
 """
 
 
-def _run(case, world, tmp_path):
+def _run(case, world, tmp_path, extra=None):
     procs, outs = [], []
     port = 29700 + os.getpid() % 200
     for r in range(world):
         out = str(tmp_path / f"{case}_{world}_{r}.json")
         env = dict(os.environ, CASE=case, OUT=out, RANK=str(r), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1",
-                   MASTER_PORT=str(port))
+                   MASTER_PORT=str(port), **(extra or {}))
         procs.append(subprocess.Popen([sys.executable, "-c", SCRIPT % {"root": ROOT}], env=env,
                                       stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
         outs.append(out)
@@ -90,14 +90,17 @@ def _run(case, world, tmp_path):
 TIGHT = ("loss_before", "loss_after", "grad_norm", "step_norm", "diag_mean", "trace_estimate", "lam")
 
 
-@pytest.mark.parametrize("case", ["pcg_tr", "sophia_g", "newton_cg"])
-def test_two_ranks_on_one_gpu_match_the_full_batch(case, tmp_path):
+@pytest.mark.parametrize("case,shard", [("pcg_tr", "0"), ("sophia_g", "0"), ("newton_cg", "0"), ("pcg_tr", "1"),
+                                        ("newton_cg", "1")])
+def test_two_ranks_on_one_gpu_match_the_full_batch(case, shard, tmp_path):
+    """shard=1: the CG vectors sharded across the two ranks (vec.cu cg_run_sharded: owner
+    reductions of the product, per-rank update passes, all-gathered directions)."""
     import paper_2603_25976_b200 as P
 
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     full = _run(case, 1, tmp_path)[0]
-    ranks = _run(case, 2, tmp_path)
+    ranks = _run(case, 2, tmp_path, {"CURVOPT_SHARD_CG": shard})
     ref = np.array(full["rows"], dtype=np.float64)
     for r, res in enumerate(ranks):
         assert res["host_comm_calls"] > 0, "the world-2 run must go through the communicator"
@@ -116,3 +119,6 @@ def test_two_ranks_on_one_gpu_match_the_full_batch(case, tmp_path):
         assert np.linalg.norm(w - wf) / np.linalg.norm(wf) < 1e-4
     # replicated decisions: both ranks hold bitwise the same weights
     assert ranks[0]["w"] == ranks[1]["w"]
+    if shard == "1":  # the sharded loop ran: its totals and all-gathers add collectives
+        plain = _run(case, 2, tmp_path, {"CURVOPT_SHARD_CG": "0"})
+        assert ranks[0]["host_comm_calls"] > plain[0]["host_comm_calls"]

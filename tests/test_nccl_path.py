@@ -47,3 +47,20 @@ def test_forced_single_rank_nccl_matches():
     b = _run({"CURVOPT_FORCE_NCCL": "1"})
     assert a["rows"] == b["rows"] or json.dumps(a["rows"]) == json.dumps(b["rows"])
     assert a["w"] == b["w"]
+
+
+def test_forced_single_rank_sharded_cg_matches():
+    """The sharded CG loop (owner reductions, totals all-reduced, all-gathers) through a
+    one-rank NCCL communicator: the same iterates up to the summation order."""
+    import numpy as np
+
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    a = _run({})
+    b = _run({"CURVOPT_FORCE_NCCL": "1", "CURVOPT_SHARD_CG": "1"})
+    ra, rb = np.array(a["rows"], dtype=np.float64), np.array(b["rows"], dtype=np.float64)
+    assert np.array_equal(np.isnan(ra), np.isnan(rb))
+    ok = ~np.isnan(ra)
+    np.testing.assert_allclose(rb[ok], ra[ok], rtol=1e-6, atol=1e-12)
+    assert abs(a["w"] - b["w"]) <= 1e-6 * abs(a["w"])
