@@ -221,6 +221,13 @@ CV_API int cv_row_rhs(cv_snap* snap, float* rhs_out /* m */);
 CV_API int cv_row_gram(cv_snap* snap, float* gram_out /* m*m, nullable: keep on device */);
 CV_API int cv_row_solve_cholesky(cv_snap* snap, double mu, const float* rhs, float* v_out);
 CV_API int cv_backproject(cv_snap* snap, const float* v_row, float* out);
+/* Distributed row lane (solvers.py:146-161 across the ranks of ctx): the
+ * same solve as cv_row_solve_cholesky with the Gram never held whole by one rank --
+ * block-cyclic 1024-row panels, SYRK strips, right-looking Cholesky with broadcast
+ * panels, distributed triangular solves and fp64 refinement.  `snap` is a whole-batch
+ * snapshot built on a world-1 context of the same device (every rank gathers the batch);
+ * rhs, v_out are the whole m-vectors, replicated.  Collective over ctx's ranks. */
+CV_API int cv_row_solve_cholesky_dist(cv_ctx* ctx, cv_snap* snap, double mu, const float* rhs, float* v_out);
 /* Row-space CG on (Gram + mu I) v = rhs with the snapshot's Gram (solvers.py:164-174,
  * method.py:270-282: row_solve_cg(lambda u: gram @ u, rhs, mu, cfg, x0)); the same
  * device-resident loop as cv_cg_solve, products are dense Gram GEMVs.  x0 nullable. */

@@ -523,6 +523,23 @@ int cv_row_solve_cholesky(cv_snap* s, double mu, const float* rhs, float* v_out)
   CV_CATCH
 }
 
+int cv_row_solve_cholesky_dist(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, float* v_out) {
+  if (!s) return CV_E_CONTRACT;
+  CV_TRY(ctx)
+  contract(s->ctx->device == _ctx->device, "snapshot and context are on different devices");
+  contract(s->ctx->world == 1, "the distributed row lane takes a whole-batch (replicated) snapshot");
+  if (s->ctx->stream != _ctx->stream) {  // the snapshot's work first
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    cudaEventRecord(e, s->ctx->stream);
+    cudaStreamWaitEvent(_ctx->stream, e, 0);
+    cudaEventDestroy(e);
+  }
+  if (dist_row_cholesky(_ctx, s, mu, rhs, v_out) != 0)
+    throw CvError(CV_E_NOT_PD, "row system is not positive definite; mu too small or gram invalid");
+  CV_CATCH
+}
+
 int cv_row_solve_cg(cv_snap* s, double mu, const float* rhs, double tol, int maxiter, int stabilise_every,
                     const float* x0, float* v_out, cv_cg_stats* stats) {
   if (!s) return CV_E_CONTRACT;

@@ -96,7 +96,7 @@ CV_DEV void epi_apply(const Epilogue& e, const EpiRt& rt, int m, int n, float v,
       return;
     }
     case EPI_GRAM: {
-      const float sa = e.sa[(int64_t)(m / e.kdiv) * e.sa_ld + n / e.kdiv];
+      const float sa = e.sa[(int64_t)((m + e.row0) / e.kdiv) * e.sa_ld + n / e.kdiv];
       float* o = e.out + (int64_t)m * e.ld + n;
       if (e.first) *o = v * sa;
       else red_add_f32(o, v * sa);
@@ -212,7 +212,7 @@ CV_DEV bool epi_applyV(const Epilogue& e, const EpiRt& rt, int m, int nb, const 
     }
     case EPI_GRAM: {
       float* out = e.out + o;
-      const float* sa = e.sa + (int64_t)(m / e.kdiv) * e.sa_ld;
+      const float* sa = e.sa + (int64_t)((m + e.row0) / e.kdiv) * e.sa_ld;
       if (!al16(out)) return false;
 #pragma unroll
       // all loads of the row segment first (the stores alias them: issued in one batch

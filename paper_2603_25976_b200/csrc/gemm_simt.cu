@@ -14,7 +14,8 @@ constexpr int SB_M = 64, SB_N = 64, SB_K = 16;
 __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs a) {
   CV_PDL_ENTRY();
   if (skip_if(a.skip)) return;
-  if (a.lower_only && (int)(blockIdx.x * SB_N) > (int)(blockIdx.y * SB_M + SB_M - 1) + a.lower_only - 1) return;
+  if (a.lower_only && (int)(blockIdx.x * SB_N) > lo_row(a, (int)(blockIdx.y * SB_M + SB_M - 1)) + a.lower_only - 1)
+    return;
   __shared__ __align__(16) float As[SB_K][SB_M + 4];
   __shared__ __align__(16) float Bs[SB_K][SB_N + 4];
   const int tid = threadIdx.x;
@@ -69,7 +70,8 @@ __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs a) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int n = n0 + tx * 4 + j;
-      if (n < a.N && (!a.lower_only || n <= m + a.lower_only - 1)) epi_apply(a.epi, rt, m, n, acc[i][j], amax, ramax);
+      if (n < a.N && (!a.lower_only || n <= lo_row(a, m) + a.lower_only - 1))
+        epi_apply(a.epi, rt, m, n, acc[i][j], amax, ramax);
     }
   }
   epi_flush_amax(a.epi, amax, ramax);

@@ -60,6 +60,7 @@ struct TcArgs {
   Epilogue epi;
   const int* skip;
   int lower_only;
+  int cyc_nb, cyc_skip;
   int tma_out;        // 0: per-thread stores; 1: fp16 split pair via TMA; 2: fp32 (out or partial) via TMA
   float* partial;     // split-K partials (nullptr: apply the epilogue directly)
   int tiles_m, tiles_n, splits;
@@ -638,7 +639,7 @@ CV_DEV void tile_epilogue(const TcArgs& a, const TcMaps& maps, const EpiRt& rt, 
     float v[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * inv;
-    const bool full_chunk = nb + 32 <= a.N && (!a.lower_only || nb + 31 <= m + a.lower_only - 1);
+    const bool full_chunk = nb + 32 <= a.N && (!a.lower_only || nb + 31 <= lo_row(a, m) + a.lower_only - 1);
     if (a.partial) {
       float* dst = a.partial + ((int64_t)split * a.M + m) * a.N + nb;
       if (full_chunk && al16(dst)) {
@@ -653,7 +654,8 @@ CV_DEV void tile_epilogue(const TcArgs& a, const TcMaps& maps, const EpiRt& rt, 
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const int n = nb + j;
-        if (n < a.N && (!a.lower_only || n <= m + a.lower_only - 1)) epi_apply(a.epi, rt, m, n, v[j], amax, ramax);
+        if (n < a.N && (!a.lower_only || n <= lo_row(a, m) + a.lower_only - 1))
+          epi_apply(a.epi, rt, m, n, v[j], amax, ramax);
       }
     }
   }
@@ -697,7 +699,7 @@ CV_DEV bool tc_work(const TcArgs& a, int w, int bm, int bn, int& m0, int& n0, in
   }
   kb0 = split * a.kb_per_split;
   nkb = min(a.kb_total, kb0 + a.kb_per_split) - kb0;
-  return !(a.lower_only && n0 > m0 + bm - 1 + a.lower_only - 1);
+  return !(a.lower_only && n0 > lo_row(a, m0 + bm - 1) + a.lower_only - 1);
 }
 
 // TMA of one operand slab: K-major = one box {64 K, rows}; MN-major = rows/64 boxes
@@ -1202,6 +1204,8 @@ static void fill_args(const GemmArgs& g, int bbox, TcMaps& maps, TcArgs& a) {
   a.epi = g.epi;
   a.skip = g.skip;
   a.lower_only = g.lower_only;
+  a.cyc_nb = g.cyc_nb;
+  a.cyc_skip = g.cyc_skip;
 }
 
 template <int BN, int STAGES>

@@ -77,6 +77,7 @@ struct Epilogue {
   const float* sa = nullptr;     // EPI_GRAM: b x b activation Gram, ld sa_ld
   int64_t sa_ld = 0;
   int kdiv = 1;                  // EPI_GRAM: rows per example
+  int64_t row0 = 0;              // EPI_GRAM: Gram row of the output's row 0 (row strips)
   int first = 0;                 // EPI_GRAM: overwrite instead of accumulate
   float alpha = 1.f;             // EPI_ACCUM
   // Fused output-layer JVP ("head", EPI_SPLIT_MASK on the last hidden layer only):
@@ -97,6 +98,12 @@ struct Epilogue {
   int64_t bits_out_ld = 0;
 };
 
+// the row index lower_only compares against (GemmArgs / TcArgs)
+template <class Args>
+__host__ __device__ inline int lo_row(const Args& a, int m) {
+  return a.cyc_nb ? m + (m / a.cyc_nb) * a.cyc_skip : m;
+}
+
 struct GemmArgs {
   int M = 0, N = 0;
   int nseg = 1;
@@ -104,6 +111,9 @@ struct GemmArgs {
   Epilogue epi;
   const int* skip = nullptr;     // device flag: kernel returns immediately when != 0
   int lower_only = 0;            // > 0: only the lower part n <= m + (lower_only - 1) (diagonal offset)
+  // lower_only on block-cyclic rows (the distributed row lane: a rank's panels of cyc_nb
+  // rows are every world-th panel of the matrix): row m counts as m + (m / cyc_nb) * cyc_skip
+  int cyc_nb = 0, cyc_skip = 0;
   cudaStream_t stream = nullptr; // nullptr: the context stream
   int max_ctas = 0;              // > 0: cap on the persistent grid (SM share when co-scheduled)
   int unsplit = 0;               // plan without split-K (the fused output head needs whole tiles)
@@ -289,6 +299,9 @@ void allreduce_f32(cv_ctx* ctx, float* buf, int64_t n);
 void allreduce_f64(cv_ctx* ctx, double* buf, int64_t n);
 void reduce_to_owners(cv_ctx* ctx, float* buf, int64_t b0, int64_t b1, int64_t chunk, cudaStream_t st);
 void allgather_f32(cv_ctx* ctx, float* buf, int64_t chunk);
+void broadcast(cv_ctx* ctx, void* buf, int64_t n, int dtype, int root);
+void comm_group(cv_ctx* ctx, bool begin);
+int dist_row_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, float* v_out);
 // Per-layer ("bucketed") all-reduce of a flat parameter-space vector being produced
 // layer by layer: ready(l, st) is called once layer l's block is final on stream st;
 // with NCCL its all-reduce starts at once on the comm stream, overlapping the GEMMs

@@ -171,12 +171,31 @@ static Operand sop(const SplitBuf& b, bool trans) {
 
 __global__ void __launch_bounds__(256) k_sym_mirror(float* G, int64_t m);
 
+// A block of Gram rows [r0, r0 + rows), columns 0 .. r0 + rows - 1 (lower part and the
+// diagonal block), stored at out with leading dimension ld: the distributed row lane's
+// block-cyclic row panels.
+struct GramStrip {
+  int64_t r0;
+  int rows;
+  float* out;
+  int64_t ld;
+};
+
+// Gram = sum_l (D_l D_l^T) o kron(A_l A_l^T, 1 1^T): into s->gram (whole, mirrored), or
+// into the given row strips only (the D chain and A_l A_l^T are formed whole either way).
+static void gram_build(cv_ctx* ctx, cv_snap* s, const std::vector<GramStrip>* strips);
+
 static void ensure_gram(cv_ctx* ctx, cv_snap* s) {
   if (s->row_state & 2) return;
+  gram_build(ctx, s, nullptr);
+  s->row_state |= 2;
+}
+
+static void gram_build(cv_ctx* ctx, cv_snap* s, const std::vector<GramStrip>* strips) {
   ensure_seeds(ctx, s);
   const int b = s->bl, c = s->c, L = s->L;
   const int64_t m = (int64_t)b * c;
-  if (!s->gram) s->gram = snap_alloc(s, m * m);
+  if (!strips && !s->gram) s->gram = snap_alloc(s, m * m);
   float* sa = snap_alloc(s, (int64_t)b * b);
   // D ping-pong buffers sized for the widest layer
   int wmax = c;
@@ -219,7 +238,22 @@ static void ensure_gram(cv_ctx* ctx, cv_snap* s) {
     h.epi.kdiv = c;
     h.epi.first = l == L - 1;
     h.lower_only = 1;  // SYRK: lower tiles only, mirrored below
-    gemm(ctx, h);
+    if (!strips) {
+      gemm(ctx, h);
+    } else {
+      for (const GramStrip& g : *strips) {  // rows [r0, r0 + rows) against rows [0, r0 + rows)
+        GemmArgs hs = h;
+        hs.M = g.rows;
+        hs.N = (int)(g.r0 + g.rows);
+        hs.seg[0].A.hi += g.r0 * ldD;
+        hs.seg[0].A.lo += g.r0 * ldD;
+        hs.epi.out = g.out;
+        hs.epi.ld = g.ld;
+        hs.epi.row0 = g.r0;
+        hs.lower_only = (int)g.r0 + 1;
+        gemm(ctx, hs);
+      }
+    }
     if (l > 0) {
       // D <- (D W_l^T) * act'(a_l) broadcast over the k rows of each example
       cudaMemsetAsync(D[cur ^ 1].sc, 0, sizeof(Scale), ctx->stream);
@@ -263,12 +297,11 @@ static void ensure_gram(cv_ctx* ctx, cv_snap* s) {
       cur ^= 1;
     }
   }
-  {
+  if (!strips) {
     const int nt = (int)((m + 31) / 32);
     launch_k(ctx->stream, k_sym_mirror, dim3(nt, nt), 256, 0, s->gram, m);
     ctx->launches++;
   }
-  s->row_state |= 2;
 }
 
 const float* row_gram_dev(cv_ctx* ctx, cv_snap* s) {
@@ -1094,6 +1127,349 @@ void row_backproject(cv_ctx* ctx, cv_snap* s, const float* v, float* out) {
   launch_k(ctx->stream, k_seed_apply, (int)((m + 255) / 256), 256, 0, s->seeds, v, s->bl, s->c, s->U2);
   ctx->launches++;
   mlp_vjp(ctx, s, s->U2, out);
+}
+
+// ---------------------------------------------------------------------------
+// Distributed row lane: (Gram + mu I) v = rhs across the ranks of the
+// context, the Gram never held whole by any rank.  The m rows are cut into panels of
+// NBO = 1024 rows dealt block-cyclically (panel p on rank p mod world), so every rank
+// holds ~m/world rows of the lower triangle and the factorization's work stays
+// balanced as the trailing matrix shrinks.  The snapshot `s` holds the whole batch on
+// every rank (the caller gathers it): the D chain and A_l A_l^T are formed whole, the
+// Gram SYRK only for the rank's row panels (gram_build with strips).
+//
+// Right-looking factorization, step k (panel column k):
+//  - the owner of panel k factors its diagonal block and forms W_k = L_kk^-1 (the
+//    single-GPU kernels: k_potrf_diag, k_panel_step, k_trtri_panel); W_k and W_k^T are
+//    broadcast (the triangular solves of every rank use them);
+//  - each rank forms L_ik = A_ik W_k^T for its panels i > k (one tensor-core GEMM over
+//    its contiguous local rows) and the panels are broadcast by their owners into a
+//    buffer in global row order (one NCCL group);
+//  - each rank applies A_ij -= L_ik L_jk^T to its panels i > k (lower part, red.add
+//    epilogue), the owner of panel k+1 first, whose diagonal block is then factored on a
+//    side stream while the rest of the update runs (look-ahead).
+// Triangular solves with replicated fp64 vectors: forward, the owner of panel k forms
+// y_k = W_k (r_k - L_k,<k y_<k) and broadcasts it; backward, every rank accumulates
+// L_i,<i^T x_i of its own panels, the k-block of those sums is all-reduced, and every
+// rank forms x_k = W_k^T (y_k - s_k) itself.  Two steps of fp64 refinement use the
+// rank's Gram strips (row part + transposed strictly-lower part, all-reduced).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_strip_lower_add_diag(const float* src, float* dst, int rows, int64_t r0,
+                                                              int64_t ld, float mu) {
+  CV_PDL_ENTRY();
+  const int64_t i0 = (int64_t)blockIdx.y * 32, j0 = (int64_t)blockIdx.x * 32;
+  if (j0 > r0 + i0 + 31) return;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int rr = ty; rr < 32; rr += 8) {
+    const int64_t i = i0 + rr, j = j0 + tx;
+    if (i >= rows || j > r0 + i) continue;
+    const float v = src[i * ld + j];
+    dst[i * ld + j] = j == r0 + i ? v + mu : v;
+  }
+}
+// out[i] += sign * sum_{j < len_i} A[i, j] x[j], len_i = ncols (diag_off < 0) or
+// diag_off + i + 1 (the lower part of a Gram strip row); one 256-thread block per row,
+// 128-bit loads, two accumulators per thread, fixed-order block reduction
+__global__ void __launch_bounds__(256) k_row_dot(const float* A, int64_t lda, int64_t ncols, int64_t diag_off,
+                                                 const double* x, double sign, double* out) {
+  CV_PDL_ENTRY();
+  const int i = blockIdx.x;
+  const float* a = A + (int64_t)i * lda;
+  const int64_t len = diag_off < 0 ? ncols : diag_off + i + 1;
+  const bool vec = ((lda & 3) == 0) && !((uintptr_t)A & 15);
+  const int64_t n4 = vec ? (len & ~(int64_t)3) : 0;
+  double s0 = 0.0, s1 = 0.0;
+  int64_t j = (int64_t)threadIdx.x * 4;
+  for (; j + 1024 < n4; j += 2048) {
+    const float4 p = *reinterpret_cast<const float4*>(a + j);
+    const float4 q = *reinterpret_cast<const float4*>(a + j + 1024);
+    s0 += (double)p.x * x[j] + (double)p.y * x[j + 1] + (double)p.z * x[j + 2] + (double)p.w * x[j + 3];
+    s1 += (double)q.x * x[j + 1024] + (double)q.y * x[j + 1025] + (double)q.z * x[j + 1026] + (double)q.w * x[j + 1027];
+  }
+  for (; j < n4; j += 1024) {
+    const float4 p = *reinterpret_cast<const float4*>(a + j);
+    s0 += (double)p.x * x[j] + (double)p.y * x[j + 1] + (double)p.z * x[j + 2] + (double)p.w * x[j + 3];
+  }
+  for (int64_t t = n4 + threadIdx.x; t < len; t += 256) s1 += (double)a[t] * x[t];
+  double v[1] = {s0 + s1};
+  block_sum<1>(v);
+  if (threadIdx.x == 0) out[i] += sign * v[0];
+}
+// Column sums in row slices: part[y][j] = sum over rows i of slice y (i >= j - r0 + 1
+// when strict) of A[i, j] x[i], for j < ncols; k_col_reduce adds the slices in order.
+constexpr int CD_SLICES = 32;
+__global__ void __launch_bounds__(256) k_col_dot_part(const float* A, int64_t lda, int rows, int64_t ncols,
+                                                      int64_t r0, int strict, const double* x, double* part) {
+  CV_PDL_ENTRY();
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= ncols) return;
+  const int per = (rows + gridDim.y - 1) / gridDim.y;
+  int i0 = blockIdx.y * per;
+  const int i1 = min(rows, i0 + per);
+  if (strict && j - r0 + 1 > i0) i0 = (int)(j - r0 + 1 < (int64_t)i1 ? j - r0 + 1 : (int64_t)i1);
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  int i = i0;
+  for (; i + 4 <= i1; i += 4)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[u] += (double)A[(int64_t)(i + u) * lda + j] * x[i + u];
+  for (; i < i1; ++i) acc[0] += (double)A[(int64_t)i * lda + j] * x[i];
+  part[(int64_t)blockIdx.y * ncols + j] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+__global__ void k_col_reduce(const double* part, int slices, int64_t ncols, double* z) {
+  CV_PDL_ENTRY();
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < ncols; j += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int y = 0; y < slices; ++y) s += part[(int64_t)y * ncols + j];
+    z[j] += s;
+  }
+}
+__global__ void k_sub_d(const double* y, const double* z, int n, double* t) {
+  CV_PDL_ENTRY();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) t[i] = y[i] - z[i];
+}
+// r = rhs - (u + mu v)
+__global__ void k_res_from(const float* rhs, const double* u, const double* v, double mu, int64_t m, double* r) {
+  CV_PDL_ENTRY();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    r[i] = (double)rhs[i] - (u[i] + mu * v[i]);
+}
+__global__ void k_flag_d(const int* flag, double* out) {
+  CV_PDL_ENTRY();
+  *out = *flag ? 1.0 : 0.0;
+}
+
+int dist_row_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, float* v_out) {
+  constexpr int NBO = TT_MAX;
+  const int W = ctx->world, R = ctx->rank;
+  const int64_t m = (int64_t)s->bl * s->c;
+  const int np = (int)((m + NBO - 1) / NBO);
+  cudaStream_t st = ctx->stream;
+  auto owner = [&](int p) { return p % W; };
+  auto mine = [&](int p) { return p % W == R; };
+  auto prow = [&](int p) { return (int)std::min<int64_t>(NBO, m - (int64_t)p * NBO); };
+  auto lrow = [&](int p) { return (int64_t)(p / W) * NBO; };  // local row of my panel p
+  int64_t lrows = 0;
+  for (int p = R; p < np; p += W) lrows += prow(p);
+  Pool& pool = ctx->pool;
+  std::vector<void*> bufs;
+  auto get = [&](size_t bytes) {
+    void* q = pool.get(bytes ? bytes : 16);
+    bufs.push_back(q);
+    return q;
+  };
+  float* gram = (float*)get(sizeof(float) * (size_t)(lrows * m));
+  float* chol = (float*)get(sizeof(float) * (size_t)(lrows * m));
+  float* dinv = (float*)get(sizeof(float) * (size_t)(((m + CH_NB - 1) / CH_NB) * CH_NB * CH_NB));
+  float* winv = (float*)get(sizeof(float) * (size_t)(2 * (int64_t)np * NBO * NBO));
+  float* winvT = winv + (int64_t)np * NBO * NBO;
+  float* gbuf = (float*)get(sizeof(float) * (size_t)(m * NBO));
+  __half* gh = (__half*)get(sizeof(__half) * (size_t)(m * NBO));
+  __half* gl = (__half*)get(sizeof(__half) * (size_t)(m * NBO));
+  __half* ah = (__half*)get(sizeof(__half) * (size_t)(lrows * NBO));
+  __half* al = (__half*)get(sizeof(__half) * (size_t)(lrows * NBO));
+  __half* wh = (__half*)get(sizeof(__half) * (size_t)NBO * NBO);
+  __half* wl = (__half*)get(sizeof(__half) * (size_t)NBO * NBO);
+  float* Lblk = (float*)get(sizeof(float) * (size_t)NBO * NBO);
+  Scale* sc = (Scale*)get(sizeof(Scale) * 4);
+  double* vecs = (double*)get(sizeof(double) * (size_t)(6 * m + 8));
+  int rc = 0;
+  try {
+    // Gram strips of my panels, then chol = their lower part + mu I
+    std::vector<GramStrip> strips;
+    for (int p = R; p < np; p += W) strips.push_back(GramStrip{(int64_t)p * NBO, prow(p), gram + lrow(p) * m, m});
+    if (!strips.empty()) gram_build(ctx, s, &strips);
+    else ensure_seeds(ctx, s);
+    for (const GramStrip& g : strips) {
+      launch_k(st, k_strip_lower_add_diag, dim3((unsigned)((m + 31) / 32), (unsigned)((g.rows + 31) / 32)), 256, 0,
+               (const float*)g.out, chol + (g.out - gram), g.rows, g.r0, m, (float)mu);
+      ctx->launches++;
+    }
+    int* flag = (int*)(ctx->scal_ws + 32);
+    cudaMemsetAsync(flag, 0, sizeof(int), st);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_panel_step, cudaFuncAttributeMaxDynamicSharedMemorySize, PS_SMEM);
+      attr = true;
+    }
+    // my diagonal block of panel k: factor, 64-block inverses, W_k and W_k^T
+    auto diag = [&](int k, cudaStream_t ds) {
+      const int nbo = prow(k);
+      const int nsub = (nbo + CH_NB - 1) / CH_NB;
+      const int64_t p0 = (int64_t)k * NBO;
+      float* Ad = chol + lrow(k) * m + p0;
+      float* dp = dinv + (p0 / CH_NB) * (int64_t)CH_NB * CH_NB;
+      launch_k(ds, k_potrf_diag, 1, 256, 0, (const float*)Ad, m, nbo < CH_NB ? nbo : CH_NB, Lblk, (int64_t)nbo, dp,
+               flag);
+      for (int j = 0; j + 1 < nsub; ++j) {
+        const int tiles = (nsub - j - 1) * (nsub - j) / 2;
+        launch_k(ds, k_panel_step, tiles, 256, PS_SMEM, Ad, m, nbo, j, Lblk, dp, flag);
+      }
+      launch_k(ds, k_trtri_panel, (nbo + TT_C - 1) / TT_C, 256, 0, (const float*)Lblk, (int64_t)nbo,
+               (const float*)dp, 0, nbo, winv + (int64_t)k * NBO * NBO, winvT + (int64_t)k * NBO * NBO);
+      ctx->launches += nsub + 1;
+    };
+    constexpr int kReserveSMs = 16;
+    int ahead = -1;  // panel whose diagonal block the previous step already factored
+    for (int k = 0; k < np; ++k) {
+      const int64_t p0 = (int64_t)k * NBO;
+      const int nbk = prow(k);
+      if (mine(k) && ahead != k) diag(k, st);
+      comm_group(ctx, true);
+      broadcast(ctx, winv + (int64_t)k * NBO * NBO, (int64_t)nbk * nbk, CV_DTYPE_F32, owner(k));
+      broadcast(ctx, winvT + (int64_t)k * NBO * NBO, (int64_t)nbk * nbk, CV_DTYPE_F32, owner(k));
+      comm_group(ctx, false);
+      const int64_t rest = m - p0 - nbk;
+      if (rest <= 0) break;
+      // L_ik = A_ik W_k^T for my panels i > k (contiguous local rows), in place
+      int pf = k + 1;
+      while (pf < np && !mine(pf)) ++pf;
+      if (pf < np) {
+        const int64_t rowsA = lrows - lrow(pf);
+        float* A21 = chol + lrow(pf) * m + p0;
+        const float* Wk = winv + (int64_t)k * NBO * NBO;
+        split_mat(ctx, A21, m, (int)rowsA, nbk, ah, al, nbk, 0, sc, 0, nullptr);
+        split_mat(ctx, Wk, nbk, nbk, nbk, wh, wl, nbk, 0, sc + 1, 0, nullptr);
+        Operand A, B;
+        A.hi = ah; A.lo = al; A.sc = sc; A.si = nbk; A.sj = 1;
+        B.hi = wh; B.lo = wl; B.sc = sc + 1; B.si = 1; B.sj = nbk;  // B(k, j) = W[j, k]
+        GemmArgs t;
+        t.M = (int)rowsA;
+        t.N = nbk;
+        t.nseg = 1;
+        t.seg[0] = GemmSeg{A, B, nbk};
+        t.epi.mode = EPI_STORE;
+        t.epi.out = A21;
+        t.epi.ld = m;
+        gemm(ctx, t);
+        for (int p = pf; p < np; p += W)  // into the global-order panel column
+          cudaMemcpy2DAsync(gbuf + (int64_t)(p - k - 1) * NBO * nbk, sizeof(float) * nbk, chol + lrow(p) * m + p0,
+                            sizeof(float) * m, sizeof(float) * nbk, prow(p), cudaMemcpyDeviceToDevice, st);
+        // my rows of the panel column, split: the A operand of my trailing update
+        split_mat(ctx, A21, m, (int)rowsA, nbk, ah, al, nbk, 0, sc + 3, 0, nullptr);
+      }
+      comm_group(ctx, true);
+      for (int p = k + 1; p < np; ++p)
+        broadcast(ctx, gbuf + (int64_t)(p - k - 1) * NBO * nbk, (int64_t)prow(p) * nbk, CV_DTYPE_F32, owner(p));
+      comm_group(ctx, false);
+      if (pf >= np) continue;  // no trailing rows here
+      // the trailing update of my panels from the (replicated) panel column
+      split_mat(ctx, gbuf, nbk, (int)rest, nbk, gh, gl, nbk, 0, sc + 2, 0, nullptr);
+      // A_ij -= L_ik L_jk^T for my panels i >= p_start (contiguous local rows) and j <= i:
+      // one GEMM, the block-cyclic lower predicate (cyc_nb / cyc_skip) skipping the tiles
+      // right of each panel's diagonal
+      auto update = [&](int p_start, int p_count, int max_ctas) {
+        const int64_t lr0 = lrow(p_start) - lrow(pf);
+        int64_t rows = 0;
+        for (int p = p_start, c = 0; p < np && c < p_count; p += W, ++c) rows += prow(p);
+        Operand A, B;
+        A.hi = ah + lr0 * nbk; A.lo = al + lr0 * nbk; A.sc = sc + 3; A.si = nbk; A.sj = 1;
+        B.hi = gh; B.lo = gl; B.sc = sc + 2; B.si = 1; B.sj = nbk;  // B(k, j) = L[j, k]
+        GemmArgs u;
+        u.M = (int)rows;
+        u.N = (int)std::min<int64_t>(rest, (int64_t)(p_start - k - 1 + (int64_t)(p_count - 1) * W) * NBO +
+                                               prow(std::min(np - 1, p_start + (p_count - 1) * W)));
+        u.nseg = 1;
+        u.seg[0] = GemmSeg{A, B, nbk};
+        u.epi.mode = EPI_ACCUM;
+        u.epi.alpha = -1.f;
+        u.epi.out = chol + lrow(p_start) * m + p0 + nbk;
+        u.epi.ld = m;
+        u.lower_only = (p_start - k - 1) * NBO + 1;
+        u.cyc_nb = NBO;
+        u.cyc_skip = (W - 1) * NBO;
+        u.max_ctas = max_ctas;
+        gemm(ctx, u);
+      };
+      const int nmine = (int)((np - 1 - pf) / W) + 1;  // my panels from pf on
+      if (pf == k + 1) {  // I own the next panel: its diagonal block first, then its factorization beside the rest
+        update(pf, 1, 0);
+        if (nmine > 1 && ctx->sm_count > 4 * kReserveSMs) {
+          cudaStream_t side = side_fork(ctx);
+          diag(pf, side);
+          ahead = pf;
+          update(pf + W, nmine - 1, ctx->sm_count - kReserveSMs);
+          side_join(ctx);
+        } else if (nmine > 1) {
+          update(pf + W, nmine - 1, 0);
+        }
+      } else {
+        update(pf, nmine, 0);
+      }
+    }
+    // not positive definite anywhere -> everywhere
+    double* fl = vecs + 6 * m;
+    launch_k(st, k_flag_d, 1, 1, 0, (const int*)flag, fl);
+    allreduce_f64(ctx, fl, 1);
+    double hflag = 0.0;
+    cudaMemcpyAsync(&hflag, fl, sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    if (hflag != 0.0) {
+      rc = 1;
+    } else {
+      double *r = vecs, *y = vecs + m, *v = vecs + 2 * m, *dv = vecs + 3 * m, *z = vecs + 4 * m, *t = vecs + 5 * m;
+      double* part = (double*)get(sizeof(double) * (size_t)(CD_SLICES * m));
+      // z[j] += sum_i A[i, j] x[i] over a row block (strict: the strictly-lower part)
+      auto col_dot = [&](const float* A, int rows, int64_t ncols, int64_t r0, int strict, const double* x,
+                         double* zz) {
+        const int slices = std::min(CD_SLICES, std::max(1, rows / 32));
+        launch_k(st, k_col_dot_part, dim3((unsigned)((ncols + 255) / 256), (unsigned)slices), 256, 0, A, m, rows,
+                 ncols, r0, strict, x, part);
+        launch_k(st, k_col_reduce, (int)std::min<int64_t>(1024, (ncols + 255) / 256), 256, 0, (const double*)part,
+                 slices, ncols, zz);
+        ctx->launches += 2;
+      };
+      auto tri_solve = [&](double* x) {  // r -> x = (L L^T)^-1 r, r consumed
+        for (int k = 0; k < np; ++k) {
+          const int64_t p0 = (int64_t)k * NBO;
+          const int nbk = prow(k);
+          if (mine(k)) {
+            if (k > 0)
+              launch_k(st, k_row_dot, nbk, 256, 0, (const float*)(chol + lrow(k) * m), m, p0, (int64_t)-1,
+                       (const double*)y, -1.0, r + p0);
+            launch_k(st, k_tri_wgemv, (nbk + 7) / 8, 256, 0, (const float*)(winv + (int64_t)k * NBO * NBO), nbk,
+                     (int)p0, (const double*)r, y);
+            ctx->launches += 2;
+          }
+          broadcast(ctx, y + p0, nbk, CV_DTYPE_F64, owner(k));
+        }
+        cudaMemsetAsync(z, 0, sizeof(double) * m, st);
+        for (int k = np - 1; k >= 0; --k) {
+          const int64_t p0 = (int64_t)k * NBO;
+          const int nbk = prow(k);
+          allreduce_f64(ctx, z + p0, nbk);
+          launch_k(st, k_sub_d, (nbk + 255) / 256, 256, 0, (const double*)(y + p0), (const double*)(z + p0), nbk, t);
+          launch_k(st, k_tri_wtgemv, (nbk + 7) / 8, 256, 0, (const float*)(winvT + (int64_t)k * NBO * NBO), nbk,
+                   (int)p0, (const double*)t, x);
+          ctx->launches += 2;
+          if (mine(k) && k > 0) col_dot((const float*)(chol + lrow(k) * m), nbk, p0, 0, 0, x + p0, z);
+        }
+      };
+      launch_k(st, k_f2d, 256, 256, 0, rhs, r, m);
+      tri_solve(v);
+      for (int it = 0; it < 2; ++it) {
+        // z = Gram v from the strips (row parts + transposed strictly-lower parts), summed over ranks
+        cudaMemsetAsync(z, 0, sizeof(double) * m, st);
+        for (const GramStrip& g : strips) {
+          launch_k(st, k_row_dot, g.rows, 256, 0, (const float*)g.out, m, (int64_t)0, g.r0, (const double*)v, 1.0,
+                   z + g.r0);
+          ctx->launches++;
+          col_dot((const float*)g.out, g.rows, g.r0 + g.rows, g.r0, 1, v + g.r0, z);
+        }
+        allreduce_f64(ctx, z, m);
+        launch_k(st, k_res_from, 256, 256, 0, rhs, (const double*)z, (const double*)v, mu, m, r);
+        tri_solve(dv);
+        launch_k(st, k_axpy_d, 256, 256, 0, (const double*)dv, v, m);
+        ctx->launches += 2;
+      }
+      launch_k(st, k_d2f, 256, 256, 0, (const double*)v, v_out, m);
+      ctx->launches += 2;
+    }
+  } catch (...) {
+    for (void* q : bufs) pool.put(q);
+    throw;
+  }
+  for (void* q : bufs) pool.put(q);
+  return rc;
 }
 
 }  // namespace cv

@@ -74,6 +74,7 @@ struct NcclApi {
   ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
                          cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -99,11 +100,12 @@ static NcclApi& nccl_api() {
   api.AllReduce = (decltype(api.AllReduce))dlsym(api.h, "ncclAllReduce");
   api.Reduce = (decltype(api.Reduce))dlsym(api.h, "ncclReduce");
   api.AllGather = (decltype(api.AllGather))dlsym(api.h, "ncclAllGather");
+  api.Broadcast = (decltype(api.Broadcast))dlsym(api.h, "ncclBroadcast");
   api.GroupStart = (decltype(api.GroupStart))dlsym(api.h, "ncclGroupStart");
   api.GroupEnd = (decltype(api.GroupEnd))dlsym(api.h, "ncclGroupEnd");
   api.GetErrorString = (decltype(api.GetErrorString))dlsym(api.h, "ncclGetErrorString");
   if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.Reduce || !api.AllGather ||
-      !api.GroupStart || !api.GroupEnd)
+      !api.Broadcast || !api.GroupStart || !api.GroupEnd)
     throw std::runtime_error("NCCL library lacks required symbols");
   return api;
 }
@@ -185,6 +187,26 @@ void allgather_f32(cv_ctx* ctx, float* buf, int64_t chunk) {
   if (!ctx->nccl) return;
   nccl_check(nccl_api().AllGather(mine, buf, (size_t)chunk, ncclFloat32, (ncclComm_t)ctx->nccl, ctx->stream),
              "AllGather");
+}
+
+// root's n elements (CV_DTYPE_*) at buf to every rank, in place, on the context stream.
+// The external communicator sums: the other ranks contribute zeros.
+void broadcast(cv_ctx* ctx, void* buf, int64_t n, int dtype, int root) {
+  if (n <= 0) return;
+  const size_t es = dtype == CV_DTYPE_F64 ? 8 : 4;
+  if (ctx->comm_fn) {
+    if (ctx->rank != root) cudaMemsetAsync(buf, 0, es * (size_t)n, ctx->stream);
+    return comm_call(ctx, dtype, buf, n, ctx->stream);
+  }
+  if (!ctx->nccl) return;
+  nccl_check(nccl_api().Broadcast(buf, buf, (size_t)n, dtype == CV_DTYPE_F64 ? ncclFloat64 : ncclFloat32, root,
+                                  (ncclComm_t)ctx->nccl, ctx->stream),
+             "Broadcast");
+}
+// NCCL calls between these two are issued as one group (no-op for the external communicator)
+void comm_group(cv_ctx* ctx, bool begin) {
+  if (!ctx->nccl || ctx->comm_fn) return;
+  nccl_check(begin ? nccl_api().GroupStart() : nccl_api().GroupEnd(), begin ? "GroupStart" : "GroupEnd");
 }
 
 void LayerAllreduce::ready(int l, cudaStream_t st) {

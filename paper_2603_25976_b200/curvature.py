@@ -20,7 +20,7 @@ from . import _lib
 from .errors import ContractError
 from .models import Batch, Model, check_layout, param_count, param_layout
 from .numeric import ParamVector, _is_torch
-from .runtime import runtime
+from .runtime import gather_rows, local_runtime, runtime
 
 CURVATURE_KINDS = ("hessian", "ggn_mse", "ggn_ce")
 
@@ -50,9 +50,38 @@ class RowOps:
         self.m = snap.batch_local * snap.model.output_dim
         self._rhs = None
         self._gram = None
+        self._whole = None
+        if snap.rt.world > 1:  # the row system is the global batch's (m = b_global * c)
+            self.m = snap.batch_size * snap.model.output_dim
+
+    # -- distributed row lane (world > 1) -------------------------------------
+    # The row system couples every example of the global batch.  Each rank gathers the
+    # batch and builds a whole-batch snapshot on a world-1 context of its GPU (the D
+    # chain, seeds and back-projection are done whole, identically on every rank); the
+    # Gram and its factorization are distributed over the ranks by
+    # cv_row_solve_cholesky_dist (block-cyclic row panels).  Row CG runs on the
+    # whole-batch snapshot (its Gram is m x m on every rank).
+    def _whole_snap(self):
+        if self._whole is None:
+            s = self._snap
+            b = s._batch
+            X, y = b.device_arrays(s.rt.device)
+            Xf = gather_rows(X, b.row_offset, s.batch_size)
+            yf = gather_rows(y, b.row_offset, s.batch_size)
+            full = Batch(Xf, yf, b.loss_kind, global_size=s.batch_size, row_offset=0)
+            self._whole = Snapshot(s.kind, s.model, ParamVector(s.w_dev, s.layout), full, local_runtime(s.rt.device.index),
+                                   grad=False)
+            s.rt.bind_stream()
+        return self._whole
+
+    @property
+    def distributed(self) -> bool:
+        return self._snap.rt.world > 1
 
     @property
     def rhs(self):
+        if self.distributed:
+            return self._whole_snap().row.rhs
         if self._rhs is None:
             s = self._snap
             out = torch.empty(self.m, dtype=torch.float32, device=s.rt.device)
@@ -62,6 +91,8 @@ class RowOps:
         return self._rhs
 
     def gram(self):
+        if self.distributed:
+            return self._whole_snap().row.gram()
         if self._gram is None:
             s = self._snap
             out = torch.empty((self.m, self.m), dtype=torch.float32, device=s.rt.device)
@@ -71,12 +102,19 @@ class RowOps:
         return self._gram
 
     def solve_cholesky(self, mu: float, rhs=None):
-        """(Gram + mu I) v = rhs on the device (solvers.py:146-161)."""
+        """(Gram + mu I) v = rhs on the device (solvers.py:146-161); distributed over
+        the ranks at world > 1."""
         s = self._snap
         r = self.rhs if rhs is None else torch.as_tensor(rhs, dtype=torch.float32, device=s.rt.device).contiguous()
+        if r.numel() != self.m:
+            raise ContractError("rhs length does not match gram")
         out = torch.empty(self.m, dtype=torch.float32, device=s.rt.device)
         s.rt.bind_stream()
-        s.rt.call("cv_row_solve_cholesky", s.h, float(mu), r.data_ptr(), out.data_ptr())
+        if self.distributed:
+            s.rt.call("cv_row_solve_cholesky_dist", s.rt.h, self._whole_snap().h, float(mu), r.data_ptr(),
+                      out.data_ptr())
+        else:
+            s.rt.call("cv_row_solve_cholesky", s.h, float(mu), r.data_ptr(), out.data_ptr())
         return out
 
     def gram_matvec(self, u):
@@ -89,6 +127,8 @@ class RowOps:
         """Row-space CG on (Gram + mu I) v = rhs (solvers.py:164-174), device resident.
 
         Returns (v, stats) without synchronising; `stats` is a cv_cg_stats buffer."""
+        if self.distributed:
+            return self._whole_snap().row.solve_cg(mu, config, x0=x0, stats=stats)
         s = self._snap
         out = torch.empty(self.m, dtype=torch.float32, device=s.rt.device)
         st = torch.empty(_lib.CG_STATS_BYTES, dtype=torch.uint8, device=s.rt.device) if stats is None else stats
@@ -101,6 +141,8 @@ class RowOps:
         return out, st
 
     def scaled_row_transpose(self, u) -> ParamVector:
+        if self.distributed:
+            return self._whole_snap().row.scaled_row_transpose(u)
         s = self._snap
         u = torch.as_tensor(u, dtype=torch.float32, device=s.rt.device).contiguous().reshape(-1)
         if u.numel() != self.m:

@@ -18,6 +18,7 @@ import os
 import torch
 
 from . import _lib
+from .errors import ContractError
 
 _RUNTIMES: dict = {}
 _LOCAL = False
@@ -139,6 +140,50 @@ def runtime(device: int | None = None) -> Runtime:
         _RUNTIMES[key] = rt
     rt.bind_stream()
     return rt
+
+
+def local_runtime(device: int | None = None) -> Runtime:
+    """A world-1 runtime on the same device: work that every rank does whole (the
+    distributed row lane's whole-batch snapshot).  Same object as runtime() at world 1."""
+    if device is None:
+        device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+    key = (device, 1)
+    rt = _RUNTIMES.get(key)
+    if rt is None:
+        rt = Runtime(device, 1, 0)
+        _RUNTIMES[key] = rt
+    rt.bind_stream()
+    return rt
+
+
+def gather_rows(t: torch.Tensor, row_offset: int, total: int) -> torch.Tensor:
+    """The global batch's rows on every rank: each rank's rows [row_offset, row_offset +
+    len) placed by offset (torch.distributed all-gather: on the device under NCCL, through
+    host memory under gloo).  Raises if the shards do not tile [0, total)."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size()
+    meta = [None] * world
+    dist.all_gather_object(meta, (int(row_offset), int(t.shape[0])))
+    spans = sorted(meta)
+    pos = 0
+    for off, n in spans:
+        if off != pos:
+            raise ContractError("batch shards do not tile the global batch")
+        pos += n
+    if pos != total:
+        raise ContractError("batch shards do not add up to the global batch size")
+    nmax = max(n for _, n in meta)
+    pad = torch.zeros((nmax,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    pad[: t.shape[0]] = t
+    if dist.get_backend() != "nccl":
+        pad = pad.cpu()
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad)
+    full = torch.empty((total,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    for (off, n), q in zip(meta, parts):
+        full[off:off + n] = q[:n].to(t.device)
+    return full
 
 
 def shutdown() -> None:

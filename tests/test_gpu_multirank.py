@@ -41,6 +41,9 @@ if case == "pcg_tr":
     meth = P.make("sgn_ce", m, solver={"cg": {"maxiter": 10}}, precond={"kind": "diag_ema"},
                   estimator={"kind": "hutchinson", "every_k": 2},
                   damping={"policy": "trust_region", "tr": {"every_k": 1}}, telemetry={"trace_every_k": 2})
+elif case == "egn_ce":
+    m = P.Model(784, (256, 256), 10, "tanh")
+    meth = P.make("egn_ce", m)
 elif case == "sophia_g":
     m = P.Model(784, (256, 256), 10, "tanh")
     meth = P.make("sophia_g", m, estimator={"kind": "gnb", "every_k": 1})
@@ -91,10 +94,12 @@ TIGHT = ("loss_before", "loss_after", "grad_norm", "step_norm", "diag_mean", "tr
 
 
 @pytest.mark.parametrize("case,shard", [("pcg_tr", "0"), ("sophia_g", "0"), ("newton_cg", "0"), ("pcg_tr", "1"),
-                                        ("newton_cg", "1")])
+                                        ("newton_cg", "1"), ("egn_ce", "0")])
 def test_two_ranks_on_one_gpu_match_the_full_batch(case, shard, tmp_path):
     """shard=1: the CG vectors sharded across the two ranks (vec.cu cg_run_sharded: owner
-    reductions of the product, per-rank update passes, all-gathered directions)."""
+    reductions of the product, per-rank update passes, all-gathered directions).
+    egn_ce: the distributed row lane (m = 10,240 rows in 10 panels, 5 per rank;
+    cv_row_solve_cholesky_dist on the gathered whole-batch snapshot)."""
     import paper_2603_25976_b200 as P
 
     if not torch.cuda.is_available():

@@ -154,3 +154,34 @@ def test_row_cholesky_lookahead_system_residual():
     assert e < 1e-6
     del G
     snap.close()
+
+
+def _dist_solve(snap, mu, rhs=None):
+    rt = snap.rt
+    r = snap.row.rhs if rhs is None else rhs
+    out = torch.empty(r.numel(), dtype=torch.float32, device=rt.device)
+    rt.bind_stream()
+    rt.call("cv_row_solve_cholesky_dist", rt.h, snap.h, float(mu), r.data_ptr(), out.data_ptr())
+    return out
+
+
+@pytest.mark.parametrize("b", [60, 300, 1024, 2560])
+def test_distributed_row_cholesky_on_one_rank(b):
+    """cv_row_solve_cholesky_dist on a one-rank context (no collectives): Gram strips,
+    panel-column buffer, per-panel trailing updates with look-ahead and the replicated-
+    vector solves must give the single-GPU solve (m = 600: one partial panel; 3000: a
+    partial last panel; 25,600: 25 panels with look-ahead)."""
+    dims = (256, 512, 512, 10)
+    m = P.Model(dims[0], dims[1:-1], dims[-1], "relu")
+    w = P.init_params(m, P.Rng(0))
+    X, y = O.synthetic_batch(b, dims[0], dims[-1])
+    snap = P.make_snapshot("ggn_ce", m, w, P.Batch(X, y, "ce"))
+    mu = float(b)
+    v1 = snap.row.solve_cholesky(mu)
+    vd = _dist_solve(snap, mu)
+    e = rel(vd, v1)
+    print(f"m={b * dims[-1]}: distributed vs single-GPU solve {e:.2e}")
+    assert e < 1e-6
+    with pytest.raises(P.ContractError, match="not positive definite"):
+        _dist_solve(snap, -1e6)
+    snap.close()

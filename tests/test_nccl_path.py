@@ -64,3 +64,32 @@ def test_forced_single_rank_sharded_cg_matches():
     ok = ~np.isnan(ra)
     np.testing.assert_allclose(rb[ok], ra[ok], rtol=1e-6, atol=1e-12)
     assert abs(a["w"] - b["w"]) <= 1e-6 * abs(a["w"])
+
+
+DIST_SCRIPT = r"""
+import sys, json; sys.path.insert(0, %r)
+import numpy as np, torch
+import paper_2603_25976_b200 as P
+from oracle import curvopt_oracle as O
+m = P.Model(256, (512, 512), 10, "relu")
+w = P.init_params(m, P.Rng(0))
+X, y = O.synthetic_batch(300, 256, 10)
+snap = P.make_snapshot("ggn_ce", m, w, P.Batch(X, y, "ce"))
+v1 = snap.row.solve_cholesky(300.0)
+rt = snap.rt
+out = torch.empty_like(v1)
+rt.call("cv_row_solve_cholesky_dist", rt.h, snap.h, 300.0, snap.row.rhs.data_ptr(), out.data_ptr())
+print(json.dumps({"e": float((out.double() - v1.double()).norm() / v1.double().norm())}))
+""" % ROOT
+
+
+def test_forced_single_rank_distributed_row_cholesky():
+    """The distributed row lane's NCCL calls (grouped panel broadcasts, solve broadcasts
+    and all-reduces) through a one-rank communicator."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ, CURVOPT_FORCE_NCCL="1")
+    out = subprocess.run([sys.executable, "-c", DIST_SCRIPT], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert json.loads(out.stdout.strip().splitlines()[-1])["e"] < 1e-6
