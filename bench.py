@@ -52,7 +52,8 @@ class Workload:
 
     def config(self, world):
         return {"workload": self.desc, "global_batch": self.b, "dims": list(self.dims),
-                "parallelism": f"dp{world}" if self.lane == "param" else "replicas only (row lane)",
+                "parallelism": f"dp{world}" if self.lane == "param" or world == 1 else
+                f"dp{world} (row lane: Gram strips + Cholesky block-cyclic over {world} ranks)",
                 "l2": "per-step working set > 126 MB L2 (no flush)"}
 
 
@@ -560,9 +561,10 @@ def run_ours(args, rank, world):
     model = P.Model(dims[0], dims[1:-1], dims[-1], "relu")
     meth = P.assemble(SPECS[wl.key](), model)
     w0 = P.init_params(model, P.Rng(0))
+    # batch-sharded on every lane; the row lane's solve is the distributed block-cyclic
+    # Cholesky (RowOps gathers the batch for the whole-batch D chain and back-projection)
+    shard_world, shard_rank = world, rank
     row = wl.lane == "row"
-    shard_world = 1 if row else world  # the row lane runs replicas
-    shard_rank = 0 if row else rank
     bl = wl.b // shard_world
     nb = 4 if wl.key == "c3" else 2
     if wl.key == "c3":
@@ -680,9 +682,10 @@ def run_ours(args, rank, world):
         peak_note = "MEASURED_PEAKS bf16 burst / 3 (3xFP16 split passes)"
     if row:
         flops = row_flops(dims, wl.b)
-        achieved = flops / (ms / args.steps * 1e-3) / 1e12
+        achieved = flops / (ms / args.steps * 1e-3) / 1e12 / world
         unit_note = (f"one row-lane planned step at b={wl.b} (m={wl.b * dims[-1]}): Gram as SYRK + potrf = "
-                     f"{flops / 1e12:.2f} TFLOP useful, {ms / args.steps:.1f} ms/step (CUDA events)")
+                     f"{flops / 1e12:.2f} TFLOP useful, {ms / args.steps:.1f} ms/step (CUDA events)"
+                     + (f", per GPU of {world}" if world > 1 else ""))
         traffic, tsrc = None, None
     else:
         kind = 1 if wl.kind == "hessian" else 0
