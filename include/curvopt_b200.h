@@ -228,6 +228,11 @@ CV_API int cv_backproject(cv_snap* snap, const float* v_row, float* out);
  * snapshot built on a world-1 context of the same device (every rank gathers the batch);
  * rhs, v_out are the whole m-vectors, replicated.  Collective over ctx's ranks. */
 CV_API int cv_row_solve_cholesky_dist(cv_ctx* ctx, cv_snap* snap, double mu, const float* rhs, float* v_out);
+/* Row-space CG across the ranks of ctx (solvers.py:164-174): the cv_row_solve_cg loop with
+ * replicated fp64 vectors, each Gram product from the ranks' block-cyclic Gram strips plus
+ * one m-vector all-reduce.  Same snapshot / vector conventions as the Cholesky above. */
+CV_API int cv_row_solve_cg_dist(cv_ctx* ctx, cv_snap* snap, double mu, const float* rhs, double tol, int maxiter,
+                                int stabilise_every, const float* x0, float* v_out, cv_cg_stats* stats);
 /* Row-space CG on (Gram + mu I) v = rhs with the snapshot's Gram (solvers.py:164-174,
  * method.py:270-282: row_solve_cg(lambda u: gram @ u, rhs, mu, cfg, x0)); the same
  * device-resident loop as cv_cg_solve, products are dense Gram GEMVs.  x0 nullable. */

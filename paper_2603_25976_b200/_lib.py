@@ -85,6 +85,7 @@ _SIGS = {
     "cv_row_gram": (C.c_int, [_P, _P]),
     "cv_row_solve_cholesky": (C.c_int, [_P, C.c_double, _P, _P]),
     "cv_row_solve_cholesky_dist": (C.c_int, [_P, _P, C.c_double, _P, _P]),
+    "cv_row_solve_cg_dist": (C.c_int, [_P, _P, C.c_double, _P, C.c_double, C.c_int, C.c_int, _P, _P, _P]),
     "cv_backproject": (C.c_int, [_P, _P, _P]),
     "cv_row_solve_cg": (C.c_int, [_P, C.c_double, _P, C.c_double, C.c_int, C.c_int, _P, _P, _P]),
     "cv_dense_cholesky_solve": (C.c_int, [_P, _P, C.c_int64, C.c_double, _P, _P]),

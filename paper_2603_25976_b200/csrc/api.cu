@@ -540,6 +540,24 @@ int cv_row_solve_cholesky_dist(cv_ctx* ctx, cv_snap* s, double mu, const float* 
   CV_CATCH
 }
 
+int cv_row_solve_cg_dist(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, double tol, int maxiter,
+                         int stabilise_every, const float* x0, float* v_out, cv_cg_stats* stats) {
+  if (!s) return CV_E_CONTRACT;
+  CV_TRY(ctx)
+  contract(s->ctx->device == _ctx->device, "snapshot and context are on different devices");
+  contract(s->ctx->world == 1, "the distributed row lane takes a whole-batch (replicated) snapshot");
+  contract(tol > 0 && maxiter >= 1, "cg tol must be positive and maxiter >= 1");
+  if (s->ctx->stream != _ctx->stream) {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    cudaEventRecord(e, s->ctx->stream);
+    cudaStreamWaitEvent(_ctx->stream, e, 0);
+    cudaEventDestroy(e);
+  }
+  dist_row_cg(_ctx, s, mu, rhs, tol, maxiter, stabilise_every, x0, v_out, stats);
+  CV_CATCH
+}
+
 int cv_row_solve_cg(cv_snap* s, double mu, const float* rhs, double tol, int maxiter, int stabilise_every,
                     const float* x0, float* v_out, cv_cg_stats* stats) {
   if (!s) return CV_E_CONTRACT;

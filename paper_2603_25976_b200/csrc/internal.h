@@ -4,6 +4,7 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 
+#include <functional>
 #include <map>
 #include <string>
 #include <vector>
@@ -302,6 +303,11 @@ void allgather_f32(cv_ctx* ctx, float* buf, int64_t chunk);
 void broadcast(cv_ctx* ctx, void* buf, int64_t n, int dtype, int root);
 void comm_group(cv_ctx* ctx, bool begin);
 int dist_row_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, float* v_out);
+void dist_row_cg(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, double tol, int maxiter, int stab,
+                 const float* x0, float* v_out, cv_cg_stats* stats);
+void dense_cg_run(cv_ctx* ctx, int64_t m, const std::function<void(const double*, double*, const int*)>& A,
+                  const float* rhs, double mu, double tol, int maxiter, int stab, const float* x0, float* xout,
+                  cv_cg_stats* stats);
 // Per-layer ("bucketed") all-reduce of a flat parameter-space vector being produced
 // layer by layer: ready(l, st) is called once layer l's block is final on stream st;
 // with NCCL its all-reduce starts at once on the comm stream, overlapping the GEMMs

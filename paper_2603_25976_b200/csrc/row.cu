@@ -1171,8 +1171,9 @@ __global__ void __launch_bounds__(256) k_strip_lower_add_diag(const float* src, 
 // diag_off + i + 1 (the lower part of a Gram strip row); one 256-thread block per row,
 // 128-bit loads, two accumulators per thread, fixed-order block reduction
 __global__ void __launch_bounds__(256) k_row_dot(const float* A, int64_t lda, int64_t ncols, int64_t diag_off,
-                                                 const double* x, double sign, double* out) {
+                                                 const double* x, double sign, double* out, const int* skip) {
   CV_PDL_ENTRY();
+  if (skip && *skip) return;
   const int i = blockIdx.x;
   const float* a = A + (int64_t)i * lda;
   const int64_t len = diag_off < 0 ? ncols : diag_off + i + 1;
@@ -1199,8 +1200,10 @@ __global__ void __launch_bounds__(256) k_row_dot(const float* A, int64_t lda, in
 // when strict) of A[i, j] x[i], for j < ncols; k_col_reduce adds the slices in order.
 constexpr int CD_SLICES = 32;
 __global__ void __launch_bounds__(256) k_col_dot_part(const float* A, int64_t lda, int rows, int64_t ncols,
-                                                      int64_t r0, int strict, const double* x, double* part) {
+                                                      int64_t r0, int strict, const double* x, double* part,
+                                                      const int* skip) {
   CV_PDL_ENTRY();
+  if (skip && *skip) return;
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= ncols) return;
   const int per = (rows + gridDim.y - 1) / gridDim.y;
@@ -1215,8 +1218,9 @@ __global__ void __launch_bounds__(256) k_col_dot_part(const float* A, int64_t ld
   for (; i < i1; ++i) acc[0] += (double)A[(int64_t)i * lda + j] * x[i];
   part[(int64_t)blockIdx.y * ncols + j] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
-__global__ void k_col_reduce(const double* part, int slices, int64_t ncols, double* z) {
+__global__ void k_col_reduce(const double* part, int slices, int64_t ncols, double* z, const int* skip) {
   CV_PDL_ENTRY();
+  if (skip && *skip) return;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < ncols; j += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
     for (int y = 0; y < slices; ++y) s += part[(int64_t)y * ncols + j];
@@ -1236,6 +1240,77 @@ __global__ void k_res_from(const float* rhs, const double* u, const double* v, d
 __global__ void k_flag_d(const int* flag, double* out) {
   CV_PDL_ENTRY();
   *out = *flag ? 1.0 : 0.0;
+}
+
+// z[j] += sum_i A[i, j] x[i] over a row block of a strip layout (ld m); strict: only
+// the strictly-lower part (rows with r0 + i > j).  part: CD_SLICES x ncols doubles.
+static void col_dot(cv_ctx* ctx, const float* A, int64_t m, int rows, int64_t ncols, int64_t r0, int strict,
+                    const double* x, double* z, double* part, const int* skip) {
+  const int slices = std::min(CD_SLICES, std::max(1, rows / 32));
+  launch_k(ctx->stream, k_col_dot_part, dim3((unsigned)((ncols + 255) / 256), (unsigned)slices), 256, 0, A, m, rows,
+           ncols, r0, strict, x, part, skip);
+  launch_k(ctx->stream, k_col_reduce, (int)std::min<int64_t>(1024, (ncols + 255) / 256), 256, 0, (const double*)part,
+           slices, ncols, z, skip);
+  ctx->launches += 2;
+}
+
+// The rank's Gram row strips (block-cyclic 1024-row panels), built from the snapshot.
+static std::vector<GramStrip> build_strips(cv_ctx* ctx, cv_snap* s, float* gram) {
+  constexpr int NBO = TT_MAX;
+  const int W = ctx->world, R = ctx->rank;
+  const int64_t m = (int64_t)s->bl * s->c;
+  const int np = (int)((m + NBO - 1) / NBO);
+  std::vector<GramStrip> strips;
+  int64_t lr = 0;
+  for (int p = R; p < np; p += W) {
+    const int rows = (int)std::min<int64_t>(NBO, m - (int64_t)p * NBO);
+    strips.push_back(GramStrip{(int64_t)p * NBO, rows, gram + lr * m, m});
+    lr += rows;
+  }
+  if (!strips.empty()) gram_build(ctx, s, &strips);
+  else ensure_seeds(ctx, s);
+  return strips;
+}
+static int64_t strip_rows(const cv_ctx* ctx, int64_t m) {
+  constexpr int NBO = TT_MAX;
+  const int np = (int)((m + NBO - 1) / NBO);
+  int64_t lr = 0;
+  for (int p = ctx->rank; p < np; p += ctx->world) lr += std::min<int64_t>(NBO, m - (int64_t)p * NBO);
+  return lr;
+}
+// z = Gram v, summed over the ranks' strips (row parts + transposed strictly-lower parts)
+static void strips_gv(cv_ctx* ctx, const std::vector<GramStrip>& strips, int64_t m, const double* v, double* z,
+                      double* part, const int* skip) {
+  cudaMemsetAsync(z, 0, sizeof(double) * m, ctx->stream);
+  for (const GramStrip& g : strips) {
+    launch_k(ctx->stream, k_row_dot, g.rows, 256, 0, (const float*)g.out, m, (int64_t)0, g.r0, v, 1.0, z + g.r0,
+             skip);
+    ctx->launches++;
+    col_dot(ctx, g.out, m, g.rows, g.r0 + g.rows, g.r0, 1, v + g.r0, z, part, skip);
+  }
+  allreduce_f64(ctx, z, m);
+}
+
+// Row-space CG (solvers.py:164-174) across the ranks: the dense CG loop (replicated fp64
+// m-vectors and decisions) with the Gram product from the rank's strips + an m-vector
+// all-reduce per product.
+void dist_row_cg(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, double tol, int maxiter, int stab,
+                 const float* x0, float* v_out, cv_cg_stats* stats) {
+  const int64_t m = (int64_t)s->bl * s->c;
+  float* gram = (float*)ctx->pool.get(sizeof(float) * (size_t)std::max<int64_t>(1, strip_rows(ctx, m) * m));
+  double* part = (double*)ctx->pool.get(sizeof(double) * (size_t)(CD_SLICES * m));
+  try {
+    const std::vector<GramStrip> strips = build_strips(ctx, s, gram);
+    dense_cg_run(ctx, m, [&](const double* in, double* out, const int* skip) {
+      strips_gv(ctx, strips, m, in, out, part, skip);
+    }, rhs, mu, tol, maxiter, stab, x0, v_out, stats);
+  } catch (...) {
+    ctx->pool.put(part);
+    ctx->pool.put(gram);
+    throw;
+  }
+  ctx->pool.put(part);
+  ctx->pool.put(gram);
 }
 
 int dist_row_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, float* v_out) {
@@ -1275,10 +1350,7 @@ int dist_row_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, floa
   int rc = 0;
   try {
     // Gram strips of my panels, then chol = their lower part + mu I
-    std::vector<GramStrip> strips;
-    for (int p = R; p < np; p += W) strips.push_back(GramStrip{(int64_t)p * NBO, prow(p), gram + lrow(p) * m, m});
-    if (!strips.empty()) gram_build(ctx, s, &strips);
-    else ensure_seeds(ctx, s);
+    const std::vector<GramStrip> strips = build_strips(ctx, s, gram);
     for (const GramStrip& g : strips) {
       launch_k(st, k_strip_lower_add_diag, dim3((unsigned)((m + 31) / 32), (unsigned)((g.rows + 31) / 32)), 256, 0,
                (const float*)g.out, chol + (g.out - gram), g.rows, g.r0, m, (float)mu);
@@ -1408,16 +1480,6 @@ int dist_row_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, floa
     } else {
       double *r = vecs, *y = vecs + m, *v = vecs + 2 * m, *dv = vecs + 3 * m, *z = vecs + 4 * m, *t = vecs + 5 * m;
       double* part = (double*)get(sizeof(double) * (size_t)(CD_SLICES * m));
-      // z[j] += sum_i A[i, j] x[i] over a row block (strict: the strictly-lower part)
-      auto col_dot = [&](const float* A, int rows, int64_t ncols, int64_t r0, int strict, const double* x,
-                         double* zz) {
-        const int slices = std::min(CD_SLICES, std::max(1, rows / 32));
-        launch_k(st, k_col_dot_part, dim3((unsigned)((ncols + 255) / 256), (unsigned)slices), 256, 0, A, m, rows,
-                 ncols, r0, strict, x, part);
-        launch_k(st, k_col_reduce, (int)std::min<int64_t>(1024, (ncols + 255) / 256), 256, 0, (const double*)part,
-                 slices, ncols, zz);
-        ctx->launches += 2;
-      };
       auto tri_solve = [&](double* x) {  // r -> x = (L L^T)^-1 r, r consumed
         for (int k = 0; k < np; ++k) {
           const int64_t p0 = (int64_t)k * NBO;
@@ -1425,7 +1487,7 @@ int dist_row_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, floa
           if (mine(k)) {
             if (k > 0)
               launch_k(st, k_row_dot, nbk, 256, 0, (const float*)(chol + lrow(k) * m), m, p0, (int64_t)-1,
-                       (const double*)y, -1.0, r + p0);
+                       (const double*)y, -1.0, r + p0, (const int*)nullptr);
             launch_k(st, k_tri_wgemv, (nbk + 7) / 8, 256, 0, (const float*)(winv + (int64_t)k * NBO * NBO), nbk,
                      (int)p0, (const double*)r, y);
             ctx->launches += 2;
@@ -1441,21 +1503,13 @@ int dist_row_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, floa
           launch_k(st, k_tri_wtgemv, (nbk + 7) / 8, 256, 0, (const float*)(winvT + (int64_t)k * NBO * NBO), nbk,
                    (int)p0, (const double*)t, x);
           ctx->launches += 2;
-          if (mine(k) && k > 0) col_dot((const float*)(chol + lrow(k) * m), nbk, p0, 0, 0, x + p0, z);
+          if (mine(k) && k > 0) col_dot(ctx, chol + lrow(k) * m, m, nbk, p0, 0, 0, x + p0, z, part, nullptr);
         }
       };
       launch_k(st, k_f2d, 256, 256, 0, rhs, r, m);
       tri_solve(v);
       for (int it = 0; it < 2; ++it) {
-        // z = Gram v from the strips (row parts + transposed strictly-lower parts), summed over ranks
-        cudaMemsetAsync(z, 0, sizeof(double) * m, st);
-        for (const GramStrip& g : strips) {
-          launch_k(st, k_row_dot, g.rows, 256, 0, (const float*)g.out, m, (int64_t)0, g.r0, (const double*)v, 1.0,
-                   z + g.r0);
-          ctx->launches++;
-          col_dot((const float*)g.out, g.rows, g.r0 + g.rows, g.r0, 1, v + g.r0, z);
-        }
-        allreduce_f64(ctx, z, m);
+        strips_gv(ctx, strips, m, v, z, part, nullptr);  // z = Gram v
         launch_k(st, k_res_from, 256, 256, 0, rhs, (const double*)z, (const double*)v, mu, m, r);
         tri_solve(dv);
         launch_k(st, k_axpy_d, 256, 256, 0, (const double*)dv, v, m);

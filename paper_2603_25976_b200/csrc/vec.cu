@@ -8,6 +8,7 @@
 #include "epilogue.cuh"
 
 #include <float.h>
+#include <functional>
 #include <stdlib.h>
 
 #include <type_traits>
@@ -895,6 +896,19 @@ __global__ void k_dcg_out(const double* x, int64_t m, float* out) {
 
 void dense_cg_solve(cv_ctx* ctx, const float* gram, int64_t m, const float* rhs, double mu, double tol, int maxiter,
                     int stab, const float* x0, float* xout, cv_cg_stats* stats) {
+  const int64_t gb = (m + 7) / 8;
+  const int ggrid = (int)(gb < 16 * (int64_t)ctx->sm_count ? gb : 16 * (int64_t)ctx->sm_count);
+  dense_cg_run(ctx, m, [&](const double* in, double* out, const int* skip) {
+    launch_k(ctx->stream, k_gram_gemv_d, ggrid, 256, 0, gram, in, m, out, skip);
+    ctx->launches++;
+  }, rhs, mu, tol, maxiter, stab, x0, xout, stats);
+}
+
+// The row-space CG loop on any Gram product A(in, out, skip) = Gram . in (fp64 vectors;
+// the damping mu is added by the loop).
+void dense_cg_run(cv_ctx* ctx, int64_t m, const std::function<void(const double*, double*, const int*)>& A,
+                  const float* rhs, double mu, double tol, int maxiter, int stab, const float* x0, float* xout,
+                  cv_cg_stats* stats) {
   CgDev* st = (CgDev*)(ctx->scal_ws + 8);
   double* ws = ctx->red_ws;
   cudaStream_t sm = ctx->stream;
@@ -902,12 +916,6 @@ void dense_cg_solve(cv_ctx* ctx, const float* gram, int64_t m, const float* rhs,
   const int64_t ms = (m + 31) / 32 * 32;
   double* buf = (double*)ctx->pool.get(sizeof(double) * (size_t)(5 * ms));
   double *b = buf, *x = buf + ms, *r = buf + 2 * ms, *p = buf + 3 * ms, *ap = buf + 4 * ms;
-  const int64_t gb = (m + 7) / 8;
-  const int ggrid = (int)(gb < 16 * (int64_t)ctx->sm_count ? gb : 16 * (int64_t)ctx->sm_count);
-  auto A = [&](const double* in, double* out, const int* skip) {
-    launch_k(sm, k_gram_gemv_d, ggrid, 256, 0, gram, in, m, out, skip);
-    ctx->launches++;
-  };
   launch_k(sm, k_cg_init, NB, NT, 0, rhs, x0, m, ws);
   launch_k(sm, k_cg_init_final, 1, NT, 0, (const double*)ws, st);
   launch_k(sm, k_dcg_setup, NB, NT, 0, rhs, x0, (const CgDev*)st, m, b, x);

@@ -59,8 +59,8 @@ class RowOps:
     # batch and builds a whole-batch snapshot on a world-1 context of its GPU (the D
     # chain, seeds and back-projection are done whole, identically on every rank); the
     # Gram and its factorization are distributed over the ranks by
-    # cv_row_solve_cholesky_dist (block-cyclic row panels).  Row CG runs on the
-    # whole-batch snapshot (its Gram is m x m on every rank).
+    # cv_row_solve_cholesky_dist / cv_row_solve_cg_dist (block-cyclic row panels; the
+    # row vectors are whole and replicated).
     def _whole_snap(self):
         if self._whole is None:
             s = self._snap
@@ -127,9 +127,16 @@ class RowOps:
         """Row-space CG on (Gram + mu I) v = rhs (solvers.py:164-174), device resident.
 
         Returns (v, stats) without synchronising; `stats` is a cv_cg_stats buffer."""
-        if self.distributed:
-            return self._whole_snap().row.solve_cg(mu, config, x0=x0, stats=stats)
         s = self._snap
+        if self.distributed:  # Gram products from the ranks' strips
+            w = self._whole_snap()
+            out = torch.empty(self.m, dtype=torch.float32, device=s.rt.device)
+            st = torch.empty(_lib.CG_STATS_BYTES, dtype=torch.uint8, device=s.rt.device) if stats is None else stats
+            xx = None if x0 is None else torch.as_tensor(x0, dtype=torch.float32, device=s.rt.device).contiguous()
+            s.rt.bind_stream()
+            s.rt.call("cv_row_solve_cg_dist", s.rt.h, w.h, float(mu), w.row.rhs.data_ptr(), float(config.tol),
+                      int(config.maxiter), int(config.stabilise_every), _lib.ptr(xx), out.data_ptr(), st.data_ptr())
+            return out, st
         out = torch.empty(self.m, dtype=torch.float32, device=s.rt.device)
         st = torch.empty(_lib.CG_STATS_BYTES, dtype=torch.uint8, device=s.rt.device) if stats is None else stats
         xx = None

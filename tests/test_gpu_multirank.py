@@ -44,6 +44,9 @@ if case == "pcg_tr":
 elif case == "egn_ce":
     m = P.Model(784, (256, 256), 10, "tanh")
     meth = P.make("egn_ce", m)
+elif case == "egn_mse_cg":
+    m = P.Model(784, (256, 256), 10, "tanh")
+    meth = P.make("egn_mse_cg", m)
 elif case == "sophia_g":
     m = P.Model(784, (256, 256), 10, "tanh")
     meth = P.make("sophia_g", m, estimator={"kind": "gnb", "every_k": 1})
@@ -55,7 +58,10 @@ st = meth.init(w, 0)
 rows = []
 for t in range(3):
     X, y = O.synthetic_batch(b, 784, 10, seed=1 + t)
-    batch = P.Batch(X[rank * bl:(rank + 1) * bl], y[rank * bl:(rank + 1) * bl], "ce", global_size=b,
+    kind = "ce"
+    if case == "egn_mse_cg":  # regression targets for the mse lane
+        kind, y = "mse", np.eye(10)[y] * 0.5 + 0.01 * X[:, :10]
+    batch = P.Batch(X[rank * bl:(rank + 1) * bl], y[rank * bl:(rank + 1) * bl], kind, global_size=b,
                     row_offset=rank * bl)
     w, st, info = meth.step(w, batch, st)
     rows.append(info.to_row())
@@ -94,7 +100,7 @@ TIGHT = ("loss_before", "loss_after", "grad_norm", "step_norm", "diag_mean", "tr
 
 
 @pytest.mark.parametrize("case,shard", [("pcg_tr", "0"), ("sophia_g", "0"), ("newton_cg", "0"), ("pcg_tr", "1"),
-                                        ("newton_cg", "1"), ("egn_ce", "0")])
+                                        ("newton_cg", "1"), ("egn_ce", "0"), ("egn_mse_cg", "0")])
 def test_two_ranks_on_one_gpu_match_the_full_batch(case, shard, tmp_path):
     """shard=1: the CG vectors sharded across the two ranks (vec.cu cg_run_sharded: owner
     reductions of the product, per-rank update passes, all-gathered directions).

@@ -185,3 +185,24 @@ def test_distributed_row_cholesky_on_one_rank(b):
     with pytest.raises(P.ContractError, match="not positive definite"):
         _dist_solve(snap, -1e6)
     snap.close()
+
+
+def test_distributed_row_cg_on_one_rank():
+    """cv_row_solve_cg_dist on a one-rank context: the Gram products from the strips
+    (row part + transposed strictly-lower part) must reproduce the single-GPU row CG."""
+    dims, b = (256, 512, 512, 10), 300
+    m = P.Model(dims[0], dims[1:-1], dims[-1], "relu")
+    w = P.init_params(m, P.Rng(0))
+    X, y = O.synthetic_batch(b, dims[0], dims[-1])
+    snap = P.make_snapshot("ggn_ce", m, w, P.Batch(X, y, "ce"))
+    cfg = P.CgConfig(tol=1e-8, maxiter=25)
+    v1, st1 = snap.row.solve_cg(float(b), cfg)
+    rt = snap.rt
+    out = torch.empty_like(v1)
+    st = torch.empty_like(st1)
+    rt.call("cv_row_solve_cg_dist", rt.h, snap.h, float(b), snap.row.rhs.data_ptr(), 1e-8, 25, 10, None,
+            out.data_ptr(), st.data_ptr())
+    e = rel(out, v1)
+    print(f"distributed row CG vs single-GPU: {e:.2e}")
+    assert e < 1e-6
+    snap.close()
