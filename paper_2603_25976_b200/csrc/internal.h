@@ -255,7 +255,7 @@ struct cv_snap {
   float* chol = nullptr;          // m x m, Cholesky factor of gram + mu I (lower)
   float* dinv = nullptr;          // inverses of the 64-wide diagonal blocks of chol
   float* winv = nullptr;          // inverses of the 512-wide diagonal (panel) blocks of chol
-  int row_state = 0;              // bit0 seeds built, bit1 gram built
+  int row_state = 0;              // bit0 seeds built, bit1 gram (lower) built, bit2 gram mirrored
   // solver scratch (lazily allocated, d each)
   float* cg_r = nullptr; float* cg_p = nullptr; float* cg_ap = nullptr;
   float* tmp_d = nullptr; float* tmp_d2 = nullptr;

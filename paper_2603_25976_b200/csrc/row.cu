@@ -185,10 +185,21 @@ struct GramStrip {
 // into the given row strips only (the D chain and A_l A_l^T are formed whole either way).
 static void gram_build(cv_ctx* ctx, cv_snap* s, const std::vector<GramStrip>* strips);
 
+// Lower triangle (+ the diagonal tiles) of the snapshot Gram: all the Cholesky path reads.
 static void ensure_gram(cv_ctx* ctx, cv_snap* s) {
   if (s->row_state & 2) return;
   gram_build(ctx, s, nullptr);
   s->row_state |= 2;
+}
+// The whole symmetric Gram (the upper half mirrored): the caller's copy and row CG's GEMV.
+static void ensure_gram_full(cv_ctx* ctx, cv_snap* s) {
+  ensure_gram(ctx, s);
+  if (s->row_state & 4) return;
+  const int64_t m = (int64_t)s->bl * s->c;
+  const int nt = (int)((m + 31) / 32);
+  launch_k(ctx->stream, k_sym_mirror, dim3(nt, nt), 256, 0, s->gram, m);
+  ctx->launches++;
+  s->row_state |= 4;
 }
 
 static void gram_build(cv_ctx* ctx, cv_snap* s, const std::vector<GramStrip>* strips) {
@@ -297,20 +308,15 @@ static void gram_build(cv_ctx* ctx, cv_snap* s, const std::vector<GramStrip>* st
       cur ^= 1;
     }
   }
-  if (!strips) {
-    const int nt = (int)((m + 31) / 32);
-    launch_k(ctx->stream, k_sym_mirror, dim3(nt, nt), 256, 0, s->gram, m);
-    ctx->launches++;
-  }
 }
 
 const float* row_gram_dev(cv_ctx* ctx, cv_snap* s) {
-  ensure_gram(ctx, s);
+  ensure_gram_full(ctx, s);
   return s->gram;
 }
 
 void row_gram(cv_ctx* ctx, cv_snap* s, float* gram_out) {
-  ensure_gram(ctx, s);
+  ensure_gram_full(ctx, s);
   const int64_t m = (int64_t)s->bl * s->c;
   if (gram_out) cudaMemcpyAsync(gram_out, s->gram, sizeof(float) * m * m, cudaMemcpyDeviceToDevice, ctx->stream);
 }
@@ -862,25 +868,91 @@ __global__ void __launch_bounds__(256) k_tri_wtgemv(const float* Wt, int nbo, in
   if (lane == 0) x[p0 + j] = s;
 }
 
-// r = rhs - (G + mu I) v, one warp per row, fp64 accumulation (refinement residual)
-__global__ void k_row_residual(const float* G, int64_t m, float mu, const float* rhs, const double* v, double* r) {
+// out[i] += sign * sum_{j < len_i} A[i, j] x[j], len_i = ncols (diag_off < 0) or
+// diag_off + i + 1 (the lower part of a Gram strip row); one 256-thread block per row,
+// 128-bit loads, two accumulators per thread, fixed-order block reduction
+__global__ void __launch_bounds__(256) k_row_dot(const float* A, int64_t lda, int64_t ncols, int64_t diag_off,
+                                                 const double* x, double sign, double* out, const int* skip) {
   CV_PDL_ENTRY();
-  const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (row >= m) return;
-  const float* g = G + row * m;
-  const bool vec = (m & 3) == 0;
-  double s = 0.0;
-  for (int64_t k = lane * 4; k < m; k += 128) {
-    if (vec && k + 3 < m) {
-      const float4 q = *reinterpret_cast<const float4*>(g + k);
-      s += (double)q.x * v[k] + (double)q.y * v[k + 1] + (double)q.z * v[k + 2] + (double)q.w * v[k + 3];
-    } else {
-      for (int64_t t = k; t < k + 4 && t < m; ++t) s += (double)g[t] * v[t];
-    }
+  if (skip && *skip) return;
+  const int i = blockIdx.x;
+  const float* a = A + (int64_t)i * lda;
+  const int64_t len = diag_off < 0 ? ncols : diag_off + i + 1;
+  const bool vec = ((lda & 3) == 0) && !((uintptr_t)A & 15);
+  const int64_t n4 = vec ? (len & ~(int64_t)3) : 0;
+  double s0 = 0.0, s1 = 0.0;
+  int64_t j = (int64_t)threadIdx.x * 4;
+  for (; j + 1024 < n4; j += 2048) {
+    const float4 p = *reinterpret_cast<const float4*>(a + j);
+    const float4 q = *reinterpret_cast<const float4*>(a + j + 1024);
+    s0 += (double)p.x * x[j] + (double)p.y * x[j + 1] + (double)p.z * x[j + 2] + (double)p.w * x[j + 3];
+    s1 += (double)q.x * x[j + 1024] + (double)q.y * x[j + 1025] + (double)q.z * x[j + 1026] + (double)q.w * x[j + 1027];
   }
-  s = warp_sum(s);
-  if (lane == 0) r[row] = (double)rhs[row] - (s + (double)mu * v[row]);
+  for (; j < n4; j += 1024) {
+    const float4 p = *reinterpret_cast<const float4*>(a + j);
+    s0 += (double)p.x * x[j] + (double)p.y * x[j + 1] + (double)p.z * x[j + 2] + (double)p.w * x[j + 3];
+  }
+  for (int64_t t = n4 + threadIdx.x; t < len; t += 256) s1 += (double)a[t] * x[t];
+  double v[1] = {s0 + s1};
+  block_sum<1>(v);
+  if (threadIdx.x == 0) out[i] += sign * v[0];
+}
+// Column sums in row slices: part[y][j] = sum over rows i of slice y (i >= j - r0 + 1
+// when strict) of A[i, j] x[i], for j < ncols; k_col_reduce adds the slices in order.
+constexpr int CD_SLICES = 32;
+__global__ void __launch_bounds__(256) k_col_dot_part(const float* A, int64_t lda, int rows, int64_t ncols,
+                                                      int64_t r0, int strict, const double* x, double* part,
+                                                      const int* skip) {
+  CV_PDL_ENTRY();
+  if (skip && *skip) return;
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= ncols) return;
+  const int per = (rows + gridDim.y - 1) / gridDim.y;
+  int i0 = blockIdx.y * per;
+  const int i1 = min(rows, i0 + per);
+  if (strict && j - r0 + 1 > i0) i0 = (int)(j - r0 + 1 < (int64_t)i1 ? j - r0 + 1 : (int64_t)i1);
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  int i = i0;
+  for (; i + 4 <= i1; i += 4)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[u] += (double)A[(int64_t)(i + u) * lda + j] * x[i + u];
+  for (; i < i1; ++i) acc[0] += (double)A[(int64_t)i * lda + j] * x[i];
+  part[(int64_t)blockIdx.y * ncols + j] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+__global__ void k_col_reduce(const double* part, int slices, int64_t ncols, double* z, const int* skip) {
+  CV_PDL_ENTRY();
+  if (skip && *skip) return;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < ncols; j += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int y = 0; y < slices; ++y) s += part[(int64_t)y * ncols + j];
+    z[j] += s;
+  }
+}
+__global__ void k_sub_d(const double* y, const double* z, int n, double* t) {
+  CV_PDL_ENTRY();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) t[i] = y[i] - z[i];
+}
+// r = rhs - (u + mu v)
+__global__ void k_res_from(const float* rhs, const double* u, const double* v, double mu, int64_t m, double* r) {
+  CV_PDL_ENTRY();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    r[i] = (double)rhs[i] - (u[i] + mu * v[i]);
+}
+__global__ void k_flag_d(const int* flag, double* out) {
+  CV_PDL_ENTRY();
+  *out = *flag ? 1.0 : 0.0;
+}
+
+// z[j] += sum_i A[i, j] x[i] over a row block of a strip layout (ld m); strict: only
+// the strictly-lower part (rows with r0 + i > j).  part: CD_SLICES x ncols doubles.
+static void col_dot(cv_ctx* ctx, const float* A, int64_t m, int rows, int64_t ncols, int64_t r0, int strict,
+                    const double* x, double* z, double* part, const int* skip) {
+  const int slices = std::min(CD_SLICES, std::max(1, rows / 32));
+  launch_k(ctx->stream, k_col_dot_part, dim3((unsigned)((ncols + 255) / 256), (unsigned)slices), 256, 0, A, m, rows,
+           ncols, r0, strict, x, part, skip);
+  launch_k(ctx->stream, k_col_reduce, (int)std::min<int64_t>(1024, (ncols + 255) / 256), 256, 0, (const double*)part,
+           slices, ncols, z, skip);
+  ctx->launches += 2;
 }
 
 __global__ void k_axpy_d(const double* x, double* y, int64_t n) {
@@ -1037,10 +1109,12 @@ int dense_cholesky_solve(cv_ctx* ctx, const float* gram, int64_t m, double mu, c
   if (hflag) return 1;
   // fp64 triangular solves, then iterative refinement against the fp32 Gram:
   // v <- v + (L L^T)^-1 (rhs - (Gram + mu I) v), residual accumulated in fp64
-  double* r = (double*)ctx->pool.get(sizeof(double) * m * 4);
+  double* r = (double*)ctx->pool.get(sizeof(double) * m * 5);
   double* y = r + m;
   double* v = r + 2 * m;
   double* dv = r + 3 * m;
+  double* zz = r + 4 * m;
+  double* cpart = (double*)ctx->pool.get(sizeof(double) * (size_t)(CD_SLICES * m));
   const int64_t nparts_max = 2 * ctx->sm_count;
   double* part = (double*)ctx->pool.get(sizeof(double) * (size_t)(nparts_max + 1) * NBO);
   double* tvec = part + nparts_max * NBO;
@@ -1077,13 +1151,21 @@ int dense_cholesky_solve(cv_ctx* ctx, const float* gram, int64_t m, double mu, c
   launch_k(st, k_f2d, 256, 256, 0, rhs, r, m);
   tri_solve(v);
   for (int it = 0; it < 2; ++it) {
-    launch_k(st, k_row_residual, (int)((m + 7) / 8), 256, 0, gram, m, (float)mu, rhs, v, r);
+    // r = rhs - (Gram + mu I) v from the lower triangle only (row parts j <= i, then the
+    // transposed strictly-lower parts): the Gram's upper half is never read
+    cudaMemsetAsync(zz, 0, sizeof(double) * m, st);
+    launch_k(st, k_row_dot, (int)m, 256, 0, gram, m, (int64_t)0, (int64_t)0, (const double*)v, 1.0, zz,
+             (const int*)nullptr);
+    ctx->launches++;
+    col_dot(ctx, gram, m, (int)m, m, 0, 1, v, zz, cpart, nullptr);
+    launch_k(st, k_res_from, 256, 256, 0, rhs, (const double*)zz, (const double*)v, mu, m, r);
     tri_solve(dv);
     launch_k(st, k_axpy_d, 256, 256, 0, dv, v, m);
     ctx->launches += 2;
   }
   launch_k(st, k_d2f, 256, 256, 0, v, v_out, m);
   ctx->launches += 2;
+  ctx->pool.put(cpart);
   ctx->pool.put(part);
   ctx->pool.put(r);
   return 0;
@@ -1167,93 +1249,6 @@ __global__ void __launch_bounds__(256) k_strip_lower_add_diag(const float* src, 
     dst[i * ld + j] = j == r0 + i ? v + mu : v;
   }
 }
-// out[i] += sign * sum_{j < len_i} A[i, j] x[j], len_i = ncols (diag_off < 0) or
-// diag_off + i + 1 (the lower part of a Gram strip row); one 256-thread block per row,
-// 128-bit loads, two accumulators per thread, fixed-order block reduction
-__global__ void __launch_bounds__(256) k_row_dot(const float* A, int64_t lda, int64_t ncols, int64_t diag_off,
-                                                 const double* x, double sign, double* out, const int* skip) {
-  CV_PDL_ENTRY();
-  if (skip && *skip) return;
-  const int i = blockIdx.x;
-  const float* a = A + (int64_t)i * lda;
-  const int64_t len = diag_off < 0 ? ncols : diag_off + i + 1;
-  const bool vec = ((lda & 3) == 0) && !((uintptr_t)A & 15);
-  const int64_t n4 = vec ? (len & ~(int64_t)3) : 0;
-  double s0 = 0.0, s1 = 0.0;
-  int64_t j = (int64_t)threadIdx.x * 4;
-  for (; j + 1024 < n4; j += 2048) {
-    const float4 p = *reinterpret_cast<const float4*>(a + j);
-    const float4 q = *reinterpret_cast<const float4*>(a + j + 1024);
-    s0 += (double)p.x * x[j] + (double)p.y * x[j + 1] + (double)p.z * x[j + 2] + (double)p.w * x[j + 3];
-    s1 += (double)q.x * x[j + 1024] + (double)q.y * x[j + 1025] + (double)q.z * x[j + 1026] + (double)q.w * x[j + 1027];
-  }
-  for (; j < n4; j += 1024) {
-    const float4 p = *reinterpret_cast<const float4*>(a + j);
-    s0 += (double)p.x * x[j] + (double)p.y * x[j + 1] + (double)p.z * x[j + 2] + (double)p.w * x[j + 3];
-  }
-  for (int64_t t = n4 + threadIdx.x; t < len; t += 256) s1 += (double)a[t] * x[t];
-  double v[1] = {s0 + s1};
-  block_sum<1>(v);
-  if (threadIdx.x == 0) out[i] += sign * v[0];
-}
-// Column sums in row slices: part[y][j] = sum over rows i of slice y (i >= j - r0 + 1
-// when strict) of A[i, j] x[i], for j < ncols; k_col_reduce adds the slices in order.
-constexpr int CD_SLICES = 32;
-__global__ void __launch_bounds__(256) k_col_dot_part(const float* A, int64_t lda, int rows, int64_t ncols,
-                                                      int64_t r0, int strict, const double* x, double* part,
-                                                      const int* skip) {
-  CV_PDL_ENTRY();
-  if (skip && *skip) return;
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= ncols) return;
-  const int per = (rows + gridDim.y - 1) / gridDim.y;
-  int i0 = blockIdx.y * per;
-  const int i1 = min(rows, i0 + per);
-  if (strict && j - r0 + 1 > i0) i0 = (int)(j - r0 + 1 < (int64_t)i1 ? j - r0 + 1 : (int64_t)i1);
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  int i = i0;
-  for (; i + 4 <= i1; i += 4)
-#pragma unroll
-    for (int u = 0; u < 4; ++u) acc[u] += (double)A[(int64_t)(i + u) * lda + j] * x[i + u];
-  for (; i < i1; ++i) acc[0] += (double)A[(int64_t)i * lda + j] * x[i];
-  part[(int64_t)blockIdx.y * ncols + j] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-}
-__global__ void k_col_reduce(const double* part, int slices, int64_t ncols, double* z, const int* skip) {
-  CV_PDL_ENTRY();
-  if (skip && *skip) return;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < ncols; j += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int y = 0; y < slices; ++y) s += part[(int64_t)y * ncols + j];
-    z[j] += s;
-  }
-}
-__global__ void k_sub_d(const double* y, const double* z, int n, double* t) {
-  CV_PDL_ENTRY();
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) t[i] = y[i] - z[i];
-}
-// r = rhs - (u + mu v)
-__global__ void k_res_from(const float* rhs, const double* u, const double* v, double mu, int64_t m, double* r) {
-  CV_PDL_ENTRY();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-    r[i] = (double)rhs[i] - (u[i] + mu * v[i]);
-}
-__global__ void k_flag_d(const int* flag, double* out) {
-  CV_PDL_ENTRY();
-  *out = *flag ? 1.0 : 0.0;
-}
-
-// z[j] += sum_i A[i, j] x[i] over a row block of a strip layout (ld m); strict: only
-// the strictly-lower part (rows with r0 + i > j).  part: CD_SLICES x ncols doubles.
-static void col_dot(cv_ctx* ctx, const float* A, int64_t m, int rows, int64_t ncols, int64_t r0, int strict,
-                    const double* x, double* z, double* part, const int* skip) {
-  const int slices = std::min(CD_SLICES, std::max(1, rows / 32));
-  launch_k(ctx->stream, k_col_dot_part, dim3((unsigned)((ncols + 255) / 256), (unsigned)slices), 256, 0, A, m, rows,
-           ncols, r0, strict, x, part, skip);
-  launch_k(ctx->stream, k_col_reduce, (int)std::min<int64_t>(1024, (ncols + 255) / 256), 256, 0, (const double*)part,
-           slices, ncols, z, skip);
-  ctx->launches += 2;
-}
-
 // The rank's Gram row strips (block-cyclic 1024-row panels), built from the snapshot.
 static std::vector<GramStrip> build_strips(cv_ctx* ctx, cv_snap* s, float* gram) {
   constexpr int NBO = TT_MAX;
