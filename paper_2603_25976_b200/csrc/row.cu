@@ -1081,10 +1081,11 @@ int dense_cholesky_solve(cv_ctx* ctx, const float* gram, int64_t m, double mu, c
     };
     // (4a) the next panel's diagonal block
     update(nx, nb1, nb1, 0, 0);
-    // look ahead only while the rest of the update outlasts the diagonal work (~1 ms on the
-    // reserved SMs); the last panels' small updates run on every SM
+    // look ahead while the rest of the update is long enough that overlapping it with the
+    // diagonal work (~0.7 ms on the reserved SMs) beats giving it every SM (measured at C4:
+    // threshold 1.0 ms -> 126.9 ms/step, 0.3 ms -> 123.9, 0 -> 124.2)
     const double rows = (double)(rest2 - nb1), upd_ms = rows * ((double)rest2 - 0.5 * rows) * 2.0 * nbo / 4.5e11;
-    if (rest2 > nb1 && upd_ms > 1.0 && ctx->sm_count > 4 * kReserveSMs) {
+    if (rest2 > nb1 && upd_ms > 0.3 && ctx->sm_count > 4 * kReserveSMs) {
       // (4b) its factorization beside (4c) the rest of the update: rows below it, columns
       // from it on (the lower part relative to the shifted diagonal)
       cudaStream_t side = side_fork(ctx);
