@@ -1,0 +1,13 @@
+set -x
+mkdir -p gpurun_out/final
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > gpurun_out/final/gpu.txt
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -5 > gpurun_out/final/gputest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final/smoke.log 2>&1
+timeout 900 python bench.py > gpurun_out/final/bench_c3.log 2>&1
+timeout 900 python bench.py --impl reference > gpurun_out/final/bench_ref.log 2>&1
+timeout 900 python bench.py --config c4 --steps 5 --warmup 3 > gpurun_out/final/bench_c4.log 2>&1
+timeout 900 python bench.py --config c5 --steps 3 --warmup 3 > gpurun_out/final/bench_c5.log 2>&1
+timeout 900 python bench.py --config cadence --steps 300 --warmup 3 > gpurun_out/final/bench_cad.log 2>&1
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29555 bench.py --gpus 1 --steps 10 --warmup 3 > gpurun_out/final/bench_torchrun1.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/final/c3_launches.csv python bench.py --steps 5 --warmup 3 --no-cpu > /dev/null 2>&1
+tail -n 2 gpurun_out/final/*.log
