@@ -220,10 +220,22 @@ CV_DEV bool epi_applyV(const Epilogue& e, const EpiRt& rt, int m, int nb, const 
       // accumulation: one fire-and-forget vector reduction per 16 bytes (the L2 does the
       // read-modify-write; each element gets exactly one add per GEMM, so the result is
       // the same rounding as load + add + store, without the read round trip in the SM)
+      // the example of column nb + j: one division per chunk, then a running (q, r) --
+      // a division per element made the epilogue of the K = 16 output-layer term the
+      // bottleneck of that GEMM
+      int q = nb / e.kdiv, r = nb - q * e.kdiv;
+      float f[NC];
+#pragma unroll
+      for (int j = 0; j < NC; ++j) {
+        f[j] = v[j] * sa[q];
+        if (++r == e.kdiv) {
+          r = 0;
+          ++q;
+        }
+      }
 #pragma unroll
       for (int j = 0; j < NC; j += 4) {
-        const float4 c = make_float4(v[j] * sa[(nb + j) / e.kdiv], v[j + 1] * sa[(nb + j + 1) / e.kdiv],
-                                     v[j + 2] * sa[(nb + j + 2) / e.kdiv], v[j + 3] * sa[(nb + j + 3) / e.kdiv]);
+        const float4 c = make_float4(f[j], f[j + 1], f[j + 2], f[j + 3]);
         if (e.first) *reinterpret_cast<float4*>(out + j) = c;
         else red_add_v4(out + j, c);
       }
