@@ -755,8 +755,15 @@ def _rank_main(args):
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        if os.environ.get("CURVOPT_BENCH_SHARED_GPU") == "1":
+            # test hook: every rank on cuda:0 over gloo (the library's host communicator) --
+            # the multi-rank bench flow on a one-GPU box; numbers from it are not bench values
+            os.environ["LOCAL_RANK"] = "0"
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+            dist.init_process_group("nccl")
     try:
         if args.config == "cadence":
             run_cadence(args, rank, world)
