@@ -833,7 +833,16 @@ __global__ void __launch_bounds__(256) k_tri_wgemv(const float* W, int nbo, int 
   const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (i >= nbo) return;
   double s = 0.0;
-  for (int j = lane; j <= i; j += 32) s += (double)W[(int64_t)i * nbo + j] * r[p0 + j];
+  const float* w = W + (int64_t)i * nbo;
+  if ((nbo & 3) == 0) {  // 128-bit rows (W is stored with explicit zeros above the diagonal)
+    for (int j = lane * 4; j <= i; j += 128) {
+      const float4 q = *reinterpret_cast<const float4*>(w + j);
+      const double* rr = r + p0 + j;
+      s += (double)q.x * rr[0] + (double)q.y * rr[1] + (double)q.z * rr[2] + (double)q.w * rr[3];
+    }
+  } else {
+    for (int j = lane; j <= i; j += 32) s += (double)w[j] * r[p0 + j];
+  }
   s = warp_sum(s);
   if (lane == 0) y[p0 + i] = s;
 }
@@ -863,7 +872,15 @@ __global__ void __launch_bounds__(256) k_tri_wtgemv(const float* Wt, int nbo, in
   const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (j >= nbo) return;
   double s = 0.0;
-  for (int i = j + lane; i < nbo; i += 32) s += (double)Wt[(int64_t)j * nbo + i] * t[i];
+  const float* w = Wt + (int64_t)j * nbo;
+  if ((nbo & 3) == 0) {  // 128-bit rows from the aligned start (W^T has zeros left of the diagonal)
+    for (int i = (j & ~3) + lane * 4; i < nbo; i += 128) {
+      const float4 q = *reinterpret_cast<const float4*>(w + i);
+      s += (double)q.x * t[i] + (double)q.y * t[i + 1] + (double)q.z * t[i + 2] + (double)q.w * t[i + 3];
+    }
+  } else {
+    for (int i = j + lane; i < nbo; i += 32) s += (double)w[i] * t[i];
+  }
   s = warp_sum(s);
   if (lane == 0) x[p0 + j] = s;
 }
