@@ -348,9 +348,11 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def product_traffic():
-    """DRAM bytes of one GGN product from the committed ncu --set full capture, or None."""
-    for name in ("r2_product_traffic.json", "r1d_product_traffic.json"):
+def product_traffic(key="c3"):
+    """DRAM bytes of one product (C3 GGN / C5 HVP) from the committed ncu --set full
+    capture, or None."""
+    names = {"c3": ("r2_product_traffic.json", "r1d_product_traffic.json"), "c5": ("r2_c5_hvp_traffic.json",)}
+    for name in names.get(key, ()):
         try:
             with open(os.path.join(ROOT, "profiles", name)) as f:
                 return float(json.load(f)["dram_bytes_per_product"]), name
@@ -708,7 +710,7 @@ def run_ours(args, rank, world):
         achieved = flops / (gv_ms * 1e-3) / 1e12
         unit_note = (f"one {'HVP' if kind else 'GGN'} product at b={bl}: {flops / 1e9:.1f} GFLOP useful, "
                      f"{gv_ms:.3f} ms avg over {n_gv} (CUDA events)")
-        traffic, tsrc = product_traffic() if wl.key == "c3" else (None, None)
+        traffic, tsrc = product_traffic(wl.key)
 
     if rank != 0:
         return

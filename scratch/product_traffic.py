@@ -3,6 +3,7 @@ kernels: sums dram__bytes_read.sum + dram__bytes_write.sum and gpu__time_duratio
 over the product's launches and writes profiles/<name>.json (read by bench.py)."""
 import csv, json, sys
 src, out = sys.argv[1], sys.argv[2]
+unit = sys.argv[3] if len(sys.argv) > 3 else "one GGN product, C3 784-1024-1024-10, b=8192"
 rows = list(csv.reader([l for l in open(src) if l.startswith('"')]))
 hdr = rows[0]
 units = rows[1] if rows[1] and rows[1][0] == "" else None
@@ -19,7 +20,7 @@ for r in data:
                  "tensor_pipe_pct": f(r, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active")
                  if "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active" in col else None})
 tot = sum(k["dram_read_B"] + k["dram_write_B"] for k in kern)
-json.dump({"unit_of_work": "one GGN product, C3 784-1024-1024-10, b=8192",
+json.dump({"unit_of_work": unit,
            "source": f"ncu --set full --clock-control none (cold-cache replay per kernel), {src}",
            "dram_bytes_per_product": tot, "kernels": kern}, open(out, "w"), indent=1)
 print(f"{len(kern)} kernels, DRAM {tot / 1e6:.1f} MB per product")
