@@ -1345,23 +1345,23 @@ int dist_row_cholesky(cv_ctx* ctx, cv_snap* s, double mu, const float* rhs, floa
     bufs.push_back(q);
     return q;
   };
-  float* gram = (float*)get(sizeof(float) * (size_t)(lrows * m));
-  float* chol = (float*)get(sizeof(float) * (size_t)(lrows * m));
-  float* dinv = (float*)get(sizeof(float) * (size_t)(((m + CH_NB - 1) / CH_NB) * CH_NB * CH_NB));
-  float* winv = (float*)get(sizeof(float) * (size_t)(2 * (int64_t)np * NBO * NBO));
-  float* winvT = winv + (int64_t)np * NBO * NBO;
-  float* gbuf = (float*)get(sizeof(float) * (size_t)(m * NBO));
-  __half* gh = (__half*)get(sizeof(__half) * (size_t)(m * NBO));
-  __half* gl = (__half*)get(sizeof(__half) * (size_t)(m * NBO));
-  __half* ah = (__half*)get(sizeof(__half) * (size_t)(lrows * NBO));
-  __half* al = (__half*)get(sizeof(__half) * (size_t)(lrows * NBO));
-  __half* wh = (__half*)get(sizeof(__half) * (size_t)NBO * NBO);
-  __half* wl = (__half*)get(sizeof(__half) * (size_t)NBO * NBO);
-  float* Lblk = (float*)get(sizeof(float) * (size_t)NBO * NBO);
-  Scale* sc = (Scale*)get(sizeof(Scale) * 4);
-  double* vecs = (double*)get(sizeof(double) * (size_t)(6 * m + 8));
   int rc = 0;
   try {
+    float* gram = (float*)get(sizeof(float) * (size_t)(lrows * m));
+    float* chol = (float*)get(sizeof(float) * (size_t)(lrows * m));
+    float* dinv = (float*)get(sizeof(float) * (size_t)(((m + CH_NB - 1) / CH_NB) * CH_NB * CH_NB));
+    float* winv = (float*)get(sizeof(float) * (size_t)(2 * (int64_t)np * NBO * NBO));
+    float* winvT = winv + (int64_t)np * NBO * NBO;
+    float* gbuf = (float*)get(sizeof(float) * (size_t)(m * NBO));
+    __half* gh = (__half*)get(sizeof(__half) * (size_t)(m * NBO));
+    __half* gl = (__half*)get(sizeof(__half) * (size_t)(m * NBO));
+    __half* ah = (__half*)get(sizeof(__half) * (size_t)(lrows * NBO));
+    __half* al = (__half*)get(sizeof(__half) * (size_t)(lrows * NBO));
+    __half* wh = (__half*)get(sizeof(__half) * (size_t)NBO * NBO);
+    __half* wl = (__half*)get(sizeof(__half) * (size_t)NBO * NBO);
+    float* Lblk = (float*)get(sizeof(float) * (size_t)NBO * NBO);
+    Scale* sc = (Scale*)get(sizeof(Scale) * 4);
+    double* vecs = (double*)get(sizeof(double) * (size_t)(6 * m + 8));
     // Gram strips of my panels, then chol = their lower part + mu I
     const std::vector<GramStrip> strips = build_strips(ctx, s, gram);
     for (const GramStrip& g : strips) {
