@@ -89,7 +89,22 @@ __global__ void __launch_bounds__(SP_NT) k_flat_amax(const float* __restrict__ x
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = base + tid; i < base + (lead < n ? lead : n); i += nth) take(i, x[i]);
   const int64_t q0 = (base + lead) / 4, q1 = (base + n) / 4;
-  for (int64_t q = q0 + tid; q < q1; q += nth) {
+  int64_t q = q0 + tid;
+  // four 16-byte loads in flight per thread (one left HBM at half its bandwidth)
+  for (; q + 3 * nth < q1; q += 4 * nth) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = *reinterpret_cast<const float4*>(x + 4 * (q + u * nth));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = 4 * (q + u * nth);
+      take(i, v[u].x);
+      take(i + 1, v[u].y);
+      take(i + 2, v[u].z);
+      take(i + 3, v[u].w);
+    }
+  }
+  for (; q < q1; q += nth) {
     const float4 v = *reinterpret_cast<const float4*>(x + 4 * q);
     take(4 * q, v.x);
     take(4 * q + 1, v.y);
