@@ -61,7 +61,8 @@ struct TcArgs {
   const int* skip;
   int lower_only;
   int cyc_nb, cyc_skip;
-  int tma_out;        // 0: per-thread stores; 1: fp16 split pair via TMA; 2: fp32 (out or partial) via TMA
+  int tma_out;        // 0: per-thread stores; 1: fp16 split pair via TMA; 2: fp32 (out or partial) via TMA;
+                      // 3: fp32 reduce-add via TMA (accumulating Gram / trailing updates)
   float* partial;     // split-K partials (nullptr: apply the epilogue directly)
   int tiles_m, tiles_n, splits;
 };
@@ -239,6 +240,13 @@ CV_DEV void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1
 CV_DEV void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
                "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+// element-wise fp32 add of a staged sub-tile into global memory (the L2 does the
+// read-modify-write, one add per element: the accumulating Gram / trailing updates)
+CV_DEV void tma_reduce_add_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
                : "memory");
 }
 CV_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
@@ -564,7 +572,22 @@ CV_DEV void tile_epilogue_tma(const TcArgs& a, const TcMaps& maps, const EpiRt& 
         bulk_commit();
       }
     } else {
-      // ---- fp32 output / split-K partial: 32 rows x 64 B, SWIZZLE_64B ----
+      // ---- fp32 output / split-K partial / Gram / accumulation: 32 rows x 64 B, SWIZZLE_64B ----
+      if (e.mode == EPI_GRAM && m < a.M) {  // Hadamard factor of the (row, column) examples
+        const float* sa = e.sa + (int64_t)((m + e.row0) / e.kdiv) * e.sa_ld;
+        int qe = nb / e.kdiv, re = nb - qe * e.kdiv;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          v[j] *= sa[qe];
+          if (++re == e.kdiv) {
+            re = 0;
+            ++qe;
+          }
+        }
+      } else if (e.mode == EPI_ACCUM) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] *= e.alpha;
+      }
       if (lane == 0) bulk_wait_read0();
       __syncwarp();
       const int sw = (lane >> 1) & 3;
@@ -576,6 +599,7 @@ CV_DEV void tile_epilogue_tma(const TcArgs& a, const TcMaps& maps, const EpiRt& 
       __syncwarp();
       if (lane == 0) {
         if (a.partial) tma_store_3d(&maps.o[0], stg, nb, r0, split);
+        else if (a.tma_out == 3) tma_reduce_add_2d(&maps.o[0], stg, nb, r0);
         else tma_store_2d(&maps.o[0], stg, nb, r0);
         bulk_commit();
       }
@@ -1117,8 +1141,14 @@ static CUtensorMap make_out_map(const void* ptr, int fp16, int64_t cols, int64_t
 // The TMA-store epilogue a GEMM's output allows without split-K partials:
 // 0 none (per-thread stores), 1 fp16 split pair, 2 fp32 (mirrors setup_out).
 static int tma_out_mode(const GemmArgs& g) {
-  if (g.lower_only) return 0;
   const Epilogue& e = g.epi;
+  if (e.mode == EPI_GRAM || e.mode == EPI_ACCUM) {
+    // whole computed tiles are written (lower-only GEMMs: also the part of a diagonal tile
+    // above the diagonal, which the row lane never reads)
+    if ((e.ld & 3) || !aligned16(e.out)) return 0;
+    return e.mode == EPI_GRAM && e.first ? 2 : 3;
+  }
+  if (g.lower_only) return 0;
   if (e.mode == EPI_STORE) return ((e.ld & 3) || !aligned16(e.out)) ? 0 : 2;
   const bool relu_mask = (e.mode == EPI_SPLIT_MASK || e.mode == EPI_HVP) && e.act == CV_ACT_RELU && !e.raw &&
                          e.mask_div == 1 && (e.mask_ld & 7) == 0 && aligned16(e.mask_hi);
@@ -1130,8 +1160,15 @@ static int tma_out_mode(const GemmArgs& g) {
 // Choose the TMA-store epilogue when the mode and layout allow it.
 static void setup_out(const GemmArgs& g, TcMaps& maps, TcArgs& a, float* partial, int splits) {
   a.tma_out = 0;
-  if (g.lower_only) return;
   const Epilogue& e = g.epi;
+  if (!partial && (e.mode == EPI_GRAM || e.mode == EPI_ACCUM)) {
+    const int mode = tma_out_mode(g);
+    if (!mode) return;
+    maps.o[0] = make_out_map(e.out, 0, g.N, g.M, 0, e.ld);
+    a.tma_out = mode;
+    return;
+  }
+  if (g.lower_only) return;
   if (partial) {
     if ((g.N & 3) || !aligned16(partial)) return;
     maps.o[0] = make_out_map(partial, 0, g.N, g.M, splits, g.N);
