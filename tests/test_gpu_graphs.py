@@ -59,3 +59,36 @@ def test_graph_replay_bitwise_equals_eager(which):
     assert ng >= 1, "no step was replayed from a graph"
     assert _same(re, rg)
     assert np.array_equal(we, wg)
+
+
+def test_graph_cache_is_bounded_and_evictions_stay_exact():
+    """Six batch shapes in rotation (six graph keys) against a cache of four graphs: the
+    least recently used graphs are released and recaptured, and the trajectory is still
+    bitwise the eager one."""
+    model = P.Model(784, (256, 128), 10, "relu")
+    sizes = (128, 192, 256, 320, 384, 448)
+    batches = [tuple(torch.from_numpy(np.asarray(a)).cuda() for a in O.synthetic_batch(n, 784, 10, seed=1 + i))
+               for i, n in enumerate(sizes)]
+    cg = P.CgConfig(tol=1e-5, maxiter=4, warm_start=False)
+    spec = P.MethodSpec(curvature=P.CurvatureSpec("ggn_ce"), solver=P.SolverSpec("cg", cg),
+                        damping=P.DampingSpec("constant", 1.0), chain=(P.transforms.scale(-1e-3),))
+
+    def run(graphs):
+        meth = P.assemble(spec, model)
+        meth.graphs = graphs
+        w = P.init_params(model, P.Rng(0)).to_device()
+        st = meth.init(w, 0)
+        rows, live = [], 0
+        for t in range(3 * len(sizes) * 2):
+            X, y = batches[(t // 2) % len(sizes)]  # each shape twice in a row: seen, then captured
+            w, st, info = meth.step(w, P.Batch(X, y, "ce"), st)
+            rows.append(info.to_row())
+            live = max(live, sum(1 for g in meth._graph_cache.values() if g))
+        meth.release_graphs()
+        return np.array(rows, dtype=np.float64), w.data.cpu().numpy(), live
+
+    re, we, _ = run(False)
+    rg, wg, live = run(True)
+    assert 1 <= live <= P.method.Method._MAX_GRAPHS
+    assert _same(re, rg)
+    assert np.array_equal(we, wg)
