@@ -35,7 +35,7 @@ if world > 1:
     dist.init_process_group("gloo", rank=rank, world_size=world)
 case = os.environ["CASE"]
 b = 1024
-bl = b // world
+lo, hi = rank * b // world, (rank + 1) * b // world  # uneven shards when world does not divide b
 if case == "pcg_tr":
     m = P.Model(784, (256, 256), 10, "tanh")
     meth = P.make("sgn_ce", m, solver={"cg": {"maxiter": 10}}, precond={"kind": "diag_ema"},
@@ -61,8 +61,7 @@ for t in range(3):
     kind = "ce"
     if case == "egn_mse_cg":  # regression targets for the mse lane
         kind, y = "mse", np.eye(10)[y] * 0.5 + 0.01 * X[:, :10]
-    batch = P.Batch(X[rank * bl:(rank + 1) * bl], y[rank * bl:(rank + 1) * bl], kind, global_size=b,
-                    row_offset=rank * bl)
+    batch = P.Batch(X[lo:hi], y[lo:hi], kind, global_size=b, row_offset=lo)
     w, st, info = meth.step(w, batch, st)
     rows.append(info.to_row())
 rt = runtime()
@@ -133,3 +132,29 @@ def test_two_ranks_on_one_gpu_match_the_full_batch(case, shard, tmp_path):
     if shard == "1":  # the sharded loop ran: its totals and all-gathers add collectives
         plain = _run(case, 2, tmp_path, {"CURVOPT_SHARD_CG": "0"})
         assert ranks[0]["host_comm_calls"] > plain[0]["host_comm_calls"]
+
+
+@pytest.mark.parametrize("case,shard", [("egn_ce", "0"), ("pcg_tr", "1")])
+def test_three_uneven_ranks_match_the_full_batch(case, shard, tmp_path):
+    """World 3 on one GPU: uneven shards (341/341/342 rows), the distributed row lane's 10
+    panels dealt 4/3/3, sharded CG vectors with a ragged last chunk."""
+    import paper_2603_25976_b200 as P
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    full = _run(case, 1, tmp_path)[0]
+    ranks = _run(case, 3, tmp_path, {"CURVOPT_SHARD_CG": shard})
+    ref = np.array(full["rows"], dtype=np.float64)
+    for res in ranks:
+        mine = np.array(res["rows"], dtype=np.float64)
+        assert np.array_equal(np.isnan(mine), np.isnan(ref))
+        for j, f in enumerate(P.STEP_INFO_FIELDS):
+            ok = ~np.isnan(ref[:, j])
+            if f in ("solver_iterations", "solver_converged", "step_index"):
+                assert np.array_equal(mine[ok, j], ref[ok, j]), f
+            else:
+                np.testing.assert_allclose(mine[ok, j], ref[ok, j], rtol=1e-4 if f in TIGHT else 1e-3, atol=1e-9,
+                                           err_msg=f)
+        w, wf = np.array(res["w"]), np.array(full["w"])
+        assert np.linalg.norm(w - wf) / np.linalg.norm(wf) < 1e-4
+    assert ranks[0]["w"] == ranks[1]["w"] == ranks[2]["w"]
