@@ -666,6 +666,307 @@ __global__ void k_cg_pnext(const float* r, const float* pre, float lam, float fl
   for (int64_t i = 4 * nq + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = minv_of(pre, i, lam, floor_) * r[i] + beta * p[i];
 }
+// ---------------------------------------------------------------------------
+// One plain (non-stabilising) (P)CG iteration after its product, in ONE launch
+// (solvers.py:90-113): pap -> alpha -> x, r update -> beta -> next direction ->
+// its per-layer scales -> the next product's input split.  The four dependent
+// reductions are separated by grid barriers instead of kernel boundaries; the
+// grid is the reduction grid (NB blocks x NT threads, 4 per SM, co-resident by
+// cooperative launch) and each thread keeps its <= CGF_MAXQ 16-byte groups of p
+// and Ap (then z) in registers across the barriers, so the pass reads p, Ap, x, r,
+// M and writes x, r, p and the split once: 9 d-vectors instead of the 16 of the
+// four separate kernels, and no per-kernel launch / last-block tails.  The
+// reductions are the separate kernels' (fixed-order fp64 block partials summed by
+// the barrier's last block, which also takes the control decision); every block
+// then reads the decided scalars.
+// ---------------------------------------------------------------------------
+constexpr int CGF_MAXQ = 4;
+struct CgFusedArgs {
+  float* x;
+  float* r;
+  float* p;
+  const float* ap;
+  const float* pre;
+  float lam, floor_;
+  CgDev* st;
+  int64_t d;
+  double* ws;
+  unsigned* bar;  // [0] arrivals, [1] generation
+  int k, maxiter;
+  double tol;
+  OffTab t;
+  float* part;  // NB x kOffTabMax block maxima
+  Scale* sc;
+  Scale* zero_sc;
+  int n_zero;
+  __half* hi;
+  __half* lo;
+};
+
+// Grid barrier whose last arriving block runs fin() (all its threads) before it
+// releases the others; then thread 0 of every block runs post() (reads of the
+// decided scalars into shared memory: one L2 request per block, not per warp).
+// The arrival counter and the generation word sit on separate 128-byte lines.  A
+// bounded spin: a grid that is not co-resident traps instead of hanging the device.
+template <typename F, typename G>
+CV_DEV void grid_sync_last(unsigned* bar, F&& fin, G&& post) {
+  __shared__ unsigned s_last, s_gen;
+  unsigned* genp = bar + 32;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_gen = *(volatile unsigned*)genp;
+    __threadfence();
+    s_last = atomicAdd(bar, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    fin();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(genp, 1u);
+    }
+  } else if (threadIdx.x == 0) {
+    unsigned spins = 0, g;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(genp) : "memory");
+      if (++spins > (1u << 26)) __trap();
+    } while (g == s_gen);
+  }
+  if (threadIdx.x == 0) post();
+  __syncthreads();
+}
+
+template <int NQ>
+__global__ void __launch_bounds__(NT, 4) k_cg_fused(CgFusedArgs a) {
+  CV_PDL_ENTRY();
+  volatile CgDev* vst = a.st;
+  __shared__ int s_done;
+  __shared__ float s_val;
+  if (threadIdx.x == 0) s_done = vst->done;
+  __syncthreads();
+  if (s_done) return;  // nothing writes the flag before the first barrier
+  const int64_t tid = blockIdx.x * (int64_t)NT + threadIdx.x, nth = (int64_t)gridDim.x * NT;
+  const int64_t nq = a.d >> 2;
+  const int64_t it = 4 * nq + tid;  // scalar tail element of this thread (d % 4 threads)
+  const bool has_t = it < a.d;
+  float4 P[NQ], A[NQ];
+  float pt = 0.f, at = 0.f;
+  const float lam = a.lam;
+  auto read_decision = [&] {
+    s_done = vst->done;
+    s_val = (float)vst->alpha;  // alpha after the pap decision, beta after the residual decision
+  };
+
+  // (1) Ap += lam p; partials p.Ap, max|p|, #nonfinite(p)  (k_cg_pap)
+  {
+    double t[3] = {0.0, 0.0, 0.0};
+    double mx = 0.0;
+    auto body = [&](float pi, float& ai) {
+      ai += lam * pi;
+      t[0] += (double)pi * ai;
+      t[2] += isfinite(pi) ? 0.0 : 1.0;
+      mx = fmax(mx, (double)fabsf(pi));
+    };
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {
+      const int64_t q = tid + j * nth;
+      if (q < nq) {
+        P[j] = ld4g(a.p + 4 * q);
+        A[j] = ld4g(a.ap + 4 * q);
+        body(P[j].x, A[j].x); body(P[j].y, A[j].y); body(P[j].z, A[j].z); body(P[j].w, A[j].w);
+      }
+    }
+    if (has_t) {
+      pt = a.p[it];
+      at = a.ap[it];
+      body(pt, at);
+    }
+    write_partials<3>(a.ws, t);
+    __shared__ double smx[NT / 32];
+    mx = warp_max_d(mx);
+    if ((threadIdx.x & 31) == 0) smx[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double m = 0.0;
+      for (int w = 0; w < NT / 32; ++w) m = fmax(m, smx[w]);
+      a.ws[blockIdx.x * 8 + 1] = m;
+    }
+    grid_sync_last(a.bar, [&] { pap_final_body(a.ws, a.st, a.k, 0); }, read_decision);
+  }
+  if (s_done) return;
+
+  // (2) x += alpha p; r -= alpha Ap; z = M^-1 r; partials ||r||^2, r.z  (k_cg_update)
+  //     and the per-layer max|z|: with the current direction's published bound
+  //     amax_l >= max|p_l|, B_l = max|z_l| + |beta| amax_l bounds the next direction,
+  //     so its split exponent is known at this barrier (no third reduction; the
+  //     exponent is the exact-amax one or one binade below it).
+  const OffTab& T = a.t;
+  __shared__ int smax[kOffTabMax];
+  __shared__ float sscale[kOffTabMax];
+  if (threadIdx.x < kOffTabMax) smax[threadIdx.x] = 0;
+  {
+    const float al = s_val;
+    double t[2] = {0.0, 0.0};
+    int l = 0;
+    float m = 0.f;
+    auto take = [&](int64_t i, float v) {
+      if (i >= T.off[l + 1]) {
+        atomicMax(&smax[l], __float_as_int(m));
+        m = 0.f;
+        while (i >= T.off[l + 1]) ++l;
+      }
+      m = fmaxf(m, fabsf(v));
+    };
+    auto body = [&](int64_t i, float& xi, float& ri, float pi, float& ai, float mi) {
+      xi += al * pi;
+      ri -= al * ai;
+      const float z = mi * ri;
+      t[0] += (double)ri * ri;
+      t[1] += (double)ri * z;
+      ai = z;
+      take(i, z);
+    };
+    auto minv = [&](float m) { return 1.f / (fmaxf(m, a.floor_) + lam); };
+    __syncthreads();  // smax zeroed
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {
+      const int64_t q = tid + j * nth;
+      if (q < nq) {
+        const int64_t i = 4 * q;
+        float4 X = ld4g(a.x + i), R = ld4g(a.r + i);
+        float4 M = make_float4(1.f, 1.f, 1.f, 1.f);
+        if (a.pre) {
+          M = ld4g(a.pre + i);
+          M = make_float4(minv(M.x), minv(M.y), minv(M.z), minv(M.w));
+        }
+        body(i, X.x, R.x, P[j].x, A[j].x, M.x); body(i + 1, X.y, R.y, P[j].y, A[j].y, M.y);
+        body(i + 2, X.z, R.z, P[j].z, A[j].z, M.z); body(i + 3, X.w, R.w, P[j].w, A[j].w, M.w);
+        *reinterpret_cast<float4*>(a.x + i) = X;
+        *reinterpret_cast<float4*>(a.r + i) = R;
+      }
+    }
+    if (has_t) {
+      float xi = a.x[it], ri = a.r[it];
+      body(it, xi, ri, pt, at, a.pre ? minv(a.pre[it]) : 1.f);
+      a.x[it] = xi;
+      a.r[it] = ri;
+    }
+    atomicMax(&smax[l], __float_as_int(m));
+    write_partials<2>(a.ws, t);  // (its barriers also publish smax)
+    if (threadIdx.x < T.L) a.part[blockIdx.x * kOffTabMax + threadIdx.x] = __int_as_float(smax[threadIdx.x]);
+    __shared__ float sh[kOffTabMax][NT / 32];
+    grid_sync_last(
+        a.bar,
+        [&] {
+          r_final_body(a.ws, a.st, a.k, a.maxiter, 0, a.tol);
+          for (int l2 = 0; l2 < T.L; ++l2) {
+            float mm = 0.f;
+            for (int b = threadIdx.x; b < (int)gridDim.x; b += NT) mm = fmaxf(mm, __ldcg(a.part + b * kOffTabMax + l2));
+            mm = warp_max_f(mm);
+            if ((threadIdx.x & 31) == 0) sh[l2][threadIdx.x >> 5] = mm;
+          }
+          __syncthreads();
+          if (threadIdx.x == 0 && !a.st->done) {
+            const float beta = fabsf((float)a.st->alpha);
+            for (int l2 = 0; l2 < T.L; ++l2) {
+              float mz = 0.f;
+              for (int w = 0; w < NT / 32; ++w) mz = fmaxf(mz, sh[l2][w]);
+              const float B = mz + beta * a.sc[l2].amax;
+              a.sc[l2].amax = B;
+              a.sc[l2].e = exp_for_bound(B);
+            }
+          }
+          if (!a.st->done)
+            for (int i = threadIdx.x; i < a.n_zero; i += NT) {
+              a.zero_sc[i].e = 0;
+              a.zero_sc[i].amax = 0.f;
+            }
+        },
+        [&] {
+          read_decision();
+          if (!s_done)
+            for (int l2 = 0; l2 < T.L; ++l2) sscale[l2] = pow2f(((volatile Scale*)a.sc)[l2].e);
+        });
+  }
+  if (s_done) return;  // converged, failed, or k == maxiter: the direction is never used
+
+  // (3) p = z + beta p (solvers.py:111-112) and the next product's input split
+  {
+    const float beta = s_val;
+    int l = 0;
+    auto scale_at = [&](int64_t i) {
+      while (i >= T.off[l + 1]) ++l;
+      return sscale[l];
+    };
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {
+      const int64_t q = tid + j * nth;
+      if (q < nq) {
+        const int64_t i = 4 * q;
+        P[j].x = A[j].x + beta * P[j].x;
+        P[j].y = A[j].y + beta * P[j].y;
+        P[j].z = A[j].z + beta * P[j].z;
+        P[j].w = A[j].w + beta * P[j].w;
+        *reinterpret_cast<float4*>(a.p + i) = P[j];
+        union { uint2 u; __half h[4]; } H, L;
+        split16(P[j].x, scale_at(i), H.h[0], L.h[0]);
+        split16(P[j].y, scale_at(i + 1), H.h[1], L.h[1]);
+        split16(P[j].z, scale_at(i + 2), H.h[2], L.h[2]);
+        split16(P[j].w, scale_at(i + 3), H.h[3], L.h[3]);
+        *reinterpret_cast<uint2*>(a.hi + i) = H.u;
+        *reinterpret_cast<uint2*>(a.lo + i) = L.u;
+      }
+    }
+    if (has_t) {
+      pt = at + beta * pt;
+      a.p[it] = pt;
+      split16(pt, scale_at(it), a.hi[it], a.lo[it]);
+    }
+  }
+}
+
+// The fused iteration applies when every thread's share fits its registers and the
+// 16-byte / 8-byte vector accesses are aligned.
+static int cg_fused_nq(int64_t d, const OffTab& t, const void* x, const void* r, const void* p, const void* ap,
+                       const void* pre, const void* hi, const void* lo) {
+  if (t.L < 1 || t.L > kOffTabMax || t.off[0] != 0) return 0;
+  if (((uintptr_t)x | (uintptr_t)r | (uintptr_t)p | (uintptr_t)ap | (uintptr_t)pre) & 15) return 0;
+  if (((uintptr_t)hi | (uintptr_t)lo) & 7) return 0;
+  const int64_t nth = (int64_t)NB * NT;
+  const int64_t nq = (d >> 2) + nth - 1;
+  const int64_t q = nq / nth;
+  return q >= 1 && q <= CGF_MAXQ ? (int)q : (d > 0 && d < 4 ? 1 : 0);
+}
+
+static bool cg_fused_enabled() {
+  static const int on = !(getenv("CURVOPT_CG_FUSED") && getenv("CURVOPT_CG_FUSED")[0] == '0');
+  return on;
+}
+
+static void launch_cg_fused(cudaStream_t st, int nq, const CgFusedArgs& a) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(NB);
+  cfg.blockDim = dim3(NT);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = 1;
+  cfg.attrs = attr;
+  static const int coop = !(getenv("CURVOPT_CG_COOP") && getenv("CURVOPT_CG_COOP")[0] == '0');
+  cfg.numAttrs = coop ? 2 : 1;
+  switch (nq) {
+    case 1: cudaLaunchKernelEx(&cfg, k_cg_fused<1>, a); break;
+    case 2: cudaLaunchKernelEx(&cfg, k_cg_fused<2>, a); break;
+    case 3: cudaLaunchKernelEx(&cfg, k_cg_fused<3>, a); break;
+    default: cudaLaunchKernelEx(&cfg, k_cg_fused<4>, a); break;
+  }
+}
+
 __global__ void k_cg_finish(const CgDev* st, cv_cg_stats* out) {
   CV_PDL_ENTRY();
   out->relres = st->relres;
@@ -979,9 +1280,24 @@ static void cg_run(cv_ctx* ctx, const CgOperator& op, const float* g, double lam
   launch_k(sm, k_cg_p0_final, 1, NT, 0, ws, st);
   ctx->launches += 4;
   unsigned* ctr = ctx->amax_counter + 1;
+  CgFusedArgs fa{};
+  int fq = 0;
+  if (s && (int)s->off.size() <= kOffTabMax && cg_fused_enabled()) {
+    fa = CgFusedArgs{x, r, p, ap, precond, flam, ffl, st, d, ws, ctx->amax_counter + 16, 0, maxiter, tol,
+                     make_off_tab(s->off, d), ctx->amax_ws, s->v_sc, s->prod_sc, s->n_prod, s->v_hi, s->v_lo};
+    fq = cg_fused_nq(d, fa.t, x, r, p, ap, precond, s->v_hi, s->v_lo);
+  }
   for (int k = 1; k <= maxiter; ++k) {
     const int is_stab = (stab > 0 && k % stab == 0) ? 1 : 0;
     op.apply(ctx, p, ap, &st->done);
+    if (!is_stab && fq) {  // pap, update, direction, scales and split in one launch
+      fa.k = k;
+      launch_cg_fused(sm, fq, fa);
+      ctx->launches++;
+      if (k == maxiter) break;
+      s->v_ready = 2;
+      continue;
+    }
     launch_k(sm, k_cg_pap, NB, NT, 0, ap, p, flam, st, d, ws, ctr, k, is_stab);
     ctx->launches++;
     if (is_stab) {
