@@ -703,62 +703,143 @@ struct CgFusedArgs {
   __half* lo;
 };
 
-// Grid barrier whose last arriving block runs fin() (all its threads) before it
-// releases the others; then thread 0 of every block runs post() (reads of the
-// decided scalars into shared memory: one L2 request per block, not per warp).
-// The arrival counter and the generation word sit on separate 128-byte lines.  A
+// Grid barrier whose last arriving block runs fin() (all its threads: the
+// fixed-order reduction and the control decision) before it releases the others;
+// then thread 0 of every block runs post() (the decided scalars into shared memory:
+// one L2 request per block, not per warp).  The arrival counter and the generation
+// word sit on separate 128-byte lines; release/acquire at gpu scope (the block's
+// writes before the bar.sync are visible to every block after the barrier).  A
 // bounded spin: a grid that is not co-resident traps instead of hanging the device.
 template <typename F, typename G>
 CV_DEV void grid_sync_last(unsigned* bar, F&& fin, G&& post) {
-  __shared__ unsigned s_last, s_gen;
+  __shared__ unsigned s_last;
   unsigned* genp = bar + 32;
+  unsigned g = 0;
   __syncthreads();
   if (threadIdx.x == 0) {
-    s_gen = *(volatile unsigned*)genp;
-    __threadfence();
-    s_last = atomicAdd(bar, 1u) == gridDim.x - 1;
+    unsigned old;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(genp) : "memory");
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+    s_last = old == gridDim.x - 1;
   }
   __syncthreads();
   if (s_last) {
-    __threadfence();
     fin();
     __syncthreads();
     if (threadIdx.x == 0) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(genp, 1u);
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(genp) : "memory");
     }
   } else if (threadIdx.x == 0) {
-    unsigned spins = 0, g;
+    unsigned spins = 0, now;
     do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(genp) : "memory");
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(now) : "l"(genp) : "memory");
       if (++spins > (1u << 26)) __trap();
-    } while (g == s_gen);
+    } while (now == g);
   }
   if (threadIdx.x == 0) post();
   __syncthreads();
 }
 
+// Fixed-order sums of the NV partials at slots [off, off + NV) of every block (as
+// sum_partials), all loads issued before the adds; result valid in thread 0.
+template <int NV>
+CV_DEV void sum_slots(const double* ws, int off, double (&t)[NV]) {
+  constexpr int U = (NB + NT - 1) / NT;
+  double v[U][NV];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int b = threadIdx.x + u * NT;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) v[u][j] = b < NB ? __ldcg(ws + b * 8 + off + j) : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    t[j] = 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) t[j] += v[u][j];
+  }
+  block_sum<NV>(t);
+}
+CV_DEV double max_slot(const double* ws, int off) {
+  constexpr int U = (NB + NT - 1) / NT;
+  double m = 0.0;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int b = threadIdx.x + u * NT;
+    if (b < NB) m = fmax(m, __ldcg(ws + b * 8 + off));
+  }
+  __shared__ double smx[NT / 32];
+  m = warp_max_d(m);
+  if ((threadIdx.x & 31) == 0) smx[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int w = 0; w < NT / 32; ++w) m = fmax(m, smx[w]);
+  __syncthreads();
+  return m;  // valid in thread 0
+}
+
+// Running per-layer max of a thread's increasing indices, folded into shared
+// memory when the layer changes (at most L times per thread).
+struct LayerMax {
+  const OffTab& T;
+  int* smax;
+  int l = 0;
+  float m = 0.f;
+  CV_DEV void take4(int64_t i, const float4& v) {
+    if (i + 3 < T.off[l + 1]) {  // the whole group in the current layer (the common case)
+      m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+      return;
+    }
+    take(i, v.x); take(i + 1, v.y); take(i + 2, v.z); take(i + 3, v.w);
+  }
+  CV_DEV void take(int64_t i, float v) {
+    if (i >= T.off[l + 1]) {
+      atomicMax(&smax[l], __float_as_int(m));
+      m = 0.f;
+      while (i >= T.off[l + 1]) ++l;
+    }
+    m = fmaxf(m, fabsf(v));
+  }
+  CV_DEV void flush() { atomicMax(&smax[l], __float_as_int(m)); }
+};
+
+// red_ws slots of the fused iteration (8 per block): 0-2 pap (p.Ap, max|p|,
+// #nonfinite), 3-4 residual (||r||^2, r.z) -- disjoint, so a fast block's residual
+// partials never overwrite pap partials a slow block is still reducing.
 template <int NQ>
 __global__ void __launch_bounds__(NT, 4) k_cg_fused(CgFusedArgs a) {
   CV_PDL_ENTRY();
-  volatile CgDev* vst = a.st;
   __shared__ int s_done;
-  __shared__ float s_val;
-  if (threadIdx.x == 0) s_done = vst->done;
+  __shared__ float s_val;  // alpha after the pap decision, beta after the residual decision
+  __shared__ float s_amax[kOffTabMax], sscale[kOffTabMax];
+  __shared__ int smax[kOffTabMax];
+  // this thread's groups of p and Ap (then z) across the barriers: shared memory
+  // (32 KB per block at NQ = 4), so the registers carry the loads in flight
+  __shared__ float4 sP[NQ][NT], sA[NQ][NT];
+  const OffTab& T = a.t;
+  volatile CgDev* vst = a.st;
+  if (threadIdx.x == 0) s_done = vst->done;  // nothing writes the flag before the first barrier
+  if (threadIdx.x < T.L) s_amax[threadIdx.x] = a.sc[threadIdx.x].amax;  // bound of the current direction
+  if (threadIdx.x < kOffTabMax) smax[threadIdx.x] = 0;
   __syncthreads();
-  if (s_done) return;  // nothing writes the flag before the first barrier
+  if (s_done) return;
+  auto read_decision = [&] {
+    s_done = vst->done;
+    s_val = (float)vst->alpha;
+  };
   const int64_t tid = blockIdx.x * (int64_t)NT + threadIdx.x, nth = (int64_t)gridDim.x * NT;
   const int64_t nq = a.d >> 2;
   const int64_t it = 4 * nq + tid;  // scalar tail element of this thread (d % 4 threads)
   const bool has_t = it < a.d;
-  float4 P[NQ], A[NQ];
+  const int tx = threadIdx.x;
   float pt = 0.f, at = 0.f;
   const float lam = a.lam;
-  auto read_decision = [&] {
-    s_done = vst->done;
-    s_val = (float)vst->alpha;  // alpha after the pap decision, beta after the residual decision
-  };
+  const float* __restrict__ gp = a.p;
+  const float* __restrict__ gap = a.ap;
+  const float* __restrict__ gpre = a.pre;
+  float* __restrict__ gx = a.x;
+  float* __restrict__ gr = a.r;
 
   // (1) Ap += lam p; partials p.Ap, max|p|, #nonfinite(p)  (k_cg_pap)
   {
@@ -770,20 +851,29 @@ __global__ void __launch_bounds__(NT, 4) k_cg_fused(CgFusedArgs a) {
       t[2] += isfinite(pi) ? 0.0 : 1.0;
       mx = fmax(mx, (double)fabsf(pi));
     };
+    float4 P[NQ], A[NQ];
 #pragma unroll
     for (int j = 0; j < NQ; ++j) {
       const int64_t q = tid + j * nth;
       if (q < nq) {
-        P[j] = ld4g(a.p + 4 * q);
-        A[j] = ld4g(a.ap + 4 * q);
+        P[j] = ld4g(gp + 4 * q);
+        A[j] = ld4g(gap + 4 * q);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {
+      if (tid + j * nth < nq) {
         body(P[j].x, A[j].x); body(P[j].y, A[j].y); body(P[j].z, A[j].z); body(P[j].w, A[j].w);
+        sP[j][tx] = P[j];
+        sA[j][tx] = A[j];
       }
     }
     if (has_t) {
-      pt = a.p[it];
-      at = a.ap[it];
+      pt = gp[it];
+      at = gap[it];
       body(pt, at);
     }
+    t[1] = 0.0;
     write_partials<3>(a.ws, t);
     __shared__ double smx[NT / 32];
     mx = warp_max_d(mx);
@@ -794,7 +884,15 @@ __global__ void __launch_bounds__(NT, 4) k_cg_fused(CgFusedArgs a) {
       for (int w = 0; w < NT / 32; ++w) m = fmax(m, smx[w]);
       a.ws[blockIdx.x * 8 + 1] = m;
     }
-    grid_sync_last(a.bar, [&] { pap_final_body(a.ws, a.st, a.k, 0); }, read_decision);
+    grid_sync_last(
+        a.bar,
+        [&] {
+          double u[3];
+          sum_slots<3>(a.ws, 0, u);
+          const double pmax = max_slot(a.ws, 1);
+          if (threadIdx.x == 0) pap_decide(u[0], pmax, u[2], a.st, a.k, 0);
+        },
+        read_decision);
   }
   if (s_done) return;
 
@@ -803,82 +901,91 @@ __global__ void __launch_bounds__(NT, 4) k_cg_fused(CgFusedArgs a) {
   //     amax_l >= max|p_l|, B_l = max|z_l| + |beta| amax_l bounds the next direction,
   //     so its split exponent is known at this barrier (no third reduction; the
   //     exponent is the exact-amax one or one binade below it).
-  const OffTab& T = a.t;
-  __shared__ int smax[kOffTabMax];
-  __shared__ float sscale[kOffTabMax];
-  if (threadIdx.x < kOffTabMax) smax[threadIdx.x] = 0;
   {
     const float al = s_val;
     double t[2] = {0.0, 0.0};
-    int l = 0;
-    float m = 0.f;
-    auto take = [&](int64_t i, float v) {
-      if (i >= T.off[l + 1]) {
-        atomicMax(&smax[l], __float_as_int(m));
-        m = 0.f;
-        while (i >= T.off[l + 1]) ++l;
-      }
-      m = fmaxf(m, fabsf(v));
-    };
-    auto body = [&](int64_t i, float& xi, float& ri, float pi, float& ai, float mi) {
+    LayerMax lm{T, smax};
+    auto minv = [&](float m) { return 1.f / (fmaxf(m, a.floor_) + lam); };
+    auto body = [&](float& xi, float& ri, float pi, float& ai, float mi) {
       xi += al * pi;
       ri -= al * ai;
       const float z = mi * ri;
       t[0] += (double)ri * ri;
       t[1] += (double)ri * z;
       ai = z;
-      take(i, z);
     };
-    auto minv = [&](float m) { return 1.f / (fmaxf(m, a.floor_) + lam); };
-    __syncthreads();  // smax zeroed
+    float4 X[NQ], R[NQ], M[NQ];
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {
+      const int64_t q = tid + j * nth;
+      if (q < nq) {
+        X[j] = ld4g(gx + 4 * q);
+        R[j] = ld4g(gr + 4 * q);
+        M[j] = gpre ? ld4g(gpre + 4 * q) : make_float4(1.f, 1.f, 1.f, 1.f);
+      }
+    }
 #pragma unroll
     for (int j = 0; j < NQ; ++j) {
       const int64_t q = tid + j * nth;
       if (q < nq) {
         const int64_t i = 4 * q;
-        float4 X = ld4g(a.x + i), R = ld4g(a.r + i);
-        float4 M = make_float4(1.f, 1.f, 1.f, 1.f);
-        if (a.pre) {
-          M = ld4g(a.pre + i);
-          M = make_float4(minv(M.x), minv(M.y), minv(M.z), minv(M.w));
-        }
-        body(i, X.x, R.x, P[j].x, A[j].x, M.x); body(i + 1, X.y, R.y, P[j].y, A[j].y, M.y);
-        body(i + 2, X.z, R.z, P[j].z, A[j].z, M.z); body(i + 3, X.w, R.w, P[j].w, A[j].w, M.w);
-        *reinterpret_cast<float4*>(a.x + i) = X;
-        *reinterpret_cast<float4*>(a.r + i) = R;
+        const float4 Pj = sP[j][tx];
+        float4 Aj = sA[j][tx], Mj = M[j];
+        if (gpre) Mj = make_float4(minv(Mj.x), minv(Mj.y), minv(Mj.z), minv(Mj.w));
+        body(X[j].x, R[j].x, Pj.x, Aj.x, Mj.x); body(X[j].y, R[j].y, Pj.y, Aj.y, Mj.y);
+        body(X[j].z, R[j].z, Pj.z, Aj.z, Mj.z); body(X[j].w, R[j].w, Pj.w, Aj.w, Mj.w);
+        *reinterpret_cast<float4*>(gx + i) = X[j];
+        *reinterpret_cast<float4*>(gr + i) = R[j];
+        sA[j][tx] = Aj;
+        lm.take4(i, Aj);
       }
     }
     if (has_t) {
-      float xi = a.x[it], ri = a.r[it];
-      body(it, xi, ri, pt, at, a.pre ? minv(a.pre[it]) : 1.f);
-      a.x[it] = xi;
-      a.r[it] = ri;
+      float xi = gx[it], ri = gr[it];
+      body(xi, ri, pt, at, gpre ? minv(gpre[it]) : 1.f);
+      gx[it] = xi;
+      gr[it] = ri;
+      lm.take(it, at);
     }
-    atomicMax(&smax[l], __float_as_int(m));
-    write_partials<2>(a.ws, t);  // (its barriers also publish smax)
+    lm.flush();
+    block_sum<2>(t);  // (its barriers also publish smax)
+    if (threadIdx.x == 0) {
+      a.ws[blockIdx.x * 8 + 3] = t[0];
+      a.ws[blockIdx.x * 8 + 4] = t[1];
+    }
     if (threadIdx.x < T.L) a.part[blockIdx.x * kOffTabMax + threadIdx.x] = __int_as_float(smax[threadIdx.x]);
     __shared__ float sh[kOffTabMax][NT / 32];
     grid_sync_last(
         a.bar,
         [&] {
-          r_final_body(a.ws, a.st, a.k, a.maxiter, 0, a.tol);
+          double tot[2];
+          sum_slots<2>(a.ws, 3, tot);
+          // per-layer max|z| over the blocks (order free)
           for (int l2 = 0; l2 < T.L; ++l2) {
             float mm = 0.f;
-            for (int b = threadIdx.x; b < (int)gridDim.x; b += NT) mm = fmaxf(mm, __ldcg(a.part + b * kOffTabMax + l2));
+#pragma unroll
+            for (int u = 0; u < (NB + NT - 1) / NT; ++u) {
+              const int b = threadIdx.x + u * NT;
+              if (b < NB) mm = fmaxf(mm, __ldcg(a.part + b * kOffTabMax + l2));
+            }
             mm = warp_max_f(mm);
             if ((threadIdx.x & 31) == 0) sh[l2][threadIdx.x >> 5] = mm;
           }
           __syncthreads();
-          if (threadIdx.x == 0 && !a.st->done) {
-            const float beta = fabsf((float)a.st->alpha);
-            for (int l2 = 0; l2 < T.L; ++l2) {
-              float mz = 0.f;
-              for (int w = 0; w < NT / 32; ++w) mz = fmaxf(mz, sh[l2][w]);
-              const float B = mz + beta * a.sc[l2].amax;
-              a.sc[l2].amax = B;
-              a.sc[l2].e = exp_for_bound(B);
+          if (threadIdx.x == 0) {
+            r_decide(tot[0], tot[1], a.st, a.k, a.maxiter, 0, a.tol);
+            if (!a.st->done) {
+              const float beta = fabsf((float)a.st->alpha);
+              for (int l2 = 0; l2 < T.L; ++l2) {
+                float mz = 0.f;
+                for (int w = 0; w < NT / 32; ++w) mz = fmaxf(mz, sh[l2][w]);
+                const float B = mz + beta * s_amax[l2];
+                a.sc[l2].amax = B;
+                a.sc[l2].e = exp_for_bound(B);
+              }
             }
           }
+          __syncthreads();
           if (!a.st->done)
             for (int i = threadIdx.x; i < a.n_zero; i += NT) {
               a.zero_sc[i].e = 0;
@@ -901,28 +1008,39 @@ __global__ void __launch_bounds__(NT, 4) k_cg_fused(CgFusedArgs a) {
       while (i >= T.off[l + 1]) ++l;
       return sscale[l];
     };
+    float* __restrict__ wp = a.p;
 #pragma unroll
     for (int j = 0; j < NQ; ++j) {
       const int64_t q = tid + j * nth;
       if (q < nq) {
         const int64_t i = 4 * q;
-        P[j].x = A[j].x + beta * P[j].x;
-        P[j].y = A[j].y + beta * P[j].y;
-        P[j].z = A[j].z + beta * P[j].z;
-        P[j].w = A[j].w + beta * P[j].w;
-        *reinterpret_cast<float4*>(a.p + i) = P[j];
+        float4 Pj = sP[j][tx];
+        const float4 Zj = sA[j][tx];
+        Pj.x = Zj.x + beta * Pj.x;
+        Pj.y = Zj.y + beta * Pj.y;
+        Pj.z = Zj.z + beta * Pj.z;
+        Pj.w = Zj.w + beta * Pj.w;
+        *reinterpret_cast<float4*>(wp + i) = Pj;
         union { uint2 u; __half h[4]; } H, L;
-        split16(P[j].x, scale_at(i), H.h[0], L.h[0]);
-        split16(P[j].y, scale_at(i + 1), H.h[1], L.h[1]);
-        split16(P[j].z, scale_at(i + 2), H.h[2], L.h[2]);
-        split16(P[j].w, scale_at(i + 3), H.h[3], L.h[3]);
+        if (i + 3 < T.off[l + 1] && i >= T.off[l]) {
+          const float sc4 = sscale[l];
+          split16(Pj.x, sc4, H.h[0], L.h[0]);
+          split16(Pj.y, sc4, H.h[1], L.h[1]);
+          split16(Pj.z, sc4, H.h[2], L.h[2]);
+          split16(Pj.w, sc4, H.h[3], L.h[3]);
+        } else {
+          split16(Pj.x, scale_at(i), H.h[0], L.h[0]);
+          split16(Pj.y, scale_at(i + 1), H.h[1], L.h[1]);
+          split16(Pj.z, scale_at(i + 2), H.h[2], L.h[2]);
+          split16(Pj.w, scale_at(i + 3), H.h[3], L.h[3]);
+        }
         *reinterpret_cast<uint2*>(a.hi + i) = H.u;
         *reinterpret_cast<uint2*>(a.lo + i) = L.u;
       }
     }
     if (has_t) {
       pt = at + beta * pt;
-      a.p[it] = pt;
+      wp[it] = pt;
       split16(pt, scale_at(it), a.hi[it], a.lo[it]);
     }
   }
