@@ -1064,6 +1064,26 @@ static bool cg_fused_enabled() {
   return on;
 }
 
+// The grid must be co-resident (cooperative launch): NB blocks on this device's
+// SMs at the kernel's occupancy (4 per SM on a full B200; a smaller partition, e.g.
+// a MIG slice, keeps the per-kernel passes).
+static bool cg_fused_fits(int nq) {
+  static int fits[CGF_MAXQ + 1] = {-1, -1, -1, -1, -1};
+  if (fits[nq] < 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const void* k = nq == 1 ? (const void*)k_cg_fused<1> : nq == 2 ? (const void*)k_cg_fused<2>
+                  : nq == 3 ? (const void*)k_cg_fused<3> : (const void*)k_cg_fused<4>;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, 0) != cudaSuccess) {
+      cudaGetLastError();
+      per_sm = 0;
+    }
+    fits[nq] = per_sm * sms >= NB;
+  }
+  return fits[nq] != 0;
+}
+
 static void launch_cg_fused(cudaStream_t st, int nq, const CgFusedArgs& a) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(NB);
@@ -1075,8 +1095,7 @@ static void launch_cg_fused(cudaStream_t st, int nq, const CgFusedArgs& a) {
   attr[1].id = cudaLaunchAttributeCooperative;
   attr[1].val.cooperative = 1;
   cfg.attrs = attr;
-  static const int coop = !(getenv("CURVOPT_CG_COOP") && getenv("CURVOPT_CG_COOP")[0] == '0');
-  cfg.numAttrs = coop ? 2 : 1;
+  cfg.numAttrs = 2;
   switch (nq) {
     case 1: cudaLaunchKernelEx(&cfg, k_cg_fused<1>, a); break;
     case 2: cudaLaunchKernelEx(&cfg, k_cg_fused<2>, a); break;
@@ -1404,6 +1423,7 @@ static void cg_run(cv_ctx* ctx, const CgOperator& op, const float* g, double lam
     fa = CgFusedArgs{x, r, p, ap, precond, flam, ffl, st, d, ws, ctx->amax_counter + 16, 0, maxiter, tol,
                      make_off_tab(s->off, d), ctx->amax_ws, s->v_sc, s->prod_sc, s->n_prod, s->v_hi, s->v_lo};
     fq = cg_fused_nq(d, fa.t, x, r, p, ap, precond, s->v_hi, s->v_lo);
+    if (fq && !cg_fused_fits(fq)) fq = 0;
   }
   for (int k = 1; k <= maxiter; ++k) {
     const int is_stab = (stab > 0 && k % stab == 0) ? 1 : 0;
