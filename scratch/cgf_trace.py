@@ -1,3 +1,7 @@
+"""Per-block timeline of k_cg_fused (globaltimer stamps per phase).  Needs a temporary
+instrumentation patch of csrc/vec.cu that is NOT in the tree: a `trace` pointer in
+CgFusedArgs read from CURVOPT_CGF_TRACE (a device address) and TR(k) stamps at kernel
+entry, barrier arrivals/releases and exit (results: profiles/r3_cg_fused.txt)."""
 import sys, os; sys.path.insert(0, ".")
 import numpy as np, torch
 buf = torch.zeros(592 * 8, dtype=torch.int64, device="cuda")
