@@ -76,7 +76,7 @@ int cv_ctx_create(int device, int world, int rank, const void* nccl_id, cv_ctx**
   if (sms > 0) c->sm_count = sms;
   c->red_ws = (double*)c->pool.get(sizeof(double) * kRedBlocks * 8);
   c->scal_ws = (double*)c->pool.get(sizeof(double) * 64);
-  c->amax_ws = (float*)c->pool.get(sizeof(float) * (kAmaxWsFloats + kOffTabMax));  // split.cu SP_NB x SP_MAXL, mr
+  c->amax_ws = (float*)c->pool.get(sizeof(float) * (2 * kAmaxWsFloats + kOffTabMax));  // split.cu SP_NB x SP_MAXL, mr; k_cg_fused
   c->amax_counter = (unsigned*)c->pool.get(sizeof(unsigned) * 64);
   cudaMemsetAsync(c->amax_counter, 0, sizeof(unsigned) * 64, c->stream);
   if (const char* e = getenv("CURVOPT_SHARD_CG")) c->shard_cg = atoi(e) != 0;  // test hook (default: by size)

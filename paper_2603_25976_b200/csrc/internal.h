@@ -338,7 +338,8 @@ inline OffTab make_off_tab(const std::vector<int64_t>& off, int64_t d) {
   t.off[t.L] = d;
   return t;
 }
-constexpr int kAmaxWsFloats = 4 * 148 * kOffTabMax;  // amax_ws block maxima; kOffTabMax floats follow
+constexpr int kAmaxWsFloats = 4 * 148 * kOffTabMax;  // amax_ws block maxima; kOffTabMax floats follow,
+                                                      // then k_cg_fused's second block-maxima table
 
 // split.cu: scaled fp16 splits with exact amax (two passes)
 void amax_into(cv_ctx* ctx, const float* x, int64_t n, Scale* slot);  // slot->amax = max|x|

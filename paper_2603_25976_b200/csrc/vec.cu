@@ -695,7 +695,8 @@ struct CgFusedArgs {
   int k, maxiter;
   double tol;
   OffTab t;
-  float* part;  // NB x kOffTabMax block maxima
+  float* part;   // NB x kOffTabMax block maxima of |z| per layer
+  float* part2;  // NB x kOffTabMax block maxima of |p| per layer
   Scale* sc;
   Scale* zero_sc;
   int n_zero;
@@ -812,16 +813,15 @@ __global__ void __launch_bounds__(NT, 4) k_cg_fused(CgFusedArgs a) {
   CV_PDL_ENTRY();
   __shared__ int s_done;
   __shared__ float s_val;  // alpha after the pap decision, beta after the residual decision
-  __shared__ float s_amax[kOffTabMax], sscale[kOffTabMax];
-  __shared__ int smax[kOffTabMax];
+  __shared__ float sscale[kOffTabMax];
+  __shared__ int smax[kOffTabMax], smaxp[kOffTabMax];
   // this thread's groups of p and Ap (then z) across the barriers: shared memory
   // (32 KB per block at NQ = 4), so the registers carry the loads in flight
   __shared__ float4 sP[NQ][NT], sA[NQ][NT];
   const OffTab& T = a.t;
   volatile CgDev* vst = a.st;
   if (threadIdx.x == 0) s_done = vst->done;  // nothing writes the flag before the first barrier
-  if (threadIdx.x < T.L) s_amax[threadIdx.x] = a.sc[threadIdx.x].amax;  // bound of the current direction
-  if (threadIdx.x < kOffTabMax) smax[threadIdx.x] = 0;
+  if (threadIdx.x < kOffTabMax) smax[threadIdx.x] = smaxp[threadIdx.x] = 0;
   __syncthreads();
   if (s_done) return;
   auto read_decision = [&] {
@@ -860,21 +860,27 @@ __global__ void __launch_bounds__(NT, 4) k_cg_fused(CgFusedArgs a) {
         A[j] = ld4g(gap + 4 * q);
       }
     }
+    LayerMax lmp{T, smaxp};
 #pragma unroll
     for (int j = 0; j < NQ; ++j) {
-      if (tid + j * nth < nq) {
+      const int64_t q = tid + j * nth;
+      if (q < nq) {
         body(P[j].x, A[j].x); body(P[j].y, A[j].y); body(P[j].z, A[j].z); body(P[j].w, A[j].w);
         sP[j][tx] = P[j];
         sA[j][tx] = A[j];
+        lmp.take4(4 * q, P[j]);
       }
     }
     if (has_t) {
       pt = gp[it];
       at = gap[it];
       body(pt, at);
+      lmp.take(it, pt);
     }
+    lmp.flush();
     t[1] = 0.0;
-    write_partials<3>(a.ws, t);
+    write_partials<3>(a.ws, t);  // (its barriers also publish smaxp)
+    if (threadIdx.x < T.L) a.part2[blockIdx.x * kOffTabMax + threadIdx.x] = __int_as_float(smaxp[threadIdx.x]);
     __shared__ double smx[NT / 32];
     mx = warp_max_d(mx);
     if ((threadIdx.x & 31) == 0) smx[threadIdx.x >> 5] = mx;
@@ -897,10 +903,11 @@ __global__ void __launch_bounds__(NT, 4) k_cg_fused(CgFusedArgs a) {
   if (s_done) return;
 
   // (2) x += alpha p; r -= alpha Ap; z = M^-1 r; partials ||r||^2, r.z  (k_cg_update)
-  //     and the per-layer max|z|: with the current direction's published bound
-  //     amax_l >= max|p_l|, B_l = max|z_l| + |beta| amax_l bounds the next direction,
-  //     so its split exponent is known at this barrier (no third reduction; the
-  //     exponent is the exact-amax one or one binade below it).
+  //     and the per-layer max|z|: with the current direction's per-layer max|p_l|
+  //     (phase 1), B_l = max|z_l| + |beta| max|p_l| bounds the next direction, so its
+  //     split exponent is known at this barrier (no third reduction; the exponent is
+  //     the exact-amax one or one binade below it; the bound is rebuilt from exact
+  //     maxima every iteration, so it never compounds).
   {
     const float al = s_val;
     double t[2] = {0.0, 0.0};
@@ -954,7 +961,7 @@ __global__ void __launch_bounds__(NT, 4) k_cg_fused(CgFusedArgs a) {
       a.ws[blockIdx.x * 8 + 4] = t[1];
     }
     if (threadIdx.x < T.L) a.part[blockIdx.x * kOffTabMax + threadIdx.x] = __int_as_float(smax[threadIdx.x]);
-    __shared__ float sh[kOffTabMax][NT / 32];
+    __shared__ float sh[kOffTabMax][NT / 32], shp[kOffTabMax][NT / 32];
     grid_sync_last(
         a.bar,
         [&] {
@@ -962,14 +969,21 @@ __global__ void __launch_bounds__(NT, 4) k_cg_fused(CgFusedArgs a) {
           sum_slots<2>(a.ws, 3, tot);
           // per-layer max|z| over the blocks (order free)
           for (int l2 = 0; l2 < T.L; ++l2) {
-            float mm = 0.f;
+            float mm = 0.f, mp = 0.f;
 #pragma unroll
             for (int u = 0; u < (NB + NT - 1) / NT; ++u) {
               const int b = threadIdx.x + u * NT;
-              if (b < NB) mm = fmaxf(mm, __ldcg(a.part + b * kOffTabMax + l2));
+              if (b < NB) {
+                mm = fmaxf(mm, __ldcg(a.part + b * kOffTabMax + l2));
+                mp = fmaxf(mp, __ldcg(a.part2 + b * kOffTabMax + l2));
+              }
             }
             mm = warp_max_f(mm);
-            if ((threadIdx.x & 31) == 0) sh[l2][threadIdx.x >> 5] = mm;
+            mp = warp_max_f(mp);
+            if ((threadIdx.x & 31) == 0) {
+              sh[l2][threadIdx.x >> 5] = mm;
+              shp[l2][threadIdx.x >> 5] = mp;
+            }
           }
           __syncthreads();
           if (threadIdx.x == 0) {
@@ -977,9 +991,12 @@ __global__ void __launch_bounds__(NT, 4) k_cg_fused(CgFusedArgs a) {
             if (!a.st->done) {
               const float beta = fabsf((float)a.st->alpha);
               for (int l2 = 0; l2 < T.L; ++l2) {
-                float mz = 0.f;
-                for (int w = 0; w < NT / 32; ++w) mz = fmaxf(mz, sh[l2][w]);
-                const float B = mz + beta * s_amax[l2];
+                float mz = 0.f, mp = 0.f;
+                for (int w = 0; w < NT / 32; ++w) {
+                  mz = fmaxf(mz, sh[l2][w]);
+                  mp = fmaxf(mp, shp[l2][w]);
+                }
+                const float B = mz + beta * mp;
                 a.sc[l2].amax = B;
                 a.sc[l2].e = exp_for_bound(B);
               }
@@ -1421,7 +1438,8 @@ static void cg_run(cv_ctx* ctx, const CgOperator& op, const float* g, double lam
   int fq = 0;
   if (s && (int)s->off.size() <= kOffTabMax && cg_fused_enabled()) {
     fa = CgFusedArgs{x, r, p, ap, precond, flam, ffl, st, d, ws, ctx->amax_counter + 16, 0, maxiter, tol,
-                     make_off_tab(s->off, d), ctx->amax_ws, s->v_sc, s->prod_sc, s->n_prod, s->v_hi, s->v_lo};
+                     make_off_tab(s->off, d), ctx->amax_ws, ctx->amax_ws + kAmaxWsFloats + kOffTabMax, s->v_sc,
+                     s->prod_sc, s->n_prod, s->v_hi, s->v_lo};
     fq = cg_fused_nq(d, fa.t, x, r, p, ap, precond, s->v_hi, s->v_lo);
     if (fq && !cg_fused_fits(fq)) fq = 0;
   }
