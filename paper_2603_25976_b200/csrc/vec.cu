@@ -1063,6 +1063,181 @@ __global__ void __launch_bounds__(NT, 4) k_cg_fused(CgFusedArgs a) {
   }
 }
 
+// The start of a (P)CG run after the warm-start product, in one launch
+// (solvers.py:76-84): r = g - (Ax + lam x) (or g), ||r||^2 -> the r0 decision ->
+// p = z = M^-1 r, r.z and the exact per-layer max|p| -> p's scales -> the first
+// product's input split.  The same reductions as k_cg_r0 / k_cg_p0 (bitwise: same
+// thread mapping and summation order) and the same exact-amax split as the product's
+// own split pass, so the iterates equal the per-kernel start's.  red_ws slots 5, 6.
+template <int NQ>
+__global__ void __launch_bounds__(NT, 4) k_cg_start(CgFusedArgs a, const float* __restrict__ g) {
+  CV_PDL_ENTRY();
+  __shared__ int s_done, s_warm;
+  __shared__ float sscale[kOffTabMax];
+  __shared__ int smax[kOffTabMax];
+  __shared__ float4 sR[NQ][NT];
+  const OffTab& T = a.t;
+  volatile CgDev* vst = a.st;
+  if (threadIdx.x == 0) {
+    s_done = vst->done;
+    s_warm = vst->x0nz;
+  }
+  if (threadIdx.x < kOffTabMax) smax[threadIdx.x] = 0;
+  __syncthreads();
+  if (s_done) return;
+  const bool warm = s_warm;
+  const int64_t tid = blockIdx.x * (int64_t)NT + threadIdx.x, nth = (int64_t)gridDim.x * NT;
+  const int64_t nq = a.d >> 2;
+  const int64_t it = 4 * nq + tid;
+  const bool has_t = it < a.d;
+  const int tx = threadIdx.x;
+  const float lam = a.lam;
+  float rt = 0.f;
+
+  // (1) r0 (k_cg_r0)
+  {
+    double t[1] = {0.0};
+    float4 G[NQ], AX[NQ], X[NQ];
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {
+      const int64_t q = tid + j * nth;
+      if (q < nq) {
+        G[j] = ld4g(g + 4 * q);
+        if (warm) {
+          AX[j] = ld4g(a.ap + 4 * q);
+          X[j] = ld4g(a.x + 4 * q);
+        }
+      }
+    }
+    auto body = [&](float& v, float av, float xv) {
+      if (warm) v = v - (av + lam * xv);
+      t[0] += (double)v * v;
+    };
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {
+      const int64_t q = tid + j * nth;
+      if (q < nq) {
+        float4 v = G[j];
+        body(v.x, AX[j].x, X[j].x); body(v.y, AX[j].y, X[j].y); body(v.z, AX[j].z, X[j].z); body(v.w, AX[j].w, X[j].w);
+        *reinterpret_cast<float4*>(a.r + 4 * q) = v;
+        sR[j][tx] = v;
+      }
+    }
+    if (has_t) {
+      rt = g[it];
+      body(rt, warm ? a.ap[it] : 0.f, warm ? a.x[it] : 0.f);
+      a.r[it] = rt;
+    }
+    block_sum<1>(t);
+    if (threadIdx.x == 0) a.ws[blockIdx.x * 8 + 5] = t[0];
+    grid_sync_last(
+        a.bar,
+        [&] {
+          double u[1];
+          sum_slots<1>(a.ws, 5, u);
+          if (threadIdx.x == 0) r0_decide(u[0], a.st, a.tol);
+        },
+        [&] { s_done = vst->done; });
+  }
+  if (s_done) return;
+
+  // (2) p = z = M^-1 r; r.z; exact per-layer max|p|  (k_cg_p0 + the product's amax pass)
+  {
+    double t[1] = {0.0};
+    LayerMax lm{T, smax};
+    auto minv = [&](float m) { return a.pre ? 1.f / (fmaxf(m, a.floor_) + lam) : 1.f; };
+    float4 M[NQ];
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {
+      const int64_t q = tid + j * nth;
+      if (q < nq) M[j] = a.pre ? ld4g(a.pre + 4 * q) : make_float4(1.f, 1.f, 1.f, 1.f);
+    }
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {
+      const int64_t q = tid + j * nth;
+      if (q < nq) {
+        const float4 rv = sR[j][tx];
+        float4 z;
+        z.x = minv(M[j].x) * rv.x; z.y = minv(M[j].y) * rv.y; z.z = minv(M[j].z) * rv.z; z.w = minv(M[j].w) * rv.w;
+        t[0] += (double)rv.x * z.x; t[0] += (double)rv.y * z.y; t[0] += (double)rv.z * z.z; t[0] += (double)rv.w * z.w;
+        *reinterpret_cast<float4*>(a.p + 4 * q) = z;
+        sR[j][tx] = z;
+        lm.take4(4 * q, z);
+      }
+    }
+    if (has_t) {
+      const float z = minv(a.pre ? a.pre[it] : 1.f) * rt;
+      t[0] += (double)rt * z;
+      rt = z;
+      a.p[it] = z;
+      lm.take(it, z);
+    }
+    lm.flush();
+    block_sum<1>(t);  // (its barriers also publish smax)
+    if (threadIdx.x == 0) a.ws[blockIdx.x * 8 + 6] = t[0];
+    if (threadIdx.x < T.L) a.part[blockIdx.x * kOffTabMax + threadIdx.x] = __int_as_float(smax[threadIdx.x]);
+    __shared__ float sh[kOffTabMax][NT / 32];
+    grid_sync_last(
+        a.bar,
+        [&] {
+          double u[1];
+          sum_slots<1>(a.ws, 6, u);
+          for (int l2 = 0; l2 < T.L; ++l2) {
+            float mm = 0.f;
+#pragma unroll
+            for (int v = 0; v < (NB + NT - 1) / NT; ++v) {
+              const int b = threadIdx.x + v * NT;
+              if (b < NB) mm = fmaxf(mm, __ldcg(a.part + b * kOffTabMax + l2));
+            }
+            mm = warp_max_f(mm);
+            if ((threadIdx.x & 31) == 0) sh[l2][threadIdx.x >> 5] = mm;
+          }
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            a.st->rz = u[0];
+            for (int l2 = 0; l2 < T.L; ++l2) {
+              float mz = 0.f;
+              for (int w = 0; w < NT / 32; ++w) mz = fmaxf(mz, sh[l2][w]);
+              a.sc[l2].amax = mz;
+              a.sc[l2].e = exp_for_bound(mz);
+            }
+          }
+          for (int i = threadIdx.x; i < a.n_zero; i += NT) {
+            a.zero_sc[i].e = 0;
+            a.zero_sc[i].amax = 0.f;
+          }
+        },
+        [&] {
+          for (int l2 = 0; l2 < T.L; ++l2) sscale[l2] = pow2f(((volatile Scale*)a.sc)[l2].e);
+        });
+  }
+
+  // (3) the first product's input split
+  {
+    int l = 0;
+    auto scale_at = [&](int64_t i) {
+      while (i >= T.off[l + 1]) ++l;
+      return sscale[l];
+    };
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {
+      const int64_t q = tid + j * nth;
+      if (q < nq) {
+        const int64_t i = 4 * q;
+        const float4 Pj = sR[j][tx];
+        union { uint2 u; __half h[4]; } H, L;
+        split16(Pj.x, scale_at(i), H.h[0], L.h[0]);
+        split16(Pj.y, scale_at(i + 1), H.h[1], L.h[1]);
+        split16(Pj.z, scale_at(i + 2), H.h[2], L.h[2]);
+        split16(Pj.w, scale_at(i + 3), H.h[3], L.h[3]);
+        *reinterpret_cast<uint2*>(a.hi + i) = H.u;
+        *reinterpret_cast<uint2*>(a.lo + i) = L.u;
+      }
+    }
+    if (has_t) split16(rt, scale_at(it), a.hi[it], a.lo[it]);
+  }
+}
+
 // The fused iteration applies when every thread's share fits its registers and the
 // 16-byte / 8-byte vector accesses are aligned.
 static int cg_fused_nq(int64_t d, const OffTab& t, const void* x, const void* r, const void* p, const void* ap,
@@ -1096,9 +1271,36 @@ static bool cg_fused_fits(int nq) {
       cudaGetLastError();
       per_sm = 0;
     }
-    fits[nq] = per_sm * sms >= NB;
+    int per_sm2 = 0;
+    const void* k2 = nq == 1 ? (const void*)k_cg_start<1> : nq == 2 ? (const void*)k_cg_start<2>
+                   : nq == 3 ? (const void*)k_cg_start<3> : (const void*)k_cg_start<4>;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k2, NT, 0) != cudaSuccess) {
+      cudaGetLastError();
+      per_sm2 = 0;
+    }
+    fits[nq] = per_sm * sms >= NB && per_sm2 * sms >= NB;
   }
   return fits[nq] != 0;
+}
+
+static void launch_cg_start(cudaStream_t st, int nq, const CgFusedArgs& a, const float* g) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(NB);
+  cfg.blockDim = dim3(NT);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  switch (nq) {
+    case 1: cudaLaunchKernelEx(&cfg, k_cg_start<1>, a, g); break;
+    case 2: cudaLaunchKernelEx(&cfg, k_cg_start<2>, a, g); break;
+    case 3: cudaLaunchKernelEx(&cfg, k_cg_start<3>, a, g); break;
+    default: cudaLaunchKernelEx(&cfg, k_cg_start<4>, a, g); break;
+  }
 }
 
 static void launch_cg_fused(cudaStream_t st, int nq, const CgFusedArgs& a) {
@@ -1428,11 +1630,6 @@ static void cg_run(cv_ctx* ctx, const CgOperator& op, const float* g, double lam
   } else {
     cudaMemsetAsync(x, 0, sizeof(float) * d, sm);
   }
-  launch_k(sm, k_cg_r0, NB, NT, 0, g, ap, x, flam, st, d, r, ws);
-  launch_k(sm, k_cg_r0_final, 1, NT, 0, ws, st, tol);
-  launch_k(sm, k_cg_p0, NB, NT, 0, r, precond, flam, ffl, st, d, p, ws);
-  launch_k(sm, k_cg_p0_final, 1, NT, 0, ws, st);
-  ctx->launches += 4;
   unsigned* ctr = ctx->amax_counter + 1;
   CgFusedArgs fa{};
   int fq = 0;
@@ -1441,7 +1638,18 @@ static void cg_run(cv_ctx* ctx, const CgOperator& op, const float* g, double lam
                      make_off_tab(s->off, d), ctx->amax_ws, ctx->amax_ws + kAmaxWsFloats + kOffTabMax, s->v_sc,
                      s->prod_sc, s->n_prod, s->v_hi, s->v_lo};
     fq = cg_fused_nq(d, fa.t, x, r, p, ap, precond, s->v_hi, s->v_lo);
-    if (fq && !cg_fused_fits(fq)) fq = 0;
+    if (fq && (((uintptr_t)g & 15) || !cg_fused_fits(fq))) fq = 0;
+  }
+  if (fq) {  // r0, p0, p0's scales and split in one launch
+    launch_cg_start(sm, fq, fa, g);
+    ctx->launches++;
+    s->v_ready = 2;
+  } else {
+    launch_k(sm, k_cg_r0, NB, NT, 0, g, ap, x, flam, st, d, r, ws);
+    launch_k(sm, k_cg_r0_final, 1, NT, 0, ws, st, tol);
+    launch_k(sm, k_cg_p0, NB, NT, 0, r, precond, flam, ffl, st, d, p, ws);
+    launch_k(sm, k_cg_p0_final, 1, NT, 0, ws, st);
+    ctx->launches += 4;
   }
   for (int k = 1; k <= maxiter; ++k) {
     const int is_stab = (stab > 0 && k % stab == 0) ? 1 : 0;
