@@ -669,16 +669,16 @@ __global__ void k_cg_pnext(const float* r, const float* pre, float lam, float fl
 // ---------------------------------------------------------------------------
 // One plain (non-stabilising) (P)CG iteration after its product, in ONE launch
 // (solvers.py:90-113): pap -> alpha -> x, r update -> beta -> next direction ->
-// its per-layer scales -> the next product's input split.  The four dependent
-// reductions are separated by grid barriers instead of kernel boundaries; the
-// grid is the reduction grid (NB blocks x NT threads, 4 per SM, co-resident by
-// cooperative launch) and each thread keeps its <= CGF_MAXQ 16-byte groups of p
-// and Ap (then z) in registers across the barriers, so the pass reads p, Ap, x, r,
-// M and writes x, r, p and the split once: 9 d-vectors instead of the 16 of the
-// four separate kernels, and no per-kernel launch / last-block tails.  The
-// reductions are the separate kernels' (fixed-order fp64 block partials summed by
-// the barrier's last block, which also takes the control decision); every block
-// then reads the decided scalars.
+// its per-layer scales -> the next product's input split.  The dependent
+// reductions are separated by two grid barriers instead of four kernel boundaries;
+// the grid is the reduction grid (NB blocks x NT threads, 4 per SM, co-resident by
+// cooperative launch) and each thread keeps its <= CGF_MAXQ 16-byte groups of p and
+// Ap (then z) in shared memory across the barriers, so the pass reads p, Ap, x, r, M
+// and writes x, r, p and the split once: 9 d-vectors instead of the 16 of the four
+// separate kernels, and no per-kernel launch / last-block tails.  The reductions are
+// the separate kernels' (fixed-order fp64 block partials summed by the barrier's
+// last block, which also takes the control decision); every block then reads the
+// decided scalars.
 // ---------------------------------------------------------------------------
 constexpr int CGF_MAXQ = 4;
 struct CgFusedArgs {
@@ -691,7 +691,7 @@ struct CgFusedArgs {
   CgDev* st;
   int64_t d;
   double* ws;
-  unsigned* bar;  // [0] arrivals, [1] generation
+  unsigned* bar;  // [0] arrivals, [32] generation (separate 128-byte lines)
   int k, maxiter;
   double tol;
   OffTab t;
