@@ -808,7 +808,11 @@ struct LayerMax {
 // red_ws slots of the fused iteration (8 per block): 0-2 pap (p.Ap, max|p|,
 // #nonfinite), 3-4 residual (||r||^2, r.z) -- disjoint, so a fast block's residual
 // partials never overwrite pap partials a slow block is still reducing.
-template <int NQ>
+// STAB: the stabilising iteration's first half (solvers.py:97-101 with k % stabilise_every
+// == 0): after the pap phase, x += alpha p with x's exact per-layer max, then x's split --
+// the input of the explicit-residual product (k_cg_pap + k_cg_xupdate + that product's
+// amax and split passes, bitwise: the same exponents as its exact-amax split).
+template <int NQ, bool STAB = false>
 __global__ void __launch_bounds__(NT, 4) k_cg_fused(CgFusedArgs a) {
   CV_PDL_ENTRY();
   __shared__ int s_done;
@@ -896,11 +900,97 @@ __global__ void __launch_bounds__(NT, 4) k_cg_fused(CgFusedArgs a) {
           double u[3];
           sum_slots<3>(a.ws, 0, u);
           const double pmax = max_slot(a.ws, 1);
-          if (threadIdx.x == 0) pap_decide(u[0], pmax, u[2], a.st, a.k, 0);
+          if (threadIdx.x == 0) pap_decide(u[0], pmax, u[2], a.st, a.k, STAB ? 1 : 0);
         },
         read_decision);
   }
   if (s_done) return;
+  if constexpr (STAB) {
+    // x += alpha p (k_cg_xupdate) and x's exact per-layer max
+    const float al = s_val;
+    float4 XV[NQ];
+    float xt = 0.f;
+    {
+      LayerMax lm{T, smax};
+      float4 X[NQ];
+#pragma unroll
+      for (int j = 0; j < NQ; ++j) {
+        const int64_t q = tid + j * nth;
+        if (q < nq) X[j] = ld4g(gx + 4 * q);
+      }
+#pragma unroll
+      for (int j = 0; j < NQ; ++j) {
+        const int64_t q = tid + j * nth;
+        if (q < nq) {
+          const float4 Pj = sP[j][tx];
+          X[j].x += al * Pj.x; X[j].y += al * Pj.y; X[j].z += al * Pj.z; X[j].w += al * Pj.w;
+          *reinterpret_cast<float4*>(gx + 4 * q) = X[j];
+          lm.take4(4 * q, X[j]);
+          XV[j] = X[j];
+        }
+      }
+      if (has_t) {
+        xt = gx[it] + al * pt;
+        gx[it] = xt;
+        lm.take(it, xt);
+      }
+      lm.flush();
+      __syncthreads();
+      if (threadIdx.x < T.L) a.part[blockIdx.x * kOffTabMax + threadIdx.x] = __int_as_float(smax[threadIdx.x]);
+      __shared__ float shx[kOffTabMax][NT / 32];
+      grid_sync_last(
+          a.bar,
+          [&] {
+            for (int l2 = 0; l2 < T.L; ++l2) {
+              float mm = 0.f;
+#pragma unroll
+              for (int v = 0; v < (NB + NT - 1) / NT; ++v) {
+                const int b = threadIdx.x + v * NT;
+                if (b < NB) mm = fmaxf(mm, __ldcg(a.part + b * kOffTabMax + l2));
+              }
+              mm = warp_max_f(mm);
+              if ((threadIdx.x & 31) == 0) shx[l2][threadIdx.x >> 5] = mm;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0)
+              for (int l2 = 0; l2 < T.L; ++l2) {
+                float mx = 0.f;
+                for (int w = 0; w < NT / 32; ++w) mx = fmaxf(mx, shx[l2][w]);
+                a.sc[l2].amax = mx;
+                a.sc[l2].e = exp_for_bound(mx);
+              }
+            for (int i = threadIdx.x; i < a.n_zero; i += NT) {
+              a.zero_sc[i].e = 0;
+              a.zero_sc[i].amax = 0.f;
+            }
+          },
+          [&] {
+            for (int l2 = 0; l2 < T.L; ++l2) sscale[l2] = pow2f(((volatile Scale*)a.sc)[l2].e);
+          });
+    }
+    // x's split: the explicit-residual product's input
+    int l = 0;
+    auto scale_at = [&](int64_t i) {
+      while (i >= T.off[l + 1]) ++l;
+      return sscale[l];
+    };
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {
+      const int64_t q = tid + j * nth;
+      if (q < nq) {
+        const int64_t i = 4 * q;
+        union { uint2 u; __half h[4]; } H, L;
+        split16(XV[j].x, scale_at(i), H.h[0], L.h[0]);
+        split16(XV[j].y, scale_at(i + 1), H.h[1], L.h[1]);
+        split16(XV[j].z, scale_at(i + 2), H.h[2], L.h[2]);
+        split16(XV[j].w, scale_at(i + 3), H.h[3], L.h[3]);
+        *reinterpret_cast<uint2*>(a.hi + i) = H.u;
+        *reinterpret_cast<uint2*>(a.lo + i) = L.u;
+      }
+    }
+    if (has_t) split16(xt, scale_at(it), a.hi[it], a.lo[it]);
+    return;
+  }
 
   // (2) x += alpha p; r -= alpha Ap; z = M^-1 r; partials ||r||^2, r.z  (k_cg_update)
   //     and the per-layer max|z|: with the current direction's per-layer max|p_l|
@@ -1271,6 +1361,14 @@ static bool cg_fused_fits(int nq) {
       cudaGetLastError();
       per_sm = 0;
     }
+    int per_sm3 = 0;
+    const void* k3 = nq == 1 ? (const void*)k_cg_fused<1, true> : nq == 2 ? (const void*)k_cg_fused<2, true>
+                   : nq == 3 ? (const void*)k_cg_fused<3, true> : (const void*)k_cg_fused<4, true>;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3, k3, NT, 0) != cudaSuccess) {
+      cudaGetLastError();
+      per_sm3 = 0;
+    }
+    per_sm = per_sm < per_sm3 ? per_sm : per_sm3;
     int per_sm2 = 0;
     const void* k2 = nq == 1 ? (const void*)k_cg_start<1> : nq == 2 ? (const void*)k_cg_start<2>
                    : nq == 3 ? (const void*)k_cg_start<3> : (const void*)k_cg_start<4>;
@@ -1303,7 +1401,7 @@ static void launch_cg_start(cudaStream_t st, int nq, const CgFusedArgs& a, const
   }
 }
 
-static void launch_cg_fused(cudaStream_t st, int nq, const CgFusedArgs& a) {
+static void launch_cg_fused(cudaStream_t st, int nq, const CgFusedArgs& a, bool stab = false) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(NB);
   cfg.blockDim = dim3(NT);
@@ -1315,12 +1413,18 @@ static void launch_cg_fused(cudaStream_t st, int nq, const CgFusedArgs& a) {
   attr[1].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  switch (nq) {
-    case 1: cudaLaunchKernelEx(&cfg, k_cg_fused<1>, a); break;
-    case 2: cudaLaunchKernelEx(&cfg, k_cg_fused<2>, a); break;
-    case 3: cudaLaunchKernelEx(&cfg, k_cg_fused<3>, a); break;
-    default: cudaLaunchKernelEx(&cfg, k_cg_fused<4>, a); break;
-  }
+  if (stab) switch (nq) {
+      case 1: cudaLaunchKernelEx(&cfg, k_cg_fused<1, true>, a); break;
+      case 2: cudaLaunchKernelEx(&cfg, k_cg_fused<2, true>, a); break;
+      case 3: cudaLaunchKernelEx(&cfg, k_cg_fused<3, true>, a); break;
+      default: cudaLaunchKernelEx(&cfg, k_cg_fused<4, true>, a); break;
+    }
+  else switch (nq) {
+      case 1: cudaLaunchKernelEx(&cfg, k_cg_fused<1>, a); break;
+      case 2: cudaLaunchKernelEx(&cfg, k_cg_fused<2>, a); break;
+      case 3: cudaLaunchKernelEx(&cfg, k_cg_fused<3>, a); break;
+      default: cudaLaunchKernelEx(&cfg, k_cg_fused<4>, a); break;
+    }
 }
 
 __global__ void k_cg_finish(const CgDev* st, cv_cg_stats* out) {
@@ -1662,11 +1766,20 @@ static void cg_run(cv_ctx* ctx, const CgOperator& op, const float* g, double lam
       s->v_ready = 2;
       continue;
     }
-    launch_k(sm, k_cg_pap, NB, NT, 0, ap, p, flam, st, d, ws, ctr, k, is_stab);
-    ctx->launches++;
-    if (is_stab) {
-      launch_k(sm, k_cg_xupdate, NB, NT, 0, x, p, st, d);
+    if (is_stab && fq) {  // pap, x update and x's split in one launch
+      fa.k = k;
+      launch_cg_fused(sm, fq, fa, true);
       ctx->launches++;
+      s->v_ready = 2;
+    } else {
+      launch_k(sm, k_cg_pap, NB, NT, 0, ap, p, flam, st, d, ws, ctr, k, is_stab);
+      ctx->launches++;
+    }
+    if (is_stab) {
+      if (!fq) {
+        launch_k(sm, k_cg_xupdate, NB, NT, 0, x, p, st, d);
+        ctx->launches++;
+      }
       op.apply(ctx, x, ap, &st->gv_skip);
       launch_k(sm, k_cg_rstab, NB, NT, 0, g, ap, x, r, precond, flam, ffl, st, d, ws, ctr, k, maxiter, tol);
     } else {
