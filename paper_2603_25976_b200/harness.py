@@ -129,10 +129,11 @@ class EpochBatcher:
     def next(self) -> Batch:
         hidx = np.ascontiguousarray(self.next_indices(), dtype=np.int64)
         idx = torch.from_numpy(hidx).to(self.dd.X.device)
-        b = Batch(self.dd.X.index_select(0, idx), self.dd.y.index_select(0, idx), self.dd.loss_kind)
+        hint = {}
         if self.dd.loss_kind == "ce":  # label-range contract from the host labels: no device read
-            b._dev["_ymax"] = int(self.dd.ds.y[hidx].max())
-        return b
+            yh = self.dd.ds.y[hidx]
+            hint = {"_ymin": int(yh.min()), "_ymax": int(yh.max())}
+        return Batch(self.dd.X.index_select(0, idx), self.dd.y.index_select(0, idx), self.dd.loss_kind, _dev=hint)
 
 
 # -- run configuration and timing (run.py:31-110) -------------------------------------

@@ -86,7 +86,10 @@ class Batch:
                     raise ContractError("ce targets must be integer class indices")
             if y.ndim != 1 or y.shape[0] != b:
                 raise ContractError("ce targets must be a (b,) index vector")
-            if int(y.min()) < 0:
+            # a loader that holds the host copy of the labels passes its minimum in
+            # _dev["_ymin"] (no device read, no sync); otherwise read it here
+            ymin = self._dev.get("_ymin")
+            if (int(y.min()) if ymin is None else ymin) < 0:
                 raise ContractError("ce class indices must be non-negative")
         else:
             raise ContractError(f"unknown loss kind {self.loss_kind!r}")

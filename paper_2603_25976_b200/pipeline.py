@@ -82,9 +82,12 @@ class BatchPrefetcher:
         compute = torch.cuda.current_stream(self.device)
         compute.wait_event(self._ready[i][0])
         X, y = self._slots[i]
-        batch = Batch(X, y, self.loss_kind, global_size=self.global_size, row_offset=self.row_offset)
-        if self.loss_kind == "ce":  # label-range contract from the host copy: no device read
-            batch._dev["_ymax"] = int(self._ready[i][2].max())
+        # label-range contract from the host copy: no device read (no sync) per batch
+        hint = {}
+        if self.loss_kind == "ce":
+            yh = self._ready[i][2]
+            hint = {"_ymin": int(yh.min()), "_ymax": int(yh.max())}
+        batch = Batch(X, y, self.loss_kind, global_size=self.global_size, row_offset=self.row_offset, _dev=hint)
         # the other slot held the previous batch: reusable once the work enqueued so far is done
         j = 1 - i
         ev = torch.cuda.Event()

@@ -131,3 +131,21 @@ def test_damping_and_rho_rules():
     assert math.isnan(rho_from_terms(1.0, 0.5, 1.0, 1.0).rho)  # pred <= 0
     assert rho_from_terms(1.0, 0.0, -1.0, 0.0).rho == 1.0
     assert rho_from_terms(10.0, -100.0, -1.0, 0.0).rho == 5.0  # clipped
+
+
+def test_batch_label_range_hint_from_host_labels():
+    """A loader holding the host copy of the labels passes their min/max (no device read);
+    a negative minimum is still the reference's contract error (models.py Batch)."""
+    import torch
+
+    from paper_2603_25976_b200 import Batch
+    from paper_2603_25976_b200.errors import ContractError
+
+    X = torch.zeros(4, 3)
+    y = torch.tensor([0, 2, 1, 2])
+    b = Batch(X, y, "ce", _dev={"_ymin": 0, "_ymax": 2})
+    assert b.max_label() == 2
+    with pytest.raises(ContractError):
+        Batch(X, y, "ce", _dev={"_ymin": -1, "_ymax": 2})
+    with pytest.raises(ContractError):
+        Batch(X, torch.tensor([0, -1, 1, 2]), "ce")
