@@ -7,6 +7,7 @@
 #include "vecutil.cuh"
 #include "epilogue.cuh"
 
+#include <algorithm>
 #include <float.h>
 #include <functional>
 #include <stdlib.h>
@@ -1349,36 +1350,34 @@ static bool cg_fused_enabled() {
 // The grid must be co-resident (cooperative launch): NB blocks on this device's
 // SMs at the kernel's occupancy (4 per SM on a full B200; a smaller partition, e.g.
 // a MIG slice, keeps the per-kernel passes).
-static bool cg_fused_fits(int nq) {
-  static int fits[CGF_MAXQ + 1] = {-1, -1, -1, -1, -1};
-  if (fits[nq] < 0) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const void* k = nq == 1 ? (const void*)k_cg_fused<1> : nq == 2 ? (const void*)k_cg_fused<2>
-                  : nq == 3 ? (const void*)k_cg_fused<3> : (const void*)k_cg_fused<4>;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, 0) != cudaSuccess) {
-      cudaGetLastError();
-      per_sm = 0;
-    }
-    int per_sm3 = 0;
-    const void* k3 = nq == 1 ? (const void*)k_cg_fused<1, true> : nq == 2 ? (const void*)k_cg_fused<2, true>
-                   : nq == 3 ? (const void*)k_cg_fused<3, true> : (const void*)k_cg_fused<4, true>;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3, k3, NT, 0) != cudaSuccess) {
-      cudaGetLastError();
-      per_sm3 = 0;
-    }
-    per_sm = per_sm < per_sm3 ? per_sm : per_sm3;
-    int per_sm2 = 0;
-    const void* k2 = nq == 1 ? (const void*)k_cg_start<1> : nq == 2 ? (const void*)k_cg_start<2>
-                   : nq == 3 ? (const void*)k_cg_start<3> : (const void*)k_cg_start<4>;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k2, NT, 0) != cudaSuccess) {
-      cudaGetLastError();
-      per_sm2 = 0;
-    }
-    fits[nq] = per_sm * sms >= NB && per_sm2 * sms >= NB;
+static int occupancy_of(const void* k) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, 0) != cudaSuccess) {
+    cudaGetLastError();
+    per_sm = 0;
   }
-  return fits[nq] != 0;
+  return per_sm;
+}
+template <int NQ>
+static bool cg_fused_fits_nq(int sms) {
+  const int per_sm = std::min({occupancy_of((const void*)k_cg_fused<NQ>), occupancy_of((const void*)k_cg_fused<NQ, true>),
+                               occupancy_of((const void*)k_cg_start<NQ>)});
+  return per_sm * sms >= NB;
+}
+static bool cg_fused_fits(int nq) {
+  constexpr int kMaxDev = 64;
+  static int fits[kMaxDev][CGF_MAXQ + 1];  // per device: 0 unknown, 1 fits, 2 does not
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDev) return false;
+  int& f = fits[dev][nq];
+  if (f == 0) {
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const bool ok = nq == 1 ? cg_fused_fits_nq<1>(sms) : nq == 2 ? cg_fused_fits_nq<2>(sms)
+                  : nq == 3 ? cg_fused_fits_nq<3>(sms) : cg_fused_fits_nq<4>(sms);
+    f = ok ? 1 : 2;
+  }
+  return f == 1;
 }
 
 static void launch_cg_start(cudaStream_t st, int nq, const CgFusedArgs& a, const float* g) {
